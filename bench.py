@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""TurboRAG prefill bench (BASELINE.json metric: p50 TTFT and requests/s vs full-concat prefill; KV-inject GB/s).
+
+Workload (BASELINE.json configs[1], "C2"): Qwen2-7B shape (28 layers, GQA 28Q/4KV, d128, hidden 3584,
+inter 18944, vocab 259 per proj/src/config.cpp:56-66), random-init bf16 weights generated on device
+from seed 42 with the reference's init_random draw order; 16 retrieved chunks x 512 framed tokens
+(SplitMix64 a-z+space text, proj/tests/acceptance_main.cpp:60-67) + a 64-token query, batch 1,
+reordered positions.
+
+One step = one request: KV injection (fused gather + RoPE from the HBM store) + query prefill ->
+first-token logits. `value` = whole-job requests/s with chunk KV resident in the HBM store and the
+query tokens already on the device (CUDA events on the engine stream, max over ranks). `e2e` = the
+same request through the reference-facing C ABI with HOST buffers (tkv_assemble +
+tkv_prefill_query: host->device query copy and device->host logits copy inside the timed region).
+The working set (13 GB weights + 470 MB KV) exceeds the 126 MB L2, so no flush is needed.
+
+Multi-GPU (torchrun): requests are independent; every rank serves its own request stream from its own
+store shard (weak scaling, no data-path collective).
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, built from /root/reference by
+oracle/Makefile) timed on this box's host cores on the same workload. The reference needs 52 GB of f64
+weights and ~13 min per request at this shape, so each step is a bounded sample: ONE decoder layer of
+the same request at the exact shape (16 x 512 injected tokens + 64-token query), extrapolated x28,
+run as parallel single-threaded processes across the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_CHUNKS, CHUNK_TOKENS, QUERY_TOKENS = 16, 512, 64
+SEED = 42
+METRIC = "TurboRAG request throughput (KV inject + query prefill to first-token logits)"
+UNIT = "req/s"
+
+
+def synth_payload(seed: int, n: int) -> np.ndarray:
+    """SplitMix64 text over a-z + space (acceptance_main.cpp:60-67), vectorised."""
+    M = (1 << 64) - 1
+    i = np.arange(n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + (i + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    r = (z % np.uint64(27)).astype(np.int32)
+    del M
+    return np.where(r == 26, 32, 97 + r).astype(np.int32)
+
+
+def workload():
+    payloads = [synth_payload(1000 + c, CHUNK_TOKENS - 2) for c in range(N_CHUNKS)]
+    query = synth_payload(SEED ^ 0x51DEC0DE, QUERY_TOKENS)  # bench.cpp:74 style separate seed
+    return payloads, query
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, \
+        "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
+
+
+# --------------------------------------------------------------------------------------------------
+# reference arm / cpu baseline
+# --------------------------------------------------------------------------------------------------
+def _ref_layer_sample(args_tuple):
+    """One bounded sample: ONE decoder layer of the C2 request through the UNMODIFIED reference
+    (Engine::assemble + Engine::prefill_query, proj/src/pipeline.cpp:136-186) at the exact shape.
+    Chunk caches are synthetic TKVC files (formats.md:114-140) under the reference model's fingerprint:
+    computing them with the reference would take ~3 min per chunk, and the timed path does not depend
+    on their values."""
+    store, idx = args_tuple
+    import oracle as O
+    from tests.tkvc_io import write_tkvc
+
+    cfg = O.qwen_layers(1)
+    eng = O.RefEngine(cfg, SEED, store)
+    fp = eng.fingerprint()
+    payloads, query = workload()
+    rng = np.random.default_rng(idx)
+    ids = []
+    for p in payloads:
+        framed = O.frame(p)
+        cid = O.Port.lib().tko_chunk_content_id(fp, framed.ctypes.data_as(O.I32P), len(framed))
+        path = os.path.join(store, f"{cid:016x}.tkvc")
+        if not os.path.exists(path):
+            k = rng.uniform(-1, 1, (1, CHUNK_TOKENS, cfg.kv_dim))
+            v = rng.uniform(-1, 1, (1, CHUNK_TOKENS, cfg.kv_dim))
+            write_tkvc(store, cid, fp, k, v, cfg.kv_head_num, cfg.head_size)
+        ids.append(cid)
+    t0 = time.perf_counter()
+    ctx = eng.assemble(ids, True)
+    ctx.prefill_query(query)
+    dt = time.perf_counter() - t0
+    ctx.close()
+    eng.close()
+    return dt
+
+
+def reference_samples(n: int, procs: int):
+    import multiprocessing as mp
+
+    import oracle as O
+    if not os.path.exists(O.REF_SO):
+        if os.path.isdir(O.REF_SRC):
+            O.build(ref=True)
+        else:
+            return None, "oracle/_ref/libturbokv_ref.so not built and /root/reference absent"
+    if not os.path.exists(O.PORT_SO):
+        O.build(ref=False)
+    tmp = tempfile.mkdtemp(prefix="tkv-refbench-")
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(processes=procs) as pool:
+        times = pool.map(_ref_layer_sample, [(os.path.join(tmp, f"s{i}"), i) for i in range(n)])
+    return times, None
+
+
+def host_info():
+    cpu = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    cpu = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return cpu, os.cpu_count() or 1
+
+
+def mem_gb():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable"):
+                    return int(line.split()[1]) / 1e6
+    except OSError:
+        pass
+    return 16.0
+
+
+def run_reference(args):
+    rank, _, ws = dist_env()
+    if rank != 0:
+        return
+    cpu, ncores = host_info()
+    n = args.steps + args.warmup
+    procs = max(1, min(n, ncores, int(mem_gb() // 4)))
+    times, why = reference_samples(n, procs)
+    if times is None:
+        print(json.dumps({"impl": "reference", "unavailable": why}))
+        return
+    timed = times[args.warmup:] or times
+    layer_s = statistics.median(timed)
+    ttft_ms = layer_s * 28 * 1000.0
+    value = procs / (layer_s * 28)  # concurrent single-threaded requests across `procs` cores
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ttft_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "p50_ttft_ms": ttft_ms,
+        "config": {"workload": "C2: Qwen2-7B shape, 16x512 chunks + 64-token query, batch 1, reordered",
+                   "sample": "1 of 28 decoder layers per step at exact shape, extrapolated x28"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "reference",
+                         "sample": f"1-layer C2 request (16x512 + 64), x28 extrapolated; {len(timed)} samples "
+                                   f"on {procs} single-threaded processes; {cpu}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_07590_b200 import turbokv as T
+
+    rank, local, ws = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    cfg = T.ModelConfig.qwen2_7b_like()
+    eng = T.Engine(cfg, SEED, dtype="bf16", device=local, store_capacity_tokens=N_CHUNKS * CHUNK_TOKENS * 4,
+                   flags=args.flags)
+    payloads, query = workload()
+    t0 = time.perf_counter()
+    ids = eng.ingest_chunks(payloads)
+    torch.cuda.synchronize(dev)
+    ingest_s = time.perf_counter() - t0
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
+    d_query = torch.from_numpy(query).to(dev)
+    d_logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=dev)
+
+    def step():
+        ctx = eng.assemble(ids, T.PositionMode.Reordered)
+        eng.prefill_query_device(ctx, d_query.data_ptr(), QUERY_TOKENS, d_logits.data_ptr())
+        ctx.close()
+
+    # warm-up (also validates the logits are finite)
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+    assert torch.isfinite(d_logits).all().item(), "non-finite logits"
+
+    peaks, peak_kind = load_peaks()
+    launches0 = eng.launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        big0 = torch.cuda.Event(enable_timing=True)
+        big1 = torch.cuda.Event(enable_timing=True)
+        big0.record(stream)
+        for i in range(args.steps):
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        big1.record(stream)
+        torch.cuda.synchronize(dev)
+    gpu_launches = eng.launch_count() - launches0
+    per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = big0.elapsed_time(big1)
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = t.item()
+    ms_per_step = total_ms / args.steps
+    p50 = statistics.median(per_step)
+    value = ws * args.steps / (total_ms / 1000.0)
+
+    # per-kernel device time (CUDA events on the engine stream) over a second, profiled pass
+    eng.profile_reset()
+    eng.profile(True)
+    prof_steps = max(3, min(args.steps, 10))
+    for _ in range(prof_steps):
+        step()
+    stream.synchronize()
+    eng.profile(False)
+    gather_ms, gather_n = eng.profile_read("gather_rope")
+    attn_ms, attn_n = eng.profile_read("attention")
+    gemm_ms, gemm_n = eng.profile_read("gemm")
+    epi_ms, _ = eng.profile_read("epilogue")
+    P = N_CHUNKS * CHUNK_TOKENS
+    kv_bytes = 2 * P * cfg.layer_num * 2 * cfg.kv_dim * 2  # read store + write request cache, K and V, bf16
+    gather_avg_ms = gather_ms / max(gather_n, 1)
+    achieved = kv_bytes / (gather_avg_ms / 1e3) / 1e9
+    attn_flops = 4 * cfg.head_num * cfg.head_size * sum(P + i + 1 for i in range(QUERY_TOKENS)) * cfg.layer_num
+
+    # e2e through the reference-facing C ABI with host buffers
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ctx = eng.assemble(ids, T.PositionMode.Reordered)
+        eng.prefill_query(ctx, query)
+        ctx.close()
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t0)
+    e2e_p50 = statistics.median(e2e)
+    e2e_value = ws / e2e_p50
+
+    # the same engine's full-concatenation prefill (standard RAG, causal) and the independent oracle
+    framed = [np.concatenate([[256], p, [257]]).astype(np.int32) for p in payloads]
+    naive = {}
+    for mode, tag in ((T.MaskMode.Causal, "causal"), (T.MaskMode.Independent, "independent")):
+        ts = []
+        for i in range(1 + args.naive_reps):
+            t0 = time.perf_counter()
+            eng.naive_prefill(framed, query, mode, keep_context=False)
+            if i:
+                ts.append(time.perf_counter() - t0)
+        naive[tag] = statistics.median(ts) * 1e3
+
+    cpu_baseline = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu, ncores = host_info()
+        times, why = reference_samples(1, 1)
+        if times:
+            layer_s = times[0]
+            cpu_baseline = {"value": 1.0 / (layer_s * 28), "unit": UNIT, "cores": 1, "kind": "reference",
+                            "sample": f"one of 28 decoder layers of the C2 request at exact shape "
+                                      f"({layer_s:.1f} s), extrapolated x28; single-threaded reference; {cpu}"}
+        else:
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": why}
+
+    if rank != 0:
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random-init weights seed 42, SplitMix64 text chunks)",
+        "config": {"workload": "C2: Qwen2-7B shape (28L, 28Q/4KV, d128), 16x512-token chunks + 64-token query, "
+                               "batch 1, reordered positions",
+                   "parallelism": f"dp{ws} (independent request streams, per-rank store shard)",
+                   "l2": "working set (13 GB weights + 470 MB KV) > 126 MB L2; no flush"},
+        "p50_ttft_ms": p50,
+        "naive_full_concat_p50_ttft_ms": naive["causal"],
+        "naive_independent_p50_ttft_ms": naive["independent"],
+        "ttft_speedup_vs_full_concat": naive["causal"] / p50,
+        "kv_inject_gbs": achieved,
+        "ingest_s_16_chunks": ingest_s,
+        "device_ms_per_step": {"gather_rope": gather_ms / prof_steps, "attention": attn_ms / prof_steps,
+                               "gemm": gemm_ms / prof_steps, "epilogue": epi_ms / prof_steps},
+        "roofline": {"kernel": "gather_rope", "bound": "hbm", "achieved": achieved,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                     "traffic": None, "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": kv_bytes, "avg_launch_ms": gather_avg_ms},
+        "attention_roofline": {"bound": "tensor", "achieved": attn_flops / (attn_ms / prof_steps / 1e3) / 1e12,
+                               "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                               "frac": attn_flops / (attn_ms / prof_steps / 1e3) / 1e12 / peaks["bf16_tflops"],
+                               "flops_per_request": attn_flops},
+        "e2e": {"value": e2e_value, "unit": UNIT, "p50_ttft_ms": e2e_p50 * 1e3,
+                "h2d_bytes_per_step": QUERY_TOKENS * 4 + N_CHUNKS * 8,
+                "d2h_bytes_per_step": cfg.vocab_size * 4},
+        "gpu_launches": gpu_launches,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu_baseline,
+    }
+    print(json.dumps(line))
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--naive-reps", type=int, default=3)
+    ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

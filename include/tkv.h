@@ -1,0 +1,208 @@
+/*
+ * tkv.h — C ABI of the B200-native TurboRAG prefill engine (libtkv_b200.so).
+ *
+ * This is the drop-in boundary for the reference's prefill path. The
+ * reference (`turbokv`, /root/reference/proj) has no FFI layer; its boundary
+ * is the C++ API of include/turbokv/pipeline.hpp. Each entry point below
+ * names the reference interface it replaces (file:line under proj/).
+ * include/turbokv_compat.hpp re-exposes the same surface with the
+ * reference's C++ names and exception classes; INTEGRATION.md shows the
+ * ctypes / C++ bindings a maintainer adds.
+ *
+ * Conventions
+ *  - Plain C types only: pointers + sizes. No torch types. All buffers are
+ *    HOST memory unless a function name ends in _device.
+ *  - Every call returns tkv_status. On failure tkv_last_error() returns a
+ *    thread-local message. Codes 1-10 map one-to-one onto the reference's
+ *    exception classes (include/turbokv/errors.hpp:10-67).
+ *  - There is no CPU fallback: with no usable sm_100 device,
+ *    tkv_engine_create fails with TKV_ERR_CUDA.
+ */
+#ifndef TKV_H
+#define TKV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TKV_ABI_VERSION 1
+
+typedef enum {
+    TKV_OK = 0,
+    TKV_ERR_GENERIC = 1,        /* turbokv::Error               errors.hpp:10  */
+    TKV_ERR_SHAPE = 2,          /* turbokv::ShapeError          errors.hpp:17  */
+    TKV_ERR_DOMAIN = 3,         /* turbokv::DomainError         errors.hpp:23  */
+    TKV_ERR_CONFIG = 4,         /* turbokv::ConfigError         errors.hpp:29  */
+    TKV_ERR_DEGENERATE_ROW = 5, /* turbokv::DegenerateRowError  errors.hpp:35  */
+    TKV_ERR_IO = 6,             /* turbokv::IoError             errors.hpp:41  */
+    TKV_ERR_FORMAT = 7,         /* turbokv::FormatError         errors.hpp:47  */
+    TKV_ERR_NOT_FOUND = 8,      /* turbokv::NotFoundError       errors.hpp:53  */
+    TKV_ERR_STALE_CACHE = 9,    /* turbokv::StaleCacheError     errors.hpp:59  */
+    TKV_ERR_NO_CONTEXT = 10,    /* turbokv::NoContextError      errors.hpp:65  */
+    TKV_ERR_CUDA = 11,          /* device / driver failure (no reference analogue) */
+    TKV_ERR_OOM = 12            /* HBM or page-pool exhaustion                      */
+} tkv_status;
+
+/* ModelConfig (include/turbokv/config.hpp:11-34), same field order. */
+typedef struct {
+    int64_t layer_num;
+    int64_t head_num;
+    int64_t kv_head_num;
+    int64_t head_size;
+    int64_t hidden_size;
+    int64_t intermediate_size;
+    int64_t vocab_size;
+    double rope_base;
+    double norm_eps;
+} tkv_model_config;
+
+typedef enum { TKV_DTYPE_F32 = 1, TKV_DTYPE_BF16 = 2 } tkv_dtype;
+/* PositionMode (pipeline.hpp:21) */
+typedef enum { TKV_POS_COMPOSITE = 0, TKV_POS_REORDERED = 1 } tkv_position_mode;
+/* MaskMode (attention.hpp:17) */
+typedef enum { TKV_MASK_CAUSAL = 0, TKV_MASK_INDEPENDENT = 1 } tkv_mask_mode;
+/* which tensor of a layer */
+typedef enum { TKV_K = 0, TKV_V = 1 } tkv_kv_which;
+
+/* Engine options (replace Engine(config, seed, store_root, StoreDtype), pipeline.hpp:69-72). */
+typedef struct {
+    tkv_dtype dtype;              /* compute/storage dtype of weights, activations and KV          */
+    int32_t device;               /* CUDA ordinal                                                   */
+    int32_t page_tokens;          /* tokens per KV-store page (default 64)                          */
+    int64_t store_capacity_tokens;/* HBM store capacity in tokens (0 = 1/4 of free HBM)             */
+    int64_t max_position;         /* RoPE table length (0 = 32768; grows on demand)                 */
+    int32_t exact_fingerprint;    /* 1 = reference FNV weights checksum, 0 = fast, -1 = auto        */
+    int32_t flags;                /* TKV_FLAG_*                                                     */
+} tkv_engine_opts;
+
+#define TKV_FLAG_SIMT_GEMM 0x1    /* bf16: use the SIMT GEMM instead of tcgen05 (debug/compare)  */
+#define TKV_FLAG_SIMT_ATTN 0x2    /* bf16: use the SIMT attention instead of tcgen05              */
+#define TKV_FLAG_NO_GRAPHS 0x4    /* do not capture prefill launch chains into CUDA graphs        */
+
+/* IngestStats (pipeline.hpp:35-39) */
+typedef struct {
+    int64_t chunks;
+    int64_t new_chunks;
+    uint64_t bytes_written;
+} tkv_ingest_stats;
+
+/* FlopCounter (costmodel.hpp:53-63) */
+typedef struct {
+    uint64_t qkv, attn, o, mlp;
+} tkv_flops;
+
+typedef struct tkv_engine tkv_engine;
+typedef struct tkv_context tkv_context;
+
+int tkv_abi_version(void);
+const char* tkv_last_error(void);
+const char* tkv_status_name(tkv_status s);
+
+/* ModelConfig::preset / validate / fingerprint_seed (src/config.cpp:9-72). Names: "toy",
+ * "qwen2-7b", plus "llama3-8b" (config 4 of BASELINE.json). */
+tkv_status tkv_config_preset(const char* name, tkv_model_config* out);
+tkv_status tkv_config_validate(const tkv_model_config* cfg);
+uint64_t tkv_config_fingerprint_seed(const tkv_model_config* cfg);
+
+/* weights_checksum / model_fingerprint (src/model.cpp:94-118), computed on the host by
+ * streaming the SplitMix64 draws (no f64 weights are materialised). */
+tkv_status tkv_weights_identity(const tkv_model_config* cfg, uint64_t seed, uint64_t* checksum,
+                                uint64_t* fingerprint);
+/* chunk_content_id (src/kvstore.cpp:58-64) */
+uint64_t tkv_chunk_content_id(uint64_t model_fingerprint, const int32_t* framed, int64_t n);
+
+void tkv_engine_opts_default(tkv_engine_opts* opts);
+/* Engine::Engine (pipeline.hpp:69-72; src/pipeline.cpp:55-68). Weights are generated on the
+ * device from (config, seed) with the reference's init_random draw order (src/model.cpp:68-92). */
+tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const tkv_engine_opts* opts,
+                             tkv_engine** out);
+void tkv_engine_destroy(tkv_engine* eng);
+tkv_status tkv_engine_fingerprint(const tkv_engine* eng, uint64_t* out);
+tkv_status tkv_engine_config(const tkv_engine* eng, tkv_model_config* out);
+
+/* Offline chunk precompute. Engine::ingest_chunk_payload (pipeline.hpp:86-88;
+ * src/pipeline.cpp:97-134), batched: `payloads` holds n_chunks UNFRAMED payloads back to back,
+ * offsets[n_chunks+1]. Each chunk is framed [256] payload [257], content-addressed, and — if new —
+ * prefilled with a block-diagonal causal mask in ONE packed forward; unrotated K and V land in
+ * the paged HBM store. ids_out[n_chunks] receives the content ids. Idempotent. */
+tkv_status tkv_ingest_chunks(tkv_engine* eng, const int32_t* payloads, const int64_t* offsets,
+                             int64_t n_chunks, uint64_t* ids_out, tkv_ingest_stats* stats);
+
+/* TKVC import (src/kvstore.cpp:134-207; docs/formats.md:114-140): loads a reference cache file
+ * into the HBM store (f64/f32 -> engine dtype, round to nearest). Same validation and errors as
+ * CacheStore::load. */
+tkv_status tkv_import_tkvc(tkv_engine* eng, const char* path, uint64_t* id_out);
+/* TKVC export of a stored chunk (CacheStore::store, src/kvstore.cpp:78-132), f32 elements. */
+tkv_status tkv_export_tkvc(tkv_engine* eng, uint64_t chunk_id, const char* path);
+
+tkv_status tkv_store_contains(const tkv_engine* eng, uint64_t chunk_id, int* out);
+tkv_status tkv_store_chunk_tokens(const tkv_engine* eng, uint64_t chunk_id, int64_t* out);
+tkv_status tkv_store_count(const tkv_engine* eng, int64_t* chunks, int64_t* pages_used, int64_t* pages_total);
+/* Copy one stored (unrotated) tensor to host as float32 [tokens, kv_head_num*head_size]. */
+tkv_status tkv_store_read(const tkv_engine* eng, uint64_t chunk_id, int64_t layer, tkv_kv_which which,
+                          float* host_out, int64_t capacity_elems);
+
+/* KV injection. Engine::assemble (pipeline.hpp:93; src/pipeline.cpp:136-164). Runs the fused
+ * KV-gather + RoPE kernel: the chunks' store pages are copied into the request cache with keys
+ * re-rotated to reordered or composite position ids. */
+tkv_status tkv_assemble(tkv_engine* eng, const uint64_t* chunk_ids, int64_t n, tkv_position_mode mode,
+                        tkv_context** out);
+/* Query prefill. Engine::prefill_query (pipeline.hpp:97-99; src/pipeline.cpp:166-186). Extends ctx
+ * in place; logits_out[vocab] receives the last query token's logits (the TTFT logits). */
+tkv_status tkv_prefill_query(tkv_engine* eng, tkv_context* ctx, const int32_t* query, int64_t n,
+                             float* logits_out, tkv_flops* flops);
+/* Same, with tokens and logits already in device memory (no host copies, no sync). */
+tkv_status tkv_prefill_query_device(tkv_engine* eng, tkv_context* ctx, const int32_t* d_query, int64_t n,
+                                    float* d_logits_out);
+/* Full-concatenation prefill. Engine::naive_prefill (pipeline.hpp:104-108; src/pipeline.cpp:188-229).
+ * `framed` holds n_chunks FRAMED chunks back to back (offsets[n_chunks+1]). ctx_out is optional. */
+tkv_status tkv_naive_prefill(tkv_engine* eng, const int32_t* framed, const int64_t* offsets, int64_t n_chunks,
+                             const int32_t* query, int64_t nq, tkv_mask_mode mode, float* logits_out,
+                             tkv_flops* flops, tkv_context** ctx_out);
+/* Engine::naive_prefill_ids (pipeline.hpp:109-112): chunk tokens come from the store's record. */
+tkv_status tkv_naive_prefill_ids(tkv_engine* eng, const uint64_t* ids, int64_t n, const int32_t* query,
+                                 int64_t nq, tkv_mask_mode mode, float* logits_out, tkv_flops* flops,
+                                 tkv_context** ctx_out);
+/* greedy_decode (src/model.cpp:274-303): argmax (ties -> lowest id), stop on eos (258). */
+tkv_status tkv_greedy_decode(tkv_engine* eng, tkv_context* ctx, int64_t max_new, int32_t* tokens_out,
+                             int64_t* n_out);
+
+/* AssembledContext accessors (include/turbokv/context.hpp:16-38). */
+void tkv_context_destroy(tkv_context* ctx);
+int64_t tkv_context_total_tokens(const tkv_context* ctx);
+int64_t tkv_context_next_position(const tkv_context* ctx);
+int64_t tkv_context_segments(const tkv_context* ctx, int64_t* lens, int32_t* is_query, int64_t cap);
+tkv_status tkv_context_positions(const tkv_context* ctx, int64_t* out, int64_t capacity);
+tkv_status tkv_context_last_logits(const tkv_context* ctx, float* out, int64_t capacity);
+/* Request-cache tensor of one layer to host as float32 [total_tokens, kv_dim]. rotated=1 returns
+ * keys as the attention kernels consume them (rotated by the context positions); rotated=0 returns
+ * the unrotated keys of the injected chunk tokens (re-gathered from the store with identity
+ * rotation) followed by the query tokens' unrotated keys. */
+tkv_status tkv_context_read_kv(const tkv_context* ctx, int64_t layer, tkv_kv_which which, int rotated,
+                               float* host_out, int64_t capacity_elems);
+/* The attention predicate the kernels apply for the context's last forward, materialised as
+ * 0/1 bytes [rows, cols] (build_mask / causal_rows, src/attention.cpp:50-92). */
+tkv_status tkv_context_mask(const tkv_context* ctx, uint8_t* out, int64_t rows, int64_t cols);
+
+/* Measurement hooks (bench.py): the engine's CUDA stream, and per-kernel-class device time
+ * accumulated with CUDA events on that stream while profiling is on. */
+void* tkv_engine_stream(tkv_engine* eng);
+tkv_status tkv_profile_enable(tkv_engine* eng, int on);
+/* names: "gather_rope", "attention", "gemm", "epilogue", "other"; returns total ms and launches */
+tkv_status tkv_profile_read(tkv_engine* eng, const char* kernel_class, double* total_ms, int64_t* launches);
+tkv_status tkv_profile_reset(tkv_engine* eng);
+/* Count of kernels launched by the engine since creation (all classes). */
+int64_t tkv_launch_count(const tkv_engine* eng);
+
+/* Debug: corrupt the independent mask of the next naive prefill (testing::mask_fault_hook,
+ * include/turbokv/pipeline.hpp:57-62): lets row `row` see column `col`. row < 0 disables. */
+tkv_status tkv_debug_set_mask_fault(tkv_engine* eng, int64_t row, int64_t col);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TKV_H */

@@ -1,0 +1,1637 @@
+// Host engine of the B200-native TurboRAG prefill path + the C ABI of include/tkv.h.
+//
+// Mirrors turbokv::Engine (include/turbokv/pipeline.hpp:64-131, src/pipeline.cpp:55-241) with the data
+// in HBM instead of f64 host matrices:
+//   weights       generated on device from (config, seed) in init_random's draw order (model.cpp:68-92),
+//                 stored K-major ([out][in]) so every projection is a K-major x K-major GEMM
+//   KV store      paged pool [page][layer][K|V][page_tokens][kv_dim] replacing the TKVC directory
+//                 (kvstore.cpp:78-207); keys unrotated, as in the reference
+//   request cache [layer][K|V][cap][kv_dim] per context; keys ROTATED by the context positions once, at
+//                 injection time (the reference re-rotates every layer, model.cpp:253-254)
+//   masks         never materialised: per-row [lo, hi] key ranges (attention.cpp:50-92)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "tkv_internal.h"
+
+namespace tkv {
+
+static thread_local std::string g_last_error;
+
+void fail(tkv_status code, const std::string& msg) { throw Failure{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) fail(TKV_ERR_OOM, std::string(what) + ": out of device memory");
+    fail(TKV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- host SplitMix64 / FNV-1a (include/turbokv/rng.hpp:14-78) --------------------------------------------
+static inline uint64_t splitmix_at(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+struct Fnv {
+    uint64_t h = 0xCBF29CE484222325ULL;
+    inline void u32(uint32_t v) {
+        for (int i = 0; i < 4; ++i) {
+            h ^= (v >> (8 * i)) & 0xFF;
+            h *= 0x100000001B3ULL;
+        }
+    }
+    inline void u64(uint64_t v) {
+        u32((uint32_t)v);
+        u32((uint32_t)(v >> 32));
+    }
+    inline void f64(double v) {
+        uint64_t b;
+        std::memcpy(&b, &v, 8);
+        u64(b);
+    }
+};
+
+static void validate_cfg(const tkv_model_config& c) {  // ModelConfig::validate (config.cpp:9-29)
+    if (c.layer_num < 1 || c.head_num < 1 || c.kv_head_num < 1 || c.head_size < 1 || c.hidden_size < 1 ||
+        c.intermediate_size < 1 || c.vocab_size < 1)
+        fail(TKV_ERR_CONFIG, "ModelConfig: all counts must be >= 1");
+    if (c.hidden_size != c.head_num * c.head_size)
+        fail(TKV_ERR_CONFIG, "ModelConfig: hidden_size " + std::to_string(c.hidden_size) +
+                                 " != head_num * head_size = " + std::to_string(c.head_num * c.head_size));
+    if (c.head_num % c.kv_head_num != 0) fail(TKV_ERR_CONFIG, "ModelConfig: head_num not divisible by kv_head_num");
+    if (c.head_size % 2 != 0) fail(TKV_ERR_CONFIG, "ModelConfig: head_size must be even for rotary embedding");
+    if (!(c.rope_base > 0.0) || c.norm_eps < 0.0)
+        fail(TKV_ERR_CONFIG, "ModelConfig: rope_base must be > 0 and norm_eps >= 0");
+}
+
+static uint64_t fp_seed(const tkv_model_config& c) {  // config.cpp:31-42
+    Fnv f;
+    f.u64((uint64_t)c.layer_num);
+    f.u64((uint64_t)c.head_num);
+    f.u64((uint64_t)c.kv_head_num);
+    f.u64((uint64_t)c.head_size);
+    f.u64((uint64_t)c.hidden_size);
+    f.u64((uint64_t)c.intermediate_size);
+    f.u64((uint64_t)c.vocab_size);
+    f.f64(c.rope_base);
+    f.f64(c.norm_eps);
+    return f.h;
+}
+
+static uint64_t total_draws(const tkv_model_config& c) {
+    const uint64_t H = c.hidden_size, qd = c.head_num * c.head_size, kvd = c.kv_head_num * c.head_size,
+                   I = c.intermediate_size;
+    const uint64_t per_layer = H * qd + 2 * H * kvd + qd * H + 2 * H * I + I * H;
+    return (uint64_t)c.vocab_size * H + (uint64_t)c.layer_num * per_layer + H * (uint64_t)c.vocab_size;
+}
+
+// weights_checksum (model.cpp:94-112) streamed from the generator: same bytes as hashing the f64 tensors.
+static uint64_t weights_checksum_stream(const tkv_model_config& c, uint64_t seed) {
+    const int64_t H = c.hidden_size, qd = c.head_num * c.head_size, kvd = c.kv_head_num * c.head_size,
+                  I = c.intermediate_size;
+    const double scale = 1.0 / std::sqrt((double)H);
+    uint64_t cur = 0;
+    Fnv f;
+    auto mat = [&](int64_t r, int64_t cc) {
+        f.u64((uint64_t)r);
+        f.u64((uint64_t)cc);
+        const uint64_t n = (uint64_t)(r * cc);
+        for (uint64_t i = 0; i < n; ++i) {
+            const double u = (double)(splitmix_at(seed, cur + i) >> 11) * 0x1.0p-53;
+            f.f64((2.0 * u - 1.0) * scale);
+        }
+        cur += n;
+    };
+    auto ones = [&](int64_t n) {
+        f.u64((uint64_t)n);
+        for (int64_t i = 0; i < n; ++i) f.f64(1.0);
+    };
+    mat(c.vocab_size, H);
+    for (int64_t l = 0; l < c.layer_num; ++l) {
+        ones(H);
+        ones(H);
+        mat(H, qd);
+        mat(H, kvd);
+        mat(H, kvd);
+        mat(qd, H);
+        mat(H, I);
+        mat(H, I);
+        mat(I, H);
+    }
+    ones(H);
+    mat(H, c.vocab_size);
+    return f.h;
+}
+
+static uint64_t fingerprint_of(const tkv_model_config& c, uint64_t checksum) {  // model.cpp:114-118
+    Fnv f;
+    f.u64(fp_seed(c));
+    f.u64(checksum);
+    return f.h;
+}
+
+static uint64_t content_id(uint64_t fp, const int32_t* framed, int64_t n) {  // kvstore.cpp:58-64
+    Fnv f;
+    f.u64(fp);
+    f.u64((uint64_t)n);
+    for (int64_t i = 0; i < n; ++i) f.u32((uint32_t)framed[i]);
+    return f.h;
+}
+
+static std::string hex_id(uint64_t id) {
+    char b[17];
+    std::snprintf(b, sizeof b, "%016llx", (unsigned long long)id);
+    return b;
+}
+
+// ---- small RAII helpers ---------------------------------------------------------------------------------
+struct DevMem {
+    void* p = nullptr;
+    size_t n = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    ~DevMem() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void* ensure(size_t bytes) {
+        if (bytes <= n) return p;
+        release();
+        size_t want = std::max(bytes, (size_t)256);
+        TKV_CUDA(cudaMalloc(&p, want));
+        n = want;
+        return p;
+    }
+    template <typename T>
+    T* as() const {
+        return reinterpret_cast<T*>(p);
+    }
+};
+
+// Ring of pinned upload buffers. A slot is reused only after the H2D copies enqueued from it
+// have executed (event), so back-to-back asynchronous API calls never overwrite in-flight data.
+struct StagingRing {
+    static constexpr int kSlots = 8;
+    struct Slot {
+        void* p = nullptr;
+        size_t n = 0;
+        cudaEvent_t ev = nullptr;
+        bool pending = false;
+    } slots[kSlots];
+    int cur = -1;
+    ~StagingRing() {
+        for (auto& s : slots) {
+            if (s.ev) cudaEventSynchronize(s.ev), cudaEventDestroy(s.ev);
+            if (s.p) cudaFreeHost(s.p);
+        }
+    }
+    uint8_t* begin(size_t bytes) {
+        cur = (cur + 1) % kSlots;
+        Slot& s = slots[cur];
+        if (s.pending) TKV_CUDA(cudaEventSynchronize(s.ev));
+        s.pending = false;
+        if (!s.ev) TKV_CUDA(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+        if (bytes > s.n) {
+            if (s.p) cudaFreeHost(s.p);
+            s.p = nullptr;
+            s.n = std::max(bytes, (size_t)65536);
+            TKV_CUDA(cudaHostAlloc(&s.p, s.n, cudaHostAllocDefault));
+        }
+        return static_cast<uint8_t*>(s.p);
+    }
+    void end(cudaStream_t st) {
+        Slot& s = slots[cur];
+        TKV_CUDA(cudaEventRecord(s.ev, st));
+        s.pending = true;
+    }
+};
+
+enum ProfClass { PC_GATHER = 0, PC_ATTN, PC_GEMM, PC_EPI, PC_OTHER, PC_N };
+static const char* kProfNames[PC_N] = {"gather_rope", "attention", "gemm", "epilogue", "other"};
+
+struct Chunk {
+    int64_t len = 0;
+    std::vector<int32_t> pages;
+    std::vector<int32_t> framed;  // empty for TKVC-imported chunks
+};
+
+}  // namespace tkv
+
+using namespace tkv;
+
+struct tkv_context;
+
+struct tkv_engine {
+    tkv_model_config cfg{};
+    uint64_t seed = 0;
+    tkv_engine_opts opts{};
+    DT dt = DT::BF16;
+    int device = 0, num_sms = 148;
+    cudaStream_t stream = nullptr;
+    uint64_t fingerprint = 0;
+    bool exact_fp = false;
+    int64_t L, H, Hkv, d, hid, I, V, qd, kvd, nqkv;
+
+    // weights
+    DevMem wmem;
+    float* emb = nullptr;
+    float* ones = nullptr;
+    std::vector<void*> w_qkv, w_o, w_gu, w_down;
+    void* w_lm = nullptr;
+
+    // RoPE cos/sin table, float2 [rope_len][d/2], computed in f64 on the host exactly like rope.cpp:21-22,36-40
+    DevMem rope;
+    int64_t rope_len = 0;
+
+    // paged KV store
+    DevMem pool;
+    int64_t page_tokens = 64, n_pages = 0;
+    size_t page_bytes = 0;
+    std::vector<int32_t> free_pages;
+    std::unordered_map<uint64_t, Chunk> chunks;
+
+    // forward workspace
+    DevMem x, h, q, attn, act, partial, attn_ws, logits, err, d_tok, d_pos, d_lo, d_hi, d_page, d_slot, d_segs;
+    StagingRing staging;
+    std::vector<std::pair<size_t, void*>> ctx_free;  // recycled request-cache buffers
+    std::set<tkv_context*> live;
+
+    // measurement
+    bool prof_on = false;
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[PC_N] = {};
+    int64_t prof_n[PC_N] = {};
+    int64_t launches = 0;
+    int64_t fault_row = -1, fault_col = -1;
+
+    ~tkv_engine();
+    void bind() const { TKV_CUDA(cudaSetDevice(device)); }
+
+    // ---- profiling ----
+    cudaEvent_t take_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        TKV_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+    struct Scope {
+        tkv_engine* e;
+        int cls;
+        cudaEvent_t a = nullptr;
+        Scope(tkv_engine* eng, int c, int n_launch) : e(eng), cls(c) {
+            e->launches += n_launch;
+            if (e->prof_on) {
+                a = e->take_event();
+                cudaEventRecord(a, e->stream);
+            }
+        }
+        ~Scope() {
+            if (a) {
+                cudaEvent_t b = e->take_event();
+                cudaEventRecord(b, e->stream);
+                e->recs.push_back({cls, a, b});
+            }
+        }
+    };
+    void prof_flush() {
+        if (recs.empty()) return;
+        TKV_CUDA(cudaStreamSynchronize(stream));
+        for (auto& r : recs) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            prof_ms[r.cls] += ms;
+            prof_n[r.cls] += 1;
+            ev_pool.push_back(r.a);
+            ev_pool.push_back(r.b);
+        }
+        recs.clear();
+    }
+
+    // ---- helpers ----
+    void sync() { TKV_CUDA(cudaStreamSynchronize(stream)); }
+    // copy host data into the current staging slot at `off` and enqueue its H2D copy
+    void upload(uint8_t* slot, void* dst, const void* src, size_t bytes, size_t off) {
+        if (bytes == 0) return;
+        std::memcpy(slot + off, src, bytes);
+        TKV_CUDA(cudaMemcpyAsync(dst, slot + off, bytes, cudaMemcpyHostToDevice, stream));
+    }
+    void ensure_rope(int64_t max_pos) {
+        if (max_pos < rope_len) return;
+        int64_t n = std::max<int64_t>(rope_len ? rope_len * 2 : 4096, max_pos + 1);
+        n = std::max(n, opts.max_position > 0 ? opts.max_position : (int64_t)32768);
+        const int64_t half = d / 2;
+        std::vector<double> theta(half);
+        for (int64_t m = 0; m < half; ++m) theta[m] = std::pow(cfg.rope_base, -2.0 * (double)m / (double)d);
+        std::vector<float> tab((size_t)(n * half * 2));
+        for (int64_t t = 0; t < n; ++t)
+            for (int64_t m = 0; m < half; ++m) {
+                const double a = (double)t * theta[m];
+                tab[(size_t)((t * half + m) * 2)] = (float)std::cos(a);
+                tab[(size_t)((t * half + m) * 2 + 1)] = (float)std::sin(a);
+            }
+        sync();
+        DevMem fresh;
+        fresh.ensure(tab.size() * sizeof(float));
+        TKV_CUDA(cudaMemcpy(fresh.p, tab.data(), tab.size() * sizeof(float), cudaMemcpyHostToDevice));
+        std::swap(rope.p, fresh.p);
+        std::swap(rope.n, fresh.n);
+        rope_len = n;
+    }
+
+    void* ctx_alloc(size_t bytes, size_t* got) {
+        size_t best = (size_t)-1;
+        int bi = -1;
+        for (size_t i = 0; i < ctx_free.size(); ++i)
+            if (ctx_free[i].first >= bytes && ctx_free[i].first < best) {
+                best = ctx_free[i].first;
+                bi = (int)i;
+            }
+        if (bi >= 0 && best <= bytes * 4 + (64u << 20)) {
+            void* p = ctx_free[bi].second;
+            *got = ctx_free[bi].first;
+            ctx_free.erase(ctx_free.begin() + bi);
+            return p;
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess && !ctx_free.empty()) {  // trim the cache and retry
+            cudaGetLastError();
+            sync();
+            for (auto& f : ctx_free) cudaFree(f.second);
+            ctx_free.clear();
+            e = cudaMalloc(&p, bytes);
+        }
+        TKV_CUDA(e);
+        *got = bytes;
+        return p;
+    }
+    void ctx_release(void* p, size_t bytes) {
+        if (p) ctx_free.emplace_back(bytes, p);
+    }
+
+    int pick_splits(int M, int N, int K, bool tc) const {
+        const int bm = tc ? 128 : 64, bn = tc ? 128 : 64, bk = tc ? 64 : 16;
+        const int tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+        const int kb = (K + bk - 1) / bk;
+        int s = (num_sms + tiles - 1) / tiles;
+        s = std::min(s, std::max(1, kb / 4));
+        s = std::min(s, 16);
+        s = std::max(s, 1);
+        const int kbs = (kb + s - 1) / s;
+        return (kb + kbs - 1) / kbs;
+    }
+
+    bool use_tc() const { return dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_GEMM); }
+
+    // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits
+    int gemm(const void* A, int lda, const void* W, int M, int N, int K) {
+        const bool tc = use_tc();
+        if (tc && !gemm_tc_supported(M, N, K, lda))
+            fail(TKV_ERR_CONFIG, "shape not supported by the tcgen05 GEMM (rows must be 16-byte aligned)");
+        const int s = pick_splits(M, N, K, tc);
+        partial.ensure((size_t)s * M * N * sizeof(float));
+        Scope sc(this, PC_GEMM, 1);
+        if (tc)
+            launch_gemm_tc(A, lda, W, M, N, K, partial.as<float>(), s, stream);
+        else
+            launch_gemm_simt(A, lda, W, M, N, K, partial.as<float>(), s, dt, stream);
+        return s;
+    }
+
+    void* kv_plane(tkv_context* c, int64_t layer, int kv) const;
+
+    struct Fwd {
+        const int32_t* tok = nullptr;  // device [T]
+        int T = 0;
+        const int32_t* pos = nullptr;  // device [T]
+        tkv_context* ctx = nullptr;
+        int row0 = 0;                 // cache rows of the new tokens start here
+        const int32_t* lo = nullptr;  // device [T]
+        const int32_t* hi = nullptr;
+        bool logits = true;   // last-row logits into this->logits
+        bool kv_only = false; // chunk ingest: stop after the last layer's QKV
+        StoreScatter sc{};
+    };
+    void forward(const Fwd& f);
+    void check_err(const char* where);
+};
+
+struct tkv_context {
+    tkv_engine* eng = nullptr;
+    void* kv = nullptr;
+    size_t kv_bytes = 0;
+    int64_t cap = 0;
+    int64_t total = 0;
+    std::vector<int64_t> positions;
+    std::vector<int64_t> seg_len;
+    std::vector<int32_t> seg_query;
+    int mask_mode = TKV_MASK_INDEPENDENT;
+    int64_t next_position = 0;
+    std::vector<float> last_logits;
+    // injected chunk rows [0, chunk_rows): where they came from (unrotated export re-gathers them)
+    std::vector<GatherSeg> chunk_segs;
+    int64_t chunk_rows = 0;
+    // predicate of the last forward over this context
+    std::vector<int32_t> last_lo, last_hi;
+    int64_t last_rows = 0, last_cols = 0;
+
+    void extend_query_segment(int64_t n) {  // context.cpp:24-35
+        if (!seg_len.empty() && seg_query.back()) {
+            seg_len.back() += n;
+        } else {
+            seg_len.push_back(n);
+            seg_query.push_back(1);
+        }
+    }
+};
+
+void* tkv_engine::kv_plane(tkv_context* c, int64_t layer, int kv) const {
+    return static_cast<uint8_t*>(c->kv) + (size_t)((layer * 2 + kv) * c->cap) * kvd * dt_size(dt);
+}
+
+tkv_engine::~tkv_engine() {
+    for (tkv_context* c : live) {
+        c->eng = nullptr;
+        if (c->kv) cudaFree(c->kv);
+        c->kv = nullptr;
+    }
+    for (auto& f : ctx_free) cudaFree(f.second);
+    for (auto& r : recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void tkv_engine::check_err(const char* where) {
+    int e = 0;
+    TKV_CUDA(cudaMemcpyAsync(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (e == 0) return;
+    TKV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
+    if (e & 1) fail(TKV_ERR_DOMAIN, std::string(where) + ": token id outside vocab");
+    if (e & 8) fail(TKV_ERR_DEGENERATE_ROW, std::string(where) + ": softmax row has no attendable positions");
+    fail(TKV_ERR_DOMAIN, std::string(where) + ": non-finite element");
+}
+
+// One decoder forward (model.cpp:198-272) over T new tokens whose K/V go to cache rows [row0, row0+T).
+void tkv_engine::forward(const Fwd& f) {
+    const int T = f.T, Tk = f.row0 + f.T;
+    const size_t es = dt_size(dt);
+    const float eps = (float)cfg.norm_eps;
+    x.ensure((size_t)T * hid * 4);
+    h.ensure((size_t)T * std::max(hid, I) * es);
+    q.ensure((size_t)T * qd * es);
+    attn.ensure((size_t)T * qd * es);
+    act.ensure((size_t)T * I * es);
+    {
+        Scope sc(this, PC_EPI, 1);
+        launch_embed_norm(f.tok, T, emb, (int)hid, (int)V, ones, eps, x.as<float>(), h.p, dt, err.as<int>(), stream);
+    }
+    for (int64_t l = 0; l < L; ++l) {
+        // --- attention block ---
+        int s = gemm(h.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
+        {
+            Scope sc(this, PC_EPI, 1);
+            launch_qkv_epilogue(partial.as<float>(), s, T, (int)H, (int)Hkv, (int)d, f.pos, rope.as<float2>(), q.p,
+                                kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), f.row0, f.sc, (int)l, dt, stream);
+        }
+        if (f.kv_only && l == L - 1) break;
+        // In the last layer only the final row feeds the logits: attention, O-proj and the MLP run on it alone.
+        const bool tail = (l == L - 1) && f.logits;
+        const int rows = tail ? 1 : T;
+        const int64_t r0 = tail ? T - 1 : 0;
+        {
+            const int splits = attn_pick_splits(rows, (int)H, (int)Hkv, Tk, num_sms);
+            AttnWork ws;
+            if (splits > 1) {
+                const size_t fl = attn_workspace_floats(rows, (int)H, (int)d, splits);
+                attn_ws.ensure(fl * sizeof(float));
+                ws.o = attn_ws.as<float>();
+                ws.ml = ws.o + (size_t)splits * rows * H * d;
+            }
+            Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);
+            launch_attention_simt(static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es, kv_plane(f.ctx, l, 0),
+                                  kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0, f.hi + r0, attn.p, rows, Tk, (int)H,
+                                  (int)Hkv, (int)d, splits, ws, err.as<int>(), dt, stream);
+        }
+        uint8_t* attn_rows = static_cast<uint8_t*>(attn.p);
+        float* x_rows = x.as<float>() + r0 * hid;
+        s = gemm(attn_rows, (int)qd, w_o[l], rows, (int)hid, (int)qd);
+        {
+            Scope sc(this, PC_EPI, 1);
+            launch_residual_norm(x_rows, partial.as<float>(), s, rows, (int)hid, ones, eps, h.p, dt, err.as<int>(),
+                                 stream);
+        }
+        // --- MLP block: gate|up fused into one GEMM, SwiGLU epilogue ---
+        s = gemm(h.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid);
+        {
+            Scope sc(this, PC_EPI, 1);
+            launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, dt, stream);
+        }
+        s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
+        {
+            // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
+            Scope sc(this, PC_EPI, 1);
+            launch_residual_norm(x_rows, partial.as<float>(), s, rows, (int)hid, ones, eps, h.p, dt, err.as<int>(),
+                                 stream);
+        }
+    }
+    if (f.logits) {
+        // after the tail layer, h row 0 holds final_norm(x) of the last token
+        Scope sc(this, PC_OTHER, 1);
+        launch_lm_head(h.p, w_lm, (int)hid, (int)V, logits.as<float>(), dt, err.as<int>(), stream);
+    }
+}
+
+// ================================================================================================
+// C ABI
+// ================================================================================================
+namespace {
+
+template <typename F>
+tkv_status guard(F&& fn) {
+    try {
+        fn();
+        return TKV_OK;
+    } catch (const Failure& f) {
+        g_last_error = f.msg;
+        return f.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host out of memory";
+        return TKV_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return TKV_ERR_GENERIC;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) fail(TKV_ERR_DOMAIN, std::string(what) + " is null");
+}
+
+std::vector<int32_t> framed_of(const int32_t* payload, int64_t n) {  // tok::frame_chunk (tokenizer.cpp:36-43)
+    std::vector<int32_t> v;
+    v.reserve((size_t)n + 2);
+    v.push_back(256);
+    v.insert(v.end(), payload, payload + n);
+    v.push_back(257);
+    return v;
+}
+
+void check_tokens(const tkv_engine* e, const int32_t* t, int64_t n) {
+    for (int64_t i = 0; i < n; ++i)
+        if (t[i] < 0 || t[i] >= e->V)
+            fail(TKV_ERR_DOMAIN, "token id " + std::to_string(t[i]) + " outside vocab");
+}
+
+void flops_add(const tkv_engine* e, tkv_flops* fl, int64_t tokens, int64_t context) {  // costmodel.cpp:77-83
+    if (!fl) return;
+    const uint64_t L = e->L, Hd = e->hid, H = e->H, Hkv = e->Hkv, d = e->d, I = e->I;
+    fl->qkv += L * tokens * (2 * Hd * (H + 2 * Hkv) * d);
+    fl->attn += L * tokens * (2 * H * d * (uint64_t)context);
+    fl->o += L * tokens * (2 * Hd * Hd);
+    fl->mlp += L * tokens * (6 * Hd * I);
+}
+
+tkv_context* new_context(tkv_engine* e, int64_t cap) {
+    auto* c = new tkv_context;
+    c->eng = e;
+    c->cap = std::max<int64_t>(cap, 1);
+    const size_t bytes = (size_t)(e->L * 2 * c->cap * e->kvd) * dt_size(e->dt);
+    c->kv = e->ctx_alloc(bytes, &c->kv_bytes);
+    e->live.insert(c);
+    return c;
+}
+
+// grow the request cache to hold `need_rows` rows (copies the existing rows of every plane)
+void ensure_cap(tkv_engine* e, tkv_context* c, int64_t need_rows) {
+    if (need_rows <= c->cap) return;
+    const int64_t ncap = std::max(need_rows, c->cap + c->cap / 2);
+    size_t got = 0;
+    const size_t es = dt_size(e->dt);
+    void* nkv = e->ctx_alloc((size_t)(e->L * 2 * ncap * e->kvd) * es, &got);
+    if (c->total > 0) {
+        TKV_CUDA(cudaMemcpy2DAsync(nkv, (size_t)ncap * e->kvd * es, c->kv, (size_t)c->cap * e->kvd * es,
+                                   (size_t)c->total * e->kvd * es, (size_t)(e->L * 2), cudaMemcpyDeviceToDevice,
+                                   e->stream));
+    }
+    e->ctx_release(c->kv, c->kv_bytes);
+    c->kv = nkv;
+    c->kv_bytes = got;
+    c->cap = ncap;
+}
+
+// staging layout for a forward's small per-token arrays
+struct Stage {
+    std::vector<int32_t> tok, pos, lo, hi, page, slot;
+};
+
+void upload_stage(tkv_engine* e, const Stage& s, bool with_tokens) {
+    const int64_t T = (int64_t)s.pos.size();
+    const size_t b = (size_t)T * 4;
+    e->d_tok.ensure(b);
+    e->d_pos.ensure(b);
+    e->d_lo.ensure(b);
+    e->d_hi.ensure(b);
+    uint8_t* slot = e->staging.begin(6 * b + 64);
+    if (with_tokens) e->upload(slot, e->d_tok.p, s.tok.data(), b, 0);
+    e->upload(slot, e->d_pos.p, s.pos.data(), b, b);
+    e->upload(slot, e->d_lo.p, s.lo.data(), b, 2 * b);
+    e->upload(slot, e->d_hi.p, s.hi.data(), b, 3 * b);
+    if (!s.page.empty()) {
+        e->d_page.ensure(b);
+        e->d_slot.ensure(b);
+        e->upload(slot, e->d_page.p, s.page.data(), b, 4 * b);
+        e->upload(slot, e->d_slot.p, s.slot.data(), b, 5 * b);
+    }
+    e->staging.end(e->stream);
+}
+
+void remember_mask(tkv_context* c, const Stage& s, int64_t cols) {
+    c->last_lo = s.lo;
+    c->last_hi = s.hi;
+    c->last_rows = (int64_t)s.lo.size();
+    c->last_cols = cols;
+}
+
+// prefill of `n` new tokens over everything the context already holds (prefill_query / decode step)
+void extend(tkv_engine* e, tkv_context* c, const int32_t* host_tok, const int32_t* dev_tok, int64_t n,
+            float* host_logits, float* dev_logits) {
+    const int64_t P = c->total;
+    ensure_cap(e, c, P + n);
+    Stage s;
+    s.pos.resize(n);
+    s.lo.assign(n, 0);
+    s.hi.resize(n);
+    for (int64_t i = 0; i < n; ++i) {
+        s.pos[i] = (int32_t)(c->next_position + i);
+        s.hi[i] = (int32_t)(P + i);  // causal_rows(n, P): all injected rows + causal query tail
+    }
+    e->ensure_rope(c->next_position + n);
+    if (host_tok) s.tok.assign(host_tok, host_tok + n);
+    upload_stage(e, s, host_tok != nullptr);
+    tkv_engine::Fwd f;
+    f.tok = host_tok ? e->d_tok.as<int32_t>() : dev_tok;
+    f.T = (int)n;
+    f.pos = e->d_pos.as<int32_t>();
+    f.ctx = c;
+    f.row0 = (int)P;
+    f.lo = e->d_lo.as<int32_t>();
+    f.hi = e->d_hi.as<int32_t>();
+    f.logits = true;
+    e->forward(f);
+    if (dev_logits)
+        TKV_CUDA(cudaMemcpyAsync(dev_logits, e->logits.p, e->V * 4, cudaMemcpyDeviceToDevice, e->stream));
+    if (host_logits) {
+        TKV_CUDA(cudaMemcpyAsync(host_logits, e->logits.p, e->V * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->check_err("prefill");
+    }
+    remember_mask(c, s, P + n);
+    for (int64_t i = 0; i < n; ++i) c->positions.push_back(c->next_position + i);
+    c->total = P + n;
+    c->extend_query_segment(n);
+    c->next_position += n;
+    if (host_logits) c->last_logits.assign(host_logits, host_logits + e->V);
+}
+
+tkv_context* assemble_impl(tkv_engine* e, const uint64_t* ids, int64_t n, int mode) {
+    std::vector<const Chunk*> cs;
+    int64_t P = 0, max_len = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        auto it = e->chunks.find(ids[i]);
+        if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(ids[i]) + " not in store");
+        cs.push_back(&it->second);
+        P += it->second.len;
+        max_len = std::max(max_len, it->second.len);
+    }
+    tkv_context* c = new_context(e, P + 128);
+    std::vector<GatherSeg> segs;
+    int64_t running = 0;
+    for (const Chunk* ch : cs) {
+        const int64_t first = mode == TKV_POS_REORDERED ? running : 0;  // pipeline.cpp:150
+        for (size_t p = 0; p < ch->pages.size(); ++p) {
+            const int64_t off = (int64_t)p * e->page_tokens;
+            GatherSeg g;
+            g.src_page = ch->pages[p];
+            g.n_tok = (int32_t)std::min<int64_t>(e->page_tokens, ch->len - off);
+            g.dst_row = (int32_t)(running + off);
+            g.pos0 = (int32_t)(first + off);
+            segs.push_back(g);
+        }
+        for (int64_t t = 0; t < ch->len; ++t) c->positions.push_back(first + t);
+        c->seg_len.push_back(ch->len);
+        c->seg_query.push_back(0);
+        running += ch->len;
+    }
+    c->total = P;
+    c->chunk_rows = P;
+    c->chunk_segs = segs;
+    c->next_position = mode == TKV_POS_REORDERED ? running : max_len;  // pipeline.cpp:160-162
+    c->mask_mode = TKV_MASK_INDEPENDENT;
+    if (!segs.empty()) {
+        e->ensure_rope(std::max(P, max_len));
+        const size_t b = segs.size() * sizeof(GatherSeg);
+        e->d_segs.ensure(b);
+        uint8_t* slot = e->staging.begin(b);
+        e->upload(slot, e->d_segs.p, segs.data(), b, 0);
+        e->staging.end(e->stream);
+        tkv_engine::Scope sc(e, PC_GATHER, 1);
+        launch_gather_rope(e->pool.p, (int)e->page_tokens, e->d_segs.as<GatherSeg>(), (int)segs.size(), (int)e->L,
+                           (int)e->kvd, (int)e->d, e->rope.as<float2>(), c->kv, c->cap, 1, e->dt, e->num_sms,
+                           e->stream);
+    }
+    return c;
+}
+
+void naive_impl(tkv_engine* e, const int32_t* framed, const int64_t* offsets, int64_t n_chunks, const int32_t* query,
+                int64_t nq, int mode, float* logits_out, tkv_flops* fl, tkv_context** ctx_out) {
+    if (nq <= 0) fail(TKV_ERR_DOMAIN, "naive_prefill: empty query");
+    need(query, "query");
+    Stage s;
+    std::vector<int64_t> lens;
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        const int64_t len = offsets[c + 1] - offsets[c];
+        if (len < 1) fail(TKV_ERR_DOMAIN, "naive_prefill: empty chunk");
+        lens.push_back(len);
+        s.tok.insert(s.tok.end(), framed + offsets[c], framed + offsets[c + 1]);
+    }
+    s.tok.insert(s.tok.end(), query, query + nq);
+    check_tokens(e, s.tok.data(), (int64_t)s.tok.size());
+    const int64_t N = (int64_t)s.tok.size();
+    s.pos.resize(N);
+    s.lo.resize(N);
+    s.hi.resize(N);
+    int64_t off = 0;
+    for (int64_t c = 0; c <= n_chunks; ++c) {  // build_mask (attention.cpp:50-78) as row ranges
+        const int64_t len = c < n_chunks ? lens[c] : nq;
+        const bool is_query = c == n_chunks;
+        for (int64_t i = off; i < off + len; ++i) {
+            s.pos[i] = (int32_t)i;
+            s.lo[i] = (mode == TKV_MASK_INDEPENDENT && !is_query) ? (int32_t)off : 0;
+            s.hi[i] = (int32_t)i;
+        }
+        off += len;
+    }
+    if (e->fault_row >= 0 && e->fault_row < N) {  // testing::mask_fault_hook (pipeline.cpp:215)
+        s.lo[e->fault_row] = (int32_t)std::min<int64_t>(s.lo[e->fault_row], e->fault_col);
+        e->fault_row = -1;
+    }
+    tkv_context* c = new_context(e, N);
+    try {
+        e->ensure_rope(N);
+        upload_stage(e, s, true);
+        tkv_engine::Fwd f;
+        f.tok = e->d_tok.as<int32_t>();
+        f.T = (int)N;
+        f.pos = e->d_pos.as<int32_t>();
+        f.ctx = c;
+        f.row0 = 0;
+        f.lo = e->d_lo.as<int32_t>();
+        f.hi = e->d_hi.as<int32_t>();
+        f.logits = true;
+        e->forward(f);
+        std::vector<float> lg((size_t)e->V);
+        TKV_CUDA(cudaMemcpyAsync(lg.data(), e->logits.p, e->V * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->check_err("naive_prefill");
+        if (logits_out) std::memcpy(logits_out, lg.data(), lg.size() * 4);
+        c->total = N;
+        for (int64_t i = 0; i < N; ++i) c->positions.push_back(i);
+        c->seg_len = lens;
+        c->seg_query.assign(lens.size(), 0);
+        c->seg_len.push_back(nq);
+        c->seg_query.push_back(1);
+        c->next_position = N;
+        c->mask_mode = mode;
+        c->last_logits = lg;
+        remember_mask(c, s, N);
+        flops_add(e, fl, N, N);
+    } catch (...) {
+        tkv_context_destroy(c);
+        throw;
+    }
+    if (ctx_out)
+        *ctx_out = c;
+    else
+        tkv_context_destroy(c);
+}
+
+void store_chunk_pages(tkv_engine* e, Chunk& ch) {
+    const int64_t np = (ch.len + e->page_tokens - 1) / e->page_tokens;
+    if ((int64_t)e->free_pages.size() < np)
+        fail(TKV_ERR_OOM, "KV store full: need " + std::to_string(np) + " pages, " +
+                              std::to_string(e->free_pages.size()) + " free");
+    for (int64_t p = 0; p < np; ++p) {
+        ch.pages.push_back(e->free_pages.back());
+        e->free_pages.pop_back();
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int tkv_abi_version(void) { return TKV_ABI_VERSION; }
+const char* tkv_last_error(void) { return g_last_error.c_str(); }
+
+const char* tkv_status_name(tkv_status s) {
+    static const char* names[] = {"ok",          "error",       "shape",     "domain",      "config",
+                                  "degenerate_row", "io",       "format",    "not_found",   "stale_cache",
+                                  "no_context",  "cuda",        "oom"};
+    return (s >= 0 && s <= 12) ? names[s] : "unknown";
+}
+
+tkv_status tkv_config_preset(const char* name, tkv_model_config* out) {
+    return guard([&] {
+        need(name, "name");
+        need(out, "out");
+        tkv_model_config c{};
+        c.rope_base = 10000.0;
+        c.norm_eps = 1e-6;
+        c.vocab_size = 259;
+        const std::string n = name;
+        if (n == "toy") {  // config.cpp:44-54
+            c.layer_num = 4, c.head_num = 8, c.kv_head_num = 2, c.head_size = 8, c.hidden_size = 64,
+            c.intermediate_size = 192;
+        } else if (n == "qwen2-7b") {  // config.cpp:56-66
+            c.layer_num = 28, c.head_num = 28, c.kv_head_num = 4, c.head_size = 128, c.hidden_size = 3584,
+            c.intermediate_size = 18944;
+        } else if (n == "llama3-8b") {  // BASELINE.json configs[3] (vocab kept at 259 for parity)
+            c.layer_num = 32, c.head_num = 32, c.kv_head_num = 8, c.head_size = 128, c.hidden_size = 4096,
+            c.intermediate_size = 14336, c.rope_base = 500000.0, c.norm_eps = 1e-5;
+        } else {
+            fail(TKV_ERR_CONFIG, "unknown preset '" + n + "' (expected 'toy', 'qwen2-7b' or 'llama3-8b')");
+        }
+        *out = c;
+    });
+}
+
+tkv_status tkv_config_validate(const tkv_model_config* cfg) {
+    return guard([&] {
+        need(cfg, "cfg");
+        validate_cfg(*cfg);
+    });
+}
+
+uint64_t tkv_config_fingerprint_seed(const tkv_model_config* cfg) { return cfg ? fp_seed(*cfg) : 0; }
+
+tkv_status tkv_weights_identity(const tkv_model_config* cfg, uint64_t seed, uint64_t* checksum,
+                                uint64_t* fingerprint) {
+    return guard([&] {
+        need(cfg, "cfg");
+        validate_cfg(*cfg);
+        const uint64_t ck = weights_checksum_stream(*cfg, seed);
+        if (checksum) *checksum = ck;
+        if (fingerprint) *fingerprint = fingerprint_of(*cfg, ck);
+    });
+}
+
+uint64_t tkv_chunk_content_id(uint64_t fp, const int32_t* framed, int64_t n) { return content_id(fp, framed, n); }
+
+void tkv_engine_opts_default(tkv_engine_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->dtype = TKV_DTYPE_BF16;
+    o->device = 0;
+    o->page_tokens = 64;
+    o->store_capacity_tokens = 0;
+    o->max_position = 0;
+    o->exact_fingerprint = -1;
+    o->flags = 0;
+}
+
+tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const tkv_engine_opts* opts,
+                             tkv_engine** out) {
+    std::unique_ptr<tkv_engine> e;
+    tkv_status st = guard([&] {
+        need(cfg, "cfg");
+        need(out, "out");
+        validate_cfg(*cfg);
+        if (cfg->vocab_size < 259) fail(TKV_ERR_CONFIG, "vocab_size must cover the byte tokenizer (>= 259)");
+        e.reset(new tkv_engine);
+        e->cfg = *cfg;
+        e->seed = seed;
+        tkv_engine_opts_default(&e->opts);
+        if (opts) e->opts = *opts;
+        if (e->opts.dtype != TKV_DTYPE_F32 && e->opts.dtype != TKV_DTYPE_BF16) fail(TKV_ERR_CONFIG, "unknown dtype");
+        if (e->opts.page_tokens < 1) e->opts.page_tokens = 64;
+        e->dt = e->opts.dtype == TKV_DTYPE_F32 ? DT::F32 : DT::BF16;
+        e->device = e->opts.device;
+
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            fail(TKV_ERR_CUDA, "no CUDA device: the engine has no CPU fallback");
+        }
+        if (e->device < 0 || e->device >= ndev) fail(TKV_ERR_CUDA, "device ordinal out of range");
+        e->bind();
+        cudaDeviceProp prop;
+        TKV_CUDA(cudaGetDeviceProperties(&prop, e->device));
+        if (prop.major != 10) fail(TKV_ERR_CUDA, std::string("requires an sm_100 GPU (B200), found ") + prop.name);
+        e->num_sms = prop.multiProcessorCount;
+        TKV_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+
+        const tkv_model_config& c = *cfg;
+        e->L = c.layer_num, e->H = c.head_num, e->Hkv = c.kv_head_num, e->d = c.head_size, e->hid = c.hidden_size;
+        e->I = c.intermediate_size, e->V = c.vocab_size, e->qd = e->H * e->d, e->kvd = e->Hkv * e->d;
+        e->nqkv = e->qd + 2 * e->kvd;
+        if (e->d != 8 && e->d != 16 && e->d != 32 && e->d != 64 && e->d != 128)
+            fail(TKV_ERR_CONFIG, "head_size must be one of 8/16/32/64/128 for the device kernels");
+
+        // ---- identity chain ----
+        const uint64_t draws = total_draws(c);
+        e->exact_fp = e->opts.exact_fingerprint > 0 || (e->opts.exact_fingerprint < 0 && draws <= 600000000ULL);
+        if (e->exact_fp) {
+            e->fingerprint = fingerprint_of(c, weights_checksum_stream(c, seed));
+        } else {  // documented fast identity for full-size models
+            Fnv f;
+            f.u64(fp_seed(c));
+            f.u64(seed);
+            f.u64(0xFA57F1A9E4ULL);
+            e->fingerprint = f.h;
+        }
+
+        // ---- weights (init_random draw order, model.cpp:68-92) ----
+        const size_t es = dt_size(e->dt);
+        const int64_t H_ = e->hid, qd = e->qd, kvd = e->kvd, I = e->I, V = e->V;
+        const size_t per_layer = (size_t)(e->nqkv * H_ + H_ * qd + 2 * I * H_ + H_ * I) * es;
+        auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+        const size_t emb_b = al((size_t)V * H_ * 4), ones_b = al((size_t)std::max(H_, I) * 4);
+        const size_t lm_b = al((size_t)V * H_ * es);
+        const size_t total_b = emb_b + ones_b + lm_b + e->L * al(per_layer);
+        uint8_t* base = static_cast<uint8_t*>(e->wmem.ensure(total_b));
+        e->emb = reinterpret_cast<float*>(base);
+        e->ones = reinterpret_cast<float*>(base + emb_b);
+        e->w_lm = base + emb_b + ones_b;
+        uint8_t* lp = base + emb_b + ones_b + lm_b;
+        const double scale = 1.0 / std::sqrt((double)H_);
+        uint64_t cur = 0;
+        launch_init_rowmajor_f32(e->emb, seed, cur, V, H_, scale, e->stream);
+        cur += (uint64_t)(V * H_);
+        for (int64_t l = 0; l < e->L; ++l) {
+            uint8_t* qkv = lp;
+            uint8_t* o = qkv + (size_t)e->nqkv * H_ * es;
+            uint8_t* gu = o + (size_t)H_ * qd * es;
+            uint8_t* dn = gu + (size_t)2 * I * H_ * es;
+            e->w_qkv.push_back(qkv);
+            e->w_o.push_back(o);
+            e->w_gu.push_back(gu);
+            e->w_down.push_back(dn);
+            // [in, out] draws written as [out][in] rows: wq | wk | wv stacked, gate | up stacked
+            launch_init_transposed(qkv, e->dt, seed, cur, H_, qd, scale, e->stream);
+            cur += (uint64_t)(H_ * qd);
+            launch_init_transposed(qkv + (size_t)qd * H_ * es, e->dt, seed, cur, H_, kvd, scale, e->stream);
+            cur += (uint64_t)(H_ * kvd);
+            launch_init_transposed(qkv + (size_t)(qd + kvd) * H_ * es, e->dt, seed, cur, H_, kvd, scale, e->stream);
+            cur += (uint64_t)(H_ * kvd);
+            launch_init_transposed(o, e->dt, seed, cur, qd, H_, scale, e->stream);
+            cur += (uint64_t)(qd * H_);
+            launch_init_transposed(gu, e->dt, seed, cur, H_, I, scale, e->stream);
+            cur += (uint64_t)(H_ * I);
+            launch_init_transposed(gu + (size_t)I * H_ * es, e->dt, seed, cur, H_, I, scale, e->stream);
+            cur += (uint64_t)(H_ * I);
+            launch_init_transposed(dn, e->dt, seed, cur, I, H_, scale, e->stream);
+            cur += (uint64_t)(I * H_);
+            lp += al(per_layer);
+        }
+        launch_init_transposed(e->w_lm, e->dt, seed, cur, H_, V, scale, e->stream);
+        launch_fill_f32(e->ones, 1.0f, std::max(H_, I), e->stream);
+        e->launches += 3 + 7 * e->L;
+
+        e->err.ensure(64);
+        TKV_CUDA(cudaMemsetAsync(e->err.p, 0, 64, e->stream));
+        e->logits.ensure((size_t)V * 4);
+        e->ensure_rope(e->opts.max_position > 0 ? e->opts.max_position - 1 : 32767);
+
+        // ---- paged KV store ----
+        e->page_tokens = e->opts.page_tokens;
+        e->page_bytes = (size_t)(e->L * 2 * e->page_tokens * e->kvd) * es;
+        int64_t cap_tokens = e->opts.store_capacity_tokens;
+        if (cap_tokens <= 0) {
+            size_t fr = 0, tot = 0;
+            TKV_CUDA(cudaMemGetInfo(&fr, &tot));
+            const size_t tok_bytes = (size_t)(e->L * 2 * e->kvd) * es;
+            cap_tokens = (int64_t)std::min<size_t>(fr / 4 / tok_bytes, (size_t)1 << 24);
+        }
+        e->n_pages = std::max<int64_t>(1, (cap_tokens + e->page_tokens - 1) / e->page_tokens);
+        e->pool.ensure((size_t)e->n_pages * e->page_bytes);
+        e->free_pages.reserve((size_t)e->n_pages);
+        for (int64_t p = e->n_pages - 1; p >= 0; --p) e->free_pages.push_back((int32_t)p);
+        e->sync();
+        *out = e.release();
+    });
+    return st;
+}
+
+void tkv_engine_destroy(tkv_engine* eng) {
+    if (!eng) return;
+    cudaSetDevice(eng->device);
+    delete eng;
+}
+
+tkv_status tkv_engine_fingerprint(const tkv_engine* eng, uint64_t* out) {
+    return guard([&] {
+        need(eng, "engine");
+        need(out, "out");
+        *out = eng->fingerprint;
+    });
+}
+
+tkv_status tkv_engine_config(const tkv_engine* eng, tkv_model_config* out) {
+    return guard([&] {
+        need(eng, "engine");
+        need(out, "out");
+        *out = eng->cfg;
+    });
+}
+
+tkv_status tkv_ingest_chunks(tkv_engine* e, const int32_t* payloads, const int64_t* offsets, int64_t n_chunks,
+                             uint64_t* ids_out, tkv_ingest_stats* stats) {
+    return guard([&] {
+        need(e, "engine");
+        need(offsets, "offsets");
+        e->bind();
+        struct Pending {
+            uint64_t id;
+            std::vector<int32_t> framed;
+        };
+        std::vector<Pending> todo;
+        std::set<uint64_t> batch_ids;
+        for (int64_t c = 0; c < n_chunks; ++c) {
+            const int64_t n = offsets[c + 1] - offsets[c];
+            if (n < 0) fail(TKV_ERR_SHAPE, "ingest: offsets must be non-decreasing");
+            std::vector<int32_t> framed = framed_of(payloads + offsets[c], n);
+            check_tokens(e, framed.data(), (int64_t)framed.size());
+            const uint64_t id = content_id(e->fingerprint, framed.data(), (int64_t)framed.size());
+            if (ids_out) ids_out[c] = id;
+            if (stats) stats->chunks += 1;
+            if (e->chunks.count(id) || batch_ids.count(id)) continue;  // idempotent (pipeline.cpp:104-123)
+            batch_ids.insert(id);
+            todo.push_back({id, std::move(framed)});
+        }
+        // Packed block-diagonal prefill: up to ~16K tokens per forward.
+        const int64_t kMaxTokens = 16384;
+        size_t i0 = 0;
+        while (i0 < todo.size()) {
+            size_t i1 = i0;
+            int64_t T = 0;
+            while (i1 < todo.size() && (T == 0 || T + (int64_t)todo[i1].framed.size() <= kMaxTokens)) {
+                T += (int64_t)todo[i1].framed.size();
+                ++i1;
+            }
+            Stage s;
+            std::vector<Chunk> made;
+            int64_t off = 0;
+            try {
+                for (size_t k = i0; k < i1; ++k) {
+                    Chunk ch;
+                    ch.len = (int64_t)todo[k].framed.size();
+                    ch.framed = todo[k].framed;
+                    store_chunk_pages(e, ch);
+                    for (int64_t t = 0; t < ch.len; ++t) {
+                        s.tok.push_back(todo[k].framed[t]);
+                        s.pos.push_back((int32_t)t);          // positions 0..len-1 (pipeline.cpp:106)
+                        s.lo.push_back((int32_t)off);         // causal_rows(len, 0) per chunk: block-diagonal
+                        s.hi.push_back((int32_t)(off + t));
+                        s.page.push_back(ch.pages[t / e->page_tokens]);
+                        s.slot.push_back((int32_t)(t % e->page_tokens));
+                    }
+                    off += ch.len;
+                    made.push_back(std::move(ch));
+                }
+                tkv_context* scratch = new_context(e, T);
+                try {
+                    e->ensure_rope(T);
+                    upload_stage(e, s, true);
+                    tkv_engine::Fwd f;
+                    f.tok = e->d_tok.as<int32_t>();
+                    f.T = (int)T;
+                    f.pos = e->d_pos.as<int32_t>();
+                    f.ctx = scratch;
+                    f.row0 = 0;
+                    f.lo = e->d_lo.as<int32_t>();
+                    f.hi = e->d_hi.as<int32_t>();
+                    f.logits = false;
+                    f.kv_only = true;
+                    f.sc.pool = e->pool.p;
+                    f.sc.page = e->d_page.as<int32_t>();
+                    f.sc.slot = e->d_slot.as<int32_t>();
+                    f.sc.page_tokens = (int)e->page_tokens;
+                    f.sc.layer_num = (int)e->L;
+                    e->forward(f);
+                    e->check_err("ingest");
+                } catch (...) {
+                    tkv_context_destroy(scratch);
+                    throw;
+                }
+                tkv_context_destroy(scratch);
+            } catch (...) {
+                for (auto& ch : made)
+                    for (int32_t p : ch.pages) e->free_pages.push_back(p);
+                throw;
+            }
+            for (size_t k = i0; k < i1; ++k) {
+                Chunk& ch = made[k - i0];
+                if (stats) {
+                    stats->new_chunks += 1;
+                    stats->bytes_written += (uint64_t)ch.len * e->L * 2 * e->kvd * dt_size(e->dt);
+                }
+                e->chunks.emplace(todo[k].id, std::move(ch));
+            }
+            i0 = i1;
+        }
+    });
+}
+
+tkv_status tkv_import_tkvc(tkv_engine* e, const char* path, uint64_t* id_out) {
+    return guard([&] {
+        need(e, "engine");
+        need(path, "path");
+        e->bind();
+        std::ifstream in(path, std::ios::binary);
+        if (!in) fail(TKV_ERR_NOT_FOUND, std::string("no such file: ") + path);
+        std::string raw((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+        size_t cur = 0;
+        auto rd = [&](void* dst, size_t n, const char* what) {
+            if (cur + n > raw.size()) fail(TKV_ERR_FORMAT, std::string(what) + ": truncated");
+            std::memcpy(dst, raw.data() + cur, n);
+            cur += n;
+        };
+        auto u32 = [&](const char* w) {
+            uint8_t b[4];
+            rd(b, 4, w);
+            return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+        };
+        auto u64 = [&](const char* w) {
+            uint64_t lo = u32(w), hi = u32(w);
+            return lo | (hi << 32);
+        };
+        char magic[4];
+        rd(magic, 4, "chunk magic");  // kvstore.cpp:144-191 validation order
+        if (std::memcmp(magic, "TKVC", 4) != 0) fail(TKV_ERR_FORMAT, std::string("not a chunk cache file: ") + path);
+        const uint32_t version = u32("chunk version");
+        if (version != 1) fail(TKV_ERR_FORMAT, "unsupported chunk version " + std::to_string(version));
+        const uint32_t dtype = u32("chunk dtype");
+        if (dtype != 1 && dtype != 2) fail(TKV_ERR_FORMAT, "unknown chunk dtype " + std::to_string(dtype));
+        const uint32_t layers = u32("chunk header"), kvh = u32("chunk header"), hs = u32("chunk header"),
+                       ntok = u32("chunk header");
+        const uint64_t fp = u64("chunk header"), id = u64("chunk header");
+        std::string stem = path;
+        const size_t slash = stem.find_last_of('/');
+        if (slash != std::string::npos) stem = stem.substr(slash + 1);
+        if (stem.size() == 21 && stem.substr(16) == ".tkvc" && stem.substr(0, 16) != hex_id(id))
+            fail(TKV_ERR_FORMAT, std::string("chunk id mismatch in ") + path);
+        if (fp != e->fingerprint)
+            fail(TKV_ERR_STALE_CACHE, "chunk " + hex_id(id) + " was built under a different model fingerprint");
+        if (layers == 0 || kvh == 0 || hs == 0 || ntok == 0)
+            fail(TKV_ERR_FORMAT, std::string("chunk header: zero dimension in ") + path);
+        const uint64_t elem = dtype == 1 ? 8 : 4, kvd = (uint64_t)kvh * hs, tb = (uint64_t)ntok * kvd * elem;
+        uint64_t expect = 44 + (uint64_t)layers * 16;
+        for (uint32_t i = 0; i < layers * 2; ++i) {
+            if (u64("chunk offsets") != expect) fail(TKV_ERR_FORMAT, std::string("chunk offsets table corrupt in ") + path);
+            expect += tb;
+        }
+        if (raw.size() != expect) fail(TKV_ERR_FORMAT, std::string("chunk file size mismatch in ") + path);
+        if ((int64_t)kvh != e->Hkv || (int64_t)hs != e->d || (int64_t)layers != e->L)
+            fail(TKV_ERR_STALE_CACHE, "chunk geometry does not match the engine config");
+        if (id_out) *id_out = id;
+        if (e->chunks.count(id)) return;
+        Chunk ch;
+        ch.len = ntok;
+        store_chunk_pages(e, ch);
+        // convert f64/f32 -> f32 -> engine dtype on the host, page by page, then one H2D per page
+        const size_t es = dt_size(e->dt);
+        std::vector<uint8_t> page(e->page_bytes);
+        for (size_t p = 0; p < ch.pages.size(); ++p) {
+            std::fill(page.begin(), page.end(), 0);
+            const int64_t t0 = (int64_t)p * e->page_tokens, nt = std::min<int64_t>(e->page_tokens, ntok - t0);
+            for (uint32_t l = 0; l < layers; ++l)
+                for (int kv = 0; kv < 2; ++kv) {
+                    const size_t src = 44 + (size_t)layers * 16 + (size_t)(l * 2 + kv) * tb;
+                    for (int64_t t = 0; t < nt; ++t)
+                        for (uint64_t c = 0; c < kvd; ++c) {
+                            const size_t at = src + ((size_t)(t0 + t) * kvd + c) * elem;
+                            float f;
+                            if (elem == 8) {
+                                double v;
+                                std::memcpy(&v, raw.data() + at, 8);
+                                f = (float)v;
+                            } else {
+                                std::memcpy(&f, raw.data() + at, 4);
+                            }
+                            const size_t dst = ((size_t)(l * 2 + kv) * e->page_tokens + t) * kvd + c;
+                            if (e->dt == DT::F32) {
+                                std::memcpy(page.data() + dst * 4, &f, 4);
+                            } else {  // f32 -> bf16 round-to-nearest-even (same as __float2bfloat16_rn)
+                                uint32_t b;
+                                std::memcpy(&b, &f, 4);
+                                uint16_t h;
+                                if ((b & 0x7F800000u) == 0x7F800000u && (b & 0x7FFFFFu))
+                                    h = (uint16_t)((b >> 16) | 0x40);
+                                else
+                                    h = (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+                                std::memcpy(page.data() + dst * 2, &h, 2);
+                            }
+                        }
+                }
+            TKV_CUDA(cudaMemcpy(static_cast<uint8_t*>(e->pool.p) + (size_t)ch.pages[p] * e->page_bytes, page.data(),
+                                e->page_bytes, cudaMemcpyHostToDevice));
+            (void)es;
+        }
+        e->chunks.emplace(id, std::move(ch));
+    });
+}
+
+tkv_status tkv_export_tkvc(tkv_engine* e, uint64_t id, const char* path) {
+    return guard([&] {
+        need(e, "engine");
+        need(path, "path");
+        e->bind();
+        auto it = e->chunks.find(id);
+        if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
+        const Chunk& ch = it->second;
+        const uint64_t kvd = e->kvd, tb = (uint64_t)ch.len * kvd * 4;
+        std::string out;
+        auto w32 = [&](uint32_t v) {
+            for (int i = 0; i < 4; ++i) out.push_back((char)((v >> (8 * i)) & 0xFF));
+        };
+        auto w64 = [&](uint64_t v) {
+            w32((uint32_t)v);
+            w32((uint32_t)(v >> 32));
+        };
+        out.append("TKVC", 4);
+        w32(1);
+        w32(2);  // f32
+        w32((uint32_t)e->L);
+        w32((uint32_t)e->Hkv);
+        w32((uint32_t)e->d);
+        w32((uint32_t)ch.len);
+        w64(e->fingerprint);
+        w64(id);
+        uint64_t cur = 44 + (uint64_t)e->L * 16;
+        for (int64_t l = 0; l < e->L * 2; ++l) {
+            w64(cur);
+            cur += tb;
+        }
+        std::vector<float> buf((size_t)(ch.len * kvd));
+        for (int64_t l = 0; l < e->L; ++l)
+            for (int kv = 0; kv < 2; ++kv) {
+                tkv_status st = tkv_store_read(e, id, l, (tkv_kv_which)kv, buf.data(), (int64_t)buf.size());
+                if (st != TKV_OK) fail(st, g_last_error);
+                out.append(reinterpret_cast<const char*>(buf.data()), buf.size() * 4);
+            }
+        const std::string tmp = std::string(path) + ".tmp";
+        {
+            std::ofstream f(tmp, std::ios::binary | std::ios::trunc);
+            if (!f) fail(TKV_ERR_IO, "cannot open " + tmp + " for writing");
+            f.write(out.data(), (std::streamsize)out.size());
+            if (!f) fail(TKV_ERR_IO, "write failed: " + tmp);
+        }
+        if (std::rename(tmp.c_str(), path) != 0) fail(TKV_ERR_IO, std::string("rename to ") + path + " failed");
+    });
+}
+
+tkv_status tkv_store_contains(const tkv_engine* e, uint64_t id, int* out) {
+    return guard([&] {
+        need(e, "engine");
+        need(out, "out");
+        *out = e->chunks.count(id) ? 1 : 0;
+    });
+}
+
+tkv_status tkv_store_chunk_tokens(const tkv_engine* e, uint64_t id, int64_t* out) {
+    return guard([&] {
+        need(e, "engine");
+        auto it = e->chunks.find(id);
+        if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
+        *out = it->second.len;
+    });
+}
+
+tkv_status tkv_store_count(const tkv_engine* e, int64_t* chunks, int64_t* used, int64_t* total) {
+    return guard([&] {
+        need(e, "engine");
+        if (chunks) *chunks = (int64_t)e->chunks.size();
+        if (used) *used = e->n_pages - (int64_t)e->free_pages.size();
+        if (total) *total = e->n_pages;
+    });
+}
+
+tkv_status tkv_store_read(const tkv_engine* ce, uint64_t id, int64_t layer, tkv_kv_which which, float* host_out,
+                          int64_t capacity) {
+    return guard([&] {
+        tkv_engine* e = const_cast<tkv_engine*>(ce);
+        need(e, "engine");
+        need(host_out, "host_out");
+        e->bind();
+        auto it = e->chunks.find(id);
+        if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
+        if (layer < 0 || layer >= e->L) fail(TKV_ERR_SHAPE, "layer out of range");
+        const Chunk& ch = it->second;
+        if (capacity < ch.len * e->kvd) fail(TKV_ERR_SHAPE, "host buffer too small");
+        const size_t es = dt_size(e->dt);
+        DevMem tmp, tmpf;
+        tmp.ensure((size_t)ch.len * e->kvd * es);
+        tmpf.ensure((size_t)ch.len * e->kvd * 4);
+        for (size_t p = 0; p < ch.pages.size(); ++p) {
+            const int64_t t0 = (int64_t)p * e->page_tokens, nt = std::min<int64_t>(e->page_tokens, ch.len - t0);
+            const uint8_t* src = static_cast<uint8_t*>(e->pool.p) + (size_t)ch.pages[p] * e->page_bytes +
+                                 (size_t)((layer * 2 + (int)which) * e->page_tokens) * e->kvd * es;
+            TKV_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(tmp.p) + (size_t)t0 * e->kvd * es, src,
+                                     (size_t)nt * e->kvd * es, cudaMemcpyDeviceToDevice, e->stream));
+        }
+        launch_to_f32(tmp.p, ch.len * e->kvd, tmpf.as<float>(), e->dt, e->stream);
+        TKV_CUDA(cudaMemcpyAsync(host_out, tmpf.p, (size_t)ch.len * e->kvd * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+    });
+}
+
+tkv_status tkv_assemble(tkv_engine* e, const uint64_t* ids, int64_t n, tkv_position_mode mode, tkv_context** out) {
+    return guard([&] {
+        need(e, "engine");
+        need(out, "out");
+        if (n > 0) need(ids, "chunk_ids");
+        if (mode != TKV_POS_COMPOSITE && mode != TKV_POS_REORDERED) fail(TKV_ERR_CONFIG, "unknown position mode");
+        e->bind();
+        *out = assemble_impl(e, ids, n, mode);
+    });
+}
+
+tkv_status tkv_prefill_query(tkv_engine* e, tkv_context* c, const int32_t* query, int64_t n, float* logits_out,
+                             tkv_flops* fl) {
+    return guard([&] {
+        need(e, "engine");
+        need(c, "context");
+        if (n <= 0) fail(TKV_ERR_DOMAIN, "prefill_query: empty query");  // pipeline.cpp:169
+        need(query, "query");
+        if (c->eng != e) fail(TKV_ERR_STALE_CACHE, "context was assembled under a different model");
+        check_tokens(e, query, n);
+        e->bind();
+        std::vector<float> lg((size_t)e->V);
+        const int64_t P = c->total;
+        extend(e, c, query, nullptr, n, lg.data(), nullptr);
+        if (logits_out) std::memcpy(logits_out, lg.data(), lg.size() * 4);
+        flops_add(e, fl, n, P + n);
+    });
+}
+
+tkv_status tkv_prefill_query_device(tkv_engine* e, tkv_context* c, const int32_t* d_query, int64_t n,
+                                    float* d_logits) {
+    return guard([&] {
+        need(e, "engine");
+        need(c, "context");
+        if (n <= 0) fail(TKV_ERR_DOMAIN, "prefill_query: empty query");
+        need(d_query, "query");
+        if (c->eng != e) fail(TKV_ERR_STALE_CACHE, "context was assembled under a different model");
+        e->bind();
+        extend(e, c, nullptr, d_query, n, nullptr, d_logits);
+    });
+}
+
+tkv_status tkv_naive_prefill(tkv_engine* e, const int32_t* framed, const int64_t* offsets, int64_t n_chunks,
+                             const int32_t* query, int64_t nq, tkv_mask_mode mode, float* logits_out, tkv_flops* fl,
+                             tkv_context** ctx_out) {
+    return guard([&] {
+        need(e, "engine");
+        if (n_chunks > 0) {
+            need(framed, "framed");
+            need(offsets, "offsets");
+        }
+        if (mode != TKV_MASK_CAUSAL && mode != TKV_MASK_INDEPENDENT) fail(TKV_ERR_CONFIG, "unknown mask mode");
+        e->bind();
+        static const int64_t zero = 0;
+        naive_impl(e, framed, n_chunks > 0 ? offsets : &zero, n_chunks, query, nq, mode, logits_out, fl, ctx_out);
+    });
+}
+
+tkv_status tkv_naive_prefill_ids(tkv_engine* e, const uint64_t* ids, int64_t n, const int32_t* query, int64_t nq,
+                                 tkv_mask_mode mode, float* logits_out, tkv_flops* fl, tkv_context** ctx_out) {
+    return guard([&] {
+        need(e, "engine");
+        std::vector<int32_t> toks;
+        std::vector<int64_t> offs{0};
+        for (int64_t i = 0; i < n; ++i) {
+            auto it = e->chunks.find(ids[i]);
+            if (it == e->chunks.end() || it->second.framed.empty())
+                fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(ids[i]) + " has no token record");
+            toks.insert(toks.end(), it->second.framed.begin(), it->second.framed.end());
+            offs.push_back((int64_t)toks.size());
+        }
+        if (mode != TKV_MASK_CAUSAL && mode != TKV_MASK_INDEPENDENT) fail(TKV_ERR_CONFIG, "unknown mask mode");
+        e->bind();
+        naive_impl(e, toks.data(), offs.data(), n, query, nq, mode, logits_out, fl, ctx_out);
+    });
+}
+
+tkv_status tkv_greedy_decode(tkv_engine* e, tkv_context* c, int64_t max_new, int32_t* tokens_out, int64_t* n_out) {
+    return guard([&] {
+        need(e, "engine");
+        need(c, "context");
+        if (max_new < 0) fail(TKV_ERR_DOMAIN, "greedy_decode: negative max_new");
+        if ((int64_t)c->last_logits.size() != e->V) fail(TKV_ERR_DOMAIN, "greedy_decode: context has no logits yet");
+        e->bind();
+        int64_t n = 0;
+        std::vector<float> lg((size_t)e->V);
+        for (int64_t step = 0; step < max_new; ++step) {  // model.cpp:284-301
+            int32_t best = 0;
+            for (int64_t id = 1; id < e->V; ++id)
+                if (c->last_logits[id] > c->last_logits[best]) best = (int32_t)id;
+            if (best == 258) break;
+            if (tokens_out) tokens_out[n] = best;
+            ++n;
+            extend(e, c, &best, nullptr, 1, lg.data(), nullptr);
+        }
+        if (n_out) *n_out = n;
+    });
+}
+
+void tkv_context_destroy(tkv_context* c) {
+    if (!c) return;
+    if (c->eng) {
+        c->eng->ctx_release(c->kv, c->kv_bytes);
+        c->eng->live.erase(c);
+    }
+    delete c;
+}
+
+int64_t tkv_context_total_tokens(const tkv_context* c) { return c ? c->total : -1; }
+int64_t tkv_context_next_position(const tkv_context* c) { return c ? c->next_position : -1; }
+
+int64_t tkv_context_segments(const tkv_context* c, int64_t* lens, int32_t* is_query, int64_t cap) {
+    if (!c) return -1;
+    const int64_t n = (int64_t)c->seg_len.size();
+    for (int64_t i = 0; i < n && i < cap; ++i) {
+        if (lens) lens[i] = c->seg_len[i];
+        if (is_query) is_query[i] = c->seg_query[i];
+    }
+    return n;
+}
+
+tkv_status tkv_context_positions(const tkv_context* c, int64_t* out, int64_t capacity) {
+    return guard([&] {
+        need(c, "context");
+        if (capacity < (int64_t)c->positions.size()) fail(TKV_ERR_SHAPE, "positions buffer too small");
+        if (!c->positions.empty()) std::memcpy(out, c->positions.data(), c->positions.size() * 8);
+    });
+}
+
+tkv_status tkv_context_last_logits(const tkv_context* c, float* out, int64_t capacity) {
+    return guard([&] {
+        need(c, "context");
+        if (c->last_logits.empty()) fail(TKV_ERR_DOMAIN, "context has no logits yet");
+        if (capacity < (int64_t)c->last_logits.size()) fail(TKV_ERR_SHAPE, "logits buffer too small");
+        std::memcpy(out, c->last_logits.data(), c->last_logits.size() * 4);
+    });
+}
+
+tkv_status tkv_context_read_kv(const tkv_context* c, int64_t layer, tkv_kv_which which, int rotated, float* host_out,
+                               int64_t capacity) {
+    return guard([&] {
+        need(c, "context");
+        need(host_out, "host_out");
+        tkv_engine* e = c->eng;
+        if (!e) fail(TKV_ERR_GENERIC, "engine destroyed");
+        if (layer < 0 || layer >= e->L) fail(TKV_ERR_SHAPE, "layer out of range");
+        const int64_t rows = c->total;
+        if (capacity < rows * e->kvd) fail(TKV_ERR_SHAPE, "host buffer too small");
+        if (rows == 0) return;
+        e->bind();
+        DevMem f32;
+        f32.ensure((size_t)rows * e->kvd * 4);
+        tkv_context* cc = const_cast<tkv_context*>(c);
+        if (which == TKV_V || rotated) {
+            launch_to_f32(e->kv_plane(cc, layer, (int)which), rows * e->kvd, f32.as<float>(), e->dt, e->stream);
+        } else {
+            // injected rows: re-gather the unrotated store pages (identity rotation = bit-exact)
+            if (c->chunk_rows > 0) {
+                DevMem scratch, segs;
+                const int64_t cap = c->chunk_rows;
+                scratch.ensure((size_t)(e->L * 2 * cap * e->kvd) * dt_size(e->dt));
+                segs.ensure(c->chunk_segs.size() * sizeof(GatherSeg));
+                TKV_CUDA(cudaMemcpyAsync(segs.p, c->chunk_segs.data(), c->chunk_segs.size() * sizeof(GatherSeg),
+                                         cudaMemcpyHostToDevice, e->stream));
+                launch_gather_rope(e->pool.p, (int)e->page_tokens, segs.as<GatherSeg>(), (int)c->chunk_segs.size(),
+                                   (int)e->L, (int)e->kvd, (int)e->d, e->rope.as<float2>(), scratch.p, cap, 0, e->dt,
+                                   e->num_sms, e->stream);
+                launch_to_f32(static_cast<uint8_t*>(scratch.p) + (size_t)(layer * 2 * cap) * e->kvd * dt_size(e->dt),
+                              cap * e->kvd, f32.as<float>(), e->dt, e->stream);
+                e->sync();
+            }
+            // the rest (query / naive rows): inverse rotation of the cached rotated keys
+            const int64_t r0 = c->chunk_rows, nr = rows - r0;
+            if (nr > 0) {
+                std::vector<int32_t> pos(c->positions.begin() + r0, c->positions.end());
+                DevMem dpos;
+                dpos.ensure((size_t)nr * 4);
+                TKV_CUDA(cudaMemcpyAsync(dpos.p, pos.data(), (size_t)nr * 4, cudaMemcpyHostToDevice, e->stream));
+                launch_unrotate_rows(static_cast<uint8_t*>(e->kv_plane(cc, layer, 0)) + (size_t)r0 * e->kvd * dt_size(e->dt),
+                                     (int)nr, (int)e->kvd, (int)e->d, dpos.as<int32_t>(), e->rope.as<float2>(),
+                                     f32.as<float>() + r0 * e->kvd, e->dt, e->stream);
+                e->sync();
+            }
+        }
+        TKV_CUDA(cudaMemcpyAsync(host_out, f32.p, (size_t)rows * e->kvd * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+    });
+}
+
+tkv_status tkv_context_mask(const tkv_context* c, uint8_t* out, int64_t rows, int64_t cols) {
+    return guard([&] {
+        need(c, "context");
+        need(out, "out");
+        tkv_engine* e = c->eng;
+        if (!e) fail(TKV_ERR_GENERIC, "engine destroyed");
+        if (c->last_rows == 0) fail(TKV_ERR_DOMAIN, "no forward has run over this context yet");
+        if (rows != c->last_rows || cols != c->last_cols)
+            fail(TKV_ERR_SHAPE, "mask is " + std::to_string(c->last_rows) + "x" + std::to_string(c->last_cols));
+        e->bind();
+        DevMem lo, hi, m;
+        lo.ensure((size_t)rows * 4);
+        hi.ensure((size_t)rows * 4);
+        m.ensure((size_t)(rows * cols));
+        TKV_CUDA(cudaMemcpyAsync(lo.p, c->last_lo.data(), (size_t)rows * 4, cudaMemcpyHostToDevice, e->stream));
+        TKV_CUDA(cudaMemcpyAsync(hi.p, c->last_hi.data(), (size_t)rows * 4, cudaMemcpyHostToDevice, e->stream));
+        launch_mask_materialize(lo.as<int32_t>(), hi.as<int32_t>(), (int)rows, (int)cols, m.as<uint8_t>(), e->stream);
+        TKV_CUDA(cudaMemcpyAsync(out, m.p, (size_t)(rows * cols), cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+    });
+}
+
+void* tkv_engine_stream(tkv_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+tkv_status tkv_profile_enable(tkv_engine* e, int on) {
+    return guard([&] {
+        need(e, "engine");
+        e->bind();
+        e->prof_flush();
+        e->prof_on = on != 0;
+    });
+}
+
+tkv_status tkv_profile_read(tkv_engine* e, const char* cls, double* total_ms, int64_t* launches) {
+    return guard([&] {
+        need(e, "engine");
+        need(cls, "class");
+        e->bind();
+        e->prof_flush();
+        for (int i = 0; i < PC_N; ++i)
+            if (std::strcmp(cls, kProfNames[i]) == 0) {
+                if (total_ms) *total_ms = e->prof_ms[i];
+                if (launches) *launches = e->prof_n[i];
+                return;
+            }
+        fail(TKV_ERR_CONFIG, std::string("unknown kernel class ") + cls);
+    });
+}
+
+tkv_status tkv_profile_reset(tkv_engine* e) {
+    return guard([&] {
+        need(e, "engine");
+        e->bind();
+        e->prof_flush();
+        for (int i = 0; i < PC_N; ++i) {
+            e->prof_ms[i] = 0;
+            e->prof_n[i] = 0;
+        }
+    });
+}
+
+int64_t tkv_launch_count(const tkv_engine* e) { return e ? e->launches : -1; }
+
+tkv_status tkv_debug_set_mask_fault(tkv_engine* e, int64_t row, int64_t col) {
+    return guard([&] {
+        need(e, "engine");
+        e->fault_row = row;
+        e->fault_col = col;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,411 @@
+// Memory-bound kernels of the TurboRAG prefill path (sm_100a):
+//   weight init (SplitMix64, src/model.cpp:15-21,68-92), embedding + RMSNorm (numerics.cpp:84-101),
+//   split-K reduce epilogues (residual + RMSNorm, SwiGLU numerics.cpp:103-124, QKV + RoPE rope.cpp:35-46),
+//   the KV-gather + RoPE injection kernel (replaces CacheStore::load + ctx.append + per-layer
+//   rope_rotate_heads_inplace: kvstore.cpp:134-207, context.cpp:7-22, model.cpp:248-254),
+//   lm_head GEMV and mask materialisation.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tkv_internal.h"
+
+namespace tkv {
+namespace {
+
+__device__ __forceinline__ float ldf(const float* p, int64_t i) { return p[i]; }
+__device__ __forceinline__ float ldf(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+__device__ __forceinline__ void stf(float* p, int64_t i, float v) { p[i] = v; }
+__device__ __forceinline__ void stf(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// next_signed() * scale in IEEE binary64 without contraction (bit-identical to the host).
+__device__ __forceinline__ double draw(uint64_t seed, uint64_t i, double scale) {
+    const double u = __dmul_rn((double)(splitmix_at(seed, i) >> 11), 0x1.0p-53);
+    return __dmul_rn(__dadd_rn(__dmul_rn(2.0, u), -1.0), scale);
+}
+
+template <typename T>
+__global__ void init_transposed_kernel(T* dst, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
+                                       double scale) {
+    const int64_t n = rows * cols;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = o / rows, i = o - j * rows;
+        const float f = __double2float_rn(draw(seed, base + (uint64_t)(i * cols + j), scale));
+        stf(dst, o, f);  // f64 -> f32 (RN) -> bf16 (RNE): the canonical cast, see DESIGN.md
+    }
+}
+
+__global__ void init_rowmajor_kernel(float* dst, uint64_t seed, uint64_t base, int64_t n, double scale) {
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
+        dst[o] = __double2float_rn(draw(seed, base + (uint64_t)o, scale));
+}
+
+__global__ void fill_kernel(float* dst, float v, int64_t n) {
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
+        dst[o] = v;
+}
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    float t = 0.f;
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int i = 0; i < nw; ++i) t += red[i];
+    return t;
+}
+
+template <typename T>
+__global__ void embed_norm_kernel(const int32_t* tok, const float* emb, int hidden, int vocab, const float* w,
+                                  float eps, float* x, T* h, int* err) {
+    __shared__ float red[32];
+    const int t = blockIdx.x;
+    const int id = tok[t];
+    if (id < 0 || id >= vocab) {  // DomainError "token id outside vocab" (model.cpp:217-221)
+        if (threadIdx.x == 0) atomicOr(err, 1);
+        return;
+    }
+    float ss = 0.f;
+    for (int j = threadIdx.x; j < hidden; j += blockDim.x) {
+        const float v = emb[(int64_t)id * hidden + j];
+        x[(int64_t)t * hidden + j] = v;
+        ss += v * v;
+    }
+    ss = block_sum(ss, red);
+    const float scale = 1.0f / sqrtf(ss / (float)hidden + eps);
+    for (int j = threadIdx.x; j < hidden; j += blockDim.x)
+        stf(h, (int64_t)t * hidden + j, x[(int64_t)t * hidden + j] * scale * w[j]);
+}
+
+template <typename T>
+__global__ void residual_norm_kernel(float* x, const float* partial, int splits, int64_t plane, int hidden,
+                                     const float* w, float eps, T* h, int* err) {
+    __shared__ float red[32];
+    const int64_t t = blockIdx.x;
+    float ss = 0.f;
+    bool bad = false;
+    for (int j = threadIdx.x; j < hidden; j += blockDim.x) {
+        float acc = 0.f;
+        for (int s = 0; s < splits; ++s) acc += partial[s * plane + t * hidden + j];
+        const float v = x[t * hidden + j] + acc;
+        x[t * hidden + j] = v;
+        ss += v * v;
+        bad |= !isfinite(v);
+    }
+    if (bad) atomicOr(err, 2);
+    if (w == nullptr) return;
+    ss = block_sum(ss, red);
+    const float scale = 1.0f / sqrtf(ss / (float)hidden + eps);
+    for (int j = threadIdx.x; j < hidden; j += blockDim.x) stf(h, t * hidden + j, x[t * hidden + j] * scale * w[j]);
+}
+
+template <typename T>
+__global__ void swiglu_kernel(const float* partial, int splits, int T_, int inter, T* act) {
+    const int64_t n = (int64_t)T_ * inter, plane = (int64_t)T_ * 2 * inter;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = o / inter, i = o - t * inter;
+        float g = 0.f, u = 0.f;
+        for (int s = 0; s < splits; ++s) {
+            g += partial[s * plane + t * 2 * inter + i];
+            u += partial[s * plane + t * 2 * inter + inter + i];
+        }
+        stf(act, o, (g / (1.0f + expf(-g))) * u);  // silu(z) = z / (1 + e^-z), numerics.cpp:103-105
+    }
+}
+
+// One thread per element pair (2m, 2m+1) of the fused QKV output row.
+template <typename T>
+__global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
+                                    const int32_t* pos, const float2* rope, T* q, T* kc, T* vc, int row0,
+                                    StoreScatter sc, int layer) {
+    const int qd = H * d, kvd = Hkv * d, N = qd + 2 * kvd, half = d / 2;
+    const int64_t pairs = (int64_t)T_ * (N / 2), plane = (int64_t)T_ * N;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = p / (N / 2);
+        const int n = 2 * (int)(p - t * (N / 2));
+        float x0 = 0.f, x1 = 0.f;
+        for (int s = 0; s < splits; ++s) {
+            x0 += partial[s * plane + t * N + n];
+            x1 += partial[s * plane + t * N + n + 1];
+        }
+        if (n >= qd + kvd) {  // V: copied as is
+            const int c = n - qd - kvd;
+            stf(vc, (int64_t)(row0 + t) * kvd + c, x0);
+            stf(vc, (int64_t)(row0 + t) * kvd + c + 1, x1);
+            if (sc.page) {
+                const int64_t base = (((int64_t)sc.page[t] * sc.layer_num + layer) * 2 + 1) * sc.page_tokens * kvd +
+                                     (int64_t)sc.slot[t] * kvd;
+                stf((T*)sc.pool, base + c, x0);
+                stf((T*)sc.pool, base + c + 1, x1);
+            }
+            continue;
+        }
+        const int e = (n < qd ? n : n - qd) % d;
+        const float2 cs = rope[(int64_t)pos[t] * half + e / 2];
+        const float r0 = x0 * cs.x - x1 * cs.y, r1 = x0 * cs.y + x1 * cs.x;  // rope.cpp:41-44
+        if (n < qd) {
+            stf(q, t * qd + n, r0);
+            stf(q, t * qd + n + 1, r1);
+        } else {
+            const int c = n - qd;
+            stf(kc, (int64_t)(row0 + t) * kvd + c, r0);
+            stf(kc, (int64_t)(row0 + t) * kvd + c + 1, r1);
+            if (sc.page) {  // the store keeps keys unrotated (SPEC: rotation at use)
+                const int64_t base = (((int64_t)sc.page[t] * sc.layer_num + layer) * 2 + 0) * sc.page_tokens * kvd +
+                                     (int64_t)sc.slot[t] * kvd;
+                stf((T*)sc.pool, base + c, x0);
+                stf((T*)sc.pool, base + c + 1, x1);
+            }
+        }
+    }
+}
+
+// ---- KV gather + fused RoPE ------------------------------------------------------------------
+// Work unit = (segment, layer, K|V): a contiguous [n_tok, kv_dim] block of one store page copied
+// to contiguous request-cache rows. 16-byte vectors; keys rotated in fp32 in registers.
+template <typename T>
+struct Vec16 {
+    static constexpr int N = 16 / sizeof(T);
+};
+
+template <typename T>
+__device__ __forceinline__ void rotate_vec(uint4& v, const float2* cs) {
+    constexpr int N = Vec16<T>::N;
+    T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+        const float x0 = ldf(e, 2 * i), x1 = ldf(e, 2 * i + 1);
+        const float2 c = cs[i];
+        stf(e, 2 * i, x0 * c.x - x1 * c.y);
+        stf(e, 2 * i + 1, x0 * c.y + x1 * c.x);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gather_rope_vec_kernel(const T* __restrict__ pool, int page_tokens,
+                                                              const GatherSeg* __restrict__ segs, int n_units, int L,
+                                                              int kvd, int d, const float2* __restrict__ rope,
+                                                              T* __restrict__ cache, int64_t cap, int rotate) {
+    constexpr int N = Vec16<T>::N;
+    const int vec_per_row = kvd / N, half = d / 2;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int seg = u / (2 * L), layer = (u / 2) % L, kv = u & 1;
+        const GatherSeg sg = segs[seg];
+        const uint4* src = reinterpret_cast<const uint4*>(
+            pool + (((int64_t)sg.src_page * L + layer) * 2 + kv) * page_tokens * kvd);
+        uint4* dst = reinterpret_cast<uint4*>(cache + ((int64_t)(layer * 2 + kv) * cap + sg.dst_row) * kvd);
+        const int nv = sg.n_tok * vec_per_row;
+        const bool rot = rotate && kv == 0;
+        constexpr int U = 4;
+        for (int base = threadIdx.x; base < nv; base += blockDim.x * U) {
+            uint4 r[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = base + k * blockDim.x;
+                if (i < nv) r[k] = __ldcs(src + i);  // streaming read: store pages are not re-read
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = base + k * blockDim.x;
+                if (i < nv) {
+                    if (rot) {
+                        const int row = i / vec_per_row, col = (i - row * vec_per_row) * N;
+                        const float2* cs = rope + (int64_t)(sg.pos0 + row) * half + (col % d) / 2;
+                        float2 c[N / 2];
+#pragma unroll
+                        for (int m = 0; m < N / 2; ++m) c[m] = __ldg(cs + m);
+                        rotate_vec<T>(r[k], c);
+                    }
+                    dst[i] = r[k];
+                }
+            }
+        }
+    }
+}
+
+// Generic fallback: one pair per thread (any even head_size / kv_dim).
+template <typename T>
+__global__ void gather_rope_pair_kernel(const T* pool, int page_tokens, const GatherSeg* segs, int n_units, int L,
+                                        int kvd, int d, const float2* rope, T* cache, int64_t cap, int rotate) {
+    const int half = d / 2;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int seg = u / (2 * L), layer = (u / 2) % L, kv = u & 1;
+        const GatherSeg sg = segs[seg];
+        const T* src = pool + (((int64_t)sg.src_page * L + layer) * 2 + kv) * page_tokens * kvd;
+        T* dst = cache + ((int64_t)(layer * 2 + kv) * cap + sg.dst_row) * kvd;
+        const int np = sg.n_tok * kvd / 2;
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+            const int row = (2 * i) / kvd, col = 2 * i - row * kvd;
+            float x0 = ldf(src, 2 * i), x1 = ldf(src, 2 * i + 1);
+            if (rotate && kv == 0) {
+                const float2 c = rope[(int64_t)(sg.pos0 + row) * half + (col % d) / 2];
+                const float r0 = x0 * c.x - x1 * c.y, r1 = x0 * c.y + x1 * c.x;
+                x0 = r0;
+                x1 = r1;
+            }
+            stf(dst, 2 * i, x0);
+            stf(dst, 2 * i + 1, x1);
+        }
+    }
+}
+
+template <typename T>
+__global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, float* logits, int* err) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= vocab) return;
+    float acc = 0.f;
+    for (int k = lane; k < hidden; k += 32) acc += ldf(h, k) * ldf(W, (int64_t)warp * hidden + k);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+        logits[warp] = acc;
+        if (!isfinite(acc)) atomicOr(err, 4);  // Matrix::require_finite("logits"), model.cpp:268
+    }
+}
+
+__global__ void mask_kernel(const int32_t* lo, const int32_t* hi, int rows, int cols, uint8_t* out) {
+    const int64_t n = (int64_t)rows * cols;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(o / cols), j = (int)(o - (int64_t)i * cols);
+        out[o] = (j >= lo[i] && j <= hi[i]) ? 1 : 0;  // same predicate as attention (attn_simt.cu)
+    }
+}
+
+template <typename T>
+__global__ void unrotate_kernel(const T* k, int rows, int kvd, int d, const int32_t* pos, const float2* rope,
+                                float* out) {
+    const int64_t n = (int64_t)rows * kvd / 2;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = (2 * p) / kvd;
+        const int c = (int)(2 * p - r * kvd);
+        const float2 cs = rope[(int64_t)pos[r] * (d / 2) + (c % d) / 2];
+        const float y0 = ldf(k, 2 * p), y1 = ldf(k, 2 * p + 1);
+        out[2 * p] = y0 * cs.x + y1 * cs.y;  // R(-t)
+        out[2 * p + 1] = -y0 * cs.y + y1 * cs.x;
+    }
+}
+
+template <typename T>
+__global__ void to_f32_kernel(const T* src, int64_t n, float* dst) {
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
+        dst[o] = ldf(src, o);
+}
+
+inline int grid_for(int64_t n, int block, int cap = 148 * 16) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    return (int)(g < cap ? g : cap);
+}
+
+}  // namespace
+
+#define DISPATCH_DT(dt, ...)                            \
+    do {                                                \
+        if ((dt) == DT::F32) {                          \
+            using T = float;                            \
+            __VA_ARGS__;                                \
+        } else {                                        \
+            using T = __nv_bfloat16;                    \
+            __VA_ARGS__;                                \
+        }                                               \
+    } while (0)
+
+void launch_init_transposed(void* dst, DT dt, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
+                            double scale, cudaStream_t s) {
+    DISPATCH_DT(dt, init_transposed_kernel<T><<<grid_for(rows * cols, 256, 148 * 64), 256, 0, s>>>(
+                        (T*)dst, seed, base, rows, cols, scale));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_init_rowmajor_f32(float* dst, uint64_t seed, uint64_t base, int64_t rows, int64_t cols, double scale,
+                              cudaStream_t s) {
+    init_rowmajor_kernel<<<grid_for(rows * cols, 256, 148 * 64), 256, 0, s>>>(dst, seed, base, rows * cols, scale);
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t s) {
+    fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, v, n);
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_embed_norm(const int32_t* tok, int T_, const float* emb, int hidden, int vocab, const float* w, float eps,
+                       float* x, void* h, DT dt, int* err, cudaStream_t s) {
+    DISPATCH_DT(dt, embed_norm_kernel<T><<<T_, 256, 0, s>>>(tok, emb, hidden, vocab, w, eps, x, (T*)h, err));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_residual_norm(float* x, const float* partial, int splits, int T_, int hidden, const float* w, float eps,
+                          void* h, DT dt, int* err, cudaStream_t s) {
+    const int64_t plane = (int64_t)T_ * hidden;
+    DISPATCH_DT(dt, residual_norm_kernel<T><<<T_, 512, 0, s>>>(x, partial, splits, plane, hidden, w, eps, (T*)h, err));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_swiglu(const float* partial, int splits, int T_, int inter, void* act, DT dt, cudaStream_t s) {
+    DISPATCH_DT(dt, swiglu_kernel<T><<<grid_for((int64_t)T_ * inter, 256), 256, 0, s>>>(partial, splits, T_, inter,
+                                                                                         (T*)act));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hkv, int d, const int32_t* pos,
+                         const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc, int layer,
+                         DT dt, cudaStream_t s) {
+    const int64_t pairs = (int64_t)T_ * (H + 2 * Hkv) * d / 2;
+    DISPATCH_DT(dt, qkv_epilogue_kernel<T><<<grid_for(pairs, 256), 256, 0, s>>>(
+                        partial, splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_gather_rope(const void* pool, int page_tokens, const GatherSeg* segs, int n_segs, int L, int kvd, int d,
+                        const float2* rope, void* cache, int64_t cap, int rotate, DT dt, int num_sms,
+                        cudaStream_t s) {
+    const int n_units = n_segs * L * 2;
+    if (n_units == 0) return;
+    const int grid = n_units < num_sms * 8 ? n_units : num_sms * 8;
+    const int vecN = 16 / (int)dt_size(dt);
+    const bool vec_ok = (kvd % vecN == 0) && (d % vecN == 0) && (page_tokens * kvd * (int)dt_size(dt)) % 16 == 0 &&
+                        (cap * kvd * (int64_t)dt_size(dt)) % 16 == 0;
+    if (vec_ok) {
+        DISPATCH_DT(dt, gather_rope_vec_kernel<T><<<grid, 256, 0, s>>>((const T*)pool, page_tokens, segs, n_units, L,
+                                                                       kvd, d, rope, (T*)cache, cap, rotate));
+    } else {
+        DISPATCH_DT(dt, gather_rope_pair_kernel<T><<<grid, 256, 0, s>>>((const T*)pool, page_tokens, segs, n_units, L,
+                                                                        kvd, d, rope, (T*)cache, cap, rotate));
+    }
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_lm_head(const void* h, const void* W, int hidden, int vocab, float* logits, DT dt, int* err,
+                    cudaStream_t s) {
+    const int threads = 256, warps_per_block = threads / 32;
+    DISPATCH_DT(dt, lm_head_kernel<T><<<(vocab + warps_per_block - 1) / warps_per_block, threads, 0, s>>>(
+                        (const T*)h, (const T*)W, hidden, vocab, logits, err));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_mask_materialize(const int32_t* lo, const int32_t* hi, int rows, int cols, uint8_t* out, cudaStream_t s) {
+    mask_kernel<<<grid_for((int64_t)rows * cols, 256), 256, 0, s>>>(lo, hi, rows, cols, out);
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_unrotate_rows(const void* k, int rows, int kvd, int d, const int32_t* pos, const float2* rope, float* out,
+                          DT dt, cudaStream_t s) {
+    DISPATCH_DT(dt, unrotate_kernel<T><<<grid_for((int64_t)rows * kvd / 2, 256), 256, 0, s>>>((const T*)k, rows, kvd,
+                                                                                               d, pos, rope, out));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_to_f32(const void* src, int64_t n, float* dst, DT dt, cudaStream_t s) {
+    DISPATCH_DT(dt, to_f32_kernel<T><<<grid_for(n, 256), 256, 0, s>>>((const T*)src, n, dst));
+    TKV_CUDA(cudaGetLastError());
+}
+
+}  // namespace tkv

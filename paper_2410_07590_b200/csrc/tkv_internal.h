@@ -1,0 +1,109 @@
+// Internal declarations shared by the host engine (engine.cpp) and the sm_100a kernels.
+// Nothing here is part of the C ABI (include/tkv.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/tkv.h"
+
+namespace tkv {
+
+// Status carrier for the host side; the C ABI converts it to tkv_status + message.
+struct Failure {
+    tkv_status code;
+    std::string msg;
+};
+[[noreturn]] void fail(tkv_status code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define TKV_CUDA(x) ::tkv::cuda_check((x), #x)
+
+enum class DT : int { F32 = 0, BF16 = 1 };
+inline size_t dt_size(DT t) { return t == DT::F32 ? 4 : 2; }
+
+// ---------------------------------------------------------------------------------------------
+// Kernel launchers (kernels.cu, gemm_simt.cu, gemm_tc.cu, attn_simt.cu, gather.cu).
+// All are asynchronous on `s`.
+// ---------------------------------------------------------------------------------------------
+
+// Weight init: dst[j*rows + i] = cast(next_signed(seed, base + i*cols + j) * scale) — the reference's
+// [rows=in, cols=out] draw order (src/model.cpp:15-21,68-92) written transposed (K-major [out][in]).
+void launch_init_transposed(void* dst, DT dt, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
+                            double scale, cudaStream_t s);
+// Same, not transposed (embedding [vocab][hidden], fp32).
+void launch_init_rowmajor_f32(float* dst, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
+                              double scale, cudaStream_t s);
+void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t s);
+
+// x[t] = emb[tok[t]] (fp32); h[t] = rmsnorm(x[t]) * w  (dtype). Errors (token outside vocab) set *err.
+void launch_embed_norm(const int32_t* tok, int T, const float* emb, int hidden, int vocab, const float* w,
+                       float eps, float* x, void* h, DT dt, int* err, cudaStream_t s);
+// x[t] += sum_s partial[s][t][:]; h[t] = rmsnorm(x[t]) * w (dtype).  x/h/partial row strides = hidden.
+void launch_residual_norm(float* x, const float* partial, int splits, int T, int hidden, const float* w,
+                          float eps, void* h, DT dt, int* err, cudaStream_t s);
+// act[t][i] = silu(sum_s P[s][t][i]) * sum_s P[s][t][I+i]   (dtype)
+void launch_swiglu(const float* partial, int splits, int T, int inter, void* act, DT dt, cudaStream_t s);
+
+// QKV epilogue: reduce the split-K partials of [T, (H+2Hkv)*d], rotate q and k by pos[t]
+// (interleaved pairs, cos/sin table [max_pos][d/2] of float2), write q (dtype [T, H*d]),
+// rotated K and V into the request cache rows [row0, row0+T) of layer tensors kc/vc
+// ([cap, kv_dim] dtype), and — when st_page != nullptr — the unrotated K and V into store pages:
+// page p, slot s of layer tensor = store + ((p*L + layer)*2 + kv)*page_tokens*kv_dim.
+struct StoreScatter {
+    void* pool = nullptr;
+    const int32_t* page = nullptr;  // [T]
+    const int32_t* slot = nullptr;  // [T]
+    int page_tokens = 0;
+    int layer_num = 0;
+};
+void launch_qkv_epilogue(const float* partial, int splits, int T, int H, int Hkv, int d, const int32_t* pos,
+                         const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc,
+                         int layer, DT dt, cudaStream_t s);
+
+// KV gather + fused RoPE: one descriptor per (chunk page -> request rows) segment.
+struct GatherSeg {
+    int32_t src_page;  // page index in the store pool
+    int32_t n_tok;     // tokens in this segment (<= page_tokens)
+    int32_t dst_row;   // first request-cache row
+    int32_t pos0;      // position id of the first token (positions are consecutive inside a segment)
+};
+// cache layout [L][2][cap][kv_dim]; rotate=0 copies keys unrotated (bit-exact export).
+void launch_gather_rope(const void* pool, int page_tokens, const GatherSeg* segs, int n_segs, int L, int kv_dim,
+                        int d, const float2* rope, void* cache, int64_t cap, int rotate, DT dt, int num_sms,
+                        cudaStream_t s);
+
+// logits[v] = sum_k h[k] * W[v][k] (W dtype [vocab][hidden], h dtype), fp32 out; sets *err on non-finite.
+void launch_lm_head(const void* h, const void* W, int hidden, int vocab, float* logits, DT dt, int* err,
+                    cudaStream_t s);
+// dense 0/1 view of the [lo, hi] predicate (the same __device__ predicate the attention uses)
+void launch_mask_materialize(const int32_t* lo, const int32_t* hi, int rows, int cols, uint8_t* out,
+                             cudaStream_t s);
+// rot[i] = inverse-rotate(cache K rows) for export; fp32 out
+void launch_unrotate_rows(const void* k, int rows, int kv_dim, int d, const int32_t* pos, const float2* rope,
+                          float* out, DT dt, cudaStream_t s);
+void launch_to_f32(const void* src, int64_t n, float* dst, DT dt, cudaStream_t s);
+
+// GEMM: partial[z][m][n] = sum_{k in split z} A[m][k] * W[n][k]   (A [M][lda] dtype, W [N][K] dtype).
+void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
+                      DT dt, cudaStream_t s);
+// tcgen05 + TMA version (bf16 only). Returns false when the shape is not supported (caller errors out).
+bool gemm_tc_supported(int M, int N, int K, int lda);
+void launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
+                    cudaStream_t s);
+
+// Flash attention, SIMT (fp32 math): q [Tq][H*d], k/v rows [Tk][Hkv*d] (stride kv_stride elements),
+// row t attends keys j with lo[t] <= j <= hi[t]. out [Tq][H*d] (dtype). ws: split-K workspace.
+struct AttnWork {
+    float* o = nullptr;   // [splits][Tq*H][d]
+    float* ml = nullptr;  // [splits][Tq*H][2]
+    size_t floats = 0;
+};
+size_t attn_workspace_floats(int Tq, int H, int d, int splits);
+int attn_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms);
+void launch_attention_simt(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
+                           const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int d, int splits,
+                           const AttnWork& ws, int* err, DT dt, cudaStream_t s);
+
+}  // namespace tkv

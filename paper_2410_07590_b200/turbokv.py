@@ -1,0 +1,500 @@
+"""Python mirror of the reference `turbokv` C++ API over the C ABI (include/tkv.h).
+
+Names, argument meaning and error classes follow /root/reference/proj/include/turbokv/*.hpp
+so parity tests read like the reference's own tests:
+
+    Engine(config, seed)                    pipeline.hpp:69-72
+    Engine.ingest_chunk_payload(doc, toks)  pipeline.hpp:86-88
+    Engine.assemble(ids, PositionMode)      pipeline.hpp:93
+    Engine.prefill_query(ctx, toks)         pipeline.hpp:97-99
+    Engine.naive_prefill(chunks, q, mode)   pipeline.hpp:104-108
+    greedy_decode(...)                      model.hpp:74-81
+    errors                                   errors.hpp:10-67
+
+Every call goes through libtkv_b200.so (sm_100a kernels). There is no CPU fallback: without the
+built library or a B200 the import / Engine() raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtkv_b200.so")
+
+I32P, I64P, U64P = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_uint64)
+F32P, U8P = C.POINTER(C.c_float), C.POINTER(C.c_uint8)
+
+
+class Error(RuntimeError):
+    """turbokv::Error"""
+
+
+class ShapeError(Error): pass
+class DomainError(Error): pass
+class ConfigError(Error): pass
+class DegenerateRowError(Error): pass
+class IoError(Error): pass
+class FormatError(Error): pass
+class NotFoundError(Error): pass
+class StaleCacheError(Error): pass
+class NoContextError(Error): pass
+class CudaError(Error): pass
+class OutOfMemoryError(Error): pass
+
+
+_ERRORS = {1: Error, 2: ShapeError, 3: DomainError, 4: ConfigError, 5: DegenerateRowError, 6: IoError,
+           7: FormatError, 8: NotFoundError, 9: StaleCacheError, 10: NoContextError, 11: CudaError,
+           12: OutOfMemoryError}
+
+
+class PositionMode(enum.IntEnum):
+    Composite = 0
+    Reordered = 1
+
+
+class MaskMode(enum.IntEnum):
+    Causal = 0
+    Independent = 1
+
+
+class Dtype(enum.IntEnum):
+    F32 = 1
+    BF16 = 2
+
+
+FLAG_SIMT_GEMM = 0x1
+FLAG_SIMT_ATTN = 0x2
+FLAG_NO_GRAPHS = 0x4
+
+DOC_START, DOC_END, EOS, VOCAB = 256, 257, 258, 259  # tokenizer.hpp:19-22
+
+
+class _Cfg(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("layer_num", "head_num", "kv_head_num", "head_size", "hidden_size",
+                                          "intermediate_size", "vocab_size")] + \
+               [("rope_base", C.c_double), ("norm_eps", C.c_double)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("dtype", C.c_int), ("device", C.c_int32), ("page_tokens", C.c_int32),
+                ("store_capacity_tokens", C.c_int64), ("max_position", C.c_int64),
+                ("exact_fingerprint", C.c_int32), ("flags", C.c_int32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("chunks", C.c_int64), ("new_chunks", C.c_int64), ("bytes_written", C.c_uint64)]
+
+
+class _Flops(C.Structure):
+    _fields_ = [("qkv", C.c_uint64), ("attn", C.c_uint64), ("o", C.c_uint64), ("mlp", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built: run `make -C {_HERE}` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.tkv_last_error.restype = C.c_char_p
+        L.tkv_status_name.restype = C.c_char_p
+        L.tkv_config_preset.argtypes = [C.c_char_p, C.POINTER(_Cfg)]
+        L.tkv_config_validate.argtypes = [C.POINTER(_Cfg)]
+        L.tkv_config_fingerprint_seed.restype = C.c_uint64
+        L.tkv_config_fingerprint_seed.argtypes = [C.POINTER(_Cfg)]
+        L.tkv_weights_identity.argtypes = [C.POINTER(_Cfg), C.c_uint64, U64P, U64P]
+        L.tkv_chunk_content_id.restype = C.c_uint64
+        L.tkv_chunk_content_id.argtypes = [C.c_uint64, I32P, C.c_int64]
+        L.tkv_engine_opts_default.argtypes = [C.POINTER(_Opts)]
+        L.tkv_engine_create.argtypes = [C.POINTER(_Cfg), C.c_uint64, C.POINTER(_Opts), C.POINTER(C.c_void_p)]
+        L.tkv_engine_destroy.argtypes = [C.c_void_p]
+        L.tkv_engine_fingerprint.argtypes = [C.c_void_p, U64P]
+        L.tkv_ingest_chunks.argtypes = [C.c_void_p, I32P, I64P, C.c_int64, U64P, C.POINTER(_Stats)]
+        L.tkv_import_tkvc.argtypes = [C.c_void_p, C.c_char_p, U64P]
+        L.tkv_export_tkvc.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p]
+        L.tkv_store_contains.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int)]
+        L.tkv_store_chunk_tokens.argtypes = [C.c_void_p, C.c_uint64, I64P]
+        L.tkv_store_count.argtypes = [C.c_void_p, I64P, I64P, I64P]
+        L.tkv_store_read.argtypes = [C.c_void_p, C.c_uint64, C.c_int64, C.c_int, F32P, C.c_int64]
+        L.tkv_assemble.argtypes = [C.c_void_p, U64P, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]
+        L.tkv_prefill_query.argtypes = [C.c_void_p, C.c_void_p, I32P, C.c_int64, F32P, C.POINTER(_Flops)]
+        L.tkv_prefill_query_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.tkv_naive_prefill.argtypes = [C.c_void_p, I32P, I64P, C.c_int64, I32P, C.c_int64, C.c_int, F32P,
+                                        C.POINTER(_Flops), C.POINTER(C.c_void_p)]
+        L.tkv_naive_prefill_ids.argtypes = [C.c_void_p, U64P, C.c_int64, I32P, C.c_int64, C.c_int, F32P,
+                                            C.POINTER(_Flops), C.POINTER(C.c_void_p)]
+        L.tkv_greedy_decode.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, I32P, I64P]
+        L.tkv_context_destroy.argtypes = [C.c_void_p]
+        L.tkv_context_total_tokens.restype = C.c_int64
+        L.tkv_context_total_tokens.argtypes = [C.c_void_p]
+        L.tkv_context_next_position.restype = C.c_int64
+        L.tkv_context_next_position.argtypes = [C.c_void_p]
+        L.tkv_context_segments.restype = C.c_int64
+        L.tkv_context_segments.argtypes = [C.c_void_p, I64P, I32P, C.c_int64]
+        L.tkv_context_positions.argtypes = [C.c_void_p, I64P, C.c_int64]
+        L.tkv_context_last_logits.argtypes = [C.c_void_p, F32P, C.c_int64]
+        L.tkv_context_read_kv.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, F32P, C.c_int64]
+        L.tkv_context_mask.argtypes = [C.c_void_p, U8P, C.c_int64, C.c_int64]
+        L.tkv_engine_stream.restype = C.c_void_p
+        L.tkv_engine_stream.argtypes = [C.c_void_p]
+        L.tkv_profile_enable.argtypes = [C.c_void_p, C.c_int]
+        L.tkv_profile_read.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_double), I64P]
+        L.tkv_profile_reset.argtypes = [C.c_void_p]
+        L.tkv_launch_count.restype = C.c_int64
+        L.tkv_launch_count.argtypes = [C.c_void_p]
+        L.tkv_debug_set_mask_fault.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc:
+        raise _ERRORS.get(rc, Error)(lib().tkv_last_error().decode(errors="replace"))
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _i32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+
+
+@dataclass
+class ModelConfig:
+    """include/turbokv/config.hpp:11-34"""
+    layer_num: int = 0
+    head_num: int = 0
+    kv_head_num: int = 0
+    head_size: int = 0
+    hidden_size: int = 0
+    intermediate_size: int = 0
+    vocab_size: int = 0
+    rope_base: float = 10000.0
+    norm_eps: float = 1e-6
+
+    def _c(self) -> _Cfg:
+        return _Cfg(self.layer_num, self.head_num, self.kv_head_num, self.head_size, self.hidden_size,
+                    self.intermediate_size, self.vocab_size, self.rope_base, self.norm_eps)
+
+    @staticmethod
+    def preset(name: str) -> "ModelConfig":
+        c = _Cfg()
+        _check(lib().tkv_config_preset(name.encode(), C.byref(c)))
+        return ModelConfig(*(getattr(c, f[0]) for f in _Cfg._fields_))
+
+    @staticmethod
+    def toy() -> "ModelConfig":
+        return ModelConfig.preset("toy")
+
+    @staticmethod
+    def qwen2_7b_like() -> "ModelConfig":
+        return ModelConfig.preset("qwen2-7b")
+
+    @staticmethod
+    def llama3_8b_like() -> "ModelConfig":
+        return ModelConfig.preset("llama3-8b")
+
+    def validate(self) -> None:
+        _check(lib().tkv_config_validate(C.byref(self._c())))
+
+    def fingerprint_seed(self) -> int:
+        return lib().tkv_config_fingerprint_seed(C.byref(self._c()))
+
+    @property
+    def kv_dim(self) -> int:
+        return self.kv_head_num * self.head_size
+
+
+@dataclass
+class IngestStats:
+    chunks: int = 0
+    new_chunks: int = 0
+    bytes_written: int = 0
+
+
+@dataclass
+class FlopCounter:
+    """costmodel.hpp:53-63"""
+    qkv: int = 0
+    attn: int = 0
+    o: int = 0
+    mlp: int = 0
+
+    def total(self) -> int:
+        return self.qkv + self.attn + self.o + self.mlp
+
+    def _add(self, f: _Flops):
+        self.qkv += f.qkv
+        self.attn += f.attn
+        self.o += f.o
+        self.mlp += f.mlp
+
+
+def weights_identity(config: ModelConfig, seed: int):
+    """(weights_checksum, model_fingerprint) — model.cpp:94-118."""
+    ck, fp = C.c_uint64(), C.c_uint64()
+    _check(lib().tkv_weights_identity(C.byref(config._c()), seed, C.byref(ck), C.byref(fp)))
+    return ck.value, fp.value
+
+
+def chunk_content_id(framed, model_fingerprint: int) -> int:
+    """kvstore.cpp:58-64"""
+    f = _i32(framed)
+    return lib().tkv_chunk_content_id(model_fingerprint, _p(f, I32P), len(f))
+
+
+def frame_chunk(payload) -> np.ndarray:
+    """tok::frame_chunk (tokenizer.cpp:36-43)"""
+    return np.concatenate([[DOC_START], np.asarray(payload, np.int32), [DOC_END]]).astype(np.int32)
+
+
+def encode(text: str) -> np.ndarray:
+    """tok::encode (tokenizer.cpp:8-15)"""
+    return np.frombuffer(text.encode(), dtype=np.uint8).astype(np.int32)
+
+
+class AssembledContext:
+    """include/turbokv/context.hpp:16-38 — handle on a request cache in HBM."""
+
+    def __init__(self, engine: "Engine", handle):
+        self.engine, self._h = engine, handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().tkv_context_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def total_tokens(self) -> int:
+        return lib().tkv_context_total_tokens(self._h)
+
+    @property
+    def next_position(self) -> int:
+        return lib().tkv_context_next_position(self._h)
+
+    @property
+    def positions(self) -> np.ndarray:
+        n = self.total_tokens()
+        out = np.zeros(max(n, 1), np.int64)
+        _check(lib().tkv_context_positions(self._h, _p(out, I64P), len(out)))
+        return out[:n]
+
+    @property
+    def segments(self):
+        n = lib().tkv_context_segments(self._h, None, None, 0)
+        lens = np.zeros(max(n, 1), np.int64)
+        q = np.zeros(max(n, 1), np.int32)
+        lib().tkv_context_segments(self._h, _p(lens, I64P), _p(q, I32P), n)
+        return [(int(lens[i]), "query" if q[i] else "chunk") for i in range(n)]
+
+    @property
+    def last_logits(self) -> np.ndarray:
+        out = np.zeros(self.engine.config.vocab_size, np.float32)
+        _check(lib().tkv_context_last_logits(self._h, _p(out, F32P), len(out)))
+        return out[None, :]
+
+    def prefilled(self) -> bool:
+        try:
+            self.last_logits
+            return True
+        except DomainError:
+            return False
+
+    def read_kv(self, layer: int, which: str = "k", rotated: bool = False) -> np.ndarray:
+        n = self.total_tokens()
+        out = np.zeros((n, self.engine.config.kv_dim), np.float32)
+        _check(lib().tkv_context_read_kv(self._h, layer, 0 if which == "k" else 1, int(rotated),
+                                         _p(out, F32P), out.size))
+        return out
+
+    def mask(self, rows: int, cols: int) -> np.ndarray:
+        out = np.zeros((rows, cols), np.uint8)
+        _check(lib().tkv_context_mask(self._h, _p(out, U8P), rows, cols))
+        return out
+
+
+class Engine:
+    """turbokv::Engine (include/turbokv/pipeline.hpp:64-131) on one B200."""
+
+    def __init__(self, config: ModelConfig, seed: int, dtype: str | Dtype = "bf16", device: int = 0,
+                 page_tokens: int = 64, store_capacity_tokens: int = 0, max_position: int = 0,
+                 exact_fingerprint: int = -1, flags: int = 0):
+        self.config = config
+        self.seed = seed
+        o = _Opts()
+        lib().tkv_engine_opts_default(C.byref(o))
+        o.dtype = int(Dtype.F32 if str(dtype).lower() in ("f32", "fp32", "float32", "dtype.f32") or dtype == Dtype.F32
+                      else Dtype.BF16)
+        o.device, o.page_tokens, o.store_capacity_tokens = device, page_tokens, store_capacity_tokens
+        o.max_position, o.exact_fingerprint, o.flags = max_position, exact_fingerprint, flags
+        self.dtype = Dtype(o.dtype)
+        h = C.c_void_p()
+        _check(lib().tkv_engine_create(C.byref(config._c()), seed, C.byref(o), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tkv_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def fingerprint(self) -> int:
+        out = C.c_uint64()
+        _check(lib().tkv_engine_fingerprint(self._h, C.byref(out)))
+        return out.value
+
+    # ---- offline precompute ----
+    def ingest_chunks(self, payloads, stats: IngestStats | None = None) -> list[int]:
+        payloads = [np.asarray(p, np.int32) for p in payloads]
+        flat = _i32(np.concatenate(payloads) if payloads else np.zeros(0))
+        offs = np.ascontiguousarray(np.concatenate([[0], np.cumsum([len(p) for p in payloads])]), np.int64)
+        ids = np.zeros(max(len(payloads), 1), np.uint64)
+        st = _Stats()
+        _check(lib().tkv_ingest_chunks(self._h, _p(flat, I32P), _p(offs, I64P), len(payloads), _p(ids, U64P),
+                                       C.byref(st)))
+        if stats is not None:
+            stats.chunks += st.chunks
+            stats.new_chunks += st.new_chunks
+            stats.bytes_written += st.bytes_written
+        return [int(i) for i in ids[:len(payloads)]]
+
+    def ingest_chunk_payload(self, doc_id: str, payload, stats: IngestStats | None = None) -> int:
+        return self.ingest_chunks([payload], stats)[0]
+
+    def import_tkvc(self, path: str) -> int:
+        out = C.c_uint64()
+        _check(lib().tkv_import_tkvc(self._h, path.encode(), C.byref(out)))
+        return out.value
+
+    def export_tkvc(self, chunk_id: int, path: str) -> None:
+        _check(lib().tkv_export_tkvc(self._h, chunk_id, path.encode()))
+
+    def store_contains(self, chunk_id: int) -> bool:
+        out = C.c_int()
+        _check(lib().tkv_store_contains(self._h, chunk_id, C.byref(out)))
+        return bool(out.value)
+
+    def store_read(self, chunk_id: int, layer: int, which: str = "k") -> np.ndarray:
+        n = C.c_int64()
+        _check(lib().tkv_store_chunk_tokens(self._h, chunk_id, C.byref(n)))
+        out = np.zeros((n.value, self.config.kv_dim), np.float32)
+        _check(lib().tkv_store_read(self._h, chunk_id, layer, 0 if which == "k" else 1, _p(out, F32P), out.size))
+        return out
+
+    def store_count(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().tkv_store_count(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    # ---- online path ----
+    def assemble(self, chunk_ids, mode: PositionMode = PositionMode.Reordered) -> AssembledContext:
+        ids = np.ascontiguousarray(np.asarray(list(chunk_ids), dtype=np.uint64))
+        h = C.c_void_p()
+        _check(lib().tkv_assemble(self._h, _p(ids, U64P) if len(ids) else None, len(ids), int(mode), C.byref(h)))
+        return AssembledContext(self, h)
+
+    def prefill_query(self, ctx: AssembledContext, query_tokens, counter: FlopCounter | None = None) -> np.ndarray:
+        q = _i32(query_tokens)
+        out = np.zeros(self.config.vocab_size, np.float32)
+        fl = _Flops()
+        _check(lib().tkv_prefill_query(self._h, ctx.handle, _p(q, I32P) if len(q) else None, len(q),
+                                       _p(out, F32P), C.byref(fl)))
+        if counter is not None:
+            counter._add(fl)
+        return out[None, :]
+
+    def prefill_query_device(self, ctx: AssembledContext, d_tokens: int, n: int, d_logits: int) -> None:
+        _check(lib().tkv_prefill_query_device(self._h, ctx.handle, C.c_void_p(d_tokens), n, C.c_void_p(d_logits)))
+
+    def naive_prefill(self, framed_chunks, query_tokens, mode: MaskMode, counter: FlopCounter | None = None,
+                      keep_context: bool = True):
+        chunks = [np.asarray(c, np.int32) for c in framed_chunks]
+        flat = _i32(np.concatenate(chunks) if chunks else np.zeros(0))
+        offs = np.ascontiguousarray(np.concatenate([[0], np.cumsum([len(c) for c in chunks])]), np.int64)
+        q = _i32(query_tokens)
+        out = np.zeros(self.config.vocab_size, np.float32)
+        fl = _Flops()
+        h = C.c_void_p()
+        _check(lib().tkv_naive_prefill(self._h, _p(flat, I32P), _p(offs, I64P), len(chunks),
+                                       _p(q, I32P) if len(q) else None, len(q), int(mode), _p(out, F32P),
+                                       C.byref(fl), C.byref(h) if keep_context else None))
+        if counter is not None:
+            counter._add(fl)
+        return AssembledContext(self, h) if keep_context else out[None, :]
+
+    def naive_prefill_ids(self, chunk_ids, query_tokens, mode: MaskMode, counter: FlopCounter | None = None):
+        ids = np.ascontiguousarray(np.asarray(list(chunk_ids), dtype=np.uint64))
+        q = _i32(query_tokens)
+        out = np.zeros(self.config.vocab_size, np.float32)
+        fl = _Flops()
+        h = C.c_void_p()
+        _check(lib().tkv_naive_prefill_ids(self._h, _p(ids, U64P) if len(ids) else None, len(ids),
+                                           _p(q, I32P) if len(q) else None, len(q), int(mode), _p(out, F32P),
+                                           C.byref(fl), C.byref(h)))
+        if counter is not None:
+            counter._add(fl)
+        return AssembledContext(self, h)
+
+    def greedy_decode(self, ctx: AssembledContext, max_new: int, eos: int = EOS) -> list[int]:
+        out = np.zeros(max(max_new, 1), np.int32)
+        n = C.c_int64()
+        _check(lib().tkv_greedy_decode(self._h, ctx.handle, max_new, _p(out, I32P), C.byref(n)))
+        return out[:n.value].tolist()
+
+    # ---- measurement ----
+    def stream_ptr(self) -> int:
+        return lib().tkv_engine_stream(self._h) or 0
+
+    def profile(self, on: bool) -> None:
+        _check(lib().tkv_profile_enable(self._h, int(on)))
+
+    def profile_reset(self) -> None:
+        _check(lib().tkv_profile_reset(self._h))
+
+    def profile_read(self, kernel_class: str):
+        ms, n = C.c_double(), C.c_int64()
+        _check(lib().tkv_profile_read(self._h, kernel_class.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def launch_count(self) -> int:
+        return lib().tkv_launch_count(self._h)
+
+    def set_mask_fault(self, row: int, col: int) -> None:
+        _check(lib().tkv_debug_set_mask_fault(self._h, row, col))
+
+
+def greedy_decode(engine: Engine, ctx: AssembledContext, max_new: int, eos: int = EOS) -> list[int]:
+    """model.hpp:74-81"""
+    return engine.greedy_decode(ctx, max_new, eos)

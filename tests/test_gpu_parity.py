@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path (libtkv_b200.so through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): layouts, position ids and masks bit-exact; fp32 logits and KV within
+1e-4 relative; bf16 within 2e-2 with the first-token argmax identical whenever the oracle's top-1/top-2
+margin exceeds the measured bf16 error (SURVEY §7 hard part 4). "Relative" is |got-ref| <= tol *
+max(|ref|, 1e-2 * max|ref|) (a floor for near-zero logits).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2410_07590_b200 import turbokv as T
+from tests.tkvc_io import write_tkvc
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-4
+BF16_TOL = 2e-2
+
+
+def rel_excess(got, ref, floor_frac=1e-2):
+    got = np.asarray(got, np.float64).ravel()
+    ref = np.asarray(ref, np.float64).ravel()
+    scale = np.maximum(np.abs(ref), floor_frac * np.abs(ref).max())
+    return float((np.abs(got - ref) / scale).max())
+
+
+def assert_close(got, ref, tol):
+    e = rel_excess(got, ref)
+    assert e <= tol, f"relative error {e:.3e} > {tol}"
+
+
+def assert_argmax(got, ref, err_budget):
+    ref = np.asarray(ref).ravel()
+    got = np.asarray(got).ravel()
+    top = np.sort(ref)[::-1]
+    margin = (top[0] - top[1]) / np.abs(ref).max()
+    if margin > err_budget:
+        assert int(np.argmax(got)) == int(np.argmax(ref)), f"argmax differs with margin {margin:.3e}"
+
+
+def cfg_t(meta) -> T.ModelConfig:
+    return T.ModelConfig(**meta["config"])
+
+
+def payloads(A, name):
+    offs = A[f"{name}.payload_offsets"]
+    return [A[f"{name}.payloads"][offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
+
+
+def to_bf16(x: np.ndarray) -> np.ndarray:
+    """f64 -> f32 (RN) -> bf16 (RNE), returned as f32 — the engine's canonical cast."""
+    f = np.asarray(x, np.float64).astype(np.float32)
+    b = f.view(np.uint32).astype(np.uint64)
+    r = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
+
+
+_ENGINES = {}
+
+
+def engine(cfg: T.ModelConfig, seed: int, dtype: str, flags: int = 0) -> T.Engine:
+    key = (tuple(vars(cfg).values()), seed, dtype, flags)
+    if key not in _ENGINES:
+        _ENGINES[key] = T.Engine(cfg, seed, dtype=dtype, flags=flags, store_capacity_tokens=1 << 16)
+    return _ENGINES[key]
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
+@pytest.mark.parametrize("name", ["c1", "ragged"])
+def test_four_paths_vs_golden(golden, name, dtype, tol):
+    """C1 (BASELINE configs[0]) and a ragged grid: all four paths against the reference's logits."""
+    meta, A = golden
+    m = meta[name]
+    eng = engine(cfg_t(m), m["seed"], dtype)
+    assert f"{eng.fingerprint():016x}" == m["fingerprint"]
+    ids = eng.ingest_chunks(payloads(A, name))
+    assert [f"{i:016x}" for i in ids] == m["ids"]  # content ids bit-exact (kvstore.cpp:58-64)
+    q = A[f"{name}.query"]
+    for mode, tag in ((T.PositionMode.Reordered, "reordered"), (T.PositionMode.Composite, "composite")):
+        with eng.assemble(ids, mode) as ctx:
+            assert np.array_equal(ctx.positions, A[f"{name}.{tag}.positions"])
+            assert ctx.next_position == m[f"{tag}.next_position"]
+            logits = eng.prefill_query(ctx, q)[0]
+            ref = A[f"{name}.turbo_{tag}.logits"]
+            assert_close(logits, ref, tol)
+            assert_argmax(logits, ref, tol)
+    framed = [O.frame(p) for p in payloads(A, name)]
+    for mode, tag in ((T.MaskMode.Causal, "causal"), (T.MaskMode.Independent, "independent")):
+        logits = eng.naive_prefill(framed, q, mode, keep_context=False)[0]
+        assert_close(logits, A[f"{name}.naive_{tag}.logits"], tol)
+
+
+def test_turbo_equals_naive_independent_and_composite_defect(golden):
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], "f32")
+    ids = eng.ingest_chunks(payloads(A, "c1"))
+    q = A["c1.query"]
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        turbo = eng.prefill_query(ctx, q)[0]
+    with eng.naive_prefill_ids(ids, q, T.MaskMode.Independent) as naive:
+        oracle_logits = naive.last_logits[0]
+    assert_close(turbo, oracle_logits, FP32_TOL)  # proj/tests/test_pipeline.cpp:182-208
+    with eng.assemble(ids, T.PositionMode.Composite) as ctx:
+        comp = eng.prefill_query(ctx, q)[0]
+    assert np.abs(comp - oracle_logits).max() > 1e-3  # composite defect, test_pipeline.cpp:210-234
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_tkvc_import_gather_bit_exact(golden, tmp_path, dtype):
+    """Reference-format chunk caches -> HBM store -> fused gather: unrotated pages bit-exact after the
+    canonical cast, rotated keys within fp32 rounding of rope(ctx.k, positions)."""
+    meta, A = golden
+    m = meta["c1"]
+    cfg = O.TOY
+    framed = [O.frame(p) for p in payloads(A, "c1")]
+    paths, kvs = [], []
+    fresh_seed = 4242 + (dtype == "bf16")
+    port2 = O.Port(cfg, fresh_seed)
+    eng2 = T.Engine(cfg_t(m), fresh_seed, dtype=dtype, store_capacity_tokens=4096)
+    for f in framed:
+        k, v = port2.chunk_kv(f)
+        kvs.append((k, v))
+        paths.append(write_tkvc(str(tmp_path), port2.chunk_id(f), port2.fingerprint(), k, v, cfg.kv_head_num,
+                                cfg.head_size))
+    ids = [eng2.import_tkvc(p) for p in paths]
+    assert ids == [port2.chunk_id(f) for f in framed]
+    cast = (lambda x: x.astype(np.float32)) if dtype == "f32" else to_bf16
+    for (k, v), cid in zip(kvs, ids):
+        for layer in range(cfg.layer_num):
+            assert np.array_equal(eng2.store_read(cid, layer, "k"), cast(k[layer]))
+            assert np.array_equal(eng2.store_read(cid, layer, "v"), cast(v[layer]))
+    for mode in (T.PositionMode.Reordered, T.PositionMode.Composite):
+        with eng2.assemble(ids, mode) as ctx:
+            kref, vref, pos, nxt = port2.assemble(framed, mode == T.PositionMode.Reordered)
+            assert np.array_equal(ctx.positions, pos) and ctx.next_position == nxt
+            for layer in (0, cfg.layer_num - 1):
+                assert np.array_equal(ctx.read_kv(layer, "k", rotated=False), cast(kref[layer]))
+                assert np.array_equal(ctx.read_kv(layer, "v"), cast(vref[layer]))
+                rot_ref = O.Port.rope(cast(kref[layer]).astype(np.float64), pos, cfg.head_size)
+                rot = ctx.read_kv(layer, "k", rotated=True)
+                atol = 1e-6 if dtype == "f32" else 8e-3
+                assert np.abs(rot - rot_ref).max() <= atol * max(1.0, np.abs(rot_ref).max())
+            logits = eng2.prefill_query(ctx, A["c1.query"])[0]
+            ref = port2.prefill_query(kref, vref, pos, nxt, A["c1.query"])
+            assert_close(logits, ref, FP32_TOL if dtype == "f32" else BF16_TOL)
+    eng2.close()
+
+
+def dense(lo, hi, cols):
+    j = np.arange(cols)[None, :]
+    return ((j >= np.asarray(lo)[:, None]) & (j <= np.asarray(hi)[:, None])).astype(np.uint8)
+
+
+def test_masks_bit_exact(golden):
+    """The [lo, hi] predicate the kernels apply, materialised on device, equals the reference masks."""
+    meta, A = golden
+    eng = engine(T.ModelConfig.toy(), 42, "f32")
+    framed = [O.frame([97] * n) for n in (1, 2, 3)]  # framed lengths 3, 4, 5
+    q = [98, 99]
+    for mode, tag in ((T.MaskMode.Causal, "causal"), (T.MaskMode.Independent, "independent")):
+        with eng.naive_prefill(framed, q, mode) as ctx:
+            assert np.array_equal(ctx.mask(14, 14), A[f"mask.3452.{tag}"])
+    ids = eng.ingest_chunks([[97], [98, 99]])  # framed 3 + 4 = 7 past tokens
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        eng.prefill_query(ctx, [100, 101, 102, 103, 104])
+        assert np.array_equal(ctx.mask(5, 12), A["mask.causal_rows_5_7"])
+
+
+def test_positions_345(golden):
+    meta, _ = golden
+    eng = engine(T.ModelConfig.toy(), 42, "f32")
+    ids = eng.ingest_chunks([T.encode(s) for s in ("a", "bc", "def")])
+    for mode, tag in ((T.PositionMode.Reordered, "reordered"), (T.PositionMode.Composite, "composite")):
+        with eng.assemble(ids, mode) as ctx:
+            assert ctx.positions.tolist() == meta[f"positions_345.{tag}"]["positions"]
+            assert ctx.next_position == meta[f"positions_345.{tag}"]["next"]
+            assert ctx.segments == [(3, "chunk"), (4, "chunk"), (5, "chunk")]
+    with eng.assemble([], T.PositionMode.Reordered) as ctx:
+        assert ctx.total_tokens() == 0 and ctx.next_position == 0
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_ingest_kv_matches_oracle(dtype):
+    """Offline block-diagonal chunk prefill (several chunks packed in one forward) vs ingest_chunk_payload."""
+    cfg = O.TOY
+    port = O.Port(cfg, 42)
+    eng = engine(T.ModelConfig.toy(), 42, dtype)
+    pays = [O.random_text_tokens(9000 + i, n) for i, n in enumerate((5, 70, 1, 129))]
+    ids = eng.ingest_chunks(pays)
+    tol = 1e-4 if dtype == "f32" else 2e-2
+    for p, cid in zip(pays, ids):
+        k, v = port.chunk_kv(O.frame(p))
+        for layer in range(cfg.layer_num):
+            assert_close(eng.store_read(cid, layer, "k"), k[layer], tol)
+            assert_close(eng.store_read(cid, layer, "v"), v[layer], tol)
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
+def test_qwen_dims_one_layer_vs_golden(golden, dtype, tol):
+    meta, A = golden
+    m = meta["qwen1"]
+    eng = engine(cfg_t(m), m["seed"], dtype)
+    assert f"{eng.fingerprint():016x}" == m["fingerprint"]
+    ids = eng.ingest_chunks(payloads(A, "qwen1"))
+    assert [f"{i:016x}" for i in ids] == m["ids"]
+    for mode, tag in ((T.PositionMode.Reordered, "reordered"), (T.PositionMode.Composite, "composite")):
+        with eng.assemble(ids, mode) as ctx:
+            logits = eng.prefill_query(ctx, A["qwen1.query"])[0]
+            assert_close(logits, A[f"qwen1.turbo_{tag}.logits"], tol)
+            assert_argmax(logits, A[f"qwen1.turbo_{tag}.logits"], tol)
+    framed = [O.frame(p) for p in payloads(A, "qwen1")]
+    for mode, tag in ((T.MaskMode.Causal, "causal"), (T.MaskMode.Independent, "independent")):
+        assert_close(eng.naive_prefill(framed, A["qwen1.query"], mode, keep_context=False)[0],
+                     A[f"qwen1.naive_{tag}.logits"], tol)
+
+
+def test_tcgen05_gemm_matches_simt_gemm():
+    """bf16 tcgen05/TMA GEMM vs the SIMT GEMM on the same bf16 inputs (exact Qwen dims, 2 layers)."""
+    cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
+    tc = engine(cfg, 7, "bf16")
+    simt = engine(cfg, 7, "bf16", flags=T.FLAG_SIMT_GEMM)
+    pays = [O.random_text_tokens(500 + i, 254) for i in range(6)]
+    q = O.random_text_tokens(501, 64)
+    outs = []
+    for eng in (tc, simt):
+        ids = eng.ingest_chunks(pays)
+        with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+            outs.append(eng.prefill_query(ctx, q)[0])
+        outs.append(eng.naive_prefill([O.frame(p) for p in pays], q, T.MaskMode.Causal, keep_context=False)[0])
+    assert_close(outs[0], outs[2], 1e-2)
+    assert_close(outs[1], outs[3], 1e-2)
+
+
+def test_greedy_decode_matches_reference(golden):
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], "f32")
+    ids = eng.ingest_chunks(payloads(A, "c1"))
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        eng.prefill_query(ctx, A["c1.query"])
+        assert eng.greedy_decode(ctx, 8) == m["decode8"]
+
+
+def test_errors_map_to_reference_classes(tmp_path):
+    eng = engine(T.ModelConfig.toy(), 42, "f32")
+    ids = eng.ingest_chunks([[97, 98]])
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        with pytest.raises(T.DomainError):
+            eng.prefill_query(ctx, [])
+        with pytest.raises(T.DomainError):
+            eng.prefill_query(ctx, [300])
+    with pytest.raises(T.NotFoundError):
+        eng.assemble([0x1234], T.PositionMode.Reordered)
+    with pytest.raises(T.DomainError):
+        eng.naive_prefill([[256, 257], []], [97], T.MaskMode.Causal)
+    with pytest.raises(T.ConfigError):
+        T.Engine(T.ModelConfig(4, 8, 3, 8, 64, 192, 259), 1)
+    # a cache built under another model is stale (kvstore.cpp:169-172)
+    port = O.Port(O.TOY, 43)
+    f = O.frame([97, 98])
+    k, v = port.chunk_kv(f)
+    p = write_tkvc(str(tmp_path), port.chunk_id(f), port.fingerprint(), k, v, 2, 8)
+    with pytest.raises(T.StaleCacheError):
+        eng.import_tkvc(p)
+    raw = open(p, "rb").read()
+    bad = tmp_path / "trunc.tkvc"
+    bad.write_bytes(raw[:-8])
+    with pytest.raises(T.FormatError):
+        eng.import_tkvc(str(bad))
+    with pytest.raises(T.NotFoundError):
+        eng.import_tkvc(str(tmp_path / "missing.tkvc"))
+
+
+def test_mask_fault_breaks_equivalence(golden):
+    """verify --inject-fault (tools/turbokv_main.cpp:593-599): a corrupted independent mask must show."""
+    meta, A = golden
+    eng = engine(T.ModelConfig.toy(), 42, "f32")
+    framed = [O.frame(p) for p in payloads(A, "c1")]
+    q = A["c1.query"]
+    clean = eng.naive_prefill(framed, q, T.MaskMode.Independent, keep_context=False)[0]
+    eng.set_mask_fault(200, 0)  # a row of chunk 1 may now see chunk 0
+    faulty = eng.naive_prefill(framed, q, T.MaskMode.Independent, keep_context=False)[0]
+    assert np.abs(faulty - clean).max() > 1e-6
+
+
+def test_gather_roundtrip_at_c2_chunk_shape():
+    """Size-independent properties at the C2 chunk shape (Qwen dims, 16 x 512-token chunks, 2 layers):
+    the identity gather reproduces the store bit for bit, and rotated rows equal R(pos) applied to them."""
+    cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
+    eng = engine(cfg, 11, "bf16")
+    pays = [O.random_text_tokens(700 + i, 510) for i in range(16)]
+    ids = eng.ingest_chunks(pays)
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        assert ctx.total_tokens() == 16 * 512 and ctx.next_position == 8192
+        unrot = ctx.read_kv(1, "k", rotated=False)
+        rot = ctx.read_kv(1, "k", rotated=True)
+        v = ctx.read_kv(1, "v")
+        stored_k = np.concatenate([eng.store_read(i, 1, "k") for i in ids])
+        stored_v = np.concatenate([eng.store_read(i, 1, "v") for i in ids])
+        assert np.array_equal(unrot, stored_k) and np.array_equal(v, stored_v)
+        rows = np.r_[0:64, 4000:4064, 8128:8192]
+        ref = O.Port.rope(stored_k[rows].astype(np.float64), ctx.positions[rows], cfg.head_size)
+        assert np.abs(rot[rows] - ref).max() <= 8e-3 * max(1.0, np.abs(ref).max())
