@@ -201,6 +201,16 @@ int64_t tkv_launch_count(const tkv_engine* eng);
  * include/turbokv/pipeline.hpp:57-62): lets row `row` see column `col`. row < 0 disables. */
 tkv_status tkv_debug_set_mask_fault(tkv_engine* eng, int64_t row, int64_t col);
 
+/* Kernel-level entry points for unit tests (host buffers in, host fp32 out; inputs are rounded to
+ * `dtype` on the device first). gemm: out[M,N] = A[M,K] . W[N,K]^T with the tcgen05 (use_tc=1) or
+ * SIMT kernel and `splits` split-K partials (0 = auto). attention: the engine's flash attention with
+ * the [lo, hi] row predicate; q [Tq, H*d], k/v [Tk, Hkv*d], out [Tq, H*d]. */
+tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* A, const float* W, int64_t M,
+                          int64_t N, int64_t K, int splits, float* out);
+tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const float* q, const float* k,
+                               const float* v, const int32_t* lo, const int32_t* hi, int64_t Tq, int64_t Tk,
+                               int64_t H, int64_t Hkv, int64_t d, float* out);
+
 #ifdef __cplusplus
 }
 #endif

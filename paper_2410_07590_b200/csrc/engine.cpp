@@ -1634,4 +1634,92 @@ tkv_status tkv_debug_set_mask_fault(tkv_engine* e, int64_t row, int64_t col) {
     });
 }
 
+// ---- kernel-level test entry points ----
+namespace {
+struct DebugDev {
+    explicit DebugDev(int device) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            fail(TKV_ERR_CUDA, "no CUDA device");
+        }
+        TKV_CUDA(cudaSetDevice(device));
+    }
+};
+void* to_dev_dt(DevMem& m, const float* host, int64_t n, DT dt) {
+    DevMem f;
+    f.ensure((size_t)n * 4);
+    TKV_CUDA(cudaMemcpy(f.p, host, (size_t)n * 4, cudaMemcpyHostToDevice));
+    m.ensure((size_t)n * dt_size(dt));
+    launch_from_f32(f.as<float>(), n, m.p, dt, 0);
+    TKV_CUDA(cudaDeviceSynchronize());
+    return m.p;
+}
+}  // namespace
+
+tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* A, const float* W, int64_t M,
+                          int64_t N, int64_t K, int splits, float* out) {
+    return guard([&] {
+        need(A, "A");
+        need(W, "W");
+        need(out, "out");
+        DebugDev dd(device);
+        const DT dt = dtype == TKV_DTYPE_F32 ? DT::F32 : DT::BF16;
+        if (use_tc && dt != DT::BF16) fail(TKV_ERR_CONFIG, "tcgen05 GEMM is bf16-only");
+        if (use_tc && !gemm_tc_supported((int)M, (int)N, (int)K, (int)K)) fail(TKV_ERR_CONFIG, "unsupported shape");
+        DevMem a, w, part, o;
+        to_dev_dt(a, A, M * K, dt);
+        to_dev_dt(w, W, N * K, dt);
+        if (splits <= 0) splits = 1;
+        part.ensure((size_t)splits * M * N * 4);
+        o.ensure((size_t)M * N * 4);
+        if (use_tc)
+            launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, part.as<float>(), splits, 0);
+        else
+            launch_gemm_simt(a.p, (int)K, w.p, (int)M, (int)N, (int)K, part.as<float>(), splits, dt, 0);
+        launch_reduce_splits(part.as<float>(), splits, M * N, o.as<float>(), 0);
+        TKV_CUDA(cudaDeviceSynchronize());
+        TKV_CUDA(cudaMemcpy(out, o.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const float* q, const float* k, const float* v,
+                               const int32_t* lo, const int32_t* hi, int64_t Tq, int64_t Tk, int64_t H, int64_t Hkv,
+                               int64_t d, float* out) {
+    return guard([&] {
+        DebugDev dd(device);
+        (void)impl;
+        const DT dt = dtype == TKV_DTYPE_F32 ? DT::F32 : DT::BF16;
+        DevMem dq, dk, dv, dlo, dhi, dout, of, ws, errm;
+        to_dev_dt(dq, q, Tq * H * d, dt);
+        to_dev_dt(dk, k, Tk * Hkv * d, dt);
+        to_dev_dt(dv, v, Tk * Hkv * d, dt);
+        dlo.ensure((size_t)Tq * 4);
+        dhi.ensure((size_t)Tq * 4);
+        TKV_CUDA(cudaMemcpy(dlo.p, lo, (size_t)Tq * 4, cudaMemcpyHostToDevice));
+        TKV_CUDA(cudaMemcpy(dhi.p, hi, (size_t)Tq * 4, cudaMemcpyHostToDevice));
+        dout.ensure((size_t)Tq * H * d * dt_size(dt));
+        of.ensure((size_t)Tq * H * d * 4);
+        errm.ensure(4);
+        TKV_CUDA(cudaMemset(errm.p, 0, 4));
+        int dev_sms = 148;
+        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+        const int splits = attn_pick_splits((int)Tq, (int)H, (int)Hkv, (int)Tk, dev_sms);
+        AttnWork w;
+        if (splits > 1) {
+            ws.ensure(attn_workspace_floats((int)Tq, (int)H, (int)d, splits) * 4);
+            w.o = ws.as<float>();
+            w.ml = w.o + (size_t)splits * Tq * H * d;
+        }
+        launch_attention_simt(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p, (int)Tq,
+                              (int)Tk, (int)H, (int)Hkv, (int)d, splits, w, errm.as<int>(), dt, 0);
+        launch_to_f32(dout.p, Tq * H * d, of.as<float>(), dt, 0);
+        TKV_CUDA(cudaDeviceSynchronize());
+        int e = 0;
+        TKV_CUDA(cudaMemcpy(&e, errm.p, 4, cudaMemcpyDeviceToHost));
+        if (e & 8) fail(TKV_ERR_DEGENERATE_ROW, "attention: row with no attendable positions");
+        TKV_CUDA(cudaMemcpy(out, of.p, (size_t)Tq * H * d * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
 }  // extern "C"

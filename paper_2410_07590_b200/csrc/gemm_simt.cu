@@ -35,6 +35,9 @@ __global__ void __launch_bounds__(THREADS) gemm_simt_kernel(const T* __restrict_
             Ws[lk + e][lr] = (kin && n0 + lr < N) ? ld(W, (int64_t)(n0 + lr) * K + k) : 0.f;
         }
         __syncthreads();
+        // two-level summation: a fresh 16-term partial per k-tile, then one add into the running sum,
+        // so rounding error grows with 16 + K/16 instead of K (fp32 path's 1e-4 budget at K = 18944)
+        float part[4][4] = {};
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
             float a[4], w[4];
@@ -45,8 +48,12 @@ __global__ void __launch_bounds__(THREADS) gemm_simt_kernel(const T* __restrict_
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) part[i][j] = fmaf(a[i], w[j], part[i][j]);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] += part[i][j];
         __syncthreads();
     }
     float* out = partial + (int64_t)z * M * N;

@@ -299,6 +299,20 @@ __global__ void to_f32_kernel(const T* src, int64_t n, float* dst) {
         dst[o] = ldf(src, o);
 }
 
+template <typename T>
+__global__ void from_f32_kernel(const float* src, int64_t n, T* dst) {
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
+        stf(dst, o, src[o]);
+}
+
+__global__ void reduce_splits_kernel(const float* p, int splits, int64_t n, float* out) {
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+        float a = 0.f;
+        for (int s = 0; s < splits; ++s) a += p[s * n + o];
+        out[o] = a;
+    }
+}
+
 inline int grid_for(int64_t n, int block, int cap = 148 * 16) {
     int64_t g = (n + block - 1) / block;
     if (g < 1) g = 1;
@@ -405,6 +419,16 @@ void launch_unrotate_rows(const void* k, int rows, int kvd, int d, const int32_t
 
 void launch_to_f32(const void* src, int64_t n, float* dst, DT dt, cudaStream_t s) {
     DISPATCH_DT(dt, to_f32_kernel<T><<<grid_for(n, 256), 256, 0, s>>>((const T*)src, n, dst));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_from_f32(const float* src, int64_t n, void* dst, DT dt, cudaStream_t s) {
+    DISPATCH_DT(dt, from_f32_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(src, n, (T*)dst));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_reduce_splits(const float* partial, int splits, int64_t n, float* out, cudaStream_t s) {
+    reduce_splits_kernel<<<grid_for(n, 256), 256, 0, s>>>(partial, splits, n, out);
     TKV_CUDA(cudaGetLastError());
 }
 

@@ -84,6 +84,9 @@ void launch_mask_materialize(const int32_t* lo, const int32_t* hi, int rows, int
 void launch_unrotate_rows(const void* k, int rows, int kv_dim, int d, const int32_t* pos, const float2* rope,
                           float* out, DT dt, cudaStream_t s);
 void launch_to_f32(const void* src, int64_t n, float* dst, DT dt, cudaStream_t s);
+void launch_from_f32(const float* src, int64_t n, void* dst, DT dt, cudaStream_t s);
+// sum split-K partials [splits][n] -> out[n]
+void launch_reduce_splits(const float* partial, int splits, int64_t n, float* out, cudaStream_t s);
 
 // GEMM: partial[z][m][n] = sum_{k in split z} A[m][k] * W[n][k]   (A [M][lda] dtype, W [N][K] dtype).
 void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,

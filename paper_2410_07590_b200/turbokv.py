@@ -150,6 +150,10 @@ def lib():
         L.tkv_launch_count.restype = C.c_int64
         L.tkv_launch_count.argtypes = [C.c_void_p]
         L.tkv_debug_set_mask_fault.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+        L.tkv_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, F32P, F32P, C.c_int64, C.c_int64, C.c_int64,
+                                     C.c_int, F32P]
+        L.tkv_debug_attention.argtypes = [C.c_int, C.c_int, C.c_int, F32P, F32P, F32P, I32P, I32P, C.c_int64,
+                                          C.c_int64, C.c_int64, C.c_int64, C.c_int64, F32P]
         _lib = L
     return _lib
 
@@ -493,6 +497,36 @@ class Engine:
 
     def set_mask_fault(self, row: int, col: int) -> None:
         _check(lib().tkv_debug_set_mask_fault(self._h, row, col))
+
+
+def debug_gemm(A: np.ndarray, W: np.ndarray, dtype: str = "bf16", use_tc: bool = True, splits: int = 1,
+               device: int = 0) -> np.ndarray:
+    """out = A . W^T through the engine's GEMM kernel (kernel unit tests)."""
+    A = np.ascontiguousarray(A, np.float32)
+    W = np.ascontiguousarray(W, np.float32)
+    M, K = A.shape
+    N = W.shape[0]
+    out = np.zeros((M, N), np.float32)
+    dt = Dtype.F32 if dtype == "f32" else Dtype.BF16
+    _check(lib().tkv_debug_gemm(device, int(dt), int(use_tc), _p(A, F32P), _p(W, F32P), M, N, K, splits,
+                                _p(out, F32P)))
+    return out
+
+
+def debug_attention(q, k, v, lo, hi, H: int, Hkv: int, d: int, dtype: str = "bf16", impl: int = 0,
+                    device: int = 0) -> np.ndarray:
+    """The engine's flash attention with the [lo, hi] row predicate (kernel unit tests)."""
+    q = np.ascontiguousarray(q, np.float32)
+    k = np.ascontiguousarray(k, np.float32)
+    v = np.ascontiguousarray(v, np.float32)
+    lo = _i32(lo)
+    hi = _i32(hi)
+    Tq, Tk = q.shape[0], k.shape[0]
+    out = np.zeros((Tq, H * d), np.float32)
+    dt = Dtype.F32 if dtype == "f32" else Dtype.BF16
+    _check(lib().tkv_debug_attention(device, int(dt), impl, _p(q, F32P), _p(k, F32P), _p(v, F32P), _p(lo, I32P),
+                                     _p(hi, I32P), Tq, Tk, H, Hkv, d, _p(out, F32P)))
+    return out
 
 
 def greedy_decode(engine: Engine, ctx: AssembledContext, max_new: int, eos: int = EOS) -> list[int]:

