@@ -204,7 +204,8 @@ tkv_status tkv_debug_set_mask_fault(tkv_engine* eng, int64_t row, int64_t col);
 /* Kernel-level entry points for unit tests (host buffers in, host fp32 out; inputs are rounded to
  * `dtype` on the device first). gemm: out[M,N] = A[M,K] . W[N,K]^T with the tcgen05 (use_tc=1) or
  * SIMT kernel and `splits` split-K partials (0 = auto). attention: the engine's flash attention with
- * the [lo, hi] row predicate; q [Tq, H*d], k/v [Tk, Hkv*d], out [Tq, H*d]. */
+ * the [lo, hi] row predicate; q [Tq, H*d], k/v [Tk, Hkv*d], out [Tq, H*d]. impl: 0 = the engine's choice
+ * (tcgen05 for bf16 head_size 128), 1 = SIMT. */
 tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* A, const float* W, int64_t M,
                           int64_t N, int64_t K, int splits, float* out);
 tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const float* q, const float* k,

@@ -13,6 +13,8 @@
 #include <float.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "tkv_internal.h"
 
 namespace tkv {
@@ -169,13 +171,7 @@ void launch_d(const void* q, const void* k, const void* v, int kv_stride, const 
     attn_simt_kernel<T, D><<<grid, THREADS, 0, s>>>((const T*)q, (const T*)k, (const T*)v, kv_stride, lo, hi, (T*)out,
                                                     ws.o, ws.ml, Tq, Tk, H, Hkv, splits, scale, err);
     TKV_CUDA(cudaGetLastError());
-    if (splits > 1) {
-        const int64_t n = (int64_t)Tq * H * D;
-        int grid2 = (int)((n + 255) / 256);
-        if (grid2 > 148 * 16) grid2 = 148 * 16;
-        attn_combine_kernel<T><<<grid2, 256, 0, s>>>(ws.o, ws.ml, Tq * H, D, splits, (T*)out, err);
-        TKV_CUDA(cudaGetLastError());
-    }
+    if (splits > 1) launch_attention_combine(ws, Tq * H, D, splits, out, err, std::is_same<T, float>::value ? DT::F32 : DT::BF16, s);
 }
 
 template <typename T>
@@ -192,6 +188,18 @@ void launch_t(int d, const void* q, const void* k, const void* v, int kv_stride,
 }
 
 }  // namespace
+
+void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, void* out, int* err, DT dt,
+                              cudaStream_t s) {
+    const int64_t n = (int64_t)rows * d;
+    int grid = (int)((n + 255) / 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    if (dt == DT::F32)
+        attn_combine_kernel<float><<<grid, 256, 0, s>>>(ws.o, ws.ml, rows, d, splits, (float*)out, err);
+    else
+        attn_combine_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(ws.o, ws.ml, rows, d, splits, (__nv_bfloat16*)out, err);
+    TKV_CUDA(cudaGetLastError());
+}
 
 size_t attn_workspace_floats(int Tq, int H, int d, int splits) {
     return splits <= 1 ? 0 : (size_t)splits * Tq * H * (d + 2);

@@ -1,0 +1,422 @@
+// tcgen05 / TMEM / TMA flash attention for head_size 128, bf16 — the query-prefill attention of the
+// TurboRAG path (and the full-concat comparison), replacing attend + softmax_rows_inplace
+// (src/attention.cpp:94-169, src/numerics.cpp:31-60) with implicit masks: row t sees key j iff
+// lo[t] <= j <= hi[t] (causal_rows / build_mask, attention.cpp:50-92).
+//
+// GQA packing: a CTA owns 128 rows of ONE kv head g, row r = (token t, head g*group + r%group), so the
+// K/V tiles it streams serve all `group` query heads (C2: 64 tokens x 7 heads = 448 rows = 3.5 tiles).
+//
+// Per CTA (192 threads): warps 0-3 = softmax (one row per thread), warp 4 = TMA producer, warp 5 = MMA
+// issuer. smem: Q [128x128] and P [128x128] (two 64-column SW128 sub-tiles each, 32 KB), two K/V stages
+// of 64 KB. TMEM (512 cols): S double buffer at cols 0/128, O tile at 256.
+//   S_j  = Q . K_j^T          tcgen05.mma kind::f16 M128 N128 K16 x8, A,B K-major
+//   P_j  = exp2(S_j*scale*log2e - m_j)  (softmax warps: TMEM -> regs -> bf16 -> swizzled smem)
+//   O_j  = P_j . V_j          tcgen05.mma, A = P (K-major), B = V (MN-major: d contiguous)
+// The running output O lives in registers (128 fp32 per thread), rescaled by exp2(m_{j-1} - m_j) each
+// tile and incremented by the O_j tile read back from TMEM. Split-K over keys writes (O, m, l) partials
+// combined by attn_combine_kernel (attn_simt.cu) — same workspace layout as the SIMT kernel.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+
+#include "tkv_internal.h"
+
+namespace tkv {
+namespace {
+
+constexpr int D = 128, BR = 128, BK = 128, THREADS = 192;
+constexpr uint32_t SUB = 128 * 64 * 2;          // one [128 rows][64 cols] bf16 SW128 sub-tile = 16 KB
+constexpr uint32_t OFF_Q = 0, OFF_P = 2 * SUB;  // 32 KB each
+constexpr uint32_t OFF_KV = 4 * SUB;            // stage s: K at OFF_KV + s*4*SUB, V at +2*SUB
+constexpr uint32_t STAGE = 4 * SUB;             // 64 KB
+constexpr uint32_t OFF_BAR = OFF_KV + 2 * STAGE;
+constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr float LOG2E = 1.4426950408889634f;
+
+// kind::f16, D=f32, A=B=bf16, M=128, N=128; PV additionally B MN-major (bit 16)
+constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+constexpr uint32_t IDESC_PV = IDESC_S | (1u << 16);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    for (uint32_t spin = 0;; ++spin) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spin > (1u << 26)) __trap();  // protocol bug -> launch error, never a hung GPU
+    }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+// K-major SW128 (rows of 128 B, 8-row atoms 1024 B apart)
+__device__ __forceinline__ uint64_t desc_k(uint32_t a) {
+    return (uint64_t)((a & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+           ((uint64_t)2 << 61);
+}
+// MN-major SW128: 64-element MN blocks LBO = 16 KB apart (the two d-halves), 8-row K groups SBO = 1024 B apart
+__device__ __forceinline__ uint64_t desc_mn(uint32_t a) {
+    return (uint64_t)((a & 0x3FFFF) >> 4) | ((uint64_t)(SUB >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+// byte offset of 16-byte chunk `c` (0..7) of row `r` inside a K-major SW128 sub-tile
+__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                   const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ lo,
+                   const int32_t* __restrict__ hi, __nv_bfloat16* __restrict__ out, float* __restrict__ ws_o,
+                   float* __restrict__ ws_ml, int Tq, int Tk, int H, int Hkv, int splits, float scale, int* err) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* kv_full = bars;       // [2]
+    uint64_t* kv_empty = bars + 2;  // [2]
+    uint64_t* s_full = bars + 4;    // [2]
+    uint64_t* p_full = bars + 6;
+    uint64_t* o_full = bars + 7;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    __shared__ int red_lo[THREADS / 32], red_hi[THREADS / 32];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int group = H / Hkv, g = blockIdx.y, split = blockIdx.z;
+    const int rows_total = Tq * group;
+    const int row = blockIdx.x * BR + tid;  // softmax threads only
+    const bool active = tid < BR && row < rows_total;
+    const int t = active ? row / group : 0;
+    const int h = g * group + (active ? row % group : 0);
+    const int my_lo = active ? lo[t] : INT32_MAX;
+    const int my_hi = active ? min(hi[t], Tk - 1) : -1;
+
+    // ---- CTA key range (union of its rows), then this split's share, in 128-key tiles ----
+    int blo = my_lo, bhi = my_hi;
+    for (int o = 16; o > 0; o >>= 1) {
+        blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+        bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+    }
+    if (lane == 0) {
+        red_lo[warp] = blo;
+        red_hi[warp] = bhi;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+            mbar_init(&s_full[s], 1);
+        }
+        mbar_init(p_full, BR);
+        mbar_init(o_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // ---- Q tile: each softmax thread stages its own row into the two swizzled sub-tiles ----
+    if (tid < BR) {
+        const uint4* src = reinterpret_cast<const uint4*>(q + (int64_t)t * H * D + (int64_t)h * D);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const uint4 v = active ? src[c] : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(smem + OFF_Q + (c >> 3) * SUB + swz(tid, c & 7)) = v;
+        }
+        fence_async_smem();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    blo = red_lo[0];
+    bhi = red_hi[0];
+    for (int w = 1; w < THREADS / 32; ++w) {
+        blo = min(blo, red_lo[w]);
+        bhi = max(bhi, red_hi[w]);
+    }
+    blo = max(blo, 0);
+    const int span = bhi - blo + 1;
+    const int chunk = span > 0 ? ((span + splits - 1) / splits + BK - 1) / BK * BK : 0;
+    const int ks = blo + split * chunk;
+    const int ke = min(bhi, ks + chunk - 1);
+    const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
+
+    if (warp == 4) {
+        if (lane == 0) {  // ---------------- TMA producer ----------------
+            for (int j = 0; j < n; ++j) {
+                const int s = j & 1;
+                mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[s], STAGE);
+                const uint32_t st = sbase + OFF_KV + s * STAGE;
+                const int key = ks + j * BK;
+                tma_load_2d(st, &tmK, &kv_full[s], g * D, key);
+                tma_load_2d(st + SUB, &tmK, &kv_full[s], g * D + 64, key);
+                tma_load_2d(st + 2 * SUB, &tmV, &kv_full[s], g * D, key);
+                tma_load_2d(st + 3 * SUB, &tmV, &kv_full[s], g * D + 64, key);
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {  // ---------------- MMA issuer ----------------
+            auto issue_s = [&](int j) {
+                const int s = j & 1;
+                mbar_wait(&kv_full[s], (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t kb = sbase + OFF_KV + s * STAGE;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
+                    umma(tmem + s * 128, desc_k(sbase + OFF_Q + off), desc_k(kb + off), IDESC_S, kk > 0);
+                }
+                umma_commit(&s_full[s]);
+            };
+            if (n > 0) issue_s(0);
+            if (n > 1) issue_s(1);
+            for (int j = 0; j < n; ++j) {
+                const int s = j & 1;
+                mbar_wait(p_full, j & 1);
+                tc_fence_after();
+                const uint32_t vb = sbase + OFF_KV + s * STAGE + 2 * SUB;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t aoff = (kk >> 2) * SUB + (kk & 3) * 32;
+                    umma(tmem + 256, desc_k(sbase + OFF_P + aoff), desc_mn(vb + kk * 2048), IDESC_PV, kk > 0);
+                }
+                umma_commit(o_full);
+                umma_commit(&kv_empty[s]);
+                if (j + 2 < n) issue_s(j + 2);
+            }
+        }
+    } else {
+        // ---------------- softmax warps: one row per thread ----------------
+        const float sl2 = scale * LOG2E;
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        float o[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) o[i] = 0.f;
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < n; ++j) {
+            const int key0 = ks + j * BK;
+            const uint32_t sa = tmem + lane_base + (uint32_t)((j & 1) * 128);
+            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            tc_fence_after();
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t v[32];
+                tmem_ld32(sa + c * 32, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int key = key0 + c * 32 + i;
+                    const bool vis = key >= my_lo && key <= my_hi;
+                    mx = fmaxf(mx, vis ? __uint_as_float(v[i]) * sl2 : -INFINITY);
+                }
+            }
+            const float m_new = fmaxf(m, mx);
+            const float alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
+            if (j > 0) {  // fold in O tile j-1 (P smem becomes free once it has landed)
+                mbar_wait(o_full, (j - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + lane_base + 256 + c * 32, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[c * 32 + i] += __uint_as_float(v[i]);
+                }
+            }
+            float rs = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t v[32];
+                tmem_ld32(sa + c * 32, v);
+                tmem_wait_ld();
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const int key = key0 + c * 32 + i;
+                    const bool v0 = key >= my_lo && key <= my_hi && m_new != -INFINITY;
+                    const bool v1 = key + 1 >= my_lo && key + 1 <= my_hi && m_new != -INFINITY;
+                    const float p0 = v0 ? ex2(__uint_as_float(v[i]) * sl2 - m_new) : 0.f;
+                    const float p1 = v1 ? ex2(__uint_as_float(v[i + 1]) * sl2 - m_new) : 0.f;
+                    rs += p0 + p1;
+                    pk[i / 2] = pack_bf16(p0, p1);
+                }
+                uint8_t* pb = smem + OFF_P + (c >> 1) * SUB;
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd)
+                    *reinterpret_cast<uint4*>(pb + swz(tid, (c & 1) * 4 + qd)) =
+                        make_uint4(pk[4 * qd], pk[4 * qd + 1], pk[4 * qd + 2], pk[4 * qd + 3]);
+            }
+            l = l * alpha + rs;
+#pragma unroll
+            for (int i = 0; i < D; ++i) o[i] *= alpha;
+            m = m_new;
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(p_full);
+        }
+        if (n > 0) {
+            mbar_wait(o_full, (n - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_base + 256 + c * 32, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) o[c * 32 + i] += __uint_as_float(v[i]);
+            }
+        }
+        if (active) {
+            const int64_t orow = (int64_t)t * H + h;
+            if (splits == 1) {
+                if (l == 0.f) {
+                    atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
+                } else {
+                    const float inv = 1.0f / l;
+                    uint4* dst = reinterpret_cast<uint4*>(out + orow * D);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        dst[c] = make_uint4(pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv),
+                                            pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
+                                            pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv),
+                                            pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+                }
+            } else {
+                float4* wo = reinterpret_cast<float4*>(ws_o + ((int64_t)split * Tq * H + orow) * D);
+#pragma unroll
+                for (int c = 0; c < 32; ++c) wo[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                ws_ml[((int64_t)split * Tq * H + orow) * 2 + 0] = m == -INFINITY ? -INFINITY : m / LOG2E;
+                ws_ml[((int64_t)split * Tq * H + orow) * 2 + 1] = l;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    if (!fn) fail(TKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap kv_map(const void* base, int rows, int cols, int ld) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    const cuuint32_t box[2] = {64, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(TKV_ERR_CUDA, "cuTensorMapEncodeTiled (attention) failed: " + std::to_string((int)r));
+    return m;
+}
+
+}  // namespace
+
+bool attention_tc_supported(int d, DT dt) { return d == 128 && dt == DT::BF16; }
+
+int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms) {
+    const int group = H / Hkv;
+    const int ctas = ((Tq * group + BR - 1) / BR) * Hkv;
+    int s = (num_sms + ctas - 1) / ctas;
+    const int max_by_keys = (Tk + 4 * BK - 1) / (4 * BK);  // >= 4 key tiles per split
+    if (s > max_by_keys) s = max_by_keys;
+    if (s > 32) s = 32;
+    return s < 1 ? 1 : s;
+}
+
+void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
+                         const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
+                         int* err, cudaStream_t s) {
+    TKV_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    const CUtensorMap tk = kv_map(k, Tk, kv_stride, kv_stride);
+    const CUtensorMap tv = kv_map(v, Tk, kv_stride, kv_stride);
+    const int group = H / Hkv;
+    dim3 grid((Tq * group + BR - 1) / BR, Hkv, splits);
+    const float scale = (float)(1.0 / sqrt((double)D));
+    attn_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(tk, tv, (const __nv_bfloat16*)q, lo, hi, (__nv_bfloat16*)out,
+                                                     ws.o, ws.ml, Tq, Tk, H, Hkv, splits, scale, err);
+    TKV_CUDA(cudaGetLastError());
+    if (splits > 1) launch_attention_combine(ws, Tq * H, D, splits, out, err, DT::BF16, s);
+}
+
+}  // namespace tkv

@@ -530,7 +530,9 @@ void tkv_engine::forward(const Fwd& f) {
         const int rows = tail ? 1 : T;
         const int64_t r0 = tail ? T - 1 : 0;
         {
-            const int splits = attn_pick_splits(rows, (int)H, (int)Hkv, Tk, num_sms);
+            const bool tc = dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_ATTN) && attention_tc_supported((int)d, dt);
+            const int splits = tc ? attn_tc_pick_splits(rows, (int)H, (int)Hkv, Tk, num_sms)
+                                  : attn_pick_splits(rows, (int)H, (int)Hkv, Tk, num_sms);
             AttnWork ws;
             if (splits > 1) {
                 const size_t fl = attn_workspace_floats(rows, (int)H, (int)d, splits);
@@ -539,9 +541,14 @@ void tkv_engine::forward(const Fwd& f) {
                 ws.ml = ws.o + (size_t)splits * rows * H * d;
             }
             Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);
-            launch_attention_simt(static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es, kv_plane(f.ctx, l, 0),
-                                  kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0, f.hi + r0, attn.p, rows, Tk, (int)H,
-                                  (int)Hkv, (int)d, splits, ws, err.as<int>(), dt, stream);
+            const void* qrows = static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es;
+            if (tc)
+                launch_attention_tc(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
+                                    f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream);
+            else
+                launch_attention_simt(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
+                                      f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, (int)d, splits, ws,
+                                      err.as<int>(), dt, stream);
         }
         uint8_t* attn_rows = static_cast<uint8_t*>(attn.p);
         float* x_rows = x.as<float>() + r0 * hid;
@@ -1688,7 +1695,6 @@ tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const floa
                                int64_t d, float* out) {
     return guard([&] {
         DebugDev dd(device);
-        (void)impl;
         const DT dt = dtype == TKV_DTYPE_F32 ? DT::F32 : DT::BF16;
         DevMem dq, dk, dv, dlo, dhi, dout, of, ws, errm;
         to_dev_dt(dq, q, Tq * H * d, dt);
@@ -1704,15 +1710,21 @@ tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const floa
         TKV_CUDA(cudaMemset(errm.p, 0, 4));
         int dev_sms = 148;
         cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-        const int splits = attn_pick_splits((int)Tq, (int)H, (int)Hkv, (int)Tk, dev_sms);
+        const bool tc = impl == 0 && attention_tc_supported((int)d, dt);
+        const int splits = tc ? attn_tc_pick_splits((int)Tq, (int)H, (int)Hkv, (int)Tk, dev_sms)
+                              : attn_pick_splits((int)Tq, (int)H, (int)Hkv, (int)Tk, dev_sms);
         AttnWork w;
         if (splits > 1) {
             ws.ensure(attn_workspace_floats((int)Tq, (int)H, (int)d, splits) * 4);
             w.o = ws.as<float>();
             w.ml = w.o + (size_t)splits * Tq * H * d;
         }
-        launch_attention_simt(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p, (int)Tq,
-                              (int)Tk, (int)H, (int)Hkv, (int)d, splits, w, errm.as<int>(), dt, 0);
+        if (tc)
+            launch_attention_tc(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p,
+                                (int)Tq, (int)Tk, (int)H, (int)Hkv, splits, w, errm.as<int>(), 0);
+        else
+            launch_attention_simt(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p,
+                                  (int)Tq, (int)Tk, (int)H, (int)Hkv, (int)d, splits, w, errm.as<int>(), dt, 0);
         launch_to_f32(dout.p, Tq * H * d, of.as<float>(), dt, 0);
         TKV_CUDA(cudaDeviceSynchronize());
         int e = 0;

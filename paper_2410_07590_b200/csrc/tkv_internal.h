@@ -109,4 +109,14 @@ void launch_attention_simt(const void* q, const void* k, const void* v, int kv_s
                            const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int d, int splits,
                            const AttnWork& ws, int* err, DT dt, cudaStream_t s);
 
+// tcgen05/TMEM/TMA attention (attn_tc.cu): head_size 128, bf16. Same predicate and workspace as SIMT.
+bool attention_tc_supported(int d, DT dt);
+int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms);
+void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
+                         const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
+                         int* err, cudaStream_t s);
+// merge split-K (O, m, l) partials into out (dtype)
+void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, void* out, int* err, DT dt,
+                              cudaStream_t s);
+
 }  // namespace tkv
