@@ -291,6 +291,9 @@ def run_ours(args):
         big1.record(stream)
         torch.cuda.synchronize(dev)
     gpu_launches = eng.launch_count() - launches0
+    if args.turbo_only:
+        print(json.dumps({"p50_ttft_ms": statistics.median([s.elapsed_time(e) for s, e in zip(starts, ends)])}))
+        return
     per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = big0.elapsed_time(big1)
     if ws > 1:
@@ -406,6 +409,7 @@ def main():
     ap.add_argument("--naive-reps", type=int, default=3)
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--turbo-only", action="store_true", help="timed turbo steps only (for ncu captures)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -138,27 +138,37 @@ __global__ void __launch_bounds__(THREADS) attn_simt_kernel(const T* __restrict_
     }
 }
 
+// Split-K merge, one warp per (token, head) row: lane s < splits holds split s's (m, l); every lane then
+// accumulates its d-columns over the splits with the broadcast weights exp(m_s - max).
 template <typename T>
-__global__ void attn_combine_kernel(const float* ws_o, const float* ws_ml, int rows, int D, int splits, T* out,
-                                    int* err) {
-    const int64_t n = (int64_t)rows * D;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / D;
-        float mx = -INFINITY;
-        for (int s = 0; s < splits; ++s) mx = fmaxf(mx, ws_ml[((int64_t)s * rows + row) * 2]);
-        if (mx == -INFINITY) {
-            if (i % D == 0) atomicOr(err, 8);
-            continue;
-        }
-        float L = 0.f, acc = 0.f;
+__global__ void attn_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_ml, int rows, int D,
+                                    int splits, T* __restrict__ out, int* err) {
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float ms = -INFINITY, ls = 0.f;
+    if (lane < splits) {
+        ms = ws_ml[((int64_t)lane * rows + row) * 2];
+        ls = ws_ml[((int64_t)lane * rows + row) * 2 + 1];
+    }
+    float mx = ms;
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (mx == -INFINITY) {  // DegenerateRowError (numerics.cpp:39-42)
+        if (lane == 0) atomicOr(err, 8);
+        return;
+    }
+    const float w = (ms == -INFINITY) ? 0.f : expf(ms - mx);
+    float L = ls * w;
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    const float inv = 1.0f / L;
+    for (int c0 = 0; c0 < D; c0 += 32) {
+        const int c = c0 + lane;
+        float acc = 0.f;
         for (int s = 0; s < splits; ++s) {
-            const float ms = ws_ml[((int64_t)s * rows + row) * 2];
-            if (ms == -INFINITY) continue;
-            const float w = expf(ms - mx);
-            L += ws_ml[((int64_t)s * rows + row) * 2 + 1] * w;
-            acc += ws_o[(int64_t)s * rows * D + i] * w;
+            const float ws = __shfl_sync(0xffffffffu, w, s);
+            if (ws != 0.f && c < D) acc = fmaf(ws_o[((int64_t)s * rows + row) * D + c], ws, acc);
         }
-        st(out, i, acc * (1.0f / L));
+        if (c < D) st(out, row * D + c, acc * inv);
     }
 }
 
@@ -191,9 +201,7 @@ void launch_t(int d, const void* q, const void* k, const void* v, int kv_stride,
 
 void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, void* out, int* err, DT dt,
                               cudaStream_t s) {
-    const int64_t n = (int64_t)rows * d;
-    int grid = (int)((n + 255) / 256);
-    if (grid > 148 * 16) grid = 148 * 16;
+    const int grid = (int)(((int64_t)rows * 32 + 255) / 256);
     if (dt == DT::F32)
         attn_combine_kernel<float><<<grid, 256, 0, s>>>(ws.o, ws.ml, rows, d, splits, (float*)out, err);
     else

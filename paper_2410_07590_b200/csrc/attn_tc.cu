@@ -257,19 +257,27 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t sa = tmem + lane_base + (uint32_t)((j & 1) * 128);
             mbar_wait(&s_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
+            // tiles entirely inside [lo, hi] skip the per-element predicate
+            const bool full = key0 >= my_lo && key0 + BK - 1 <= my_hi;
+            const int clo = my_lo - key0, chi = my_hi - key0;  // visible tile columns [clo, chi]
             float mx = -INFINITY;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t v[32];
                 tmem_ld32(sa + c * 32, v);
                 tmem_wait_ld();
+                if (full) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int key = key0 + c * 32 + i;
-                    const bool vis = key >= my_lo && key <= my_hi;
-                    mx = fmaxf(mx, vis ? __uint_as_float(v[i]) * sl2 : -INFINITY);
+                    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int col = c * 32 + i;
+                        mx = fmaxf(mx, (col >= clo && col <= chi) ? __uint_as_float(v[i]) : -INFINITY);
+                    }
                 }
             }
+            mx = mx == -INFINITY ? -INFINITY : mx * sl2;
             const float m_new = fmaxf(m, mx);
             const float alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
             if (j > 0) {  // fold in O tile j-1 (P smem becomes free once it has landed)
@@ -291,15 +299,25 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tmem_ld32(sa + c * 32, v);
                 tmem_wait_ld();
                 uint32_t pk[16];
+                if (full) {
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const int key = key0 + c * 32 + i;
-                    const bool v0 = key >= my_lo && key <= my_hi && m_new != -INFINITY;
-                    const bool v1 = key + 1 >= my_lo && key + 1 <= my_hi && m_new != -INFINITY;
-                    const float p0 = v0 ? ex2(__uint_as_float(v[i]) * sl2 - m_new) : 0.f;
-                    const float p1 = v1 ? ex2(__uint_as_float(v[i + 1]) * sl2 - m_new) : 0.f;
-                    rs += p0 + p1;
-                    pk[i / 2] = pack_bf16(p0, p1);
+                    for (int i = 0; i < 32; i += 2) {
+                        const float p0 = ex2(fmaf(__uint_as_float(v[i]), sl2, -m_new));
+                        const float p1 = ex2(fmaf(__uint_as_float(v[i + 1]), sl2, -m_new));
+                        rs += p0 + p1;
+                        pk[i / 2] = pack_bf16(p0, p1);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const int col = c * 32 + i;
+                        const bool v0 = col >= clo && col <= chi && m_new != -INFINITY;
+                        const bool v1 = col + 1 >= clo && col + 1 <= chi && m_new != -INFINITY;
+                        const float p0 = v0 ? ex2(fmaf(__uint_as_float(v[i]), sl2, -m_new)) : 0.f;
+                        const float p1 = v1 ? ex2(fmaf(__uint_as_float(v[i + 1]), sl2, -m_new)) : 0.f;
+                        rs += p0 + p1;
+                        pk[i / 2] = pack_bf16(p0, p1);
+                    }
                 }
                 uint8_t* pb = smem + OFF_P + (c >> 1) * SUB;
 #pragma unroll
@@ -397,7 +415,7 @@ bool attention_tc_supported(int d, DT dt) { return d == 128 && dt == DT::BF16; }
 int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms) {
     const int group = H / Hkv;
     const int ctas = ((Tq * group + BR - 1) / BR) * Hkv;
-    int s = (num_sms + ctas - 1) / ctas;
+    int s = num_sms / ctas;  // 1 CTA per SM (192 KB smem): stay within one wave
     const int max_by_keys = (Tk + 4 * BK - 1) / (4 * BK);  // >= 4 key tiles per split
     if (s > max_by_keys) s = max_by_keys;
     if (s > 32) s = 32;

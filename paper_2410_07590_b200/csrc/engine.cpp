@@ -249,6 +249,7 @@ struct tkv_engine {
     uint64_t fingerprint = 0;
     bool exact_fp = false;
     int64_t L, H, Hkv, d, hid, I, V, qd, kvd, nqkv;
+    bool gu_interleaved = false;
 
     // weights
     DevMem wmem;
@@ -397,8 +398,8 @@ struct tkv_engine {
     }
 
     int pick_splits(int M, int N, int K, bool tc) const {
-        const int bm = tc ? 128 : 64, bn = tc ? 128 : 64, bk = tc ? 64 : 16;
-        const int tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+        const int bk = tc ? 64 : 16;
+        const int tiles = tc ? gemm_tc_tiles(M, N) : ((M + 63) / 64) * ((N + 63) / 64);
         const int kb = (K + bk - 1) / bk;
         int s = (num_sms + tiles - 1) / tiles;
         s = std::min(s, std::max(1, kb / 4));
@@ -410,14 +411,19 @@ struct tkv_engine {
 
     bool use_tc() const { return dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_GEMM); }
 
-    // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits
-    int gemm(const void* A, int lda, const void* W, int M, int N, int K) {
+    // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits. With swiglu_act, a tcgen05 GEMM whose
+    // K range fits one CTA writes silu(gate)*up straight to swiglu_act and returns 0.
+    int gemm(const void* A, int lda, const void* W, int M, int N, int K, void* swiglu_act = nullptr) {
         const bool tc = use_tc();
         if (tc && !gemm_tc_supported(M, N, K, lda))
             fail(TKV_ERR_CONFIG, "shape not supported by the tcgen05 GEMM (rows must be 16-byte aligned)");
         const int s = pick_splits(M, N, K, tc);
-        partial.ensure((size_t)s * M * N * sizeof(float));
         Scope sc(this, PC_GEMM, 1);
+        if (tc && swiglu_act && s == 1 && gu_interleaved) {
+            launch_gemm_tc(A, lda, W, M, N, K, nullptr, 1, stream, swiglu_act);
+            return 0;
+        }
+        partial.ensure((size_t)s * M * N * sizeof(float));
         if (tc)
             launch_gemm_tc(A, lda, W, M, N, K, partial.as<float>(), s, stream);
         else
@@ -559,10 +565,10 @@ void tkv_engine::forward(const Fwd& f) {
                                  stream);
         }
         // --- MLP block: gate|up fused into one GEMM, SwiGLU epilogue ---
-        s = gemm(h.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid);
-        {
+        s = gemm(h.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
+        if (s > 0) {
             Scope sc(this, PC_EPI, 1);
-            launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, dt, stream);
+            launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, dt, stream, gu_interleaved);
         }
         s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
         {
@@ -970,6 +976,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         e->L = c.layer_num, e->H = c.head_num, e->Hkv = c.kv_head_num, e->d = c.head_size, e->hid = c.hidden_size;
         e->I = c.intermediate_size, e->V = c.vocab_size, e->qd = e->H * e->d, e->kvd = e->Hkv * e->d;
         e->nqkv = e->qd + 2 * e->kvd;
+        e->gu_interleaved = e->I % 64 == 0;
         if (e->d != 8 && e->d != 16 && e->d != 32 && e->d != 64 && e->d != 128)
             fail(TKV_ERR_CONFIG, "head_size must be one of 8/16/32/64/128 for the device kernels");
 
@@ -1021,9 +1028,12 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
             cur += (uint64_t)(H_ * kvd);
             launch_init_transposed(o, e->dt, seed, cur, qd, H_, scale, e->stream);
             cur += (uint64_t)(qd * H_);
-            launch_init_transposed(gu, e->dt, seed, cur, H_, I, scale, e->stream);
+            // gate | up rows: interleaved in 64-row blocks when I % 64 == 0 (fused SwiGLU epilogue)
+            const int rb = e->gu_interleaved ? 64 : 0;
+            launch_init_transposed(gu, e->dt, seed, cur, H_, I, scale, e->stream, rb, 0);
             cur += (uint64_t)(H_ * I);
-            launch_init_transposed(gu + (size_t)I * H_ * es, e->dt, seed, cur, H_, I, scale, e->stream);
+            launch_init_transposed(rb ? gu : gu + (size_t)I * H_ * es, e->dt, seed, cur, H_, I, scale, e->stream, rb,
+                                   rb ? 64 : 0);
             cur += (uint64_t)(H_ * I);
             launch_init_transposed(dn, e->dt, seed, cur, I, H_, scale, e->stream);
             cur += (uint64_t)(I * H_);

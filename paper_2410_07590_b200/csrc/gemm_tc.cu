@@ -1,20 +1,28 @@
-// tcgen05 + TMA bf16 GEMM for sm_100a with split-K fp32 partial output:
-//   partial[z][m][n] = sum_{k in split z} A[m][k] * W[n][k]
-// A = activations [M][lda] (K-major), W = weights [N][K] (K-major, the engine stores every projection
-// transposed so both operands are K-major). Replaces the reference's f64 matmul (src/numerics.cpp:8-29)
-// for the QKV / O / gate-up / down projections of forward_tokens (src/model.cpp:240-264).
+// tcgen05 + TMA bf16 GEMM for sm_100a:  C[m][n] = sum_k A[m][k] * W[n][k]
+// A = activations [M][lda] (K-major), W = weights [N][K] (K-major: the engine stores every projection
+// transposed). Replaces the reference's f64 matmul (src/numerics.cpp:8-29) for the QKV / O / gate-up /
+// down projections of forward_tokens (src/model.cpp:240-264).
 //
-// Structure (one 128x128 output tile per CTA, 4 warps):
-//   warp 0 / lane 0 : TMA producer — STAGES-deep ring of {A 128x64, W 128x64} bf16 tiles, SWIZZLE_128B,
-//                     mbarrier full/empty handshake
-//   warp 1 / lane 0 : MMA issuer — tcgen05.mma.cta_group::1.kind::f16 (M=128, N=128, K=16) x 4 per
-//                     stage, accumulator in TMEM (128 lanes x 128 fp32 columns); tcgen05.commit frees
-//                     the smem slot and finally signals the epilogue
-//   warps 0-3       : epilogue — tcgen05.ld 32x32b (each warp owns 32 TMEM lanes = 32 rows), fp32 store
+// Two tilings, one kernel template:
+//   normal  (M > 128 tokens: full-concat prefill, chunk ingest): UMMA M=128 over tokens, N=128 over
+//           weight rows; TMEM lane = token row.
+//   swapped (M <= 128 tokens: query prefill, decode): UMMA M=128 over WEIGHT rows, N = M rounded up to 16
+//           over tokens — no half-empty tile at batch-1 query sizes, and the epilogue (TMEM lane = weight
+//           row) stores consecutive n per warp, i.e. coalesced.
+// Epilogues: fp32 split-K partials partial[z][m][n] (reduced by the consumer kernel), or — when the
+// whole K range is in one CTA — SwiGLU fused: W_gu rows are stored in blocks of 64 gate rows followed by
+// the 64 matching up rows, so a 128-row tile holds complete (gate, up) pairs and the epilogue writes
+// act = silu(g) * u (numerics.cpp:103-124) in bf16 directly.
+//
+// Warp roles (128 threads): warp 0 lane 0 = TMA producer (STAGES-deep ring, SWIZZLE_128B, mbarrier
+// full/empty), warp 1 lane 0 = MMA issuer (tcgen05.mma.cta_group::1.kind::f16, fp32 accumulator in TMEM,
+// tcgen05.commit frees smem slots), all 4 warps = epilogue (tcgen05.ld 32x32b, warp w owns lanes 32w..).
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "tkv_internal.h"
@@ -22,22 +30,18 @@
 namespace tkv {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 6, THREADS = 128;
-constexpr uint32_t TILE_A = BM * BK * 2, TILE_B = BN * BK * 2, STAGE_BYTES = TILE_A + TILE_B;
-constexpr uint32_t TMEM_COLS = BN;  // fp32 accumulator columns
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256;
+constexpr int BK = 64, THREADS = 128;
+constexpr uint32_t TILE_W = 128 * BK * 2;  // 16 KB: 128 rows x 64 k, bf16
+constexpr int SMEM_BUDGET = 200 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-
 // Bounded spin: a protocol bug traps (launch error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
@@ -54,7 +58,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         if (spin > (1u << 26)) __trap();
     }
 }
-
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -62,63 +65,69 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
-
-// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: rows of 128 B, 8-row swizzle atoms 1024 B apart.
-//   [0,14) start>>4, [16,30) LBO>>4 (unused for swizzled K-major; 1), [32,46) SBO>>4 = 1024>>4,
-//   [46,48) version = 1 (sm_100), [61,64) layout = 2 (SWIZZLE_128B).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(1024 >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
-    return d;
+// UMMA smem descriptor, K-major SWIZZLE_128B: 128 B rows, 8-row atoms 1024 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t desc_k(uint32_t saddr) {
+    return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-
-// Instruction descriptor kind::f16: D=f32 (bit 4), A=B=bf16 (bits 7,10), K-major A/B, N>>3 at 17, M>>4 at 24.
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+// kind::f16 instruction descriptor: D=f32, A=B=bf16, both K-major, N>>3 at bit 17, M>>4 at bit 24.
+__device__ __forceinline__ uint32_t idesc(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+        "l"(a), "l"(b), "r"(id), "r"(acc));
 }
-
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
-
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ float silu(float z) { return z / (1.0f + __expf(-z)); }
 
+struct GemmArgs {
+    int M, N, K;
+    int kb_per_split;
+    int ntok;         // swapped: tokens per tile (N of the MMA, multiple of 16); normal: 128
+    uint32_t a_bytes; // bytes of the activation tile per stage
+    int stages;
+    uint32_t tmem_cols;
+    float* partial;   // EPI_PARTIAL
+    __nv_bfloat16* act;  // EPI_SWIGLU: [M][N/2]
+};
+
+enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
+
+template <bool SWAP, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, int M, int N,
-                   int K, float* __restrict__ partial, int kb_per_split) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, GemmArgs g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* tiles = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* done = empty + STAGES;
+    const uint32_t stage_bytes = TILE_W + g.a_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.stages * stage_bytes);
+    uint64_t* empty = full + g.stages;
+    uint64_t* done = empty + g.stages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, z = blockIdx.z;
-    const int kb_total = (K + BK - 1) / BK;
-    const int kb0 = z * kb_per_split;
-    const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+    // weight rows (n) tile along x, token rows (m) tile along y
+    const int n0 = blockIdx.x * 128, m0 = blockIdx.y * (SWAP ? g.ntok : 128), z = blockIdx.z;
+    const int kb_total = (g.K + BK - 1) / BK;
+    const int kb0 = z * g.kb_per_split;
+    const int nkb = min(kb_total, kb0 + g.kb_per_split) - kb0;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < g.stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -129,7 +138,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
+                     "r"(g.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -138,32 +147,31 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (nkb > 0) {
-        if (warp == 0 && lane == 0) {
-            // TMA producer
+        if (warp == 0 && lane == 0) {  // TMA producer
             for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                uint8_t* a = tiles + s * STAGE_BYTES;
-                uint8_t* b = a + TILE_A;
-                mbar_expect_tx(&full[s], STAGE_BYTES);
+                const int s = i % g.stages;
+                mbar_wait(&empty[s], ((uint32_t)(i / g.stages) & 1u) ^ 1u);
+                uint8_t* w = smem + s * stage_bytes;
+                uint8_t* a = w + TILE_W;
+                mbar_expect_tx(&full[s], stage_bytes);
                 const int kc = (kb0 + i) * BK;
+                tma_load_2d(w, &tmW, &full[s], kc, n0);
                 tma_load_2d(a, &tmA, &full[s], kc, m0);
-                tma_load_2d(b, &tmW, &full[s], kc, n0);
             }
-        } else if (warp == 1 && lane == 0) {
-            // MMA issuer
+        } else if (warp == 1 && lane == 0) {  // MMA issuer
+            const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128);
             for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-                mbar_wait(&full[s], ph);
+                const int s = i % g.stages;
+                mbar_wait(&full[s], (uint32_t)(i / g.stages) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a = smem_u32(tiles + s * STAGE_BYTES);
-                const uint32_t b = a + TILE_A;
+                const uint32_t w = smem_u32(smem + s * stage_bytes);
+                const uint32_t a = w + TILE_W;
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    // advance 16 bf16 = 32 B along K inside the 128 B swizzle row
-                    umma_f16(tmem, umma_desc_sw128(a + k * 32), umma_desc_sw128(b + k * 32), (i | k) != 0);
+                for (int k = 0; k < BK / 16; ++k) {  // 16 bf16 = 32 B along K inside the 128 B swizzle row
+                    if (SWAP)
+                        umma_f16(tmem, desc_k(w + k * 32), desc_k(a + k * 32), id, (i | k) != 0);
+                    else
+                        umma_f16(tmem, desc_k(a + k * 32), desc_k(w + k * 32), id, (i | k) != 0);
                 }
                 umma_commit(&empty[s]);
             }
@@ -174,31 +182,111 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
 
-    // Epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows.
-    const int row = m0 + warp * 32 + lane;
-    float* out = partial + (int64_t)z * M * N + (int64_t)row * N;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    if (SWAP) {
+        // TMEM lane = weight row n, column = token
+        const int n = n0 + warp * 32 + lane;
+        if (EPI == EPI_PARTIAL) {
+            float* out = g.partial + (int64_t)z * g.M * g.N;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        if (nkb > 0) {
-            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, r);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int c = 0; c < g.ntok; c += 16) {
+                uint32_t r[16];
+                if (nkb > 0) {
+                    tmem_ld16(tmem + lane_base + (uint32_t)c, r);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) r[j] = 0u;
+                }
+                if (n < g.N) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int m = m0 + c + j;
+                        if (m < g.M) out[(int64_t)m * g.N + n] = __uint_as_float(r[j]);
+                    }
+                }
+            }
         } else {
+            // rows 0-63 of the tile are gate, 64-127 the matching up rows (interleaved W_gu layout)
+            float* up = reinterpret_cast<float*>(smem);  // pipeline smem is idle now: [64][ntok+1]
+            const int ld = g.ntok + 1;
+            if (warp >= 2) {
+#pragma unroll 1
+                for (int c = 0; c < g.ntok; c += 16) {
+                    uint32_t r[16];
+                    tmem_ld16(tmem + lane_base + (uint32_t)c, r);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = 0u;
+                    for (int j = 0; j < 16; ++j) up[((warp - 2) * 32 + lane) * ld + c + j] = __uint_as_float(r[j]);
+                }
+            }
+            __syncthreads();
+            if (warp < 2) {
+                const int inter = g.N / 2;
+                const int i = blockIdx.x * 64 + warp * 32 + lane;
+#pragma unroll 1
+                for (int c = 0; c < g.ntok; c += 16) {
+                    uint32_t r[16];
+                    tmem_ld16(tmem + lane_base + (uint32_t)c, r);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int m = m0 + c + j;
+                        if (m < g.M && i < inter)
+                            g.act[(int64_t)m * inter + i] =
+                                __float2bfloat16_rn(silu(__uint_as_float(r[j])) * up[(warp * 32 + lane) * ld + c + j]);
+                    }
+                }
+            }
         }
-        if (row < M) {
-            const int n = n0 + c;
-            if (n + 16 <= N && (N % 4) == 0) {
-                float4* o4 = reinterpret_cast<float4*>(out + n);
+    } else {
+        // TMEM lane = token row m, column = weight row
+        const int m = m0 + warp * 32 + lane;
+        if (EPI == EPI_PARTIAL) {
+            float* out = g.partial + (int64_t)z * g.M * g.N + (int64_t)m * g.N;
+#pragma unroll 1
+            for (int c = 0; c < 128; c += 16) {
+                uint32_t r[16];
+                if (nkb > 0) {
+                    tmem_ld16(tmem + lane_base + (uint32_t)c, r);
+                } else {
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            } else {
+                    for (int j = 0; j < 16; ++j) r[j] = 0u;
+                }
+                if (m < g.M) {
+                    const int n = n0 + c;
+                    if (n + 16 <= g.N && (g.N % 4) == 0) {
+                        float4* o4 = reinterpret_cast<float4*>(out + n);
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (n + j < N) out[n + j] = __uint_as_float(r[j]);
+                        for (int j = 0; j < 4; ++j)
+                            o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (n + j < g.N) out[n + j] = __uint_as_float(r[j]);
+                    }
+                }
+            }
+        } else {
+            const int inter = g.N / 2;
+            const int i0 = blockIdx.x * 64;
+#pragma unroll 1
+            for (int c = 0; c < 64; c += 16) {
+                uint32_t gr[16], ur[16];
+                tmem_ld16(tmem + lane_base + (uint32_t)c, gr);
+                tmem_ld16(tmem + lane_base + (uint32_t)(64 + c), ur);
+                if (m < g.M) {
+                    __align__(16) __nv_bfloat16 o[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        o[j] = __float2bfloat16_rn(silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]));
+                    __nv_bfloat16* dst = g.act + (int64_t)m * inter + i0 + c;
+                    if (i0 + c + 16 <= inter && (inter % 8) == 0) {
+                        reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<uint4*>(o)[0];
+                        reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<uint4*>(o)[1];
+                    } else {
+                        for (int j = 0; j < 16; ++j)
+                            if (i0 + c + j < inter) dst[j] = o[j];
+                    }
+                }
             }
         }
     }
@@ -206,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
     }
 }
 
@@ -228,17 +316,25 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-CUtensorMap make_map(const void* base, int rows, int cols_k, int ld_elems) {
+CUtensorMap make_map(const void* base, int rows, int cols_k, int ld_elems, int box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {(cuuint64_t)cols_k, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)ld_elems * 2};
-    const cuuint32_t box[2] = {BK, 128};
+    const cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(TKV_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     return m;
+}
+
+template <bool SWAP, int EPI>
+void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g, dim3 grid, cudaStream_t s) {
+    const size_t smem = 1024 + (size_t)g.stages * (TILE_W + g.a_bytes) + 256;
+    TKV_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<SWAP, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gemm_tc_kernel<SWAP, EPI><<<grid, THREADS, smem, s>>>(ta, tw, g);
+    TKV_CUDA(cudaGetLastError());
 }
 
 }  // namespace
@@ -248,20 +344,36 @@ bool gemm_tc_supported(int M, int N, int K, int lda) {
     return M >= 1 && N >= 1 && K >= 8 && (lda * 2) % 16 == 0 && (K * 2) % 16 == 0;
 }
 
+int gemm_tc_tiles(int M, int N) {
+    const bool swap = M <= 128;
+    return ((N + 127) / 128) * (swap ? 1 : (M + 127) / 128);
+}
+
 void launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
-                    cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        TKV_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-        attr_set = true;
-    }
-    const CUtensorMap ta = make_map(A, M, K, lda);
-    const CUtensorMap tw = make_map(W, N, K, K);
+                    cudaStream_t s, void* swiglu_act) {
+    const bool swap = M <= 128;
+    GemmArgs g{};
+    g.M = M;
+    g.N = N;
+    g.K = K;
     const int kb_total = (K + BK - 1) / BK;
-    const int kbs = (kb_total + splits - 1) / splits;
-    dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, splits);
-    gemm_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tw, M, N, K, partial, kbs);
-    TKV_CUDA(cudaGetLastError());
+    g.kb_per_split = (kb_total + splits - 1) / splits;
+    g.ntok = swap ? ((M + 15) / 16) * 16 : 128;
+    g.a_bytes = (uint32_t)g.ntok * BK * 2;
+    g.stages = (int)std::min<uint32_t>(8, SMEM_BUDGET / (TILE_W + g.a_bytes));
+    g.tmem_cols = 32;
+    while (g.tmem_cols < (uint32_t)g.ntok) g.tmem_cols <<= 1;
+    g.partial = partial;
+    g.act = (__nv_bfloat16*)swiglu_act;
+    const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
+    const CUtensorMap tw = make_map(W, N, K, K, 128);
+    dim3 grid((N + 127) / 128, swap ? 1 : (M + 127) / 128, splits);
+    if (swiglu_act) {
+        if (splits != 1) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the whole K range in one CTA");
+        swap ? launch_t<true, EPI_SWIGLU>(ta, tw, g, grid, s) : launch_t<false, EPI_SWIGLU>(ta, tw, g, grid, s);
+    } else {
+        swap ? launch_t<true, EPI_PARTIAL>(ta, tw, g, grid, s) : launch_t<false, EPI_PARTIAL>(ta, tw, g, grid, s);
+    }
 }
 
 }  // namespace tkv

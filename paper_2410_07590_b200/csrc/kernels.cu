@@ -33,12 +33,13 @@ __device__ __forceinline__ double draw(uint64_t seed, uint64_t i, double scale) 
 
 template <typename T>
 __global__ void init_transposed_kernel(T* dst, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
-                                       double scale) {
+                                       double scale, int row_block, int row_off) {
     const int64_t n = rows * cols;
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = o / rows, i = o - j * rows;
+        const int64_t pj = row_block ? (j / row_block) * 2 * row_block + row_off + j % row_block : j;
         const float f = __double2float_rn(draw(seed, base + (uint64_t)(i * cols + j), scale));
-        stf(dst, o, f);  // f64 -> f32 (RN) -> bf16 (RNE): the canonical cast, see DESIGN.md
+        stf(dst, pj * rows + i, f);  // f64 -> f32 (RN) -> bf16 (RNE): the canonical cast, see DESIGN.md
     }
 }
 
@@ -86,9 +87,60 @@ __global__ void embed_norm_kernel(const int32_t* tok, const float* emb, int hidd
         stf(h, (int64_t)t * hidden + j, x[(int64_t)t * hidden + j] * scale * w[j]);
 }
 
+// One CTA per row: x += sum of split-K partials, then h = rmsnorm(x) * w. float4 vectorised; the row
+// (hidden <= 8192) stays in registers between the two passes.
 template <typename T>
-__global__ void residual_norm_kernel(float* x, const float* partial, int splits, int64_t plane, int hidden,
-                                     const float* w, float eps, T* h, int* err) {
+__global__ void __launch_bounds__(256) residual_norm_kernel(float* x, const float* partial, int splits,
+                                                            int64_t plane, int hidden, const float* w, float eps,
+                                                            T* h, int* err) {
+    __shared__ float red[32];
+    constexpr int MAXV = 8;
+    const int64_t t = blockIdx.x;
+    const int n4 = hidden >> 2;
+    float4* x4 = reinterpret_cast<float4*>(x + t * hidden);
+    float4 v[MAXV];
+    float ss = 0.f;
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < MAXV; ++u) {
+        const int idx = threadIdx.x + u * blockDim.x;
+        if (idx < n4) {
+            float4 a = x4[idx];
+            for (int s = 0; s < splits; ++s) {
+                const float4 p = reinterpret_cast<const float4*>(partial + s * plane + t * hidden)[idx];
+                a.x += p.x;
+                a.y += p.y;
+                a.z += p.z;
+                a.w += p.w;
+            }
+            x4[idx] = a;
+            v[u] = a;
+            ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+            bad |= !(isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w));
+        }
+    }
+    if (bad) atomicOr(err, 2);
+    if (w == nullptr) return;
+    ss = block_sum(ss, red);
+    const float scale = 1.0f / sqrtf(ss / (float)hidden + eps);
+#pragma unroll
+    for (int u = 0; u < MAXV; ++u) {
+        const int idx = threadIdx.x + u * blockDim.x;
+        if (idx < n4) {
+            const float4 ww = reinterpret_cast<const float4*>(w)[idx];
+            const int64_t b = t * hidden + 4 * idx;
+            stf(h, b + 0, v[u].x * scale * ww.x);
+            stf(h, b + 1, v[u].y * scale * ww.y);
+            stf(h, b + 2, v[u].z * scale * ww.z);
+            stf(h, b + 3, v[u].w * scale * ww.w);
+        }
+    }
+}
+
+// generic fallback (hidden % 4 != 0 or hidden > 8192)
+template <typename T>
+__global__ void residual_norm_scalar_kernel(float* x, const float* partial, int splits, int64_t plane, int hidden,
+                                            const float* w, float eps, T* h, int* err) {
     __shared__ float red[32];
     const int64_t t = blockIdx.x;
     float ss = 0.f;
@@ -109,14 +161,16 @@ __global__ void residual_norm_kernel(float* x, const float* partial, int splits,
 }
 
 template <typename T>
-__global__ void swiglu_kernel(const float* partial, int splits, int T_, int inter, T* act) {
+__global__ void swiglu_kernel(const float* partial, int splits, int T_, int inter, T* act, int interleave64) {
     const int64_t n = (int64_t)T_ * inter, plane = (int64_t)T_ * 2 * inter;
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = o / inter, i = o - t * inter;
+        const int64_t gc = interleave64 ? (i >> 6) * 128 + (i & 63) : i;
+        const int64_t uc = interleave64 ? gc + 64 : inter + i;
         float g = 0.f, u = 0.f;
         for (int s = 0; s < splits; ++s) {
-            g += partial[s * plane + t * 2 * inter + i];
-            u += partial[s * plane + t * 2 * inter + inter + i];
+            g += partial[s * plane + t * 2 * inter + gc];
+            u += partial[s * plane + t * 2 * inter + uc];
         }
         stf(act, o, (g / (1.0f + expf(-g))) * u);  // silu(z) = z / (1 + e^-z), numerics.cpp:103-105
     }
@@ -333,9 +387,9 @@ inline int grid_for(int64_t n, int block, int cap = 148 * 16) {
     } while (0)
 
 void launch_init_transposed(void* dst, DT dt, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
-                            double scale, cudaStream_t s) {
+                            double scale, cudaStream_t s, int row_block, int row_off) {
     DISPATCH_DT(dt, init_transposed_kernel<T><<<grid_for(rows * cols, 256, 148 * 64), 256, 0, s>>>(
-                        (T*)dst, seed, base, rows, cols, scale));
+                        (T*)dst, seed, base, rows, cols, scale, row_block, row_off));
     TKV_CUDA(cudaGetLastError());
 }
 
@@ -359,13 +413,20 @@ void launch_embed_norm(const int32_t* tok, int T_, const float* emb, int hidden,
 void launch_residual_norm(float* x, const float* partial, int splits, int T_, int hidden, const float* w, float eps,
                           void* h, DT dt, int* err, cudaStream_t s) {
     const int64_t plane = (int64_t)T_ * hidden;
-    DISPATCH_DT(dt, residual_norm_kernel<T><<<T_, 512, 0, s>>>(x, partial, splits, plane, hidden, w, eps, (T*)h, err));
+    if (hidden % 4 == 0 && hidden <= 8 * 4 * 256) {
+        DISPATCH_DT(dt, residual_norm_kernel<T><<<T_, 256, 0, s>>>(x, partial, splits, plane, hidden, w, eps, (T*)h,
+                                                                   err));
+    } else {
+        DISPATCH_DT(dt, residual_norm_scalar_kernel<T><<<T_, 512, 0, s>>>(x, partial, splits, plane, hidden, w, eps,
+                                                                          (T*)h, err));
+    }
     TKV_CUDA(cudaGetLastError());
 }
 
-void launch_swiglu(const float* partial, int splits, int T_, int inter, void* act, DT dt, cudaStream_t s) {
+void launch_swiglu(const float* partial, int splits, int T_, int inter, void* act, DT dt, cudaStream_t s,
+                   bool interleave64) {
     DISPATCH_DT(dt, swiglu_kernel<T><<<grid_for((int64_t)T_ * inter, 256), 256, 0, s>>>(partial, splits, T_, inter,
-                                                                                         (T*)act));
+                                                                                         (T*)act, (int)interleave64));
     TKV_CUDA(cudaGetLastError());
 }
 

@@ -30,8 +30,10 @@ inline size_t dt_size(DT t) { return t == DT::F32 ? 4 : 2; }
 
 // Weight init: dst[j*rows + i] = cast(next_signed(seed, base + i*cols + j) * scale) — the reference's
 // [rows=in, cols=out] draw order (src/model.cpp:15-21,68-92) written transposed (K-major [out][in]).
+// row_block > 0 places output row j at (j / row_block) * 2 * row_block + row_off + j % row_block (the
+// interleaved gate/up layout of the fused SwiGLU epilogue).
 void launch_init_transposed(void* dst, DT dt, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
-                            double scale, cudaStream_t s);
+                            double scale, cudaStream_t s, int row_block = 0, int row_off = 0);
 // Same, not transposed (embedding [vocab][hidden], fp32).
 void launch_init_rowmajor_f32(float* dst, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
                               double scale, cudaStream_t s);
@@ -43,8 +45,10 @@ void launch_embed_norm(const int32_t* tok, int T, const float* emb, int hidden, 
 // x[t] += sum_s partial[s][t][:]; h[t] = rmsnorm(x[t]) * w (dtype).  x/h/partial row strides = hidden.
 void launch_residual_norm(float* x, const float* partial, int splits, int T, int hidden, const float* w,
                           float eps, void* h, DT dt, int* err, cudaStream_t s);
-// act[t][i] = silu(sum_s P[s][t][i]) * sum_s P[s][t][I+i]   (dtype)
-void launch_swiglu(const float* partial, int splits, int T, int inter, void* act, DT dt, cudaStream_t s);
+// act[t][i] = silu(sum_s P[s][t][gate(i)]) * sum_s P[s][t][up(i)]   (dtype). interleave64: gate/up columns
+// in 64-wide blocks (gate(i) = (i/64)*128 + i%64, up = gate + 64); else gate(i) = i, up(i) = I + i.
+void launch_swiglu(const float* partial, int splits, int T, int inter, void* act, DT dt, cudaStream_t s,
+                   bool interleave64 = false);
 
 // QKV epilogue: reduce the split-K partials of [T, (H+2Hkv)*d], rotate q and k by pos[t]
 // (interleaved pairs, cos/sin table [max_pos][d/2] of float2), write q (dtype [T, H*d]),
@@ -92,9 +96,12 @@ void launch_reduce_splits(const float* partial, int splits, int64_t n, float* ou
 void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
                       DT dt, cudaStream_t s);
 // tcgen05 + TMA version (bf16 only). Returns false when the shape is not supported (caller errors out).
+// M <= 128 uses the swapped tiling (weights on the UMMA M side). With swiglu_act != nullptr (splits must
+// be 1, W rows interleaved in 64-row gate/up blocks) the epilogue writes act[M][N/2] = silu(g)*u in bf16.
 bool gemm_tc_supported(int M, int N, int K, int lda);
+int gemm_tc_tiles(int M, int N);
 void launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
-                    cudaStream_t s);
+                    cudaStream_t s, void* swiglu_act = nullptr);
 
 // Flash attention, SIMT (fp32 math): q [Tq][H*d], k/v rows [Tk][Hkv*d] (stride kv_stride elements),
 // row t attends keys j with lo[t] <= j <= hi[t]. out [Tq][H*d] (dtype). ws: split-K workspace.
