@@ -161,6 +161,25 @@ __global__ void attn_combine_kernel(const float* __restrict__ ws_o, const float*
     float L = ls * w;
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
     const float inv = 1.0f / L;
+    if (D == 128) {  // lane owns 4 consecutive columns: one float4 per split, loads batched
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4* src = reinterpret_cast<const float4*>(ws_o) + row * 32 + lane;
+#pragma unroll 4
+        for (int s = 0; s < splits; ++s) {
+            const float ws = __shfl_sync(0xffffffffu, w, s);
+            const float4 v = src[(int64_t)s * rows * 32];
+            acc.x = fmaf(v.x, ws, acc.x);
+            acc.y = fmaf(v.y, ws, acc.y);
+            acc.z = fmaf(v.z, ws, acc.z);
+            acc.w = fmaf(v.w, ws, acc.w);
+        }
+        const int64_t b = row * D + lane * 4;
+        st(out, b + 0, acc.x * inv);
+        st(out, b + 1, acc.y * inv);
+        st(out, b + 2, acc.z * inv);
+        st(out, b + 3, acc.w * inv);
+        return;
+    }
     for (int c0 = 0; c0 < D; c0 += 32) {
         const int c = c0 + lane;
         float acc = 0.f;

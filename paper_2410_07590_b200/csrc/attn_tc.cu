@@ -6,13 +6,14 @@
 // GQA packing: a CTA owns 128 rows of ONE kv head g, row r = (token t, head g*group + r%group), so the
 // K/V tiles it streams serve all `group` query heads (C2: 64 tokens x 7 heads = 448 rows = 3.5 tiles).
 //
-// Per CTA (192 threads): warps 0-3 = softmax (one row per thread), warp 4 = TMA producer, warp 5 = MMA
-// issuer. smem: Q [128x128] and P [128x128] (two 64-column SW128 sub-tiles each, 32 KB), two K/V stages
+// Per CTA (320 threads): warps 0-7 = softmax (two threads per row: warps w and w+4 share TMEM lanes
+// 32(w%4).., each owns 64 of the S columns and 64 of the O columns; row maxima are exchanged through
+// shared memory), warp 8 = TMA producer, warp 9 = MMA issuer. smem: Q [128x128] and P [128x128] (two 64-column SW128 sub-tiles each, 32 KB), two K/V stages
 // of 64 KB. TMEM (512 cols): S double buffer at cols 0/128, O tile at 256.
 //   S_j  = Q . K_j^T          tcgen05.mma kind::f16 M128 N128 K16 x8, A,B K-major
 //   P_j  = exp2(S_j*scale*log2e - m_j)  (softmax warps: TMEM -> regs -> bf16 -> swizzled smem)
 //   O_j  = P_j . V_j          tcgen05.mma, A = P (K-major), B = V (MN-major: d contiguous)
-// The running output O lives in registers (128 fp32 per thread), rescaled by exp2(m_{j-1} - m_j) each
+// The running output O lives in registers (64 fp32 per thread), rescaled by exp2(m_{j-1} - m_j) each
 // tile and incremented by the O_j tile read back from TMEM. Split-K over keys writes (O, m, l) partials
 // combined by attn_combine_kernel (attn_simt.cu) — same workspace layout as the SIMT kernel.
 #include <cuda.h>
@@ -27,7 +28,7 @@
 namespace tkv {
 namespace {
 
-constexpr int D = 128, BR = 128, BK = 128, THREADS = 192;
+constexpr int D = 128, BR = 128, BK = 128, SOFTMAX_WARPS = 8, THREADS = SOFTMAX_WARPS * 32 + 64;
 constexpr uint32_t SUB = 128 * 64 * 2;          // one [128 rows][64 cols] bf16 SW128 sub-tile = 16 KB
 constexpr uint32_t OFF_Q = 0, OFF_P = 2 * SUB;  // 32 KB each
 constexpr uint32_t OFF_KV = 4 * SUB;            // stage s: K at OFF_KV + s*4*SUB, V at +2*SUB
@@ -136,12 +137,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* o_full = bars + 7;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
     __shared__ int red_lo[THREADS / 32], red_hi[THREADS / 32];
+    __shared__ float xmax[2][2][BR];  // [tile parity][half][row]: per-half row maxima exchanged each tile
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int group = H / Hkv, g = blockIdx.y, split = blockIdx.z;
     const int rows_total = Tq * group;
-    const int row = blockIdx.x * BR + tid;  // softmax threads only
-    const bool active = tid < BR && row < rows_total;
+    const bool softmax = warp < SOFTMAX_WARPS;
+    const int r = tid & (BR - 1);           // tile row (TMEM lane) of a softmax thread
+    const int half = softmax ? warp >> 2 : 0;  // which 64 S columns / 64 O columns this thread owns
+    const int row = blockIdx.x * BR + r;
+    const bool active = softmax && row < rows_total;
     const int t = active ? row / group : 0;
     const int h = g * group + (active ? row % group : 0);
     const int my_lo = active ? lo[t] : INT32_MAX;
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&kv_empty[s], 1);
             mbar_init(&s_full[s], 1);
         }
-        mbar_init(p_full, BR);
+        mbar_init(p_full, SOFTMAX_WARPS * 32);
         mbar_init(o_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -172,13 +177,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // ---- Q tile: each softmax thread stages its own row into the two swizzled sub-tiles ----
-    if (tid < BR) {
-        const uint4* src = reinterpret_cast<const uint4*>(q + (int64_t)t * H * D + (int64_t)h * D);
+    // ---- Q tile: each softmax thread stages its half of its row (sub-tile `half`) ----
+    if (softmax) {
+        const uint4* src = reinterpret_cast<const uint4*>(q + (int64_t)t * H * D + (int64_t)h * D) + half * 8;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < 8; ++c) {
             const uint4 v = active ? src[c] : make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4*>(smem + OFF_Q + (c >> 3) * SUB + swz(tid, c & 7)) = v;
+            *reinterpret_cast<uint4*>(smem + OFF_Q + half * SUB + swz(r, c)) = v;
         }
         fence_async_smem();
     }
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int ke = min(bhi, ks + chunk - 1);
     const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
 
-    if (warp == 4) {
+    if (warp == SOFTMAX_WARPS) {
         if (lane == 0) {  // ---------------- TMA producer ----------------
             for (int j = 0; j < n; ++j) {
                 const int s = j & 1;
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tma_load_2d(st + 3 * SUB, &tmV, &kv_full[s], g * D + 64, key);
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == SOFTMAX_WARPS + 1) {
         if (lane == 0) {  // ---------------- MMA issuer ----------------
             auto issue_s = [&](int j) {
                 const int s = j & 1;
@@ -245,89 +250,89 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        // ---------------- softmax warps: one row per thread ----------------
+        // ---------------- softmax: two threads per row, 64 S / 64 O columns each ----------------
         const float sl2 = scale * LOG2E;
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-        float o[D];
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t col0 = (uint32_t)(half * 64);
+        float o[64];
 #pragma unroll
-        for (int i = 0; i < D; ++i) o[i] = 0.f;
+        for (int i = 0; i < 64; ++i) o[i] = 0.f;
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < n; ++j) {
-            const int key0 = ks + j * BK;
-            const uint32_t sa = tmem + lane_base + (uint32_t)((j & 1) * 128);
+            const int key0 = ks + j * BK + half * 64;  // first key of this thread's 64 columns
+            const uint32_t sa = tmem + lane_base + (uint32_t)((j & 1) * 128) + col0;
+            const bool full = key0 >= my_lo && key0 + 63 <= my_hi;
+            const int clo = my_lo - key0, chi = my_hi - key0;
             mbar_wait(&s_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
-            // tiles entirely inside [lo, hi] skip the per-element predicate
-            const bool full = key0 >= my_lo && key0 + BK - 1 <= my_hi;
-            const int clo = my_lo - key0, chi = my_hi - key0;  // visible tile columns [clo, chi]
-            float mx = -INFINITY;
+            uint32_t v0[32], v1[32];
+            tmem_ld32(sa, v0);
+            tmem_ld32(sa + 32, v1);
+            tmem_wait_ld();
+            float mx8[8];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t v[32];
-                tmem_ld32(sa + c * 32, v);
-                tmem_wait_ld();
-                if (full) {
+            for (int a = 0; a < 8; ++a) mx8[a] = -INFINITY;
+            if (full) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
-                } else {
+                for (int i = 0; i < 32; ++i) {
+                    mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v0[i]));
+                    mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v1[i]));
+                }
+            } else {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int col = c * 32 + i;
-                        mx = fmaxf(mx, (col >= clo && col <= chi) ? __uint_as_float(v[i]) : -INFINITY);
-                    }
+                for (int i = 0; i < 32; ++i) {
+                    mx8[i & 7] = fmaxf(mx8[i & 7], (i >= clo && i <= chi) ? __uint_as_float(v0[i]) : -INFINITY);
+                    mx8[i & 7] =
+                        fmaxf(mx8[i & 7], (i + 32 >= clo && i + 32 <= chi) ? __uint_as_float(v1[i]) : -INFINITY);
                 }
             }
+            float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+            // exchange with the thread owning the other 64 columns of this row
+            xmax[j & 1][half][r] = mx;
+            asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
+            mx = fmaxf(mx, xmax[j & 1][half ^ 1][r]);
             mx = mx == -INFINITY ? -INFINITY : mx * sl2;
             const float m_new = fmaxf(m, mx);
             const float alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
-            if (j > 0) {  // fold in O tile j-1 (P smem becomes free once it has landed)
+            if (j > 0) {  // fold in O tile j-1 (after it lands, the P buffer is free again)
                 mbar_wait(o_full, (j - 1) & 1);
                 tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t v[32];
-                    tmem_ld32(tmem + lane_base + 256 + c * 32, v);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) o[c * 32 + i] += __uint_as_float(v[i]);
-                }
-            }
-            float rs = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t v[32];
-                tmem_ld32(sa + c * 32, v);
+                uint32_t w0[32], w1[32];
+                tmem_ld32(tmem + lane_base + 256 + col0, w0);
+                tmem_ld32(tmem + lane_base + 256 + col0 + 32, w1);
                 tmem_wait_ld();
-                uint32_t pk[16];
-                if (full) {
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const float p0 = ex2(fmaf(__uint_as_float(v[i]), sl2, -m_new));
-                        const float p1 = ex2(fmaf(__uint_as_float(v[i + 1]), sl2, -m_new));
-                        rs += p0 + p1;
-                        pk[i / 2] = pack_bf16(p0, p1);
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const int col = c * 32 + i;
-                        const bool v0 = col >= clo && col <= chi && m_new != -INFINITY;
-                        const bool v1 = col + 1 >= clo && col + 1 <= chi && m_new != -INFINITY;
-                        const float p0 = v0 ? ex2(fmaf(__uint_as_float(v[i]), sl2, -m_new)) : 0.f;
-                        const float p1 = v1 ? ex2(fmaf(__uint_as_float(v[i + 1]), sl2, -m_new)) : 0.f;
-                        rs += p0 + p1;
-                        pk[i / 2] = pack_bf16(p0, p1);
-                    }
+                for (int i = 0; i < 32; ++i) {
+                    o[i] += __uint_as_float(w0[i]);
+                    o[32 + i] += __uint_as_float(w1[i]);
                 }
-                uint8_t* pb = smem + OFF_P + (c >> 1) * SUB;
-#pragma unroll
-                for (int qd = 0; qd < 4; ++qd)
-                    *reinterpret_cast<uint4*>(pb + swz(tid, (c & 1) * 4 + qd)) =
-                        make_uint4(pk[4 * qd], pk[4 * qd + 1], pk[4 * qd + 2], pk[4 * qd + 3]);
             }
+            float rs8[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) rs8[a] = 0.f;
+            uint32_t pk[32];
+            const bool live = m_new != -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) {
+                const float s0 = __uint_as_float(i < 32 ? v0[i] : v1[i - 32]);
+                const float s1 = __uint_as_float(i + 1 < 32 ? v0[i + 1] : v1[i - 31]);
+                const bool ok0 = live && (full || (i >= clo && i <= chi));
+                const bool ok1 = live && (full || (i + 1 >= clo && i + 1 <= chi));
+                const float p0 = ok0 ? ex2(fmaf(s0, sl2, -m_new)) : 0.f;
+                const float p1 = ok1 ? ex2(fmaf(s1, sl2, -m_new)) : 0.f;
+                rs8[(i >> 1) & 7] += p0 + p1;
+                pk[i >> 1] = pack_bf16(p0, p1);
+            }
+            uint8_t* pb = smem + OFF_P + half * SUB;  // keys [half*64, half*64+64) = P sub-tile `half`
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4*>(pb + swz(r, c)) =
+                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
             l = l * alpha + rs;
 #pragma unroll
-            for (int i = 0; i < D; ++i) o[i] *= alpha;
+            for (int i = 0; i < 64; ++i) o[i] *= alpha;
             m = m_new;
             fence_async_smem();
             tc_fence_before();
@@ -336,36 +341,43 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (n > 0) {
             mbar_wait(o_full, (n - 1) & 1);
             tc_fence_after();
+            uint32_t w0[32], w1[32];
+            tmem_ld32(tmem + lane_base + 256 + col0, w0);
+            tmem_ld32(tmem + lane_base + 256 + col0 + 32, w1);
+            tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t v[32];
-                tmem_ld32(tmem + lane_base + 256 + c * 32, v);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) o[c * 32 + i] += __uint_as_float(v[i]);
+            for (int i = 0; i < 32; ++i) {
+                o[i] += __uint_as_float(w0[i]);
+                o[32 + i] += __uint_as_float(w1[i]);
             }
         }
+        // the two halves of a row hold partial sums l over disjoint key columns (same running max)
+        xmax[0][half][r] = l;
+        asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
+        l += xmax[0][half ^ 1][r];
         if (active) {
             const int64_t orow = (int64_t)t * H + h;
             if (splits == 1) {
                 if (l == 0.f) {
-                    atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
+                    if (half == 0) atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
                 } else {
                     const float inv = 1.0f / l;
-                    uint4* dst = reinterpret_cast<uint4*>(out + orow * D);
+                    uint4* dst = reinterpret_cast<uint4*>(out + orow * D + half * 64);
 #pragma unroll
-                    for (int c = 0; c < 16; ++c)
+                    for (int c = 0; c < 8; ++c)
                         dst[c] = make_uint4(pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv),
                                             pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
                                             pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv),
                                             pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
                 }
             } else {
-                float4* wo = reinterpret_cast<float4*>(ws_o + ((int64_t)split * Tq * H + orow) * D);
+                float4* wo = reinterpret_cast<float4*>(ws_o + ((int64_t)split * Tq * H + orow) * D + half * 64);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) wo[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-                ws_ml[((int64_t)split * Tq * H + orow) * 2 + 0] = m == -INFINITY ? -INFINITY : m / LOG2E;
-                ws_ml[((int64_t)split * Tq * H + orow) * 2 + 1] = l;
+                for (int c = 0; c < 16; ++c) wo[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                if (half == 0) {
+                    ws_ml[((int64_t)split * Tq * H + orow) * 2 + 0] = m == -INFINITY ? -INFINITY : m / LOG2E;
+                    ws_ml[((int64_t)split * Tq * H + orow) * 2 + 1] = l;
+                }
             }
         }
     }

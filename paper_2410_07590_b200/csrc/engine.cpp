@@ -401,7 +401,8 @@ struct tkv_engine {
         const int bk = tc ? 64 : 16;
         const int tiles = tc ? gemm_tc_tiles(M, N) : ((M + 63) / 64) * ((N + 63) / 64);
         const int kb = (K + bk - 1) / bk;
-        int s = (num_sms + tiles - 1) / tiles;
+        // tcgen05 CTAs hold ~200 KB smem (1 per SM): round DOWN so splits x tiles fits one wave
+        int s = tc ? num_sms / tiles : (num_sms + tiles - 1) / tiles;
         s = std::min(s, std::max(1, kb / 4));
         s = std::min(s, 16);
         s = std::max(s, 1);
