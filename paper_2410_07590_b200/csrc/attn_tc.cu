@@ -31,9 +31,10 @@ namespace {
 constexpr int D = 128, BR = 128, BK = 128, SOFTMAX_WARPS = 8, THREADS = SOFTMAX_WARPS * 32 + 64;
 constexpr uint32_t SUB = 128 * 64 * 2;          // one [128 rows][64 cols] bf16 SW128 sub-tile = 16 KB
 constexpr uint32_t OFF_Q = 0, OFF_P = 2 * SUB;  // 32 KB each
-constexpr uint32_t OFF_KV = 4 * SUB;            // stage s: K at OFF_KV + s*4*SUB, V at +2*SUB
-constexpr uint32_t STAGE = 4 * SUB;             // 64 KB
-constexpr uint32_t OFF_BAR = OFF_KV + 2 * STAGE;
+constexpr uint32_t OFF_K = 4 * SUB;             // K ring: 2 stages x 32 KB
+constexpr uint32_t OFF_V = 8 * SUB;             // V ring: 2 stages x 32 KB (separate ring: K_{j+2} loads once
+constexpr uint32_t KSTAGE = 2 * SUB;            //   S_j is done, without waiting for PV_j)
+constexpr uint32_t OFF_BAR = 12 * SUB;
 constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float LOG2E = 1.4426950408889634f;
@@ -130,12 +131,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-    uint64_t* kv_full = bars;       // [2]
-    uint64_t* kv_empty = bars + 2;  // [2]
-    uint64_t* s_full = bars + 4;    // [2]
-    uint64_t* p_full = bars + 6;
-    uint64_t* o_full = bars + 7;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    uint64_t* k_full = bars;        // [2]
+    uint64_t* k_empty = bars + 2;   // [2]
+    uint64_t* v_full = bars + 4;    // [2]
+    uint64_t* v_empty = bars + 6;   // [2]
+    uint64_t* s_full = bars + 8;    // [2]
+    uint64_t* p_full = bars + 10;
+    uint64_t* o_full = bars + 11;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
     __shared__ int red_lo[THREADS / 32], red_hi[THREADS / 32];
     __shared__ float xmax[2][2][BR];  // [tile parity][half][row]: per-half row maxima exchanged each tile
 
@@ -164,8 +167,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&kv_full[s], 1);
-            mbar_init(&kv_empty[s], 1);
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
             mbar_init(&s_full[s], 1);
         }
         mbar_init(p_full, SOFTMAX_WARPS * 32);
@@ -208,44 +213,50 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {  // ---------------- TMA producer ----------------
             for (int j = 0; j < n; ++j) {
                 const int s = j & 1;
-                mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-                mbar_expect_tx(&kv_full[s], STAGE);
-                const uint32_t st = sbase + OFF_KV + s * STAGE;
+                const uint32_t par = ((j >> 1) & 1) ^ 1;
                 const int key = ks + j * BK;
-                tma_load_2d(st, &tmK, &kv_full[s], g * D, key);
-                tma_load_2d(st + SUB, &tmK, &kv_full[s], g * D + 64, key);
-                tma_load_2d(st + 2 * SUB, &tmV, &kv_full[s], g * D, key);
-                tma_load_2d(st + 3 * SUB, &tmV, &kv_full[s], g * D + 64, key);
+                mbar_wait(&k_empty[s], par);
+                mbar_expect_tx(&k_full[s], KSTAGE);
+                const uint32_t kd = sbase + OFF_K + s * KSTAGE;
+                tma_load_2d(kd, &tmK, &k_full[s], g * D, key);
+                tma_load_2d(kd + SUB, &tmK, &k_full[s], g * D + 64, key);
+                mbar_wait(&v_empty[s], par);
+                mbar_expect_tx(&v_full[s], KSTAGE);
+                const uint32_t vd = sbase + OFF_V + s * KSTAGE;
+                tma_load_2d(vd, &tmV, &v_full[s], g * D, key);
+                tma_load_2d(vd + SUB, &tmV, &v_full[s], g * D + 64, key);
             }
         }
     } else if (warp == SOFTMAX_WARPS + 1) {
         if (lane == 0) {  // ---------------- MMA issuer ----------------
             auto issue_s = [&](int j) {
                 const int s = j & 1;
-                mbar_wait(&kv_full[s], (j >> 1) & 1);
+                mbar_wait(&k_full[s], (j >> 1) & 1);
                 tc_fence_after();
-                const uint32_t kb = sbase + OFF_KV + s * STAGE;
+                const uint32_t kb = sbase + OFF_K + s * KSTAGE;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
                     umma(tmem + s * 128, desc_k(sbase + OFF_Q + off), desc_k(kb + off), IDESC_S, kk > 0);
                 }
                 umma_commit(&s_full[s]);
+                umma_commit(&k_empty[s]);
             };
             if (n > 0) issue_s(0);
             if (n > 1) issue_s(1);
             for (int j = 0; j < n; ++j) {
                 const int s = j & 1;
                 mbar_wait(p_full, j & 1);
+                mbar_wait(&v_full[s], (j >> 1) & 1);
                 tc_fence_after();
-                const uint32_t vb = sbase + OFF_KV + s * STAGE + 2 * SUB;
+                const uint32_t vb = sbase + OFF_V + s * KSTAGE;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t aoff = (kk >> 2) * SUB + (kk & 3) * 32;
                     umma(tmem + 256, desc_k(sbase + OFF_P + aoff), desc_mn(vb + kk * 2048), IDESC_PV, kk > 0);
                 }
                 umma_commit(o_full);
-                umma_commit(&kv_empty[s]);
+                umma_commit(&v_empty[s]);
                 if (j + 2 < n) issue_s(j + 2);
             }
         }
