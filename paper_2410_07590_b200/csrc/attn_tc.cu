@@ -6,14 +6,14 @@
 // GQA packing: a CTA owns 128 rows of ONE kv head g, row r = (token t, head g*group + r%group), so the
 // K/V tiles it streams serve all `group` query heads (C2: 64 tokens x 7 heads = 448 rows = 3.5 tiles).
 //
-// Per CTA (320 threads): warps 0-7 = softmax (two threads per row: warps w and w+4 share TMEM lanes
-// 32(w%4).., each owns 64 of the S columns and 64 of the O columns; row maxima are exchanged through
-// shared memory), warp 8 = TMA producer, warp 9 = MMA issuer. smem: Q [128x128] and P [128x128] (two 64-column SW128 sub-tiles each, 32 KB), two K/V stages
+// Per CTA (576 threads): warps 0-15 = softmax (four threads per row: warps w, w+4, w+8, w+12 share TMEM
+// lanes 32(w%4).., each owns 32 of the S columns and 32 of the O columns; partial row maxima are
+// exchanged through shared memory), warp 16 = TMA producer, warp 17 = MMA issuer. smem: Q [128x128] and P [128x128] (two 64-column SW128 sub-tiles each, 32 KB), two K/V stages
 // of 64 KB. TMEM (512 cols): S double buffer at cols 0/128, O tile at 256.
 //   S_j  = Q . K_j^T          tcgen05.mma kind::f16 M128 N128 K16 x8, A,B K-major
 //   P_j  = exp2(S_j*scale*log2e - m_j)  (softmax warps: TMEM -> regs -> bf16 -> swizzled smem)
 //   O_j  = P_j . V_j          tcgen05.mma, A = P (K-major), B = V (MN-major: d contiguous)
-// The running output O lives in registers (64 fp32 per thread), rescaled by exp2(m_{j-1} - m_j) each
+// The running output O lives in registers (32 fp32 per thread), rescaled by exp2(m_{j-1} - m_j) each
 // tile and incremented by the O_j tile read back from TMEM. Split-K over keys writes (O, m, l) partials
 // combined by attn_combine_kernel (attn_simt.cu) — same workspace layout as the SIMT kernel.
 #include <cuda.h>
@@ -28,7 +28,10 @@
 namespace tkv {
 namespace {
 
-constexpr int D = 128, BR = 128, BK = 128, SOFTMAX_WARPS = 8, THREADS = SOFTMAX_WARPS * 32 + 64;
+constexpr int D = 128, BR = 128, BK = 128;
+constexpr int NQ = 4;                       // softmax threads per row
+constexpr int CPT = 128 / NQ;               // S / O columns per softmax thread
+constexpr int SOFTMAX_WARPS = 4 * NQ, THREADS = SOFTMAX_WARPS * 32 + 64;
 constexpr uint32_t SUB = 128 * 64 * 2;          // one [128 rows][64 cols] bf16 SW128 sub-tile = 16 KB
 constexpr uint32_t OFF_Q = 0, OFF_P = 2 * SUB;  // 32 KB each
 constexpr uint32_t OFF_K = 4 * SUB;             // K ring: 2 stages x 32 KB
@@ -106,6 +109,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -121,6 +131,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 // byte offset of 16-byte chunk `c` (0..7) of row `r` inside a K-major SW128 sub-tile
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -140,14 +153,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* o_full = bars + 11;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
     __shared__ int red_lo[THREADS / 32], red_hi[THREADS / 32];
-    __shared__ float xmax[2][2][BR];  // [tile parity][half][row]: per-half row maxima exchanged each tile
+    __shared__ float xmax[2][NQ][BR];  // [tile parity][quarter][row]: partial row maxima exchanged each tile
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int group = H / Hkv, g = blockIdx.y, split = blockIdx.z;
     const int rows_total = Tq * group;
     const bool softmax = warp < SOFTMAX_WARPS;
-    const int r = tid & (BR - 1);           // tile row (TMEM lane) of a softmax thread
-    const int half = softmax ? warp >> 2 : 0;  // which 64 S columns / 64 O columns this thread owns
+    const int r = tid & (BR - 1);             // tile row (TMEM lane) of a softmax thread
+    const int qtr = softmax ? warp >> 2 : 0;  // which CPT S columns / CPT O columns this thread owns
     const int row = blockIdx.x * BR + r;
     const bool active = softmax && row < rows_total;
     const int t = active ? row / group : 0;
@@ -182,13 +195,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // ---- Q tile: each softmax thread stages its half of its row (sub-tile `half`) ----
+    // ---- Q tile: each softmax thread stages its CPT columns of its row ----
     if (softmax) {
-        const uint4* src = reinterpret_cast<const uint4*>(q + (int64_t)t * H * D + (int64_t)h * D) + half * 8;
+        constexpr int CH = CPT / 8;  // 16-byte chunks per thread
+        const uint4* src = reinterpret_cast<const uint4*>(q + (int64_t)t * H * D + (int64_t)h * D) + qtr * CH;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < CH; ++c) {
             const uint4 v = active ? src[c] : make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4*>(smem + OFF_Q + half * SUB + swz(r, c)) = v;
+            const int chunk = qtr * CH + c;  // 0..15 over the 128 columns
+            const uint32_t a = sbase + OFF_Q + (chunk >> 3) * SUB + swz(r, chunk & 7);
+            sts128(a, v.x, v.y, v.z, v.w);
         }
         fence_async_smem();
     }
@@ -261,89 +277,73 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        // ---------------- softmax: two threads per row, 64 S / 64 O columns each ----------------
+        // ---------------- softmax: NQ threads per row, CPT S / CPT O columns each ----------------
         const float sl2 = scale * LOG2E;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t col0 = (uint32_t)(half * 64);
-        float o[64];
+        const uint32_t col0 = (uint32_t)(qtr * CPT);
+        float o[CPT];
 #pragma unroll
-        for (int i = 0; i < 64; ++i) o[i] = 0.f;
+        for (int i = 0; i < CPT; ++i) o[i] = 0.f;
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < n; ++j) {
-            const int key0 = ks + j * BK + half * 64;  // first key of this thread's 64 columns
-            const uint32_t sa = tmem + lane_base + (uint32_t)((j & 1) * 128) + col0;
-            const bool full = key0 >= my_lo && key0 + 63 <= my_hi;
+            const int key0 = ks + j * BK + qtr * CPT;  // first key of this thread's columns
+            const bool full = key0 >= my_lo && key0 + CPT - 1 <= my_hi;
             const int clo = my_lo - key0, chi = my_hi - key0;
             mbar_wait(&s_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
-            uint32_t v0[32], v1[32];
-            tmem_ld32(sa, v0);
-            tmem_ld32(sa + 32, v1);
+            uint32_t v[CPT];
+            tmem_ld32(tmem + lane_base + (uint32_t)((j & 1) * 128) + col0, v);
             tmem_wait_ld();
-            float mx8[8];
+            if (!full) {  // masked columns -> -inf (branch is per tile, uniform inside the common case)
 #pragma unroll
-            for (int a = 0; a < 8; ++a) mx8[a] = -INFINITY;
-            if (full) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v0[i]));
-                    mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v1[i]));
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    mx8[i & 7] = fmaxf(mx8[i & 7], (i >= clo && i <= chi) ? __uint_as_float(v0[i]) : -INFINITY);
-                    mx8[i & 7] =
-                        fmaxf(mx8[i & 7], (i + 32 >= clo && i + 32 <= chi) ? __uint_as_float(v1[i]) : -INFINITY);
-                }
+                for (int i = 0; i < CPT; ++i)
+                    v[i] = (i >= clo && i <= chi) ? v[i] : __float_as_uint(-INFINITY);
             }
-            float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-            // exchange with the thread owning the other 64 columns of this row
-            xmax[j & 1][half][r] = mx;
+            float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(v[i]));
+            float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+            xmax[j & 1][qtr][r] = mx;
             asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
-            mx = fmaxf(mx, xmax[j & 1][half ^ 1][r]);
+#pragma unroll
+            for (int k = 1; k < NQ; ++k) mx = fmaxf(mx, xmax[j & 1][(qtr + k) & (NQ - 1)][r]);
             mx = mx == -INFINITY ? -INFINITY : mx * sl2;
             const float m_new = fmaxf(m, mx);
             const float alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
             if (j > 0) {  // fold in O tile j-1 (after it lands, the P buffer is free again)
                 mbar_wait(o_full, (j - 1) & 1);
                 tc_fence_after();
-                uint32_t w0[32], w1[32];
-                tmem_ld32(tmem + lane_base + 256 + col0, w0);
-                tmem_ld32(tmem + lane_base + 256 + col0 + 32, w1);
-                tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    o[i] += __uint_as_float(w0[i]);
-                    o[32 + i] += __uint_as_float(w1[i]);
+                for (int hh = 0; hh < CPT / 16; ++hh) {  // 16 columns at a time keeps register pressure down
+                    uint32_t w[16];
+                    tmem_ld16(tmem + lane_base + 256 + col0 + hh * 16, w);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) o[hh * 16 + i] += __uint_as_float(w[i]);
                 }
             }
-            float rs8[8];
+            // p = exp2(s*scale*log2e - m); masked entries hold -inf -> ex2 -> 0; a row with nothing visible
+            // yet (m_new = -inf) uses offset 0 so every p is exactly 0.
+            const float moff = m_new == -INFINITY ? 0.f : m_new;
+            float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+            uint32_t pk[CPT / 2];
 #pragma unroll
-            for (int a = 0; a < 8; ++a) rs8[a] = 0.f;
-            uint32_t pk[32];
-            const bool live = m_new != -INFINITY;
-#pragma unroll
-            for (int i = 0; i < 64; i += 2) {
-                const float s0 = __uint_as_float(i < 32 ? v0[i] : v1[i - 32]);
-                const float s1 = __uint_as_float(i + 1 < 32 ? v0[i + 1] : v1[i - 31]);
-                const bool ok0 = live && (full || (i >= clo && i <= chi));
-                const bool ok1 = live && (full || (i + 1 >= clo && i + 1 <= chi));
-                const float p0 = ok0 ? ex2(fmaf(s0, sl2, -m_new)) : 0.f;
-                const float p1 = ok1 ? ex2(fmaf(s1, sl2, -m_new)) : 0.f;
-                rs8[(i >> 1) & 7] += p0 + p1;
+            for (int i = 0; i < CPT; i += 2) {
+                const float p0 = ex2(fmaf(__uint_as_float(v[i]), sl2, -moff));
+                const float p1 = ex2(fmaf(__uint_as_float(v[i + 1]), sl2, -moff));
+                rs4[(i >> 1) & 3] += p0 + p1;
                 pk[i >> 1] = pack_bf16(p0, p1);
             }
-            uint8_t* pb = smem + OFF_P + half * SUB;  // keys [half*64, half*64+64) = P sub-tile `half`
+            // keys [qtr*CPT, qtr*CPT+CPT) of this row -> P sub-tile (qtr*CPT)/64, chunks ((qtr*CPT)%64)/8 ..
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<uint4*>(pb + swz(r, c)) =
-                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-            const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-            l = l * alpha + rs;
+            for (int c = 0; c < CPT / 8; ++c) {
+                const int chunk = (qtr * CPT) / 8 + c;
+                sts128(sbase + OFF_P + (chunk >> 3) * SUB + swz(r, chunk & 7), pk[4 * c], pk[4 * c + 1],
+                       pk[4 * c + 2], pk[4 * c + 3]);
+            }
+            l = l * alpha + ((rs4[0] + rs4[1]) + (rs4[2] + rs4[3]));
 #pragma unroll
-            for (int i = 0; i < 64; ++i) o[i] *= alpha;
+            for (int i = 0; i < CPT; ++i) o[i] *= alpha;
             m = m_new;
             fence_async_smem();
             tc_fence_before();
@@ -352,40 +352,39 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (n > 0) {
             mbar_wait(o_full, (n - 1) & 1);
             tc_fence_after();
-            uint32_t w0[32], w1[32];
-            tmem_ld32(tmem + lane_base + 256 + col0, w0);
-            tmem_ld32(tmem + lane_base + 256 + col0 + 32, w1);
+            uint32_t w[CPT];
+            tmem_ld32(tmem + lane_base + 256 + col0, w);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                o[i] += __uint_as_float(w0[i]);
-                o[32 + i] += __uint_as_float(w1[i]);
-            }
+            for (int i = 0; i < CPT; ++i) o[i] += __uint_as_float(w[i]);
         }
-        // the two halves of a row hold partial sums l over disjoint key columns (same running max)
-        xmax[0][half][r] = l;
+        // the NQ threads of a row hold partial sums l over disjoint key columns (same running max)
         asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
-        l += xmax[0][half ^ 1][r];
+        xmax[0][qtr][r] = l;
+        asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
+#pragma unroll
+        for (int k = 1; k < NQ; ++k) l += xmax[0][(qtr + k) & (NQ - 1)][r];
         if (active) {
             const int64_t orow = (int64_t)t * H + h;
             if (splits == 1) {
                 if (l == 0.f) {
-                    if (half == 0) atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
+                    if (qtr == 0) atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
                 } else {
                     const float inv = 1.0f / l;
-                    uint4* dst = reinterpret_cast<uint4*>(out + orow * D + half * 64);
+                    uint4* dst = reinterpret_cast<uint4*>(out + orow * D + qtr * CPT);
 #pragma unroll
-                    for (int c = 0; c < 8; ++c)
+                    for (int c = 0; c < CPT / 8; ++c)
                         dst[c] = make_uint4(pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv),
                                             pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
                                             pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv),
                                             pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
                 }
             } else {
-                float4* wo = reinterpret_cast<float4*>(ws_o + ((int64_t)split * Tq * H + orow) * D + half * 64);
+                float4* wo = reinterpret_cast<float4*>(ws_o + ((int64_t)split * Tq * H + orow) * D + qtr * CPT);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) wo[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-                if (half == 0) {
+                for (int c = 0; c < CPT / 4; ++c)
+                    wo[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                if (qtr == 0) {
                     ws_ml[((int64_t)split * Tq * H + orow) * 2 + 0] = m == -INFINITY ? -INFINITY : m / LOG2E;
                     ws_ml[((int64_t)split * Tq * H + orow) * 2 + 1] = l;
                 }
