@@ -81,6 +81,7 @@ typedef struct {
 #define TKV_FLAG_SIMT_GEMM 0x1    /* bf16: use the SIMT GEMM instead of tcgen05 (debug/compare)  */
 #define TKV_FLAG_SIMT_ATTN 0x2    /* bf16: use the SIMT attention instead of tcgen05              */
 #define TKV_FLAG_NO_GRAPHS 0x4    /* do not capture prefill launch chains into CUDA graphs        */
+#define TKV_FLAG_NO_PDL 0x8       /* launch kernels without programmatic dependent launch          */
 
 /* IngestStats (pipeline.hpp:35-39) */
 typedef struct {

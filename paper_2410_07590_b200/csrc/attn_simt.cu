@@ -15,6 +15,7 @@
 
 #include <type_traits>
 
+#include "dev_common.cuh"
 #include "tkv_internal.h"
 
 namespace tkv {
@@ -35,6 +36,8 @@ __global__ void __launch_bounds__(THREADS) attn_simt_kernel(const T* __restrict_
                                                             float* __restrict__ ws_o, float* __restrict__ ws_ml,
                                                             int Tq, int Tk, int H, int Hkv, int splits, float scale,
                                                             int* err) {
+    pdl_launch();
+    pdl_wait();
     constexpr int E = D / LPR;
     __shared__ float Ks[KT][D];
     __shared__ float Vs[KT][D];
@@ -143,6 +146,8 @@ __global__ void __launch_bounds__(THREADS) attn_simt_kernel(const T* __restrict_
 template <typename T>
 __global__ void attn_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_ml, int rows, int D,
                                     int splits, T* __restrict__ out, int* err) {
+    pdl_launch();
+    pdl_wait();
     const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
@@ -197,7 +202,7 @@ void launch_d(const void* q, const void* k, const void* v, int kv_stride, const 
     const int group = H / Hkv;
     dim3 grid((Tq * group + ROWS - 1) / ROWS, Hkv, splits);
     const float scale = (float)(1.0 / sqrt((double)D));
-    attn_simt_kernel<T, D><<<grid, THREADS, 0, s>>>((const T*)q, (const T*)k, (const T*)v, kv_stride, lo, hi, (T*)out,
+    launch_k(attn_simt_kernel<T, D>, grid, THREADS, 0, s, (const T*)q, (const T*)k, (const T*)v, kv_stride, lo, hi, (T*)out,
                                                     ws.o, ws.ml, Tq, Tk, H, Hkv, splits, scale, err);
     TKV_CUDA(cudaGetLastError());
     if (splits > 1) launch_attention_combine(ws, Tq * H, D, splits, out, err, std::is_same<T, float>::value ? DT::F32 : DT::BF16, s);
@@ -222,9 +227,9 @@ void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, v
                               cudaStream_t s) {
     const int grid = (int)(((int64_t)rows * 32 + 255) / 256);
     if (dt == DT::F32)
-        attn_combine_kernel<float><<<grid, 256, 0, s>>>(ws.o, ws.ml, rows, d, splits, (float*)out, err);
+        launch_k(attn_combine_kernel<float>, grid, 256, 0, s, ws.o, ws.ml, rows, d, splits, (float*)out, err);
     else
-        attn_combine_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(ws.o, ws.ml, rows, d, splits, (__nv_bfloat16*)out, err);
+        launch_k(attn_combine_kernel<__nv_bfloat16>, grid, 256, 0, s, ws.o, ws.ml, rows, d, splits, (__nv_bfloat16*)out, err);
     TKV_CUDA(cudaGetLastError());
 }
 

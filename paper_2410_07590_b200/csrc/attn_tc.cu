@@ -23,6 +23,7 @@
 
 #include <mutex>
 
+#include "dev_common.cuh"
 #include "tkv_internal.h"
 
 namespace tkv {
@@ -155,6 +156,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     __shared__ int red_lo[THREADS / 32], red_hi[THREADS / 32];
     __shared__ float xmax[2][NQ][BR];  // [tile parity][quarter][row]: partial row maxima exchanged each tile
 
+    pdl_launch();
+    pdl_wait();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int group = H / Hkv, g = blockIdx.y, split = blockIdx.z;
     const int rows_total = Tq * group;
@@ -453,7 +456,7 @@ void launch_attention_tc(const void* q, const void* k, const void* v, int kv_str
     const int group = H / Hkv;
     dim3 grid((Tq * group + BR - 1) / BR, Hkv, splits);
     const float scale = (float)(1.0 / sqrt((double)D));
-    attn_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(tk, tv, (const __nv_bfloat16*)q, lo, hi, (__nv_bfloat16*)out,
+    launch_k(attn_tc_kernel, grid, THREADS, SMEM_BYTES, s, tk, tv, (const __nv_bfloat16*)q, lo, hi, (__nv_bfloat16*)out,
                                                      ws.o, ws.ml, Tq, Tk, H, Hkv, splits, scale, err);
     TKV_CUDA(cudaGetLastError());
     if (splits > 1) launch_attention_combine(ws, Tq * H, D, splits, out, err, DT::BF16, s);

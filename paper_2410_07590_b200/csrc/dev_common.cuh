@@ -1,0 +1,39 @@
+// Launch plumbing shared by every kernel of the engine: Programmatic Dependent Launch (PDL).
+//
+// Every kernel is launched with cudaLaunchAttributeProgrammaticStreamSerialization. A kernel calls
+// pdl_launch() at its start so the NEXT kernel's CTAs may be scheduled as SMs free up, and pdl_wait()
+// before it touches anything an earlier kernel produced (griddepcontrol.wait returns once the preceding
+// grid has completed and its writes are visible; since every grid waits on its predecessor, all earlier
+// grids are complete too). Work that does not depend on earlier kernels — barrier init, TMEM alloc,
+// tensor-map prefetch and, in the GEMM, the TMA loads of WEIGHT tiles — runs before the wait and so
+// overlaps the previous kernel's tail.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "tkv_internal.h"
+
+namespace tkv {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// cudaLaunchKernelEx with the PDL attribute (when enabled process-wide, see pdl_enabled()).
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TKV_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
+}  // namespace tkv

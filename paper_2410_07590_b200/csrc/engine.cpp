@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -29,6 +30,9 @@
 namespace tkv {
 
 static thread_local std::string g_last_error;
+static std::atomic<bool> g_pdl{true};
+bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed); }
+void set_pdl_enabled(bool on) { g_pdl.store(on, std::memory_order_relaxed); }
 
 void fail(tkv_status code, const std::string& msg) { throw Failure{code, msg}; }
 
@@ -959,6 +963,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         if (e->opts.page_tokens < 1) e->opts.page_tokens = 64;
         e->dt = e->opts.dtype == TKV_DTYPE_F32 ? DT::F32 : DT::BF16;
         e->device = e->opts.device;
+        set_pdl_enabled(!(e->opts.flags & TKV_FLAG_NO_PDL));
 
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "dev_common.cuh"
 #include "tkv_internal.h"
 
 namespace tkv {
@@ -19,6 +20,8 @@ template <typename T>
 __global__ void __launch_bounds__(THREADS) gemm_simt_kernel(const T* __restrict__ A, int lda, const T* __restrict__ W,
                                                             int M, int N, int K, float* __restrict__ partial,
                                                             int kchunk) {
+    pdl_launch();
+    pdl_wait();
     __shared__ float As[BK][BM + 4];
     __shared__ float Ws[BK][BN + 4];
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
@@ -77,10 +80,10 @@ void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K
     const int kchunk = ((K + splits - 1) / splits + BK - 1) / BK * BK;
     dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, splits);
     if (dt == DT::F32)
-        gemm_simt_kernel<float><<<grid, THREADS, 0, s>>>((const float*)A, lda, (const float*)W, M, N, K, partial,
+        launch_k(gemm_simt_kernel<float>, grid, THREADS, 0, s, (const float*)A, lda, (const float*)W, M, N, K, partial,
                                                          kchunk);
     else
-        gemm_simt_kernel<__nv_bfloat16><<<grid, THREADS, 0, s>>>((const __nv_bfloat16*)A, lda,
+        launch_k(gemm_simt_kernel<__nv_bfloat16>, grid, THREADS, 0, s, (const __nv_bfloat16*)A, lda,
                                                                  (const __nv_bfloat16*)W, M, N, K, partial, kchunk);
     TKV_CUDA(cudaGetLastError());
 }

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <mutex>
 
+#include "dev_common.cuh"
 #include "tkv_internal.h"
 
 namespace tkv {
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* done = empty + g.stages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
+    pdl_launch();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // weight rows (n) tile along x, token rows (m) tile along y
     const int n0 = blockIdx.x * 128, m0 = blockIdx.y * (SWAP ? g.ntok : 128), z = blockIdx.z;
@@ -145,10 +147,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (!(warp == 0 && lane == 0)) pdl_wait();  // the producer waits after its weight prefetch
 
     if (nkb > 0) {
         if (warp == 0 && lane == 0) {  // TMA producer
-            for (int i = 0; i < nkb; ++i) {
+            // Weight tiles do not depend on earlier kernels: fill the whole ring with them BEFORE waiting on
+            // the previous grid (PDL), so the weight stream overlaps the preceding kernel's tail.
+            const int pre = min(nkb, g.stages);
+            for (int i = 0; i < pre; ++i) {
+                mbar_expect_tx(&full[i], stage_bytes);
+                tma_load_2d(smem + i * stage_bytes, &tmW, &full[i], (kb0 + i) * BK, n0);
+            }
+            pdl_wait();
+            for (int i = 0; i < pre; ++i)
+                tma_load_2d(smem + i * stage_bytes + TILE_W, &tmA, &full[i], (kb0 + i) * BK, m0);
+            for (int i = pre; i < nkb; ++i) {
                 const int s = i % g.stages;
                 mbar_wait(&empty[s], ((uint32_t)(i / g.stages) & 1u) ^ 1u);
                 uint8_t* w = smem + s * stage_bytes;
@@ -333,7 +346,7 @@ template <bool SWAP, int EPI>
 void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g, dim3 grid, cudaStream_t s) {
     const size_t smem = 1024 + (size_t)g.stages * (TILE_W + g.a_bytes) + 256;
     TKV_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<SWAP, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    gemm_tc_kernel<SWAP, EPI><<<grid, THREADS, smem, s>>>(ta, tw, g);
+    launch_k(gemm_tc_kernel<SWAP, EPI>, grid, THREADS, smem, s, ta, tw, g);
     TKV_CUDA(cudaGetLastError());
 }
 

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dev_common.cuh"
 #include "tkv_internal.h"
 
 namespace tkv {
@@ -34,6 +35,8 @@ __device__ __forceinline__ double draw(uint64_t seed, uint64_t i, double scale) 
 template <typename T>
 __global__ void init_transposed_kernel(T* dst, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
                                        double scale, int row_block, int row_off) {
+    pdl_launch();
+    pdl_wait();
     const int64_t n = rows * cols;
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = o / rows, i = o - j * rows;
@@ -44,11 +47,15 @@ __global__ void init_transposed_kernel(T* dst, uint64_t seed, uint64_t base, int
 }
 
 __global__ void init_rowmajor_kernel(float* dst, uint64_t seed, uint64_t base, int64_t n, double scale) {
+    pdl_launch();
+    pdl_wait();
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
         dst[o] = __double2float_rn(draw(seed, base + (uint64_t)o, scale));
 }
 
 __global__ void fill_kernel(float* dst, float v, int64_t n) {
+    pdl_launch();
+    pdl_wait();
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
         dst[o] = v;
 }
@@ -68,6 +75,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 template <typename T>
 __global__ void embed_norm_kernel(const int32_t* tok, const float* emb, int hidden, int vocab, const float* w,
                                   float eps, float* x, T* h, int* err) {
+    pdl_launch();
+    pdl_wait();
     __shared__ float red[32];
     const int t = blockIdx.x;
     const int id = tok[t];
@@ -93,6 +102,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) residual_norm_kernel(float* x, const float* partial, int splits,
                                                             int64_t plane, int hidden, const float* w, float eps,
                                                             T* h, int* err) {
+    pdl_launch();
+    pdl_wait();
     __shared__ float red[32];
     constexpr int MAXV = 8;
     const int64_t t = blockIdx.x;
@@ -141,6 +152,8 @@ __global__ void __launch_bounds__(256) residual_norm_kernel(float* x, const floa
 template <typename T>
 __global__ void residual_norm_scalar_kernel(float* x, const float* partial, int splits, int64_t plane, int hidden,
                                             const float* w, float eps, T* h, int* err) {
+    pdl_launch();
+    pdl_wait();
     __shared__ float red[32];
     const int64_t t = blockIdx.x;
     float ss = 0.f;
@@ -162,6 +175,8 @@ __global__ void residual_norm_scalar_kernel(float* x, const float* partial, int 
 
 template <typename T>
 __global__ void swiglu_kernel(const float* partial, int splits, int T_, int inter, T* act, int interleave64) {
+    pdl_launch();
+    pdl_wait();
     const int64_t n = (int64_t)T_ * inter, plane = (int64_t)T_ * 2 * inter;
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = o / inter, i = o - t * inter;
@@ -181,6 +196,8 @@ template <typename T>
 __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
                                     const int32_t* pos, const float2* rope, T* q, T* kc, T* vc, int row0,
                                     StoreScatter sc, int layer) {
+    pdl_launch();
+    pdl_wait();
     const int qd = H * d, kvd = Hkv * d, N = qd + 2 * kvd, half = d / 2;
     const int64_t pairs = (int64_t)T_ * (N / 2), plane = (int64_t)T_ * N;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * blockDim.x) {
@@ -249,6 +266,8 @@ __global__ void __launch_bounds__(256) gather_rope_vec_kernel(const T* __restric
                                                               const GatherSeg* __restrict__ segs, int n_units, int L,
                                                               int kvd, int d, const float2* __restrict__ rope,
                                                               T* __restrict__ cache, int64_t cap, int rotate) {
+    pdl_launch();
+    pdl_wait();
     constexpr int N = Vec16<T>::N;
     const int vec_per_row = kvd / N, half = d / 2;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -290,6 +309,8 @@ __global__ void __launch_bounds__(256) gather_rope_vec_kernel(const T* __restric
 template <typename T>
 __global__ void gather_rope_pair_kernel(const T* pool, int page_tokens, const GatherSeg* segs, int n_units, int L,
                                         int kvd, int d, const float2* rope, T* cache, int64_t cap, int rotate) {
+    pdl_launch();
+    pdl_wait();
     const int half = d / 2;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int seg = u / (2 * L), layer = (u / 2) % L, kv = u & 1;
@@ -314,6 +335,8 @@ __global__ void gather_rope_pair_kernel(const T* pool, int page_tokens, const Ga
 
 template <typename T>
 __global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, float* logits, int* err) {
+    pdl_launch();
+    pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= vocab) return;
     float acc = 0.f;
@@ -326,6 +349,8 @@ __global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, fl
 }
 
 __global__ void mask_kernel(const int32_t* lo, const int32_t* hi, int rows, int cols, uint8_t* out) {
+    pdl_launch();
+    pdl_wait();
     const int64_t n = (int64_t)rows * cols;
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(o / cols), j = (int)(o - (int64_t)i * cols);
@@ -336,6 +361,8 @@ __global__ void mask_kernel(const int32_t* lo, const int32_t* hi, int rows, int 
 template <typename T>
 __global__ void unrotate_kernel(const T* k, int rows, int kvd, int d, const int32_t* pos, const float2* rope,
                                 float* out) {
+    pdl_launch();
+    pdl_wait();
     const int64_t n = (int64_t)rows * kvd / 2;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = (2 * p) / kvd;
@@ -349,17 +376,23 @@ __global__ void unrotate_kernel(const T* k, int rows, int kvd, int d, const int3
 
 template <typename T>
 __global__ void to_f32_kernel(const T* src, int64_t n, float* dst) {
+    pdl_launch();
+    pdl_wait();
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
         dst[o] = ldf(src, o);
 }
 
 template <typename T>
 __global__ void from_f32_kernel(const float* src, int64_t n, T* dst) {
+    pdl_launch();
+    pdl_wait();
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
         stf(dst, o, src[o]);
 }
 
 __global__ void reduce_splits_kernel(const float* p, int splits, int64_t n, float* out) {
+    pdl_launch();
+    pdl_wait();
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
         float a = 0.f;
         for (int s = 0; s < splits; ++s) a += p[s * n + o];
@@ -388,25 +421,25 @@ inline int grid_for(int64_t n, int block, int cap = 148 * 16) {
 
 void launch_init_transposed(void* dst, DT dt, uint64_t seed, uint64_t base, int64_t rows, int64_t cols,
                             double scale, cudaStream_t s, int row_block, int row_off) {
-    DISPATCH_DT(dt, init_transposed_kernel<T><<<grid_for(rows * cols, 256, 148 * 64), 256, 0, s>>>(
+    DISPATCH_DT(dt, launch_k(init_transposed_kernel<T>, grid_for(rows * cols, 256, 148 * 64), 256, 0, s, 
                         (T*)dst, seed, base, rows, cols, scale, row_block, row_off));
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_init_rowmajor_f32(float* dst, uint64_t seed, uint64_t base, int64_t rows, int64_t cols, double scale,
                               cudaStream_t s) {
-    init_rowmajor_kernel<<<grid_for(rows * cols, 256, 148 * 64), 256, 0, s>>>(dst, seed, base, rows * cols, scale);
+    launch_k(init_rowmajor_kernel, grid_for(rows * cols, 256, 148 * 64), 256, 0, s, dst, seed, base, rows * cols, scale);
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t s) {
-    fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, v, n);
+    launch_k(fill_kernel, grid_for(n, 256), 256, 0, s, dst, v, n);
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_embed_norm(const int32_t* tok, int T_, const float* emb, int hidden, int vocab, const float* w, float eps,
                        float* x, void* h, DT dt, int* err, cudaStream_t s) {
-    DISPATCH_DT(dt, embed_norm_kernel<T><<<T_, 256, 0, s>>>(tok, emb, hidden, vocab, w, eps, x, (T*)h, err));
+    DISPATCH_DT(dt, launch_k(embed_norm_kernel<T>, T_, 256, 0, s, tok, emb, hidden, vocab, w, eps, x, (T*)h, err));
     TKV_CUDA(cudaGetLastError());
 }
 
@@ -414,10 +447,10 @@ void launch_residual_norm(float* x, const float* partial, int splits, int T_, in
                           void* h, DT dt, int* err, cudaStream_t s) {
     const int64_t plane = (int64_t)T_ * hidden;
     if (hidden % 4 == 0 && hidden <= 8 * 4 * 256) {
-        DISPATCH_DT(dt, residual_norm_kernel<T><<<T_, 256, 0, s>>>(x, partial, splits, plane, hidden, w, eps, (T*)h,
+        DISPATCH_DT(dt, launch_k(residual_norm_kernel<T>, T_, 256, 0, s, x, partial, splits, plane, hidden, w, eps, (T*)h,
                                                                    err));
     } else {
-        DISPATCH_DT(dt, residual_norm_scalar_kernel<T><<<T_, 512, 0, s>>>(x, partial, splits, plane, hidden, w, eps,
+        DISPATCH_DT(dt, launch_k(residual_norm_scalar_kernel<T>, T_, 512, 0, s, x, partial, splits, plane, hidden, w, eps,
                                                                           (T*)h, err));
     }
     TKV_CUDA(cudaGetLastError());
@@ -425,7 +458,7 @@ void launch_residual_norm(float* x, const float* partial, int splits, int T_, in
 
 void launch_swiglu(const float* partial, int splits, int T_, int inter, void* act, DT dt, cudaStream_t s,
                    bool interleave64) {
-    DISPATCH_DT(dt, swiglu_kernel<T><<<grid_for((int64_t)T_ * inter, 256), 256, 0, s>>>(partial, splits, T_, inter,
+    DISPATCH_DT(dt, launch_k(swiglu_kernel<T>, grid_for((int64_t)T_ * inter, 256), 256, 0, s, partial, splits, T_, inter,
                                                                                          (T*)act, (int)interleave64));
     TKV_CUDA(cudaGetLastError());
 }
@@ -434,7 +467,7 @@ void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hk
                          const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc, int layer,
                          DT dt, cudaStream_t s) {
     const int64_t pairs = (int64_t)T_ * (H + 2 * Hkv) * d / 2;
-    DISPATCH_DT(dt, qkv_epilogue_kernel<T><<<grid_for(pairs, 256), 256, 0, s>>>(
+    DISPATCH_DT(dt, launch_k(qkv_epilogue_kernel<T>, grid_for(pairs, 256), 256, 0, s, 
                         partial, splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer));
     TKV_CUDA(cudaGetLastError());
 }
@@ -449,10 +482,10 @@ void launch_gather_rope(const void* pool, int page_tokens, const GatherSeg* segs
     const bool vec_ok = (kvd % vecN == 0) && (d % vecN == 0) && (page_tokens * kvd * (int)dt_size(dt)) % 16 == 0 &&
                         (cap * kvd * (int64_t)dt_size(dt)) % 16 == 0;
     if (vec_ok) {
-        DISPATCH_DT(dt, gather_rope_vec_kernel<T><<<grid, 256, 0, s>>>((const T*)pool, page_tokens, segs, n_units, L,
+        DISPATCH_DT(dt, launch_k(gather_rope_vec_kernel<T>, grid, 256, 0, s, (const T*)pool, page_tokens, segs, n_units, L,
                                                                        kvd, d, rope, (T*)cache, cap, rotate));
     } else {
-        DISPATCH_DT(dt, gather_rope_pair_kernel<T><<<grid, 256, 0, s>>>((const T*)pool, page_tokens, segs, n_units, L,
+        DISPATCH_DT(dt, launch_k(gather_rope_pair_kernel<T>, grid, 256, 0, s, (const T*)pool, page_tokens, segs, n_units, L,
                                                                         kvd, d, rope, (T*)cache, cap, rotate));
     }
     TKV_CUDA(cudaGetLastError());
@@ -461,35 +494,35 @@ void launch_gather_rope(const void* pool, int page_tokens, const GatherSeg* segs
 void launch_lm_head(const void* h, const void* W, int hidden, int vocab, float* logits, DT dt, int* err,
                     cudaStream_t s) {
     const int threads = 256, warps_per_block = threads / 32;
-    DISPATCH_DT(dt, lm_head_kernel<T><<<(vocab + warps_per_block - 1) / warps_per_block, threads, 0, s>>>(
+    DISPATCH_DT(dt, launch_k(lm_head_kernel<T>, (vocab + warps_per_block - 1) / warps_per_block, threads, 0, s, 
                         (const T*)h, (const T*)W, hidden, vocab, logits, err));
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_mask_materialize(const int32_t* lo, const int32_t* hi, int rows, int cols, uint8_t* out, cudaStream_t s) {
-    mask_kernel<<<grid_for((int64_t)rows * cols, 256), 256, 0, s>>>(lo, hi, rows, cols, out);
+    launch_k(mask_kernel, grid_for((int64_t)rows * cols, 256), 256, 0, s, lo, hi, rows, cols, out);
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_unrotate_rows(const void* k, int rows, int kvd, int d, const int32_t* pos, const float2* rope, float* out,
                           DT dt, cudaStream_t s) {
-    DISPATCH_DT(dt, unrotate_kernel<T><<<grid_for((int64_t)rows * kvd / 2, 256), 256, 0, s>>>((const T*)k, rows, kvd,
+    DISPATCH_DT(dt, launch_k(unrotate_kernel<T>, grid_for((int64_t)rows * kvd / 2, 256), 256, 0, s, (const T*)k, rows, kvd,
                                                                                                d, pos, rope, out));
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_to_f32(const void* src, int64_t n, float* dst, DT dt, cudaStream_t s) {
-    DISPATCH_DT(dt, to_f32_kernel<T><<<grid_for(n, 256), 256, 0, s>>>((const T*)src, n, dst));
+    DISPATCH_DT(dt, launch_k(to_f32_kernel<T>, grid_for(n, 256), 256, 0, s, (const T*)src, n, dst));
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_from_f32(const float* src, int64_t n, void* dst, DT dt, cudaStream_t s) {
-    DISPATCH_DT(dt, from_f32_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(src, n, (T*)dst));
+    DISPATCH_DT(dt, launch_k(from_f32_kernel<T>, grid_for(n, 256), 256, 0, s, src, n, (T*)dst));
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_reduce_splits(const float* partial, int splits, int64_t n, float* out, cudaStream_t s) {
-    reduce_splits_kernel<<<grid_for(n, 256), 256, 0, s>>>(partial, splits, n, out);
+    launch_k(reduce_splits_kernel, grid_for(n, 256), 256, 0, s, partial, splits, n, out);
     TKV_CUDA(cudaGetLastError());
 }
 

@@ -21,6 +21,10 @@ void cuda_check(cudaError_t e, const char* what);
 #define TKV_CUDA(x) ::tkv::cuda_check((x), #x)
 
 enum class DT : int { F32 = 0, BF16 = 1 };
+
+// Programmatic Dependent Launch on/off for every kernel launch (process-wide; TKV_FLAG_NO_PDL disables).
+bool pdl_enabled();
+void set_pdl_enabled(bool on);
 inline size_t dt_size(DT t) { return t == DT::F32 ? 4 : 2; }
 
 // ---------------------------------------------------------------------------------------------
