@@ -98,47 +98,60 @@ __device__ __forceinline__ float silu(float z) { return z / (1.0f + __expf(-z));
 
 struct GemmArgs {
     int M, N, K;
-    int kb_per_split;
-    int ntok;         // swapped: tokens per tile (N of the MMA, multiple of 16); normal: 128
-    uint32_t a_bytes; // bytes of the activation tile per stage
+    int kb_total, kb_per_split;
+    int n_tiles, m_tiles, units;  // work units = n_tiles * m_tiles * splits (persistent loop over them)
+    int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128
+    uint32_t a_bytes;             // bytes of the activation tile per stage
     int stages;
+    uint32_t acc_cols;            // TMEM columns of one accumulator buffer (two buffers)
     uint32_t tmem_cols;
-    float* partial;   // EPI_PARTIAL
-    __nv_bfloat16* act;  // EPI_SWIGLU: [M][N/2]
+    uint32_t scratch_off;         // SwiGLU exchange scratch (swapped): byte offset after the ring
+    float* partial;               // EPI_PARTIAL
+    __nv_bfloat16* act;           // EPI_SWIGLU: [M][N/2]
 };
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
+constexpr int THREADS_P = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
 
+__device__ __forceinline__ void unit_coords(const GemmArgs& g, int u, int& nt, int& mt, int& z) {
+    const int per = g.n_tiles * g.m_tiles;
+    z = u / per;
+    const int rem = u - z * per;
+    mt = rem / g.n_tiles;
+    nt = rem - mt * g.n_tiles;
+}
+
+// Persistent: grid = min(units, #SMs); CTA b owns units b, b + grid, ... The smem ring of {W, A} stages
+// flows across units without draining; two TMEM accumulators let the epilogue of unit i overlap the
+// mainloop of unit i+1.
 template <bool SWAP, int EPI>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS_P, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, GemmArgs g) {
+    pdl_launch();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t stage_bytes = TILE_W + g.a_bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.stages * stage_bytes);
     uint64_t* empty = full + g.stages;
-    uint64_t* done = empty + g.stages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-
-    pdl_launch();
+    uint64_t* tfull = empty + g.stages;  // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;        // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // weight rows (n) tile along x, token rows (m) tile along y
-    const int n0 = blockIdx.x * 128, m0 = blockIdx.y * (SWAP ? g.ntok : 128), z = blockIdx.z;
-    const int kb_total = (g.K + BK - 1) / BK;
-    const int kb0 = z * g.kb_per_split;
-    const int nkb = min(kb_total, kb0 + g.kb_per_split) - kb0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < g.stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(done, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     }
-    if (warp == 0) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(g.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -147,165 +160,187 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    if (!(warp == 0 && lane == 0)) pdl_wait();  // the producer waits after its weight prefetch
+    const int mstep = SWAP ? g.ntok : 128;
 
-    if (nkb > 0) {
-        if (warp == 0 && lane == 0) {  // TMA producer
-            // Weight tiles do not depend on earlier kernels: fill the whole ring with them BEFORE waiting on
-            // the previous grid (PDL), so the weight stream overlaps the preceding kernel's tail.
-            const int pre = min(nkb, g.stages);
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer ----------------
+            // Weight tiles do not depend on earlier kernels: fill the ring with the first unit's weights
+            // BEFORE waiting on the previous grid (PDL), so the weight stream overlaps its tail.
+            int nt, mt, z;
+            unit_coords(g, blockIdx.x, nt, mt, z);
+            const int kb0 = z * g.kb_per_split;
+            const int nkb0 = min(g.kb_total, kb0 + g.kb_per_split) - kb0;
+            const int pre = min(nkb0, g.stages);
             for (int i = 0; i < pre; ++i) {
                 mbar_expect_tx(&full[i], stage_bytes);
-                tma_load_2d(smem + i * stage_bytes, &tmW, &full[i], (kb0 + i) * BK, n0);
+                tma_load_2d(smem + i * stage_bytes, &tmW, &full[i], (kb0 + i) * BK, nt * 128);
             }
             pdl_wait();
             for (int i = 0; i < pre; ++i)
-                tma_load_2d(smem + i * stage_bytes + TILE_W, &tmA, &full[i], (kb0 + i) * BK, m0);
-            for (int i = pre; i < nkb; ++i) {
-                const int s = i % g.stages;
-                mbar_wait(&empty[s], ((uint32_t)(i / g.stages) & 1u) ^ 1u);
-                uint8_t* w = smem + s * stage_bytes;
-                uint8_t* a = w + TILE_W;
-                mbar_expect_tx(&full[s], stage_bytes);
-                const int kc = (kb0 + i) * BK;
-                tma_load_2d(w, &tmW, &full[s], kc, n0);
-                tma_load_2d(a, &tmA, &full[s], kc, m0);
-            }
-        } else if (warp == 1 && lane == 0) {  // MMA issuer
-            const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % g.stages;
-                mbar_wait(&full[s], (uint32_t)(i / g.stages) & 1u);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t w = smem_u32(smem + s * stage_bytes);
-                const uint32_t a = w + TILE_W;
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {  // 16 bf16 = 32 B along K inside the 128 B swizzle row
-                    if (SWAP)
-                        umma_f16(tmem, desc_k(w + k * 32), desc_k(a + k * 32), id, (i | k) != 0);
-                    else
-                        umma_f16(tmem, desc_k(a + k * 32), desc_k(w + k * 32), id, (i | k) != 0);
+                tma_load_2d(smem + i * stage_bytes + TILE_W, &tmA, &full[i], (kb0 + i) * BK, mt * mstep);
+            int it = pre;
+            for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+                unit_coords(g, u, nt, mt, z);
+                const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
+                for (int i = (u == (int)blockIdx.x ? pre : 0); i < nkb; ++i, ++it) {
+                    const int s = it % g.stages;
+                    mbar_wait(&empty[s], ((uint32_t)(it / g.stages) & 1u) ^ 1u);
+                    uint8_t* w = smem + s * stage_bytes;
+                    mbar_expect_tx(&full[s], stage_bytes);
+                    tma_load_2d(w, &tmW, &full[s], (k0 + i) * BK, nt * 128);
+                    tma_load_2d(w + TILE_W, &tmA, &full[s], (k0 + i) * BK, mt * mstep);
                 }
-                umma_commit(&empty[s]);
             }
-            umma_commit(done);
         }
-        __syncwarp();
-        mbar_wait(done, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    if (SWAP) {
-        // TMEM lane = weight row n, column = token
-        const int n = n0 + warp * 32 + lane;
-        if (EPI == EPI_PARTIAL) {
-            float* out = g.partial + (int64_t)z * g.M * g.N;
-#pragma unroll 1
-            for (int c = 0; c < g.ntok; c += 16) {
-                uint32_t r[16];
-                if (nkb > 0) {
-                    tmem_ld16(tmem + lane_base + (uint32_t)c, r);
-                } else {
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer ----------------
+            const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128);
+            int it = 0, lu = 0;
+            for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++lu) {
+                int nt, mt, z;
+                unit_coords(g, u, nt, mt, z);
+                const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
+                const int b = lu & 1;
+                mbar_wait(&tempty[b], ((uint32_t)(lu >> 1) & 1u) ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t acc = tmem + (uint32_t)b * g.acc_cols;
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % g.stages;
+                    mbar_wait(&full[s], (uint32_t)(it / g.stages) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t w = smem_u32(smem + s * stage_bytes);
+                    const uint32_t a = w + TILE_W;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) r[j] = 0u;
-                }
-                if (n < g.N) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int m = m0 + c + j;
-                        if (m < g.M) out[(int64_t)m * g.N + n] = __uint_as_float(r[j]);
+                    for (int k = 0; k < BK / 16; ++k) {  // 16 bf16 = 32 B along K inside the 128 B swizzle row
+                        if (SWAP)
+                            umma_f16(acc, desc_k(w + k * 32), desc_k(a + k * 32), id, (i | k) != 0);
+                        else
+                            umma_f16(acc, desc_k(a + k * 32), desc_k(w + k * 32), id, (i | k) != 0);
                     }
+                    umma_commit(&empty[s]);
                 }
-            }
-        } else {
-            // rows 0-63 of the tile are gate, 64-127 the matching up rows (interleaved W_gu layout)
-            float* up = reinterpret_cast<float*>(smem);  // pipeline smem is idle now: [64][ntok+1]
-            const int ld = g.ntok + 1;
-            if (warp >= 2) {
-#pragma unroll 1
-                for (int c = 0; c < g.ntok; c += 16) {
-                    uint32_t r[16];
-                    tmem_ld16(tmem + lane_base + (uint32_t)c, r);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) up[((warp - 2) * 32 + lane) * ld + c + j] = __uint_as_float(r[j]);
-                }
-            }
-            __syncthreads();
-            if (warp < 2) {
-                const int inter = g.N / 2;
-                const int i = blockIdx.x * 64 + warp * 32 + lane;
-#pragma unroll 1
-                for (int c = 0; c < g.ntok; c += 16) {
-                    uint32_t r[16];
-                    tmem_ld16(tmem + lane_base + (uint32_t)c, r);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int m = m0 + c + j;
-                        if (m < g.M && i < inter)
-                            g.act[(int64_t)m * inter + i] =
-                                __float2bfloat16_rn(silu(__uint_as_float(r[j])) * up[(warp * 32 + lane) * ld + c + j]);
-                    }
-                }
+                umma_commit(&tfull[b]);
             }
         }
     } else {
-        // TMEM lane = token row m, column = weight row
-        const int m = m0 + warp * 32 + lane;
-        if (EPI == EPI_PARTIAL) {
-            float* out = g.partial + (int64_t)z * g.M * g.N + (int64_t)m * g.N;
+        // ---------------- epilogue warps 2-5: TMEM lane group = warp % 4 ----------------
+        pdl_wait();
+        const int lg = warp & 3;
+        const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+        const int et = threadIdx.x - 64;  // 0..127
+        int lu = 0;
+        for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++lu) {
+            int nt, mt, z;
+            unit_coords(g, u, nt, mt, z);
+            const int b = lu & 1;
+            mbar_wait(&tfull[b], (uint32_t)(lu >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t acc = tmem + lane_base + (uint32_t)b * g.acc_cols;
+            const int n0 = nt * 128, m0 = mt * mstep;
+            if (SWAP) {
+                const int n = n0 + lg * 32 + lane;  // TMEM lane = weight row n, column = token
+                if (EPI == EPI_PARTIAL) {
+                    float* out = g.partial + (int64_t)z * g.M * g.N;
 #pragma unroll 1
-            for (int c = 0; c < 128; c += 16) {
-                uint32_t r[16];
-                if (nkb > 0) {
-                    tmem_ld16(tmem + lane_base + (uint32_t)c, r);
+                    for (int c = 0; c < g.ntok; c += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(acc + (uint32_t)c, r);
+                        if (n < g.N) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const int m = m0 + c + j;
+                                if (m < g.M) out[(int64_t)m * g.N + n] = __uint_as_float(r[j]);
+                            }
+                        }
+                    }
                 } else {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) r[j] = 0u;
-                }
-                if (m < g.M) {
-                    const int n = n0 + c;
-                    if (n + 16 <= g.N && (g.N % 4) == 0) {
-                        float4* o4 = reinterpret_cast<float4*>(out + n);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (n + j < g.N) out[n + j] = __uint_as_float(r[j]);
-                    }
-                }
-            }
-        } else {
-            const int inter = g.N / 2;
-            const int i0 = blockIdx.x * 64;
+                    // tile rows 0-63 = gate, 64-127 = the matching up rows (interleaved W_gu layout)
+                    float* up = reinterpret_cast<float*>(smem + g.scratch_off);  // [64][ntok+1]
+                    const int ld = g.ntok + 1;
+                    if (lg >= 2) {
 #pragma unroll 1
-            for (int c = 0; c < 64; c += 16) {
-                uint32_t gr[16], ur[16];
-                tmem_ld16(tmem + lane_base + (uint32_t)c, gr);
-                tmem_ld16(tmem + lane_base + (uint32_t)(64 + c), ur);
-                if (m < g.M) {
-                    __align__(16) __nv_bfloat16 o[16];
+                        for (int c = 0; c < g.ntok; c += 16) {
+                            uint32_t r[16];
+                            tmem_ld16(acc + (uint32_t)c, r);
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        o[j] = __float2bfloat16_rn(silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]));
-                    __nv_bfloat16* dst = g.act + (int64_t)m * inter + i0 + c;
-                    if (i0 + c + 16 <= inter && (inter % 8) == 0) {
-                        reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<uint4*>(o)[0];
-                        reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<uint4*>(o)[1];
-                    } else {
-                        for (int j = 0; j < 16; ++j)
-                            if (i0 + c + j < inter) dst[j] = o[j];
+                            for (int j = 0; j < 16; ++j) up[((lg - 2) * 32 + lane) * ld + c + j] = __uint_as_float(r[j]);
+                        }
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (lg < 2) {
+                        const int inter = g.N / 2;
+                        const int i = nt * 64 + lg * 32 + lane;
+#pragma unroll 1
+                        for (int c = 0; c < g.ntok; c += 16) {
+                            uint32_t r[16];
+                            tmem_ld16(acc + (uint32_t)c, r);
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const int m = m0 + c + j;
+                                if (m < g.M && i < inter)
+                                    g.act[(int64_t)m * inter + i] = __float2bfloat16_rn(
+                                        silu(__uint_as_float(r[j])) * up[(lg * 32 + lane) * ld + c + j]);
+                            }
+                        }
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");  // scratch reusable by the next unit
+                }
+            } else {
+                const int m = m0 + lg * 32 + lane;  // TMEM lane = token row m, column = weight row
+                if (EPI == EPI_PARTIAL) {
+                    float* out = g.partial + (int64_t)z * g.M * g.N + (int64_t)m * g.N;
+#pragma unroll 1
+                    for (int c = 0; c < 128; c += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(acc + (uint32_t)c, r);
+                        if (m < g.M) {
+                            const int n = n0 + c;
+                            if (n + 16 <= g.N && (g.N % 4) == 0) {
+                                float4* o4 = reinterpret_cast<float4*>(out + n);
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+                                    o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    if (n + j < g.N) out[n + j] = __uint_as_float(r[j]);
+                            }
+                        }
+                    }
+                } else {
+                    const int inter = g.N / 2;
+                    const int i0 = nt * 64;
+#pragma unroll 1
+                    for (int c = 0; c < 64; c += 16) {
+                        uint32_t gr[16], ur[16];
+                        tmem_ld16(acc + (uint32_t)c, gr);
+                        tmem_ld16(acc + (uint32_t)(64 + c), ur);
+                        if (m < g.M) {
+                            __align__(16) __nv_bfloat16 o[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                o[j] = __float2bfloat16_rn(silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]));
+                            __nv_bfloat16* dst = g.act + (int64_t)m * inter + i0 + c;
+                            if (i0 + c + 16 <= inter && (inter % 8) == 0) {
+                                reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<uint4*>(o)[0];
+                                reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<uint4*>(o)[1];
+                            } else {
+                                for (int j = 0; j < 16; ++j)
+                                    if (i0 + c + j < inter) dst[j] = o[j];
+                            }
+                        }
                     }
                 }
             }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
+            (void)et;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
     }
@@ -343,11 +378,9 @@ CUtensorMap make_map(const void* base, int rows, int cols_k, int ld_elems, int b
 }
 
 template <bool SWAP, int EPI>
-void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g, dim3 grid, cudaStream_t s) {
-    const size_t smem = 1024 + (size_t)g.stages * (TILE_W + g.a_bytes) + 256;
+void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g, int grid, size_t smem, cudaStream_t s) {
     TKV_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<SWAP, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_k(gemm_tc_kernel<SWAP, EPI>, grid, THREADS, smem, s, ta, tw, g);
-    TKV_CUDA(cudaGetLastError());
+    launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(THREADS_P), smem, s, ta, tw, g);
 }
 
 }  // namespace
@@ -369,23 +402,35 @@ void launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, 
     g.M = M;
     g.N = N;
     g.K = K;
-    const int kb_total = (K + BK - 1) / BK;
-    g.kb_per_split = (kb_total + splits - 1) / splits;
+    g.kb_total = (K + BK - 1) / BK;
+    g.kb_per_split = (g.kb_total + splits - 1) / splits;
+    const int eff_splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;  // every unit non-empty
+    g.n_tiles = (N + 127) / 128;
+    g.m_tiles = swap ? 1 : (M + 127) / 128;
+    g.units = g.n_tiles * g.m_tiles * eff_splits;
     g.ntok = swap ? ((M + 15) / 16) * 16 : 128;
     g.a_bytes = (uint32_t)g.ntok * BK * 2;
-    g.stages = (int)std::min<uint32_t>(8, SMEM_BUDGET / (TILE_W + g.a_bytes));
+    g.acc_cols = swap ? (uint32_t)g.ntok : 128u;
     g.tmem_cols = 32;
-    while (g.tmem_cols < (uint32_t)g.ntok) g.tmem_cols <<= 1;
+    while (g.tmem_cols < 2 * g.acc_cols) g.tmem_cols <<= 1;
+    const uint32_t scratch = (swap && swiglu_act) ? (uint32_t)(64 * (g.ntok + 1) * 4 + 1023) / 1024 * 1024 : 0;
+    g.stages = (int)std::min<uint32_t>(8, (SMEM_BUDGET - scratch) / (TILE_W + g.a_bytes));
+    g.scratch_off = (uint32_t)g.stages * (TILE_W + g.a_bytes) + 256;  // after the ring and its barriers
+    g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;
     g.partial = partial;
     g.act = (__nv_bfloat16*)swiglu_act;
+    const size_t smem = 1024 + (size_t)g.scratch_off + scratch;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min(g.units, sms);
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
     const CUtensorMap tw = make_map(W, N, K, K, 128);
-    dim3 grid((N + 127) / 128, swap ? 1 : (M + 127) / 128, splits);
     if (swiglu_act) {
-        if (splits != 1) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the whole K range in one CTA");
-        swap ? launch_t<true, EPI_SWIGLU>(ta, tw, g, grid, s) : launch_t<false, EPI_SWIGLU>(ta, tw, g, grid, s);
+        if (eff_splits != 1) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the whole K range in one unit");
+        swap ? launch_t<true, EPI_SWIGLU>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_SWIGLU>(ta, tw, g, grid, smem, s);
     } else {
-        swap ? launch_t<true, EPI_PARTIAL>(ta, tw, g, grid, s) : launch_t<false, EPI_PARTIAL>(ta, tw, g, grid, s);
+        swap ? launch_t<true, EPI_PARTIAL>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_PARTIAL>(ta, tw, g, grid, smem, s);
     }
 }
 
