@@ -429,10 +429,8 @@ struct tkv_engine {
             return 0;
         }
         partial.ensure((size_t)s * M * N * sizeof(float));
-        if (tc)
-            launch_gemm_tc(A, lda, W, M, N, K, partial.as<float>(), s, stream);
-        else
-            launch_gemm_simt(A, lda, W, M, N, K, partial.as<float>(), s, dt, stream);
+        if (tc) return launch_gemm_tc(A, lda, W, M, N, K, partial.as<float>(), s, stream);
+        launch_gemm_simt(A, lda, W, M, N, K, partial.as<float>(), s, dt, stream);
         return s;
     }
 
@@ -1697,7 +1695,7 @@ tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* 
         part.ensure((size_t)splits * M * N * 4);
         o.ensure((size_t)M * N * 4);
         if (use_tc)
-            launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, part.as<float>(), splits, 0);
+            splits = launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, part.as<float>(), splits, 0);
         else
             launch_gemm_simt(a.p, (int)K, w.p, (int)M, (int)N, (int)K, part.as<float>(), splits, dt, 0);
         launch_reduce_splits(part.as<float>(), splits, M * N, o.as<float>(), 0);

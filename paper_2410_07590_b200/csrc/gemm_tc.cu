@@ -395,8 +395,8 @@ int gemm_tc_tiles(int M, int N) {
     return ((N + 127) / 128) * (swap ? 1 : (M + 127) / 128);
 }
 
-void launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
-                    cudaStream_t s, void* swiglu_act) {
+int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
+                   cudaStream_t s, void* swiglu_act) {
     const bool swap = M <= 128;
     GemmArgs g{};
     g.M = M;
@@ -432,6 +432,7 @@ void launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, 
     } else {
         swap ? launch_t<true, EPI_PARTIAL>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_PARTIAL>(ta, tw, g, grid, smem, s);
     }
+    return eff_splits;
 }
 
 }  // namespace tkv

@@ -104,8 +104,9 @@ void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K
 // be 1, W rows interleaved in 64-row gate/up blocks) the epilogue writes act[M][N/2] = silu(g)*u in bf16.
 bool gemm_tc_supported(int M, int N, int K, int lda);
 int gemm_tc_tiles(int M, int N);
-void launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
-                    cudaStream_t s, void* swiglu_act = nullptr);
+// Returns the number of split-K partial planes actually written (<= splits: every split is non-empty).
+int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
+                   cudaStream_t s, void* swiglu_act = nullptr);
 
 // Flash attention, SIMT (fp32 math): q [Tq][H*d], k/v rows [Tk][Hkv*d] (stride kv_stride elements),
 // row t attends keys j with lo[t] <= j <= hi[t]. out [Tq][H*d] (dtype). ws: split-K workspace.
