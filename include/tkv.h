@@ -188,6 +188,30 @@ tkv_status tkv_context_read_kv(const tkv_context* ctx, int64_t layer, tkv_kv_whi
  * 0/1 bytes [rows, cols] (build_mask / causal_rows, src/attention.cpp:50-92). */
 tkv_status tkv_context_mask(const tkv_context* ctx, uint8_t* out, int64_t rows, int64_t cols);
 
+/* Multi-GPU (one engine per GPU; requests data-parallel; the store sharded by document). A remote chunk
+ * is registered under a peer slot and read by the gather kernel straight from the peer's HBM over
+ * NVLink (P2P loads fused with the RoPE pass), or copied once into the local store (fetch_remote). */
+typedef struct {
+    uint8_t bytes[64];
+} tkv_ipc_handle;
+/* cudaIpcGetMemHandle of this engine's page pool (one process per GPU: share it with the peers). */
+tkv_status tkv_store_export_ipc(tkv_engine* eng, tkv_ipc_handle* out, uint64_t* pool_bytes);
+/* Map a peer process's pool (cudaIpcOpenMemHandle, lazy peer access) into peer slot `slot` (1..15). */
+tkv_status tkv_store_attach_ipc(tkv_engine* eng, int32_t slot, const tkv_ipc_handle* handle);
+/* Same, for a peer engine in this process (possibly another GPU: enables peer access). */
+tkv_status tkv_store_attach_engine(tkv_engine* eng, int32_t slot, tkv_engine* peer);
+/* Directory entry of a locally owned chunk: its page indices and token count. */
+tkv_status tkv_store_chunk_pages(const tkv_engine* eng, uint64_t chunk_id, int32_t* pages, int64_t capacity,
+                                 int64_t* n_pages, int64_t* len);
+/* Register a chunk owned by the peer in `slot` (its page list from tkv_store_chunk_pages on the owner).
+ * `framed` (nullable, len tokens) enables naive_prefill_ids for it. No-op if the id is already known. */
+tkv_status tkv_store_register_remote(tkv_engine* eng, uint64_t chunk_id, int32_t slot, int64_t len,
+                                     const int32_t* pages, int64_t n_pages, const int32_t* framed);
+/* Copy a registered remote chunk into the local store (fetch-once cache policy). */
+tkv_status tkv_store_fetch_remote(tkv_engine* eng, uint64_t chunk_id);
+/* KV bytes read from peer pools so far (NVLink traffic of the gather + fetches). */
+int64_t tkv_remote_bytes(const tkv_engine* eng);
+
 /* Measurement hooks (bench.py): the engine's CUDA stream, and per-kernel-class device time
  * accumulated with CUDA events on that stream while profiling is on. */
 void* tkv_engine_stream(tkv_engine* eng);

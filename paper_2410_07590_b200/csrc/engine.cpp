@@ -235,6 +235,7 @@ struct Chunk {
     int64_t len = 0;
     std::vector<int32_t> pages;
     std::vector<int32_t> framed;  // empty for TKVC-imported chunks
+    int32_t slot = 0;             // page pool holding the pages: 0 = local HBM, >0 = a peer GPU (NVLink)
 };
 
 }  // namespace tkv
@@ -272,6 +273,9 @@ struct tkv_engine {
     size_t page_bytes = 0;
     std::vector<int32_t> free_pages;
     std::unordered_map<uint64_t, Chunk> chunks;
+    PoolTable pools;                     // slot 0 = pool.p; peers attached via IPC or same-process P2P
+    std::vector<void*> ipc_opened;       // peer pools opened with cudaIpcOpenMemHandle (closed on destroy)
+    int64_t remote_bytes = 0;            // bytes of KV gathered from peer pools (bench reporting)
 
     // forward workspace
     DevMem x, h, q, attn, act, partial, attn_ws, logits, err, d_tok, d_pos, d_lo, d_hi, d_page, d_slot, d_segs;
@@ -486,6 +490,7 @@ void* tkv_engine::kv_plane(tkv_context* c, int64_t layer, int kv) const {
 }
 
 tkv_engine::~tkv_engine() {
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     for (tkv_context* c : live) {
         c->eng = nullptr;
         if (c->kv) cudaFree(c->kv);
@@ -761,6 +766,7 @@ tkv_context* assemble_impl(tkv_engine* e, const uint64_t* ids, int64_t n, int mo
             g.n_tok = (int32_t)std::min<int64_t>(e->page_tokens, ch->len - off);
             g.dst_row = (int32_t)(running + off);
             g.pos0 = (int32_t)(first + off);
+            g.pool = ch->slot;
             segs.push_back(g);
         }
         for (int64_t t = 0; t < ch->len; ++t) c->positions.push_back(first + t);
@@ -781,7 +787,9 @@ tkv_context* assemble_impl(tkv_engine* e, const uint64_t* ids, int64_t n, int mo
         e->upload(slot, e->d_segs.p, segs.data(), b, 0);
         e->staging.end(e->stream);
         tkv_engine::Scope sc(e, PC_GATHER, 1);
-        launch_gather_rope(e->pool.p, (int)e->page_tokens, e->d_segs.as<GatherSeg>(), (int)segs.size(), (int)e->L,
+        for (const Chunk* ch : cs)
+            if (ch->slot) e->remote_bytes += ch->len * e->L * 2 * e->kvd * (int64_t)dt_size(e->dt);
+        launch_gather_rope(e->pools, (int)e->page_tokens, e->d_segs.as<GatherSeg>(), (int)segs.size(), (int)e->L,
                            (int)e->kvd, (int)e->d, e->rope.as<float2>(), c->kv, c->cap, 1, e->dt, e->num_sms,
                            e->stream);
     }
@@ -1064,6 +1072,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         }
         e->n_pages = std::max<int64_t>(1, (cap_tokens + e->page_tokens - 1) / e->page_tokens);
         e->pool.ensure((size_t)e->n_pages * e->page_bytes);
+        e->pools.p[0] = e->pool.p;
         e->free_pages.reserve((size_t)e->n_pages);
         for (int64_t p = e->n_pages - 1; p >= 0; --p) e->free_pages.push_back((int32_t)p);
         e->sync();
@@ -1384,7 +1393,7 @@ tkv_status tkv_store_read(const tkv_engine* ce, uint64_t id, int64_t layer, tkv_
         tmpf.ensure((size_t)ch.len * e->kvd * 4);
         for (size_t p = 0; p < ch.pages.size(); ++p) {
             const int64_t t0 = (int64_t)p * e->page_tokens, nt = std::min<int64_t>(e->page_tokens, ch.len - t0);
-            const uint8_t* src = static_cast<uint8_t*>(e->pool.p) + (size_t)ch.pages[p] * e->page_bytes +
+            const uint8_t* src = static_cast<const uint8_t*>(e->pools.p[ch.slot]) + (size_t)ch.pages[p] * e->page_bytes +
                                  (size_t)((layer * 2 + (int)which) * e->page_tokens) * e->kvd * es;
             TKV_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(tmp.p) + (size_t)t0 * e->kvd * es, src,
                                      (size_t)nt * e->kvd * es, cudaMemcpyDeviceToDevice, e->stream));
@@ -1559,7 +1568,7 @@ tkv_status tkv_context_read_kv(const tkv_context* c, int64_t layer, tkv_kv_which
                 segs.ensure(c->chunk_segs.size() * sizeof(GatherSeg));
                 TKV_CUDA(cudaMemcpyAsync(segs.p, c->chunk_segs.data(), c->chunk_segs.size() * sizeof(GatherSeg),
                                          cudaMemcpyHostToDevice, e->stream));
-                launch_gather_rope(e->pool.p, (int)e->page_tokens, segs.as<GatherSeg>(), (int)c->chunk_segs.size(),
+                launch_gather_rope(e->pools, (int)e->page_tokens, segs.as<GatherSeg>(), (int)c->chunk_segs.size(),
                                    (int)e->L, (int)e->kvd, (int)e->d, e->rope.as<float2>(), scratch.p, cap, 0, e->dt,
                                    e->num_sms, e->stream);
                 launch_to_f32(static_cast<uint8_t*>(scratch.p) + (size_t)(layer * 2 * cap) * e->kvd * dt_size(e->dt),
@@ -1654,6 +1663,122 @@ tkv_status tkv_debug_set_mask_fault(tkv_engine* e, int64_t row, int64_t col) {
         e->fault_col = col;
     });
 }
+
+// ---- multi-GPU: document-sharded stores, remote chunks read over NVLink ----
+namespace {
+void check_slot(int32_t slot) {
+    if (slot < 1 || slot >= kMaxPools) fail(TKV_ERR_CONFIG, "peer slot must be in [1, " + std::to_string(kMaxPools) + ")");
+}
+}  // namespace
+
+tkv_status tkv_store_export_ipc(tkv_engine* e, tkv_ipc_handle* out, uint64_t* pool_bytes) {
+    return guard([&] {
+        need(e, "engine");
+        need(out, "out");
+        static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(tkv_ipc_handle), "ipc handle size");
+        e->bind();
+        cudaIpcMemHandle_t h;
+        TKV_CUDA(cudaIpcGetMemHandle(&h, e->pool.p));
+        std::memset(out, 0, sizeof *out);
+        std::memcpy(out->bytes, &h, sizeof h);
+        if (pool_bytes) *pool_bytes = (uint64_t)e->pool.n;
+    });
+}
+
+tkv_status tkv_store_attach_ipc(tkv_engine* e, int32_t slot, const tkv_ipc_handle* h) {
+    return guard([&] {
+        need(e, "engine");
+        need(h, "handle");
+        check_slot(slot);
+        e->bind();
+        cudaIpcMemHandle_t mh;
+        std::memcpy(&mh, h->bytes, sizeof mh);
+        void* p = nullptr;
+        TKV_CUDA(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+        e->ipc_opened.push_back(p);
+        e->pools.p[slot] = p;
+    });
+}
+
+tkv_status tkv_store_attach_engine(tkv_engine* e, int32_t slot, tkv_engine* peer) {
+    return guard([&] {
+        need(e, "engine");
+        need(peer, "peer");
+        check_slot(slot);
+        if (peer->fingerprint != e->fingerprint || peer->page_bytes != e->page_bytes)
+            fail(TKV_ERR_STALE_CACHE, "peer store was built under a different model or page geometry");
+        e->bind();
+        if (peer->device != e->device) {
+            int ok = 0;
+            TKV_CUDA(cudaDeviceCanAccessPeer(&ok, e->device, peer->device));
+            if (!ok) fail(TKV_ERR_CUDA, "no peer access between the two GPUs");
+            const cudaError_t r = cudaDeviceEnablePeerAccess(peer->device, 0);
+            if (r != cudaSuccess && r != cudaErrorPeerAccessAlreadyEnabled) TKV_CUDA(r);
+            cudaGetLastError();
+        }
+        e->pools.p[slot] = peer->pool.p;
+    });
+}
+
+tkv_status tkv_store_chunk_pages(const tkv_engine* e, uint64_t id, int32_t* pages, int64_t capacity, int64_t* n_pages,
+                                 int64_t* len) {
+    return guard([&] {
+        need(e, "engine");
+        auto it = e->chunks.find(id);
+        if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
+        if (it->second.slot != 0) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " is not owned by this store");
+        const int64_t np = (int64_t)it->second.pages.size();
+        if (n_pages) *n_pages = np;
+        if (len) *len = it->second.len;
+        if (pages) {
+            if (capacity < np) fail(TKV_ERR_SHAPE, "pages buffer too small");
+            std::memcpy(pages, it->second.pages.data(), (size_t)np * 4);
+        }
+    });
+}
+
+tkv_status tkv_store_register_remote(tkv_engine* e, uint64_t id, int32_t slot, int64_t len, const int32_t* pages,
+                                     int64_t n_pages, const int32_t* framed) {
+    return guard([&] {
+        need(e, "engine");
+        need(pages, "pages");
+        check_slot(slot);
+        if (!e->pools.p[slot]) fail(TKV_ERR_CONFIG, "peer slot " + std::to_string(slot) + " is not attached");
+        if (len < 1 || n_pages != (len + e->page_tokens - 1) / e->page_tokens)
+            fail(TKV_ERR_SHAPE, "remote chunk: page count does not match its length");
+        if (e->chunks.count(id)) return;  // already local (or registered): keep the local copy
+        Chunk ch;
+        ch.len = len;
+        ch.slot = slot;
+        ch.pages.assign(pages, pages + n_pages);
+        if (framed) ch.framed.assign(framed, framed + len);
+        e->chunks.emplace(id, std::move(ch));
+    });
+}
+
+tkv_status tkv_store_fetch_remote(tkv_engine* e, uint64_t id) {
+    return guard([&] {
+        need(e, "engine");
+        e->bind();
+        auto it = e->chunks.find(id);
+        if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
+        Chunk& ch = it->second;
+        if (ch.slot == 0) return;
+        Chunk local;
+        local.len = ch.len;
+        local.framed = ch.framed;
+        store_chunk_pages(e, local);
+        for (size_t p = 0; p < ch.pages.size(); ++p)  // page-sized copies over NVLink (copy engine)
+            TKV_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(e->pool.p) + (size_t)local.pages[p] * e->page_bytes,
+                                     static_cast<const uint8_t*>(e->pools.p[ch.slot]) + (size_t)ch.pages[p] * e->page_bytes,
+                                     e->page_bytes, cudaMemcpyDefault, e->stream));
+        e->remote_bytes += (int64_t)(ch.pages.size() * e->page_bytes);
+        e->sync();
+        ch = std::move(local);
+    });
+}
+
+int64_t tkv_remote_bytes(const tkv_engine* e) { return e ? e->remote_bytes : -1; }
 
 // ---- kernel-level test entry points ----
 namespace {

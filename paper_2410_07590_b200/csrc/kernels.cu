@@ -262,7 +262,7 @@ __device__ __forceinline__ void rotate_vec(uint4& v, const float2* cs) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) gather_rope_vec_kernel(const T* __restrict__ pool, int page_tokens,
+__global__ void __launch_bounds__(256) gather_rope_vec_kernel(PoolTable pools, int page_tokens,
                                                               const GatherSeg* __restrict__ segs, int n_units, int L,
                                                               int kvd, int d, const float2* __restrict__ rope,
                                                               T* __restrict__ cache, int64_t cap, int rotate) {
@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(256) gather_rope_vec_kernel(const T* __restric
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int seg = u / (2 * L), layer = (u / 2) % L, kv = u & 1;
         const GatherSeg sg = segs[seg];
+        const T* pool = reinterpret_cast<const T*>(pools.p[sg.pool]);  // local HBM or a peer GPU over NVLink
         const uint4* src = reinterpret_cast<const uint4*>(
             pool + (((int64_t)sg.src_page * L + layer) * 2 + kv) * page_tokens * kvd);
         uint4* dst = reinterpret_cast<uint4*>(cache + ((int64_t)(layer * 2 + kv) * cap + sg.dst_row) * kvd);
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(256) gather_rope_vec_kernel(const T* __restric
 
 // Generic fallback: one pair per thread (any even head_size / kv_dim).
 template <typename T>
-__global__ void gather_rope_pair_kernel(const T* pool, int page_tokens, const GatherSeg* segs, int n_units, int L,
+__global__ void gather_rope_pair_kernel(PoolTable pools, int page_tokens, const GatherSeg* segs, int n_units, int L,
                                         int kvd, int d, const float2* rope, T* cache, int64_t cap, int rotate) {
     pdl_launch();
     pdl_wait();
@@ -315,7 +316,8 @@ __global__ void gather_rope_pair_kernel(const T* pool, int page_tokens, const Ga
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int seg = u / (2 * L), layer = (u / 2) % L, kv = u & 1;
         const GatherSeg sg = segs[seg];
-        const T* src = pool + (((int64_t)sg.src_page * L + layer) * 2 + kv) * page_tokens * kvd;
+        const T* src = reinterpret_cast<const T*>(pools.p[sg.pool]) +
+                       (((int64_t)sg.src_page * L + layer) * 2 + kv) * page_tokens * kvd;
         T* dst = cache + ((int64_t)(layer * 2 + kv) * cap + sg.dst_row) * kvd;
         const int np = sg.n_tok * kvd / 2;
         for (int i = threadIdx.x; i < np; i += blockDim.x) {
@@ -472,8 +474,8 @@ void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hk
     TKV_CUDA(cudaGetLastError());
 }
 
-void launch_gather_rope(const void* pool, int page_tokens, const GatherSeg* segs, int n_segs, int L, int kvd, int d,
-                        const float2* rope, void* cache, int64_t cap, int rotate, DT dt, int num_sms,
+void launch_gather_rope(const PoolTable& pools, int page_tokens, const GatherSeg* segs, int n_segs, int L, int kvd,
+                        int d, const float2* rope, void* cache, int64_t cap, int rotate, DT dt, int num_sms,
                         cudaStream_t s) {
     const int n_units = n_segs * L * 2;
     if (n_units == 0) return;
@@ -482,10 +484,10 @@ void launch_gather_rope(const void* pool, int page_tokens, const GatherSeg* segs
     const bool vec_ok = (kvd % vecN == 0) && (d % vecN == 0) && (page_tokens * kvd * (int)dt_size(dt)) % 16 == 0 &&
                         (cap * kvd * (int64_t)dt_size(dt)) % 16 == 0;
     if (vec_ok) {
-        DISPATCH_DT(dt, launch_k(gather_rope_vec_kernel<T>, grid, 256, 0, s, (const T*)pool, page_tokens, segs, n_units, L,
+        DISPATCH_DT(dt, launch_k(gather_rope_vec_kernel<T>, grid, 256, 0, s, pools, page_tokens, segs, n_units, L,
                                                                        kvd, d, rope, (T*)cache, cap, rotate));
     } else {
-        DISPATCH_DT(dt, launch_k(gather_rope_pair_kernel<T>, grid, 256, 0, s, (const T*)pool, page_tokens, segs, n_units, L,
+        DISPATCH_DT(dt, launch_k(gather_rope_pair_kernel<T>, grid, 256, 0, s, pools, page_tokens, segs, n_units, L,
                                                                         kvd, d, rope, (T*)cache, cap, rotate));
     }
     TKV_CUDA(cudaGetLastError());

@@ -76,11 +76,18 @@ struct GatherSeg {
     int32_t n_tok;     // tokens in this segment (<= page_tokens)
     int32_t dst_row;   // first request-cache row
     int32_t pos0;      // position id of the first token (positions are consecutive inside a segment)
+    int32_t pool;      // which page pool: 0 = this GPU's store, 1.. = a peer GPU's store (NVLink P2P reads)
+};
+// Page pools the gather kernel may read: slot 0 is local HBM, other slots are peer GPUs' pools mapped
+// into this process (cudaIpcOpenMemHandle, or peer access inside one process).
+constexpr int kMaxPools = 16;
+struct PoolTable {
+    const void* p[kMaxPools] = {};
 };
 // cache layout [L][2][cap][kv_dim]; rotate=0 copies keys unrotated (bit-exact export).
-void launch_gather_rope(const void* pool, int page_tokens, const GatherSeg* segs, int n_segs, int L, int kv_dim,
-                        int d, const float2* rope, void* cache, int64_t cap, int rotate, DT dt, int num_sms,
-                        cudaStream_t s);
+void launch_gather_rope(const PoolTable& pools, int page_tokens, const GatherSeg* segs, int n_segs, int L,
+                        int kv_dim, int d, const float2* rope, void* cache, int64_t cap, int rotate, DT dt,
+                        int num_sms, cudaStream_t s);
 
 // logits[v] = sum_k h[k] * W[v][k] (W dtype [vocab][hidden], h dtype), fp32 out; sets *err on non-finite.
 void launch_lm_head(const void* h, const void* W, int hidden, int vocab, float* logits, DT dt, int* err,

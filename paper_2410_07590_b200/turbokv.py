@@ -90,6 +90,10 @@ class _Stats(C.Structure):
     _fields_ = [("chunks", C.c_int64), ("new_chunks", C.c_int64), ("bytes_written", C.c_uint64)]
 
 
+class _Ipc(C.Structure):
+    _fields_ = [("bytes", C.c_uint8 * 64)]
+
+
 class _Flops(C.Structure):
     _fields_ = [("qkv", C.c_uint64), ("attn", C.c_uint64), ("o", C.c_uint64), ("mlp", C.c_uint64)]
 
@@ -150,6 +154,14 @@ def lib():
         L.tkv_launch_count.restype = C.c_int64
         L.tkv_launch_count.argtypes = [C.c_void_p]
         L.tkv_debug_set_mask_fault.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+        L.tkv_store_export_ipc.argtypes = [C.c_void_p, C.POINTER(_Ipc), C.POINTER(C.c_uint64)]
+        L.tkv_store_attach_ipc.argtypes = [C.c_void_p, C.c_int32, C.POINTER(_Ipc)]
+        L.tkv_store_attach_engine.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+        L.tkv_store_chunk_pages.argtypes = [C.c_void_p, C.c_uint64, I32P, C.c_int64, I64P, I64P]
+        L.tkv_store_register_remote.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, I32P, C.c_int64, I32P]
+        L.tkv_store_fetch_remote.argtypes = [C.c_void_p, C.c_uint64]
+        L.tkv_remote_bytes.restype = C.c_int64
+        L.tkv_remote_bytes.argtypes = [C.c_void_p]
         L.tkv_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, F32P, F32P, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_int, F32P]
         L.tkv_debug_attention.argtypes = [C.c_int, C.c_int, C.c_int, F32P, F32P, F32P, I32P, I32P, C.c_int64,
@@ -476,6 +488,39 @@ class Engine:
         n = C.c_int64()
         _check(lib().tkv_greedy_decode(self._h, ctx.handle, max_new, _p(out, I32P), C.byref(n)))
         return out[:n.value].tolist()
+
+    # ---- multi-GPU store sharding (include/tkv.h, "Multi-GPU") ----
+    def export_ipc(self) -> bytes:
+        h = _Ipc()
+        _check(lib().tkv_store_export_ipc(self._h, C.byref(h), None))
+        return bytes(h.bytes)
+
+    def attach_ipc(self, slot: int, handle: bytes) -> None:
+        h = _Ipc()
+        C.memmove(h.bytes, handle, 64)
+        _check(lib().tkv_store_attach_ipc(self._h, slot, C.byref(h)))
+
+    def attach_engine(self, slot: int, peer: "Engine") -> None:
+        _check(lib().tkv_store_attach_engine(self._h, slot, peer.handle))
+
+    def chunk_pages(self, chunk_id: int):
+        n, ln = C.c_int64(), C.c_int64()
+        _check(lib().tkv_store_chunk_pages(self._h, chunk_id, None, 0, C.byref(n), C.byref(ln)))
+        pages = np.zeros(max(n.value, 1), np.int32)
+        _check(lib().tkv_store_chunk_pages(self._h, chunk_id, _p(pages, I32P), len(pages), C.byref(n), C.byref(ln)))
+        return pages[:n.value], ln.value
+
+    def register_remote(self, chunk_id: int, slot: int, length: int, pages, framed=None) -> None:
+        pages = _i32(pages)
+        fr = _i32(framed) if framed is not None else None
+        _check(lib().tkv_store_register_remote(self._h, chunk_id, slot, length, _p(pages, I32P), len(pages),
+                                               _p(fr, I32P) if fr is not None else None))
+
+    def fetch_remote(self, chunk_id: int) -> None:
+        _check(lib().tkv_store_fetch_remote(self._h, chunk_id))
+
+    def remote_bytes(self) -> int:
+        return lib().tkv_remote_bytes(self._h)
 
     # ---- measurement ----
     def stream_ptr(self) -> int:

@@ -309,3 +309,38 @@ def test_gather_roundtrip_at_c2_chunk_shape():
         rows = np.r_[0:64, 4000:4064, 8128:8192]
         ref = O.Port.rope(stored_k[rows].astype(np.float64), ctx.positions[rows], cfg.head_size)
         assert np.abs(rot[rows] - ref).max() <= 8e-3 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("policy", ["direct", "fetch"])
+def test_remote_chunks_gathered_from_peer_pool(policy):
+    """Two engines (two shards); engine A serves a request whose chunks live partly in B's pool: the gather
+    kernel reads B's pages through the peer pool table (or after a fetch-once copy). The logits must equal
+    a single engine holding every chunk locally, bit for bit."""
+    cfg = T.ModelConfig.toy()
+    a = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=4096)
+    b = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=4096)
+    whole = engine(cfg, 42, "bf16")
+    pays = [O.random_text_tokens(8800 + i, n) for i, n in enumerate((70, 5, 130, 64))]
+    ids = whole.ingest_chunks(pays)
+    assert a.ingest_chunks([pays[0], pays[2]]) == [ids[0], ids[2]]
+    assert b.ingest_chunks([pays[1], pays[3]]) == [ids[1], ids[3]]
+    a.attach_engine(1, b)
+    for i in (1, 3):
+        pages, length = b.chunk_pages(ids[i])
+        a.register_remote(ids[i], 1, length, pages, O.frame(pays[i]))
+    if policy == "fetch":
+        for i in (1, 3):
+            a.fetch_remote(ids[i])
+    q = O.random_text_tokens(8899, 21)
+    with whole.assemble(ids, T.PositionMode.Reordered) as c0, a.assemble(ids, T.PositionMode.Reordered) as c1:
+        ref = whole.prefill_query(c0, q)
+        got = a.prefill_query(c1, q)
+        assert np.array_equal(got, ref)
+        assert np.array_equal(c1.read_kv(2, "v"), c0.read_kv(2, "v"))
+    per_token = cfg.layer_num * 2 * cfg.kv_dim * 2  # K and V, bf16
+    if policy == "direct":  # the 7- and 66-token chunks were read over the peer pool by one gather
+        assert a.remote_bytes() == (7 + 66) * per_token
+    else:  # copied once, page by page (1 + 2 pages of 64 tokens)
+        assert a.remote_bytes() == 3 * 64 * per_token
+    a.close()
+    b.close()
