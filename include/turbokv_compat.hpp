@@ -232,6 +232,26 @@ inline std::vector<Token> greedy_decode(Engine& engine, AssembledContext& ctx, i
     return out;
 }
 
+// tokenizer.hpp:13-26 (byte tokenizer; framing only is on the prefill path)
+namespace tok {
+constexpr Token kDocStart = 256;
+constexpr Token kDocEnd = 257;
+constexpr Token kEos = 258;
+inline std::vector<Token> encode(const std::string& text) {
+    std::vector<Token> out;
+    out.reserve(text.size());
+    for (unsigned char c : text) out.push_back(static_cast<Token>(c));
+    return out;
+}
+inline std::vector<Token> frame_chunk(const std::vector<Token>& payload) {
+    std::vector<Token> framed{kDocStart};
+    framed.insert(framed.end(), payload.begin(), payload.end());
+    framed.push_back(kDocEnd);
+    return framed;
+}
+}  // namespace tok
+using tok::encode;
+
 // kvstore.cpp:58-64
 inline uint64_t chunk_content_id(const std::vector<Token>& framed, uint64_t model_fingerprint) {
     return tkv_chunk_content_id(model_fingerprint, framed.data(), static_cast<int64_t>(framed.size()));
