@@ -20,6 +20,15 @@ namespace tkv {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// RMSNorm folded into the consumer (numerics.cpp:84-101): the producer of x writes xb = x * w and per-block
+// partial sums of squares ssp[t][0..nb) (fixed order, deterministic); a consumer of a linear map of xb
+// multiplies by this per-row scale, since rms(x) . W = scale(x) * ((x * w) . W).
+__device__ __forceinline__ float row_scale(const float* __restrict__ ssp, int nb, int64_t t, int hidden, float eps) {
+    float ss = 0.f;
+    for (int b = 0; b < nb; ++b) ss += ssp[t * nb + b];
+    return 1.0f / sqrtf(ss / (float)hidden + eps);
+}
+
 // cudaLaunchKernelEx with the PDL attribute (when enabled process-wide, see pdl_enabled()).
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {

@@ -278,7 +278,9 @@ struct tkv_engine {
     int64_t remote_bytes = 0;            // bytes of KV gathered from peer pools (bench reporting)
 
     // forward workspace
-    DevMem x, h, q, attn, act, partial, attn_ws, logits, err, d_tok, d_pos, d_lo, d_hi, d_page, d_slot, d_segs;
+    // x: fp32 residual stream; xb = x * norm_w (GEMM input; the RMSNorm scale is folded into consumers); ssp:
+    // per-row partial sums of squares (norm_blocks(hid) per row)
+    DevMem x, xb, ssp, q, attn, act, partial, attn_ws, logits, err, d_tok, d_pos, d_lo, d_hi, d_page, d_slot, d_segs;
     StagingRing staging;
     std::vector<std::pair<size_t, void*>> ctx_free;  // recycled request-cache buffers
     std::set<tkv_context*> live;
@@ -423,13 +425,14 @@ struct tkv_engine {
     // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits. With swiglu_act, a tcgen05 GEMM whose
     // K range fits one CTA writes silu(gate)*up straight to swiglu_act and returns 0.
     int gemm(const void* A, int lda, const void* W, int M, int N, int K, void* swiglu_act = nullptr) {
+        const int nb = norm_blocks((int)hid);
         const bool tc = use_tc();
         if (tc && !gemm_tc_supported(M, N, K, lda))
             fail(TKV_ERR_CONFIG, "shape not supported by the tcgen05 GEMM (rows must be 16-byte aligned)");
         const int s = pick_splits(M, N, K, tc);
         Scope sc(this, PC_GEMM, 1);
         if (tc && swiglu_act && s == 1 && gu_interleaved) {
-            launch_gemm_tc(A, lda, W, M, N, K, nullptr, 1, stream, swiglu_act);
+            launch_gemm_tc(A, lda, W, M, N, K, nullptr, 1, stream, swiglu_act, ssp.as<float>(), nb, (float)cfg.norm_eps);
             return 0;
         }
         partial.ensure((size_t)s * M * N * sizeof(float));
@@ -522,21 +525,25 @@ void tkv_engine::forward(const Fwd& f) {
     const size_t es = dt_size(dt);
     const float eps = (float)cfg.norm_eps;
     x.ensure((size_t)T * hid * 4);
-    h.ensure((size_t)T * std::max(hid, I) * es);
+    xb.ensure((size_t)T * hid * es);
+    const int nb = norm_blocks((int)hid);
+    ssp.ensure((size_t)T * nb * 4);
     q.ensure((size_t)T * qd * es);
     attn.ensure((size_t)T * qd * es);
     act.ensure((size_t)T * I * es);
     {
         Scope sc(this, PC_EPI, 1);
-        launch_embed_norm(f.tok, T, emb, (int)hid, (int)V, ones, eps, x.as<float>(), h.p, dt, err.as<int>(), stream);
+        launch_embed(f.tok, T, emb, (int)hid, (int)V, ones, x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
+                     stream);
     }
     for (int64_t l = 0; l < L; ++l) {
         // --- attention block ---
-        int s = gemm(h.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
+        int s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
         {
             Scope sc(this, PC_EPI, 1);
             launch_qkv_epilogue(partial.as<float>(), s, T, (int)H, (int)Hkv, (int)d, f.pos, rope.as<float2>(), q.p,
-                                kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), f.row0, f.sc, (int)l, dt, stream);
+                                kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), f.row0, f.sc, (int)l, ssp.as<float>(), nb,
+                                (int)hid, eps, dt, stream);
         }
         if (f.kv_only && l == L - 1) break;
         // In the last layer only the final row feeds the logits: attention, O-proj and the MLP run on it alone.
@@ -569,27 +576,29 @@ void tkv_engine::forward(const Fwd& f) {
         s = gemm(attn_rows, (int)qd, w_o[l], rows, (int)hid, (int)qd);
         {
             Scope sc(this, PC_EPI, 1);
-            launch_residual_norm(x_rows, partial.as<float>(), s, rows, (int)hid, ones, eps, h.p, dt, err.as<int>(),
-                                 stream);
+            launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, ones, xb.p, ssp.as<float>(), dt,
+                            err.as<int>(), stream);
         }
-        // --- MLP block: gate|up fused into one GEMM, SwiGLU epilogue ---
-        s = gemm(h.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
+        // --- MLP block: gate|up fused into one GEMM, SwiGLU (with the folded mlp_norm scale) in its epilogue ---
+        s = gemm(xb.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
         if (s > 0) {
             Scope sc(this, PC_EPI, 1);
-            launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, dt, stream, gu_interleaved);
+            launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, ssp.as<float>(), nb, (int)hid, eps, dt, stream,
+                          gu_interleaved);
         }
         s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
         {
             // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
             Scope sc(this, PC_EPI, 1);
-            launch_residual_norm(x_rows, partial.as<float>(), s, rows, (int)hid, ones, eps, h.p, dt, err.as<int>(),
-                                 stream);
+            launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, ones, xb.p, ssp.as<float>(), dt,
+                            err.as<int>(), stream);
         }
     }
     if (f.logits) {
         // after the tail layer, h row 0 holds final_norm(x) of the last token
         Scope sc(this, PC_OTHER, 1);
-        launch_lm_head(h.p, w_lm, (int)hid, (int)V, logits.as<float>(), dt, err.as<int>(), stream);
+        launch_lm_head(xb.p, w_lm, (int)hid, (int)V, logits.as<float>(), ssp.as<float>(), nb, eps, dt, err.as<int>(),
+                       stream);
     }
 }
 

@@ -108,6 +108,9 @@ struct GemmArgs {
     uint32_t scratch_off;         // SwiGLU exchange scratch (swapped): byte offset after the ring
     float* partial;               // EPI_PARTIAL
     __nv_bfloat16* act;           // EPI_SWIGLU: [M][N/2]
+    const float* ssp;             // EPI_SWIGLU: folded RMSNorm partial sums (row_scale), nb blocks per token
+    int nb;
+    float eps;
 };
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
@@ -277,9 +280,11 @@ __global__ void __launch_bounds__(THREADS_P, 1)
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
                                 const int m = m0 + c + j;
-                                if (m < g.M && i < inter)
+                                if (m < g.M && i < inter) {
+                                    const float sc = row_scale(g.ssp, g.nb, m, g.K, g.eps);  // folded mlp_norm
                                     g.act[(int64_t)m * inter + i] = __float2bfloat16_rn(
-                                        silu(__uint_as_float(r[j])) * up[(lg * 32 + lane) * ld + c + j]);
+                                        silu(sc * __uint_as_float(r[j])) * (sc * up[(lg * 32 + lane) * ld + c + j]));
+                                }
                             }
                         }
                     }
@@ -317,10 +322,11 @@ __global__ void __launch_bounds__(THREADS_P, 1)
                         tmem_ld16(acc + (uint32_t)c, gr);
                         tmem_ld16(acc + (uint32_t)(64 + c), ur);
                         if (m < g.M) {
+                            const float sc = row_scale(g.ssp, g.nb, m, g.K, g.eps);  // folded mlp_norm
                             __align__(16) __nv_bfloat16 o[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
-                                o[j] = __float2bfloat16_rn(silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]));
+                                o[j] = __float2bfloat16_rn(silu(sc * __uint_as_float(gr[j])) * (sc * __uint_as_float(ur[j])));
                             __nv_bfloat16* dst = g.act + (int64_t)m * inter + i0 + c;
                             if (i0 + c + 16 <= inter && (inter % 8) == 0) {
                                 reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<uint4*>(o)[0];
@@ -396,7 +402,7 @@ int gemm_tc_tiles(int M, int N) {
 }
 
 int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
-                   cudaStream_t s, void* swiglu_act) {
+                   cudaStream_t s, void* swiglu_act, const float* ssp, int nb, float eps) {
     const bool swap = M <= 128;
     GemmArgs g{};
     g.M = M;
@@ -419,6 +425,10 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;
     g.partial = partial;
     g.act = (__nv_bfloat16*)swiglu_act;
+    g.ssp = ssp;
+    g.nb = nb;
+    g.eps = eps;
+    if (swiglu_act && !ssp) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the folded-norm partial sums");
     const size_t smem = 1024 + (size_t)g.scratch_off + scratch;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -72,109 +72,84 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
     return t;
 }
 
+// Block of 1024 columns of one row: 256 threads x 4. Writes x, xb = x * w and ssp[t][blockIdx.x].
 template <typename T>
-__global__ void embed_norm_kernel(const int32_t* tok, const float* emb, int hidden, int vocab, const float* w,
-                                  float eps, float* x, T* h, int* err) {
+__device__ __forceinline__ void finish_row_block(float* __restrict__ xrow, const float* __restrict__ w, T* xbrow,
+                                                 float* ssp_slot, float (&v)[4], int c0, int hidden, float* red,
+                                                 int* err) {
+    float ss = 0.f;
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int c = c0 + e;
+        if (c < hidden) {
+            xrow[c] = v[e];
+            stf(xbrow, c, v[e] * w[c]);
+            ss += v[e] * v[e];
+            bad |= !isfinite(v[e]);
+        }
+    }
+    if (bad) atomicOr(err, 2);
+    ss = block_sum(ss, red);
+    if (threadIdx.x == 0) *ssp_slot = ss;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) embed_kernel(const int32_t* tok, const float* emb, int hidden, int vocab,
+                                                    const float* w, float* x, T* xb, float* ssp, int* err) {
     pdl_launch();
     pdl_wait();
     __shared__ float red[32];
-    const int t = blockIdx.x;
+    const int t = blockIdx.y, nb = gridDim.x;
     const int id = tok[t];
     if (id < 0 || id >= vocab) {  // DomainError "token id outside vocab" (model.cpp:217-221)
         if (threadIdx.x == 0) atomicOr(err, 1);
         return;
     }
-    float ss = 0.f;
-    for (int j = threadIdx.x; j < hidden; j += blockDim.x) {
-        const float v = emb[(int64_t)id * hidden + j];
-        x[(int64_t)t * hidden + j] = v;
-        ss += v * v;
-    }
-    ss = block_sum(ss, red);
-    const float scale = 1.0f / sqrtf(ss / (float)hidden + eps);
-    for (int j = threadIdx.x; j < hidden; j += blockDim.x)
-        stf(h, (int64_t)t * hidden + j, x[(int64_t)t * hidden + j] * scale * w[j]);
+    const int c0 = blockIdx.x * 1024 + threadIdx.x * 4;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = (c0 + e < hidden) ? emb[(int64_t)id * hidden + c0 + e] : 0.f;
+    finish_row_block(x + (int64_t)t * hidden, w, xb + (int64_t)t * hidden, ssp + (int64_t)t * nb + blockIdx.x, v, c0,
+                     hidden, red, err);
 }
 
-// One CTA per row: x += sum of split-K partials, then h = rmsnorm(x) * w. float4 vectorised; the row
-// (hidden <= 8192) stays in registers between the two passes.
+// Residual add of the split-K partials (x += a . W), many CTAs per row (nb x T grid).
 template <typename T>
-__global__ void __launch_bounds__(256) residual_norm_kernel(float* x, const float* partial, int splits,
-                                                            int64_t plane, int hidden, const float* w, float eps,
-                                                            T* h, int* err) {
+__global__ void __launch_bounds__(256) residual_kernel(float* x, const float* partial, int splits, int64_t plane,
+                                                       int hidden, const float* w, T* xb, float* ssp, int* err) {
     pdl_launch();
     pdl_wait();
     __shared__ float red[32];
-    constexpr int MAXV = 8;
-    const int64_t t = blockIdx.x;
-    const int n4 = hidden >> 2;
-    float4* x4 = reinterpret_cast<float4*>(x + t * hidden);
-    float4 v[MAXV];
-    float ss = 0.f;
-    bool bad = false;
+    const int64_t t = blockIdx.y;
+    const int nb = gridDim.x;
+    const int c0 = blockIdx.x * 1024 + threadIdx.x * 4;
+    float v[4];
+    float* xrow = x + t * hidden;
+    if ((hidden & 3) == 0 && c0 + 3 < hidden) {
+        const float4 a = *reinterpret_cast<const float4*>(xrow + c0);
+        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+        for (int s = 0; s < splits; ++s) {
+            const float4 p = *reinterpret_cast<const float4*>(partial + s * plane + t * hidden + c0);
+            v[0] += p.x, v[1] += p.y, v[2] += p.z, v[3] += p.w;
+        }
+    } else {
 #pragma unroll
-    for (int u = 0; u < MAXV; ++u) {
-        const int idx = threadIdx.x + u * blockDim.x;
-        if (idx < n4) {
-            float4 a = x4[idx];
-            for (int s = 0; s < splits; ++s) {
-                const float4 p = reinterpret_cast<const float4*>(partial + s * plane + t * hidden)[idx];
-                a.x += p.x;
-                a.y += p.y;
-                a.z += p.z;
-                a.w += p.w;
+        for (int e = 0; e < 4; ++e) {
+            v[e] = 0.f;
+            if (c0 + e < hidden) {
+                float acc = xrow[c0 + e];
+                for (int s = 0; s < splits; ++s) acc += partial[s * plane + t * hidden + c0 + e];
+                v[e] = acc;
             }
-            x4[idx] = a;
-            v[u] = a;
-            ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
-            bad |= !(isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w));
         }
     }
-    if (bad) atomicOr(err, 2);
-    if (w == nullptr) return;
-    ss = block_sum(ss, red);
-    const float scale = 1.0f / sqrtf(ss / (float)hidden + eps);
-#pragma unroll
-    for (int u = 0; u < MAXV; ++u) {
-        const int idx = threadIdx.x + u * blockDim.x;
-        if (idx < n4) {
-            const float4 ww = reinterpret_cast<const float4*>(w)[idx];
-            const int64_t b = t * hidden + 4 * idx;
-            stf(h, b + 0, v[u].x * scale * ww.x);
-            stf(h, b + 1, v[u].y * scale * ww.y);
-            stf(h, b + 2, v[u].z * scale * ww.z);
-            stf(h, b + 3, v[u].w * scale * ww.w);
-        }
-    }
-}
-
-// generic fallback (hidden % 4 != 0 or hidden > 8192)
-template <typename T>
-__global__ void residual_norm_scalar_kernel(float* x, const float* partial, int splits, int64_t plane, int hidden,
-                                            const float* w, float eps, T* h, int* err) {
-    pdl_launch();
-    pdl_wait();
-    __shared__ float red[32];
-    const int64_t t = blockIdx.x;
-    float ss = 0.f;
-    bool bad = false;
-    for (int j = threadIdx.x; j < hidden; j += blockDim.x) {
-        float acc = 0.f;
-        for (int s = 0; s < splits; ++s) acc += partial[s * plane + t * hidden + j];
-        const float v = x[t * hidden + j] + acc;
-        x[t * hidden + j] = v;
-        ss += v * v;
-        bad |= !isfinite(v);
-    }
-    if (bad) atomicOr(err, 2);
-    if (w == nullptr) return;
-    ss = block_sum(ss, red);
-    const float scale = 1.0f / sqrtf(ss / (float)hidden + eps);
-    for (int j = threadIdx.x; j < hidden; j += blockDim.x) stf(h, t * hidden + j, x[t * hidden + j] * scale * w[j]);
+    finish_row_block(xrow, w, xb + t * hidden, ssp + t * nb + blockIdx.x, v, c0, hidden, red, err);
 }
 
 template <typename T>
-__global__ void swiglu_kernel(const float* partial, int splits, int T_, int inter, T* act, int interleave64) {
+__global__ void swiglu_kernel(const float* partial, int splits, int T_, int inter, T* act, const float* ssp, int nb,
+                              int hidden, float eps, int interleave64) {
     pdl_launch();
     pdl_wait();
     const int64_t n = (int64_t)T_ * inter, plane = (int64_t)T_ * 2 * inter;
@@ -187,6 +162,9 @@ __global__ void swiglu_kernel(const float* partial, int splits, int T_, int inte
             g += partial[s * plane + t * 2 * inter + gc];
             u += partial[s * plane + t * 2 * inter + uc];
         }
+        const float sc = row_scale(ssp, nb, t, hidden, eps);
+        g *= sc;
+        u *= sc;
         stf(act, o, (g / (1.0f + expf(-g))) * u);  // silu(z) = z / (1 + e^-z), numerics.cpp:103-105
     }
 }
@@ -195,7 +173,7 @@ __global__ void swiglu_kernel(const float* partial, int splits, int T_, int inte
 template <typename T>
 __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
                                     const int32_t* pos, const float2* rope, T* q, T* kc, T* vc, int row0,
-                                    StoreScatter sc, int layer) {
+                                    StoreScatter sc, int layer, const float* ssp, int nb, int hidden, float eps) {
     pdl_launch();
     pdl_wait();
     const int qd = H * d, kvd = Hkv * d, N = qd + 2 * kvd, half = d / 2;
@@ -208,6 +186,9 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
             x0 += partial[s * plane + t * N + n];
             x1 += partial[s * plane + t * N + n + 1];
         }
+        const float rs = row_scale(ssp, nb, t, hidden, eps);  // folded attn RMSNorm
+        x0 *= rs;
+        x1 *= rs;
         if (n >= qd + kvd) {  // V: copied as is
             const int c = n - qd - kvd;
             stf(vc, (int64_t)(row0 + t) * kvd + c, x0);
@@ -336,7 +317,8 @@ __global__ void gather_rope_pair_kernel(PoolTable pools, int page_tokens, const 
 }
 
 template <typename T>
-__global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, float* logits, int* err) {
+__global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, float* logits, const float* ssp, int nb,
+                               float eps, int* err) {
     pdl_launch();
     pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -345,6 +327,7 @@ __global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, fl
     for (int k = lane; k < hidden; k += 32) acc += ldf(h, k) * ldf(W, (int64_t)warp * hidden + k);
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
+        acc *= row_scale(ssp, nb, 0, hidden, eps);  // folded final_norm
         logits[warp] = acc;
         if (!isfinite(acc)) atomicOr(err, 4);  // Matrix::require_finite("logits"), model.cpp:268
     }
@@ -439,38 +422,34 @@ void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t s) {
     TKV_CUDA(cudaGetLastError());
 }
 
-void launch_embed_norm(const int32_t* tok, int T_, const float* emb, int hidden, int vocab, const float* w, float eps,
-                       float* x, void* h, DT dt, int* err, cudaStream_t s) {
-    DISPATCH_DT(dt, launch_k(embed_norm_kernel<T>, T_, 256, 0, s, tok, emb, hidden, vocab, w, eps, x, (T*)h, err));
+void launch_embed(const int32_t* tok, int T_, const float* emb, int hidden, int vocab, const float* w, float* x,
+                  void* xb, float* ssp, DT dt, int* err, cudaStream_t s) {
+    const dim3 grid(norm_blocks(hidden), T_);
+    DISPATCH_DT(dt, launch_k(embed_kernel<T>, grid, 256, 0, s, tok, emb, hidden, vocab, w, x, (T*)xb, ssp, err));
     TKV_CUDA(cudaGetLastError());
 }
 
-void launch_residual_norm(float* x, const float* partial, int splits, int T_, int hidden, const float* w, float eps,
-                          void* h, DT dt, int* err, cudaStream_t s) {
+void launch_residual(float* x, const float* partial, int splits, int T_, int hidden, const float* w, void* xb,
+                     float* ssp, DT dt, int* err, cudaStream_t s) {
     const int64_t plane = (int64_t)T_ * hidden;
-    if (hidden % 4 == 0 && hidden <= 8 * 4 * 256) {
-        DISPATCH_DT(dt, launch_k(residual_norm_kernel<T>, T_, 256, 0, s, x, partial, splits, plane, hidden, w, eps, (T*)h,
-                                                                   err));
-    } else {
-        DISPATCH_DT(dt, launch_k(residual_norm_scalar_kernel<T>, T_, 512, 0, s, x, partial, splits, plane, hidden, w, eps,
-                                                                          (T*)h, err));
-    }
+    const dim3 grid(norm_blocks(hidden), T_);
+    DISPATCH_DT(dt, launch_k(residual_kernel<T>, grid, 256, 0, s, x, partial, splits, plane, hidden, w, (T*)xb, ssp,
+                             err));
     TKV_CUDA(cudaGetLastError());
 }
 
-void launch_swiglu(const float* partial, int splits, int T_, int inter, void* act, DT dt, cudaStream_t s,
-                   bool interleave64) {
-    DISPATCH_DT(dt, launch_k(swiglu_kernel<T>, grid_for((int64_t)T_ * inter, 256), 256, 0, s, partial, splits, T_, inter,
-                                                                                         (T*)act, (int)interleave64));
+void launch_swiglu(const float* partial, int splits, int T_, int inter, void* act, const float* ssp, int nb,
+                   int hidden, float eps, DT dt, cudaStream_t s, bool interleave64) {
+    DISPATCH_DT(dt, launch_k(swiglu_kernel<T>, grid_for((int64_t)T_ * inter, 256), 256, 0, s, partial, splits, T_, inter, (T*)act, ssp, nb, hidden, eps, (int)interleave64));
     TKV_CUDA(cudaGetLastError());
 }
 
 void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hkv, int d, const int32_t* pos,
                          const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc, int layer,
-                         DT dt, cudaStream_t s) {
+                         const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s) {
     const int64_t pairs = (int64_t)T_ * (H + 2 * Hkv) * d / 2;
     DISPATCH_DT(dt, launch_k(qkv_epilogue_kernel<T>, grid_for(pairs, 256), 256, 0, s, 
-                        partial, splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer));
+                        partial, splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden, eps));
     TKV_CUDA(cudaGetLastError());
 }
 
@@ -493,11 +472,11 @@ void launch_gather_rope(const PoolTable& pools, int page_tokens, const GatherSeg
     TKV_CUDA(cudaGetLastError());
 }
 
-void launch_lm_head(const void* h, const void* W, int hidden, int vocab, float* logits, DT dt, int* err,
-                    cudaStream_t s) {
+void launch_lm_head(const void* h, const void* W, int hidden, int vocab, float* logits, const float* ssp, int nb,
+                    float eps, DT dt, int* err, cudaStream_t s) {
     const int threads = 256, warps_per_block = threads / 32;
     DISPATCH_DT(dt, launch_k(lm_head_kernel<T>, (vocab + warps_per_block - 1) / warps_per_block, threads, 0, s, 
-                        (const T*)h, (const T*)W, hidden, vocab, logits, err));
+                        (const T*)h, (const T*)W, hidden, vocab, logits, ssp, nb, eps, err));
     TKV_CUDA(cudaGetLastError());
 }
 

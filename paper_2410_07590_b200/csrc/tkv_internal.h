@@ -43,16 +43,19 @@ void launch_init_rowmajor_f32(float* dst, uint64_t seed, uint64_t base, int64_t 
                               double scale, cudaStream_t s);
 void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t s);
 
-// x[t] = emb[tok[t]] (fp32); h[t] = rmsnorm(x[t]) * w  (dtype). Errors (token outside vocab) set *err.
-void launch_embed_norm(const int32_t* tok, int T, const float* emb, int hidden, int vocab, const float* w,
-                       float eps, float* x, void* h, DT dt, int* err, cudaStream_t s);
-// x[t] += sum_s partial[s][t][:]; h[t] = rmsnorm(x[t]) * w (dtype).  x/h/partial row strides = hidden.
-void launch_residual_norm(float* x, const float* partial, int splits, int T, int hidden, const float* w,
-                          float eps, void* h, DT dt, int* err, cudaStream_t s);
-// act[t][i] = silu(sum_s P[s][t][gate(i)]) * sum_s P[s][t][up(i)]   (dtype). interleave64: gate/up columns
-// in 64-wide blocks (gate(i) = (i/64)*128 + i%64, up = gate + 64); else gate(i) = i, up(i) = I + i.
-void launch_swiglu(const float* partial, int splits, int T, int inter, void* act, DT dt, cudaStream_t s,
-                   bool interleave64 = false);
+// RMSNorm folding (see dev_common.cuh:row_scale): x rows are produced together with xb = dtype(x * w) and
+// ssp[t][b] = sum of x^2 over the b-th 1024-column block of row t; nb = norm_blocks(hidden).
+inline int norm_blocks(int hidden) { return (hidden + 1023) / 1024; }
+// x[t] = emb[tok[t]] (fp32), xb, ssp. Errors (token outside vocab) set *err.
+void launch_embed(const int32_t* tok, int T, const float* emb, int hidden, int vocab, const float* w, float* x,
+                  void* xb, float* ssp, DT dt, int* err, cudaStream_t s);
+// x[t] += sum_s partial[s][t][:] (the residual add), then xb, ssp as above. Grid = nb x T CTAs.
+void launch_residual(float* x, const float* partial, int splits, int T, int hidden, const float* w, void* xb,
+                     float* ssp, DT dt, int* err, cudaStream_t s);
+// act[t][i] = silu(s_t * sum_s P[s][t][gate(i)]) * (s_t * sum_s P[s][t][up(i)]), s_t = row_scale(ssp, t)
+// (dtype). interleave64: gate/up columns in 64-wide blocks (gate(i) = (i/64)*128 + i%64, up = gate + 64).
+void launch_swiglu(const float* partial, int splits, int T, int inter, void* act, const float* ssp, int nb,
+                   int hidden, float eps, DT dt, cudaStream_t s, bool interleave64 = false);
 
 // QKV epilogue: reduce the split-K partials of [T, (H+2Hkv)*d], rotate q and k by pos[t]
 // (interleaved pairs, cos/sin table [max_pos][d/2] of float2), write q (dtype [T, H*d]),
@@ -66,9 +69,10 @@ struct StoreScatter {
     int page_tokens = 0;
     int layer_num = 0;
 };
+// The projections were computed from xb: every output is first multiplied by row_scale(ssp, t).
 void launch_qkv_epilogue(const float* partial, int splits, int T, int H, int Hkv, int d, const int32_t* pos,
                          const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc,
-                         int layer, DT dt, cudaStream_t s);
+                         int layer, const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s);
 
 // KV gather + fused RoPE: one descriptor per (chunk page -> request rows) segment.
 struct GatherSeg {
@@ -89,9 +93,9 @@ void launch_gather_rope(const PoolTable& pools, int page_tokens, const GatherSeg
                         int kv_dim, int d, const float2* rope, void* cache, int64_t cap, int rotate, DT dt,
                         int num_sms, cudaStream_t s);
 
-// logits[v] = sum_k h[k] * W[v][k] (W dtype [vocab][hidden], h dtype), fp32 out; sets *err on non-finite.
-void launch_lm_head(const void* h, const void* W, int hidden, int vocab, float* logits, DT dt, int* err,
-                    cudaStream_t s);
+// logits[v] = row_scale(ssp, 0) * sum_k xb[k] * W[v][k] (final RMSNorm folded), fp32; *err on non-finite.
+void launch_lm_head(const void* xb, const void* W, int hidden, int vocab, float* logits, const float* ssp, int nb,
+                    float eps, DT dt, int* err, cudaStream_t s);
 // dense 0/1 view of the [lo, hi] predicate (the same __device__ predicate the attention uses)
 void launch_mask_materialize(const int32_t* lo, const int32_t* hi, int rows, int cols, uint8_t* out,
                              cudaStream_t s);
@@ -112,8 +116,10 @@ void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K
 bool gemm_tc_supported(int M, int N, int K, int lda);
 int gemm_tc_tiles(int M, int N);
 // Returns the number of split-K partial planes actually written (<= splits: every split is non-empty).
+// The SwiGLU epilogue applies the folded RMSNorm scale row_scale(ssp, token) (ssp/nb/eps: see launch_residual).
 int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
-                   cudaStream_t s, void* swiglu_act = nullptr);
+                   cudaStream_t s, void* swiglu_act = nullptr, const float* ssp = nullptr, int nb = 0,
+                   float eps = 0.f);
 
 // Flash attention, SIMT (fp32 math): q [Tq][H*d], k/v rows [Tk][Hkv*d] (stride kv_stride elements),
 // row t attends keys j with lo[t] <= j <= hi[t]. out [Tq][H*d] (dtype). ws: split-K workspace.
