@@ -260,6 +260,8 @@ __global__ void __launch_bounds__(THREADS_P, 1)
                     // tile rows 0-63 = gate, 64-127 = the matching up rows (interleaved W_gu layout)
                     float* up = reinterpret_cast<float*>(smem + g.scratch_off);  // [64][ntok+1]
                     const int ld = g.ntok + 1;
+                    float* tok_scale = up + 64 * ld;  // [ntok]: folded mlp_norm scale per token
+                    if (et < g.ntok) tok_scale[et] = m0 + et < g.M ? row_scale(g.ssp, g.nb, m0 + et, g.K, g.eps) : 0.f;
                     if (lg >= 2) {
 #pragma unroll 1
                         for (int c = 0; c < g.ntok; c += 16) {
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(THREADS_P, 1)
                             for (int j = 0; j < 16; ++j) {
                                 const int m = m0 + c + j;
                                 if (m < g.M && i < inter) {
-                                    const float sc = row_scale(g.ssp, g.nb, m, g.K, g.eps);  // folded mlp_norm
+                                    const float sc = tok_scale[c + j];
                                     g.act[(int64_t)m * inter + i] = __float2bfloat16_rn(
                                         silu(sc * __uint_as_float(r[j])) * (sc * up[(lg * 32 + lane) * ld + c + j]));
                                 }
@@ -316,13 +318,13 @@ __global__ void __launch_bounds__(THREADS_P, 1)
                 } else {
                     const int inter = g.N / 2;
                     const int i0 = nt * 64;
+                    const float sc = m < g.M ? row_scale(g.ssp, g.nb, m, g.K, g.eps) : 0.f;  // folded mlp_norm
 #pragma unroll 1
                     for (int c = 0; c < 64; c += 16) {
                         uint32_t gr[16], ur[16];
                         tmem_ld16(acc + (uint32_t)c, gr);
                         tmem_ld16(acc + (uint32_t)(64 + c), ur);
                         if (m < g.M) {
-                            const float sc = row_scale(g.ssp, g.nb, m, g.K, g.eps);  // folded mlp_norm
                             __align__(16) __nv_bfloat16 o[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
@@ -341,7 +343,6 @@ __global__ void __launch_bounds__(THREADS_P, 1)
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
-            (void)et;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -419,7 +420,8 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.acc_cols = swap ? (uint32_t)g.ntok : 128u;
     g.tmem_cols = 32;
     while (g.tmem_cols < 2 * g.acc_cols) g.tmem_cols <<= 1;
-    const uint32_t scratch = (swap && swiglu_act) ? (uint32_t)(64 * (g.ntok + 1) * 4 + 1023) / 1024 * 1024 : 0;
+    const uint32_t scratch =
+        (swap && swiglu_act) ? (uint32_t)((64 * (g.ntok + 1) + g.ntok) * 4 + 1023) / 1024 * 1024 : 0;
     g.stages = (int)std::min<uint32_t>(8, (SMEM_BUDGET - scratch) / (TILE_W + g.a_bytes));
     g.scratch_off = (uint32_t)g.stages * (TILE_W + g.a_bytes) + 256;  // after the ring and its barriers
     g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;

@@ -178,15 +178,20 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
     pdl_wait();
     const int qd = H * d, kvd = Hkv * d, N = qd + 2 * kvd, half = d / 2;
     const int64_t pairs = (int64_t)T_ * (N / 2), plane = (int64_t)T_ * N;
+    int64_t cached_t = -1;
+    float rs = 0.f;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = p / (N / 2);
+        if (t != cached_t) {  // folded attn RMSNorm scale, once per token per thread
+            rs = row_scale(ssp, nb, t, hidden, eps);
+            cached_t = t;
+        }
         const int n = 2 * (int)(p - t * (N / 2));
         float x0 = 0.f, x1 = 0.f;
         for (int s = 0; s < splits; ++s) {
             x0 += partial[s * plane + t * N + n];
             x1 += partial[s * plane + t * N + n + 1];
         }
-        const float rs = row_scale(ssp, nb, t, hidden, eps);  // folded attn RMSNorm
         x0 *= rs;
         x1 *= rs;
         if (n >= qd + kvd) {  // V: copied as is
