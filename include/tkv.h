@@ -233,6 +233,11 @@ tkv_status tkv_debug_set_mask_fault(tkv_engine* eng, int64_t row, int64_t col);
  * (tcgen05 for bf16 head_size 128), 1 = SIMT. */
 tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* A, const float* W, int64_t M,
                           int64_t N, int64_t K, int splits, float* out);
+/* GEMM tuning/timing (tools/gemm_sweep.py): knobs = ring stages, smem budget KB, CTAs per SM, weight
+ * stream L2 evict_first (0 = default for the first three). bench: device-resident buffers, mean ms. */
+tkv_status tkv_debug_set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first);
+tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int splits, int swiglu, int iters,
+                                double* ms_per_launch);
 tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const float* q, const float* k,
                                const float* v, const int32_t* lo, const int32_t* hi, int64_t Tq, int64_t Tk,
                                int64_t H, int64_t Hkv, int64_t d, float* out);

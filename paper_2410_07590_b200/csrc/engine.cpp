@@ -1838,6 +1838,54 @@ tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* 
     });
 }
 
+tkv_status tkv_debug_set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first) {
+    return guard([&] { set_gemm_knobs(stages, smem_kb, ctas_per_sm, w_evict_first); });
+}
+
+// Device-resident GEMM timing: buffers filled on the device (no host copies), `iters` back-to-back
+// launches timed with CUDA events; returns the mean ms per launch.
+tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int splits, int swiglu, int iters,
+                                double* ms_per_launch) {
+    return guard([&] {
+        DebugDev dd(device);
+        DevMem a, w, part, act, ssp;
+        a.ensure((size_t)M * K * 2);
+        w.ensure((size_t)N * K * 2);
+        launch_init_transposed(a.p, DT::BF16, 1, 0, K, M, 0.01, 0);
+        launch_init_transposed(w.p, DT::BF16, 2, 0, K, N, 0.01, 0);
+        const int nb = norm_blocks((int)K);
+        ssp.ensure((size_t)M * nb * 4);
+        launch_fill_f32(ssp.as<float>(), 1.0f, M * nb, 0);
+        if (splits < 1) splits = 1;
+        part.ensure((size_t)splits * M * N * 4);
+        act.ensure((size_t)M * (N / 2) * 2);
+        cudaStream_t st;
+        TKV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        TKV_CUDA(cudaDeviceSynchronize());
+        auto run = [&] {
+            if (swiglu)
+                launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, nullptr, 1, st, act.p, ssp.as<float>(), nb,
+                               1e-6f);
+            else
+                launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, part.as<float>(), splits, st);
+        };
+        for (int i = 0; i < 3; ++i) run();
+        cudaEvent_t e0, e1;
+        TKV_CUDA(cudaEventCreate(&e0));
+        TKV_CUDA(cudaEventCreate(&e1));
+        TKV_CUDA(cudaEventRecord(e0, st));
+        for (int i = 0; i < iters; ++i) run();
+        TKV_CUDA(cudaEventRecord(e1, st));
+        TKV_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        TKV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        *ms_per_launch = ms / iters;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
+    });
+}
+
 tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const float* q, const float* k, const float* v,
                                const int32_t* lo, const int32_t* hi, int64_t Tq, int64_t Tk, int64_t H, int64_t Hkv,
                                int64_t d, float* out) {

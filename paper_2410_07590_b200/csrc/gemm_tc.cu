@@ -35,6 +35,13 @@ constexpr int BK = 64, THREADS = 128;
 constexpr uint32_t TILE_W = 128 * BK * 2;  // 16 KB: 128 rows x 64 k, bf16
 constexpr int SMEM_BUDGET = 200 * 1024;
 
+// Tuning knobs (tkv_debug_set_gemm_knobs; 0 = default): ring depth, smem budget (KB), CTAs per SM,
+// L2 eviction policy of the weight stream (1 = evict_first).
+struct Knobs {
+    int stages = 0, smem_kb = 0, ctas_per_sm = 0, w_evict_first = 1;
+};
+Knobs g_knobs;
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -66,6 +73,21 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// Same with an L2 cache-policy hint (weights are streamed once: evict_first keeps L2 for activations/KV).
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 // UMMA smem descriptor, K-major SWIZZLE_128B: 128 B rows, 8-row atoms 1024 B apart (SBO), version 1.
 __device__ __forceinline__ uint64_t desc_k(uint32_t saddr) {
     return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
@@ -111,6 +133,7 @@ struct GemmArgs {
     const float* ssp;             // EPI_SWIGLU: folded RMSNorm partial sums (row_scale), nb blocks per token
     int nb;
     float eps;
+    int w_evict_first;
 };
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
@@ -128,7 +151,7 @@ __device__ __forceinline__ void unit_coords(const GemmArgs& g, int u, int& nt, i
 // flows across units without draining; two TMEM accumulators let the epilogue of unit i overlap the
 // mainloop of unit i+1.
 template <bool SWAP, int EPI>
-__global__ void __launch_bounds__(THREADS_P, 1)
+__global__ void __launch_bounds__(THREADS_P)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, GemmArgs g) {
     pdl_launch();
     extern __shared__ uint8_t smem_raw[];
@@ -167,6 +190,13 @@ __global__ void __launch_bounds__(THREADS_P, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer ----------------
+            const uint64_t wpol = policy_evict_first();
+            auto load_w = [&](void* dst, uint64_t* bar, int c0, int c1) {
+                if (g.w_evict_first)
+                    tma_load_2d_hint(dst, &tmW, bar, c0, c1, wpol);
+                else
+                    tma_load_2d(dst, &tmW, bar, c0, c1);
+            };
             // Weight tiles do not depend on earlier kernels: fill the ring with the first unit's weights
             // BEFORE waiting on the previous grid (PDL), so the weight stream overlaps its tail.
             int nt, mt, z;
@@ -176,7 +206,7 @@ __global__ void __launch_bounds__(THREADS_P, 1)
             const int pre = min(nkb0, g.stages);
             for (int i = 0; i < pre; ++i) {
                 mbar_expect_tx(&full[i], stage_bytes);
-                tma_load_2d(smem + i * stage_bytes, &tmW, &full[i], (kb0 + i) * BK, nt * 128);
+                load_w(smem + i * stage_bytes, &full[i], (kb0 + i) * BK, nt * 128);
             }
             pdl_wait();
             for (int i = 0; i < pre; ++i)
@@ -190,7 +220,7 @@ __global__ void __launch_bounds__(THREADS_P, 1)
                     mbar_wait(&empty[s], ((uint32_t)(it / g.stages) & 1u) ^ 1u);
                     uint8_t* w = smem + s * stage_bytes;
                     mbar_expect_tx(&full[s], stage_bytes);
-                    tma_load_2d(w, &tmW, &full[s], (k0 + i) * BK, nt * 128);
+                    load_w(w, &full[s], (k0 + i) * BK, nt * 128);
                     tma_load_2d(w + TILE_W, &tmA, &full[s], (k0 + i) * BK, mt * mstep);
                 }
             }
@@ -422,7 +452,11 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     while (g.tmem_cols < 2 * g.acc_cols) g.tmem_cols <<= 1;
     const uint32_t scratch =
         (swap && swiglu_act) ? (uint32_t)((64 * (g.ntok + 1) + g.ntok) * 4 + 1023) / 1024 * 1024 : 0;
-    g.stages = (int)std::min<uint32_t>(8, (SMEM_BUDGET - scratch) / (TILE_W + g.a_bytes));
+    const int budget = (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET);
+    g.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
+                                       (uint32_t)(budget - (int)scratch) / (TILE_W + g.a_bytes));
+    if (g.stages < 2) fail(TKV_ERR_CONFIG, "GEMM smem budget too small");
+    g.w_evict_first = g_knobs.w_evict_first;
     g.scratch_off = (uint32_t)g.stages * (TILE_W + g.a_bytes) + 256;  // after the ring and its barriers
     g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;
     g.partial = partial;
@@ -435,7 +469,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min(g.units, sms);
+    const int grid = std::min(g.units, sms * std::max(1, g_knobs.ctas_per_sm));
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
     const CUtensorMap tw = make_map(W, N, K, K, 128);
     if (swiglu_act) {
@@ -445,6 +479,13 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
         swap ? launch_t<true, EPI_PARTIAL>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_PARTIAL>(ta, tw, g, grid, smem, s);
     }
     return eff_splits;
+}
+
+void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first) {
+    g_knobs.stages = stages;
+    g_knobs.smem_kb = smem_kb;
+    g_knobs.ctas_per_sm = ctas_per_sm;
+    g_knobs.w_evict_first = w_evict_first;
 }
 
 }  // namespace tkv
