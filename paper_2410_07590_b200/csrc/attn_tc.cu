@@ -117,6 +117,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
+// Bulk L2 prefetch (no smem destination): warms the NEXT projections' weights while attention runs.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -140,7 +144,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                    const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ lo,
                    const int32_t* __restrict__ hi, __nv_bfloat16* __restrict__ out, float* __restrict__ ws_o,
-                   float* __restrict__ ws_ml, int Tq, int Tk, int H, int Hkv, int splits, float scale, int* err) {
+                   float* __restrict__ ws_ml, int Tq, int Tk, int H, int Hkv, int splits, float scale, int* err,
+                   L2Prefetch pf) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
@@ -229,6 +234,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
 
     if (warp == SOFTMAX_WARPS) {
+        if (lane == 1) {  // idle lane: this CTA's share of the next projections' weights -> L2
+            const int ncta = gridDim.x * gridDim.y * gridDim.z;
+            const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+            for (int r = 0; r < 2; ++r) {
+                const size_t total = pf.bytes[r] & ~size_t(15);
+                if (!pf.ptr[r] || total == 0) continue;
+                const size_t share = ((total + ncta - 1) / ncta + 15) & ~size_t(15);
+                const size_t b0 = (size_t)cta * share, b1 = b0 + share < total ? b0 + share : total;
+                for (size_t off = b0; off < b1; off += 32768)
+                    prefetch_l2(static_cast<const uint8_t*>(pf.ptr[r]) + off,
+                                (uint32_t)((b1 - off) < 32768 ? (b1 - off) : 32768));
+            }
+        }
         if (lane == 0) {  // ---------------- TMA producer ----------------
             for (int j = 0; j < n; ++j) {
                 const int s = j & 1;
@@ -449,7 +467,7 @@ int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms) {
 
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
-                         int* err, cudaStream_t s) {
+                         int* err, cudaStream_t s, const L2Prefetch& pf) {
     TKV_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
     const CUtensorMap tk = kv_map(k, Tk, kv_stride, kv_stride);
     const CUtensorMap tv = kv_map(v, Tk, kv_stride, kv_stride);
@@ -457,7 +475,7 @@ void launch_attention_tc(const void* q, const void* k, const void* v, int kv_str
     dim3 grid((Tq * group + BR - 1) / BR, Hkv, splits);
     const float scale = (float)(1.0 / sqrt((double)D));
     launch_k(attn_tc_kernel, grid, THREADS, SMEM_BYTES, s, tk, tv, (const __nv_bfloat16*)q, lo, hi, (__nv_bfloat16*)out,
-                                                     ws.o, ws.ml, Tq, Tk, H, Hkv, splits, scale, err);
+                                                     ws.o, ws.ml, Tq, Tk, H, Hkv, splits, scale, err, pf);
     TKV_CUDA(cudaGetLastError());
     if (splits > 1) launch_attention_combine(ws, Tq * H, D, splits, out, err, DT::BF16, s);
 }

@@ -564,8 +564,22 @@ void tkv_engine::forward(const Fwd& f) {
             Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);
             const void* qrows = static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es;
             if (tc)
+            {
+                // Small-token forwards are weight-bound and HBM idles during attention: warm L2 with this
+                // layer's O-proj weights and the next layer's QKV weights (59 MB at Qwen2-7B shape).
+                L2Prefetch pf;
+                if (T <= 128 && !(opts.flags & TKV_FLAG_NO_L2_PREFETCH)) {
+                    pf.ptr[0] = w_o[l];
+                    pf.bytes[0] = (size_t)hid * qd * es;
+                    if (l + 1 < L) {
+                        pf.ptr[1] = w_qkv[l + 1];
+                        pf.bytes[1] = (size_t)nqkv * hid * es;
+                    }
+                }
                 launch_attention_tc(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
-                                    f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream);
+                                    f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream,
+                                    pf);
+            }
             else
                 launch_attention_simt(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
                                       f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, (int)d, splits, ws,

@@ -38,7 +38,7 @@ constexpr int SMEM_BUDGET = 200 * 1024;
 // Tuning knobs (tkv_debug_set_gemm_knobs; 0 = default): ring depth, smem budget (KB), CTAs per SM,
 // L2 eviction policy of the weight stream (1 = evict_first).
 struct Knobs {
-    int stages = 0, smem_kb = 0, ctas_per_sm = 0, w_evict_first = 1;
+    int stages = 0, smem_kb = 110, ctas_per_sm = 2, w_evict_first = 1;  // measured best (tools/gemm_sweep.py)
 };
 Knobs g_knobs;
 
@@ -482,9 +482,10 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
 }
 
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first) {
+    const Knobs d;
     g_knobs.stages = stages;
-    g_knobs.smem_kb = smem_kb;
-    g_knobs.ctas_per_sm = ctas_per_sm;
+    g_knobs.smem_kb = smem_kb > 0 ? smem_kb : d.smem_kb;
+    g_knobs.ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : d.ctas_per_sm;
     g_knobs.w_evict_first = w_evict_first;
 }
 

@@ -135,12 +135,17 @@ void launch_attention_simt(const void* q, const void* k, const void* v, int kv_s
                            const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int d, int splits,
                            const AttnWork& ws, int* err, DT dt, cudaStream_t s);
 
+// Up to two global regions the attention kernel prefetches into L2 (bulk prefetch from an idle lane).
+struct L2Prefetch {
+    const void* ptr[2] = {nullptr, nullptr};
+    size_t bytes[2] = {0, 0};
+};
 // tcgen05/TMEM/TMA attention (attn_tc.cu): head_size 128, bf16. Same predicate and workspace as SIMT.
 bool attention_tc_supported(int d, DT dt);
 int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms);
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
-                         int* err, cudaStream_t s);
+                         int* err, cudaStream_t s, const L2Prefetch& pf = L2Prefetch());
 // merge split-K (O, m, l) partials into out (dtype)
 void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, void* out, int* err, DT dt,
                               cudaStream_t s);
