@@ -82,7 +82,7 @@ typedef struct {
 #define TKV_FLAG_SIMT_ATTN 0x2    /* bf16: use the SIMT attention instead of tcgen05              */
 #define TKV_FLAG_NO_GRAPHS 0x4    /* do not capture prefill launch chains into CUDA graphs        */
 #define TKV_FLAG_NO_PDL 0x8       /* launch kernels without programmatic dependent launch          */
-#define TKV_FLAG_NO_L2_PREFETCH 0x10 /* do not warm L2 with the next projections during attention  */
+#define TKV_FLAG_L2_PREFETCH 0x10  /* warm L2 with the next projections during attention (measured: no gain) */
 
 /* IngestStats (pipeline.hpp:35-39) */
 typedef struct {
@@ -236,6 +236,8 @@ tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* 
                           int64_t N, int64_t K, int splits, float* out);
 /* GEMM tuning/timing (tools/gemm_sweep.py): knobs = ring stages, smem budget KB, CTAs per SM, weight
  * stream L2 evict_first (0 = default for the first three). bench: device-resident buffers, mean ms. */
+/* attention pipeline timeline of CTA (0,0,0): on=1 arms it; out != NULL reads [32 tiles][10 events] clock64 */
+tkv_status tkv_debug_attn_trace(int on, uint64_t* out, int64_t capacity);
 tkv_status tkv_debug_set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first);
 tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int splits, int swiglu, int iters,
                                 double* ms_per_launch);

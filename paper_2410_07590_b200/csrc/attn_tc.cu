@@ -121,6 +121,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+// Debug timeline (tkv_debug_attn_trace): CTA (0,0,0) stamps clock64 at pipeline events, slot [j][e].
+__device__ unsigned long long* g_attn_trace = nullptr;
+constexpr int TRACE_EV = 10, TRACE_TILES = 32;
+__device__ __forceinline__ void trace(int j, int e) {
+    if (g_attn_trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < TRACE_TILES) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+        g_attn_trace[j * TRACE_EV + e] = t;
+    }
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -253,11 +263,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t par = ((j >> 1) & 1) ^ 1;
                 const int key = ks + j * BK;
                 mbar_wait(&k_empty[s], par);
+                trace(j, 7);
                 mbar_expect_tx(&k_full[s], KSTAGE);
                 const uint32_t kd = sbase + OFF_K + s * KSTAGE;
                 tma_load_2d(kd, &tmK, &k_full[s], g * D, key);
                 tma_load_2d(kd + SUB, &tmK, &k_full[s], g * D + 64, key);
                 mbar_wait(&v_empty[s], par);
+                trace(j, 8);
                 mbar_expect_tx(&v_full[s], KSTAGE);
                 const uint32_t vd = sbase + OFF_V + s * KSTAGE;
                 tma_load_2d(vd, &tmV, &v_full[s], g * D, key);
@@ -278,12 +290,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 umma_commit(&s_full[s]);
                 umma_commit(&k_empty[s]);
+                trace(j, 6);
             };
             if (n > 0) issue_s(0);
             if (n > 1) issue_s(1);
             for (int j = 0; j < n; ++j) {
                 const int s = j & 1;
                 mbar_wait(p_full, j & 1);
+                trace(j, 4);
                 mbar_wait(&v_full[s], (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t vb = sbase + OFF_V + s * KSTAGE;
@@ -294,6 +308,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 umma_commit(o_full);
                 umma_commit(&v_empty[s]);
+                trace(j, 5);
                 if (j + 2 < n) issue_s(j + 2);
             }
         }
@@ -311,6 +326,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const bool full = key0 >= my_lo && key0 + CPT - 1 <= my_hi;
             const int clo = my_lo - key0, chi = my_hi - key0;
             mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            if (tid == 0) trace(j, 0);
             tc_fence_after();
             uint32_t v[CPT];
             tmem_ld32(tmem + lane_base + (uint32_t)((j & 1) * 128) + col0, v);
@@ -328,11 +344,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
 #pragma unroll
             for (int k = 1; k < NQ; ++k) mx = fmaxf(mx, xmax[j & 1][(qtr + k) & (NQ - 1)][r]);
+            if (tid == 0) trace(j, 1);
             mx = mx == -INFINITY ? -INFINITY : mx * sl2;
             const float m_new = fmaxf(m, mx);
             const float alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
             if (j > 0) {  // fold in O tile j-1 (after it lands, the P buffer is free again)
                 mbar_wait(o_full, (j - 1) & 1);
+                if (tid == 0) trace(j, 2);
                 tc_fence_after();
 #pragma unroll
                 for (int hh = 0; hh < CPT / 16; ++hh) {  // 16 columns at a time keeps register pressure down
@@ -369,6 +387,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             fence_async_smem();
             tc_fence_before();
             mbar_arrive(p_full);
+            if (tid == 0) trace(j, 3);
         }
         if (n > 0) {
             mbar_wait(o_full, (n - 1) & 1);
@@ -452,6 +471,17 @@ CUtensorMap kv_map(const void* base, int rows, int cols, int ld) {
 }
 
 }  // namespace
+
+void attn_trace_enable(bool on, unsigned long long** host_view) {
+    static unsigned long long* buf = nullptr;
+    if (on && !buf) {
+        TKV_CUDA(cudaMalloc(&buf, TRACE_EV * TRACE_TILES * 8));
+        TKV_CUDA(cudaMemset(buf, 0, TRACE_EV * TRACE_TILES * 8));
+    }
+    unsigned long long* v = on ? buf : nullptr;
+    TKV_CUDA(cudaMemcpyToSymbol(g_attn_trace, &v, sizeof v));
+    if (host_view) *host_view = buf;
+}
 
 bool attention_tc_supported(int d, DT dt) { return d == 128 && dt == DT::BF16; }
 

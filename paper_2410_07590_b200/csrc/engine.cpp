@@ -568,7 +568,7 @@ void tkv_engine::forward(const Fwd& f) {
                 // Small-token forwards are weight-bound and HBM idles during attention: warm L2 with this
                 // layer's O-proj weights and the next layer's QKV weights (59 MB at Qwen2-7B shape).
                 L2Prefetch pf;
-                if (T <= 128 && !(opts.flags & TKV_FLAG_NO_L2_PREFETCH)) {
+                if (T <= 128 && (opts.flags & TKV_FLAG_L2_PREFETCH)) {
                     pf.ptr[0] = w_o[l];
                     pf.bytes[0] = (size_t)hid * qd * es;
                     if (l + 1 < L) {
@@ -1849,6 +1849,18 @@ tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* 
         launch_reduce_splits(part.as<float>(), splits, M * N, o.as<float>(), 0);
         TKV_CUDA(cudaDeviceSynchronize());
         TKV_CUDA(cudaMemcpy(out, o.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+tkv_status tkv_debug_attn_trace(int on, uint64_t* out, int64_t capacity) {
+    return guard([&] {
+        unsigned long long* buf = nullptr;
+        if (out) {  // read back the last trace
+            attn_trace_enable(true, &buf);
+            TKV_CUDA(cudaDeviceSynchronize());
+            TKV_CUDA(cudaMemcpy(out, buf, (size_t)std::min<int64_t>(capacity, 320) * 8, cudaMemcpyDeviceToHost));
+        }
+        attn_trace_enable(on != 0, &buf);
     });
 }
 

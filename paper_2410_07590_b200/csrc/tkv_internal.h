@@ -142,6 +142,7 @@ struct L2Prefetch {
 };
 // tcgen05/TMEM/TMA attention (attn_tc.cu): head_size 128, bf16. Same predicate and workspace as SIMT.
 bool attention_tc_supported(int d, DT dt);
+void attn_trace_enable(bool on, unsigned long long** device_buf);  // debug timeline of CTA (0,0,0)
 int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms);
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
