@@ -140,18 +140,6 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// 2^x on the FMA pipe (Cody-Waite split + degree-3 minimax, max rel err 8.8e-5 — far below the bf16 rounding
-// of P): balances the softmax between MUFU.EX2 (16/clk/SM on B200) and the FMA pipe (128/clk/SM).
-__device__ __forceinline__ float ex2_poly(float x) {
-    const float xc = fmaxf(x, -126.0f);
-    const float xi = floorf(xc);
-    const float f = xc - xi;
-    float p = fmaf(f, 0.077119089663028717041015625f, 0.227564394474029541015625f);
-    p = fmaf(f, p, 0.695146143436431884765625f);
-    p = fmaf(f, p, 1.0f);
-    const float r = __int_as_float(__float_as_int(p) + ((int)xi << 23));
-    return x < -126.0f ? 0.0f : r;
-}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -380,11 +368,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t pk[CPT / 2];
 #pragma unroll
             for (int i = 0; i < CPT; i += 2) {
-                const float a0 = fmaf(__uint_as_float(v[i]), sl2, -moff);
-                const float a1 = fmaf(__uint_as_float(v[i + 1]), sl2, -moff);
-                const bool fma_pipe = (i & 2) != 0;  // half the pairs on the FMA pipe, half on MUFU
-                const float p0 = fma_pipe ? ex2_poly(a0) : ex2(a0);
-                const float p1 = fma_pipe ? ex2_poly(a1) : ex2(a1);
+                const float p0 = ex2(fmaf(__uint_as_float(v[i]), sl2, -moff));
+                const float p1 = ex2(fmaf(__uint_as_float(v[i + 1]), sl2, -moff));
                 rs4[(i >> 1) & 3] += p0 + p1;
                 pk[i >> 1] = pack_bf16(p0, p1);
             }
