@@ -6,6 +6,9 @@
 // GQA packing: a CTA owns 128 rows of ONE kv head g, row r = (token t, head g*group + r%group), so the
 // K/V tiles it streams serve all `group` query heads (C2: 64 tokens x 7 heads = 448 rows = 3.5 tiles).
 //
+// v3: O accumulates in TMEM across KV tiles (FA4-style lazy rescale only when a row max grows by > 2^8), P is
+// double-buffered in TMEM and fed to the PV MMA as the A operand (tcgen05.mma with A in TMEM), so the softmax
+// of tile j+1 overlaps PV_j on the tensor pipe.
 // Per CTA (576 threads): warps 0-15 = softmax (four threads per row: warps w, w+4, w+8, w+12 share TMEM
 // lanes 32(w%4).., each owns 32 of the S columns and 32 of the O columns; partial row maxima are
 // exchanged through shared memory), warp 16 = TMA producer, warp 17 = MMA issuer. smem: Q [128x128] and P [128x128] (two 64-column SW128 sub-tiles each, 32 KB), two K/V stages
@@ -34,11 +37,14 @@ constexpr int NQ = 4;                       // softmax threads per row
 constexpr int CPT = 128 / NQ;               // S / O columns per softmax thread
 constexpr int SOFTMAX_WARPS = 4 * NQ, THREADS = SOFTMAX_WARPS * 32 + 64;
 constexpr uint32_t SUB = 128 * 64 * 2;          // one [128 rows][64 cols] bf16 SW128 sub-tile = 16 KB
-constexpr uint32_t OFF_Q = 0, OFF_P = 2 * SUB;  // 32 KB each
-constexpr uint32_t OFF_K = 4 * SUB;             // K ring: 2 stages x 32 KB
-constexpr uint32_t OFF_V = 8 * SUB;             // V ring: 2 stages x 32 KB (separate ring: K_{j+2} loads once
+constexpr uint32_t OFF_Q = 0;                   // Q tile: 32 KB
+constexpr uint32_t OFF_K = 2 * SUB;             // K ring: 2 stages x 32 KB
+constexpr uint32_t OFF_V = 6 * SUB;             // V ring: 2 stages x 32 KB (separate ring: K_{j+2} loads once
 constexpr uint32_t KSTAGE = 2 * SUB;            //   S_j is done, without waiting for PV_j)
-constexpr uint32_t OFF_BAR = 12 * SUB;
+constexpr uint32_t OFF_BAR = 10 * SUB;
+// TMEM columns: S double buffer (fp32), O accumulator (fp32), P double buffer (bf16 pairs: 128 keys -> 64 cols)
+constexpr uint32_t TM_S = 0, TM_O = 256, TM_P = 384;
+constexpr float RESCALE_LOG2 = 8.0f;  // lazy O rescale: only when a row max grows by more than 2^8
 constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float LOG2E = 1.4426950408889634f;
@@ -150,6 +156,32 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                    const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ lo,
@@ -164,10 +196,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* k_empty = bars + 2;   // [2]
     uint64_t* v_full = bars + 4;    // [2]
     uint64_t* v_empty = bars + 6;   // [2]
-    uint64_t* s_full = bars + 8;    // [2]
-    uint64_t* p_full = bars + 10;
-    uint64_t* o_full = bars + 11;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* s_full = bars + 8;    // [2] S_j in TMEM
+    uint64_t* p_full = bars + 10;   // [2] P_j in TMEM (all softmax threads arrived)
+    uint64_t* pv_done = bars + 12;  // [2] PV_j retired: P buffer j&1 free, O current through j
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
     __shared__ int red_lo[THREADS / 32], red_hi[THREADS / 32];
     __shared__ float xmax[2][NQ][BR];  // [tile parity][quarter][row]: partial row maxima exchanged each tile
 
@@ -203,9 +235,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&v_full[s], 1);
             mbar_init(&v_empty[s], 1);
             mbar_init(&s_full[s], 1);
+            mbar_init(&p_full[s], SOFTMAX_WARPS * 32);
+            mbar_init(&pv_done[s], 1);
         }
-        mbar_init(p_full, SOFTMAX_WARPS * 32);
-        mbar_init(o_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -221,8 +253,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < CH; ++c) {
             const uint4 v = active ? src[c] : make_uint4(0, 0, 0, 0);
             const int chunk = qtr * CH + c;  // 0..15 over the 128 columns
-            const uint32_t a = sbase + OFF_Q + (chunk >> 3) * SUB + swz(r, chunk & 7);
-            sts128(a, v.x, v.y, v.z, v.w);
+            sts128(sbase + OFF_Q + (chunk >> 3) * SUB + swz(r, chunk & 7), v.x, v.y, v.z, v.w);
         }
         fence_async_smem();
     }
@@ -244,16 +275,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
 
     if (warp == SOFTMAX_WARPS) {
-        if (lane == 1) {  // idle lane: this CTA's share of the next projections' weights -> L2
+        if (lane == 1) {  // idle lane: optional L2 warm-up of the next projections' weights
             const int ncta = gridDim.x * gridDim.y * gridDim.z;
             const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-            for (int r = 0; r < 2; ++r) {
-                const size_t total = pf.bytes[r] & ~size_t(15);
-                if (!pf.ptr[r] || total == 0) continue;
+            for (int rr = 0; rr < 2; ++rr) {
+                const size_t total = pf.bytes[rr] & ~size_t(15);
+                if (!pf.ptr[rr] || total == 0) continue;
                 const size_t share = ((total + ncta - 1) / ncta + 15) & ~size_t(15);
                 const size_t b0 = (size_t)cta * share, b1 = b0 + share < total ? b0 + share : total;
                 for (size_t off = b0; off < b1; off += 32768)
-                    prefetch_l2(static_cast<const uint8_t*>(pf.ptr[r]) + off,
+                    prefetch_l2(static_cast<const uint8_t*>(pf.ptr[rr]) + off,
                                 (uint32_t)((b1 - off) < 32768 ? (b1 - off) : 32768));
             }
         }
@@ -286,7 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
-                    umma(tmem + s * 128, desc_k(sbase + OFF_Q + off), desc_k(kb + off), IDESC_S, kk > 0);
+                    umma(tmem + TM_S + s * 128, desc_k(sbase + OFF_Q + off), desc_k(kb + off), IDESC_S, kk > 0);
                 }
                 umma_commit(&s_full[s]);
                 umma_commit(&k_empty[s]);
@@ -296,31 +327,27 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (n > 1) issue_s(1);
             for (int j = 0; j < n; ++j) {
                 const int s = j & 1;
-                mbar_wait(p_full, j & 1);
+                mbar_wait(&p_full[s], (j >> 1) & 1);
                 trace(j, 4);
                 mbar_wait(&v_full[s], (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t vb = sbase + OFF_V + s * KSTAGE;
+                // O += P_j . V_j : A = P_j from TMEM (8 columns = 16 keys per MMA), B = V (MN-major)
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t aoff = (kk >> 2) * SUB + (kk & 3) * 32;
-                    umma(tmem + 256, desc_k(sbase + OFF_P + aoff), desc_mn(vb + kk * 2048), IDESC_PV, kk > 0);
-                }
-                umma_commit(o_full);
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_ts(tmem + TM_O, tmem + TM_P + s * 64 + kk * 8, desc_mn(vb + kk * 2048), IDESC_PV,
+                            (j > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&pv_done[s]);
                 umma_commit(&v_empty[s]);
                 trace(j, 5);
                 if (j + 2 < n) issue_s(j + 2);
             }
         }
     } else {
-        // ---------------- softmax: NQ threads per row, CPT S / CPT O columns each ----------------
+        // ---------------- softmax: NQ threads per row, CPT columns each; O stays in TMEM ----------------
         const float sl2 = scale * LOG2E;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t col0 = (uint32_t)(qtr * CPT);
-        float o[CPT];
-#pragma unroll
-        for (int i = 0; i < CPT; ++i) o[i] = 0.f;
-        float m = -INFINITY, l = 0.f;
+        float m_used = -INFINITY, l = 0.f;  // running max actually used for exp2, row-sum share
         for (int j = 0; j < n; ++j) {
             const int key0 = ks + j * BK + qtr * CPT;  // first key of this thread's columns
             const bool full = key0 >= my_lo && key0 + CPT - 1 <= my_hi;
@@ -329,9 +356,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (tid == 0) trace(j, 0);
             tc_fence_after();
             uint32_t v[CPT];
-            tmem_ld32(tmem + lane_base + (uint32_t)((j & 1) * 128) + col0, v);
+            tmem_ld32(tmem + lane_base + TM_S + (uint32_t)((j & 1) * 128) + qtr * CPT, v);
             tmem_wait_ld();
-            if (!full) {  // masked columns -> -inf (branch is per tile, uniform inside the common case)
+            if (!full) {  // masked columns -> -inf (per-tile branch; uniform in the common case)
 #pragma unroll
                 for (int i = 0; i < CPT; ++i)
                     v[i] = (i >= clo && i <= chi) ? v[i] : __float_as_uint(-INFINITY);
@@ -346,24 +373,28 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int k = 1; k < NQ; ++k) mx = fmaxf(mx, xmax[j & 1][(qtr + k) & (NQ - 1)][r]);
             if (tid == 0) trace(j, 1);
             mx = mx == -INFINITY ? -INFINITY : mx * sl2;
-            const float m_new = fmaxf(m, mx);
-            const float alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
-            if (j > 0) {  // fold in O tile j-1 (after it lands, the P buffer is free again)
-                mbar_wait(o_full, (j - 1) & 1);
-                if (tid == 0) trace(j, 2);
+            if (m_used == -INFINITY) {
+                m_used = mx;  // first visible keys: O is still all zeros, nothing to rescale
+            } else if (mx > m_used + RESCALE_LOG2) {
+                // rare: the row max grew by more than 2^8 -> rescale O (in TMEM) and l to the new max.
+                // All four threads of the row take this branch together (same mx, same m_used).
+                mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);  // O current through PV_{j-1}
                 tc_fence_after();
+                const float alpha = ex2(m_used - mx);
+                uint32_t w[CPT];
+                tmem_ld32(tmem + lane_base + TM_O + qtr * CPT, w);
+                tmem_wait_ld();
 #pragma unroll
-                for (int hh = 0; hh < CPT / 16; ++hh) {  // 16 columns at a time keeps register pressure down
-                    uint32_t w[16];
-                    tmem_ld16(tmem + lane_base + 256 + col0 + hh * 16, w);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) o[hh * 16 + i] += __uint_as_float(w[i]);
-                }
+                for (int i = 0; i < CPT; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
+                tmem_st32(tmem + lane_base + TM_O + qtr * CPT, w);
+                tmem_wait_st();
+                l *= alpha;
+                m_used = mx;
             }
-            // p = exp2(s*scale*log2e - m); masked entries hold -inf -> ex2 -> 0; a row with nothing visible
-            // yet (m_new = -inf) uses offset 0 so every p is exactly 0.
-            const float moff = m_new == -INFINITY ? 0.f : m_new;
+            if (tid == 0) trace(j, 2);
+            // P buffer j&1 is free once PV_{j-2} retired
+            if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
+            const float moff = m_used == -INFINITY ? 0.f : m_used;  // nothing visible yet -> all p = 0
             float rs4[4] = {0.f, 0.f, 0.f, 0.f};
             uint32_t pk[CPT / 2];
 #pragma unroll
@@ -373,32 +404,29 @@ __global__ void __launch_bounds__(THREADS, 1)
                 rs4[(i >> 1) & 3] += p0 + p1;
                 pk[i >> 1] = pack_bf16(p0, p1);
             }
-            // keys [qtr*CPT, qtr*CPT+CPT) of this row -> P sub-tile (qtr*CPT)/64, chunks ((qtr*CPT)%64)/8 ..
-#pragma unroll
-            for (int c = 0; c < CPT / 8; ++c) {
-                const int chunk = (qtr * CPT) / 8 + c;
-                sts128(sbase + OFF_P + (chunk >> 3) * SUB + swz(r, chunk & 7), pk[4 * c], pk[4 * c + 1],
-                       pk[4 * c + 2], pk[4 * c + 3]);
-            }
-            l = l * alpha + ((rs4[0] + rs4[1]) + (rs4[2] + rs4[3]));
-#pragma unroll
-            for (int i = 0; i < CPT; ++i) o[i] *= alpha;
-            m = m_new;
-            fence_async_smem();
+            // keys [qtr*CPT, +CPT) of this row = P columns [qtr*CPT/2, +CPT/2) of buffer j&1 (bf16 pairs)
+            tc_fence_after();
+            tmem_st16(tmem + lane_base + TM_P + (uint32_t)((j & 1) * 64) + qtr * (CPT / 2), pk);
+            tmem_wait_st();
+            l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
             tc_fence_before();
-            mbar_arrive(p_full);
+            mbar_arrive(&p_full[j & 1]);
             if (tid == 0) trace(j, 3);
         }
+        float o[CPT];
         if (n > 0) {
-            mbar_wait(o_full, (n - 1) & 1);
+            mbar_wait(&pv_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
             tc_fence_after();
             uint32_t w[CPT];
-            tmem_ld32(tmem + lane_base + 256 + col0, w);
+            tmem_ld32(tmem + lane_base + TM_O + qtr * CPT, w);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < CPT; ++i) o[i] += __uint_as_float(w[i]);
+            for (int i = 0; i < CPT; ++i) o[i] = __uint_as_float(w[i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) o[i] = 0.f;
         }
-        // the NQ threads of a row hold partial sums l over disjoint key columns (same running max)
+        // the NQ threads of a row hold partial sums l over disjoint key columns (same m_used)
         asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
         xmax[0][qtr][r] = l;
         asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
@@ -425,7 +453,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int c = 0; c < CPT / 4; ++c)
                     wo[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
                 if (qtr == 0) {
-                    ws_ml[((int64_t)split * Tq * H + orow) * 2 + 0] = m == -INFINITY ? -INFINITY : m / LOG2E;
+                    ws_ml[((int64_t)split * Tq * H + orow) * 2 + 0] = m_used == -INFINITY ? -INFINITY : m_used / LOG2E;
                     ws_ml[((int64_t)split * Tq * H + orow) * 2 + 1] = l;
                 }
             }
