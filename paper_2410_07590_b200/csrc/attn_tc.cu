@@ -3,22 +3,30 @@
 // (src/attention.cpp:94-169, src/numerics.cpp:31-60) with implicit masks: row t sees key j iff
 // lo[t] <= j <= hi[t] (causal_rows / build_mask, attention.cpp:50-92).
 //
-// GQA packing: a CTA owns 128 rows of ONE kv head g, row r = (token t, head g*group + r%group), so the
-// K/V tiles it streams serve all `group` query heads (C2: 64 tokens x 7 heads = 448 rows = 3.5 tiles).
+// GQA packing: rows of ONE kv head g are (token t, head g*group + i), so every K/V tile a CTA streams
+// serves all `group` query heads (C2: 64 tokens x 7 heads = 448 rows per kv head).
 //
-// v3: O accumulates in TMEM across KV tiles (FA4-style lazy rescale only when a row max grows by > 2^8), P is
-// double-buffered in TMEM and fed to the PV MMA as the A operand (tcgen05.mma with A in TMEM), so the softmax
-// of tile j+1 overlaps PV_j on the tensor pipe.
-// Per CTA (576 threads): warps 0-15 = softmax (four threads per row: warps w, w+4, w+8, w+12 share TMEM
-// lanes 32(w%4).., each owns 32 of the S columns and 32 of the O columns; partial row maxima are
-// exchanged through shared memory), warp 16 = TMA producer, warp 17 = MMA issuer. smem: Q [128x128] and P [128x128] (two 64-column SW128 sub-tiles each, 32 KB), two K/V stages
-// of 64 KB. TMEM (512 cols): S double buffer at cols 0/128, O tile at 256.
-//   S_j  = Q . K_j^T          tcgen05.mma kind::f16 M128 N128 K16 x8, A,B K-major
-//   P_j  = exp2(S_j*scale*log2e - m_j)  (softmax warps: TMEM -> regs -> bf16 -> swizzled smem)
-//   O_j  = P_j . V_j          tcgen05.mma, A = P (K-major), B = V (MN-major: d contiguous)
-// The running output O lives in registers (32 fp32 per thread), rescaled by exp2(m_{j-1} - m_j) each
-// tile and incremented by the O_j tile read back from TMEM. Split-K over keys writes (O, m, l) partials
-// combined by attn_combine_kernel (attn_simt.cu) — same workspace layout as the SIMT kernel.
+// v4 (ping-pong): a CTA owns a ROW GROUP of 256 rows = two 128-row tiles A and B of the same kv head and
+// streams one split of the key range through them:
+//   tensor pipe:  [PV_A(j-1) S_A(j)] [PV_B(j-1) S_B(j)] [PV_A(j) S_A(j+1)] ...
+//   softmax WG A works on S_A(j) while the pipe runs the B bracket, and vice versa, so the tensor pipe
+//   and the softmax (MUFU + FMA pipes) overlap; every K/V tile is read once for 256 rows.
+// Warps 0-3 = softmax A, 4-7 = softmax B (ONE thread per row: no cross-thread max exchange), warp 8 =
+// TMA producer, warp 9 = MMA issuer. TMEM (512 cols): S_A 0, O_A 128, S_B 256, O_B 384; P_X (bf16 pairs,
+// 64 cols) is written over the first half of S_X and fed to the PV tcgen05.mma as the A operand from TMEM.
+// O accumulates in TMEM; it is rescaled lazily, only when a row max grows by more than 2^8 (the stale max
+// keeps every p <= 2^8, exact in fp32 and bf16 range).
+// exp2 runs on two pipes: most pairs on MUFU.EX2, POLY_PAIRS of every 16 on the FMA pipe (Cody-Waite +
+// degree-3 minimax, max rel err 7.5e-5, far below the bf16 rounding of P), with packed f32x2 FFMA2/FADD2
+// and three-input FMNMX3 to keep the issue rate down.
+// Context K/V rows below `kv_ready` were written before this forward began (the embed kernel that starts
+// every forward does not release its dependents before its own griddepcontrol.wait), so their TMA loads
+// are issued BEFORE griddepcontrol.wait and overlap the previous kernel's tail.
+// Split-K over keys: every split stages its normalized output O/l (bf16) in shared memory, writes it
+// coalesced to a per-row-group workspace with (m, l), and exits; attn_tc_combine_kernel (launched with PDL
+// right behind, one warp per row, every load in flight) merges the splits. An in-kernel merge behind a
+// grid-wide arrive counter was measured slower: the row group's CTAs wait for the slowest sibling and
+// the merge loads then run at low memory-level parallelism.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -32,29 +40,29 @@
 namespace tkv {
 namespace {
 
-constexpr int D = 128, BR = 128, BK = 128;
-constexpr int NQ = 4;                       // softmax threads per row
-constexpr int CPT = 128 / NQ;               // S / O columns per softmax thread
-constexpr int SOFTMAX_WARPS = 4 * NQ, THREADS = SOFTMAX_WARPS * 32 + 64;
-constexpr uint32_t SUB = 128 * 64 * 2;          // one [128 rows][64 cols] bf16 SW128 sub-tile = 16 KB
-constexpr uint32_t OFF_Q = 0;                   // Q tile: 32 KB
-constexpr uint32_t OFF_K = 2 * SUB;             // K ring: 2 stages x 32 KB
-constexpr uint32_t OFF_V = 6 * SUB;             // V ring: 2 stages x 32 KB (separate ring: K_{j+2} loads once
-constexpr uint32_t KSTAGE = 2 * SUB;            //   S_j is done, without waiting for PV_j)
-constexpr uint32_t OFF_BAR = 10 * SUB;
-// TMEM columns: S double buffer (fp32), O accumulator (fp32), P double buffer (bf16 pairs: 128 keys -> 64 cols)
-constexpr uint32_t TM_S = 0, TM_O = 256, TM_P = 384;
-constexpr float RESCALE_LOG2 = 8.0f;  // lazy O rescale: only when a row max grows by more than 2^8
+constexpr int D = 128, BR = 128, BK = 128, RG = 2 * BR;  // rows per tile, keys per tile, rows per CTA
+constexpr int KST = 3, VST = 2;                          // K / V ring depths
+constexpr int SM_THREADS = 256, THREADS = SM_THREADS + 64;
+#ifndef POLY_PAIRS
+#define POLY_PAIRS 6
+#endif
+constexpr int kPolyPairs = POLY_PAIRS;                          // of every 16 exp2 pairs, this many on the FMA pipe
+constexpr uint32_t SUB = 128 * 64 * 2;                   // [128 rows][64 cols] bf16 SW128 sub-tile = 16 KB
+constexpr uint32_t TILE = 2 * SUB;                       // 128 x 128 bf16
+constexpr uint32_t OFF_Q = 0;                            // Q_A, Q_B
+constexpr uint32_t OFF_K = 2 * TILE;
+constexpr uint32_t OFF_V = OFF_K + KST * TILE;
+constexpr uint32_t OFF_BAR = OFF_V + VST * TILE;
 constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_LOG2 = 8.0f;
 
 // kind::f16, D=f32, A=B=bf16, M=128, N=128; PV additionally B MN-major (bit 16)
 constexpr uint32_t IDESC_S = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 constexpr uint32_t IDESC_PV = IDESC_S | (1u << 16);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -64,9 +72,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Bounded wait: a protocol bug traps (launch error) after ~2 s instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t done = 0;
+    uint64_t t0 = 0;
     for (uint32_t spin = 0;; ++spin) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -76,7 +91,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(addr), "r"(parity)
             : "memory");
         if (done) return;
-        if (spin > (1u << 26)) __trap();  // protocol bug -> launch error, never a hung GPU
+        if ((spin & 1023) == 1023) {
+            const uint64_t now = globaltimer_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 2000000000ull) __trap();
+        }
     }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -102,11 +121,19 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, ui
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// A operand from TMEM (P), B from shared memory (V)
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -116,61 +143,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-// Bulk L2 prefetch (no smem destination): warms the NEXT projections' weights while attention runs.
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-// Debug timeline (tkv_debug_attn_trace): CTA (0,0,0) stamps clock64 at pipeline events, slot [j][e].
-__device__ unsigned long long* g_attn_trace = nullptr;
-constexpr int TRACE_EV = 10, TRACE_TILES = 32;
-__device__ __forceinline__ void trace(int j, int e) {
-    if (g_attn_trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < TRACE_TILES) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
-        g_attn_trace[j * TRACE_EV + e] = t;
-    }
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ float ex2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-}
-// byte offset of 16-byte chunk `c` (0..7) of row `r` inside a K-major SW128 sub-tile
-__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-
-__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
         "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
@@ -180,291 +153,544 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// ---- packed f32x2 arithmetic (FFMA2 / FADD2) ----
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void up2(uint64_t v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// 2^x for a pair on the FMA pipe: x = j + f (j = rint(x) via the 1.5*2^23 shifter, f in [-0.5, 0.5]),
+// 2^f by a degree-3 minimax polynomial (rel err 7.5e-5), 2^j added into the exponent field with one IMAD.
+// 10 instructions per pair: 2 FMNMX, 2 FADD2, 4 FFMA2, 2 IMAD.
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t xv) {
+    float x0, x1;
+    up2(xv, x0, x1);
+    const uint64_t x = pk2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));  // keeps the result's biased exponent >= 0
+    const uint64_t t = add2(x, pk2(12582912.0f, 12582912.0f));
+    const uint64_t r = add2(t, pk2(-12582912.0f, -12582912.0f));
+    const uint64_t f = fma2(r, pk2(-1.0f, -1.0f), x);
+    uint64_t p = fma2(pk2(0.05517112836241722f, 0.05517112836241722f), f, pk2(0.24261008203029633f, 0.24261008203029633f));
+    p = fma2(p, f, pk2(0.6932609677314758f, 0.6932609677314758f));
+    p = fma2(p, f, pk2(0.9999281167984009f, 0.9999281167984009f));
+    uint32_t tl, th, pl, ph;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(tl), "=r"(th) : "l"(t));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(pl), "=r"(ph) : "l"(p));
+    uint64_t out;
+    asm("{\n\t.reg .u32 a, b;\n\t"
+        "mad.lo.u32 a, %1, 8388608, %3;\n\t"
+        "mad.lo.u32 b, %2, 8388608, %4;\n\t"
+        "mov.b64 %0, {a, b};\n\t}"
+        : "=l"(out) : "r"(tl), "r"(th), "r"(pl), "r"(ph));
+    return out;
+}
+__device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// byte offset of 16-byte chunk `c` (0..7) of row `r` inside a K-major SW128 sub-tile
+__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Debug timeline (tkv_debug_attn_trace): CTA (0,0,0) stamps clock64 at pipeline events, slot [j][e]. The
+// buffer pointer travels in the kernel arguments (a uniform constant-bank read, no global load on the path).
+unsigned long long* g_trace_host = nullptr;
+constexpr int TRACE_EV = 10, TRACE_TILES = 32, TRACE_CTA0 = TRACE_EV * TRACE_TILES, TRACE_CTAS = 1024;
+__device__ __forceinline__ void trace_at(unsigned long long* buf, int j, int e) {
+    if (buf && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < TRACE_TILES) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+        buf[j * TRACE_EV + e] = t;
+    }
+}
+#define trace(j, e) trace_at(a.trace, (j), (e))
+#ifndef TRACE_SM
+#define TRACE_SM 0  // 1: events 4-8 stamp softmax-internal points of thread 0 instead of the MMA/TMA warps
+#endif
+#define trace_pipe(j, e) do { if (!TRACE_SM) trace(j, e); } while (0)
+#define trace_mma(j, e) do { if (TRACE_SM == 2) trace(j, e); } while (0)
+#define trace_sm(j, e) do { if (TRACE_SM == 1 && tid == 0) trace(j, e); } while (0)
+
+struct AttnArgs {
+    const __nv_bfloat16* q;
+    const int32_t* lo;
+    const int32_t* hi;
+    __nv_bfloat16* out;
+    float* ws_o;       // bf16 [splits][row groups][256][D]: each split's normalized O/l (sized as fp32 ws)
+    float* ws_ml;      // [splits][row groups][256] (m in log2 units, l)
+    int* err;
+    int Tq, Tk, H, Hkv, splits, kv_ready;
+    float scale;
+    unsigned long long* trace;
+};
+
+// 10 warps: 3 share an SM sub-partition's 16K registers -> at most 168 registers per thread
 __global__ void __launch_bounds__(THREADS, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                   const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ lo,
-                   const int32_t* __restrict__ hi, __nv_bfloat16* __restrict__ out, float* __restrict__ ws_o,
-                   float* __restrict__ ws_ml, int Tq, int Tk, int H, int Hkv, int splits, float scale, int* err,
-                   L2Prefetch pf) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-    uint64_t* k_full = bars;        // [2]
-    uint64_t* k_empty = bars + 2;   // [2]
-    uint64_t* v_full = bars + 4;    // [2]
-    uint64_t* v_empty = bars + 6;   // [2]
-    uint64_t* s_full = bars + 8;    // [2] S_j in TMEM
-    uint64_t* p_full = bars + 10;   // [2] P_j in TMEM (all softmax threads arrived)
-    uint64_t* pv_done = bars + 12;  // [2] PV_j retired: P buffer j&1 free, O current through j
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-    __shared__ int red_lo[THREADS / 32], red_hi[THREADS / 32];
-    __shared__ float xmax[2][NQ][BR];  // [tile parity][quarter][row]: partial row maxima exchanged each tile
+    uint64_t* k_full = bars;                 // [KST]
+    uint64_t* k_empty = bars + KST;          // [KST]
+    uint64_t* v_full = bars + 2 * KST;       // [VST]
+    uint64_t* v_empty = v_full + VST;        // [VST]
+    uint64_t* s_full = v_empty + VST;        // [2] S_X(j) in TMEM
+    uint64_t* p_full = s_full + 2;           // [2][4] chunk c (32 keys) of P_X(j) in TMEM (128 threads arrived)
+    uint64_t* o_done = p_full + 8;           // [1] every MMA retired
+    uint64_t* q_ready = o_done + 1;          // [1] Q tiles staged (256 threads arrived)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 1);
+    __shared__ int sh_range[2];
 
     pdl_launch();
-    pdl_wait();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int group = H / Hkv, g = blockIdx.y, split = blockIdx.z;
-    const int rows_total = Tq * group;
-    const bool softmax = warp < SOFTMAX_WARPS;
-    const int r = tid & (BR - 1);             // tile row (TMEM lane) of a softmax thread
-    const int qtr = softmax ? warp >> 2 : 0;  // which CPT S columns / CPT O columns this thread owns
-    const int row = blockIdx.x * BR + r;
-    const bool active = softmax && row < rows_total;
-    const int t = active ? row / group : 0;
-    const int h = g * group + (active ? row % group : 0);
-    const int my_lo = active ? lo[t] : INT32_MAX;
-    const int my_hi = active ? min(hi[t], Tk - 1) : -1;
+    const int group = a.H / a.Hkv, g = blockIdx.y, split = blockIdx.z;
+    const int rows_total = a.Tq * group;
+    const int rr0 = blockIdx.x * RG;                       // first row of this row group
+    const int rows_here = min(RG, rows_total - rr0);
+    const bool hasB = rows_here > BR;
 
-    // ---- CTA key range (union of its rows), then this split's share, in 128-key tiles ----
-    int blo = my_lo, bhi = my_hi;
-    for (int o = 16; o > 0; o >>= 1) {
-        blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
-        bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
-    }
-    if (lane == 0) {
-        red_lo[warp] = blo;
-        red_hi[warp] = bhi;
-    }
+    const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (tid == 0 && a.trace && cta_lin < TRACE_CTAS) a.trace[TRACE_CTA0 + 2 * cta_lin] = globaltimer_ns();
     if (tid == 0) {
-        for (int s = 0; s < 2; ++s) {
+        trace(0, 9);
+        for (int s = 0; s < KST; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < VST; ++s) {
             mbar_init(&v_full[s], 1);
             mbar_init(&v_empty[s], 1);
-            mbar_init(&s_full[s], 1);
-            mbar_init(&p_full[s], SOFTMAX_WARPS * 32);
-            mbar_init(&pv_done[s], 1);
         }
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(&s_full[x], 1);
+            for (int c = 0; c < 4; ++c) mbar_init(&p_full[x * 4 + c], BR);
+        }
+        mbar_init(o_done, 1);
+        mbar_init(q_ready, SM_THREADS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {
+    if (warp == 8) {
+        // key range of the row group = union of its tokens' [lo, hi] (lo/hi were uploaded before the forward)
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
+        }
+        const int t0 = rr0 / group, t1 = (rr0 + rows_here - 1) / group;
+        int blo = INT32_MAX, bhi = -1;
+        for (int t = t0 + lane; t <= t1; t += 32) {
+            blo = min(blo, a.lo[t]);
+            bhi = max(bhi, min(a.hi[t], a.Tk - 1));
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+            bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+        }
+        if (lane == 0) {
+            sh_range[0] = max(blo, 0);
+            sh_range[1] = bhi;
+        }
+    }
+    if (warp == 9) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    // ---- Q tile: each softmax thread stages its CPT columns of its row ----
-    if (softmax) {
-        constexpr int CH = CPT / 8;  // 16-byte chunks per thread
-        const uint4* src = reinterpret_cast<const uint4*>(q + (int64_t)t * H * D + (int64_t)h * D) + qtr * CH;
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-            const uint4 v = active ? src[c] : make_uint4(0, 0, 0, 0);
-            const int chunk = qtr * CH + c;  // 0..15 over the 128 columns
-            sts128(sbase + OFF_Q + (chunk >> 3) * SUB + swz(r, chunk & 7), v.x, v.y, v.z, v.w);
-        }
-        fence_async_smem();
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    blo = red_lo[0];
-    bhi = red_hi[0];
-    for (int w = 1; w < THREADS / 32; ++w) {
-        blo = min(blo, red_lo[w]);
-        bhi = max(bhi, red_hi[w]);
-    }
-    blo = max(blo, 0);
+    const int blo = sh_range[0], bhi = sh_range[1];
     const int span = bhi - blo + 1;
-    const int chunk = span > 0 ? ((span + splits - 1) / splits + BK - 1) / BK * BK : 0;
+    const int chunk = span > 0 ? ((span + a.splits - 1) / a.splits + BK - 1) / BK * BK : 0;
     const int ks = blo + split * chunk;
     const int ke = min(bhi, ks + chunk - 1);
     const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
 
-    if (warp == SOFTMAX_WARPS) {
-        if (lane == 1) {  // idle lane: optional L2 warm-up of the next projections' weights
-            const int ncta = gridDim.x * gridDim.y * gridDim.z;
-            const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-            for (int rr = 0; rr < 2; ++rr) {
-                const size_t total = pf.bytes[rr] & ~size_t(15);
-                if (!pf.ptr[rr] || total == 0) continue;
-                const size_t share = ((total + ncta - 1) / ncta + 15) & ~size_t(15);
-                const size_t b0 = (size_t)cta * share, b1 = b0 + share < total ? b0 + share : total;
-                for (size_t off = b0; off < b1; off += 32768)
-                    prefetch_l2(static_cast<const uint8_t*>(pf.ptr[rr]) + off,
-                                (uint32_t)((b1 - off) < 32768 ? (b1 - off) : 32768));
-            }
-        }
+    if (warp == 8) {
         if (lane == 0) {  // ---------------- TMA producer ----------------
+            bool waited = false;
             for (int j = 0; j < n; ++j) {
-                const int s = j & 1;
-                const uint32_t par = ((j >> 1) & 1) ^ 1;
                 const int key = ks + j * BK;
-                mbar_wait(&k_empty[s], par);
-                trace(j, 7);
-                mbar_expect_tx(&k_full[s], KSTAGE);
-                const uint32_t kd = sbase + OFF_K + s * KSTAGE;
-                tma_load_2d(kd, &tmK, &k_full[s], g * D, key);
-                tma_load_2d(kd + SUB, &tmK, &k_full[s], g * D + 64, key);
-                mbar_wait(&v_empty[s], par);
-                trace(j, 8);
-                mbar_expect_tx(&v_full[s], KSTAGE);
-                const uint32_t vd = sbase + OFF_V + s * KSTAGE;
-                tma_load_2d(vd, &tmV, &v_full[s], g * D, key);
-                tma_load_2d(vd + SUB, &tmV, &v_full[s], g * D + 64, key);
+                if (!waited && key + BK > a.kv_ready) {  // rows written by the previous kernels of this forward
+                    pdl_wait();
+                    waited = true;
+                }
+                const int sk = j % KST, sv = j % VST;
+                mbar_wait(&k_empty[sk], ((uint32_t)(j / KST) & 1u) ^ 1u);
+                mbar_expect_tx(&k_full[sk], TILE);
+                const uint32_t kd = sbase + OFF_K + sk * TILE;
+                tma_load_2d(kd, &tmK, &k_full[sk], g * D, key);
+                tma_load_2d(kd + SUB, &tmK, &k_full[sk], g * D + 64, key);
+                trace_pipe(j, 6);
+                mbar_wait(&v_empty[sv], ((uint32_t)(j / VST) & 1u) ^ 1u);
+                mbar_expect_tx(&v_full[sv], TILE);
+                const uint32_t vd = sbase + OFF_V + sv * TILE;
+                tma_load_2d(vd, &tmV, &v_full[sv], g * D, key);
+                tma_load_2d(vd + SUB, &tmV, &v_full[sv], g * D + 64, key);
+                trace_pipe(j, 7);
             }
         }
-    } else if (warp == SOFTMAX_WARPS + 1) {
+    } else if (warp == 9) {
         if (lane == 0) {  // ---------------- MMA issuer ----------------
-            auto issue_s = [&](int j) {
-                const int s = j & 1;
-                mbar_wait(&k_full[s], (j >> 1) & 1);
-                tc_fence_after();
-                const uint32_t kb = sbase + OFF_K + s * KSTAGE;
+            auto issue_s = [&](int x, int j) {  // S_x = Q_x . K_j^T
+                const uint32_t qb = sbase + OFF_Q + x * TILE, kb = sbase + OFF_K + (j % KST) * TILE;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
-                    umma(tmem + TM_S + s * 128, desc_k(sbase + OFF_Q + off), desc_k(kb + off), IDESC_S, kk > 0);
+                    umma(tmem + x * 256, desc_k(qb + off), desc_k(kb + off), IDESC_S, kk > 0);
                 }
-                umma_commit(&s_full[s]);
-                umma_commit(&k_empty[s]);
-                trace(j, 6);
+                umma_commit(&s_full[x]);
             };
-            if (n > 0) issue_s(0);
-            if (n > 1) issue_s(1);
-            for (int j = 0; j < n; ++j) {
-                const int s = j & 1;
-                mbar_wait(&p_full[s], (j >> 1) & 1);
-                trace(j, 4);
-                mbar_wait(&v_full[s], (j >> 1) & 1);
-                tc_fence_after();
-                const uint32_t vb = sbase + OFF_V + s * KSTAGE;
-                // O += P_j . V_j : A = P_j from TMEM (8 columns = 16 keys per MMA), B = V (MN-major)
+            // O_x += P_x . V_j, P from TMEM (8 cols = 16 keys per MMA), chunk by chunk as the softmax stores it
+            auto issue_pv = [&](int x, int j) {
+                const uint32_t vb = sbase + OFF_V + (j % VST) * TILE;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    umma_ts(tmem + TM_O, tmem + TM_P + s * 64 + kk * 8, desc_mn(vb + kk * 2048), IDESC_PV,
-                            (j > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&pv_done[s]);
-                umma_commit(&v_empty[s]);
-                trace(j, 5);
-                if (j + 2 < n) issue_s(j + 2);
+                for (int c = 0; c < 4; ++c) {
+                    mbar_wait(&p_full[x * 4 + c], (uint32_t)j & 1u);
+                    tc_fence_after();
+#pragma unroll
+                    for (int k2 = 0; k2 < 2; ++k2) {
+                        const int kk = 2 * c + k2;
+                        umma_ts(tmem + x * 256 + 128, tmem + x * 256 + kk * 8, desc_mn(vb + kk * 2048), IDESC_PV,
+                                (j > 0 || kk > 0) ? 1u : 0u);
+                    }
+                }
+            };
+            mbar_wait(q_ready, 0);
+            tc_fence_after();
+            trace_pipe(0, 8);
+            if (n > 0) {
+                mbar_wait(&k_full[0], 0);
+                tc_fence_after();
+                issue_s(0, 0);
+                if (hasB) issue_s(1, 0);
+                umma_commit(&k_empty[0]);
             }
+            for (int j = 0; j < n; ++j) {
+                const bool more = j + 1 < n;
+                const int sk1 = (j + 1) % KST;
+                mbar_wait(&v_full[j % VST], (uint32_t)(j / VST) & 1u);
+                trace_mma(j, 4);
+                tc_fence_after();
+                issue_pv(0, j);
+                trace_pipe(j, 4);
+                trace_mma(j, 5);
+                if (more) {
+                    mbar_wait(&k_full[sk1], (uint32_t)((j + 1) / KST) & 1u);
+                    trace_mma(j, 6);
+                    tc_fence_after();
+                    issue_s(0, j + 1);
+                    trace_mma(j, 7);
+                }
+                if (hasB) {
+                    trace_mma(j, 8);
+                    issue_pv(1, j);
+                    trace_pipe(j, 5);
+                }
+                umma_commit(&v_empty[j % VST]);
+                if (more) {
+                    if (hasB) issue_s(1, j + 1);
+                    umma_commit(&k_empty[sk1]);
+                }
+            }
+            umma_commit(o_done);
         }
     } else {
-        // ---------------- softmax: NQ threads per row, CPT columns each; O stays in TMEM ----------------
-        const float sl2 = scale * LOG2E;
+        // ---------------- softmax: warps 0-3 tile A, 4-7 tile B; one thread per row ----------------
+        const int x = warp >> 2;
+        const int r = (warp & 3) * 32 + lane;  // TMEM lane = tile row
+        const int rr = rr0 + x * BR + r;
+        const bool active = rr < rows_total;
+        const int t = active ? rr / group : 0;
+        const int h = g * group + (active ? rr % group : 0);
+        const int my_lo = active ? a.lo[t] : INT32_MAX;
+        const int my_hi = active ? min(a.hi[t], a.Tk - 1) : -1;
+        pdl_wait();  // q is produced by the previous kernel
+        {
+            // Coalesced staging: warp w of this tile loads its 32 rows two at a time (16 lanes x 16 B per row),
+            // all 16 loads in flight before the swizzled stores.
+            const uint32_t qb = sbase + OFF_Q + x * TILE;
+            const int c = lane & 15;
+            uint4 v[16];
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+                const int row = (warp & 3) * 32 + it * 2 + (lane >> 4);
+                const int qr = rr0 + x * BR + row;
+                v[it] = make_uint4(0, 0, 0, 0);
+                if (qr < rows_total)
+                    v[it] = *(reinterpret_cast<const uint4*>(a.q + ((int64_t)(qr / group) * a.H + g * group + qr % group) * D) + c);
+            }
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+                const int row = (warp & 3) * 32 + it * 2 + (lane >> 4);
+                sts128(qb + (c >> 3) * SUB + swz(row, c & 7), v[it]);
+            }
+            fence_async_smem();
+            mbar_arrive(q_ready);
+        }
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        float m_used = -INFINITY, l = 0.f;  // running max actually used for exp2, row-sum share
-        for (int j = 0; j < n; ++j) {
-            const int key0 = ks + j * BK + qtr * CPT;  // first key of this thread's columns
-            const bool full = key0 >= my_lo && key0 + CPT - 1 <= my_hi;
-            const int clo = my_lo - key0, chi = my_hi - key0;
-            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+        const uint32_t tS = tmem + lane_base + x * 256, tO = tS + 128;
+        const float sl2 = a.scale * LOG2E;
+        float m_used = -INFINITY, l = 0.f;
+        const int nx = (x == 1 && !hasB) ? 0 : n;
+        for (int j = 0; j < nx; ++j) {
+            mbar_wait(&s_full[x], (uint32_t)j & 1u);
+            tc_fence_after();
             if (tid == 0) trace(j, 0);
-            tc_fence_after();
-            uint32_t v[CPT];
-            tmem_ld32(tmem + lane_base + TM_S + (uint32_t)((j & 1) * 128) + qtr * CPT, v);
+            if (tid == 128) trace(j, 2);
+            uint32_t s[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
             tmem_wait_ld();
-            if (!full) {  // masked columns -> -inf (per-tile branch; uniform in the common case)
+            trace_sm(j, 4);
+            const int key0 = ks + j * BK;
+            if (!(key0 >= my_lo && key0 + BK - 1 <= my_hi)) {  // partially visible tile: masked -> -inf
+                const int clo = my_lo - key0, chi = my_hi - key0;
 #pragma unroll
-                for (int i = 0; i < CPT; ++i)
-                    v[i] = (i >= clo && i <= chi) ? v[i] : __float_as_uint(-INFINITY);
+                for (int i = 0; i < 128; ++i)
+                    if (i < clo || i > chi) s[i] = __float_as_uint(-INFINITY);
             }
-            float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            float m0 = __uint_as_float(s[0]), m1 = __uint_as_float(s[1]), m2 = __uint_as_float(s[2]),
+                  m3 = __uint_as_float(s[3]);
 #pragma unroll
-            for (int i = 0; i < CPT; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(v[i]));
-            float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-            xmax[j & 1][qtr][r] = mx;
-            asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
+            for (int i = 4; i < 124; i += 8) {
+                m0 = max3(m0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+                m1 = max3(m1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+                m2 = max3(m2, __uint_as_float(s[i + 4]), __uint_as_float(s[i + 5]));
+                m3 = max3(m3, __uint_as_float(s[i + 6]), __uint_as_float(s[i + 7]));
+            }
+            m0 = max3(m0, __uint_as_float(s[124]), __uint_as_float(s[125]));
+            m1 = max3(m1, __uint_as_float(s[126]), __uint_as_float(s[127]));
+            const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+            trace_sm(j, 5);
+            const float mxs = mx == -INFINITY ? -INFINITY : mx * sl2;
+            // lazy rescale. tcgen05.ld/st are warp-collective (.sync.aligned): the whole warp takes the branch
+            // when any of its rows needs it; rows that do not get alpha = 1.
+            bool grow = false;
+            if (m_used == -INFINITY)
+                m_used = mxs;  // first visible keys: O is still all zeros, nothing to rescale
+            else
+                grow = mxs > m_used + RESCALE_LOG2;
+            if (__any_sync(0xffffffffu, grow)) {
+                // O_x is current through PV_x(j-1): it retired before S_x(j) (in-order tensor pipe)
+                const float alpha = grow ? ex2(m_used - mxs) : 1.0f;
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t w[32];
+                    tmem_ld32(tO + c * 32, w);
+                    tmem_wait_ld();
 #pragma unroll
-            for (int k = 1; k < NQ; ++k) mx = fmaxf(mx, xmax[j & 1][(qtr + k) & (NQ - 1)][r]);
-            if (tid == 0) trace(j, 1);
-            mx = mx == -INFINITY ? -INFINITY : mx * sl2;
-            if (m_used == -INFINITY) {
-                m_used = mx;  // first visible keys: O is still all zeros, nothing to rescale
-            } else if (mx > m_used + RESCALE_LOG2) {
-                // rare: the row max grew by more than 2^8 -> rescale O (in TMEM) and l to the new max.
-                // All four threads of the row take this branch together (same mx, same m_used).
-                mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);  // O current through PV_{j-1}
-                tc_fence_after();
-                const float alpha = ex2(m_used - mx);
-                uint32_t w[CPT];
-                tmem_ld32(tmem + lane_base + TM_O + qtr * CPT, w);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < CPT; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
-                tmem_st32(tmem + lane_base + TM_O + qtr * CPT, w);
+                    for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
+                    tmem_st32(tO + c * 32, w);
+                }
                 tmem_wait_st();
-                l *= alpha;
-                m_used = mx;
+                if (grow) {
+                    l *= alpha;
+                    m_used = mxs;
+                }
             }
-            if (tid == 0) trace(j, 2);
-            // P buffer j&1 is free once PV_{j-2} retired
-            if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
             const float moff = m_used == -INFINITY ? 0.f : m_used;  // nothing visible yet -> all p = 0
-            float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-            uint32_t pk[CPT / 2];
+            const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(-moff, -moff);
+            uint64_t acc0 = 0, acc1 = 0;  // (+0, +0) pairs
 #pragma unroll
-            for (int i = 0; i < CPT; i += 2) {
-                const float p0 = ex2(fmaf(__uint_as_float(v[i]), sl2, -moff));
-                const float p1 = ex2(fmaf(__uint_as_float(v[i + 1]), sl2, -moff));
-                rs4[(i >> 1) & 3] += p0 + p1;
-                pk[i >> 1] = pack_bf16(p0, p1);
-            }
-            // keys [qtr*CPT, +CPT) of this row = P columns [qtr*CPT/2, +CPT/2) of buffer j&1 (bf16 pairs)
-            tc_fence_after();
-            tmem_st16(tmem + lane_base + TM_P + (uint32_t)((j & 1) * 64) + qtr * (CPT / 2), pk);
-            tmem_wait_st();
-            l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-            tc_fence_before();
-            mbar_arrive(&p_full[j & 1]);
-            if (tid == 0) trace(j, 3);
-        }
-        float o[CPT];
-        if (n > 0) {
-            mbar_wait(&pv_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
-            tc_fence_after();
-            uint32_t w[CPT];
-            tmem_ld32(tmem + lane_base + TM_O + qtr * CPT, w);
-            tmem_wait_ld();
+            for (int c = 0; c < 4; ++c) {  // 32 keys per chunk -> 16 P columns (bf16 pairs), stored as soon as done
+                uint32_t pk[16];
 #pragma unroll
-            for (int i = 0; i < CPT; ++i) o[i] = __uint_as_float(w[i]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < CPT; ++i) o[i] = 0.f;
-        }
-        // the NQ threads of a row hold partial sums l over disjoint key columns (same m_used)
-        asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
-        xmax[0][qtr][r] = l;
-        asm volatile("bar.sync 1, %0;" ::"r"(SOFTMAX_WARPS * 32) : "memory");
-#pragma unroll
-        for (int k = 1; k < NQ; ++k) l += xmax[0][(qtr + k) & (NQ - 1)][r];
-        if (active) {
-            const int64_t orow = (int64_t)t * H + h;
-            if (splits == 1) {
-                if (l == 0.f) {
-                    if (qtr == 0) atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
-                } else {
-                    const float inv = 1.0f / l;
-                    uint4* dst = reinterpret_cast<uint4*>(out + orow * D + qtr * CPT);
-#pragma unroll
-                    for (int c = 0; c < CPT / 8; ++c)
-                        dst[c] = make_uint4(pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv),
-                                            pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
-                                            pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv),
-                                            pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+                for (int i = 0; i < 16; ++i) {
+                    const int e = c * 32 + 2 * i;
+                    const uint64_t xv = fma2(pk2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sc2, nm2);
+                    uint64_t p;
+                    if (i < kPolyPairs) {
+                        p = ex2_poly2(xv);
+                    } else {
+                        float x0, x1;
+                        up2(xv, x0, x1);
+                        p = pk2(ex2(x0), ex2(x1));
+                    }
+                    if (i & 1)
+                        acc1 = add2(acc1, p);
+                    else
+                        acc0 = add2(acc0, p);
+                    float p0, p1;
+                    up2(p, p0, p1);
+                    pk[i] = bf16x2_bits(p0, p1);
                 }
+                tmem_st16(tS + c * 16, pk);
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&p_full[x * 4 + c]);  // the PV MMA on these 32 keys may start
+                if (c == 1) trace_sm(j, 6);
+                if (c == 3) trace_sm(j, 7);
+            }
+            float a0, a1, a2, a3;
+            up2(acc0, a0, a1);
+            up2(acc1, a2, a3);
+            l += (a0 + a1) + (a2 + a3);
+            trace_sm(j, 8);
+            if (tid == 0) trace(j, 1);
+            if (tid == 128) trace(j, 3);
+        }
+        if (nx > 0) {
+            mbar_wait(o_done, 0);
+            tc_fence_after();
+        }
+        if (tid == 0) trace(31, 0);
+        // ---- epilogue: O/l as bf16, staged row-per-thread into the (now idle) Q_x tile with the SW128 chunk
+        // swizzle (conflict-free), then copied out coalesced: 16 lanes x 16 B per 256-byte row ----
+        const bool degenerate = active && l == 0.f;
+        const float inv = l > 0.f ? 1.0f / l : 0.f;
+        const uint32_t stage = sbase + OFF_Q + x * TILE;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t w[32];
+            if (nx > 0) {
+                tmem_ld32(tO + c * 32, w);  // warp-collective
+                tmem_wait_ld();
             } else {
-                float4* wo = reinterpret_cast<float4*>(ws_o + ((int64_t)split * Tq * H + orow) * D + qtr * CPT);
 #pragma unroll
-                for (int c = 0; c < CPT / 4; ++c)
-                    wo[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-                if (qtr == 0) {
-                    ws_ml[((int64_t)split * Tq * H + orow) * 2 + 0] = m_used == -INFINITY ? -INFINITY : m_used / LOG2E;
-                    ws_ml[((int64_t)split * Tq * H + orow) * 2 + 1] = l;
+                for (int i = 0; i < 32; ++i) w[i] = 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int chunk = c * 4 + k;  // 16-byte chunk (8 columns) of the 256-byte row
+                sts128(stage + (chunk >> 3) * SUB + swz(r, chunk & 7),
+                       make_uint4(bf16x2_bits(__uint_as_float(w[8 * k + 0]) * inv, __uint_as_float(w[8 * k + 1]) * inv),
+                                  bf16x2_bits(__uint_as_float(w[8 * k + 2]) * inv, __uint_as_float(w[8 * k + 3]) * inv),
+                                  bf16x2_bits(__uint_as_float(w[8 * k + 4]) * inv, __uint_as_float(w[8 * k + 5]) * inv),
+                                  bf16x2_bits(__uint_as_float(w[8 * k + 6]) * inv, __uint_as_float(w[8 * k + 7]) * inv)));
+            }
+        }
+        if (tid == 0) trace(31, 4);
+        named_bar(2 + x, BR);  // this tile's 128 rows are staged
+        if (tid == 0) trace(31, 5);
+        const int gid = blockIdx.y * gridDim.x + blockIdx.x;
+        const int ngroups = gridDim.x * gridDim.y;
+        // workspace of split s, row group gid: rows [256][D] bf16 (contiguous) and (m, l) [256]
+        const int64_t wrow0 = ((int64_t)split * ngroups + gid) * RG;
+        {
+            const int cc = lane & 15;
+#pragma unroll 4
+            for (int it = 0; it < 16; ++it) {
+                const int row = (warp & 3) * 32 + it * 2 + (lane >> 4);
+                const int qr = rr0 + x * BR + row;
+                uint4 v;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                             : "r"(stage + (cc >> 3) * SUB + swz(row, cc & 7)));
+                if (a.splits == 1) {
+                    if (qr < rows_total)
+                        reinterpret_cast<uint4*>(a.out + ((int64_t)(qr / group) * a.H + g * group + qr % group) * D)[cc] = v;
+                } else {
+                    reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.ws_o) + (wrow0 + x * BR + row) * D)[cc] = v;
                 }
             }
+        }
+        if (tid == 0) trace(31, 6);
+        if (a.splits == 1) {
+            if (degenerate) atomicOr(a.err, 8);  // DegenerateRowError (numerics.cpp:39-42)
+        } else {
+            reinterpret_cast<float2*>(a.ws_ml)[wrow0 + x * BR + r] = make_float2(active ? m_used : -INFINITY, l);
+            if (tid == 0) trace(31, 1);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (tid == 0 && a.trace && cta_lin < TRACE_CTAS) a.trace[TRACE_CTA0 + 2 * cta_lin + 1] = globaltimer_ns();
+    if (warp == 9) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
+}
+
+// Split merge (PDL-launched right behind the attention grid): one warp per row of a row group, lane = 4
+// columns; all `splits` partial loads are issued before use. out = sum_s w_s (O_s / l_s) / sum_s w_s,
+// w_s = 2^(m_s - M) * l_s (numerics.cpp:31-60 softmax, regrouped over key splits).
+__global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat16* __restrict__ ws_o,
+                                                              const float2* __restrict__ ws_ml,
+                                                              __nv_bfloat16* __restrict__ out, int* err, int Tq, int H,
+                                                              int Hkv, int splits, int groups_x) {
+    pdl_launch();
+    const int lane = threadIdx.x & 31;
+    const int grow = blockIdx.x * 8 + (threadIdx.x >> 5);  // row over all row groups: gid * RG + i
+    const int gid = grow / RG, i = grow % RG;
+    const int g = gid / groups_x, rr = (gid % groups_x) * RG + i;  // kv head, row within the kv head
+    const int group = H / Hkv;
+    const bool ok = rr < Tq * group;
+    const int64_t plane = (int64_t)groups_x * Hkv * RG;
+    pdl_wait();
+    if (!ok) return;  // warp-uniform
+    const uint2* src = reinterpret_cast<const uint2*>(ws_o + (int64_t)grow * D) + lane;
+    uint2 v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        if (k < splits) v[k] = src[(int64_t)k * plane * (D / 4)];
+    const float2 ml = lane < splits ? ws_ml[lane * plane + grow] : make_float2(-INFINITY, 0.f);
+    float M = ml.x;
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float wl = ml.x == -INFINITY ? 0.f : ex2(ml.x - M) * ml.y;
+    float L = wl;
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (M == -INFINITY || L == 0.f) {
+        if (lane == 0) atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
+        return;
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        if (k >= splits) break;
+        const float w = __shfl_sync(0xffffffffu, wl, k);
+        acc[0] = fmaf(__uint_as_float(v[k].x << 16), w, acc[0]);
+        acc[1] = fmaf(__uint_as_float(v[k].x & 0xFFFF0000u), w, acc[1]);
+        acc[2] = fmaf(__uint_as_float(v[k].y << 16), w, acc[2]);
+        acc[3] = fmaf(__uint_as_float(v[k].y & 0xFFFF0000u), w, acc[3]);
+    }
+    const float inv = 1.0f / L;
+    const int64_t mo = (int64_t)(rr / group) * H + g * group + rr % group;
+    reinterpret_cast<uint2*>(out + mo * D)[lane] =
+        make_uint2(bf16x2_bits(acc[0] * inv, acc[1] * inv), bf16x2_bits(acc[2] * inv, acc[3] * inv));
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -503,21 +729,29 @@ CUtensorMap kv_map(const void* base, int rows, int cols, int ld) {
 void attn_trace_enable(bool on, unsigned long long** host_view) {
     static unsigned long long* buf = nullptr;
     if (on && !buf) {
-        TKV_CUDA(cudaMalloc(&buf, TRACE_EV * TRACE_TILES * 8));
-        TKV_CUDA(cudaMemset(buf, 0, TRACE_EV * TRACE_TILES * 8));
+        TKV_CUDA(cudaMalloc(&buf, (TRACE_CTA0 + 2 * TRACE_CTAS) * 8));
+        TKV_CUDA(cudaMemset(buf, 0, (TRACE_CTA0 + 2 * TRACE_CTAS) * 8));
     }
-    unsigned long long* v = on ? buf : nullptr;
-    TKV_CUDA(cudaMemcpyToSymbol(g_attn_trace, &v, sizeof v));
+    g_trace_host = on ? buf : nullptr;
     if (host_view) *host_view = buf;
 }
 
 bool attention_tc_supported(int d, DT dt) { return d == 128 && dt == DT::BF16; }
 
+int attn_tc_row_groups(int Tq, int H, int Hkv) { return ((Tq * (H / Hkv) + RG - 1) / RG) * Hkv; }
+
+size_t attn_tc_workspace_floats(int Tq, int H, int Hkv, int splits, size_t* ml_offset) {
+    if (splits <= 1) return 0;
+    const size_t rows = (size_t)splits * attn_tc_row_groups(Tq, H, Hkv) * RG;
+    if (ml_offset) *ml_offset = rows * D / 2;  // bf16 partials first, then (m, l) pairs
+    return rows * D / 2 + rows * 2;
+}
+
 int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms) {
-    const int group = H / Hkv;
-    const int ctas = ((Tq * group + BR - 1) / BR) * Hkv;
-    int s = num_sms / ctas;  // 1 CTA per SM (192 KB smem): stay within one wave
-    const int max_by_keys = (Tk + 4 * BK - 1) / (4 * BK);  // >= 4 key tiles per split
+    const int groups = attn_tc_row_groups(Tq, H, Hkv);
+    if (groups * 2 > num_sms) return 1;  // already >= half a wave of row groups: no split-K
+    int s = num_sms / groups;            // one wave (1 CTA / SM)
+    const int max_by_keys = ((Tk + BK - 1) / BK + 1) / 2;  // >= 2 key tiles per split
     if (s > max_by_keys) s = max_by_keys;
     if (s > 32) s = 32;
     return s < 1 ? 1 : s;
@@ -525,17 +759,37 @@ int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms) {
 
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
-                         int* err, cudaStream_t s, const L2Prefetch& pf) {
+                         int* err, cudaStream_t s, int kv_ready) {
     TKV_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    const int group = H / Hkv;
+    dim3 grid((Tq * group + RG - 1) / RG, Hkv, splits);
+    if (splits > 1 && !ws.o) fail(TKV_ERR_CONFIG, "attention split-K needs its workspace");
+    AttnArgs a{};
+    a.q = (const __nv_bfloat16*)q;
+    a.lo = lo;
+    a.hi = hi;
+    a.out = (__nv_bfloat16*)out;
+    a.ws_o = ws.o;
+    a.ws_ml = ws.ml;
+    a.err = err;
+    a.Tq = Tq;
+    a.Tk = Tk;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.splits = splits;
+    a.kv_ready = kv_ready;
+    a.scale = (float)(1.0 / sqrt((double)D));
+    a.trace = g_trace_host;
     const CUtensorMap tk = kv_map(k, Tk, kv_stride, kv_stride);
     const CUtensorMap tv = kv_map(v, Tk, kv_stride, kv_stride);
-    const int group = H / Hkv;
-    dim3 grid((Tq * group + BR - 1) / BR, Hkv, splits);
-    const float scale = (float)(1.0 / sqrt((double)D));
-    launch_k(attn_tc_kernel, grid, THREADS, SMEM_BYTES, s, tk, tv, (const __nv_bfloat16*)q, lo, hi, (__nv_bfloat16*)out,
-                                                     ws.o, ws.ml, Tq, Tk, H, Hkv, splits, scale, err, pf);
+    launch_k(attn_tc_kernel, grid, THREADS, SMEM_BYTES, s, tk, tv, a);
     TKV_CUDA(cudaGetLastError());
-    if (splits > 1) launch_attention_combine(ws, Tq * H, D, splits, out, err, DT::BF16, s);
+    if (splits > 1) {
+        const int rows = (int)(grid.x * grid.y) * RG;
+        launch_k(attn_tc_combine_kernel, dim3(rows / 8), dim3(256), 0, s, (const __nv_bfloat16*)ws.o,
+                 (const float2*)ws.ml, (__nv_bfloat16*)out, err, Tq, H, Hkv, splits, (int)grid.x);
+        TKV_CUDA(cudaGetLastError());
+    }
 }
 
 }  // namespace tkv

@@ -556,29 +556,19 @@ void tkv_engine::forward(const Fwd& f) {
                                   : attn_pick_splits(rows, (int)H, (int)Hkv, Tk, num_sms);
             AttnWork ws;
             if (splits > 1) {
-                const size_t fl = attn_workspace_floats(rows, (int)H, (int)d, splits);
+                size_t mloff = (size_t)splits * rows * H * d;
+                const size_t fl = tc ? attn_tc_workspace_floats(rows, (int)H, (int)Hkv, splits, &mloff)
+                                     : attn_workspace_floats(rows, (int)H, (int)d, splits);
                 attn_ws.ensure(fl * sizeof(float));
                 ws.o = attn_ws.as<float>();
-                ws.ml = ws.o + (size_t)splits * rows * H * d;
+                ws.ml = ws.o + mloff;
             }
-            Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);
+            Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);  // + the split-merge launch
             const void* qrows = static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es;
-            if (tc)
-            {
-                // Small-token forwards are weight-bound and HBM idles during attention: warm L2 with this
-                // layer's O-proj weights and the next layer's QKV weights (59 MB at Qwen2-7B shape).
-                L2Prefetch pf;
-                if (T <= 128 && (opts.flags & TKV_FLAG_L2_PREFETCH)) {
-                    pf.ptr[0] = w_o[l];
-                    pf.bytes[0] = (size_t)hid * qd * es;
-                    if (l + 1 < L) {
-                        pf.ptr[1] = w_qkv[l + 1];
-                        pf.bytes[1] = (size_t)nqkv * hid * es;
-                    }
-                }
+            if (tc) {
                 launch_attention_tc(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
                                     f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream,
-                                    pf);
+                                    f.row0);
             }
             else
                 launch_attention_simt(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
@@ -1858,7 +1848,7 @@ tkv_status tkv_debug_attn_trace(int on, uint64_t* out, int64_t capacity) {
         if (out) {  // read back the last trace
             attn_trace_enable(true, &buf);
             TKV_CUDA(cudaDeviceSynchronize());
-            TKV_CUDA(cudaMemcpy(out, buf, (size_t)std::min<int64_t>(capacity, 320) * 8, cudaMemcpyDeviceToHost));
+            TKV_CUDA(cudaMemcpy(out, buf, (size_t)std::min<int64_t>(capacity, 320 + 2048) * 8, cudaMemcpyDeviceToHost));
         }
         attn_trace_enable(on != 0, &buf);
     });
@@ -1937,13 +1927,15 @@ tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const floa
                               : attn_pick_splits((int)Tq, (int)H, (int)Hkv, (int)Tk, dev_sms);
         AttnWork w;
         if (splits > 1) {
-            ws.ensure(attn_workspace_floats((int)Tq, (int)H, (int)d, splits) * 4);
+            size_t mloff = (size_t)splits * Tq * H * d;
+            ws.ensure((tc ? attn_tc_workspace_floats((int)Tq, (int)H, (int)Hkv, splits, &mloff)
+                          : attn_workspace_floats((int)Tq, (int)H, (int)d, splits)) * 4);
             w.o = ws.as<float>();
-            w.ml = w.o + (size_t)splits * Tq * H * d;
+            w.ml = w.o + mloff;
         }
         if (tc)
             launch_attention_tc(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p,
-                                (int)Tq, (int)Tk, (int)H, (int)Hkv, splits, w, errm.as<int>(), 0);
+                                (int)Tq, (int)Tk, (int)H, (int)Hkv, splits, w, errm.as<int>(), 0, (int)Tk);
         else
             launch_attention_simt(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p,
                                   (int)Tq, (int)Tk, (int)H, (int)Hkv, (int)d, splits, w, errm.as<int>(), dt, 0);

@@ -97,8 +97,11 @@ __device__ __forceinline__ void finish_row_block(float* __restrict__ xrow, const
 template <typename T>
 __global__ void __launch_bounds__(256) embed_kernel(const int32_t* tok, const float* emb, int hidden, int vocab,
                                                     const float* w, float* x, T* xb, float* ssp, int* err) {
-    pdl_launch();
+    // First kernel of every forward: release dependents only AFTER the wait, so any later kernel of this
+    // forward that starts implies every earlier grid (previous forwards, the KV gather, uploads) has
+    // completed — the attention kernel relies on this to TMA-load context K/V before its own wait.
     pdl_wait();
+    pdl_launch();
     __shared__ float red[32];
     const int t = blockIdx.y, nb = gridDim.x;
     const int id = tok[t];

@@ -135,18 +135,18 @@ void launch_attention_simt(const void* q, const void* k, const void* v, int kv_s
                            const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int d, int splits,
                            const AttnWork& ws, int* err, DT dt, cudaStream_t s);
 
-// Up to two global regions the attention kernel prefetches into L2 (bulk prefetch from an idle lane).
-struct L2Prefetch {
-    const void* ptr[2] = {nullptr, nullptr};
-    size_t bytes[2] = {0, 0};
-};
-// tcgen05/TMEM/TMA attention (attn_tc.cu): head_size 128, bf16. Same predicate and workspace as SIMT.
+// tcgen05/TMEM/TMA attention (attn_tc.cu): head_size 128, bf16. Same predicate and workspace layout as
+// SIMT; split-K partials (bf16 O/l) are merged by a PDL-launched combine kernel. Key rows
+// < kv_ready were written before the current forward began and are loaded before griddepcontrol.wait.
 bool attention_tc_supported(int d, DT dt);
 void attn_trace_enable(bool on, unsigned long long** device_buf);  // debug timeline of CTA (0,0,0)
+int attn_tc_row_groups(int Tq, int H, int Hkv);
+// workspace of the tcgen05 kernel's split merge (floats); ws.ml = ws.o + *ml_offset
+size_t attn_tc_workspace_floats(int Tq, int H, int Hkv, int splits, size_t* ml_offset);
 int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms);
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
-                         int* err, cudaStream_t s, const L2Prefetch& pf = L2Prefetch());
+                         int* err, cudaStream_t s, int kv_ready);
 // merge split-K (O, m, l) partials into out (dtype)
 void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, void* out, int* err, DT dt,
                               cudaStream_t s);

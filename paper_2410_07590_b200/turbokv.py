@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtkv_b200.so")
+LIB_PATH = os.environ.get("TKV_LIB_PATH") or os.path.join(_HERE, "libtkv_b200.so")  # override: variant builds (tools/)
 
 I32P, I64P, U64P = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_uint64)
 F32P, U8P = C.POINTER(C.c_float), C.POINTER(C.c_uint8)

@@ -56,6 +56,10 @@ ATTN_CASES = [
     (300, 300, 28, 4, 128, "causal"),
     (700, 700, 28, 4, 128, "indep"),
     (5, 1030, 32, 8, 128, "query"),
+    (1, 8256, 28, 4, 128, "query"),     # last-layer tail row (splits = 32)
+    (37, 2000, 32, 8, 128, "query"),    # group 4: 148 rows -> tile B partially filled
+    (64, 3000, 28, 4, 128, "query_hot"),  # large scores: exercises the lazy O rescale
+    (20, 20, 28, 4, 128, "causal"),     # one key tile, heavy masking
 ]
 
 
@@ -68,7 +72,13 @@ def test_attention_vs_torch(Tq, Tk, H, Hkv, d, kind, dtype):
     v = rng.uniform(-1, 1, (Tk, Hkv * d)).astype(np.float32)
     if dtype == "bf16":
         q, k, v = bf16_round(q), bf16_round(k), bf16_round(v)
-    if kind == "query":
+    if kind == "query_hot":
+        # growing score scale along the keys forces the running max up tile after tile
+        q = q * 6.0
+        k = k * np.linspace(0.2, 1.5, Tk, dtype=np.float32)[:, None]
+        if dtype == "bf16":
+            q, k = bf16_round(q), bf16_round(k)
+    if kind.startswith("query"):
         P = Tk - Tq
         lo, hi = np.zeros(Tq, np.int32), (P + np.arange(Tq)).astype(np.int32)
     elif kind == "causal":
