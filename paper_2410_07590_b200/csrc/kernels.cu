@@ -250,6 +250,17 @@ __device__ __forceinline__ void rotate_vec(uint4& v, const float2* cs) {
     }
 }
 
+// Work unit = (segment, layer, K|V, block of ROWS_PER_UNIT rows): fine-grained so the last wave of the
+// grid-stride loop is short (C2: 14 336 units over 1 184 resident CTAs). Every thread issues
+// all of its 16-byte loads (and, for keys, its cos/sin loads) before the first store.
+#ifndef GATHER_ROWS_CFG
+#define GATHER_ROWS_CFG 32
+#endif
+#ifndef GATHER_U_CFG
+#define GATHER_U_CFG 4
+#endif
+constexpr int GATHER_ROWS = GATHER_ROWS_CFG;
+
 template <typename T>
 __global__ void __launch_bounds__(256) gather_rope_vec_kernel(PoolTable pools, int page_tokens,
                                                               const GatherSeg* __restrict__ segs, int n_units, int L,
@@ -258,37 +269,49 @@ __global__ void __launch_bounds__(256) gather_rope_vec_kernel(PoolTable pools, i
     pdl_launch();
     pdl_wait();
     constexpr int N = Vec16<T>::N;
+    constexpr int U = GATHER_U_CFG;
     const int vec_per_row = kvd / N, half = d / 2;
+    const int blocks_per_page = (page_tokens + GATHER_ROWS - 1) / GATHER_ROWS;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const int seg = u / (2 * L), layer = (u / 2) % L, kv = u & 1;
+        const int rb = u % blocks_per_page;
+        const int rest = u / blocks_per_page;
+        const int seg = rest / (2 * L), layer = (rest / 2) % L, kv = rest & 1;
         const GatherSeg sg = segs[seg];
+        const int r0 = rb * GATHER_ROWS;
+        const int nrows = min(GATHER_ROWS, sg.n_tok - r0);
+        if (nrows <= 0) continue;
         const T* pool = reinterpret_cast<const T*>(pools.p[sg.pool]);  // local HBM or a peer GPU over NVLink
         const uint4* src = reinterpret_cast<const uint4*>(
-            pool + (((int64_t)sg.src_page * L + layer) * 2 + kv) * page_tokens * kvd);
-        uint4* dst = reinterpret_cast<uint4*>(cache + ((int64_t)(layer * 2 + kv) * cap + sg.dst_row) * kvd);
-        const int nv = sg.n_tok * vec_per_row;
+            pool + ((((int64_t)sg.src_page * L + layer) * 2 + kv) * page_tokens + r0) * kvd);
+        uint4* dst = reinterpret_cast<uint4*>(cache + ((int64_t)(layer * 2 + kv) * cap + sg.dst_row + r0) * kvd);
+        const int nv = nrows * vec_per_row;
         const bool rot = rotate && kv == 0;
-        constexpr int U = 4;
         for (int base = threadIdx.x; base < nv; base += blockDim.x * U) {
             uint4 r[U];
+            float2 c[U][N / 2];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int i = base + k * blockDim.x;
                 if (i < nv) r[k] = __ldcs(src + i);  // streaming read: store pages are not re-read
             }
+            if (rot) {
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    const int i = base + k * blockDim.x;
+                    if (i < nv) {
+                        const int row = i / vec_per_row, col = (i - row * vec_per_row) * N;
+                        const float2* cs = rope + (int64_t)(sg.pos0 + r0 + row) * half + (col % d) / 2;
+#pragma unroll
+                        for (int m = 0; m < N / 2; ++m) c[k][m] = __ldg(cs + m);
+                    }
+                }
+            }
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int i = base + k * blockDim.x;
                 if (i < nv) {
-                    if (rot) {
-                        const int row = i / vec_per_row, col = (i - row * vec_per_row) * N;
-                        const float2* cs = rope + (int64_t)(sg.pos0 + row) * half + (col % d) / 2;
-                        float2 c[N / 2];
-#pragma unroll
-                        for (int m = 0; m < N / 2; ++m) c[m] = __ldg(cs + m);
-                        rotate_vec<T>(r[k], c);
-                    }
-                    dst[i] = r[k];
+                    if (rot) rotate_vec<T>(r[k], c[k]);
+                    __stcs(dst + i, r[k]);  // the 470 MB request cache does not fit L2: stream it out
                 }
             }
         }
@@ -464,12 +487,12 @@ void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hk
 void launch_gather_rope(const PoolTable& pools, int page_tokens, const GatherSeg* segs, int n_segs, int L, int kvd,
                         int d, const float2* rope, void* cache, int64_t cap, int rotate, DT dt, int num_sms,
                         cudaStream_t s) {
-    const int n_units = n_segs * L * 2;
-    if (n_units == 0) return;
-    const int grid = n_units < num_sms * 8 ? n_units : num_sms * 8;
     const int vecN = 16 / (int)dt_size(dt);
     const bool vec_ok = (kvd % vecN == 0) && (d % vecN == 0) && (page_tokens * kvd * (int)dt_size(dt)) % 16 == 0 &&
-                        (cap * kvd * (int64_t)dt_size(dt)) % 16 == 0;
+                        (cap * kvd * (int64_t)dt_size(dt)) % 16 == 0 && (GATHER_ROWS * kvd * (int)dt_size(dt)) % 16 == 0;
+    const int n_units = n_segs * L * 2 * (vec_ok ? (page_tokens + GATHER_ROWS - 1) / GATHER_ROWS : 1);
+    if (n_units == 0) return;
+    const int grid = n_units < num_sms * 8 ? n_units : num_sms * 8;
     if (vec_ok) {
         DISPATCH_DT(dt, launch_k(gather_rope_vec_kernel<T>, grid, 256, 0, s, pools, page_tokens, segs, n_units, L,
                                                                        kvd, d, rope, (T*)cache, cap, rotate));
