@@ -82,7 +82,7 @@ typedef struct {
 #define TKV_FLAG_SIMT_ATTN 0x2    /* bf16: use the SIMT attention instead of tcgen05              */
 #define TKV_FLAG_NO_GRAPHS 0x4    /* do not capture prefill launch chains into CUDA graphs        */
 #define TKV_FLAG_NO_PDL 0x8       /* launch kernels without programmatic dependent launch          */
-#define TKV_FLAG_L2_PREFETCH 0x10  /* warm L2 with the next projections during attention (measured: no gain) */
+#define TKV_FLAG_L2_PREFETCH 0x10  /* reserved (attention-time L2 weight prefetch: measured no gain) */
 
 /* IngestStats (pipeline.hpp:35-39) */
 typedef struct {

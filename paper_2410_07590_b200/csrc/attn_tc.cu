@@ -228,6 +228,9 @@ __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 12
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -264,6 +267,7 @@ struct AttnArgs {
     int Tq, Tk, H, Hkv, splits, kv_ready;
     float scale;
     unsigned long long* trace;
+    L2Prefetch pf;  // weights of the next projections, warmed into L2 by idle producer lanes
 };
 
 // 10 warps: 3 share an SM sub-partition's 16K registers -> at most 168 registers per thread
@@ -350,6 +354,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
 
     if (warp == 8) {
+        if (lane != 0) {
+            // HBM is mostly idle during attention at query-prefill sizes: lanes 1-31 warm L2 with this CTA's
+            // share of the next projections' weights (bulk prefetch, no completion tracking)
+            const int ncta = gridDim.x * gridDim.y * gridDim.z;
+            for (int rg2 = 0; rg2 < 2; ++rg2) {
+                const size_t total = a.pf.bytes[rg2] & ~size_t(15);
+                if (!a.pf.ptr[rg2] || total == 0) continue;
+                const size_t share = ((total + ncta - 1) / ncta + 15) & ~size_t(15);
+                const size_t b0 = (size_t)cta_lin * share, b1 = min(b0 + share, total);
+                for (size_t off = b0 + (size_t)(lane - 1) * 65536; off < b1; off += (size_t)31 * 65536)
+                    prefetch_l2(static_cast<const uint8_t*>(a.pf.ptr[rg2]) + off, (uint32_t)min((size_t)65536, b1 - off));
+            }
+        }
         if (lane == 0) {  // ---------------- TMA producer ----------------
             bool waited = false;
             for (int j = 0; j < n; ++j) {
@@ -759,7 +776,7 @@ int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms) {
 
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
-                         int* err, cudaStream_t s, int kv_ready) {
+                         int* err, cudaStream_t s, int kv_ready, const L2Prefetch& pf) {
     TKV_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
     const int group = H / Hkv;
     dim3 grid((Tq * group + RG - 1) / RG, Hkv, splits);
@@ -780,6 +797,7 @@ void launch_attention_tc(const void* q, const void* k, const void* v, int kv_str
     a.kv_ready = kv_ready;
     a.scale = (float)(1.0 / sqrt((double)D));
     a.trace = g_trace_host;
+    a.pf = pf;
     const CUtensorMap tk = kv_map(k, Tk, kv_stride, kv_stride);
     const CUtensorMap tv = kv_map(v, Tk, kv_stride, kv_stride);
     launch_k(attn_tc_kernel, grid, THREADS, SMEM_BYTES, s, tk, tv, a);

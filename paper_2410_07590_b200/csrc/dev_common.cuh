@@ -25,7 +25,16 @@ __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.laun
 // multiplies by this per-row scale, since rms(x) . W = scale(x) * ((x * w) . W).
 __device__ __forceinline__ float row_scale(const float* __restrict__ ssp, int nb, int64_t t, int hidden, float eps) {
     float ss = 0.f;
-    for (int b = 0; b < nb; ++b) ss += ssp[t * nb + b];
+    const float* p = ssp + t * nb;
+    if (nb <= 32) {  // every load in flight at once (one memory round trip), summed in fixed order
+        float v[32];
+#pragma unroll
+        for (int b = 0; b < 32; ++b) v[b] = b < nb ? p[b] : 0.f;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) ss += v[b];
+    } else {
+        for (int b = 0; b < nb; ++b) ss += p[b];
+    }
     return 1.0f / sqrtf(ss / (float)hidden + eps);
 }
 

@@ -407,12 +407,16 @@ struct tkv_engine {
         if (p) ctx_free.emplace_back(bytes, p);
     }
 
+    size_t l2_prefetch_bytes = 0;  // TKV_L2_PREFETCH_MB (tuning knob)
+    int skip_mask = 0;             // TKV_TIMING_SKIP: drop kernels for cost attribution (results invalid)
+
     int pick_splits(int M, int N, int K, bool tc) const {
         const int bk = tc ? 64 : 16;
         const int tiles = tc ? gemm_tc_tiles(M, N) : ((M + 63) / 64) * ((N + 63) / 64);
         const int kb = (K + bk - 1) / bk;
-        // tcgen05 CTAs hold ~200 KB smem (1 per SM): round DOWN so splits x tiles fits one wave
-        int s = tc ? num_sms / tiles : (num_sms + tiles - 1) / tiles;
+        // tcgen05: gemm_tc_ctas_per_sm() persistent CTAs per SM; round DOWN so splits x tiles fills one wave of
+        // them (every resident CTA streams weights; at 1 unit per SM half the CTA slots idled)
+        int s = tc ? num_sms * gemm_tc_ctas_per_sm() / tiles : (num_sms + tiles - 1) / tiles;
         s = std::min(s, std::max(1, kb / 4));
         s = std::min(s, 16);
         s = std::max(s, 1);
@@ -539,7 +543,7 @@ void tkv_engine::forward(const Fwd& f) {
     for (int64_t l = 0; l < L; ++l) {
         // --- attention block ---
         int s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
-        {
+        if (!(skip_mask & 4)) {
             Scope sc(this, PC_EPI, 1);
             launch_qkv_epilogue(partial.as<float>(), s, T, (int)H, (int)Hkv, (int)d, f.pos, rope.as<float2>(), q.p,
                                 kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), f.row0, f.sc, (int)l, ssp.as<float>(), nb,
@@ -565,10 +569,21 @@ void tkv_engine::forward(const Fwd& f) {
             }
             Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);  // + the split-merge launch
             const void* qrows = static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es;
-            if (tc) {
+            if (skip_mask & 8) {
+            } else if (tc) {
+                // Weight-bound small forwards: warm L2 with this layer's O-proj weights and the head of its
+                // gate/up weights while attention runs (l2_prefetch_bytes total, 0 = off)
+                L2Prefetch pf;
+                if (T <= 128 && l2_prefetch_bytes > 0) {
+                    const size_t ob = (size_t)hid * qd * es, gb = (size_t)2 * I * hid * es;
+                    pf.ptr[0] = w_o[l];
+                    pf.bytes[0] = std::min(ob, l2_prefetch_bytes);
+                    pf.ptr[1] = w_gu[l];
+                    pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
+                }
                 launch_attention_tc(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
                                     f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream,
-                                    f.row0);
+                                    f.row0, pf);
             }
             else
                 launch_attention_simt(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
@@ -578,7 +593,7 @@ void tkv_engine::forward(const Fwd& f) {
         uint8_t* attn_rows = static_cast<uint8_t*>(attn.p);
         float* x_rows = x.as<float>() + r0 * hid;
         s = gemm(attn_rows, (int)qd, w_o[l], rows, (int)hid, (int)qd);
-        {
+        if (!(skip_mask & 1)) {
             Scope sc(this, PC_EPI, 1);
             launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, ones, xb.p, ssp.as<float>(), dt,
                             err.as<int>(), stream);
@@ -591,7 +606,7 @@ void tkv_engine::forward(const Fwd& f) {
                           gu_interleaved);
         }
         s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
-        {
+        if (!(skip_mask & 2)) {
             // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
             Scope sc(this, PC_EPI, 1);
             launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, ones, xb.p, ssp.as<float>(), dt,
@@ -1069,6 +1084,12 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         e->launches += 3 + 7 * e->L;
 
         e->err.ensure(64);
+        if (const char* pfm = getenv("TKV_L2_PREFETCH_MB")) e->l2_prefetch_bytes = (size_t)atol(pfm) << 20;
+        if (const char* sk = getenv("TKV_TIMING_SKIP")) e->skip_mask = atoi(sk);
+        if (const char* gk = getenv("TKV_GEMM_KNOBS")) {  // "stages,smem_kb,ctas_per_sm,evict_first" (tuning)
+            int st = 0, sm = 0, cps = 0, ef = 1;
+            if (sscanf(gk, "%d,%d,%d,%d", &st, &sm, &cps, &ef) >= 3) set_gemm_knobs(st, sm, cps, ef);
+        }
         TKV_CUDA(cudaMemsetAsync(e->err.p, 0, 64, e->stream));
         e->logits.ensure((size_t)V * 4);
         e->ensure_rope(e->opts.max_position > 0 ? e->opts.max_position - 1 : 32767);

@@ -427,6 +427,8 @@ bool gemm_tc_supported(int M, int N, int K, int lda) {
     return M >= 1 && N >= 1 && K >= 8 && (lda * 2) % 16 == 0 && (K * 2) % 16 == 0;
 }
 
+int gemm_tc_ctas_per_sm() { return std::max(1, g_knobs.ctas_per_sm); }
+
 int gemm_tc_tiles(int M, int N) {
     const bool swap = M <= 128;
     return ((N + 127) / 128) * (swap ? 1 : (M + 127) / 128);

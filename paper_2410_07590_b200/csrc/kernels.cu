@@ -72,10 +72,11 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
     return t;
 }
 
-// Block of 1024 columns of one row: 256 threads x 4. Writes x, xb = x * w and ssp[t][blockIdx.x].
+// Block of 1024 columns of one row: 256 threads x 4. Writes x, xb = x * w and, per warp (128 columns),
+// ssp_row[blockIdx.x * 8 + warp] (norm_blocks(hidden) slots per row).
 template <typename T>
 __device__ __forceinline__ void finish_row_block(float* __restrict__ xrow, const float* __restrict__ w, T* xbrow,
-                                                 float* ssp_slot, float (&v)[4], int c0, int hidden, float* red,
+                                                 float* ssp_row, float (&v)[4], int c0, int hidden, float* red,
                                                  int* err) {
     float ss = 0.f;
     bool bad = false;
@@ -90,8 +91,9 @@ __device__ __forceinline__ void finish_row_block(float* __restrict__ xrow, const
         }
     }
     if (bad) atomicOr(err, 2);
-    ss = block_sum(ss, red);
-    if (threadIdx.x == 0) *ssp_slot = ss;
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const int slot = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if ((threadIdx.x & 31) == 0 && slot < norm_blocks(hidden)) ssp_row[slot] = ss;
 }
 
 template <typename T>
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* tok, const fl
     pdl_wait();
     pdl_launch();
     __shared__ float red[32];
-    const int t = blockIdx.y, nb = gridDim.x;
+    const int t = blockIdx.y, nb = norm_blocks(hidden);
     const int id = tok[t];
     if (id < 0 || id >= vocab) {  // DomainError "token id outside vocab" (model.cpp:217-221)
         if (threadIdx.x == 0) atomicOr(err, 1);
@@ -113,8 +115,8 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* tok, const fl
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) v[e] = (c0 + e < hidden) ? emb[(int64_t)id * hidden + c0 + e] : 0.f;
-    finish_row_block(x + (int64_t)t * hidden, w, xb + (int64_t)t * hidden, ssp + (int64_t)t * nb + blockIdx.x, v, c0,
-                     hidden, red, err);
+    finish_row_block(x + (int64_t)t * hidden, w, xb + (int64_t)t * hidden, ssp + (int64_t)t * nb, v, c0, hidden, red,
+                     err);
 }
 
 // Residual add of the split-K partials (x += a . W), many CTAs per row (nb x T grid).
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(256) residual_kernel(float* x, const float* pa
     pdl_wait();
     __shared__ float red[32];
     const int64_t t = blockIdx.y;
-    const int nb = gridDim.x;
+    const int nb = norm_blocks(hidden);
     const int c0 = blockIdx.x * 1024 + threadIdx.x * 4;
     float v[4];
     float* xrow = x + t * hidden;
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(256) residual_kernel(float* x, const float* pa
             }
         }
     }
-    finish_row_block(xrow, w, xb + t * hidden, ssp + t * nb + blockIdx.x, v, c0, hidden, red, err);
+    finish_row_block(xrow, w, xb + t * hidden, ssp + t * nb, v, c0, hidden, red, err);
 }
 
 template <typename T>
@@ -455,7 +457,7 @@ void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t s) {
 
 void launch_embed(const int32_t* tok, int T_, const float* emb, int hidden, int vocab, const float* w, float* x,
                   void* xb, float* ssp, DT dt, int* err, cudaStream_t s) {
-    const dim3 grid(norm_blocks(hidden), T_);
+    const dim3 grid(row_ctas(hidden), T_);
     DISPATCH_DT(dt, launch_k(embed_kernel<T>, grid, 256, 0, s, tok, emb, hidden, vocab, w, x, (T*)xb, ssp, err));
     TKV_CUDA(cudaGetLastError());
 }
@@ -463,7 +465,7 @@ void launch_embed(const int32_t* tok, int T_, const float* emb, int hidden, int 
 void launch_residual(float* x, const float* partial, int splits, int T_, int hidden, const float* w, void* xb,
                      float* ssp, DT dt, int* err, cudaStream_t s) {
     const int64_t plane = (int64_t)T_ * hidden;
-    const dim3 grid(norm_blocks(hidden), T_);
+    const dim3 grid(row_ctas(hidden), T_);
     DISPATCH_DT(dt, launch_k(residual_kernel<T>, grid, 256, 0, s, x, partial, splits, plane, hidden, w, (T*)xb, ssp,
                              err));
     TKV_CUDA(cudaGetLastError());

@@ -44,8 +44,11 @@ void launch_init_rowmajor_f32(float* dst, uint64_t seed, uint64_t base, int64_t 
 void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t s);
 
 // RMSNorm folding (see dev_common.cuh:row_scale): x rows are produced together with xb = dtype(x * w) and
-// ssp[t][b] = sum of x^2 over the b-th 1024-column block of row t; nb = norm_blocks(hidden).
-inline int norm_blocks(int hidden) { return (hidden + 1023) / 1024; }
+// ssp[t][b] = sum of x^2 over the b-th 128-column block of row t; nb = norm_blocks(hidden).
+// ssp holds one partial sum per 128-column block (the GEMM n-tile width, so a fused GEMM epilogue can
+// produce it per tile); embed/residual kernels cover 1024 columns per CTA (8 blocks, one per warp).
+__host__ __device__ inline int norm_blocks(int hidden) { return (hidden + 127) / 128; }
+inline int row_ctas(int hidden) { return (hidden + 1023) / 1024; }
 // x[t] = emb[tok[t]] (fp32), xb, ssp. Errors (token outside vocab) set *err.
 void launch_embed(const int32_t* tok, int T, const float* emb, int hidden, int vocab, const float* w, float* x,
                   void* xb, float* ssp, DT dt, int* err, cudaStream_t s);
@@ -116,6 +119,7 @@ void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K
 bool gemm_tc_supported(int M, int N, int K, int lda);
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first);
 int gemm_tc_tiles(int M, int N);
+int gemm_tc_ctas_per_sm();  // resident GEMM CTAs per SM the launcher plans for (knob)
 // Returns the number of split-K partial planes actually written (<= splits: every split is non-empty).
 // The SwiGLU epilogue applies the folded RMSNorm scale row_scale(ssp, token) (ssp/nb/eps: see launch_residual).
 int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
@@ -135,6 +139,11 @@ void launch_attention_simt(const void* q, const void* k, const void* v, int kv_s
                            const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int d, int splits,
                            const AttnWork& ws, int* err, DT dt, cudaStream_t s);
 
+// Up to two global regions the attention kernel warms into L2 (bulk prefetch from idle producer lanes).
+struct L2Prefetch {
+    const void* ptr[2] = {nullptr, nullptr};
+    size_t bytes[2] = {0, 0};
+};
 // tcgen05/TMEM/TMA attention (attn_tc.cu): head_size 128, bf16. Same predicate and workspace layout as
 // SIMT; split-K partials (bf16 O/l) are merged by a PDL-launched combine kernel. Key rows
 // < kv_ready were written before the current forward began and are loaded before griddepcontrol.wait.
@@ -146,7 +155,7 @@ size_t attn_tc_workspace_floats(int Tq, int H, int Hkv, int splits, size_t* ml_o
 int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms);
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
-                         int* err, cudaStream_t s, int kv_ready);
+                         int* err, cudaStream_t s, int kv_ready, const L2Prefetch& pf = L2Prefetch());
 // merge split-K (O, m, l) partials into out (dtype)
 void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, void* out, int* err, DT dt,
                               cudaStream_t s);
