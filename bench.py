@@ -376,6 +376,19 @@ def run_ours(args):
             dist.barrier()
             dist.destroy_process_group()
         return
+    # DRAM traffic per launch of the dominant kernels from the round's committed `ncu --set full` captures
+    # (profiles/ncu_traffic.json, written by tools/ncu_collect.py); null when absent
+    ncu_traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            ncu_traffic = json.load(f).get("kernels", {})
+    except (OSError, ValueError):
+        pass
+
+    def traffic_of(k):
+        v = ncu_traffic.get(k)
+        return v[0]["dram_bytes"] if v else None
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -396,12 +409,12 @@ def run_ours(args):
                                "gemm": gemm_ms / prof_steps, "epilogue": epi_ms / prof_steps},
         "roofline": {"kernel": "gather_rope", "bound": "hbm", "achieved": achieved,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                     "traffic": None, "peak_source": peak_kind,
+                     "traffic": traffic_of("gather_rope"), "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": kv_bytes, "avg_launch_ms": gather_avg_ms},
         "attention_roofline": {"bound": "tensor", "achieved": attn_flops / (attn_ms / prof_steps / 1e3) / 1e12,
                                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                                "frac": attn_flops / (attn_ms / prof_steps / 1e3) / 1e12 / peaks["bf16_tflops"],
-                               "flops_per_request": attn_flops},
+                               "flops_per_request": attn_flops, "traffic": traffic_of("attn_tc_kernel")},
         "e2e": {"value": e2e_value, "unit": UNIT, "p50_ttft_ms": e2e_p50 * 1e3,
                 "h2d_bytes_per_step": QUERY_TOKENS * 4 + N_CHUNKS * 8,
                 "d2h_bytes_per_step": cfg.vocab_size * 4},
