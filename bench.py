@@ -359,6 +359,38 @@ def run_ours(args):
                 ts.append(time.perf_counter() - t0)
         naive[tag] = statistics.median(ts) * 1e3
 
+    # C5 (BASELINE configs[4]) sample: offline KV precompute = block-diagonal prefill of 512-token chunks into
+    # the paged store, ring-overwritten (evicted after each round); 32 chunks (16 384 tokens) per forward
+    c5 = None
+    if args.c5_rounds > 0:
+        rng = np.random.default_rng(0xC5)
+        per_round = 32
+        flop_tok_gemm = 2 * cfg.hidden_size * (cfg.head_num + 2 * cfg.kv_head_num) * cfg.head_size \
+            + 2 * cfg.head_num * cfg.head_size * cfg.hidden_size + 6 * cfg.hidden_size * cfg.intermediate_size
+        flop_tok_qkv = 2 * cfg.hidden_size * (cfg.head_num + 2 * cfg.kv_head_num) * cfg.head_size
+        c = CHUNK_TOKENS
+        # the last layer stops after its QKV projection (only K/V are needed); attention is causal within a chunk
+        flop_chunk = c * ((cfg.layer_num - 1) * flop_tok_gemm + flop_tok_qkv) \
+            + (cfg.layer_num - 1) * 4 * cfg.head_num * cfg.head_size * c * (c + 1) // 2
+        ts = []
+        for r in range(1 + args.c5_rounds):
+            pl = [rng.integers(97, 123, CHUNK_TOKENS - 2).astype(np.int32) for _ in range(per_round)]
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            cids = eng.ingest_chunks(pl)
+            torch.cuda.synchronize(dev)
+            if r:
+                ts.append(time.perf_counter() - t0)
+            for cid in cids:
+                eng.store_evict(cid)
+        sec = statistics.median(ts)
+        c5 = {"workload": "C5 sample: block-diagonal prefill of 32 x 512-token chunks per forward into the paged "
+                          f"store (ring: evicted after each round), median of {args.c5_rounds} rounds",
+              "chunks_per_s": per_round / sec, "tokens_per_s": per_round * c / sec,
+              "tflops": per_round * flop_chunk / sec / 1e12,
+              "tensor_frac": per_round * flop_chunk / sec / 1e12 / peaks["bf16_tflops"],
+              "flop_per_chunk": flop_chunk, "kv_bytes_per_chunk": c * cfg.layer_num * 2 * cfg.kv_dim * 2}
+
     cpu_baseline = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu, ncores = host_info()
@@ -403,6 +435,7 @@ def run_ours(args):
         "ttft_speedup_vs_full_concat": naive["causal"] / p50,
         "kv_inject_gbs": achieved,
         "ingest_s_16_chunks": ingest_s,
+        "c5_ingest": c5,
         "store": {"sharding": f"by document over {ws} GPU(s)", "remote_chunk_token_fraction": remote_frac,
                   "remote_policy": args.remote if ws > 1 else "n/a"},
         "device_ms_per_step": {"gather_rope": gather_ms / prof_steps, "attention": attn_ms / prof_steps,
@@ -438,6 +471,7 @@ def main():
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--turbo-only", action="store_true", help="timed turbo steps only (for ncu captures)")
+    ap.add_argument("--c5-rounds", type=int, default=3, help="C5 offline-precompute sample rounds (0 = skip)")
     ap.add_argument("--remote", choices=["direct", "fetch"], default="direct",
                     help="N>1: read peer-owned chunks over NVLink every request, or copy them once")
     args = ap.parse_args()

@@ -143,6 +143,10 @@ tkv_status tkv_export_tkvc(tkv_engine* eng, uint64_t chunk_id, const char* path)
 tkv_status tkv_store_contains(const tkv_engine* eng, uint64_t chunk_id, int* out);
 tkv_status tkv_store_chunk_tokens(const tkv_engine* eng, uint64_t chunk_id, int64_t* out);
 tkv_status tkv_store_count(const tkv_engine* eng, int64_t* chunks, int64_t* pages_used, int64_t* pages_total);
+/* Drop a chunk from the store and return its pages (no reference analogue: the reference store is a directory
+ * of TKVC files, kvstore.cpp:78-211; this is the capacity policy of the HBM store). Contexts assembled earlier
+ * keep their gathered KV; only their unrotated re-read (tkv_context_read_kv, rotated=0) then fails StaleCache. */
+tkv_status tkv_store_evict(tkv_engine* eng, uint64_t chunk_id);
 /* Copy one stored (unrotated) tensor to host as float32 [tokens, kv_head_num*head_size]. */
 tkv_status tkv_store_read(const tkv_engine* eng, uint64_t chunk_id, int64_t layer, tkv_kv_which which,
                           float* host_out, int64_t capacity_elems);

@@ -272,6 +272,7 @@ struct tkv_engine {
     int64_t page_tokens = 64, n_pages = 0;
     size_t page_bytes = 0;
     std::vector<int32_t> free_pages;
+    uint64_t store_epoch = 0;  // bumped by every eviction (contexts that re-read store pages check it)
     std::unordered_map<uint64_t, Chunk> chunks;
     PoolTable pools;                     // slot 0 = pool.p; peers attached via IPC or same-process P2P
     std::vector<void*> ipc_opened;       // peer pools opened with cudaIpcOpenMemHandle (closed on destroy)
@@ -477,6 +478,7 @@ struct tkv_context {
     std::vector<float> last_logits;
     // injected chunk rows [0, chunk_rows): where they came from (unrotated export re-gathers them)
     std::vector<GatherSeg> chunk_segs;
+    uint64_t store_epoch = 0;  // engine store epoch when chunk_segs were taken
     int64_t chunk_rows = 0;
     // predicate of the last forward over this context
     std::vector<int32_t> last_lo, last_hi;
@@ -805,6 +807,7 @@ tkv_context* assemble_impl(tkv_engine* e, const uint64_t* ids, int64_t n, int mo
     c->total = P;
     c->chunk_rows = P;
     c->chunk_segs = segs;
+    c->store_epoch = e->store_epoch;
     c->next_position = mode == TKV_POS_REORDERED ? running : max_len;  // pipeline.cpp:160-162
     c->mask_mode = TKV_MASK_INDEPENDENT;
     if (!segs.empty()) {
@@ -1391,6 +1394,18 @@ tkv_status tkv_store_contains(const tkv_engine* e, uint64_t id, int* out) {
     });
 }
 
+tkv_status tkv_store_evict(tkv_engine* e, uint64_t id) {
+    return guard([&] {
+        need(e, "engine");
+        auto it = e->chunks.find(id);
+        if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
+        if (it->second.slot == 0)  // local pages return to the pool; peer-registered chunks only drop the entry
+            for (int32_t p : it->second.pages) e->free_pages.push_back(p);
+        e->chunks.erase(it);
+        e->store_epoch += 1;
+    });
+}
+
 tkv_status tkv_store_chunk_tokens(const tkv_engine* e, uint64_t id, int64_t* out) {
     return guard([&] {
         need(e, "engine");
@@ -1595,6 +1610,8 @@ tkv_status tkv_context_read_kv(const tkv_context* c, int64_t layer, tkv_kv_which
             launch_to_f32(e->kv_plane(cc, layer, (int)which), rows * e->kvd, f32.as<float>(), e->dt, e->stream);
         } else {
             // injected rows: re-gather the unrotated store pages (identity rotation = bit-exact)
+            if (c->chunk_rows > 0 && c->store_epoch != e->store_epoch)
+                fail(TKV_ERR_STALE_CACHE, "store chunks were evicted since this context was assembled");
             if (c->chunk_rows > 0) {
                 DevMem scratch, segs;
                 const int64_t cap = c->chunk_rows;

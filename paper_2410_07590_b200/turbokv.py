@@ -126,6 +126,7 @@ def lib():
         L.tkv_store_contains.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int)]
         L.tkv_store_chunk_tokens.argtypes = [C.c_void_p, C.c_uint64, I64P]
         L.tkv_store_count.argtypes = [C.c_void_p, I64P, I64P, I64P]
+        L.tkv_store_evict.argtypes = [C.c_void_p, C.c_uint64]
         L.tkv_store_read.argtypes = [C.c_void_p, C.c_uint64, C.c_int64, C.c_int, F32P, C.c_int64]
         L.tkv_assemble.argtypes = [C.c_void_p, U64P, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]
         L.tkv_prefill_query.argtypes = [C.c_void_p, C.c_void_p, I32P, C.c_int64, F32P, C.POINTER(_Flops)]
@@ -420,6 +421,9 @@ class Engine:
 
     def export_tkvc(self, chunk_id: int, path: str) -> None:
         _check(lib().tkv_export_tkvc(self._h, chunk_id, path.encode()))
+
+    def store_evict(self, chunk_id: int) -> None:
+        _check(lib().tkv_store_evict(self._h, chunk_id))
 
     def store_contains(self, chunk_id: int) -> bool:
         out = C.c_int()

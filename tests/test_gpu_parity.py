@@ -344,3 +344,33 @@ def test_remote_chunks_gathered_from_peer_pool(policy):
         assert a.remote_bytes() == 3 * 64 * per_token
     a.close()
     b.close()
+
+
+@pytest.mark.gpu
+def test_store_evict_reuses_pages_and_guards_stale_reads():
+    cfg = T.ModelConfig.toy()
+    eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=512)
+    payloads = [O.random_text_tokens(3000 + i, 126) for i in range(3)]
+    ids = eng.ingest_chunks(payloads)
+    n0, used0, total = eng.store_count()
+    ctx = eng.assemble(ids[:2], T.PositionMode.Reordered)
+    before = eng.prefill_query(ctx, O.random_text_tokens(7, 16))[0]
+    eng.store_evict(ids[0])
+    assert not eng.store_contains(ids[0]) and eng.store_contains(ids[1])
+    assert eng.store_count()[1] == used0 - 2  # a 128-token chunk owns two 64-token pages
+    with pytest.raises(T.StaleCacheError):
+        ctx.read_kv(0, "k", rotated=False)
+    ctx.read_kv(0, "k", rotated=True)  # the gathered cache itself is unaffected
+    with pytest.raises(T.NotFoundError):
+        eng.store_evict(ids[0])
+    with pytest.raises(T.NotFoundError):
+        eng.assemble(ids[:1], T.PositionMode.Reordered)
+    # re-ingest: same content id, pages reused; logits agree to bf16 tolerance (a lone 128-token chunk takes
+    # the swapped GEMM tiling, the original 3-chunk batch the normal one: different fp32 summation order)
+    assert eng.ingest_chunks(payloads[:1])[0] == ids[0]
+    ctx2 = eng.assemble(ids[:2], T.PositionMode.Reordered)
+    after = eng.prefill_query(ctx2, O.random_text_tokens(7, 16))[0]
+    assert np.abs(before - after).max() <= 2e-2 * np.abs(before).max()
+    ctx.close()
+    ctx2.close()
+    eng.close()
