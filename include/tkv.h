@@ -163,6 +163,12 @@ tkv_status tkv_prefill_query(tkv_engine* eng, tkv_context* ctx, const int32_t* q
 /* Same, with tokens and logits already in device memory (no host copies, no sync). */
 tkv_status tkv_prefill_query_device(tkv_engine* eng, tkv_context* ctx, const int32_t* d_query, int64_t n,
                                     float* d_logits_out);
+/* Batched query prefill (BASELINE config 3: batch 32): request r prefills queries[offsets[r], offsets[r+1]) over
+ * its own context ctxs[r] exactly as tkv_prefill_query would (pipeline.cpp:166-186); the projections and the MLP
+ * run once over all requests' tokens (one large-M GEMM per projection), attention per request on its own cache.
+ * logits_out: [n_req][vocab] (last token of each request). flops accumulates every request's cost. */
+tkv_status tkv_prefill_query_batch(tkv_engine* eng, tkv_context* const* ctxs, int64_t n_req, const int32_t* queries,
+                                   const int64_t* offsets, float* logits_out, tkv_flops* flops);
 /* Full-concatenation prefill. Engine::naive_prefill (pipeline.hpp:104-108; src/pipeline.cpp:188-229).
  * `framed` holds n_chunks FRAMED chunks back to back (offsets[n_chunks+1]). ctx_out is optional. */
 tkv_status tkv_naive_prefill(tkv_engine* eng, const int32_t* framed, const int64_t* offsets, int64_t n_chunks,

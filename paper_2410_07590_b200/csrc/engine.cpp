@@ -459,6 +459,13 @@ struct tkv_engine {
         bool logits = true;   // last-row logits into this->logits
         bool kv_only = false; // chunk ingest: stop after the last layer's QKV
         StoreScatter sc{};
+        // batched query prefill (tkv_prefill_query_batch): request r owns tokens [tok0, tok0 + n) of this forward,
+        // its K/V go to its own context at rows [row0, row0 + n); logits of its last token -> logits[r]
+        struct Req {
+            tkv_context* ctx;
+            int tok0, n, row0;
+        };
+        std::vector<Req> reqs;
     };
     void forward(const Fwd& f);
     void check_err(const char* where);
@@ -528,6 +535,7 @@ void tkv_engine::check_err(const char* where) {
 // One decoder forward (model.cpp:198-272) over T new tokens whose K/V go to cache rows [row0, row0+T).
 void tkv_engine::forward(const Fwd& f) {
     const int T = f.T, Tk = f.row0 + f.T;
+    const bool batch = !f.reqs.empty();
     const size_t es = dt_size(dt);
     const float eps = (float)cfg.norm_eps;
     x.ensure((size_t)T * hid * 4);
@@ -545,7 +553,15 @@ void tkv_engine::forward(const Fwd& f) {
     for (int64_t l = 0; l < L; ++l) {
         // --- attention block ---
         int s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
-        if (!(skip_mask & 4)) {
+        if (batch) {
+            Scope sc(this, PC_EPI, (int)f.reqs.size());
+            for (const Fwd::Req& r : f.reqs)
+                launch_qkv_epilogue(partial.as<float>() + (size_t)r.tok0 * nqkv, s, r.n, (int)H, (int)Hkv, (int)d,
+                                    f.pos + r.tok0, rope.as<float2>(), static_cast<uint8_t*>(q.p) + (size_t)r.tok0 * qd * es,
+                                    kv_plane(r.ctx, l, 0), kv_plane(r.ctx, l, 1), r.row0, StoreScatter{}, (int)l,
+                                    ssp.as<float>() + (size_t)r.tok0 * nb, nb, (int)hid, eps, dt, stream,
+                                    (int64_t)T * nqkv);
+        } else if (!(skip_mask & 4)) {
             Scope sc(this, PC_EPI, 1);
             launch_qkv_epilogue(partial.as<float>(), s, T, (int)H, (int)Hkv, (int)d, f.pos, rope.as<float2>(), q.p,
                                 kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), f.row0, f.sc, (int)l, ssp.as<float>(), nb,
@@ -553,24 +569,24 @@ void tkv_engine::forward(const Fwd& f) {
         }
         if (f.kv_only && l == L - 1) break;
         // In the last layer only the final row feeds the logits: attention, O-proj and the MLP run on it alone.
-        const bool tail = (l == L - 1) && f.logits;
+        const bool tail = (l == L - 1) && f.logits && !batch;
         const int rows = tail ? 1 : T;
         const int64_t r0 = tail ? T - 1 : 0;
-        {
+        auto attend = [&](const void* qrows, tkv_context* actx, const int32_t* lo, const int32_t* hi, void* out,
+                          int arows, int aTk, int kv_ready) {
             const bool tc = dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_ATTN) && attention_tc_supported((int)d, dt);
-            const int splits = tc ? attn_tc_pick_splits(rows, (int)H, (int)Hkv, Tk, num_sms)
-                                  : attn_pick_splits(rows, (int)H, (int)Hkv, Tk, num_sms);
+            const int splits = tc ? attn_tc_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms)
+                                  : attn_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms);
             AttnWork ws;
             if (splits > 1) {
-                size_t mloff = (size_t)splits * rows * H * d;
-                const size_t fl = tc ? attn_tc_workspace_floats(rows, (int)H, (int)Hkv, splits, &mloff)
-                                     : attn_workspace_floats(rows, (int)H, (int)d, splits);
+                size_t mloff = (size_t)splits * arows * H * d;
+                const size_t fl = tc ? attn_tc_workspace_floats(arows, (int)H, (int)Hkv, splits, &mloff)
+                                     : attn_workspace_floats(arows, (int)H, (int)d, splits);
                 attn_ws.ensure(fl * sizeof(float));
                 ws.o = attn_ws.as<float>();
                 ws.ml = ws.o + mloff;
             }
             Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);  // + the split-merge launch
-            const void* qrows = static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es;
             if (skip_mask & 8) {
             } else if (tc) {
                 // Weight-bound small forwards: warm L2 with this layer's O-proj weights and the head of its
@@ -583,14 +599,20 @@ void tkv_engine::forward(const Fwd& f) {
                     pf.ptr[1] = w_gu[l];
                     pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
                 }
-                launch_attention_tc(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
-                                    f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream,
-                                    f.row0, pf);
+                launch_attention_tc(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
+                                    aTk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream, kv_ready, pf);
+            } else {
+                launch_attention_simt(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
+                                      aTk, (int)H, (int)Hkv, (int)d, splits, ws, err.as<int>(), dt, stream);
             }
-            else
-                launch_attention_simt(qrows, kv_plane(f.ctx, l, 0), kv_plane(f.ctx, l, 1), (int)kvd, f.lo + r0,
-                                      f.hi + r0, attn.p, rows, Tk, (int)H, (int)Hkv, (int)d, splits, ws,
-                                      err.as<int>(), dt, stream);
+        };
+        if (batch) {
+            for (const Fwd::Req& r : f.reqs)
+                attend(static_cast<uint8_t*>(q.p) + (size_t)r.tok0 * qd * es, r.ctx, f.lo + r.tok0, f.hi + r.tok0,
+                       static_cast<uint8_t*>(attn.p) + (size_t)r.tok0 * qd * es, r.n, r.row0 + r.n, r.row0);
+        } else {
+            attend(static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es, f.ctx, f.lo + r0, f.hi + r0, attn.p, rows, Tk,
+                   f.row0);
         }
         uint8_t* attn_rows = static_cast<uint8_t*>(attn.p);
         float* x_rows = x.as<float>() + r0 * hid;
@@ -615,7 +637,16 @@ void tkv_engine::forward(const Fwd& f) {
                             err.as<int>(), stream);
         }
     }
-    if (f.logits) {
+    if (f.logits && batch) {
+        logits.ensure((size_t)f.reqs.size() * V * 4);
+        Scope sc(this, PC_OTHER, (int)f.reqs.size());
+        for (size_t i = 0; i < f.reqs.size(); ++i) {  // final_norm folded; the last token of each request
+            const int last = f.reqs[i].tok0 + f.reqs[i].n - 1;
+            launch_lm_head(static_cast<uint8_t*>(xb.p) + (size_t)last * hid * es, w_lm, (int)hid, (int)V,
+                           logits.as<float>() + i * V, ssp.as<float>() + (size_t)last * nb, nb, eps, dt,
+                           err.as<int>(), stream);
+        }
+    } else if (f.logits) {
         // after the tail layer, h row 0 holds final_norm(x) of the last token
         Scope sc(this, PC_OTHER, 1);
         launch_lm_head(xb.p, w_lm, (int)hid, (int)V, logits.as<float>(), ssp.as<float>(), nb, eps, dt, err.as<int>(),
@@ -1479,6 +1510,70 @@ tkv_status tkv_prefill_query(tkv_engine* e, tkv_context* c, const int32_t* query
         extend(e, c, query, nullptr, n, lg.data(), nullptr);
         if (logits_out) std::memcpy(logits_out, lg.data(), lg.size() * 4);
         flops_add(e, fl, n, P + n);
+    });
+}
+
+tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int64_t n_req, const int32_t* queries,
+                                   const int64_t* offsets, float* logits_out, tkv_flops* fl) {
+    return guard([&] {
+        need(e, "engine");
+        need(ctxs, "contexts");
+        need(offsets, "offsets");
+        if (n_req <= 0) fail(TKV_ERR_DOMAIN, "prefill_query_batch: empty batch");
+        std::set<const tkv_context*> seen;
+        for (int64_t r = 0; r < n_req; ++r) {
+            need(ctxs[r], "context");
+            if (ctxs[r]->eng != e) fail(TKV_ERR_STALE_CACHE, "context was assembled under a different model");
+            if (!seen.insert(ctxs[r]).second) fail(TKV_ERR_CONFIG, "prefill_query_batch: a context appears twice");
+            if (offsets[r + 1] - offsets[r] <= 0) fail(TKV_ERR_DOMAIN, "prefill_query: empty query");  // pipeline.cpp:169
+        }
+        const int64_t T = offsets[n_req] - offsets[0];
+        need(queries, "queries");
+        check_tokens(e, queries + offsets[0], T);
+        e->bind();
+        Stage s;
+        tkv_engine::Fwd f;
+        int64_t max_pos = 0;
+        for (int64_t r = 0; r < n_req; ++r) {
+            tkv_context* c = ctxs[r];
+            const int64_t n = offsets[r + 1] - offsets[r], P = c->total;
+            ensure_cap(e, c, P + n);
+            f.reqs.push_back({c, (int)s.pos.size(), (int)n, (int)P});
+            for (int64_t i = 0; i < n; ++i) {
+                s.tok.push_back(queries[offsets[r] + i]);
+                s.pos.push_back((int32_t)(c->next_position + i));
+                s.lo.push_back(0);
+                s.hi.push_back((int32_t)(P + i));  // causal_rows(n, P) of this request
+            }
+            max_pos = std::max(max_pos, c->next_position + n);
+        }
+        e->ensure_rope(max_pos);
+        upload_stage(e, s, true);
+        f.tok = e->d_tok.as<int32_t>();
+        f.T = (int)T;
+        f.pos = e->d_pos.as<int32_t>();
+        f.lo = e->d_lo.as<int32_t>();
+        f.hi = e->d_hi.as<int32_t>();
+        f.logits = true;
+        e->forward(f);
+        std::vector<float> lg((size_t)n_req * e->V);
+        TKV_CUDA(cudaMemcpyAsync(lg.data(), e->logits.p, lg.size() * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->check_err("prefill_query_batch");
+        if (logits_out) std::memcpy(logits_out, lg.data(), lg.size() * 4);
+        for (int64_t r = 0; r < n_req; ++r) {  // the same bookkeeping as prefill_query (pipeline.cpp:166-186)
+            tkv_context* c = ctxs[r];
+            const int64_t n = offsets[r + 1] - offsets[r], P = c->total;
+            Stage sr;
+            sr.lo.assign(s.lo.begin() + f.reqs[r].tok0, s.lo.begin() + f.reqs[r].tok0 + n);
+            sr.hi.assign(s.hi.begin() + f.reqs[r].tok0, s.hi.begin() + f.reqs[r].tok0 + n);
+            remember_mask(c, sr, P + n);
+            for (int64_t i = 0; i < n; ++i) c->positions.push_back(c->next_position + i);
+            c->total = P + n;
+            c->extend_query_segment(n);
+            c->next_position += n;
+            c->last_logits.assign(lg.begin() + r * e->V, lg.begin() + (r + 1) * e->V);
+            flops_add(e, fl, n, P + n);
+        }
     });
 }
 

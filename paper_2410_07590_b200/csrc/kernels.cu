@@ -178,11 +178,12 @@ __global__ void swiglu_kernel(const float* partial, int splits, int T_, int inte
 template <typename T>
 __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
                                     const int32_t* pos, const float2* rope, T* q, T* kc, T* vc, int row0,
-                                    StoreScatter sc, int layer, const float* ssp, int nb, int hidden, float eps) {
+                                    StoreScatter sc, int layer, const float* ssp, int nb, int hidden, float eps,
+                                    int64_t plane) {
     pdl_launch();
     pdl_wait();
     const int qd = H * d, kvd = Hkv * d, N = qd + 2 * kvd, half = d / 2;
-    const int64_t pairs = (int64_t)T_ * (N / 2), plane = (int64_t)T_ * N;
+    const int64_t pairs = (int64_t)T_ * (N / 2);
     int64_t cached_t = -1;
     float rs = 0.f;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * blockDim.x) {
@@ -479,10 +480,12 @@ void launch_swiglu(const float* partial, int splits, int T_, int inter, void* ac
 
 void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hkv, int d, const int32_t* pos,
                          const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc, int layer,
-                         const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s) {
+                         const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s, int64_t plane) {
     const int64_t pairs = (int64_t)T_ * (H + 2 * Hkv) * d / 2;
-    DISPATCH_DT(dt, launch_k(qkv_epilogue_kernel<T>, grid_for(pairs, 256), 256, 0, s, 
-                        partial, splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden, eps));
+    if (plane <= 0) plane = (int64_t)T_ * (H + 2 * Hkv) * d;
+    DISPATCH_DT(dt, launch_k(qkv_epilogue_kernel<T>, grid_for(pairs, 256), 256, 0, s,
+                        partial, splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden,
+                        eps, plane));
     TKV_CUDA(cudaGetLastError());
 }
 

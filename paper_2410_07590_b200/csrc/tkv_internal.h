@@ -75,7 +75,9 @@ struct StoreScatter {
 // The projections were computed from xb: every output is first multiplied by row_scale(ssp, t).
 void launch_qkv_epilogue(const float* partial, int splits, int T, int H, int Hkv, int d, const int32_t* pos,
                          const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc,
-                         int layer, const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s);
+                         int layer, const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s,
+                         int64_t plane = 0);  // split-plane stride in floats (0 = T * N; batched forwards pass
+                                              // the whole batch's plane and a row-offset partial pointer)
 
 // KV gather + fused RoPE: one descriptor per (chunk page -> request rows) segment.
 struct GatherSeg {

@@ -127,6 +127,8 @@ def lib():
         L.tkv_store_chunk_tokens.argtypes = [C.c_void_p, C.c_uint64, I64P]
         L.tkv_store_count.argtypes = [C.c_void_p, I64P, I64P, I64P]
         L.tkv_store_evict.argtypes = [C.c_void_p, C.c_uint64]
+        L.tkv_prefill_query_batch.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int64, I32P, I64P, F32P,
+                                              C.POINTER(_Flops)]
         L.tkv_store_read.argtypes = [C.c_void_p, C.c_uint64, C.c_int64, C.c_int, F32P, C.c_int64]
         L.tkv_assemble.argtypes = [C.c_void_p, U64P, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]
         L.tkv_prefill_query.argtypes = [C.c_void_p, C.c_void_p, I32P, C.c_int64, F32P, C.POINTER(_Flops)]
@@ -458,6 +460,20 @@ class Engine:
         if counter is not None:
             counter._add(fl)
         return out[None, :]
+
+    def prefill_query_batch(self, ctxs, queries, counter: FlopCounter | None = None) -> np.ndarray:
+        """tkv_prefill_query_batch: one forward over every request's query tokens; returns [n_req, vocab]."""
+        qs = [_i32(q) for q in queries]
+        flat = _i32(np.concatenate(qs))
+        offs = np.ascontiguousarray(np.concatenate([[0], np.cumsum([len(q) for q in qs])]), np.int64)
+        hs = (C.c_void_p * len(ctxs))(*[c.handle for c in ctxs])
+        out = np.zeros((len(ctxs), self.config.vocab_size), np.float32)
+        fl = _Flops()
+        _check(lib().tkv_prefill_query_batch(self._h, hs, len(ctxs), _p(flat, I32P), _p(offs, I64P), _p(out, F32P),
+                                             C.byref(fl)))
+        if counter is not None:
+            counter._add(fl)
+        return out
 
     def prefill_query_device(self, ctx: AssembledContext, d_tokens: int, n: int, d_logits: int) -> None:
         _check(lib().tkv_prefill_query_device(self._h, ctx.handle, C.c_void_p(d_tokens), n, C.c_void_p(d_logits)))

@@ -374,3 +374,44 @@ def test_store_evict_reuses_pages_and_guards_stale_reads():
     ctx.close()
     ctx2.close()
     eng.close()
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
+@pytest.mark.parametrize("name", ["c1", "ragged", "qwen1"])
+def test_batched_prefill_vs_golden(golden, name, dtype, tol):
+    """tkv_prefill_query_batch (C3's batched path): a reordered and a composite context of the same chunks in ONE
+    forward, each against the reference's logits, plus a third request over a chunk subset against the same
+    engine's single-request prefill; context bookkeeping identical to prefill_query."""
+    meta, A = golden
+    m = meta[name]
+    eng = engine(cfg_t(m), m["seed"], dtype)
+    ids = eng.ingest_chunks(payloads(A, name))
+    q = A[f"{name}.query"]
+    ctxs = [eng.assemble(ids, T.PositionMode.Reordered), eng.assemble(ids, T.PositionMode.Composite),
+            eng.assemble(ids[::-1][:max(1, len(ids) - 1)], T.PositionMode.Reordered)]
+    q3 = np.asarray(q[: max(1, len(q) // 2)])
+    logits = eng.prefill_query_batch(ctxs, [q, q, q3])
+    for r, tag in ((0, "reordered"), (1, "composite")):
+        ref = A[f"{name}.turbo_{tag}.logits"]
+        assert_close(logits[r], ref, tol)
+        assert_argmax(logits[r], ref, tol)
+        assert ctxs[r].total_tokens() == len(ctxs[r].positions)
+        assert ctxs[r].next_position == m[f"{tag}.next_position"] + len(q)
+    with eng.assemble(ids[::-1][:max(1, len(ids) - 1)], T.PositionMode.Reordered) as single:
+        ref3 = eng.prefill_query(single, q3)[0]
+        assert_close(logits[2], ref3, tol)
+        assert np.array_equal(single.positions, ctxs[2].positions)
+    for c in ctxs:
+        c.close()
+
+
+def test_batched_prefill_rejects_bad_batches(golden):
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], "bf16")
+    ids = eng.ingest_chunks(payloads(A, "c1"))
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        with pytest.raises(T.ConfigError):
+            eng.prefill_query_batch([ctx, ctx], [A["c1.query"], A["c1.query"]])
+        with pytest.raises(T.DomainError):
+            eng.prefill_query_batch([ctx], [np.zeros(0, np.int32)])
