@@ -41,6 +41,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_CHUNKS, CHUNK_TOKENS, QUERY_TOKENS = 16, 512, 64
+C3_BATCH, C3_CHUNKS, C3_CHUNK_TOKENS, C3_CORPUS = 32, 20, 800, 160  # BASELINE configs[2] (LongBench-multidoc shape)
 SEED = 42
 METRIC = "TurboRAG request throughput (KV inject + query prefill to first-token logits)"
 UNIT = "req/s"
@@ -251,7 +252,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
 
     cfg = T.ModelConfig.qwen2_7b_like()
-    eng = T.Engine(cfg, SEED, dtype="bf16", device=local, store_capacity_tokens=N_CHUNKS * CHUNK_TOKENS * 4,
+    eng = T.Engine(cfg, SEED, dtype="bf16", device=local,
+                   store_capacity_tokens=N_CHUNKS * CHUNK_TOKENS * 4 + C3_CORPUS * C3_CHUNK_TOKENS,
                    flags=args.flags)
     payloads, query = workload()
     t0 = time.perf_counter()
@@ -391,6 +393,38 @@ def run_ours(args):
               "tensor_frac": per_round * flop_chunk / sec / 1e12 / peaks["bf16_tflops"],
               "flop_per_chunk": flop_chunk, "kv_bytes_per_chunk": c * cfg.layer_num * 2 * cfg.kv_dim * 2}
 
+    # C3 (BASELINE configs[2]) sample: LongBench-multidoc shape, batch 32 requests x (20 chunks x 800 tokens
+    # + 64-token query), chunks retrieved from a 160-chunk corpus; one step = assemble 32 contexts + one batched
+    # prefill (tkv_prefill_query_batch); composite vs reordered positions
+    c3 = None
+    if args.c3_steps > 0:
+        rng = np.random.default_rng(0xC3)
+        corpus = [rng.integers(97, 123, C3_CHUNK_TOKENS - 2).astype(np.int32) for _ in range(C3_CORPUS)]
+        t0 = time.perf_counter()
+        cids = eng.ingest_chunks(corpus)
+        torch.cuda.synchronize(dev)
+        c3_ingest_s = time.perf_counter() - t0
+        picks = [rng.choice(C3_CORPUS, C3_CHUNKS, replace=False) for _ in range(C3_BATCH)]
+        queries = [rng.integers(97, 123, QUERY_TOKENS).astype(np.int32) for _ in range(C3_BATCH)]
+        c3 = {"workload": f"C3 sample: batch {C3_BATCH} x ({C3_CHUNKS} chunks x {C3_CHUNK_TOKENS} tokens + "
+                          f"{QUERY_TOKENS}-token query) from a {C3_CORPUS}-chunk corpus; step = assemble + batched "
+                          f"prefill, median of {args.c3_steps} steps after 1 warm-up",
+              "corpus_ingest_s": c3_ingest_s}
+        for mode, tag in ((T.PositionMode.Reordered, "reordered"), (T.PositionMode.Composite, "composite")):
+            ts = []
+            for i in range(1 + args.c3_steps):
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                ctxs = [eng.assemble([cids[j] for j in pk], mode) for pk in picks]
+                eng.prefill_query_batch(ctxs, queries)
+                torch.cuda.synchronize(dev)
+                if i:
+                    ts.append(time.perf_counter() - t0)
+                for c in ctxs:
+                    c.close()
+            sec = statistics.median(ts)
+            c3[tag] = {"requests_per_s": C3_BATCH / sec, "batch_latency_ms": sec * 1e3}
+
     cpu_baseline = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu, ncores = host_info()
@@ -436,6 +470,7 @@ def run_ours(args):
         "kv_inject_gbs": achieved,
         "ingest_s_16_chunks": ingest_s,
         "c5_ingest": c5,
+        "c3_batch": c3,
         "store": {"sharding": f"by document over {ws} GPU(s)", "remote_chunk_token_fraction": remote_frac,
                   "remote_policy": args.remote if ws > 1 else "n/a"},
         "device_ms_per_step": {"gather_rope": gather_ms / prof_steps, "attention": attn_ms / prof_steps,
@@ -472,6 +507,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--turbo-only", action="store_true", help="timed turbo steps only (for ncu captures)")
     ap.add_argument("--c5-rounds", type=int, default=3, help="C5 offline-precompute sample rounds (0 = skip)")
+    ap.add_argument("--c3-steps", type=int, default=2, help="C3 batch-32 sample steps per position mode (0 = skip)")
     ap.add_argument("--remote", choices=["direct", "fetch"], default="direct",
                     help="N>1: read peer-owned chunks over NVLink every request, or copy them once")
     args = ap.parse_args()
