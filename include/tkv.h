@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TKV_ABI_VERSION 1
+#define TKV_ABI_VERSION 2
 
 typedef enum {
     TKV_OK = 0,
@@ -76,6 +76,8 @@ typedef struct {
     int64_t max_position;         /* RoPE table length (0 = 32768; grows on demand)                 */
     int32_t exact_fingerprint;    /* 1 = reference FNV weights checksum, 0 = fast, -1 = auto        */
     int32_t flags;                /* TKV_FLAG_*                                                     */
+    int64_t host_spill_tokens;    /* pinned, device-mapped host tier for chunks that do not fit the  */
+                                  /* HBM store (0 = none); the gather kernel reads it zero-copy      */
 } tkv_engine_opts;
 
 #define TKV_FLAG_SIMT_GEMM 0x1    /* bf16: use the SIMT GEMM instead of tcgen05 (debug/compare)  */
@@ -147,6 +149,11 @@ tkv_status tkv_store_count(const tkv_engine* eng, int64_t* chunks, int64_t* page
  * of TKVC files, kvstore.cpp:78-211; this is the capacity policy of the HBM store). Contexts assembled earlier
  * keep their gathered KV; only their unrotated re-read (tkv_context_read_kv, rotated=0) then fails StaleCache. */
 tkv_status tkv_store_evict(tkv_engine* eng, uint64_t chunk_id);
+/* Two-tier store occupancy in pages: HBM pool and the pinned host spill tier (host_spill_tokens). New chunks go
+ * to HBM while it has room, then to the host tier; tier of a chunk: 0 = HBM, 1 = pinned host, 2 = a peer GPU. */
+tkv_status tkv_store_tiers(const tkv_engine* eng, int64_t* hbm_used, int64_t* hbm_total, int64_t* host_used,
+                           int64_t* host_total);
+tkv_status tkv_store_chunk_tier(const tkv_engine* eng, uint64_t chunk_id, int32_t* tier);
 /* Copy one stored (unrotated) tensor to host as float32 [tokens, kv_head_num*head_size]. */
 tkv_status tkv_store_read(const tkv_engine* eng, uint64_t chunk_id, int64_t layer, tkv_kv_which which,
                           float* host_out, int64_t capacity_elems);

@@ -272,6 +272,10 @@ struct tkv_engine {
     int64_t page_tokens = 64, n_pages = 0;
     size_t page_bytes = 0;
     std::vector<int32_t> free_pages;
+    // pinned host spill tier (opts.host_spill_tokens): device-mapped, pool slot kHostPool
+    void* host_pool = nullptr;
+    int64_t n_host_pages = 0;
+    std::vector<int32_t> host_free;
     uint64_t store_epoch = 0;  // bumped by every eviction (contexts that re-read store pages check it)
     std::unordered_map<uint64_t, Chunk> chunks;
     PoolTable pools;                     // slot 0 = pool.p; peers attached via IPC or same-process P2P
@@ -397,6 +401,7 @@ struct tkv_engine {
             cudaGetLastError();
             sync();
             for (auto& f : ctx_free) cudaFree(f.second);
+    if (host_pool) cudaFreeHost(host_pool);
             ctx_free.clear();
             e = cudaMalloc(&p, bytes);
         }
@@ -930,15 +935,35 @@ void naive_impl(tkv_engine* e, const int32_t* framed, const int64_t* offsets, in
         tkv_context_destroy(c);
 }
 
+// Page placement: HBM while it has room for the whole chunk, else the pinned host spill tier (a chunk lives in one tier).
 void store_chunk_pages(tkv_engine* e, Chunk& ch) {
     const int64_t np = (ch.len + e->page_tokens - 1) / e->page_tokens;
-    if ((int64_t)e->free_pages.size() < np)
-        fail(TKV_ERR_OOM, "KV store full: need " + std::to_string(np) + " pages, " +
-                              std::to_string(e->free_pages.size()) + " free");
-    for (int64_t p = 0; p < np; ++p) {
-        ch.pages.push_back(e->free_pages.back());
-        e->free_pages.pop_back();
+    std::vector<int32_t>* fl = &e->free_pages;
+    ch.slot = 0;
+    if ((int64_t)fl->size() < np && (int64_t)e->host_free.size() >= np) {
+        fl = &e->host_free;
+        ch.slot = kHostPool;
     }
+    if ((int64_t)fl->size() < np)
+        fail(TKV_ERR_OOM, "KV store full: need " + std::to_string(np) + " pages, " +
+                              std::to_string(e->free_pages.size()) + " free in HBM, " +
+                              std::to_string(e->host_free.size()) + " in the host tier");
+    for (int64_t p = 0; p < np; ++p) {
+        ch.pages.push_back(fl->back());
+        fl->pop_back();
+    }
+}
+
+void release_chunk_pages(tkv_engine* e, const Chunk& ch) {
+    if (ch.slot == 0)
+        e->free_pages.insert(e->free_pages.end(), ch.pages.begin(), ch.pages.end());
+    else if (ch.slot == kHostPool)
+        e->host_free.insert(e->host_free.end(), ch.pages.begin(), ch.pages.end());
+    // peer-registered chunks do not own pages here
+}
+
+uint8_t* page_ptr(tkv_engine* e, int slot, int32_t page) {
+    return static_cast<uint8_t*>(const_cast<void*>(e->pools.p[slot])) + (size_t)page * e->page_bytes;
 }
 
 }  // namespace
@@ -1143,6 +1168,16 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         e->pools.p[0] = e->pool.p;
         e->free_pages.reserve((size_t)e->n_pages);
         for (int64_t p = e->n_pages - 1; p >= 0; --p) e->free_pages.push_back((int32_t)p);
+        if (e->opts.host_spill_tokens > 0) {  // pinned host tier, mapped into the device address space
+            e->n_host_pages = (e->opts.host_spill_tokens + e->page_tokens - 1) / e->page_tokens;
+            TKV_CUDA(cudaHostAlloc(&e->host_pool, (size_t)e->n_host_pages * e->page_bytes,
+                                   cudaHostAllocMapped | cudaHostAllocPortable));
+            void* dp = nullptr;
+            TKV_CUDA(cudaHostGetDevicePointer(&dp, e->host_pool, 0));
+            e->pools.p[kHostPool] = dp;
+            e->host_free.reserve((size_t)e->n_host_pages);
+            for (int64_t p = e->n_host_pages - 1; p >= 0; --p) e->host_free.push_back((int32_t)p);
+        }
         e->sync();
         *out = e.release();
     });
@@ -1219,7 +1254,8 @@ tkv_status tkv_ingest_chunks(tkv_engine* e, const int32_t* payloads, const int64
                         s.pos.push_back((int32_t)t);          // positions 0..len-1 (pipeline.cpp:106)
                         s.lo.push_back((int32_t)off);         // causal_rows(len, 0) per chunk: block-diagonal
                         s.hi.push_back((int32_t)(off + t));
-                        s.page.push_back(ch.pages[t / e->page_tokens]);
+                        const int32_t pg = ch.pages[t / e->page_tokens];
+                        s.page.push_back(ch.slot == kHostPool ? (int32_t)e->n_pages + pg : pg);  // host_base = n_pages
                         s.slot.push_back((int32_t)(t % e->page_tokens));
                     }
                     off += ch.len;
@@ -1244,6 +1280,8 @@ tkv_status tkv_ingest_chunks(tkv_engine* e, const int32_t* payloads, const int64
                     f.sc.slot = e->d_slot.as<int32_t>();
                     f.sc.page_tokens = (int)e->page_tokens;
                     f.sc.layer_num = (int)e->L;
+                    f.sc.host_pool = const_cast<void*>(e->pools.p[kHostPool]);
+                    f.sc.host_base = (int32_t)e->n_pages;
                     e->forward(f);
                     e->check_err("ingest");
                 } catch (...) {
@@ -1252,8 +1290,7 @@ tkv_status tkv_ingest_chunks(tkv_engine* e, const int32_t* payloads, const int64
                 }
                 tkv_context_destroy(scratch);
             } catch (...) {
-                for (auto& ch : made)
-                    for (int32_t p : ch.pages) e->free_pages.push_back(p);
+                for (auto& ch : made) release_chunk_pages(e, ch);
                 throw;
             }
             for (size_t k = i0; k < i1; ++k) {
@@ -1360,8 +1397,7 @@ tkv_status tkv_import_tkvc(tkv_engine* e, const char* path, uint64_t* id_out) {
                             }
                         }
                 }
-            TKV_CUDA(cudaMemcpy(static_cast<uint8_t*>(e->pool.p) + (size_t)ch.pages[p] * e->page_bytes, page.data(),
-                                e->page_bytes, cudaMemcpyHostToDevice));
+            TKV_CUDA(cudaMemcpy(page_ptr(e, ch.slot, ch.pages[p]), page.data(), e->page_bytes, cudaMemcpyDefault));
             (void)es;
         }
         e->chunks.emplace(id, std::move(ch));
@@ -1430,10 +1466,30 @@ tkv_status tkv_store_evict(tkv_engine* e, uint64_t id) {
         need(e, "engine");
         auto it = e->chunks.find(id);
         if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
-        if (it->second.slot == 0)  // local pages return to the pool; peer-registered chunks only drop the entry
-            for (int32_t p : it->second.pages) e->free_pages.push_back(p);
+        release_chunk_pages(e, it->second);  // peer-registered chunks only drop the entry
         e->chunks.erase(it);
         e->store_epoch += 1;
+    });
+}
+
+tkv_status tkv_store_tiers(const tkv_engine* e, int64_t* hbm_used, int64_t* hbm_total, int64_t* host_used,
+                           int64_t* host_total) {
+    return guard([&] {
+        need(e, "engine");
+        if (hbm_used) *hbm_used = e->n_pages - (int64_t)e->free_pages.size();
+        if (hbm_total) *hbm_total = e->n_pages;
+        if (host_used) *host_used = e->n_host_pages - (int64_t)e->host_free.size();
+        if (host_total) *host_total = e->n_host_pages;
+    });
+}
+
+tkv_status tkv_store_chunk_tier(const tkv_engine* e, uint64_t id, int32_t* tier) {
+    return guard([&] {
+        need(e, "engine");
+        need(tier, "tier");
+        auto it = e->chunks.find(id);
+        if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
+        *tier = it->second.slot == 0 ? 0 : (it->second.slot == kHostPool ? 1 : 2);
     });
 }
 
@@ -1476,7 +1532,7 @@ tkv_status tkv_store_read(const tkv_engine* ce, uint64_t id, int64_t layer, tkv_
             const uint8_t* src = static_cast<const uint8_t*>(e->pools.p[ch.slot]) + (size_t)ch.pages[p] * e->page_bytes +
                                  (size_t)((layer * 2 + (int)which) * e->page_tokens) * e->kvd * es;
             TKV_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(tmp.p) + (size_t)t0 * e->kvd * es, src,
-                                     (size_t)nt * e->kvd * es, cudaMemcpyDeviceToDevice, e->stream));
+                                     (size_t)nt * e->kvd * es, cudaMemcpyDefault, e->stream));  // HBM, host tier or peer
         }
         launch_to_f32(tmp.p, ch.len * e->kvd, tmpf.as<float>(), e->dt, e->stream);
         TKV_CUDA(cudaMemcpyAsync(host_out, tmpf.p, (size_t)ch.len * e->kvd * 4, cudaMemcpyDeviceToHost, e->stream));
@@ -1813,7 +1869,7 @@ tkv_status tkv_debug_set_mask_fault(tkv_engine* e, int64_t row, int64_t col) {
 // ---- multi-GPU: document-sharded stores, remote chunks read over NVLink ----
 namespace {
 void check_slot(int32_t slot) {
-    if (slot < 1 || slot >= kMaxPools) fail(TKV_ERR_CONFIG, "peer slot must be in [1, " + std::to_string(kMaxPools) + ")");
+    if (slot < 1 || slot >= kHostPool) fail(TKV_ERR_CONFIG, "peer slot must be in [1, " + std::to_string(kHostPool) + ")");
 }
 }  // namespace
 
@@ -1915,8 +1971,7 @@ tkv_status tkv_store_fetch_remote(tkv_engine* e, uint64_t id) {
         local.framed = ch.framed;
         store_chunk_pages(e, local);
         for (size_t p = 0; p < ch.pages.size(); ++p)  // page-sized copies over NVLink (copy engine)
-            TKV_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(e->pool.p) + (size_t)local.pages[p] * e->page_bytes,
-                                     static_cast<const uint8_t*>(e->pools.p[ch.slot]) + (size_t)ch.pages[p] * e->page_bytes,
+            TKV_CUDA(cudaMemcpyAsync(page_ptr(e, local.slot, local.pages[p]), page_ptr(e, ch.slot, ch.pages[p]),
                                      e->page_bytes, cudaMemcpyDefault, e->stream));
         e->remote_bytes += (int64_t)(ch.pages.size() * e->page_bytes);
         e->sync();

@@ -174,6 +174,18 @@ __global__ void swiglu_kernel(const float* partial, int splits, int T_, int inte
     }
 }
 
+// Element offset of token t's row of (layer, K|V) inside its store page; HBM pool or the host spill tier.
+template <typename T>
+__device__ __forceinline__ int64_t store_base(const StoreScatter& sc, int64_t t, int layer, int kv, int kvd, T*& pool) {
+    int64_t page = sc.page[t];
+    pool = (T*)sc.pool;
+    if (page >= sc.host_base) {
+        page -= sc.host_base;
+        pool = (T*)sc.host_pool;
+    }
+    return ((page * sc.layer_num + layer) * 2 + kv) * sc.page_tokens * kvd + (int64_t)sc.slot[t] * kvd;
+}
+
 // One thread per element pair (2m, 2m+1) of the fused QKV output row.
 template <typename T>
 __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
@@ -205,10 +217,10 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
             stf(vc, (int64_t)(row0 + t) * kvd + c, x0);
             stf(vc, (int64_t)(row0 + t) * kvd + c + 1, x1);
             if (sc.page) {
-                const int64_t base = (((int64_t)sc.page[t] * sc.layer_num + layer) * 2 + 1) * sc.page_tokens * kvd +
-                                     (int64_t)sc.slot[t] * kvd;
-                stf((T*)sc.pool, base + c, x0);
-                stf((T*)sc.pool, base + c + 1, x1);
+                T* pool;
+                const int64_t base = store_base(sc, t, layer, 1, kvd, pool);
+                stf(pool, base + c, x0);
+                stf(pool, base + c + 1, x1);
             }
             continue;
         }
@@ -223,10 +235,10 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
             stf(kc, (int64_t)(row0 + t) * kvd + c, r0);
             stf(kc, (int64_t)(row0 + t) * kvd + c + 1, r1);
             if (sc.page) {  // the store keeps keys unrotated (SPEC: rotation at use)
-                const int64_t base = (((int64_t)sc.page[t] * sc.layer_num + layer) * 2 + 0) * sc.page_tokens * kvd +
-                                     (int64_t)sc.slot[t] * kvd;
-                stf((T*)sc.pool, base + c, x0);
-                stf((T*)sc.pool, base + c + 1, x1);
+                T* pool;
+                const int64_t base = store_base(sc, t, layer, 0, kvd, pool);
+                stf(pool, base + c, x0);
+                stf(pool, base + c + 1, x1);
             }
         }
     }

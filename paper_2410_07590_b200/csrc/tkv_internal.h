@@ -71,6 +71,8 @@ struct StoreScatter {
     const int32_t* slot = nullptr;  // [T]
     int page_tokens = 0;
     int layer_num = 0;
+    void* host_pool = nullptr;      // pinned host spill tier (device-mapped): page >= host_base -> host page
+    int32_t host_base = INT32_MAX;  //   (page - host_base)
 };
 // The projections were computed from xb: every output is first multiplied by row_scale(ssp, t).
 void launch_qkv_epilogue(const float* partial, int splits, int T, int H, int Hkv, int d, const int32_t* pos,
@@ -90,6 +92,7 @@ struct GatherSeg {
 // Page pools the gather kernel may read: slot 0 is local HBM, other slots are peer GPUs' pools mapped
 // into this process (cudaIpcOpenMemHandle, or peer access inside one process).
 constexpr int kMaxPools = 16;
+constexpr int kHostPool = kMaxPools - 1;  // slot of the pinned host spill tier (peers use 1 .. kHostPool - 1)
 struct PoolTable {
     const void* p[kMaxPools] = {};
 };

@@ -83,7 +83,7 @@ class _Cfg(C.Structure):
 class _Opts(C.Structure):
     _fields_ = [("dtype", C.c_int), ("device", C.c_int32), ("page_tokens", C.c_int32),
                 ("store_capacity_tokens", C.c_int64), ("max_position", C.c_int64),
-                ("exact_fingerprint", C.c_int32), ("flags", C.c_int32)]
+                ("exact_fingerprint", C.c_int32), ("flags", C.c_int32), ("host_spill_tokens", C.c_int64)]
 
 
 class _Stats(C.Structure):
@@ -127,6 +127,8 @@ def lib():
         L.tkv_store_chunk_tokens.argtypes = [C.c_void_p, C.c_uint64, I64P]
         L.tkv_store_count.argtypes = [C.c_void_p, I64P, I64P, I64P]
         L.tkv_store_evict.argtypes = [C.c_void_p, C.c_uint64]
+        L.tkv_store_tiers.argtypes = [C.c_void_p, I64P, I64P, I64P, I64P]
+        L.tkv_store_chunk_tier.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32)]
         L.tkv_prefill_query_batch.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int64, I32P, I64P, F32P,
                                               C.POINTER(_Flops)]
         L.tkv_store_read.argtypes = [C.c_void_p, C.c_uint64, C.c_int64, C.c_int, F32P, C.c_int64]
@@ -364,7 +366,7 @@ class Engine:
 
     def __init__(self, config: ModelConfig, seed: int, dtype: str | Dtype = "bf16", device: int = 0,
                  page_tokens: int = 64, store_capacity_tokens: int = 0, max_position: int = 0,
-                 exact_fingerprint: int = -1, flags: int = 0):
+                 exact_fingerprint: int = -1, flags: int = 0, host_spill_tokens: int = 0):
         self.config = config
         self.seed = seed
         o = _Opts()
@@ -373,6 +375,7 @@ class Engine:
                       else Dtype.BF16)
         o.device, o.page_tokens, o.store_capacity_tokens = device, page_tokens, store_capacity_tokens
         o.max_position, o.exact_fingerprint, o.flags = max_position, exact_fingerprint, flags
+        o.host_spill_tokens = host_spill_tokens
         self.dtype = Dtype(o.dtype)
         h = C.c_void_p()
         _check(lib().tkv_engine_create(C.byref(config._c()), seed, C.byref(o), C.byref(h)))
@@ -423,6 +426,17 @@ class Engine:
 
     def export_tkvc(self, chunk_id: int, path: str) -> None:
         _check(lib().tkv_export_tkvc(self._h, chunk_id, path.encode()))
+
+    def store_tiers(self) -> dict:
+        v = [C.c_int64() for _ in range(4)]
+        _check(lib().tkv_store_tiers(self._h, *[C.byref(x) for x in v]))
+        return {"hbm_used": v[0].value, "hbm_total": v[1].value, "host_used": v[2].value, "host_total": v[3].value}
+
+    def store_chunk_tier(self, chunk_id: int) -> int:
+        """0 = HBM, 1 = pinned host spill tier, 2 = a peer GPU's pool."""
+        t = C.c_int32()
+        _check(lib().tkv_store_chunk_tier(self._h, chunk_id, C.byref(t)))
+        return t.value
 
     def store_evict(self, chunk_id: int) -> None:
         _check(lib().tkv_store_evict(self._h, chunk_id))

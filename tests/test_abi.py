@@ -26,7 +26,7 @@ def test_every_declared_symbol_is_exported():
     assert len(names) >= 40
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.tkv_abi_version() == 1
+    assert lib.tkv_abi_version() == 2
 
 
 def test_status_codes_mirror_reference_error_classes():

@@ -415,3 +415,37 @@ def test_batched_prefill_rejects_bad_batches(golden):
             eng.prefill_query_batch([ctx, ctx], [A["c1.query"], A["c1.query"]])
         with pytest.raises(T.DomainError):
             eng.prefill_query_batch([ctx], [np.zeros(0, np.int32)])
+
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_host_spill_tier_is_bit_exact_and_transparent(golden, dtype):
+    """Chunks that do not fit the HBM store land in the pinned host tier: ingest writes their pages over the
+    mapped host pointer, the gather kernel reads them zero-copy; pages, gathered KV and logits are identical
+    to an all-HBM engine (north star subsystem 1: HBM store + pinned host when it spills)."""
+    meta, A = golden
+    m = meta["c1"]
+    cfg = cfg_t(m)
+    ref = engine(cfg, m["seed"], dtype)
+    spill = T.Engine(cfg, m["seed"], dtype=dtype, store_capacity_tokens=256, host_spill_tokens=1024)
+    pl = payloads(A, "c1")
+    ids_ref, ids = ref.ingest_chunks(pl), spill.ingest_chunks(pl)
+    assert ids == ids_ref
+    tiers = [spill.store_chunk_tier(i) for i in ids]
+    assert tiers[:2] == [0, 0] and tiers[2:] == [1, 1]  # 2 x 128 tokens fill the 256-token HBM store
+    t = spill.store_tiers()
+    assert t["hbm_used"] == t["hbm_total"] == 4 and t["host_used"] == 4 and t["host_total"] == 16
+    for i in ids:
+        for layer in (0, cfg.layer_num - 1):
+            for which in ("k", "v"):
+                assert np.array_equal(spill.store_read(i, layer, which), ref.store_read(i, layer, which))
+    q = A["c1.query"]
+    with spill.assemble(ids, T.PositionMode.Reordered) as c1, ref.assemble(ids, T.PositionMode.Reordered) as c0:
+        for layer in (0, cfg.layer_num - 1):
+            assert np.array_equal(c1.read_kv(layer, "k", rotated=True), c0.read_kv(layer, "k", rotated=True))
+            assert np.array_equal(c1.read_kv(layer, "v"), c0.read_kv(layer, "v"))
+        assert np.array_equal(spill.prefill_query(c1, q)[0], ref.prefill_query(c0, q)[0])
+    spill.store_evict(ids[2])
+    assert spill.store_tiers()["host_used"] == 2
+    spill.close()
