@@ -42,6 +42,7 @@ sys.path.insert(0, ROOT)
 
 N_CHUNKS, CHUNK_TOKENS, QUERY_TOKENS = 16, 512, 64
 C3_BATCH, C3_CHUNKS, C3_CHUNK_TOKENS, C3_CORPUS = 32, 20, 800, 160  # BASELINE configs[2] (LongBench-multidoc shape)
+C4_SHARD, C4_CHUNK_TOKENS, C4_K = 4096, 64, 16  # BASELINE configs[3], scaled per-GPU shard
 SEED = 42
 METRIC = "TurboRAG request throughput (KV inject + query prefill to first-token logits)"
 UNIT = "req/s"
@@ -425,6 +426,49 @@ def run_ours(args):
             sec = statistics.median(ts)
             c3[tag] = {"requests_per_s": C3_BATCH / sec, "batch_latency_ms": sec * 1e3}
 
+    # C4 (BASELINE configs[3]) sample, one GPU's shard: Llama-3-8B shape, 64-token chunks, Zipf(1.1) retrieval of
+    # k = 16 chunks per request; the Zipf-hot half of the shard is resident in HBM, the cold half in the pinned
+    # host tier (read zero-copy by the gather kernel). Shard scaled to C4_SHARD chunks so the sample ingests in
+    # seconds (the full 200K-chunk store is 25K chunks per GPU at 8 GPUs).
+    c4 = None
+    if args.c4_requests > 0:
+        lcfg = T.ModelConfig.llama3_8b_like()
+        hbm_chunks = C4_SHARD // 2
+        eng4 = T.Engine(lcfg, SEED, dtype="bf16", device=local, store_capacity_tokens=hbm_chunks * C4_CHUNK_TOKENS,
+                        host_spill_tokens=(C4_SHARD - hbm_chunks) * C4_CHUNK_TOKENS + 4 * C4_CHUNK_TOKENS)
+        rng = np.random.default_rng(0xC4)
+        corpus = [rng.integers(97, 123, C4_CHUNK_TOKENS - 2).astype(np.int32) for _ in range(C4_SHARD)]
+        t0 = time.perf_counter()
+        ids4 = eng4.ingest_chunks(corpus)  # rank order = popularity order: the hottest half fills HBM first
+        torch.cuda.synchronize(dev)
+        ingest4 = time.perf_counter() - t0
+        w = 1.0 / np.arange(1, C4_SHARD + 1) ** 1.1
+        w /= w.sum()
+        ts, hbm_tok, all_tok = [], 0, 0
+        for i in range(3 + args.c4_requests):
+            pick = rng.choice(C4_SHARD, C4_K, replace=False, p=w)
+            q = rng.integers(97, 123, QUERY_TOKENS).astype(np.int32)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            ctx = eng4.assemble([ids4[j] for j in pick], T.PositionMode.Reordered)
+            eng4.prefill_query(ctx, q)
+            torch.cuda.synchronize(dev)
+            if i >= 3:
+                ts.append(time.perf_counter() - t0)
+                hbm_tok += sum(C4_CHUNK_TOKENS for j in pick if eng4.store_chunk_tier(ids4[j]) == 0)
+                all_tok += C4_K * C4_CHUNK_TOKENS
+            ctx.close()
+        tiers = eng4.store_tiers()
+        c4 = {"workload": f"C4 sample (one GPU's shard): Llama-3-8B shape, {C4_SHARD} chunks x {C4_CHUNK_TOKENS} "
+                          f"tokens, Zipf(1.1) retrieval of k={C4_K}, + {QUERY_TOKENS}-token query, batch 1; "
+                          f"{args.c4_requests} requests after 3 warm-up",
+              "p50_ttft_ms": statistics.median(ts) * 1e3, "requests_per_s": 1.0 / statistics.median(ts),
+              "hbm_resident_chunk_fraction": tiers["hbm_used"] / max(1, tiers["hbm_used"] + tiers["host_used"]),
+              "hbm_hit_token_fraction": hbm_tok / max(1, all_tok), "shard_ingest_s": ingest4,
+              "store_pages": tiers}
+        eng4.close()
+        torch.cuda.empty_cache()
+
     cpu_baseline = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu, ncores = host_info()
@@ -471,6 +515,7 @@ def run_ours(args):
         "ingest_s_16_chunks": ingest_s,
         "c5_ingest": c5,
         "c3_batch": c3,
+        "c4_zipf_store": c4,
         "store": {"sharding": f"by document over {ws} GPU(s)", "remote_chunk_token_fraction": remote_frac,
                   "remote_policy": args.remote if ws > 1 else "n/a"},
         "device_ms_per_step": {"gather_rope": gather_ms / prof_steps, "attention": attn_ms / prof_steps,
@@ -508,6 +553,7 @@ def main():
     ap.add_argument("--turbo-only", action="store_true", help="timed turbo steps only (for ncu captures)")
     ap.add_argument("--c5-rounds", type=int, default=3, help="C5 offline-precompute sample rounds (0 = skip)")
     ap.add_argument("--c3-steps", type=int, default=2, help="C3 batch-32 sample steps per position mode (0 = skip)")
+    ap.add_argument("--c4-requests", type=int, default=20, help="C4 Zipf-store sample requests (0 = skip)")
     ap.add_argument("--remote", choices=["direct", "fetch"], default="direct",
                     help="N>1: read peer-owned chunks over NVLink every request, or copy them once")
     args = ap.parse_args()
