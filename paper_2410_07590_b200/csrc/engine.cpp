@@ -1145,9 +1145,10 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         e->err.ensure(64);
         if (const char* pfm = getenv("TKV_L2_PREFETCH_MB")) e->l2_prefetch_bytes = (size_t)atol(pfm) << 20;
         if (const char* sk = getenv("TKV_TIMING_SKIP")) e->skip_mask = atoi(sk);
-        if (const char* gk = getenv("TKV_GEMM_KNOBS")) {  // "stages,smem_kb,ctas_per_sm,evict_first" (tuning)
-            int st = 0, sm = 0, cps = 0, ef = 1;
-            if (sscanf(gk, "%d,%d,%d,%d", &st, &sm, &cps, &ef) >= 3) set_gemm_knobs(st, sm, cps, ef);
+        if (const char* gk = getenv("TKV_GEMM_KNOBS")) {  // "stages,smem_kb,ctas_per_sm,evict_first[,np[,pf]]"
+            int st = 0, sm = 0, cps = 0, ef = 1, np = 0, pf = -1, kr = -1;
+            if (sscanf(gk, "%d,%d,%d,%d,%d,%d,%d", &st, &sm, &cps, &ef, &np, &pf, &kr) >= 3)
+                set_gemm_knobs(st, sm, cps, ef, np, pf, kr);
         }
         TKV_CUDA(cudaMemsetAsync(e->err.p, 0, 64, e->stream));
         e->logits.ensure((size_t)V * 4);

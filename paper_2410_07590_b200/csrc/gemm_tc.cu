@@ -38,7 +38,10 @@ constexpr int SMEM_BUDGET = 200 * 1024;
 // Tuning knobs (tkv_debug_set_gemm_knobs; 0 = default): ring depth, smem budget (KB), CTAs per SM,
 // L2 eviction policy of the weight stream (1 = evict_first).
 struct Knobs {
-    int stages = 0, smem_kb = 110, ctas_per_sm = 2, w_evict_first = 1;  // measured best (tools/gemm_sweep.py)
+    // swapped (<= 128 tokens) tiling: np 128-row weight tiles per unit share one activation tile per stage
+    // (np = 2 with one 208 KB CTA per SM measured slower than np = 1 at 2 x 110 KB); pf = L2 prefetch distance
+    // of the weight stream in k-blocks (0 = off)
+    int stages = 0, smem_kb = 110, ctas_per_sm = 2, w_evict_first = 1, np = 1, pf = 0, krot = 1;
 };
 Knobs g_knobs;
 
@@ -82,6 +85,13 @@ __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
+// L2 prefetch of a tensor-map box (no smem destination): pulls weight tiles PD stages ahead of the ring so
+// the DRAM stream has more bytes in flight than shared memory can hold.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -122,6 +132,7 @@ struct GemmArgs {
     int M, N, K;
     int kb_total, kb_per_split;
     int n_tiles, m_tiles, units;  // work units = n_tiles * m_tiles * splits (persistent loop over them)
+    int np;                       // swapped: 128-row weight tiles per unit (n_tiles counts units along N)
     int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128
     uint32_t a_bytes;             // bytes of the activation tile per stage
     int stages;
@@ -134,6 +145,9 @@ struct GemmArgs {
     int nb;
     float eps;
     int w_evict_first;
+    int pf;                       // weight L2 prefetch distance (k-blocks ahead of the ring)
+    int krot;                     // rotate each unit's k-block order (spreads the shared activation tiles'
+                                  // L2 reads over time instead of every CTA hitting the same lines at once)
 };
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
@@ -156,7 +170,8 @@ __global__ void __launch_bounds__(THREADS_P)
     pdl_launch();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t stage_bytes = TILE_W + g.a_bytes;
+    const uint32_t wbytes = (uint32_t)g.np * TILE_W;  // weight bytes per stage
+    const uint32_t stage_bytes = wbytes + g.a_bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.stages * stage_bytes);
     uint64_t* empty = full + g.stages;
     uint64_t* tfull = empty + g.stages;  // [2] accumulator ready
@@ -203,25 +218,35 @@ __global__ void __launch_bounds__(THREADS_P)
             unit_coords(g, blockIdx.x, nt, mt, z);
             const int kb0 = z * g.kb_per_split;
             const int nkb0 = min(g.kb_total, kb0 + g.kb_per_split) - kb0;
+            // k-block of iteration i of unit u (the MMA only accumulates, so any order is valid)
+            auto kblk = [&](int k0, int nkb, int i, int u) { return k0 + (g.krot ? (i + (u * 37) % nkb) % nkb : i); };
             const int pre = min(nkb0, g.stages);
             for (int i = 0; i < pre; ++i) {
                 mbar_expect_tx(&full[i], stage_bytes);
-                load_w(smem + i * stage_bytes, &full[i], (kb0 + i) * BK, nt * 128);
+                load_w(smem + i * stage_bytes, &full[i], kblk(kb0, nkb0, i, blockIdx.x) * BK, nt * 128 * g.np);
             }
             pdl_wait();
             for (int i = 0; i < pre; ++i)
-                tma_load_2d(smem + i * stage_bytes + TILE_W, &tmA, &full[i], (kb0 + i) * BK, mt * mstep);
+                tma_load_2d(smem + i * stage_bytes + wbytes, &tmA, &full[i], kblk(kb0, nkb0, i, blockIdx.x) * BK, mt * mstep);
+            // L2 prefetch of the first unit's next pf weight tiles (beyond the ring)
+            for (int i = pre; i < min(nkb0, pre + g.pf); ++i)
+                tma_prefetch_2d(&tmW, kblk(kb0, nkb0, i, blockIdx.x) * BK, nt * 128 * g.np);
             int it = pre;
             for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
                 unit_coords(g, u, nt, mt, z);
                 const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
+                if (u != (int)blockIdx.x)
+                    for (int i = 0; i < min(nkb, g.pf); ++i) tma_prefetch_2d(&tmW, kblk(k0, nkb, i, u) * BK, nt * 128 * g.np);
                 for (int i = (u == (int)blockIdx.x ? pre : 0); i < nkb; ++i, ++it) {
+                    if (g.pf > 0 && i + g.pf < nkb && i + g.pf >= (u == (int)blockIdx.x ? pre + g.pf : g.pf))
+                        tma_prefetch_2d(&tmW, kblk(k0, nkb, i + g.pf, u) * BK, nt * 128 * g.np);
                     const int s = it % g.stages;
                     mbar_wait(&empty[s], ((uint32_t)(it / g.stages) & 1u) ^ 1u);
                     uint8_t* w = smem + s * stage_bytes;
                     mbar_expect_tx(&full[s], stage_bytes);
-                    load_w(w, &full[s], (k0 + i) * BK, nt * 128);
-                    tma_load_2d(w + TILE_W, &tmA, &full[s], (k0 + i) * BK, mt * mstep);
+                    const int kb = kblk(k0, nkb, i, u);
+                    load_w(w, &full[s], kb * BK, nt * 128 * g.np);
+                    tma_load_2d(w + wbytes, &tmA, &full[s], kb * BK, mt * mstep);
                 }
             }
         }
@@ -242,13 +267,16 @@ __global__ void __launch_bounds__(THREADS_P)
                     mbar_wait(&full[s], (uint32_t)(it / g.stages) & 1u);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint32_t w = smem_u32(smem + s * stage_bytes);
-                    const uint32_t a = w + TILE_W;
+                    const uint32_t a = w + wbytes;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {  // 16 bf16 = 32 B along K inside the 128 B swizzle row
-                        if (SWAP)
-                            umma_f16(acc, desc_k(w + k * 32), desc_k(a + k * 32), id, (i | k) != 0);
-                        else
+                        if (SWAP) {
+                            for (int p = 0; p < g.np; ++p)  // one activation tile, np weight tiles
+                                umma_f16(acc + (uint32_t)(p * g.ntok), desc_k(w + p * TILE_W + k * 32),
+                                         desc_k(a + k * 32), id, (i | k) != 0);
+                        } else {
                             umma_f16(acc, desc_k(a + k * 32), desc_k(w + k * 32), id, (i | k) != 0);
+                        }
                     }
                     umma_commit(&empty[s]);
                 }
@@ -268,8 +296,11 @@ __global__ void __launch_bounds__(THREADS_P)
             const int b = lu & 1;
             mbar_wait(&tfull[b], (uint32_t)(lu >> 1) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t acc = tmem + lane_base + (uint32_t)b * g.acc_cols;
-            const int n0 = nt * 128, m0 = mt * mstep;
+            const uint32_t acc_u = tmem + lane_base + (uint32_t)b * g.acc_cols;
+            const int m0 = mt * mstep;
+            for (int p = 0; p < (SWAP ? g.np : 1); ++p) {
+            const uint32_t acc = acc_u + (uint32_t)(p * (SWAP ? g.ntok : 0));
+            const int n0 = (nt * (SWAP ? g.np : 1) + p) * 128;
             if (SWAP) {
                 const int n = n0 + lg * 32 + lane;  // TMEM lane = weight row n, column = token
                 if (EPI == EPI_PARTIAL) {
@@ -304,7 +335,7 @@ __global__ void __launch_bounds__(THREADS_P)
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (lg < 2) {
                         const int inter = g.N / 2;
-                        const int i = nt * 64 + lg * 32 + lane;
+                        const int i = (n0 / 128) * 64 + lg * 32 + lane;
 #pragma unroll 1
                         for (int c = 0; c < g.ntok; c += 16) {
                             uint32_t r[16];
@@ -371,6 +402,7 @@ __global__ void __launch_bounds__(THREADS_P)
                     }
                 }
             }
+            }  // p
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
         }
@@ -429,9 +461,12 @@ bool gemm_tc_supported(int M, int N, int K, int lda) {
 
 int gemm_tc_ctas_per_sm() { return std::max(1, g_knobs.ctas_per_sm); }
 
+static int np_for(int M, int N) { return (M <= 128 && (N + 127) / 128 >= 2) ? std::max(1, g_knobs.np) : 1; }
+
 int gemm_tc_tiles(int M, int N) {
     const bool swap = M <= 128;
-    return ((N + 127) / 128) * (swap ? 1 : (M + 127) / 128);
+    const int np = np_for(M, N);
+    return ((N + 128 * np - 1) / (128 * np)) * (swap ? 1 : (M + 127) / 128);
 }
 
 int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
@@ -444,22 +479,23 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.kb_total = (K + BK - 1) / BK;
     g.kb_per_split = (g.kb_total + splits - 1) / splits;
     const int eff_splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;  // every unit non-empty
-    g.n_tiles = (N + 127) / 128;
+    g.np = np_for(M, N);
+    g.n_tiles = (N + 128 * g.np - 1) / (128 * g.np);
     g.m_tiles = swap ? 1 : (M + 127) / 128;
     g.units = g.n_tiles * g.m_tiles * eff_splits;
     g.ntok = swap ? ((M + 15) / 16) * 16 : 128;
     g.a_bytes = (uint32_t)g.ntok * BK * 2;
-    g.acc_cols = swap ? (uint32_t)g.ntok : 128u;
+    g.acc_cols = swap ? (uint32_t)(g.ntok * g.np) : 128u;
     g.tmem_cols = 32;
     while (g.tmem_cols < 2 * g.acc_cols) g.tmem_cols <<= 1;
     const uint32_t scratch =
         (swap && swiglu_act) ? (uint32_t)((64 * (g.ntok + 1) + g.ntok) * 4 + 1023) / 1024 * 1024 : 0;
     const int budget = (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET);
     g.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
-                                       (uint32_t)(budget - (int)scratch) / (TILE_W + g.a_bytes));
+                                       (uint32_t)(budget - (int)scratch) / (g.np * TILE_W + g.a_bytes));
     if (g.stages < 2) fail(TKV_ERR_CONFIG, "GEMM smem budget too small");
     g.w_evict_first = g_knobs.w_evict_first;
-    g.scratch_off = (uint32_t)g.stages * (TILE_W + g.a_bytes) + 256;  // after the ring and its barriers
+    g.scratch_off = (uint32_t)g.stages * (g.np * TILE_W + g.a_bytes) + 256;  // after the ring and its barriers
     g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;
     g.partial = partial;
     g.act = (__nv_bfloat16*)swiglu_act;
@@ -473,7 +509,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = std::min(g.units, sms * std::max(1, g_knobs.ctas_per_sm));
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
-    const CUtensorMap tw = make_map(W, N, K, K, 128);
+    const CUtensorMap tw = make_map(W, N, K, K, 128 * g.np);
     if (swiglu_act) {
         if (eff_splits != 1) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the whole K range in one unit");
         swap ? launch_t<true, EPI_SWIGLU>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_SWIGLU>(ta, tw, g, grid, smem, s);
@@ -483,12 +519,15 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     return eff_splits;
 }
 
-void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first) {
+void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np, int pf, int krot) {
     const Knobs d;
+    g_knobs.krot = krot >= 0 ? krot : d.krot;
+    g_knobs.pf = pf >= 0 ? pf : d.pf;
     g_knobs.stages = stages;
     g_knobs.smem_kb = smem_kb > 0 ? smem_kb : d.smem_kb;
     g_knobs.ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : d.ctas_per_sm;
     g_knobs.w_evict_first = w_evict_first;
+    g_knobs.np = np > 0 ? np : d.np;
 }
 
 }  // namespace tkv

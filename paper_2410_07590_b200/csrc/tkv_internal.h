@@ -122,7 +122,8 @@ void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K
 // M <= 128 uses the swapped tiling (weights on the UMMA M side). With swiglu_act != nullptr (splits must
 // be 1, W rows interleaved in 64-row gate/up blocks) the epilogue writes act[M][N/2] = silu(g)*u in bf16.
 bool gemm_tc_supported(int M, int N, int K, int lda);
-void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first);
+void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np = 0, int pf = -1,
+                    int krot = -1);
 int gemm_tc_tiles(int M, int N);
 int gemm_tc_ctas_per_sm();  // resident GEMM CTAs per SM the launcher plans for (knob)
 // Returns the number of split-K partial planes actually written (<= splits: every split is non-empty).
