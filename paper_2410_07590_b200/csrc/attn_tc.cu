@@ -466,26 +466,35 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int my_lo = active ? a.lo[t] : INT32_MAX;
         const int my_hi = active ? min(a.hi[t], a.Tk - 1) : -1;
         pdl_wait();  // q is produced by the previous kernel
+        if (tid == 0) trace(30, 3);
         {
             // Coalesced staging: warp w of this tile loads its 32 rows two at a time (16 lanes x 16 B per row),
             // all 16 loads in flight before the swizzled stores.
             const uint32_t qb = sbase + OFF_Q + x * TILE;
             const int c = lane & 15;
             uint4 v[16];
+            // row qr = token * group + head-in-group, walked two rows at a time without per-row division
+            int qr = rr0 + x * BR + (warp & 3) * 32 + (lane >> 4);
+            int qt = qr / group, qi = qr - qt * group;
+            const uint4* qbase = reinterpret_cast<const uint4*>(a.q) + c + (int64_t)g * group * (D / 8);
 #pragma unroll
             for (int it = 0; it < 16; ++it) {
-                const int row = (warp & 3) * 32 + it * 2 + (lane >> 4);
-                const int qr = rr0 + x * BR + row;
-                v[it] = make_uint4(0, 0, 0, 0);
-                if (qr < rows_total)
-                    v[it] = *(reinterpret_cast<const uint4*>(a.q + ((int64_t)(qr / group) * a.H + g * group + qr % group) * D) + c);
+                v[it] = qr < rows_total ? qbase[((int64_t)qt * a.H + qi) * (D / 8)] : make_uint4(0, 0, 0, 0);
+                qr += 2;
+                qi += 2;
+                while (qi >= group) {
+                    qi -= group;
+                    ++qt;
+                }
             }
+            if (tid == 0 && a.trace) trace_at(a.trace, 30, 4 + (v[0].x == 0x7fc00001u && v[15].w == 1u ? 5 : 0));
 #pragma unroll
             for (int it = 0; it < 16; ++it) {
                 const int row = (warp & 3) * 32 + it * 2 + (lane >> 4);
                 sts128(qb + (c >> 3) * SUB + swz(row, c & 7), v[it]);
             }
             fence_async_smem();
+            if (tid == 0) trace(30, 5);
             mbar_arrive(q_ready);
         }
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;

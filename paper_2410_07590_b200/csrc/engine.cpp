@@ -415,6 +415,7 @@ struct tkv_engine {
 
     size_t l2_prefetch_bytes = 0;  // TKV_L2_PREFETCH_MB (tuning knob)
     int skip_mask = 0;             // TKV_TIMING_SKIP: drop kernels for cost attribution (results invalid)
+    int trace_layer = -1;          // TKV_TRACE_LAYER: clock64 pipeline trace of that layer's attention launch
 
     int pick_splits(int M, int N, int K, bool tc) const {
         const int bk = tc ? 64 : 16;
@@ -604,8 +605,10 @@ void tkv_engine::forward(const Fwd& f) {
                     pf.ptr[1] = w_gu[l];
                     pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
                 }
+                if (trace_layer == (int)l) attn_trace_enable(true, nullptr);
                 launch_attention_tc(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
                                     aTk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream, kv_ready, pf);
+                if (trace_layer == (int)l) attn_trace_enable(false, nullptr);
             } else {
                 launch_attention_simt(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
                                       aTk, (int)H, (int)Hkv, (int)d, splits, ws, err.as<int>(), dt, stream);
@@ -1145,6 +1148,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         e->err.ensure(64);
         if (const char* pfm = getenv("TKV_L2_PREFETCH_MB")) e->l2_prefetch_bytes = (size_t)atol(pfm) << 20;
         if (const char* sk = getenv("TKV_TIMING_SKIP")) e->skip_mask = atoi(sk);
+        if (const char* tl = getenv("TKV_TRACE_LAYER")) e->trace_layer = atoi(tl);
         if (const char* gk = getenv("TKV_GEMM_KNOBS")) {  // "stages,smem_kb,ctas_per_sm,evict_first[,np[,pf]]"
             int st = 0, sm = 0, cps = 0, ef = 1, np = 0, pf = -1, kr = -1;
             if (sscanf(gk, "%d,%d,%d,%d,%d,%d,%d", &st, &sm, &cps, &ef, &np, &pf, &kr) >= 3)

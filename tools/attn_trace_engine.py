@@ -1,0 +1,41 @@
+"""clock64 timeline of one attention launch INSIDE the C2 turbo forward (layer TKV_TRACE_LAYER, default 14):
+the engine context (PDL overlap with the QKV epilogue, K/V from HBM) rather than the standalone kernel."""
+import os
+import sys
+
+import numpy as np
+
+os.environ.setdefault("TKV_TRACE_LAYER", "14")
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_2410_07590_b200 import turbokv as T  # noqa: E402
+
+cfg = T.ModelConfig.qwen2_7b_like()
+eng = T.Engine(cfg, bench.SEED, dtype="bf16", store_capacity_tokens=bench.N_CHUNKS * bench.CHUNK_TOKENS * 2)
+payloads, query = bench.workload()
+ids = eng.ingest_chunks(payloads)
+L = T.lib()
+for _ in range(3):
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        eng.prefill_query(ctx, query)
+out = np.zeros(320 + 2048, np.uint64)
+T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 320 + 2048))
+ev = out[:320].reshape(32, 10).astype(np.int64)
+cta = out[320:].reshape(1024, 2).astype(np.int64)
+cta = cta[cta[:, 0] > 0]
+s0 = cta[:, 0].min()
+st, en = (cta[:, 0] - s0) / 1e3, (cta[:, 1] - s0) / 1e3
+print(f"layer {os.environ['TKV_TRACE_LAYER']}: {len(cta)} CTAs, start spread {st.max():.2f} us, "
+      f"end min/median/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f} us")
+t0 = ev[0, 9]
+names = ["smA:S ready", "smA:P arrive", "smB:S ready", "smB:P arrive", "mma:PV_A issued", "mma:PV_B issued",
+         "tma:K(j) issue", "tma:V(j) issue", "mma:Q ready"]
+print("cycles since CTA (0,0,0) entry")
+print("previous kernel done (softmax pdl_wait returned) %d, Q loads back %d, Q staged %d"
+      % (ev[30, 3] - t0, ev[30, 4] - t0, ev[30, 5] - t0))
+print("epilogue: o_done %d, partials written %d" % (ev[31, 0] - t0, ev[31, 1] - t0))
+print("j   " + " ".join(f"{n:>16s}" for n in names))
+for j in range(30):
+    if (ev[j, :9] == 0).all():
+        continue
+    print(f"{j:<3d} " + " ".join(f"{(ev[j, e] - t0) if ev[j, e] else -1:16d}" for e in range(9)))

@@ -1,0 +1,91 @@
+// Weight-stream ceiling through shared memory: one producer thread per CTA fills a STAGES-deep ring either with
+// TMA 2D tensor boxes (128 rows x 64 cols of a [N][K] bf16 matrix: 128 row segments 7 KB apart) or with 1-D bulk
+// copies of contiguous 16 KB blocks (a pre-tiled layout); a consumer thread releases slots (no math).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+__device__ __forceinline__ uint32_t su(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
+    uint32_t d = 0;
+    while (!d)
+        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                     : "=r"(d) : "r"(su(b)), "r"(ph) : "memory");
+}
+template <int MODE>
+__global__ void stream(const __grid_constant__ CUtensorMap tm, const uint8_t* w, int n_tiles, int kb, int stages) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + stages * 16384);
+    uint64_t* empty = full + stages;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&empty[s])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int total = ((n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x) * kb;
+    if (threadIdx.x == 0) {
+        for (int it = 0; it < total; ++it) {
+            const int s = it % stages;
+            wait(&empty[s], ((it / stages) & 1) ^ 1);
+            const int t = blockIdx.x + (it / kb) * gridDim.x, k = it % kb;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16384;" ::"r"(su(&full[s])) : "memory");
+            if (MODE == 0)
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                             ::"r"(su(ring + s * 16384)), "l"((uint64_t)&tm), "r"(su(&full[s])), "r"(k * 64), "r"(t * 128) : "memory");
+            else
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];"
+                             ::"r"(su(ring + s * 16384)), "l"(w + ((size_t)t * kb + k) * 16384), "r"(su(&full[s])) : "memory");
+        }
+    } else if (threadIdx.x == 32) {
+        for (int it = 0; it < total; ++it) {
+            const int s = it % stages;
+            wait(&full[s], (it / stages) & 1);
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su(&empty[s])) : "memory");
+        }
+    }
+}
+typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                        const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int main() {
+    const int N = 37888, K = 3584, kb = K / 64, n_tiles = N / 128;
+    const size_t bytes = (size_t)N * K * 2;
+    uint8_t* w;
+    cudaMalloc(&w, bytes);
+    cudaMemset(w, 1, bytes);
+    void* fn;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    CUtensorMap tm;
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)N}, str[1] = {(cuuint64_t)K * 2};
+    const cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+    ((Enc)fn)(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int mode = 0; mode < 2; ++mode)
+        for (int cfg = 0; cfg < 4; ++cfg) {
+            const int cps = cfg < 2 ? 2 : 1, stages = cfg == 0 ? 4 : cfg == 1 ? 6 : cfg == 2 ? 8 : 12;
+            const size_t smem = 1024 + stages * 16384 + 256;
+            auto k = mode == 0 ? stream<0> : stream<1>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            float best = 1e9;
+            for (int it = 0; it < 5; ++it) {
+                cudaEventRecord(e0);
+                k<<<148 * cps, 64, smem>>>(tm, w, n_tiles, kb, stages);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+            }
+            printf("%s: %d CTAs/SM x %d stages (16 KB): %.0f GB/s  %s\n", mode ? "bulk 1-D contiguous" : "TMA 2-D box",
+                   cps, stages, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+        }
+    return 0;
+}
