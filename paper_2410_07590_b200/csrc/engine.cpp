@@ -416,6 +416,9 @@ struct tkv_engine {
     size_t l2_prefetch_bytes = 0;  // TKV_L2_PREFETCH_MB (tuning knob)
     int skip_mask = 0;             // TKV_TIMING_SKIP: drop kernels for cost attribution (results invalid)
     int trace_layer = -1;          // TKV_TRACE_LAYER: clock64 pipeline trace of that layer's attention launch
+    int attn_split_override = 0;   // TKV_ATTN_SPLITS: force the tcgen05 attention's split-K count
+    int64_t decode_rows_max = 0;   // TKV_DECODE_ROWS: (rows x group) at or below which attention runs SIMT
+                                   // (measured slower than tcgen05 even for one row: default off)
 
     int pick_splits(int M, int N, int K, bool tc) const {
         const int bk = tc ? 64 : 16;
@@ -580,9 +583,14 @@ void tkv_engine::forward(const Fwd& f) {
         const int64_t r0 = tail ? T - 1 : 0;
         auto attend = [&](const void* qrows, tkv_context* actx, const int32_t* lo, const int32_t* hi, void* out,
                           int arows, int aTk, int kv_ready) {
-            const bool tc = dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_ATTN) && attention_tc_supported((int)d, dt);
-            const int splits = tc ? attn_tc_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms)
-                                  : attn_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms);
+            // decode-sized row counts (the last layer's single row, greedy decode): a 128-row tcgen05 tile would be
+            // <= 1/8 full; the split-K SIMT kernel streams the keys with far less per-CTA overhead
+            const bool tiny = (int64_t)arows * (H / Hkv) <= decode_rows_max;
+            const bool tc = dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_ATTN) && !tiny &&
+                            attention_tc_supported((int)d, dt);
+            int splits = tc ? attn_tc_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms)
+                            : attn_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms);
+            if (tc && attn_split_override > 0) splits = attn_split_override;  // TKV_ATTN_SPLITS (tuning)
             AttnWork ws;
             if (splits > 1) {
                 size_t mloff = (size_t)splits * arows * H * d;
@@ -1149,6 +1157,8 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         if (const char* pfm = getenv("TKV_L2_PREFETCH_MB")) e->l2_prefetch_bytes = (size_t)atol(pfm) << 20;
         if (const char* sk = getenv("TKV_TIMING_SKIP")) e->skip_mask = atoi(sk);
         if (const char* tl = getenv("TKV_TRACE_LAYER")) e->trace_layer = atoi(tl);
+        if (const char* as = getenv("TKV_ATTN_SPLITS")) e->attn_split_override = atoi(as);
+        if (const char* dr = getenv("TKV_DECODE_ROWS")) e->decode_rows_max = atol(dr);
         if (const char* gk = getenv("TKV_GEMM_KNOBS")) {  // "stages,smem_kb,ctas_per_sm,evict_first[,np[,pf]]"
             int st = 0, sm = 0, cps = 0, ef = 1, np = 0, pf = -1, kr = -1;
             if (sscanf(gk, "%d,%d,%d,%d,%d,%d,%d", &st, &sm, &cps, &ef, &np, &pf, &kr) >= 3)

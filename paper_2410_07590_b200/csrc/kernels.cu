@@ -370,7 +370,32 @@ __global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, fl
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= vocab) return;
     float acc = 0.f;
-    for (int k = lane; k < hidden; k += 32) acc += ldf(h, k) * ldf(W, (int64_t)warp * hidden + k);
+    constexpr int N = 16 / sizeof(T);  // elements per 16-byte vector
+    if ((hidden % (32 * N)) == 0) {
+        // one warp per vocab row: every 16-byte load of the row (and of h) issued before the FMAs
+        const uint4* wr = reinterpret_cast<const uint4*>(W + (int64_t)warp * hidden);
+        const uint4* hr = reinterpret_cast<const uint4*>(h);
+        const int nv = hidden / N;
+        for (int v0 = lane; v0 < nv; v0 += 32 * 8) {
+            uint4 a[8], b[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (v0 + 32 * u < nv) {
+                    a[u] = __ldcs(wr + v0 + 32 * u);
+                    b[u] = hr[v0 + 32 * u];
+                }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (v0 + 32 * u < nv) {
+                    const T* x = reinterpret_cast<const T*>(&a[u]);
+                    const T* y = reinterpret_cast<const T*>(&b[u]);
+#pragma unroll
+                    for (int e = 0; e < N; ++e) acc += ldf(y, e) * ldf(x, e);
+                }
+        }
+    } else {
+        for (int k = lane; k < hidden; k += 32) acc += ldf(h, k) * ldf(W, (int64_t)warp * hidden + k);
+    }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
         acc *= row_scale(ssp, nb, 0, hidden, eps);  // folded final_norm
