@@ -425,6 +425,30 @@ def run_ours(args):
                     c.close()
             sec = statistics.median(ts)
             c3[tag] = {"requests_per_s": C3_BATCH / sec, "batch_latency_ms": sec * 1e3}
+        # device time of the batched kernels over one profiled step (CUDA events on the engine stream): the
+        # attention here is ONE launch per layer over all 32 requests, no split-K
+        ctxs = [eng.assemble([cids[j] for j in pk], T.PositionMode.Reordered) for pk in picks]
+        eng.profile_reset()
+        eng.profile(True)
+        eng.prefill_query_batch(ctxs, queries)
+        torch.cuda.synchronize(dev)
+        eng.profile(False)
+        for c in ctxs:
+            c.close()
+        a_ms, _ = eng.profile_read("attention")
+        g_ms, _ = eng.profile_read("gemm")
+        P3 = C3_CHUNKS * C3_CHUNK_TOKENS
+        a_flops = C3_BATCH * 4 * cfg.head_num * cfg.head_size * sum(P3 + i + 1 for i in range(QUERY_TOKENS)) * cfg.layer_num
+        g_flops = C3_BATCH * QUERY_TOKENS * cfg.layer_num * (
+            2 * cfg.hidden_size * (cfg.head_num + 2 * cfg.kv_head_num) * cfg.head_size
+            + 2 * cfg.head_num * cfg.head_size * cfg.hidden_size + 6 * cfg.hidden_size * cfg.intermediate_size)
+        c3["attention_roofline"] = {"bound": "tensor", "device_ms": a_ms, "flops": a_flops,
+                                    "achieved": a_flops / (a_ms / 1e3) / 1e12, "peak": peaks["bf16_tflops"],
+                                    "unit": "TFLOP/s", "frac": a_flops / (a_ms / 1e3) / 1e12 / peaks["bf16_tflops"]}
+        c3["projection_gemm_roofline"] = {"bound": "tensor", "device_ms": g_ms, "flops": g_flops,
+                                          "achieved": g_flops / (g_ms / 1e3) / 1e12, "peak": peaks["bf16_tflops"],
+                                          "unit": "TFLOP/s",
+                                          "frac": g_flops / (g_ms / 1e3) / 1e12 / peaks["bf16_tflops"]}
 
     # C4 (BASELINE configs[3]) sample, one GPU's shard: Llama-3-8B shape, 64-token chunks, Zipf(1.1) retrieval of
     # k = 16 chunks per request; the Zipf-hot half of the shard is resident in HBM, the cold half in the pinned

@@ -85,6 +85,7 @@ typedef struct {
 #define TKV_FLAG_NO_GRAPHS 0x4    /* do not capture prefill launch chains into CUDA graphs        */
 #define TKV_FLAG_NO_PDL 0x8       /* launch kernels without programmatic dependent launch          */
 #define TKV_FLAG_L2_PREFETCH 0x10  /* reserved (attention-time L2 weight prefetch: measured no gain) */
+#define TKV_FLAG_BATCH_ATTN 0x20   /* batched prefill: one attention launch even when the batch cannot fill the GPU */
 
 /* IngestStats (pipeline.hpp:35-39) */
 typedef struct {

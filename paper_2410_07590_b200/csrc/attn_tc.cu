@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "dev_common.cuh"
@@ -102,6 +103,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
 // K-major SW128 (rows of 128 B, 8-row atoms 1024 B apart)
@@ -268,6 +275,12 @@ struct AttnArgs {
     float scale;
     unsigned long long* trace;
     L2Prefetch pf;  // weights of the next projections, warmed into L2 by idle producer lanes
+    // batched query prefill (n_req > 0): blockIdx.y = request * Hkv + kv head; request r's rows are tokens
+    // [tok0, tok0 + n) of q/lo/hi/out, its keys the 3-D map maps3[r] over its cache ([2L][Tk][kvd], plane
+    // 2 * layer + K|V)
+    const AttnReq* reqs;
+    const CUtensorMap* maps3;
+    int n_req, layer;
 };
 
 // 10 warps: 3 share an SM sub-partition's 16K registers -> at most 168 registers per thread
@@ -290,10 +303,32 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     pdl_launch();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int group = a.H / a.Hkv, g = blockIdx.y, split = blockIdx.z;
-    const int rows_total = a.Tq * group;
+    const int group = a.H / a.Hkv, split = blockIdx.z;
+    int g = blockIdx.y, Tq = a.Tq, Tk = a.Tk, kv_ready = a.kv_ready;
+    const __nv_bfloat16* qp = a.q;
+    const int32_t* lop = a.lo;
+    const int32_t* hip = a.hi;
+    __nv_bfloat16* outp = a.out;
+    const CUtensorMap* mK = &tmK;
+    const CUtensorMap* mV = &tmV;
+    if (a.n_req > 0) {  // batched: this CTA's request (the table was uploaded before the forward began)
+        const int req = blockIdx.y / a.Hkv;
+        g = blockIdx.y - req * a.Hkv;
+        const AttnReq R = a.reqs[req];
+        Tq = R.n;
+        Tk = R.row0 + R.n;
+        kv_ready = R.row0;
+        qp += (int64_t)R.tok0 * a.H * D;
+        outp += (int64_t)R.tok0 * a.H * D;
+        lop += R.tok0;
+        hip += R.tok0;
+        mK = mV = a.maps3 + req;
+    }
+    const bool b3 = a.n_req > 0;
+    const int rows_total = Tq * group;
     const int rr0 = blockIdx.x * RG;                       // first row of this row group
     const int rows_here = min(RG, rows_total - rr0);
+    if (rows_here <= 0) return;                            // batched grid sized for the longest request
     const bool hasB = rows_here > BR;
 
     const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -319,14 +354,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 8) {
         // key range of the row group = union of its tokens' [lo, hi] (lo/hi were uploaded before the forward)
         if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(mK)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(mV)) : "memory");
         }
         const int t0 = rr0 / group, t1 = (rr0 + rows_here - 1) / group;
         int blo = INT32_MAX, bhi = -1;
         for (int t = t0 + lane; t <= t1; t += 32) {
-            blo = min(blo, a.lo[t]);
-            bhi = max(bhi, min(a.hi[t], a.Tk - 1));
+            blo = min(blo, lop[t]);
+            bhi = max(bhi, min(hip[t], Tk - 1));
         }
         for (int o = 16; o > 0; o >>= 1) {
             blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
@@ -371,7 +406,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             bool waited = false;
             for (int j = 0; j < n; ++j) {
                 const int key = ks + j * BK;
-                if (!waited && key + BK > a.kv_ready) {  // rows written by the previous kernels of this forward
+                if (!waited && key + BK > kv_ready) {  // rows written by the previous kernels of this forward
                     pdl_wait();
                     waited = true;
                 }
@@ -379,14 +414,24 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_wait(&k_empty[sk], ((uint32_t)(j / KST) & 1u) ^ 1u);
                 mbar_expect_tx(&k_full[sk], TILE);
                 const uint32_t kd = sbase + OFF_K + sk * TILE;
-                tma_load_2d(kd, &tmK, &k_full[sk], g * D, key);
-                tma_load_2d(kd + SUB, &tmK, &k_full[sk], g * D + 64, key);
+                if (b3) {
+                    tma_load_3d(kd, mK, &k_full[sk], g * D, key, 2 * a.layer);
+                    tma_load_3d(kd + SUB, mK, &k_full[sk], g * D + 64, key, 2 * a.layer);
+                } else {
+                    tma_load_2d(kd, mK, &k_full[sk], g * D, key);
+                    tma_load_2d(kd + SUB, mK, &k_full[sk], g * D + 64, key);
+                }
                 trace_pipe(j, 6);
                 mbar_wait(&v_empty[sv], ((uint32_t)(j / VST) & 1u) ^ 1u);
                 mbar_expect_tx(&v_full[sv], TILE);
                 const uint32_t vd = sbase + OFF_V + sv * TILE;
-                tma_load_2d(vd, &tmV, &v_full[sv], g * D, key);
-                tma_load_2d(vd + SUB, &tmV, &v_full[sv], g * D + 64, key);
+                if (b3) {
+                    tma_load_3d(vd, mV, &v_full[sv], g * D, key, 2 * a.layer + 1);
+                    tma_load_3d(vd + SUB, mV, &v_full[sv], g * D + 64, key, 2 * a.layer + 1);
+                } else {
+                    tma_load_2d(vd, mV, &v_full[sv], g * D, key);
+                    tma_load_2d(vd + SUB, mV, &v_full[sv], g * D + 64, key);
+                }
                 trace_pipe(j, 7);
             }
         }
@@ -463,8 +508,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool active = rr < rows_total;
         const int t = active ? rr / group : 0;
         const int h = g * group + (active ? rr % group : 0);
-        const int my_lo = active ? a.lo[t] : INT32_MAX;
-        const int my_hi = active ? min(a.hi[t], a.Tk - 1) : -1;
+        const int my_lo = active ? lop[t] : INT32_MAX;
+        const int my_hi = active ? min(hip[t], Tk - 1) : -1;
         pdl_wait();  // q is produced by the previous kernel
         if (tid == 0) trace(30, 3);
         {
@@ -476,7 +521,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // row qr = token * group + head-in-group, walked two rows at a time without per-row division
             int qr = rr0 + x * BR + (warp & 3) * 32 + (lane >> 4);
             int qt = qr / group, qi = qr - qt * group;
-            const uint4* qbase = reinterpret_cast<const uint4*>(a.q) + c + (int64_t)g * group * (D / 8);
+            const uint4* qbase = reinterpret_cast<const uint4*>(qp) + c + (int64_t)g * group * (D / 8);
 #pragma unroll
             for (int it = 0; it < 16; ++it) {
                 v[it] = qr < rows_total ? qbase[((int64_t)qt * a.H + qi) * (D / 8)] : make_uint4(0, 0, 0, 0);
@@ -560,41 +605,46 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             const float moff = m_used == -INFINITY ? 0.f : m_used;  // nothing visible yet -> all p = 0
             const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(-moff, -moff);
-            uint64_t acc0 = 0, acc1 = 0;  // (+0, +0) pairs
+            uint64_t accv = 0;  // (+0, +0)
 #pragma unroll
             for (int c = 0; c < 4; ++c) {  // 32 keys per chunk -> 16 P columns (bf16 pairs), stored as soon as done
-                uint32_t pk[16];
+                // every pair's exponent first (independent MUFU / FMA-pipe work), then conversions and a
+                // log-depth sum: no serial accumulation chain behind the MUFU latency
+                uint64_t pv[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int e = c * 32 + 2 * i;
                     const uint64_t xv = fma2(pk2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sc2, nm2);
-                    uint64_t p;
                     if (i < kPolyPairs) {
-                        p = ex2_poly2(xv);
+                        pv[i] = ex2_poly2(xv);
                     } else {
                         float x0, x1;
                         up2(xv, x0, x1);
-                        p = pk2(ex2(x0), ex2(x1));
+                        pv[i] = pk2(ex2(x0), ex2(x1));
                     }
-                    if (i & 1)
-                        acc1 = add2(acc1, p);
-                    else
-                        acc0 = add2(acc0, p);
+                }
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
                     float p0, p1;
-                    up2(p, p0, p1);
+                    up2(pv[i], p0, p1);
                     pk[i] = bf16x2_bits(p0, p1);
                 }
                 tmem_st16(tS + c * 16, pk);
+#pragma unroll
+                for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+                    for (int i = 0; i < w; ++i) pv[i] = add2(pv[i], pv[i + w]);
+                accv = add2(accv, pv[0]);
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&p_full[x * 4 + c]);  // the PV MMA on these 32 keys may start
                 if (c == 1) trace_sm(j, 6);
                 if (c == 3) trace_sm(j, 7);
             }
-            float a0, a1, a2, a3;
-            up2(acc0, a0, a1);
-            up2(acc1, a2, a3);
-            l += (a0 + a1) + (a2 + a3);
+            float a0, a1;
+            up2(accv, a0, a1);
+            l += a0 + a1;
             trace_sm(j, 8);
             if (tid == 0) trace(j, 1);
             if (tid == 128) trace(j, 3);
@@ -648,7 +698,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                              : "r"(stage + (cc >> 3) * SUB + swz(row, cc & 7)));
                 if (a.splits == 1) {
                     if (qr < rows_total)
-                        reinterpret_cast<uint4*>(a.out + ((int64_t)(qr / group) * a.H + g * group + qr % group) * D)[cc] = v;
+                        reinterpret_cast<uint4*>(outp + ((int64_t)(qr / group) * a.H + g * group + qr % group) * D)[cc] = v;
                 } else {
                     reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.ws_o) + (wrow0 + x * BR + row) * D)[cc] = v;
                 }
@@ -751,6 +801,47 @@ CUtensorMap kv_map(const void* base, int rows, int cols, int ld) {
 }
 
 }  // namespace
+
+void attn_tc_cache_map(const void* cache, int64_t rows, int64_t cap, int kv_dim, int L, void* map128) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {(cuuint64_t)kv_dim, (cuuint64_t)rows, (cuuint64_t)(2 * L)};
+    const cuuint64_t strides[2] = {(cuuint64_t)kv_dim * 2, (cuuint64_t)(cap * kv_dim * 2)};
+    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(cache), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(TKV_ERR_CUDA, "cuTensorMapEncodeTiled (cache map) failed: " + std::to_string((int)r));
+    static_assert(sizeof(CUtensorMap) == 128, "tensor map size");
+    memcpy(map128, &m, sizeof m);
+}
+
+void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* maps, int n_req, int max_rows, int H,
+                               int Hkv, int layer, const int32_t* lo, const int32_t* hi, void* out, int* err,
+                               cudaStream_t s) {
+    TKV_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    const int group = H / Hkv;
+    AttnArgs a{};
+    a.q = (const __nv_bfloat16*)q;
+    a.lo = lo;
+    a.hi = hi;
+    a.out = (__nv_bfloat16*)out;
+    a.err = err;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.splits = 1;
+    a.scale = (float)(1.0 / sqrt((double)D));
+    a.trace = g_trace_host;
+    a.reqs = reqs;
+    a.maps3 = static_cast<const CUtensorMap*>(maps);
+    a.n_req = n_req;
+    a.layer = layer;
+    CUtensorMap unused;
+    memset(&unused, 0, sizeof unused);
+    launch_k(attn_tc_kernel, dim3((max_rows * group + RG - 1) / RG, Hkv * n_req, 1), THREADS, SMEM_BYTES, s, unused,
+             unused, a);
+    TKV_CUDA(cudaGetLastError());
+}
 
 void attn_trace_enable(bool on, unsigned long long** host_view) {
     static unsigned long long* buf = nullptr;

@@ -285,7 +285,7 @@ struct tkv_engine {
     // forward workspace
     // x: fp32 residual stream; xb = x * norm_w (GEMM input; the RMSNorm scale is folded into consumers); ssp:
     // per-row partial sums of squares (norm_blocks(hid) per row)
-    DevMem x, xb, ssp, q, attn, act, partial, attn_ws, logits, err, d_tok, d_pos, d_lo, d_hi, d_page, d_slot, d_segs;
+    DevMem x, xb, ssp, q, attn, act, partial, attn_ws, d_breq, d_bmaps, logits, err, d_tok, d_pos, d_lo, d_hi, d_page, d_slot, d_segs;
     StagingRing staging;
     std::vector<std::pair<size_t, void*>> ctx_free;  // recycled request-cache buffers
     std::set<tkv_context*> live;
@@ -475,6 +475,9 @@ struct tkv_engine {
             int tok0, n, row0;
         };
         std::vector<Req> reqs;
+        const AttnReq* batch_reqs = nullptr;  // device request table + cache maps of the batched attention
+        const void* batch_maps = nullptr;
+        int batch_max_n = 0;
     };
     void forward(const Fwd& f);
     void check_err(const char* where);
@@ -622,7 +625,12 @@ void tkv_engine::forward(const Fwd& f) {
                                       aTk, (int)H, (int)Hkv, (int)d, splits, ws, err.as<int>(), dt, stream);
             }
         };
-        if (batch) {
+        if (batch && f.batch_maps) {
+            // one launch for the whole batch (enough row groups to fill the GPU without split-K)
+            Scope sc(this, PC_ATTN, 1);
+            launch_attention_tc_batch(q.p, f.batch_reqs, f.batch_maps, (int)f.reqs.size(), f.batch_max_n, (int)H,
+                                      (int)Hkv, (int)l, f.lo, f.hi, attn.p, err.as<int>(), stream);
+        } else if (batch) {
             for (const Fwd::Req& r : f.reqs)
                 attend(static_cast<uint8_t*>(q.p) + (size_t)r.tok0 * qd * es, r.ctx, f.lo + r.tok0, f.hi + r.tok0,
                        static_cast<uint8_t*>(attn.p) + (size_t)r.tok0 * qd * es, r.n, r.row0 + r.n, r.row0);
@@ -1620,6 +1628,31 @@ tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int6
         }
         e->ensure_rope(max_pos);
         upload_stage(e, s, true);
+        // batched attention: one launch when the batch alone fills the GPU (bf16, head_size 128)
+        const int group = (int)(e->H / e->Hkv);
+        int64_t row_groups = 0;
+        int max_n = 0;
+        for (const auto& r : f.reqs) {
+            row_groups += ((int64_t)r.n * group + 255) / 256 * e->Hkv;
+            max_n = std::max(max_n, r.n);
+        }
+        if (e->dt == DT::BF16 && !(e->opts.flags & TKV_FLAG_SIMT_ATTN) && attention_tc_supported((int)e->d, e->dt) &&
+            (row_groups >= e->num_sms || (e->opts.flags & TKV_FLAG_BATCH_ATTN))) {
+            std::vector<AttnReq> rq;
+            std::vector<uint8_t> maps((size_t)n_req * 128);
+            for (size_t r = 0; r < f.reqs.size(); ++r) {
+                const auto& q = f.reqs[r];
+                rq.push_back({q.tok0, q.n, q.row0, 0});
+                attn_tc_cache_map(q.ctx->kv, q.row0 + q.n, q.ctx->cap, (int)e->kvd, (int)e->L, maps.data() + r * 128);
+            }
+            e->d_breq.ensure(rq.size() * sizeof(AttnReq));
+            e->d_bmaps.ensure(maps.size());
+            TKV_CUDA(cudaMemcpyAsync(e->d_breq.p, rq.data(), rq.size() * sizeof(AttnReq), cudaMemcpyHostToDevice, e->stream));
+            TKV_CUDA(cudaMemcpyAsync(e->d_bmaps.p, maps.data(), maps.size(), cudaMemcpyHostToDevice, e->stream));
+            f.batch_reqs = e->d_breq.as<AttnReq>();
+            f.batch_maps = e->d_bmaps.p;
+            f.batch_max_n = max_n;
+        }
         f.tok = e->d_tok.as<int32_t>();
         f.T = (int)T;
         f.pos = e->d_pos.as<int32_t>();

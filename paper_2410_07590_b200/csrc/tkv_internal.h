@@ -154,6 +154,16 @@ struct L2Prefetch {
 // SIMT; split-K partials (bf16 O/l) are merged by a PDL-launched combine kernel. Key rows
 // < kv_ready were written before the current forward began and are loaded before griddepcontrol.wait.
 bool attention_tc_supported(int d, DT dt);
+// Batched query prefill: one launch covers every request (rows of request r are tokens [tok0, tok0 + n) of the
+// forward; its keys are [0, row0 + n) of its own cache, read through a 3-D tensor map over the cache
+// [2L][row0 + n][kv_dim] encoded by attn_tc_cache_map). No split-K: the batch supplies the CTAs.
+struct AttnReq {
+    int tok0, n, row0, pad;
+};
+void attn_tc_cache_map(const void* cache, int64_t rows, int64_t cap, int kv_dim, int L, void* map128);
+void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* maps, int n_req, int max_rows, int H,
+                               int Hkv, int layer, const int32_t* lo, const int32_t* hi, void* out, int* err,
+                               cudaStream_t s);
 void attn_trace_enable(bool on, unsigned long long** device_buf);  // debug timeline of CTA (0,0,0)
 int attn_tc_row_groups(int Tq, int H, int Hkv);
 // workspace of the tcgen05 kernel's split merge (floats); ws.ml = ws.o + *ml_offset

@@ -449,3 +449,27 @@ def test_host_spill_tier_is_bit_exact_and_transparent(golden, dtype):
     spill.store_evict(ids[2])
     assert spill.store_tiers()["host_used"] == 2
     spill.close()
+
+
+
+@pytest.mark.parametrize("name", ["qwen1"])
+def test_batched_attention_single_launch_vs_golden(golden, name):
+    """The batched prefill's single attention launch over every request's cache (3-D tensor maps; the C3 path),
+    forced on a small batch, against the reference's logits and the per-request path."""
+    meta, A = golden
+    m = meta[name]
+    eng = engine(cfg_t(m), m["seed"], "bf16", flags=0x20)  # TKV_FLAG_BATCH_ATTN
+    ids = eng.ingest_chunks(payloads(A, name))
+    q = A[f"{name}.query"]
+    ctxs = [eng.assemble(ids, T.PositionMode.Reordered), eng.assemble(ids, T.PositionMode.Composite),
+            eng.assemble(ids[:1], T.PositionMode.Reordered)]
+    q3 = np.asarray(q[:5])
+    logits = eng.prefill_query_batch(ctxs, [q, q, q3])
+    for r, tag in ((0, "reordered"), (1, "composite")):
+        ref = A[f"{name}.turbo_{tag}.logits"]
+        assert_close(logits[r], ref, BF16_TOL)
+        assert_argmax(logits[r], ref, BF16_TOL)
+    with eng.assemble(ids[:1], T.PositionMode.Reordered) as single:
+        assert_close(logits[2], eng.prefill_query(single, q3)[0], BF16_TOL)
+    for c in ctxs:
+        c.close()

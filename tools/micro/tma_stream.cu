@@ -13,10 +13,12 @@ __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
                      : "=r"(d) : "r"(su(b)), "r"(ph) : "memory");
 }
 template <int MODE>
-__global__ void stream(const __grid_constant__ CUtensorMap tm, const uint8_t* w, int n_tiles, int kb, int stages) {
+__global__ void stream(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap ta, const uint8_t* w,
+                       int n_tiles, int kb, int stages) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + stages * 16384);
+    constexpr uint32_t SB = MODE == 2 ? 16384 + 8192 : 16384;  // stage bytes
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + stages * SB);
     uint64_t* empty = full + stages;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -32,13 +34,16 @@ __global__ void stream(const __grid_constant__ CUtensorMap tm, const uint8_t* w,
             const int s = it % stages;
             wait(&empty[s], ((it / stages) & 1) ^ 1);
             const int t = blockIdx.x + (it / kb) * gridDim.x, k = it % kb;
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16384;" ::"r"(su(&full[s])) : "memory");
-            if (MODE == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&full[s])), "r"(SB) : "memory");
+            if (MODE == 2)
                 asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-                             ::"r"(su(ring + s * 16384)), "l"((uint64_t)&tm), "r"(su(&full[s])), "r"(k * 64), "r"(t * 128) : "memory");
+                             ::"r"(su(ring + s * SB + 16384)), "l"((uint64_t)&ta), "r"(su(&full[s])), "r"(k * 64), "r"(0) : "memory");
+            if (MODE == 0 || MODE == 2)
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                             ::"r"(su(ring + s * SB)), "l"((uint64_t)&tm), "r"(su(&full[s])), "r"(k * 64), "r"(t * 128) : "memory");
             else
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];"
-                             ::"r"(su(ring + s * 16384)), "l"(w + ((size_t)t * kb + k) * 16384), "r"(su(&full[s])) : "memory");
+                             ::"r"(su(ring + s * SB)), "l"(w + ((size_t)t * kb + k) * 16384), "r"(su(&full[s])) : "memory");
         }
     } else if (threadIdx.x == 32) {
         for (int it = 0; it < total; ++it) {
@@ -65,26 +70,36 @@ int main() {
     const cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
     ((Enc)fn)(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    uint8_t* act;
+    cudaMalloc(&act, (size_t)64 * K * 2);
+    cudaMemset(act, 1, (size_t)64 * K * 2);
+    CUtensorMap ta;
+    const cuuint64_t adims[2] = {(cuuint64_t)K, 64}, astr[1] = {(cuuint64_t)K * 2};
+    const cuuint32_t abox[2] = {64, 64};
+    ((Enc)fn)(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, act, adims, astr, abox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int mode = 0; mode < 2; ++mode)
+    for (int mode = 0; mode < 3; ++mode)
         for (int cfg = 0; cfg < 4; ++cfg) {
             const int cps = cfg < 2 ? 2 : 1, stages = cfg == 0 ? 4 : cfg == 1 ? 6 : cfg == 2 ? 8 : 12;
-            const size_t smem = 1024 + stages * 16384 + 256;
-            auto k = mode == 0 ? stream<0> : stream<1>;
+            const size_t smem = 1024 + stages * (mode == 2 ? 24576 : 16384) + 256;
+            if (smem > 232448) continue;
+            auto k = mode == 0 ? stream<0> : mode == 1 ? stream<1> : stream<2>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             float best = 1e9;
             for (int it = 0; it < 5; ++it) {
                 cudaEventRecord(e0);
-                k<<<148 * cps, 64, smem>>>(tm, w, n_tiles, kb, stages);
+                k<<<148 * cps, 64, smem>>>(tm, ta, w, n_tiles, kb, stages);
                 cudaEventRecord(e1);
                 cudaEventSynchronize(e1);
                 float ms;
                 cudaEventElapsedTime(&ms, e0, e1);
                 best = ms < best ? ms : best;
             }
-            printf("%s: %d CTAs/SM x %d stages (16 KB): %.0f GB/s  %s\n", mode ? "bulk 1-D contiguous" : "TMA 2-D box",
+            printf("%s: %d CTAs/SM x %d stages: %.0f GB/s of weights  %s\n",
+                   mode == 0 ? "TMA 2-D box" : mode == 1 ? "bulk 1-D contiguous" : "TMA box + 8 KB activation box",
                    cps, stages, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
         }
     return 0;
