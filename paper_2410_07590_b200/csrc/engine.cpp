@@ -426,7 +426,7 @@ struct tkv_engine {
         const int kb = (K + bk - 1) / bk;
         // tcgen05: gemm_tc_ctas_per_sm() persistent CTAs per SM; round DOWN so splits x tiles fills one wave of
         // them (every resident CTA streams weights; at 1 unit per SM half the CTA slots idled)
-        int s = tc ? num_sms * gemm_tc_ctas_per_sm() / tiles : (num_sms + tiles - 1) / tiles;
+        int s = tc ? num_sms * gemm_tc_ctas_per_sm(M) / tiles : (num_sms + tiles - 1) / tiles;
         s = std::min(s, std::max(1, kb / 4));
         s = std::min(s, 16);
         s = std::max(s, 1);

@@ -42,6 +42,9 @@ struct Knobs {
     // (np = 2 with one 208 KB CTA per SM measured slower than np = 1 at 2 x 110 KB); pf = L2 prefetch distance
     // of the weight stream in k-blocks (0 = off)
     int stages = 0, smem_kb = 110, ctas_per_sm = 2, w_evict_first = 1, np = 1, pf = 0, krot = 1;
+    // normal (> 128 tokens) tiling: nsnp 128-column halves per MMA (UMMA N = 128 * nsnp); N = 256 halves the
+    // shared-memory traffic per FLOP of the SS-mode MMA (the 128 x 128 tile is smem-bandwidth bound at ~50 %)
+    int nsnp = 2, ns_smem_kb = 208;
 };
 Knobs g_knobs;
 
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(THREADS_P)
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer ----------------
-            const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128);
+            const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128 * g.np);
             int it = 0, lu = 0;
             for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++lu) {
                 int nt, mt, z;
@@ -298,9 +301,9 @@ __global__ void __launch_bounds__(THREADS_P)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t acc_u = tmem + lane_base + (uint32_t)b * g.acc_cols;
             const int m0 = mt * mstep;
-            for (int p = 0; p < (SWAP ? g.np : 1); ++p) {
-            const uint32_t acc = acc_u + (uint32_t)(p * (SWAP ? g.ntok : 0));
-            const int n0 = (nt * (SWAP ? g.np : 1) + p) * 128;
+            for (int p = 0; p < g.np; ++p) {
+            const uint32_t acc = acc_u + (uint32_t)(p * (SWAP ? g.ntok : 128));
+            const int n0 = (nt * g.np + p) * 128;
             if (SWAP) {
                 const int n = n0 + lg * 32 + lane;  // TMEM lane = weight row n, column = token
                 if (EPI == EPI_PARTIAL) {
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(THREADS_P)
                     }
                 } else {
                     const int inter = g.N / 2;
-                    const int i0 = nt * 64;
+                    const int i0 = (n0 / 128) * 64;
                     const float sc = m < g.M ? row_scale(g.ssp, g.nb, m, g.K, g.eps) : 0.f;  // folded mlp_norm
 #pragma unroll 1
                     for (int c = 0; c < 64; c += 16) {
@@ -459,9 +462,12 @@ bool gemm_tc_supported(int M, int N, int K, int lda) {
     return M >= 1 && N >= 1 && K >= 8 && (lda * 2) % 16 == 0 && (K * 2) % 16 == 0;
 }
 
-int gemm_tc_ctas_per_sm() { return std::max(1, g_knobs.ctas_per_sm); }
+int gemm_tc_ctas_per_sm(int M) { return M <= 128 ? std::max(1, g_knobs.ctas_per_sm) : 1; }
 
-static int np_for(int M, int N) { return (M <= 128 && (N + 127) / 128 >= 2) ? std::max(1, g_knobs.np) : 1; }
+static int np_for(int M, int N) {
+    if ((N + 127) / 128 < 2) return 1;
+    return M <= 128 ? std::max(1, g_knobs.np) : std::max(1, std::min(2, g_knobs.nsnp));
+}
 
 int gemm_tc_tiles(int M, int N) {
     const bool swap = M <= 128;
@@ -485,12 +491,12 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.units = g.n_tiles * g.m_tiles * eff_splits;
     g.ntok = swap ? ((M + 15) / 16) * 16 : 128;
     g.a_bytes = (uint32_t)g.ntok * BK * 2;
-    g.acc_cols = swap ? (uint32_t)(g.ntok * g.np) : 128u;
+    g.acc_cols = swap ? (uint32_t)(g.ntok * g.np) : 128u * (uint32_t)g.np;
     g.tmem_cols = 32;
     while (g.tmem_cols < 2 * g.acc_cols) g.tmem_cols <<= 1;
     const uint32_t scratch =
         (swap && swiglu_act) ? (uint32_t)((64 * (g.ntok + 1) + g.ntok) * 4 + 1023) / 1024 * 1024 : 0;
-    const int budget = (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET);
+    const int budget = swap ? (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET) : g_knobs.ns_smem_kb * 1024;
     g.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
                                        (uint32_t)(budget - (int)scratch) / (g.np * TILE_W + g.a_bytes));
     if (g.stages < 2) fail(TKV_ERR_CONFIG, "GEMM smem budget too small");
@@ -507,7 +513,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min(g.units, sms * std::max(1, g_knobs.ctas_per_sm));
+    const int grid = std::min(g.units, sms * gemm_tc_ctas_per_sm(M));
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
     const CUtensorMap tw = make_map(W, N, K, K, 128 * g.np);
     if (swiglu_act) {

@@ -125,7 +125,7 @@ bool gemm_tc_supported(int M, int N, int K, int lda);
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np = 0, int pf = -1,
                     int krot = -1);
 int gemm_tc_tiles(int M, int N);
-int gemm_tc_ctas_per_sm();  // resident GEMM CTAs per SM the launcher plans for (knob)
+int gemm_tc_ctas_per_sm(int M);  // resident GEMM CTAs per SM the launcher plans for M tokens
 // Returns the number of split-K partial planes actually written (<= splits: every split is non-empty).
 // The SwiGLU epilogue applies the folded RMSNorm scale row_scale(ssp, token) (ssp/nb/eps: see launch_residual).
 int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
