@@ -148,6 +148,9 @@ class Port:
             L.tko_rope_rotate.argtypes = [F64P, C.c_int64, C.c_int64, I64P, C.c_int64, C.c_double]
             L.tko_flops_total.restype = C.c_uint64
             L.tko_flops_total.argtypes = [C.POINTER(OracleCfg), C.c_int64, C.c_int64, C.c_int64]
+            L.tko_embed.argtypes = [I32P, C.c_int64, C.c_int64, F64P]
+            L.tko_top_k.restype = C.c_int64
+            L.tko_top_k.argtypes = [F64P, U64P, C.c_int64, C.c_int64, F64P, C.c_int64, U64P, F64P]
             cls._lib = L
         return cls._lib
 
@@ -275,6 +278,30 @@ class Port:
     def flops_total(cfg: Cfg, n_input, n_context, batch=1) -> int:
         return Port.lib().tko_flops_total(C.byref(cfg.c()), n_input, n_context, batch)
 
+    @staticmethod
+    def embed(tokens, dim: int = 256) -> np.ndarray:
+        """retrieval.cpp:64-88 restated."""
+        t = np.ascontiguousarray(tokens, np.int32)
+        out = np.zeros(dim, np.float64)
+        rc = Port.lib().tko_embed(ptr(t, I32P), len(t), dim, ptr(out, F64P))
+        if rc:
+            raise OracleError(rc, Port.lib().tko_last_error().decode())
+        return out
+
+    @staticmethod
+    def top_k(emb: np.ndarray, ids, query: np.ndarray, k: int):
+        """RetrievalIndex::top_k (retrieval.cpp:117-133) restated: (ids, cosines)."""
+        emb = np.ascontiguousarray(emb, np.float64)
+        idv = np.ascontiguousarray(ids, np.uint64)
+        q = np.ascontiguousarray(query, np.float64)
+        oi = np.zeros(max(1, min(k, len(idv))), np.uint64)
+        os_ = np.zeros(len(oi), np.float64)
+        n = Port.lib().tko_top_k(ptr(emb, F64P), ptr(idv, U64P), len(idv), emb.shape[1], ptr(q, F64P), k,
+                                 ptr(oi, U64P), ptr(os_, F64P))
+        if n < 0:
+            raise OracleError(-n, Port.lib().tko_last_error().decode())
+        return oi[:n], os_[:n]
+
 
 class Ref:
     """The reference library itself (proj/src compiled in place + oracle/ref_capi.cpp)."""
@@ -321,6 +348,8 @@ class Ref:
                                      C.c_int64, F64P]
             L.ref_flops_compare.argtypes = [C.POINTER(OracleCfg), C.c_int64, C.c_int64, C.c_int64, U64P, U64P,
                                             F64P]
+            L.ref_embed.argtypes = [I32P, C.c_int64, C.c_int64, F64P]
+            L.ref_top_k.argtypes = [F64P, U64P, C.c_int64, C.c_int64, F64P, C.c_int64, U64P, I64P]
             cls._lib = L
         return cls._lib
 
@@ -328,6 +357,24 @@ class Ref:
     def check(cls, rc: int):
         if rc:
             raise OracleError(rc, cls.lib().ref_last_error().decode())
+
+    @classmethod
+    def embed(cls, tokens, dim: int = 256) -> np.ndarray:
+        t = np.ascontiguousarray(tokens, np.int32)
+        out = np.zeros(dim, np.float64)
+        cls.check(cls.lib().ref_embed(ptr(t, I32P), len(t), dim, ptr(out, F64P)))
+        return out
+
+    @classmethod
+    def top_k(cls, emb: np.ndarray, ids, query: np.ndarray, k: int) -> np.ndarray:
+        emb = np.ascontiguousarray(emb, np.float64)
+        idv = np.ascontiguousarray(ids, np.uint64)
+        q = np.ascontiguousarray(query, np.float64)
+        out = np.zeros(max(1, min(k, len(idv))), np.uint64)
+        n = C.c_int64()
+        cls.check(cls.lib().ref_top_k(ptr(emb, F64P), ptr(idv, U64P), len(idv), emb.shape[1], ptr(q, F64P), k,
+                                      ptr(out, U64P), C.byref(n)))
+        return out[:n.value]
 
     @classmethod
     def identity(cls, cfg: Cfg, seed: int):

@@ -24,6 +24,7 @@
 #include "turbokv/errors.hpp"
 #include "turbokv/model.hpp"
 #include "turbokv/pipeline.hpp"
+#include "turbokv/retrieval.hpp"
 #include "turbokv/rng.hpp"
 #include "turbokv/rope.hpp"
 
@@ -116,6 +117,31 @@ void copy_ctx_out(const AssembledContext& ctx, int64_t* positions, int64_t* next
 }  // namespace
 
 extern "C" {
+
+// retrieval.cpp:64-88 (embed) and :117-133 (RetrievalIndex::top_k over records built from `emb`/`ids`)
+int ref_embed(const int32_t* tokens, int64_t n, int64_t dim, double* out) {
+    return guard([&] {
+        std::vector<Token> t(tokens, tokens + n);
+        auto v = embed(t, dim);
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
+int ref_top_k(const double* emb, const uint64_t* ids, int64_t n, int64_t dim, const double* query, int64_t k,
+              uint64_t* ids_out, int64_t* n_out) {
+    return guard([&] {
+        RetrievalIndex idx;
+        for (int64_t r = 0; r < n; ++r) {
+            ChunkRecord rec;
+            rec.chunk_id = ids[r];
+            rec.embedding.assign(emb + r * dim, emb + (r + 1) * dim);
+            idx.add(std::move(rec));
+        }
+        auto top = idx.top_k(std::vector<double>(query, query + dim), k);
+        std::memcpy(ids_out, top.data(), top.size() * sizeof(uint64_t));
+        *n_out = (int64_t)top.size();
+    });
+}
 
 const char* ref_last_error() { return g_err.c_str(); }
 

@@ -558,3 +558,68 @@ uint64_t tko_flops_total(const tko_config* c, int64_t n_input, int64_t n_context
     const uint64_t mlp = 6ULL * (uint64_t)c->hidden_size * (uint64_t)c->intermediate_size;
     return (uint64_t)batch * (uint64_t)n_input * (uint64_t)c->layer_num * (qkv + attn + o + mlp);
 }
+
+
+/* ---- retrieval (retrieval.cpp) ---- */
+int tko_embed(const int32_t* tokens, int64_t n, int64_t dim, double* out) {
+    if (n < 1) return fail(3, "embed: empty token list");
+    if (dim < 1) return fail(3, "embed: dimension must be >= 1");
+    for (int64_t i = 0; i < dim; ++i) out[i] = 0.0;
+    int32_t prev = -1; /* sentinel precedes the first token (retrieval.cpp:70) */
+    for (int64_t i = 0; i < n; ++i) {
+        fnv f;
+        fnv_init(&f);
+        fnv_u32(&f, (uint32_t)prev);
+        fnv_u32(&f, (uint32_t)tokens[i]);
+        const uint64_t h = f.h;
+        out[h % (uint64_t)dim] += (h >> 63) ? -1.0 : 1.0;
+        prev = tokens[i];
+    }
+    double ss = 0.0;
+    for (int64_t i = 0; i < dim; ++i) ss += out[i] * out[i];
+    if (ss == 0.0) { /* signed counts cancelled exactly (retrieval.cpp:80-84) */
+        out[0] = 1.0;
+        ss = 1.0;
+    }
+    const double inv = 1.0 / sqrt(ss);
+    for (int64_t i = 0; i < dim; ++i) out[i] *= inv;
+    return 0;
+}
+
+typedef struct {
+    double score;
+    uint64_t id;
+} tko_scored;
+
+static int scored_cmp(const void* pa, const void* pb) {
+    const tko_scored* a = (const tko_scored*)pa;
+    const tko_scored* b = (const tko_scored*)pb;
+    if (a->score != b->score) return a->score > b->score ? -1 : 1;
+    return a->id < b->id ? -1 : (a->id > b->id ? 1 : 0);
+}
+
+int64_t tko_top_k(const double* emb, const uint64_t* ids, int64_t n, int64_t dim, const double* q, int64_t k,
+                  uint64_t* ids_out, double* scores_out) {
+    if (k < 1) return -fail(3, "top_k: k must be >= 1");
+    if (n < 1) return -fail(3, "top_k: empty index");
+    tko_scored* sc = (tko_scored*)malloc((size_t)n * sizeof *sc);
+    for (int64_t r = 0; r < n; ++r) {
+        const double* b = emb + r * dim;
+        double dot = 0.0, na = 0.0, nb = 0.0; /* cosine, retrieval.cpp:90-100 (same operation order) */
+        for (int64_t i = 0; i < dim; ++i) {
+            dot += q[i] * b[i];
+            na += q[i] * q[i];
+            nb += b[i] * b[i];
+        }
+        sc[r].score = dot / sqrt(na * nb);
+        sc[r].id = ids[r];
+    }
+    qsort(sc, (size_t)n, sizeof *sc, scored_cmp);
+    const int64_t take = k < n ? k : n;
+    for (int64_t i = 0; i < take; ++i) {
+        ids_out[i] = sc[i].id;
+        if (scores_out) scores_out[i] = sc[i].score;
+    }
+    free(sc);
+    return take;
+}

@@ -85,6 +85,13 @@ int tko_rope_rotate(double* rows, int64_t n_rows, int64_t cols, const int64_t* p
 /* Appendix-C cost model (costmodel.cpp:11-83). */
 uint64_t tko_flops_total(const tko_config* c, int64_t n_input, int64_t n_context, int64_t batch);
 
+/* Retrieval (retrieval.cpp:64-88 embed, :90-100 cosine, :117-133 top_k). embed: feature-hashed token bigrams
+ * with a leading -1 sentinel, FNV-1a over the two u32s, bucket h % dim, sign by the top bit, L2-normalised.
+ * top_k: cosine against every row, sorted by cosine descending then chunk id ascending; returns min(k, n). */
+int tko_embed(const int32_t* tokens, int64_t n, int64_t dim, double* out);
+int64_t tko_top_k(const double* emb, const uint64_t* ids, int64_t n, int64_t dim, const double* query, int64_t k,
+                  uint64_t* ids_out, double* scores_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -139,3 +139,25 @@ def test_restatement_equals_reference_random_grid(tmp_path):
             framed = [O.frame(x) for x in pays]
             k, v, pos, nxt = p.assemble(framed, True)
             assert np.array_equal(p.prefill_query(k, v, pos, nxt, q), ref_logits)
+
+
+def test_retrieval_restatement_matches_reference():
+    """embed (retrieval.cpp:64-88) and top_k (retrieval.cpp:117-133): the C restatement against the reference
+    itself, bit for bit, including cosine ties broken by ascending chunk id and the cancelled-counts edge case."""
+    rng = np.random.default_rng(5)
+    docs = [O.random_text_tokens(100 + i, int(rng.integers(1, 300))) for i in range(60)]
+    docs += [np.array([97, 98], np.int32), np.array([97], np.int32)]
+    docs += [docs[3].copy(), docs[7].copy()]  # duplicates: identical cosines, tie-break by id
+    emb = np.stack([O.Port.embed(d) for d in docs])
+    for d, e in zip(docs, emb):
+        assert np.array_equal(e, O.Ref.embed(d))
+        assert abs(np.linalg.norm(e) - 1.0) < 1e-12
+    ids = rng.permutation(np.arange(1, len(docs) + 1, dtype=np.uint64) * 0x9E3779B97F4A7C15)
+    for qseed in range(5):
+        q = O.Port.embed(O.random_text_tokens(7000 + qseed, 50))
+        for k in (1, 5, 16, 200):
+            got, scores = O.Port.top_k(emb, ids, q, k)
+            assert np.array_equal(got, O.Ref.top_k(emb, ids, q, k))
+            assert np.all(np.diff(scores) <= 0)
+    with pytest.raises(O.OracleError):
+        O.Port.top_k(emb, ids, q, 0)
