@@ -483,12 +483,21 @@ def run_ours(args):
                 all_tok += C4_K * C4_CHUNK_TOKENS
             ctx.close()
         tiers = eng4.store_tiers()
+        # retrieval (§8f row 3): cosine top-16 over the shard's index (auto-built by ingest), GPU scoring + top-k
+        rq = [rng.integers(97, 123, QUERY_TOKENS).astype(np.int32) for _ in range(5)]
+        eng4.top_k(rq[0], C4_K)
+        tr = []
+        for qv in rq:
+            t0 = time.perf_counter()
+            eng4.top_k(qv, C4_K)
+            tr.append(time.perf_counter() - t0)
         c4 = {"workload": f"C4 sample (one GPU's shard): Llama-3-8B shape, {C4_SHARD} chunks x {C4_CHUNK_TOKENS} "
                           f"tokens, Zipf(1.1) retrieval of k={C4_K}, + {QUERY_TOKENS}-token query, batch 1; "
                           f"{args.c4_requests} requests after 3 warm-up",
               "p50_ttft_ms": statistics.median(ts) * 1e3, "requests_per_s": 1.0 / statistics.median(ts),
               "hbm_resident_chunk_fraction": tiers["hbm_used"] / max(1, tiers["hbm_used"] + tiers["host_used"]),
               "hbm_hit_token_fraction": hbm_tok / max(1, all_tok), "shard_ingest_s": ingest4,
+              "retrieval_top16_ms": statistics.median(tr) * 1e3, "index_size": eng4.index_size(),
               "store_pages": tiers}
         eng4.close()
         torch.cuda.empty_cache()

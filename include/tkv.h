@@ -150,6 +150,15 @@ tkv_status tkv_store_count(const tkv_engine* eng, int64_t* chunks, int64_t* page
  * of TKVC files, kvstore.cpp:78-211; this is the capacity policy of the HBM store). Contexts assembled earlier
  * keep their gathered KV; only their unrotated re-read (tkv_context_read_kv, rotated=0) then fails StaleCache. */
 tkv_status tkv_store_evict(tkv_engine* eng, uint64_t chunk_id);
+/* Retrieval: embed (retrieval.cpp:64-88) on the host, exhaustive cosine top-k over the index
+ * in HBM (retrieval.cu), ranking identical to RetrievalIndex::top_k (retrieval.cpp:117-133): cosine descending,
+ * ties by ascending chunk id, min(k, size) results, k in [1, 256] when the index holds more than 256 chunks.
+ * tkv_ingest_chunks indexes every newly ingested chunk over its unframed payload; tkv_index_add adds one. */
+tkv_status tkv_embed(const int32_t* tokens, int64_t n, int64_t dim, double* out);
+tkv_status tkv_index_add(tkv_engine* eng, uint64_t chunk_id, const int32_t* payload, int64_t n, int* added);
+int64_t tkv_index_size(const tkv_engine* eng);
+tkv_status tkv_index_top_k(tkv_engine* eng, const int32_t* query, int64_t n, int64_t k, uint64_t* ids_out,
+                           double* scores_out, int64_t* n_out);
 /* Two-tier store occupancy in pages: HBM pool and the pinned host spill tier (host_spill_tokens). New chunks go
  * to HBM while it has room, then to the host tier; tier of a chunk: 0 = HBM, 1 = pinned host, 2 = a peer GPU. */
 tkv_status tkv_store_tiers(const tkv_engine* eng, int64_t* hbm_used, int64_t* hbm_total, int64_t* host_used,

@@ -70,6 +70,37 @@ struct Fnv {
     }
 };
 
+// embed (retrieval.cpp:64-88): feature-hashed token bigrams (leading -1 sentinel), FNV-1a over the two u32s,
+// bucket h % dim, sign from the top bit, L2-normalised; all-cancelled counts pin e_0 = 1.
+static void embed_tokens(const int32_t* t, int64_t n, int64_t dim, double* out) {
+    if (n < 1) fail(TKV_ERR_DOMAIN, "embed: empty token list");
+    if (dim < 1) fail(TKV_ERR_DOMAIN, "embed: dimension must be >= 1");
+    std::fill(out, out + dim, 0.0);
+    int32_t prev = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        Fnv f;
+        f.u32((uint32_t)prev);
+        f.u32((uint32_t)t[i]);
+        out[f.h % (uint64_t)dim] += (f.h >> 63) ? -1.0 : 1.0;
+        prev = t[i];
+    }
+    double ss = 0.0;
+    for (int64_t i = 0; i < dim; ++i) ss += out[i] * out[i];
+    if (ss == 0.0) {
+        out[0] = 1.0;
+        ss = 1.0;
+    }
+    const double inv = 1.0 / std::sqrt(ss);
+    for (int64_t i = 0; i < dim; ++i) out[i] *= inv;
+}
+
+// sum of squares in the reference cosine's order (retrieval.cpp:93-97)
+static double sumsq(const double* v, int64_t dim) {
+    double ss = 0.0;
+    for (int64_t i = 0; i < dim; ++i) ss += v[i] * v[i];
+    return ss;
+}
+
 static void validate_cfg(const tkv_model_config& c) {  // ModelConfig::validate (config.cpp:9-29)
     if (c.layer_num < 1 || c.head_num < 1 || c.kv_head_num < 1 || c.head_size < 1 || c.hidden_size < 1 ||
         c.intermediate_size < 1 || c.vocab_size < 1)
@@ -277,6 +308,13 @@ struct tkv_engine {
     int64_t n_host_pages = 0;
     std::vector<int32_t> host_free;
     uint64_t store_epoch = 0;  // bumped by every eviction (contexts that re-read store pages check it)
+    // retrieval index (RetrievalIndex, retrieval.hpp:33-60): embeddings in HBM, transposed [kIndexDim][cap]
+    std::unordered_map<uint64_t, int64_t> idx_row;
+    std::vector<uint64_t> idx_ids;
+    std::vector<double> idx_nb;
+    int64_t idx_cap = 0;
+    DevMem d_idx_emb, d_idx_nb, d_idx_ids, d_idx_q, d_idx_scratch;
+    void index_add(uint64_t id, const int32_t* payload, int64_t n, bool* added);
     std::unordered_map<uint64_t, Chunk> chunks;
     PoolTable pools;                     // slot 0 = pool.p; peers attached via IPC or same-process P2P
     std::vector<void*> ipc_opened;       // peer pools opened with cudaIpcOpenMemHandle (closed on destroy)
@@ -987,9 +1025,97 @@ uint8_t* page_ptr(tkv_engine* e, int slot, int32_t page) {
 
 }  // namespace
 
+void tkv_engine::index_add(uint64_t id, const int32_t* payload, int64_t n, bool* added) {
+    if (idx_row.count(id)) {  // content dedup (RetrievalIndex::add returns false)
+        if (added) *added = false;
+        return;
+    }
+    std::vector<double> e(kIndexDim);
+    embed_tokens(payload, n, kIndexDim, e.data());
+    const int64_t r = (int64_t)idx_ids.size();
+    if (r >= idx_cap) {  // grow: copy the transposed matrix into a wider one
+        const int64_t ncap = std::max<int64_t>(1024, 2 * idx_cap);
+        DevMem ne, nn, ni;
+        ne.ensure((size_t)kIndexDim * ncap * 8);
+        nn.ensure((size_t)ncap * 8);
+        ni.ensure((size_t)ncap * 8);
+        if (r > 0) {
+            TKV_CUDA(cudaMemcpy2DAsync(ne.p, (size_t)ncap * 8, d_idx_emb.p, (size_t)idx_cap * 8, (size_t)r * 8, kIndexDim,
+                                       cudaMemcpyDeviceToDevice, stream));
+            TKV_CUDA(cudaMemcpyAsync(nn.p, d_idx_nb.p, (size_t)r * 8, cudaMemcpyDeviceToDevice, stream));
+            TKV_CUDA(cudaMemcpyAsync(ni.p, d_idx_ids.p, (size_t)r * 8, cudaMemcpyDeviceToDevice, stream));
+        }
+        sync();
+        std::swap(d_idx_emb.p, ne.p);
+        std::swap(d_idx_emb.n, ne.n);
+        std::swap(d_idx_nb.p, nn.p);
+        std::swap(d_idx_nb.n, nn.n);
+        std::swap(d_idx_ids.p, ni.p);
+        std::swap(d_idx_ids.n, ni.n);
+        idx_cap = ncap;
+    }
+    const double nb = sumsq(e.data(), kIndexDim);
+    TKV_CUDA(cudaMemcpy2DAsync(static_cast<double*>(d_idx_emb.p) + r, (size_t)idx_cap * 8, e.data(), 8, 8, kIndexDim,
+                               cudaMemcpyHostToDevice, stream));
+    TKV_CUDA(cudaMemcpyAsync(static_cast<double*>(d_idx_nb.p) + r, &nb, 8, cudaMemcpyHostToDevice, stream));
+    TKV_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(d_idx_ids.p) + r, &id, 8, cudaMemcpyHostToDevice, stream));
+    sync();
+    idx_row[id] = r;
+    idx_ids.push_back(id);
+    idx_nb.push_back(nb);
+    if (added) *added = true;
+}
+
 extern "C" {
 
 int tkv_abi_version(void) { return TKV_ABI_VERSION; }
+
+tkv_status tkv_embed(const int32_t* tokens, int64_t n, int64_t dim, double* out) {
+    return guard([&] {
+        if (n > 0) need(tokens, "tokens");
+        need(out, "out");
+        embed_tokens(tokens, n, dim, out);
+    });
+}
+
+tkv_status tkv_index_add(tkv_engine* e, uint64_t chunk_id, const int32_t* payload, int64_t n, int* added) {
+    return guard([&] {
+        need(e, "engine");
+        if (n > 0) need(payload, "payload");
+        e->bind();
+        bool a = false;
+        e->index_add(chunk_id, payload, n, &a);
+        if (added) *added = a ? 1 : 0;
+    });
+}
+
+int64_t tkv_index_size(const tkv_engine* e) { return e ? (int64_t)e->idx_ids.size() : -1; }
+
+tkv_status tkv_index_top_k(tkv_engine* e, const int32_t* query, int64_t n, int64_t k, uint64_t* ids_out,
+                           double* scores_out, int64_t* n_out) {
+    return guard([&] {
+        need(e, "engine");
+        need(ids_out, "ids_out");
+        if (k < 1) fail(TKV_ERR_DOMAIN, "top_k: k must be >= 1");      // retrieval.cpp:119
+        if (e->idx_ids.empty()) fail(TKV_ERR_DOMAIN, "top_k: empty index");  // retrieval.cpp:120
+        if (n > 0) need(query, "query");
+        std::vector<double> q(kIndexDim);
+        embed_tokens(query, n, kIndexDim, q.data());
+        const double na = sumsq(q.data(), kIndexDim);
+        e->bind();
+        const int64_t rows = (int64_t)e->idx_ids.size();
+        const int kk = (int)std::min<int64_t>(k, std::min<int64_t>(rows, kIndexMaxK));
+        if (k > kIndexMaxK && rows > kIndexMaxK) fail(TKV_ERR_CONFIG, "top_k: k > 256 over a larger index is not supported");
+        e->d_idx_q.ensure((size_t)kIndexDim * 8);
+        TKV_CUDA(cudaMemcpyAsync(e->d_idx_q.p, q.data(), (size_t)kIndexDim * 8, cudaMemcpyHostToDevice, e->stream));
+        e->d_idx_scratch.ensure(index_topk_scratch_bytes(rows, kk));
+        const int64_t got = launch_index_top_k(e->d_idx_emb.as<double>(), e->d_idx_nb.as<double>(),
+                                               static_cast<const uint64_t*>(e->d_idx_ids.p), rows, e->idx_cap,
+                                               e->d_idx_q.as<double>(), na, kk, e->d_idx_scratch.p, ids_out, scores_out,
+                                               e->stream);
+        if (n_out) *n_out = got;
+    });
+}
 const char* tkv_last_error(void) { return g_last_error.c_str(); }
 
 const char* tkv_status_name(tkv_status s) {
@@ -1322,6 +1448,9 @@ tkv_status tkv_ingest_chunks(tkv_engine* e, const int32_t* payloads, const int64
                     stats->new_chunks += 1;
                     stats->bytes_written += (uint64_t)ch.len * e->L * 2 * e->kvd * dt_size(e->dt);
                 }
+                // the retrieval index entry over the unframed payload (Engine::ingest_chunk_payload adds the
+                // ChunkRecord, pipeline.cpp:97-134; ChunkRecord.embedding, retrieval.hpp:25-30)
+                if (ch.framed.size() > 2) e->index_add(todo[k].id, ch.framed.data() + 1, (int64_t)ch.framed.size() - 2, nullptr);
                 e->chunks.emplace(todo[k].id, std::move(ch));
             }
             i0 = i1;

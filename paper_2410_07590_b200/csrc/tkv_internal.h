@@ -172,6 +172,13 @@ int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms);
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
                          int* err, cudaStream_t s, int kv_ready, const L2Prefetch& pf = L2Prefetch());
+// Retrieval index (retrieval.cu): emb is [kIndexDim][cap] f64 (transposed), nb[r] = sum of squares of row r
+// (host, reference order); returns min(k, n) ids / cosines in RetrievalIndex::top_k order (retrieval.cpp:117-133).
+constexpr int kIndexDim = 256, kIndexMaxK = 256;  // kEmbedDim (retrieval.hpp:11)
+size_t index_topk_scratch_bytes(int64_t n, int k);
+int64_t launch_index_top_k(const double* emb, const double* nb, const uint64_t* ids, int64_t n, int64_t cap,
+                           const double* q, double na, int k, void* scratch, uint64_t* ids_out, double* scores_out,
+                           cudaStream_t s);
 // merge split-K (O, m, l) partials into out (dtype)
 void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, void* out, int* err, DT dt,
                               cudaStream_t s);

@@ -127,6 +127,11 @@ def lib():
         L.tkv_store_chunk_tokens.argtypes = [C.c_void_p, C.c_uint64, I64P]
         L.tkv_store_count.argtypes = [C.c_void_p, I64P, I64P, I64P]
         L.tkv_store_evict.argtypes = [C.c_void_p, C.c_uint64]
+        L.tkv_embed.argtypes = [I32P, C.c_int64, C.c_int64, C.POINTER(C.c_double)]
+        L.tkv_index_add.argtypes = [C.c_void_p, C.c_uint64, I32P, C.c_int64, C.POINTER(C.c_int)]
+        L.tkv_index_size.restype = C.c_int64
+        L.tkv_index_size.argtypes = [C.c_void_p]
+        L.tkv_index_top_k.argtypes = [C.c_void_p, I32P, C.c_int64, C.c_int64, U64P, C.POINTER(C.c_double), I64P]
         L.tkv_store_tiers.argtypes = [C.c_void_p, I64P, I64P, I64P, I64P]
         L.tkv_store_chunk_tier.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32)]
         L.tkv_prefill_query_batch.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int64, I32P, I64P, F32P,
@@ -427,6 +432,27 @@ class Engine:
     def export_tkvc(self, chunk_id: int, path: str) -> None:
         _check(lib().tkv_export_tkvc(self._h, chunk_id, path.encode()))
 
+    # ---- retrieval (retrieval.hpp) ----
+    def index_add(self, chunk_id: int, payload) -> bool:
+        p = _i32(payload)
+        a = C.c_int()
+        _check(lib().tkv_index_add(self._h, chunk_id, _p(p, I32P) if len(p) else None, len(p), C.byref(a)))
+        return bool(a.value)
+
+    def index_size(self) -> int:
+        return lib().tkv_index_size(self._h)
+
+    def top_k(self, query_tokens, k: int):
+        """RetrievalIndex::top_k over embed(query): (chunk ids, cosines), best first."""
+        q = _i32(query_tokens)
+        n = max(1, min(int(k), max(1, self.index_size()), 256))
+        ids = np.zeros(n, np.uint64)
+        sc = np.zeros(n, np.float64)
+        got = C.c_int64()
+        _check(lib().tkv_index_top_k(self._h, _p(q, I32P) if len(q) else None, len(q), k, _p(ids, U64P),
+                                     sc.ctypes.data_as(C.POINTER(C.c_double)), C.byref(got)))
+        return ids[:got.value], sc[:got.value]
+
     def store_tiers(self) -> dict:
         v = [C.c_int64() for _ in range(4)]
         _check(lib().tkv_store_tiers(self._h, *[C.byref(x) for x in v]))
@@ -593,6 +619,14 @@ def debug_gemm(A: np.ndarray, W: np.ndarray, dtype: str = "bf16", use_tc: bool =
     dt = Dtype.F32 if dtype == "f32" else Dtype.BF16
     _check(lib().tkv_debug_gemm(device, int(dt), int(use_tc), _p(A, F32P), _p(W, F32P), M, N, K, splits,
                                 _p(out, F32P)))
+    return out
+
+
+def embed(tokens, dim: int = 256) -> np.ndarray:
+    """embed (retrieval.cpp:64-88)."""
+    t = _i32(tokens)
+    out = np.zeros(dim, np.float64)
+    _check(lib().tkv_embed(_p(t, I32P) if len(t) else None, len(t), dim, out.ctypes.data_as(C.POINTER(C.c_double))))
     return out
 
 

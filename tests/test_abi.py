@@ -76,3 +76,16 @@ def test_cpp_shim_compiles_and_links(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "checksum 783fe06586f74dc9 fingerprint 8dd32810bd252fd1" in r.stdout
+
+
+def test_embed_matches_reference():
+    """tkv_embed (host side of the retrieval path) against the restatement and the reference itself."""
+    import oracle as O
+
+    for seed, n in ((1, 1), (2, 2), (3, 57), (4, 400)):
+        t = O.random_text_tokens(seed, n)
+        e = T.embed(t)
+        assert np.array_equal(e, O.Port.embed(t))
+        assert np.array_equal(e, O.Ref.embed(t))
+    with pytest.raises(T.DomainError):
+        T.embed([])

@@ -473,3 +473,40 @@ def test_batched_attention_single_launch_vs_golden(golden, name):
         assert_close(logits[2], eng.prefill_query(single, q3)[0], BF16_TOL)
     for c in ctxs:
         c.close()
+
+
+def test_index_top_k_matches_reference():
+    """GPU cosine top-k (retrieval.cu) over a 3000-chunk index: ids AND cosines bit-identical to the reference's
+    RetrievalIndex::top_k, incl. exact ties (same payload under two ids -> ascending id) and k > size."""
+    cfg = T.ModelConfig.toy()
+    eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=4096)
+    rng = np.random.default_rng(11)
+    payloads = [O.random_text_tokens(20000 + i, int(rng.integers(1, 200))) for i in range(3000)]
+    ids = [int(x) for x in np.unique(rng.integers(1, 1 << 40, 3100, dtype=np.int64))[:3000]]
+    rng.shuffle(ids)
+    for i, p in zip(ids, payloads):
+        assert eng.index_add(i, p)
+    twin = ids[17] + 1 if ids[17] + 1 not in ids else ids[17] - 1
+    assert eng.index_add(twin, payloads[17])       # exact cosine tie with ids[17]
+    assert not eng.index_add(ids[5], payloads[5])  # content dedup by id
+    ingested = eng.ingest_chunks([O.random_text_tokens(99, 126)])  # auto-indexed by ingest
+    assert eng.index_size() == 3002
+    all_ids = np.array(ids + [twin, ingested[0]], np.uint64)
+    emb = np.stack([O.Port.embed(p) for p in payloads + [payloads[17], O.random_text_tokens(99, 126)]])
+    for qs, k in ((1, 1), (2, 16), (3, 100), (4, 256)):
+        q = O.random_text_tokens(40000 + qs, 60) if qs != 4 else payloads[17]
+        got, scores = eng.top_k(q, k)
+        ref_ids, ref_scores = O.Port.top_k(emb, all_ids, O.Port.embed(q), k)
+        assert np.array_equal(got, ref_ids)
+        assert np.array_equal(scores, ref_scores)
+        if qs == 1:
+            assert np.array_equal(got, O.Ref.top_k(emb, all_ids, O.Port.embed(q), k))
+    small = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=1024)
+    small.index_add(5, payloads[0])
+    small.index_add(3, payloads[1])
+    got, _ = small.top_k(payloads[1], 10)  # k beyond the index size returns everything
+    assert list(got) == [3, 5]
+    with pytest.raises(T.DomainError):
+        small.top_k(payloads[1], 0)
+    small.close()
+    eng.close()
