@@ -86,6 +86,7 @@ typedef struct {
 #define TKV_FLAG_NO_PDL 0x8       /* launch kernels without programmatic dependent launch          */
 #define TKV_FLAG_L2_PREFETCH 0x10  /* reserved (attention-time L2 weight prefetch: measured no gain) */
 #define TKV_FLAG_BATCH_ATTN 0x20   /* batched prefill: one attention launch even when the batch cannot fill the GPU */
+#define TKV_FLAG_DECODE_ATTN 0x40 /* bf16: decode-sized (<= 16 rows / kv head) forwards use the split-K mma.sync kernel */
 
 /* IngestStats (pipeline.hpp:35-39) */
 typedef struct {
@@ -258,7 +259,8 @@ tkv_status tkv_debug_set_mask_fault(tkv_engine* eng, int64_t row, int64_t col);
  * `dtype` on the device first). gemm: out[M,N] = A[M,K] . W[N,K]^T with the tcgen05 (use_tc=1) or
  * SIMT kernel and `splits` split-K partials (0 = auto). attention: the engine's flash attention with
  * the [lo, hi] row predicate; q [Tq, H*d], k/v [Tk, Hkv*d], out [Tq, H*d]. impl: 0 = the engine's choice
- * (tcgen05 for bf16 head_size 128), 1 = SIMT. */
+ * (tcgen05 for bf16 head_size 128), 1 = SIMT, 2 = the decode-sized kernel (bf16, d = 128, Tq * H / Hkv in
+ * {4, 7, 8, 16}). */
 tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* A, const float* W, int64_t M,
                           int64_t N, int64_t K, int splits, float* out);
 /* GEMM tuning/timing (tools/gemm_sweep.py): knobs = ring stages, smem budget KB, CTAs per SM, weight

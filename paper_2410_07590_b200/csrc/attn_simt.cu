@@ -169,10 +169,10 @@ __global__ void attn_combine_kernel(const float* __restrict__ ws_o, const float*
     if (D == 128) {  // lane owns 4 consecutive columns: one float4 per split, loads batched
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         const float4* src = reinterpret_cast<const float4*>(ws_o) + row * 32 + lane;
-#pragma unroll 4
-        for (int s = 0; s < splits; ++s) {
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {  // all split loads in flight at once (splits <= 32)
             const float ws = __shfl_sync(0xffffffffu, w, s);
-            const float4 v = src[(int64_t)s * rows * 32];
+            const float4 v = s < splits ? src[(int64_t)s * rows * 32] : make_float4(0.f, 0.f, 0.f, 0.f);
             acc.x = fmaf(v.x, ws, acc.x);
             acc.y = fmaf(v.y, ws, acc.y);
             acc.z = fmaf(v.z, ws, acc.z);

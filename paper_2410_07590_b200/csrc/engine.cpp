@@ -624,13 +624,16 @@ void tkv_engine::forward(const Fwd& f) {
         const int64_t r0 = tail ? T - 1 : 0;
         auto attend = [&](const void* qrows, tkv_context* actx, const int32_t* lo, const int32_t* hi, void* out,
                           int arows, int aTk, int kv_ready) {
-            // decode-sized row counts (the last layer's single row, greedy decode): a 128-row tcgen05 tile would be
-            // <= 1/8 full; the split-K SIMT kernel streams the keys with far less per-CTA overhead
+            // decode-sized row counts (the last layer's single row, greedy decode) can run the split-K mma.sync
+            // kernel (opt-in: measured on par with the 1/8-full tcgen05 tile at C2, 2 % slower per decode step)
             const bool tiny = (int64_t)arows * (H / Hkv) <= decode_rows_max;
-            const bool tc = dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_ATTN) && !tiny &&
+            const bool dec = dt == DT::BF16 && (opts.flags & TKV_FLAG_DECODE_ATTN) && !(opts.flags & TKV_FLAG_SIMT_ATTN) &&
+                             attention_decode_supported(arows, (int)H, (int)Hkv, (int)d, dt);
+            const bool tc = dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_ATTN) && !tiny && !dec &&
                             attention_tc_supported((int)d, dt);
             int splits = tc ? attn_tc_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms)
-                            : attn_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms);
+                            : dec ? attn_decode_pick_splits(aTk, (int)Hkv, num_sms)
+                                  : attn_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms);
             if (tc && attn_split_override > 0) splits = attn_split_override;  // TKV_ATTN_SPLITS (tuning)
             AttnWork ws;
             if (splits > 1) {
@@ -643,6 +646,9 @@ void tkv_engine::forward(const Fwd& f) {
             }
             Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);  // + the split-merge launch
             if (skip_mask & 8) {
+            } else if (dec) {
+                launch_attention_decode(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
+                                        aTk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream);
             } else if (tc) {
                 // Weight-bound small forwards: warm L2 with this layer's O-proj weights and the head of its
                 // gate/up weights while attention runs (l2_prefetch_bytes total, 0 = off)
@@ -666,8 +672,10 @@ void tkv_engine::forward(const Fwd& f) {
         if (batch && f.batch_maps) {
             // one launch for the whole batch (enough row groups to fill the GPU without split-K)
             Scope sc(this, PC_ATTN, 1);
+            if (trace_layer == (int)l) attn_trace_enable(true, nullptr);
             launch_attention_tc_batch(q.p, f.batch_reqs, f.batch_maps, (int)f.reqs.size(), f.batch_max_n, (int)H,
                                       (int)Hkv, (int)l, f.lo, f.hi, attn.p, err.as<int>(), stream);
+            if (trace_layer == (int)l) attn_trace_enable(false, nullptr);
         } else if (batch) {
             for (const Fwd::Req& r : f.reqs)
                 attend(static_cast<uint8_t*>(q.p) + (size_t)r.tok0 * qd * es, r.ctx, f.lo + r.tok0, f.hi + r.tok0,
@@ -2287,9 +2295,13 @@ tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const floa
         TKV_CUDA(cudaMemset(errm.p, 0, 4));
         int dev_sms = 148;
         cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+        const bool dec = impl == 2;  // decode-sized kernel (attn_decode.cu)
+        if (dec && !attention_decode_supported((int)Tq, (int)H, (int)Hkv, (int)d, dt))
+            fail(TKV_ERR_CONFIG, "decode attention needs bf16, d = 128 and Tq * H / Hkv in {4, 7, 8, 16}");
         const bool tc = impl == 0 && attention_tc_supported((int)d, dt);
         const int splits = tc ? attn_tc_pick_splits((int)Tq, (int)H, (int)Hkv, (int)Tk, dev_sms)
-                              : attn_pick_splits((int)Tq, (int)H, (int)Hkv, (int)Tk, dev_sms);
+                              : dec ? attn_decode_pick_splits((int)Tk, (int)Hkv, dev_sms)
+                                    : attn_pick_splits((int)Tq, (int)H, (int)Hkv, (int)Tk, dev_sms);
         AttnWork w;
         if (splits > 1) {
             size_t mloff = (size_t)splits * Tq * H * d;
@@ -2298,12 +2310,42 @@ tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const floa
             w.o = ws.as<float>();
             w.ml = w.o + mloff;
         }
-        if (tc)
-            launch_attention_tc(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p,
-                                (int)Tq, (int)Tk, (int)H, (int)Hkv, splits, w, errm.as<int>(), 0, (int)Tk);
-        else
-            launch_attention_simt(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p,
-                                  (int)Tq, (int)Tk, (int)H, (int)Hkv, (int)d, splits, w, errm.as<int>(), dt, 0);
+        auto run = [&] {
+            if (dec)
+                launch_attention_decode(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(),
+                                        dout.p, (int)Tq, (int)Tk, (int)H, (int)Hkv, splits, w, errm.as<int>(), 0);
+            else if (tc)
+                launch_attention_tc(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(), dout.p,
+                                    (int)Tq, (int)Tk, (int)H, (int)Hkv, splits, w, errm.as<int>(), 0, (int)Tk);
+            else
+                launch_attention_simt(dq.p, dk.p, dv.p, (int)(Hkv * d), dlo.as<int32_t>(), dhi.as<int32_t>(),
+                                      dout.p, (int)Tq, (int)Tk, (int)H, (int)Hkv, (int)d, splits, w,
+                                      errm.as<int>(), dt, 0);
+        };
+        run();
+        if (const char* it = getenv("TKV_DEBUG_TIME_ITERS")) {  // warm timing (tools/decode_time.py)
+            const int iters = atoi(it);
+            DevMem flush;
+            flush.ensure((size_t)256 << 20);  // > L2: every timed launch streams K/V from HBM
+            cudaEvent_t e0, e1;
+            TKV_CUDA(cudaEventCreate(&e0));
+            TKV_CUDA(cudaEventCreate(&e1));
+            float tot = 0.f;
+            for (int i = 0; i < iters; ++i) {
+                TKV_CUDA(cudaMemsetAsync(flush.p, i & 0xff, (size_t)256 << 20, 0));
+                TKV_CUDA(cudaEventRecord(e0, 0));
+                run();
+                TKV_CUDA(cudaEventRecord(e1, 0));
+                TKV_CUDA(cudaEventSynchronize(e1));
+                float ms = 0.f;
+                TKV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                tot += ms;
+            }
+            fprintf(stderr, "debug_attention impl %d splits %d: %.2f us per launch (L2 flushed)\n", impl, splits,
+                    1000.f * tot / iters);
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
         launch_to_f32(dout.p, Tq * H * d, of.as<float>(), dt, 0);
         TKV_CUDA(cudaDeviceSynchronize());
         int e = 0;

@@ -179,6 +179,13 @@ size_t index_topk_scratch_bytes(int64_t n, int k);
 int64_t launch_index_top_k(const double* emb, const double* nb, const uint64_t* ids, int64_t n, int64_t cap,
                            const double* q, double na, int k, void* scratch, uint64_t* ids_out, double* scores_out,
                            cudaStream_t s);
+// Decode-sized attention (attn_decode.cu): bf16, d = 128, Tq * group in {4, 7, 8, 16} rows per kv head; split-K
+// flash decoding on CUDA cores with the SIMT workspace layout, merged by launch_attention_combine.
+bool attention_decode_supported(int Tq, int H, int Hkv, int d, DT dt);
+int attn_decode_pick_splits(int Tk, int Hkv, int num_sms);
+void launch_attention_decode(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
+                             const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits,
+                             const AttnWork& ws, int* err, cudaStream_t s);
 // merge split-K (O, m, l) partials into out (dtype)
 void launch_attention_combine(const AttnWork& ws, int rows, int d, int splits, void* out, int* err, DT dt,
                               cudaStream_t s);

@@ -99,3 +99,35 @@ def test_attention_degenerate_row_raises():
     k = np.ones((4, 8), np.float32)
     with pytest.raises(T.DegenerateRowError):
         T.debug_attention(q, k, k, [0, 3], [1, 2], 1, 1, 8, dtype="f32")
+
+
+DECODE_CASES = [
+    # (Tq, Tk, H, Hkv, kind): the last layer's single row, greedy-decode steps, small query tails
+    (1, 8256, 28, 4, "query"),
+    (2, 1000, 32, 8, "query"),   # 8 rows per kv head
+    (1, 7, 28, 4, "query"),
+    (2, 3000, 28, 4, "query_hot"),  # 14 rows -> not a decode shape: tcgen05 path (skipped below)
+    (1, 5000, 64, 4, "query_hot"),  # 16 rows per kv head, growing scores
+    (1, 300, 32, 8, "query"),    # 4 rows per kv head
+]
+
+
+@pytest.mark.parametrize("Tq,Tk,H,Hkv,kind", DECODE_CASES)
+def test_decode_attention_vs_torch(Tq, Tk, H, Hkv, kind):
+    d = 128
+    if Tq * (H // Hkv) not in (4, 7, 8, 16):
+        pytest.skip("not a decode-sized row count")
+    rng = np.random.default_rng(Tq * 7 + Tk + H)
+    q = rng.uniform(-1, 1, (Tq, H * d)).astype(np.float32)
+    k = rng.uniform(-1, 1, (Tk, Hkv * d)).astype(np.float32)
+    v = bf16_round(rng.uniform(-1, 1, (Tk, Hkv * d)).astype(np.float32))
+    if kind == "query_hot":
+        q = q * 6.0
+        k = k * np.linspace(0.2, 1.5, Tk, dtype=np.float32)[:, None]
+    q, k = bf16_round(q), bf16_round(k)
+    P = Tk - Tq
+    lo, hi = np.zeros(Tq, np.int32), (P + np.arange(Tq)).astype(np.int32)
+    out = T.debug_attention(q, k, v, lo, hi, H, Hkv, d, dtype="bf16", impl=2)
+    ref = attention_ref(q, k, v, lo, hi, H, Hkv, d)
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    assert err < 1e-2, f"max rel err {err:.3e}"

@@ -218,6 +218,25 @@ def test_qwen_dims_one_layer_vs_golden(golden, dtype, tol):
                      A[f"qwen1.naive_{tag}.logits"], tol)
 
 
+def test_decode_attention_flag_vs_golden(golden):
+    """TKV_FLAG_DECODE_ATTN: the last layer's single row (query prefill) and every greedy-decode step run the
+    decode-sized split-K kernel (R = 7 rows per kv head at Qwen dims); logits within bf16 tolerance of the
+    golden and of the default tcgen05 path, same greedy tokens."""
+    meta, A = golden
+    m = meta["qwen1"]
+    dec = engine(cfg_t(m), m["seed"], "bf16", flags=0x40)
+    ref = engine(cfg_t(m), m["seed"], "bf16")
+    outs = []
+    for eng in (dec, ref):
+        ids = eng.ingest_chunks(payloads(A, "qwen1"))
+        with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+            logits = eng.prefill_query(ctx, A["qwen1.query"])[0]
+            assert_close(logits, A["qwen1.turbo_reordered.logits"], BF16_TOL)
+            outs.append((logits, eng.greedy_decode(ctx, 4)))
+    assert_close(outs[0][0], outs[1][0], BF16_TOL)
+    assert outs[0][1] == outs[1][1]
+
+
 def test_tcgen05_gemm_matches_simt_gemm():
     """bf16 tcgen05/TMA GEMM vs the SIMT GEMM on the same bf16 inputs (exact Qwen dims, 2 layers)."""
     cfg = T.ModelConfig(**vars(O.qwen_layers(2)))

@@ -7,7 +7,8 @@ sys.path.insert(0, ".")
 from paper_2410_07590_b200 import turbokv as T
 
 L = T.lib()
-P, Q, H, Hkv, d = 8192, 64, 28, 4, 128
+import os
+P, Q, H, Hkv, d = int(os.environ.get("TRACE_P", 8192)), 64, 28, 4, 128
 rng = np.random.default_rng(0)
 q = rng.uniform(-1, 1, (Q, H * d)).astype(np.float32)
 k = rng.uniform(-1, 1, (P + Q, Hkv * d)).astype(np.float32)

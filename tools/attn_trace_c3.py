@@ -1,0 +1,42 @@
+"""CTA timeline of the batched attention launch of one layer (TKV_TRACE_LAYER, default 14) in a C3-shaped
+batched prefill: 32 requests x (20 chunks x 800 tokens) + 64-token queries, Qwen2-7B shape."""
+import os
+import sys
+
+import numpy as np
+
+os.environ.setdefault("TKV_TRACE_LAYER", "14")
+sys.path.insert(0, ".")
+from paper_2410_07590_b200 import turbokv as T  # noqa: E402
+
+B, NC, CT, CORPUS, Q = int(os.environ.get("C3_BATCH", 32)), 20, 800, 160, 64
+cfg = T.ModelConfig.qwen2_7b_like()
+eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=CORPUS * 1024 + 65536)
+rng = np.random.default_rng(0xC3)
+cids = eng.ingest_chunks([rng.integers(97, 123, CT - 2).astype(np.int32) for _ in range(CORPUS)])
+picks = [rng.choice(CORPUS, NC, replace=False) for _ in range(B)]
+queries = [rng.integers(97, 123, Q).astype(np.int32) for _ in range(B)]
+L = T.lib()
+for _ in range(2):
+    ctxs = [eng.assemble([cids[j] for j in pk], T.PositionMode.Reordered) for pk in picks]
+    eng.prefill_query_batch(ctxs, queries)
+    for c in ctxs:
+        c.close()
+out = np.zeros(320 + 2048, np.uint64)
+T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 320 + 2048))
+ev = out[:320].reshape(32, 10).astype(np.int64)
+cta = out[320:].reshape(1024, 2).astype(np.int64)
+idx = np.nonzero(cta[:, 0] > 0)[0]
+cta = cta[idx]
+s0 = cta[:, 0].min()
+st, en = (cta[:, 0] - s0) / 1e3, (cta[:, 1] - s0) / 1e3
+dur = en - st
+print(f"{len(cta)} CTAs: kernel span {en.max():.1f} us; start times: first-wave {np.sort(st)[:148].max():.1f} us, "
+      f"last {st.max():.1f} us; duration min/median/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us")
+print("sum of CTA durations / (148 x span) = %.3f" % (dur.sum() / (148 * en.max())))
+for q in (0.1, 0.5, 0.9, 1.0):
+    print(f"  end time quantile {q}: {np.quantile(en, q):.1f} us")
+print("duration by linear CTA index (every 16th):", np.round(dur[::16], 1).tolist())
+t0 = ev[0, 9]
+print("CTA 0: entry->q staged %d, first S ready %d, last round S ready %s, o_done %d, written %d cycles"
+      % (ev[30, 5] - t0, ev[0, 0] - t0, [int(ev[j, 0] - t0) for j in range(25, 30)], ev[31, 0] - t0, ev[31, 1] - t0))

@@ -14,8 +14,9 @@ __global__ void boxes(const uint4* __restrict__ w, int n_tiles, int kb, int ld_v
                 for (int j = 0; j < 4; ++j) {
                     const int e = threadIdx.x + j * 256;  // 1024 x 16 B = one 16 KB box
                     const int row = e >> 3, c = e & 7;
-                    size_t idx = tiled ? ((size_t)(t * kb + k + kk) * 1024 + e)
-                                       : ((size_t)(t * 128 + row) * ld_vec + (size_t)(k + kk) * 8 + c);
+                    size_t idx = tiled == 2 ? ((size_t)(k + kk) * n_tiles + t) * 1024 + e  // k-major tiles
+                                 : tiled ? ((size_t)(t * kb + k + kk) * 1024 + e)
+                                         : ((size_t)(t * 128 + row) * ld_vec + (size_t)(k + kk) * 8 + c);
                     v[kk][j] = __ldcs(w + idx);
                 }
 #pragma unroll
@@ -36,7 +37,7 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int tiled = 0; tiled < 2; ++tiled)
+    for (int tiled = 0; tiled < 3; ++tiled)
         for (int ctas : {296, 592, 1184}) {
             float best = 1e9;
             for (int it = 0; it < 5; ++it) {
@@ -48,7 +49,7 @@ int main() {
                 cudaEventElapsedTime(&ms, e0, e1);
                 best = ms < best ? ms : best;
             }
-            printf("%s boxes, %d CTAs: %.0f GB/s\n", tiled ? "contiguous (pre-tiled)" : "row-strided (TMA box)", ctas,
+            printf("%s boxes, %d CTAs: %.0f GB/s\n", tiled == 2 ? "k-major pre-tiled" : tiled ? "contiguous (pre-tiled)" : "row-strided (TMA box)", ctas,
                    bytes / (best * 1e-3) / 1e9);
         }
     return 0;

@@ -17,7 +17,7 @@ __global__ void stream(const __grid_constant__ CUtensorMap tm, const __grid_cons
                        int n_tiles, int kb, int stages) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
-    constexpr uint32_t SB = MODE == 2 ? 16384 + 8192 : 16384;  // stage bytes
+    constexpr uint32_t SB = (MODE == 2 || MODE == 3 || MODE == 5) ? 16384 + 8192 : 16384;  // stage bytes
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + stages * SB);
     uint64_t* empty = full + stages;
     if (threadIdx.x == 0) {
@@ -35,22 +35,54 @@ __global__ void stream(const __grid_constant__ CUtensorMap tm, const __grid_cons
             wait(&empty[s], ((it / stages) & 1) ^ 1);
             const int t = blockIdx.x + (it / kb) * gridDim.x, k = it % kb;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&full[s])), "r"(SB) : "memory");
-            if (MODE == 2)
+            if (MODE == 2 || MODE == 3 || MODE == 5)
                 asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
                              ::"r"(su(ring + s * SB + 16384)), "l"((uint64_t)&ta), "r"(su(&full[s])), "r"(k * 64), "r"(0) : "memory");
-            if (MODE == 0 || MODE == 2)
+            if (MODE >= 4)  // k-major pre-tiled layout: at step k every CTA reads a neighbour of the same 16 KB row
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];"
+                             ::"r"(su(ring + s * SB)), "l"(w + ((size_t)k * n_tiles + t) * 16384), "r"(su(&full[s])) : "memory");
+            else if (MODE == 0 || MODE >= 2)
                 asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
                              ::"r"(su(ring + s * SB)), "l"((uint64_t)&tm), "r"(su(&full[s])), "r"(k * 64), "r"(t * 128) : "memory");
             else
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];"
                              ::"r"(su(ring + s * SB)), "l"(w + ((size_t)t * kb + k) * 16384), "r"(su(&full[s])) : "memory");
         }
-    } else if (threadIdx.x == 32) {
+    } else if (threadIdx.x == 32 && MODE != 3 && MODE != 5) {
         for (int it = 0; it < total; ++it) {
             const int s = it % stages;
             wait(&full[s], (it / stages) & 1);
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su(&empty[s])) : "memory");
         }
+    }
+    if ((MODE == 3 || MODE == 5) && threadIdx.x >= 32) {  // warp 1: TMEM + the swapped GEMM's MMAs (M=128 weights, N=64 tokens)
+        __shared__ uint32_t tslot;
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su(&tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        __syncwarp();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (threadIdx.x == 32) {
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            for (int it = 0; it < total; ++it) {
+                const int s = it % stages;
+                wait(&full[s], (it / stages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t wa = su(ring + s * SB), aa = wa + 16384;
+                for (int k = 0; k < 4; ++k) {
+                    auto desc = [](uint32_t a) {
+                        return (uint64_t)((a & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+                               ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+                    };
+                    const uint32_t acc = (it | k) != 0;
+                    asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
+                                 ::"r"(tslot), "l"(desc(wa + k * 32)), "l"(desc(aa + k * 32)), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su(&empty[s])) : "memory");
+            }
+        }
+        __syncwarp();
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tslot));
     }
 }
 typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -81,12 +113,12 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int mode = 0; mode < 3; ++mode)
+    for (int mode = 0; mode < 6; ++mode)
         for (int cfg = 0; cfg < 4; ++cfg) {
             const int cps = cfg < 2 ? 2 : 1, stages = cfg == 0 ? 4 : cfg == 1 ? 6 : cfg == 2 ? 8 : 12;
-            const size_t smem = 1024 + stages * (mode == 2 ? 24576 : 16384) + 256;
+            const size_t smem = 1024 + stages * ((mode == 2 || mode == 3 || mode == 5) ? 24576 : 16384) + 256;
             if (smem > 232448) continue;
-            auto k = mode == 0 ? stream<0> : mode == 1 ? stream<1> : stream<2>;
+            auto k = mode == 0 ? stream<0> : mode == 1 ? stream<1> : mode == 2 ? stream<2> : mode == 3 ? stream<3> : mode == 4 ? stream<4> : stream<5>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             float best = 1e9;
             for (int it = 0; it < 5; ++it) {
@@ -99,7 +131,9 @@ int main() {
                 best = ms < best ? ms : best;
             }
             printf("%s: %d CTAs/SM x %d stages: %.0f GB/s of weights  %s\n",
-                   mode == 0 ? "TMA 2-D box" : mode == 1 ? "bulk 1-D contiguous" : "TMA box + 8 KB activation box",
+                   mode == 0 ? "TMA 2-D box" : mode == 1 ? "bulk 1-D contiguous"
+                             : mode == 2 ? "TMA box + 8 KB activation box" : mode == 3 ? "box + activation + 4 tcgen05.mma/stage"
+                             : mode == 4 ? "bulk 1-D k-major tiles" : "bulk k-major + activation + mma",
                    cps, stages, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
         }
     return 0;
