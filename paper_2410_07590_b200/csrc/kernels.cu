@@ -15,6 +15,30 @@ namespace tkv {
 namespace {
 
 __device__ __forceinline__ float ldf(const float* p, int64_t i) { return p[i]; }
+
+// Split-K partial sums in ascending split order (the order of the previous serial loop, so results are
+// unchanged), with a batch of SB loads in flight instead of one dependent L2/HBM round trip per split.
+template <typename V>
+__device__ __forceinline__ void add_to(V& a, const V& b);
+template <>
+__device__ __forceinline__ void add_to<float>(float& a, const float& b) { a += b; }
+template <>
+__device__ __forceinline__ void add_to<float2>(float2& a, const float2& b) { a.x += b.x, a.y += b.y; }
+template <>
+__device__ __forceinline__ void add_to<float4>(float4& a, const float4& b) { a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w; }
+template <typename V, int SB = 8>
+__device__ __forceinline__ V sum_splits(const float* p, int splits, int64_t plane, V acc) {
+    for (int s0 = 0; s0 < splits; s0 += SB) {
+        V v[SB];
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (s0 + i < splits) v[i] = *reinterpret_cast<const V*>(p + (int64_t)(s0 + i) * plane);
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (s0 + i < splits) add_to(acc, v[i]);
+    }
+    return acc;
+}
 __device__ __forceinline__ float ldf(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
 __device__ __forceinline__ void stf(float* p, int64_t i, float v) { p[i] = v; }
 __device__ __forceinline__ void stf(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
@@ -132,12 +156,8 @@ __global__ void __launch_bounds__(256) residual_kernel(float* x, const float* pa
     float v[4];
     float* xrow = x + t * hidden;
     if ((hidden & 3) == 0 && c0 + 3 < hidden) {
-        const float4 a = *reinterpret_cast<const float4*>(xrow + c0);
+        const float4 a = sum_splits<float4, 16>(partial + t * hidden + c0, splits, plane, *reinterpret_cast<const float4*>(xrow + c0));
         v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
-        for (int s = 0; s < splits; ++s) {
-            const float4 p = *reinterpret_cast<const float4*>(partial + s * plane + t * hidden + c0);
-            v[0] += p.x, v[1] += p.y, v[2] += p.z, v[3] += p.w;
-        }
     } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -162,11 +182,8 @@ __global__ void swiglu_kernel(const float* partial, int splits, int T_, int inte
         const int64_t t = o / inter, i = o - t * inter;
         const int64_t gc = interleave64 ? (i >> 6) * 128 + (i & 63) : i;
         const int64_t uc = interleave64 ? gc + 64 : inter + i;
-        float g = 0.f, u = 0.f;
-        for (int s = 0; s < splits; ++s) {
-            g += partial[s * plane + t * 2 * inter + gc];
-            u += partial[s * plane + t * 2 * inter + uc];
-        }
+        float g = sum_splits(partial + t * 2 * inter + gc, splits, plane, 0.f);
+        float u = sum_splits(partial + t * 2 * inter + uc, splits, plane, 0.f);
         const float sc = row_scale(ssp, nb, t, hidden, eps);
         g *= sc;
         u *= sc;
@@ -205,11 +222,8 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
             cached_t = t;
         }
         const int n = 2 * (int)(p - t * (N / 2));
-        float x0 = 0.f, x1 = 0.f;
-        for (int s = 0; s < splits; ++s) {
-            x0 += partial[s * plane + t * N + n];
-            x1 += partial[s * plane + t * N + n + 1];
-        }
+        const float2 xs = sum_splits(partial + t * N + n, splits, plane, make_float2(0.f, 0.f));  // n even: 8 B aligned
+        float x0 = xs.x, x1 = xs.y;
         x0 *= rs;
         x1 *= rs;
         if (n >= qd + kvd) {  // V: copied as is
@@ -450,9 +464,7 @@ __global__ void reduce_splits_kernel(const float* p, int splits, int64_t n, floa
     pdl_launch();
     pdl_wait();
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
-        float a = 0.f;
-        for (int s = 0; s < splits; ++s) a += p[s * n + o];
-        out[o] = a;
+        out[o] = sum_splits(p + o, splits, n, 0.f);
     }
 }
 
