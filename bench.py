@@ -247,8 +247,13 @@ def run_ours(args):
     from paper_2410_07590_b200 import turbokv as T
 
     rank, local, ws = dist_env()
+    # TKV_BENCH_SAME_GPU=1: every rank on cuda:0 with gloo host collectives -- a dry run of the multi-GPU path
+    # (document-sharded store, IPC pool exchange, peer-slot gathers) on a one-GPU box; not a scaling number
+    same_gpu = os.environ.get("TKV_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     if ws > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group("nccl" if torch.cuda.is_available() and not same_gpu else "gloo")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -313,7 +318,7 @@ def run_ours(args):
     per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = big0.elapsed_time(big1)
     if ws > 1:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms], device="cpu" if same_gpu else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = t.item()
     ms_per_step = total_ms / args.steps
