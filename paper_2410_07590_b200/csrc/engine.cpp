@@ -600,8 +600,15 @@ void tkv_engine::forward(const Fwd& f) {
         launch_embed(f.tok, T, emb, (int)hid, (int)V, ones, x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
                      stream);
     }
+    // the next GEMM of the forward, for the current GEMM's tail L2 warm-up (TKV_GEMM_NEXT_PF)
+    auto next = [&](const void* W, int M, int N, int K) {
+        if (use_tc()) set_gemm_next(W, M, N, K, pick_splits(M, N, K, true));
+    };
     for (int64_t l = 0; l < L; ++l) {
+        const bool last_rows1 = (l == L - 1) && f.logits && !batch;  // the last layer's O-proj / MLP run one row
+        const int rows_next = last_rows1 ? 1 : T;
         // --- attention block ---
+        if (!(f.kv_only && l == L - 1)) next(w_o[l], rows_next, (int)hid, (int)qd);
         int s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
         if (batch) {
             Scope sc(this, PC_EPI, (int)f.reqs.size());
@@ -686,6 +693,7 @@ void tkv_engine::forward(const Fwd& f) {
         }
         uint8_t* attn_rows = static_cast<uint8_t*>(attn.p);
         float* x_rows = x.as<float>() + r0 * hid;
+        next(w_gu[l], rows, (int)(2 * I), (int)hid);
         s = gemm(attn_rows, (int)qd, w_o[l], rows, (int)hid, (int)qd);
         if (!(skip_mask & 1)) {
             Scope sc(this, PC_EPI, 1);
@@ -693,12 +701,14 @@ void tkv_engine::forward(const Fwd& f) {
                             err.as<int>(), stream);
         }
         // --- MLP block: gate|up fused into one GEMM, SwiGLU (with the folded mlp_norm scale) in its epilogue ---
+        next(w_down[l], rows, (int)hid, (int)I);
         s = gemm(xb.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
         if (s > 0) {
             Scope sc(this, PC_EPI, 1);
             launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, ssp.as<float>(), nb, (int)hid, eps, dt, stream,
                           gu_interleaved);
         }
+        if (l + 1 < L) next(w_qkv[l + 1], T, (int)nqkv, (int)hid);
         s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
         if (!(skip_mask & 2)) {
             // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
@@ -1301,6 +1311,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         if (const char* tl = getenv("TKV_TRACE_LAYER")) e->trace_layer = atoi(tl);
         if (const char* as = getenv("TKV_ATTN_SPLITS")) e->attn_split_override = atoi(as);
         if (const char* dr = getenv("TKV_DECODE_ROWS")) e->decode_rows_max = atol(dr);
+        if (const char* np = getenv("TKV_GEMM_NEXT_PF")) set_gemm_next_pf(atoi(np));
         if (const char* gk = getenv("TKV_GEMM_KNOBS")) {  // "stages,smem_kb,ctas_per_sm,evict_first[,np[,pf]]"
             int st = 0, sm = 0, cps = 0, ef = 1, np = 0, pf = -1, kr = -1;
             if (sscanf(gk, "%d,%d,%d,%d,%d,%d,%d", &st, &sm, &cps, &ef, &np, &pf, &kr) >= 3)

@@ -42,6 +42,7 @@ struct Knobs {
     // (np = 2 with one 208 KB CTA per SM measured slower than np = 1 at 2 x 110 KB); pf = L2 prefetch distance
     // of the weight stream in k-blocks (0 = off)
     int stages = 0, smem_kb = 110, ctas_per_sm = 2, w_evict_first = 1, np = 1, pf = 0, krot = 1;
+    int next_pf = 0;  // k-blocks per unit of the NEXT GEMM warmed into L2 at this GEMM's tail (0 = off)
     // normal (> 128 tokens) tiling: nsnp 128-column halves per MMA (UMMA N = 128 * nsnp); N = 256 halves the
     // shared-memory traffic per FLOP of the SS-mode MMA (the 128 x 128 tile is smem-bandwidth bound at ~50 %)
     int nsnp = 2, ns_smem_kb = 208;
@@ -151,6 +152,10 @@ struct GemmArgs {
     int pf;                       // weight L2 prefetch distance (k-blocks ahead of the ring)
     int krot;                     // rotate each unit's k-block order (spreads the shared activation tiles'
                                   // L2 reads over time instead of every CTA hitting the same lines at once)
+    // next GEMM of the forward (swapped): once this CTA has issued its last loads, it warms L2 with the first
+    // nx_pf weight k-blocks of the next GEMM's units blockIdx.x, blockIdx.x + grid, ... (tmN), so that GEMM's
+    // ring fill hits L2 while this one drains and runs its epilogue
+    int nx_pf, nx_units, nx_n_tiles, nx_kb_total, nx_kb_per_split, nx_np;
 };
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
@@ -169,7 +174,8 @@ __device__ __forceinline__ void unit_coords(const GemmArgs& g, int u, int& nt, i
 // mainloop of unit i+1.
 template <bool SWAP, int EPI>
 __global__ void __launch_bounds__(THREADS_P)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, GemmArgs g) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+                   const __grid_constant__ CUtensorMap tmN, GemmArgs g) {
     pdl_launch();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -252,6 +258,13 @@ __global__ void __launch_bounds__(THREADS_P)
                     tma_load_2d(w + wbytes, &tmA, &full[s], kb * BK, mt * mstep);
                 }
             }
+            if (g.nx_pf > 0)
+                for (int u = blockIdx.x; u < g.nx_units; u += gridDim.x) {
+                    const int z2 = u / g.nx_n_tiles, nt2 = u - z2 * g.nx_n_tiles;
+                    const int k0 = z2 * g.nx_kb_per_split, nkb = min(g.nx_kb_total, k0 + g.nx_kb_per_split) - k0;
+                    for (int i = 0; i < min(nkb, g.nx_pf); ++i)
+                        tma_prefetch_2d(&tmN, kblk(k0, nkb, i, u) * BK, nt2 * 128 * g.nx_np);
+                }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer ----------------
@@ -450,10 +463,16 @@ CUtensorMap make_map(const void* base, int rows, int cols_k, int ld_elems, int b
 }
 
 template <bool SWAP, int EPI>
-void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g, int grid, size_t smem, cudaStream_t s) {
+void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const CUtensorMap& tn, const GemmArgs& g, int grid,
+              size_t smem, cudaStream_t s) {
     TKV_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<SWAP, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(THREADS_P), smem, s, ta, tw, g);
+    launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(THREADS_P), smem, s, ta, tw, tn, g);
 }
+
+struct NextGemm {
+    const void* W = nullptr;
+    int M = 0, N = 0, K = 0, splits = 1;
+} g_next;
 
 }  // namespace
 
@@ -516,14 +535,30 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     const int grid = std::min(g.units, sms * gemm_tc_ctas_per_sm(M));
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
     const CUtensorMap tw = make_map(W, N, K, K, 128 * g.np);
+    CUtensorMap tn = tw;
+    if (g_knobs.next_pf > 0 && swap && g_next.W && g_next.M <= 128) {
+        const NextGemm& nx = g_next;
+        g.nx_pf = g_knobs.next_pf;
+        g.nx_np = np_for(nx.M, nx.N);
+        g.nx_n_tiles = (nx.N + 128 * g.nx_np - 1) / (128 * g.nx_np);
+        g.nx_kb_total = (nx.K + BK - 1) / BK;
+        g.nx_kb_per_split = (g.nx_kb_total + nx.splits - 1) / nx.splits;
+        g.nx_units = g.nx_n_tiles * ((g.nx_kb_total + g.nx_kb_per_split - 1) / g.nx_kb_per_split);
+        tn = make_map(nx.W, nx.N, nx.K, nx.K, 128 * g.nx_np);
+    }
+    g_next = NextGemm{};
     if (swiglu_act) {
         if (eff_splits != 1) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the whole K range in one unit");
-        swap ? launch_t<true, EPI_SWIGLU>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_SWIGLU>(ta, tw, g, grid, smem, s);
+        swap ? launch_t<true, EPI_SWIGLU>(ta, tw, tn, g, grid, smem, s) : launch_t<false, EPI_SWIGLU>(ta, tw, tn, g, grid, smem, s);
     } else {
-        swap ? launch_t<true, EPI_PARTIAL>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_PARTIAL>(ta, tw, g, grid, smem, s);
+        swap ? launch_t<true, EPI_PARTIAL>(ta, tw, tn, g, grid, smem, s) : launch_t<false, EPI_PARTIAL>(ta, tw, tn, g, grid, smem, s);
     }
     return eff_splits;
 }
+
+void set_gemm_next(const void* W, int M, int N, int K, int splits) { g_next = NextGemm{W, M, N, K, splits}; }
+
+void set_gemm_next_pf(int kblocks) { g_knobs.next_pf = kblocks; }
 
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np, int pf, int krot) {
     const Knobs d;

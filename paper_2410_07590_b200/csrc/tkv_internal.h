@@ -122,6 +122,10 @@ void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K
 // M <= 128 uses the swapped tiling (weights on the UMMA M side). With swiglu_act != nullptr (splits must
 // be 1, W rows interleaved in 64-row gate/up blocks) the epilogue writes act[M][N/2] = silu(g)*u in bf16.
 bool gemm_tc_supported(int M, int N, int K, int lda);
+// The GEMM that follows the next launch_gemm_tc in the forward (consumed by that launch) and how many of its
+// weight k-blocks per unit the current GEMM warms into L2 at its tail (0 = off)
+void set_gemm_next(const void* W, int M, int N, int K, int splits);
+void set_gemm_next_pf(int kblocks);
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np = 0, int pf = -1,
                     int krot = -1);
 int gemm_tc_tiles(int M, int N);
