@@ -46,6 +46,11 @@ struct Knobs {
     // normal (> 128 tokens) tiling: nsnp 128-column halves per MMA (UMMA N = 128 * nsnp); N = 256 halves the
     // shared-memory traffic per FLOP of the SS-mode MMA (the 128 x 128 tile is smem-bandwidth bound at ~50 %)
     int nsnp = 2, ns_smem_kb = 208;
+    // normal tiling: nsmp 128-row activation tiles per unit share each weight tile (M = 128 * nsmp per unit):
+    // the per-FLOP L2 -> smem traffic drops by 1/3 at nsmp = 2 (A 32 KB + W 32 KB per 64-deep k-block for
+    // 2 x 128 x 256 outputs); the two 128 x 256 fp32 accumulators fill TMEM, so a unit's epilogue is not
+    // overlapped with the next mainloop
+    int nsmp = 2;
 };
 Knobs g_knobs;
 
@@ -137,7 +142,9 @@ struct GemmArgs {
     int kb_total, kb_per_split;
     int n_tiles, m_tiles, units;  // work units = n_tiles * m_tiles * splits (persistent loop over them)
     int np;                       // swapped: 128-row weight tiles per unit (n_tiles counts units along N)
-    int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128
+    int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128 * mp
+    int mp;                       // normal: 128-row activation sub-tiles per unit (each its own MMA + accumulator)
+    int nbuf;                     // TMEM accumulator buffers (2: epilogue overlaps the next unit's mainloop)
     uint32_t a_bytes;             // bytes of the activation tile per stage
     int stages;
     uint32_t acc_cols;            // TMEM columns of one accumulator buffer (two buffers)
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(THREADS_P)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const int mstep = SWAP ? g.ntok : 128;
+    const int mstep = SWAP ? g.ntok : 128 * g.mp;
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer ----------------
@@ -274,8 +281,8 @@ __global__ void __launch_bounds__(THREADS_P)
                 int nt, mt, z;
                 unit_coords(g, u, nt, mt, z);
                 const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
-                const int b = lu & 1;
-                mbar_wait(&tempty[b], ((uint32_t)(lu >> 1) & 1u) ^ 1u);
+                const int b = lu % g.nbuf;
+                mbar_wait(&tempty[b], ((uint32_t)(lu / g.nbuf) & 1u) ^ 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t acc = tmem + (uint32_t)b * g.acc_cols;
                 for (int i = 0; i < nkb; ++i, ++it) {
@@ -291,7 +298,9 @@ __global__ void __launch_bounds__(THREADS_P)
                                 umma_f16(acc + (uint32_t)(p * g.ntok), desc_k(w + p * TILE_W + k * 32),
                                          desc_k(a + k * 32), id, (i | k) != 0);
                         } else {
-                            umma_f16(acc, desc_k(a + k * 32), desc_k(w + k * 32), id, (i | k) != 0);
+                            for (int mi = 0; mi < g.mp; ++mi)  // mp activation sub-tiles share the weight tile
+                                umma_f16(acc + (uint32_t)(mi * 128 * g.np), desc_k(a + mi * 16384 + k * 32),
+                                         desc_k(w + k * 32), id, (i | k) != 0);
                         }
                     }
                     umma_commit(&empty[s]);
@@ -309,13 +318,14 @@ __global__ void __launch_bounds__(THREADS_P)
         for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++lu) {
             int nt, mt, z;
             unit_coords(g, u, nt, mt, z);
-            const int b = lu & 1;
-            mbar_wait(&tfull[b], (uint32_t)(lu >> 1) & 1u);
+            const int b = lu % g.nbuf;
+            mbar_wait(&tfull[b], (uint32_t)(lu / g.nbuf) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t acc_u = tmem + lane_base + (uint32_t)b * g.acc_cols;
             const int m0 = mt * mstep;
-            for (int p = 0; p < g.np; ++p) {
-            const uint32_t acc = acc_u + (uint32_t)(p * (SWAP ? g.ntok : 128));
+            for (int pm = 0; pm < g.np * (SWAP ? 1 : g.mp); ++pm) {
+            const int p = pm % g.np, mi = pm / g.np;  // weight sub-tile, activation sub-tile (normal tiling)
+            const uint32_t acc = acc_u + (uint32_t)(SWAP ? p * g.ntok : (mi * g.np + p) * 128);
             const int n0 = (nt * g.np + p) * 128;
             if (SWAP) {
                 const int n = n0 + lg * 32 + lane;  // TMEM lane = weight row n, column = token
@@ -370,7 +380,7 @@ __global__ void __launch_bounds__(THREADS_P)
                     asm volatile("bar.sync 1, 128;" ::: "memory");  // scratch reusable by the next unit
                 }
             } else {
-                const int m = m0 + lg * 32 + lane;  // TMEM lane = token row m, column = weight row
+                const int m = m0 + mi * 128 + lg * 32 + lane;  // TMEM lane = token row m, column = weight row
                 if (EPI == EPI_PARTIAL) {
                     float* out = g.partial + (int64_t)z * g.M * g.N + (int64_t)m * g.N;
 #pragma unroll 1
@@ -488,10 +498,12 @@ static int np_for(int M, int N) {
     return M <= 128 ? std::max(1, g_knobs.np) : std::max(1, std::min(2, g_knobs.nsnp));
 }
 
+static int mp_for(int M) { return M <= 128 ? 1 : (M >= 256 ? std::max(1, std::min(2, g_knobs.nsmp)) : 1); }
+
 int gemm_tc_tiles(int M, int N) {
     const bool swap = M <= 128;
-    const int np = np_for(M, N);
-    return ((N + 128 * np - 1) / (128 * np)) * (swap ? 1 : (M + 127) / 128);
+    const int np = np_for(M, N), mp = mp_for(M);
+    return ((N + 128 * np - 1) / (128 * np)) * (swap ? 1 : (M + 128 * mp - 1) / (128 * mp));
 }
 
 int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
@@ -505,14 +517,16 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.kb_per_split = (g.kb_total + splits - 1) / splits;
     const int eff_splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;  // every unit non-empty
     g.np = np_for(M, N);
+    g.mp = mp_for(M);
     g.n_tiles = (N + 128 * g.np - 1) / (128 * g.np);
-    g.m_tiles = swap ? 1 : (M + 127) / 128;
+    g.m_tiles = swap ? 1 : (M + 128 * g.mp - 1) / (128 * g.mp);
     g.units = g.n_tiles * g.m_tiles * eff_splits;
-    g.ntok = swap ? ((M + 15) / 16) * 16 : 128;
+    g.ntok = swap ? ((M + 15) / 16) * 16 : 128 * g.mp;
     g.a_bytes = (uint32_t)g.ntok * BK * 2;
-    g.acc_cols = swap ? (uint32_t)(g.ntok * g.np) : 128u * (uint32_t)g.np;
+    g.acc_cols = swap ? (uint32_t)(g.ntok * g.np) : 128u * (uint32_t)(g.np * g.mp);
+    g.nbuf = 2 * g.acc_cols <= 512 ? 2 : 1;
     g.tmem_cols = 32;
-    while (g.tmem_cols < 2 * g.acc_cols) g.tmem_cols <<= 1;
+    while (g.tmem_cols < (uint32_t)g.nbuf * g.acc_cols) g.tmem_cols <<= 1;
     const uint32_t scratch =
         (swap && swiglu_act) ? (uint32_t)((64 * (g.ntok + 1) + g.ntok) * 4 + 1023) / 1024 * 1024 : 0;
     const int budget = swap ? (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET) : g_knobs.ns_smem_kb * 1024;
@@ -559,6 +573,8 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
 void set_gemm_next(const void* W, int M, int N, int K, int splits) { g_next = NextGemm{W, M, N, K, splits}; }
 
 void set_gemm_next_pf(int kblocks) { g_knobs.next_pf = kblocks; }
+
+void set_gemm_nsmp(int mp) { g_knobs.nsmp = mp > 0 ? mp : 1; }
 
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np, int pf, int krot) {
     const Knobs d;
