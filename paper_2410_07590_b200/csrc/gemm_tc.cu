@@ -51,6 +51,9 @@ struct Knobs {
     // 2 x 128 x 256 outputs); the two 128 x 256 fp32 accumulators fill TMEM, so a unit's epilogue is not
     // overlapped with the next mainloop
     int nsmp = 2;
+    int raster = 1;  // normal tiling unit order: 0 = n-fastest, 1 = m-fastest when N > M (W larger), 2 = m-fastest,
+                     // 3 = m-fastest in groups of group_mb MB of activation rows (always)
+    int group_mb = 32;
 };
 Knobs g_knobs;
 
@@ -145,6 +148,9 @@ struct GemmArgs {
     int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128 * mp
     int mp;                       // normal: 128-row activation sub-tiles per unit (each its own MMA + accumulator)
     int nbuf;                     // TMEM accumulator buffers (2: epilogue overlaps the next unit's mainloop)
+    int m_group;                  // unit raster (normal tiling): 0 = n-tiles fastest; G > 0 = groups of G m-tiles,
+                                  // m fastest inside a group and the group's activation rows kept L2-resident
+                                  // while every n-tile streams past them (W from DRAM once per group)
     uint32_t a_bytes;             // bytes of the activation tile per stage
     int stages;
     uint32_t acc_cols;            // TMEM columns of one accumulator buffer (two buffers)
@@ -172,8 +178,16 @@ __device__ __forceinline__ void unit_coords(const GemmArgs& g, int u, int& nt, i
     const int per = g.n_tiles * g.m_tiles;
     z = u / per;
     const int rem = u - z * per;
-    mt = rem / g.n_tiles;
-    nt = rem - mt * g.n_tiles;
+    if (g.m_group > 0) {
+        const int span = g.m_group * g.n_tiles;
+        const int gi = rem / span, r = rem - gi * span;
+        const int gsz = min(g.m_group, g.m_tiles - gi * g.m_group);
+        nt = r / gsz;
+        mt = gi * g.m_group + (r - nt * gsz);
+    } else {
+        mt = rem / g.n_tiles;
+        nt = rem - mt * g.n_tiles;
+    }
 }
 
 // Persistent: grid = min(units, #SMs); CTA b owns units b, b + grid, ... The smem ring of {W, A} stages
@@ -525,6 +539,14 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.a_bytes = (uint32_t)g.ntok * BK * 2;
     g.acc_cols = swap ? (uint32_t)(g.ntok * g.np) : 128u * (uint32_t)(g.np * g.mp);
     g.nbuf = 2 * g.acc_cols <= 512 ? 2 : 1;
+    g.m_group = 0;
+    if (!swap && g_knobs.raster != 0 && (g_knobs.raster == 2 || N > M)) {
+        g.m_group = g.m_tiles;  // raster 1/2: all m-tiles in one group
+        if (g_knobs.raster == 3 || (g_knobs.raster == 1 && g_knobs.group_mb > 0)) {
+            const double a_tile = 128.0 * g.mp * K * 2;  // bytes of one m-tile's activation rows
+            g.m_group = std::max(1, std::min(g.m_tiles, (int)(g_knobs.group_mb * 1048576.0 / a_tile)));
+        }
+    }
     g.tmem_cols = 32;
     while (g.tmem_cols < (uint32_t)g.nbuf * g.acc_cols) g.tmem_cols <<= 1;
     const uint32_t scratch =
@@ -575,6 +597,11 @@ void set_gemm_next(const void* W, int M, int N, int K, int splits) { g_next = Ne
 void set_gemm_next_pf(int kblocks) { g_knobs.next_pf = kblocks; }
 
 void set_gemm_nsmp(int mp) { g_knobs.nsmp = mp > 0 ? mp : 1; }
+
+void set_gemm_raster(int r, int group_mb) {
+    g_knobs.raster = r;
+    if (group_mb >= 0) g_knobs.group_mb = group_mb;
+}
 
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np, int pf, int krot) {
     const Knobs d;

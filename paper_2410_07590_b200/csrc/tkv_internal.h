@@ -126,7 +126,10 @@ bool gemm_tc_supported(int M, int N, int K, int lda);
 // weight k-blocks per unit the current GEMM warms into L2 at its tail (0 = off)
 void set_gemm_next(const void* W, int M, int N, int K, int splits);
 void set_gemm_next_pf(int kblocks);
-void set_gemm_nsmp(int mp);  // normal (> 128-token) tiling: 128-row activation tiles per unit (1 or 2)
+void set_gemm_nsmp(int mp);
+// normal tiling unit order (0 n-fastest, 1 m-fastest when N > M, 2 m-fastest; group_mb > 0: m-tile groups of
+// that many MB of activation rows)
+void set_gemm_raster(int r, int group_mb = -1);  // normal (> 128-token) tiling: 128-row activation tiles per unit (1 or 2)
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np = 0, int pf = -1,
                     int krot = -1);
 int gemm_tc_tiles(int M, int N);
