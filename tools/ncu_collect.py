@@ -25,7 +25,7 @@ def rows_of(path):
 
 def main(tag, src="gpurun_out", dst="profiles"):
     out, traffic = [], {}
-    for k in ["gather_rope", "attn_tc_kernel", "attn_tc_combine", "gemm_tc_kernel"]:
+    for k in ["gather_rope", "attn_tc_kernel", "attn_tc_combine", "gemm_tc_kernel", "gemm_bigM"]:
         path = os.path.join(src, f"{tag}_full_{k}.ncu-rep")
         if not os.path.exists(path):
             continue

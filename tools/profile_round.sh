@@ -15,3 +15,7 @@ for spec in "gather_rope:3:1" "attn_tc_kernel:90:1" "attn_tc_combine:90:1" "gemm
     -o gpurun_out/${TAG}_full_$k $B > gpurun_out/${TAG}_ncu_$k.log 2>&1
   echo "$k rc=$?"
 done
+# large-M (8256-token full-concat prefill) gate/up + down GEMMs: the tensor-bound tiling
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 2 -c 2 \
+  -o gpurun_out/${TAG}_full_gemm_bigM python tools/naive_once.py > gpurun_out/${TAG}_ncu_gemm_bigM.log 2>&1
+echo "gemm_bigM rc=$?"
