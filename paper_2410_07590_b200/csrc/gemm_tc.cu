@@ -54,6 +54,7 @@ struct Knobs {
     int raster = 1;  // normal tiling unit order: 0 = n-fastest, 1 = m-fastest when N > M (W larger), 2 = m-fastest,
                      // 3 = m-fastest in groups of group_mb MB of activation rows (always)
     int group_mb = 32;
+    int cluster = 1;  // normal tiling: 2 = CTA pairs share (multicast) each weight tile
 };
 Knobs g_knobs;
 
@@ -104,6 +105,28 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
                  "r"(c0), "r"(c1)
                  : "memory");
 }
+// Multicast variants (2-CTA clusters, normal tiling): the weight tile lands at the same smem offset in every CTA
+// of ctaMask and completes bytes on each CTA's barrier at the same offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -148,6 +171,8 @@ struct GemmArgs {
     int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128 * mp
     int mp;                       // normal: 128-row activation sub-tiles per unit (each its own MMA + accumulator)
     int nbuf;                     // TMEM accumulator buffers (2: epilogue overlaps the next unit's mainloop)
+    int cl;                       // normal tiling: CTAs per cluster (2: the pair computes m-tiles 2i and 2i+1 of
+                                  // one n-tile; rank 0 multicasts the weight tile to both; m_tiles counts pairs)
     int m_group;                  // unit raster (normal tiling): 0 = n-tiles fastest; G > 0 = groups of G m-tiles,
                                   // m fastest inside a group and the group's activation rows kept L2-resident
                                   // while every n-tile streams past them (W from DRAM once per group)
@@ -208,11 +233,18 @@ __global__ void __launch_bounds__(THREADS_P)
     uint64_t* tempty = tfull + 2;        // [2] accumulator drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cl = SWAP ? 1 : g.cl;
+    const int rank = cl > 1 ? (int)cluster_rank() : 0;
+    const int u0 = blockIdx.x / cl, ustep = gridDim.x / cl;  // this CTA's (pair) units: u0, u0 + ustep, ...
+    auto coords = [&](int u, int& nt, int& mt, int& z) {
+        unit_coords(g, u, nt, mt, z);
+        if (cl > 1) mt = mt * cl + rank;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < g.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], cl);  // released by the MMA of every CTA whose tile reads the stage's weights
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
@@ -229,6 +261,7 @@ __global__ void __launch_bounds__(THREADS_P)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (cl > 1) cluster_sync_all();  // the partner's barriers are initialised before any multicast targets them
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     const int mstep = SWAP ? g.ntok : 128 * g.mp;
@@ -237,7 +270,9 @@ __global__ void __launch_bounds__(THREADS_P)
         if (lane == 0) {  // ---------------- TMA producer ----------------
             const uint64_t wpol = policy_evict_first();
             auto load_w = [&](void* dst, uint64_t* bar, int c0, int c1) {
-                if (g.w_evict_first)
+                if (cl > 1) {  // rank 0 brings the weight tile into both CTAs
+                    if (rank == 0) tma_load_2d_mc(dst, &tmW, bar, c0, c1, (uint16_t)((1u << cl) - 1), wpol);
+                } else if (g.w_evict_first)
                     tma_load_2d_hint(dst, &tmW, bar, c0, c1, wpol);
                 else
                     tma_load_2d(dst, &tmW, bar, c0, c1);
@@ -245,7 +280,7 @@ __global__ void __launch_bounds__(THREADS_P)
             // Weight tiles do not depend on earlier kernels: fill the ring with the first unit's weights
             // BEFORE waiting on the previous grid (PDL), so the weight stream overlaps its tail.
             int nt, mt, z;
-            unit_coords(g, blockIdx.x, nt, mt, z);
+            coords(u0, nt, mt, z);
             const int kb0 = z * g.kb_per_split;
             const int nkb0 = min(g.kb_total, kb0 + g.kb_per_split) - kb0;
             // k-block of iteration i of unit u (the MMA only accumulates, so any order is valid)
@@ -253,22 +288,22 @@ __global__ void __launch_bounds__(THREADS_P)
             const int pre = min(nkb0, g.stages);
             for (int i = 0; i < pre; ++i) {
                 mbar_expect_tx(&full[i], stage_bytes);
-                load_w(smem + i * stage_bytes, &full[i], kblk(kb0, nkb0, i, blockIdx.x) * BK, nt * 128 * g.np);
+                load_w(smem + i * stage_bytes, &full[i], kblk(kb0, nkb0, i, u0) * BK, nt * 128 * g.np);
             }
             pdl_wait();
             for (int i = 0; i < pre; ++i)
-                tma_load_2d(smem + i * stage_bytes + wbytes, &tmA, &full[i], kblk(kb0, nkb0, i, blockIdx.x) * BK, mt * mstep);
+                tma_load_2d(smem + i * stage_bytes + wbytes, &tmA, &full[i], kblk(kb0, nkb0, i, u0) * BK, mt * mstep);
             // L2 prefetch of the first unit's next pf weight tiles (beyond the ring)
             for (int i = pre; i < min(nkb0, pre + g.pf); ++i)
-                tma_prefetch_2d(&tmW, kblk(kb0, nkb0, i, blockIdx.x) * BK, nt * 128 * g.np);
+                tma_prefetch_2d(&tmW, kblk(kb0, nkb0, i, u0) * BK, nt * 128 * g.np);
             int it = pre;
-            for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-                unit_coords(g, u, nt, mt, z);
+            for (int u = u0; u < g.units; u += ustep) {
+                coords(u, nt, mt, z);
                 const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
-                if (u != (int)blockIdx.x)
+                if (u != u0)
                     for (int i = 0; i < min(nkb, g.pf); ++i) tma_prefetch_2d(&tmW, kblk(k0, nkb, i, u) * BK, nt * 128 * g.np);
-                for (int i = (u == (int)blockIdx.x ? pre : 0); i < nkb; ++i, ++it) {
-                    if (g.pf > 0 && i + g.pf < nkb && i + g.pf >= (u == (int)blockIdx.x ? pre + g.pf : g.pf))
+                for (int i = (u == u0 ? pre : 0); i < nkb; ++i, ++it) {
+                    if (g.pf > 0 && i + g.pf < nkb && i + g.pf >= (u == u0 ? pre + g.pf : g.pf))
                         tma_prefetch_2d(&tmW, kblk(k0, nkb, i + g.pf, u) * BK, nt * 128 * g.np);
                     const int s = it % g.stages;
                     mbar_wait(&empty[s], ((uint32_t)(it / g.stages) & 1u) ^ 1u);
@@ -291,9 +326,9 @@ __global__ void __launch_bounds__(THREADS_P)
         if (lane == 0) {  // ---------------- MMA issuer ----------------
             const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128 * g.np);
             int it = 0, lu = 0;
-            for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++lu) {
+            for (int u = u0; u < g.units; u += ustep, ++lu) {
                 int nt, mt, z;
-                unit_coords(g, u, nt, mt, z);
+                coords(u, nt, mt, z);
                 const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
                 const int b = lu % g.nbuf;
                 mbar_wait(&tempty[b], ((uint32_t)(lu / g.nbuf) & 1u) ^ 1u);
@@ -317,7 +352,10 @@ __global__ void __launch_bounds__(THREADS_P)
                                          desc_k(w + k * 32), id, (i | k) != 0);
                         }
                     }
-                    umma_commit(&empty[s]);
+                    if (cl > 1)
+                        umma_commit_mc(&empty[s], (uint16_t)((1u << cl) - 1));  // both CTAs read the weight tile
+                    else
+                        umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[b]);
             }
@@ -329,9 +367,9 @@ __global__ void __launch_bounds__(THREADS_P)
         const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
         const int et = threadIdx.x - 64;  // 0..127
         int lu = 0;
-        for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++lu) {
+        for (int u = u0; u < g.units; u += ustep, ++lu) {
             int nt, mt, z;
-            unit_coords(g, u, nt, mt, z);
+            coords(u, nt, mt, z);
             const int b = lu % g.nbuf;
             mbar_wait(&tfull[b], (uint32_t)(lu / g.nbuf) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -449,6 +487,7 @@ __global__ void __launch_bounds__(THREADS_P)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (cl > 1) cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
@@ -490,7 +529,25 @@ template <bool SWAP, int EPI>
 void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const CUtensorMap& tn, const GemmArgs& g, int grid,
               size_t smem, cudaStream_t s) {
     TKV_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<SWAP, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(THREADS_P), smem, s, ta, tw, tn, g);
+    if (SWAP || g.cl <= 1) {
+        launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(THREADS_P), smem, s, ta, tw, tn, g);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS_P);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)g.cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    TKV_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<SWAP, EPI>, ta, tw, tn, g));
 }
 
 struct NextGemm {
@@ -534,6 +591,8 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.mp = mp_for(M);
     g.n_tiles = (N + 128 * g.np - 1) / (128 * g.np);
     g.m_tiles = swap ? 1 : (M + 128 * g.mp - 1) / (128 * g.mp);
+    g.cl = (!swap && g_knobs.cluster > 1 && g.m_tiles >= 2) ? 2 : 1;
+    if (g.cl > 1) g.m_tiles = (g.m_tiles + 1) / 2;  // units count m-tile PAIRS (the odd tail's partner is all OOB)
     g.units = g.n_tiles * g.m_tiles * eff_splits;
     g.ntok = swap ? ((M + 15) / 16) * 16 : 128 * g.mp;
     g.a_bytes = (uint32_t)g.ntok * BK * 2;
@@ -568,7 +627,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min(g.units, sms * gemm_tc_ctas_per_sm(M));
+    int grid = std::min(g.units, sms * gemm_tc_ctas_per_sm(M) / g.cl) * g.cl;  // cluster mode: whole pairs
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
     const CUtensorMap tw = make_map(W, N, K, K, 128 * g.np);
     CUtensorMap tn = tw;
@@ -597,6 +656,8 @@ void set_gemm_next(const void* W, int M, int N, int K, int splits) { g_next = Ne
 void set_gemm_next_pf(int kblocks) { g_knobs.next_pf = kblocks; }
 
 void set_gemm_nsmp(int mp) { g_knobs.nsmp = mp > 0 ? mp : 1; }
+
+void set_gemm_cluster(int c) { g_knobs.cluster = c; }
 
 void set_gemm_raster(int r, int group_mb) {
     g_knobs.raster = r;
