@@ -7,6 +7,9 @@ margin exceeds the measured bf16 error (SURVEY §7 hard part 4).
 near-zero logits). For bf16 the floor is max|ref| itself, i.e. max|got-ref| <= 2e-2 * max|ref|:
 bf16 carries 8 mantissa bits, so a per-element bound on logits near zero would test rounding noise.
 """
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -529,3 +532,34 @@ def test_index_top_k_matches_reference():
         small.top_k(payloads[1], 0)
     small.close()
     eng.close()
+
+
+_TILING_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import oracle as O
+from paper_2410_07590_b200 import turbokv as T
+cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
+eng = T.Engine(cfg, 7, dtype="bf16", store_capacity_tokens=1 << 16)
+pays = [O.random_text_tokens(700 + i, 510) for i in range(5)]
+q = O.random_text_tokens(701, 64)
+out = eng.naive_prefill([O.frame(p) for p in pays], q, T.MaskMode.Causal, keep_context=False)[0]
+np.save(sys.argv[1], out)
+"""
+
+
+@pytest.mark.parametrize("env", [{"TKV_GEMM_NSMP": "1", "TKV_GEMM_RASTER": "0"}, {"TKV_GEMM_CLUSTER": "2"}])
+def test_large_m_gemm_tilings_agree(tmp_path, env):
+    """The large-M (> 128 tokens) GEMM variants -- one 128-row activation tile per unit with n-fastest raster, and
+    2-CTA clusters multicasting the weight tile -- give the default tiling's full-concat logits (bf16 tolerance);
+    each runs in a fresh process because the tiling knobs are process-wide."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "run.py"
+    script.write_text(_TILING_SCRIPT.format(root=root))
+    outs = []
+    for e in ({}, env):
+        path = tmp_path / f"out{len(outs)}.npy"
+        subprocess.run([sys.executable, str(script), str(path)], check=True, env={**os.environ, **e}, timeout=300)
+        outs.append(np.load(path))
+    assert_close(outs[1], outs[0], BF16_TOL)
