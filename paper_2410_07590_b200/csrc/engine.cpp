@@ -1314,6 +1314,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         if (const char* np = getenv("TKV_GEMM_NEXT_PF")) set_gemm_next_pf(atoi(np));
         if (const char* mp = getenv("TKV_GEMM_NSMP")) set_gemm_nsmp(atoi(mp));
         if (const char* gc = getenv("TKV_GEMM_CLUSTER")) set_gemm_cluster(atoi(gc));
+        if (const char* se = getenv("TKV_GEMM_SKIP_EPI")) set_gemm_skip_epi(atoi(se));
         if (const char* ra = getenv("TKV_GEMM_RASTER")) set_gemm_raster(atoi(ra));
         if (const char* gm = getenv("TKV_GEMM_GROUP_MB")) set_gemm_raster(1, atoi(gm));
         if (const char* gk = getenv("TKV_GEMM_KNOBS")) {  // "stages,smem_kb,ctas_per_sm,evict_first[,np[,pf]]"

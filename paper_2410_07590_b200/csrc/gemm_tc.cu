@@ -55,6 +55,7 @@ struct Knobs {
                      // 3 = m-fastest in groups of group_mb MB of activation rows (always)
     int group_mb = 32;
     int cluster = 1;  // normal tiling: 2 = CTA pairs share (multicast) each weight tile
+    int skip_epi = 0;
 };
 Knobs g_knobs;
 
@@ -171,6 +172,7 @@ struct GemmArgs {
     int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128 * mp
     int mp;                       // normal: 128-row activation sub-tiles per unit (each its own MMA + accumulator)
     int nbuf;                     // TMEM accumulator buffers (2: epilogue overlaps the next unit's mainloop)
+    int skip_epi;                 // debug timing knob: normal-tiling partial epilogue skipped (results invalid)
     int cl;                       // normal tiling: CTAs per cluster (2: the pair computes m-tiles 2i and 2i+1 of
                                   // one n-tile; rank 0 multicasts the weight tile to both; m_tiles counts pairs)
     int m_group;                  // unit raster (normal tiling): 0 = n-tiles fastest; G > 0 = groups of G m-tiles,
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(THREADS_P)
                 const int m = m0 + mi * 128 + lg * 32 + lane;  // TMEM lane = token row m, column = weight row
                 if (EPI == EPI_PARTIAL) {
                     float* out = g.partial + (int64_t)z * g.M * g.N + (int64_t)m * g.N;
+                    if (g.skip_epi) continue;  // timing experiment only (TKV_GEMM_SKIP_EPI): results invalid
 #pragma unroll 1
                     for (int c = 0; c < 128; c += 16) {
                         uint32_t r[16];
@@ -592,6 +595,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.n_tiles = (N + 128 * g.np - 1) / (128 * g.np);
     g.m_tiles = swap ? 1 : (M + 128 * g.mp - 1) / (128 * g.mp);
     g.cl = (!swap && g_knobs.cluster > 1 && g.m_tiles >= 2) ? 2 : 1;
+    g.skip_epi = g_knobs.skip_epi;
     if (g.cl > 1) g.m_tiles = (g.m_tiles + 1) / 2;  // units count m-tile PAIRS (the odd tail's partner is all OOB)
     g.units = g.n_tiles * g.m_tiles * eff_splits;
     g.ntok = swap ? ((M + 15) / 16) * 16 : 128 * g.mp;
@@ -658,6 +662,8 @@ void set_gemm_next_pf(int kblocks) { g_knobs.next_pf = kblocks; }
 void set_gemm_nsmp(int mp) { g_knobs.nsmp = mp > 0 ? mp : 1; }
 
 void set_gemm_cluster(int c) { g_knobs.cluster = c; }
+
+void set_gemm_skip_epi(int v) { g_knobs.skip_epi = v; }
 
 void set_gemm_raster(int r, int group_mb) {
     g_knobs.raster = r;

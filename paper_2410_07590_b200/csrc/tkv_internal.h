@@ -127,7 +127,8 @@ bool gemm_tc_supported(int M, int N, int K, int lda);
 void set_gemm_next(const void* W, int M, int N, int K, int splits);
 void set_gemm_next_pf(int kblocks);
 void set_gemm_nsmp(int mp);
-void set_gemm_cluster(int c);  // normal tiling: 2 = CTA pairs share each weight tile through TMA multicast
+void set_gemm_cluster(int c);
+void set_gemm_skip_epi(int v);  // timing experiments only: skip the normal-tiling partial stores  // normal tiling: 2 = CTA pairs share each weight tile through TMA multicast
 // normal tiling unit order (0 n-fastest, 1 m-fastest when N > M, 2 m-fastest; group_mb > 0: m-tile groups of
 // that many MB of activation rows)
 void set_gemm_raster(int r, int group_mb = -1);  // normal (> 128-token) tiling: 128-row activation tiles per unit (1 or 2)
