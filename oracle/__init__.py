@@ -330,6 +330,7 @@ class Ref:
             L.ref_engine_fingerprint.restype = C.c_uint64
             L.ref_engine_fingerprint.argtypes = [C.c_void_p]
             L.ref_ingest.argtypes = [C.c_void_p, I32P, C.c_int64, U64P]
+            L.ref_bench_ingest.argtypes = [C.c_void_p, I64P, C.c_int64, C.c_uint64, U64P, C.c_int64, I64P]
             L.ref_store_path.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p, C.c_int64]
             L.ref_assemble.argtypes = [C.c_void_p, U64P, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]
             L.ref_ctx_destroy.argtypes = [C.c_void_p]
@@ -422,6 +423,15 @@ class RefEngine:
         out = C.c_uint64()
         Ref.check(Ref.lib().ref_ingest(self.h, ptr(payload, I32P), len(payload), C.byref(out)))
         return out.value
+
+    def bench_ingest(self, doc_grid, seed: int) -> list:
+        """bench.cpp ingest_synthetic: the reference's bench corpus, chunk ids in ingest order."""
+        grid = np.ascontiguousarray(doc_grid, np.int64)
+        out = np.zeros(4096, np.uint64)
+        n = C.c_int64()
+        Ref.check(Ref.lib().ref_bench_ingest(self.h, ptr(grid, I64P), len(grid), seed, ptr(out, U64P), len(out),
+                                             C.byref(n)))
+        return [int(x) for x in out[:n.value]]
 
     def store_path(self, chunk_id: int) -> str:
         buf = C.create_string_buffer(4096)

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "turbokv/attention.hpp"
+#include "turbokv/bench.hpp"
 #include "turbokv/costmodel.hpp"
 #include "turbokv/errors.hpp"
 #include "turbokv/model.hpp"
@@ -197,6 +198,19 @@ int ref_engine_create(const RefConfig* c, uint64_t seed, const char* store_root,
 void ref_engine_destroy(void* e) { delete static_cast<RefEngine*>(e); }
 
 uint64_t ref_engine_fingerprint(void* e) { return static_cast<RefEngine*>(e)->engine->fingerprint(); }
+
+// bench.cpp ingest_synthetic (the reference's own bench corpus): chunk ids in ingest order
+int ref_bench_ingest(void* e, const int64_t* grid, int64_t n_grid, uint64_t seed, uint64_t* ids_out, int64_t cap,
+                     int64_t* n_out) {
+    return guard([&] {
+        BenchConfig cfg;
+        cfg.doc_grid.assign(grid, grid + n_grid);
+        cfg.seed = seed;
+        const std::vector<uint64_t> ids = ingest_synthetic(*static_cast<RefEngine*>(e)->engine, cfg);
+        *n_out = (int64_t)ids.size();
+        for (size_t i = 0; i < ids.size() && (int64_t)i < cap; ++i) ids_out[i] = ids[i];
+    });
+}
 
 int ref_ingest(void* e, const int32_t* payload, int64_t n, uint64_t* id_out) {
     return guard([&] {

@@ -1,0 +1,84 @@
+"""The reference's bench API mirror (paper_2410_07590_b200/bench_api.py vs proj/src/bench.cpp).
+
+CPU: the bench corpus is the reference's own (chunk ids equal to those of the UNMODIFIED reference's
+ingest_synthetic), the CSV/summary formats and the validation errors. GPU: run_bench on exact Qwen2-7B dims
+(2 layers) -- one row per (grid point, path, rep), FlopCounter totals equal to the reference cost model, and the
+reference acceptance criterion (acceptance_main.cpp:296-329): speedup monotone over the grid, >= 3x at 4096.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2410_07590_b200 import bench_api as B
+from paper_2410_07590_b200 import turbokv as T
+
+
+def test_splitmix_stream_matches_reference_at():
+    rng = B.SplitMix64(42)
+    assert [rng.next() for _ in range(5)] == [O.splitmix_at(42, i) for i in range(5)]
+
+
+@pytest.mark.parametrize("grid,seed", [([64, 192], 42), ([128, 512, 320], 7)])
+def test_corpus_chunk_ids_equal_reference_ingest_synthetic(tmp_path, grid, seed):
+    payloads = B.synthetic_payloads(B.BenchConfig(doc_grid=grid, seed=seed))
+    assert len(payloads) == max(grid) // 64 and all(len(p) == 62 for p in payloads)
+    port = O.Port(O.TOY, 42)
+    ours = [port.chunk_id(O.frame(p)) for p in payloads]
+    if not O.Ref.available():
+        pytest.skip("reference sources absent (GPU box)")
+    ref = O.RefEngine(O.TOY, 42, str(tmp_path / "store"))
+    try:
+        assert ours == ref.bench_ingest(grid, seed)
+    finally:
+        ref.close()
+
+
+def test_query_is_seeded_letters():
+    q = B.bench_query(B.BenchConfig(doc_grid=[64], query_tokens=64, seed=42))
+    assert len(q) == 64 and ((q >= 97) & (q <= 122)).all()
+    assert np.array_equal(q, B.bench_query(B.BenchConfig(doc_grid=[128], query_tokens=64, seed=42)))
+
+
+def test_csv_and_summary_formats():
+    rows = [B.BenchRow(64, 8, "turbo-reordered", 0, 12.3456789, 100), B.BenchRow(64, 8, "turbo-reordered", 1, 0.5, 100),
+            B.BenchRow(64, 8, "naive-independent", 0, 1234567.0, 900),
+            B.BenchRow(64, 8, "naive-independent", 1, 3.0, 900)]
+    csv = B.bench_csv(rows).splitlines()
+    assert csv[0] == "doc_tokens,query_tokens,path,rep,ttft_ms,measured_flops"
+    assert csv[1:] == ["64,8,turbo-reordered,0,12.3457,100", "64,8,turbo-reordered,1,0.5,100",
+                       "64,8,naive-independent,0,1.23457e+06,900", "64,8,naive-independent,1,3,900"]
+    (s,) = B.summarize(rows)
+    assert s.doc_tokens == 64 and s.turbo_median_ms == pytest.approx((12.3456789 + 0.5) / 2)
+    assert s.naive_median_ms == pytest.approx((1234567.0 + 3.0) / 2)
+    assert s.speedup == pytest.approx(s.naive_median_ms / s.turbo_median_ms)
+    with pytest.raises(T.DomainError):
+        B.summarize(rows[:2])
+
+
+@pytest.mark.parametrize("cfg", [B.BenchConfig(doc_grid=[]), B.BenchConfig(doc_grid=[63]),
+                                 B.BenchConfig(doc_grid=[0])])
+def test_grid_validation(cfg):
+    with pytest.raises(T.DomainError):
+        B.synthetic_payloads(cfg)
+
+
+@pytest.mark.gpu
+def test_run_bench_qwen_dims_rows_flops_and_acceptance():
+    cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
+    eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=1 << 14)
+    for bad in (B.BenchConfig(doc_grid=[64], reps=0), B.BenchConfig(doc_grid=[64], query_tokens=0)):
+        with pytest.raises(T.DomainError):
+            B.run_bench(eng, bad)
+    config = B.BenchConfig(doc_grid=[512, 1024, 2048, 4096], query_tokens=64, reps=3, seed=42)
+    rows = B.run_bench(eng, config)
+    assert len(rows) == 4 * 2 * 3
+    oc = O.qwen_layers(2)
+    for r in rows:
+        n = r.doc_tokens + r.query_tokens
+        want = O.Port.flops_total(oc, r.query_tokens, n) if r.path == "turbo-reordered" else O.Port.flops_total(oc, n, n)
+        assert r.measured_flops == want
+    summary = B.summarize(rows)
+    speedups = [s.speedup for s in summary]
+    assert speedups == sorted(speedups), f"speedup not monotone over the grid: {speedups}"
+    assert summary[-1].doc_tokens == 4096 and summary[-1].turbo_median_ms * 3.0 <= summary[-1].naive_median_ms
+    eng.close()
