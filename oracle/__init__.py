@@ -330,6 +330,8 @@ class Ref:
             L.ref_engine_fingerprint.restype = C.c_uint64
             L.ref_engine_fingerprint.argtypes = [C.c_void_p]
             L.ref_ingest.argtypes = [C.c_void_p, I32P, C.c_int64, U64P]
+            L.ref_answer.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.c_int, C.c_int64, U64P, C.c_int64, I64P,
+                                     I32P, C.c_int64, I64P, U64P]
             L.ref_bench_ingest.argtypes = [C.c_void_p, I64P, C.c_int64, C.c_uint64, U64P, C.c_int64, I64P]
             L.ref_store_path.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p, C.c_int64]
             L.ref_assemble.argtypes = [C.c_void_p, U64P, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]
@@ -423,6 +425,18 @@ class RefEngine:
         out = C.c_uint64()
         Ref.check(Ref.lib().ref_ingest(self.h, ptr(payload, I32P), len(payload), C.byref(out)))
         return out.value
+
+    def answer(self, question: str, k: int, mode: int, max_new: int) -> dict:
+        """Engine::answer: retrieved ids, tokens, counters."""
+        ids = np.zeros(256, np.uint64)
+        toks = np.zeros(max(max_new, 1), np.int32)
+        st = np.zeros(5, np.uint64)
+        ni, nt = C.c_int64(), C.c_int64()
+        Ref.check(Ref.lib().ref_answer(self.h, question.encode(), k, mode, max_new, ptr(ids, U64P), len(ids),
+                                       C.byref(ni), ptr(toks, I32P), len(toks), C.byref(nt), ptr(st, U64P)))
+        return {"retrieved": [int(x) for x in ids[:ni.value]], "tokens": [int(x) for x in toks[:nt.value]],
+                "prefill_flops": int(st[0]), "modeled_prefill_flops": int(st[1]), "decode_flops": int(st[2]),
+                "context_tokens": int(st[3]), "query_tokens": int(st[4])}
 
     def bench_ingest(self, doc_grid, seed: int) -> list:
         """bench.cpp ingest_synthetic: the reference's bench corpus, chunk ids in ingest order."""

@@ -199,6 +199,24 @@ void ref_engine_destroy(void* e) { delete static_cast<RefEngine*>(e); }
 
 uint64_t ref_engine_fingerprint(void* e) { return static_cast<RefEngine*>(e)->engine->fingerprint(); }
 
+// Engine::answer (pipeline.cpp:247-308): retrieved ids, answer tokens and the counters
+// stats = {prefill_flops, modeled_prefill_flops, decode_flops, context_tokens, query_tokens}
+int ref_answer(void* e, const char* question, int64_t k, int mode, int64_t max_new, uint64_t* ids_out, int64_t ids_cap,
+               int64_t* n_ids, int32_t* tokens_out, int64_t tok_cap, int64_t* n_tok, uint64_t* stats) {
+    return guard([&] {
+        const AnswerResult r = static_cast<RefEngine*>(e)->engine->answer(question, k, static_cast<PathMode>(mode), max_new);
+        *n_ids = (int64_t)r.retrieved.size();
+        for (size_t i = 0; i < r.retrieved.size() && (int64_t)i < ids_cap; ++i) ids_out[i] = r.retrieved[i];
+        *n_tok = (int64_t)r.tokens.size();
+        for (size_t i = 0; i < r.tokens.size() && (int64_t)i < tok_cap; ++i) tokens_out[i] = r.tokens[i];
+        stats[0] = r.prefill_flops;
+        stats[1] = r.modeled_prefill_flops;
+        stats[2] = r.decode_flops;
+        stats[3] = (uint64_t)r.context_tokens;
+        stats[4] = (uint64_t)r.query_tokens;
+    });
+}
+
 // bench.cpp ingest_synthetic (the reference's own bench corpus): chunk ids in ingest order
 int ref_bench_ingest(void* e, const int64_t* grid, int64_t n_grid, uint64_t seed, uint64_t* ids_out, int64_t cap,
                      int64_t* n_out) {

@@ -1,0 +1,162 @@
+"""Engine::answer (src/pipeline.cpp:247-308) and the Appendix-C cost model (src/costmodel.cpp:11-83) over the B200
+engine: the reference's top-level caller of the hot path (retrieval -> KV injection or full-concat prefill ->
+first-token logits -> greedy decode), with the same result fields (include/turbokv/pipeline.hpp:42-55).
+
+Retrieval runs on the GPU index (cosine top-k, ranking bit-identical to RetrievalIndex::top_k), the turbo
+window covers assemble (KV gather + RoPE) and the query prefill, the naive window the full-concat prefill with
+the chunk tokens in hand; decode FLOPs are counted per generated token as forward_tokens' FlopCounter does
+(add_forward with one new token over the grown context).
+"""
+from __future__ import annotations
+
+import enum
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import turbokv as T
+
+PREAMBLE = ("Answer the question using only the documents provided. "
+            "If the documents do not contain the answer, refuse to answer.\n"
+            "Question: ")  # pipeline.cpp:20-23
+DOC_START, DOC_END, EOS = 256, 257, 258
+
+
+class PathMode(enum.IntEnum):
+    """pipeline.hpp:25"""
+    TurboReordered = 0
+    TurboComposite = 1
+    NaiveCausal = 2
+    NaiveIndependent = 3
+
+
+@dataclass
+class FlopsReport:
+    """costmodel.hpp FlopsReport"""
+    c_qkv: int
+    c_attn: int
+    c_o: int
+    c_mlp: int
+    n_input: int
+    n_context: int
+    batch: int
+    total: int
+
+
+def flops(config: T.ModelConfig, n_input: int, n_context: int, batch: int = 1) -> FlopsReport:
+    """costmodel.cpp:28-46 (Appendix C): total = batch * n_input * L * (c_qkv + c_attn(n_context) + c_o + c_mlp)."""
+    if n_input < 1 or n_context < 1 or batch < 1:
+        raise T.DomainError("flops: n_input, n_context and batch must be >= 1")
+    if n_context < n_input:
+        raise T.DomainError("flops: n_context < n_input")
+    c = config
+    qkv = 2 * c.hidden_size * (c.head_num + 2 * c.kv_head_num) * c.head_size
+    attn = 2 * c.head_num * c.head_size * n_context
+    o = 2 * c.hidden_size * c.hidden_size
+    mlp = 2 * 3 * c.hidden_size * c.intermediate_size
+    return FlopsReport(qkv, attn, o, mlp, n_input, n_context, batch, batch * n_input * c.layer_num * (qkv + attn + o + mlp))
+
+
+@dataclass
+class FlopsComparison:
+    naive: FlopsReport
+    turbo: FlopsReport
+    reduction_percent: float
+
+
+def compare(config: T.ModelConfig, chunk_tokens: int, query_tokens: int, batch: int = 1) -> FlopsComparison:
+    """costmodel.cpp:48-62"""
+    if chunk_tokens < 0 or query_tokens < 1:
+        raise T.DomainError("compare: need chunk_tokens >= 0 and query_tokens >= 1")
+    total = chunk_tokens + query_tokens
+    naive, turbo = flops(config, total, total, batch), flops(config, query_tokens, total, batch)
+    return FlopsComparison(naive, turbo, 100.0 * (1.0 - turbo.total / naive.total))
+
+
+@dataclass
+class AnswerResult:
+    """pipeline.hpp:42-55"""
+    text: str = ""
+    tokens: list = field(default_factory=list)
+    retrieved: list = field(default_factory=list)
+    retrieval_ms: float = 0.0
+    cache_load_ms: float = 0.0  # inside ttft_ms for turbo paths
+    ttft_ms: float = 0.0        # inputs ready -> first-token logits
+    decode_ms: float = 0.0
+    prefill_flops: int = 0
+    modeled_prefill_flops: int = 0
+    decode_flops: int = 0
+    context_tokens: int = 0     # chunk tokens attended over
+    query_tokens: int = 0
+
+
+def encode(text: str) -> np.ndarray:
+    return np.frombuffer(text.encode("utf-8"), np.uint8).astype(np.int32)
+
+
+def decode(tokens) -> str:
+    """tokenizer.cpp:17-34 (bytes -> text; invalid UTF-8 rendered with U+FFFD, as the JSON report does)."""
+    out = bytearray()
+    for t in tokens:
+        if 0 <= t < 256:
+            out.append(t)
+        elif t == DOC_START:
+            out += b"<|doc_start|>"
+        elif t == DOC_END:
+            out += b"<|doc_end|>"
+        elif t == EOS:
+            pass
+        else:
+            raise T.DomainError(f"decode: unknown token id {t}")
+    return out.decode("utf-8", errors="replace")
+
+
+def build_query_tokens(question: str) -> np.ndarray:
+    """pipeline.cpp:243-245"""
+    return encode(PREAMBLE + question + "\nAnswer:")
+
+
+def answer(engine: T.Engine, question: str, k: int, mode: PathMode, max_new: int) -> AnswerResult:
+    """pipeline.cpp:247-308"""
+    if not question:
+        raise T.DomainError("answer: empty question")
+    if engine.index_size() == 0:
+        raise T.NoContextError("nothing has been ingested; refusing to answer")
+    cfg = engine.config
+    r = AnswerResult()
+    t0 = time.perf_counter()
+    ids, _ = engine.top_k(encode(question), k)
+    r.retrieved = [int(i) for i in ids]
+    r.retrieval_ms = (time.perf_counter() - t0) * 1e3
+    q = build_query_tokens(question)
+    r.query_tokens = len(q)
+    r.context_tokens = sum(engine.store_chunk_tokens(i) for i in r.retrieved)
+    total = r.context_tokens + r.query_tokens
+    counter = T.FlopCounter()
+    if mode in (PathMode.TurboReordered, PathMode.TurboComposite):
+        pos = T.PositionMode.Reordered if mode == PathMode.TurboReordered else T.PositionMode.Composite
+        t0 = time.perf_counter()
+        ctx = engine.assemble(r.retrieved, pos)
+        r.cache_load_ms = (time.perf_counter() - t0) * 1e3
+        engine.prefill_query(ctx, q, counter)
+        r.ttft_ms = (time.perf_counter() - t0) * 1e3
+        r.modeled_prefill_flops = flops(cfg, r.query_tokens, total).total
+    else:
+        mask = T.MaskMode.Causal if mode == PathMode.NaiveCausal else T.MaskMode.Independent
+        chunks = [engine.chunk_framed_tokens(i) for i in r.retrieved]
+        t0 = time.perf_counter()
+        ctx = engine.naive_prefill(chunks, q, mask, counter)
+        r.ttft_ms = (time.perf_counter() - t0) * 1e3
+        r.modeled_prefill_flops = flops(cfg, total, total).total
+    r.prefill_flops = counter.total()
+    try:
+        t0 = time.perf_counter()
+        r.tokens = engine.greedy_decode(ctx, max_new)
+        r.decode_ms = (time.perf_counter() - t0) * 1e3
+    finally:
+        ctx.close()
+    # forward_tokens charges add_forward(1 new token, past + 1) per generated token (model.cpp:270, 274-303)
+    r.decode_flops = sum(flops(cfg, 1, total + i + 1).total for i in range(len(r.tokens)))
+    r.text = decode(r.tokens)
+    return r

@@ -374,6 +374,7 @@ class Engine:
                  exact_fingerprint: int = -1, flags: int = 0, host_spill_tokens: int = 0):
         self.config = config
         self.seed = seed
+        self._framed = {}  # chunk id -> framed tokens (host copy for the naive path / answer)
         o = _Opts()
         lib().tkv_engine_opts_default(C.byref(o))
         o.dtype = int(Dtype.F32 if str(dtype).lower() in ("f32", "fp32", "float32", "dtype.f32") or dtype == Dtype.F32
@@ -419,7 +420,10 @@ class Engine:
             stats.chunks += st.chunks
             stats.new_chunks += st.new_chunks
             stats.bytes_written += st.bytes_written
-        return [int(i) for i in ids[:len(payloads)]]
+        out = [int(i) for i in ids[:len(payloads)]]
+        for cid, p in zip(out, payloads):
+            self._framed.setdefault(cid, np.concatenate([[256], p, [257]]).astype(np.int32))
+        return out
 
     def ingest_chunk_payload(self, doc_id: str, payload, stats: IngestStats | None = None) -> int:
         return self.ingest_chunks([payload], stats)[0]
@@ -466,11 +470,24 @@ class Engine:
 
     def store_evict(self, chunk_id: int) -> None:
         _check(lib().tkv_store_evict(self._h, chunk_id))
+        self._framed.pop(chunk_id, None)
 
     def store_contains(self, chunk_id: int) -> bool:
         out = C.c_int()
         _check(lib().tkv_store_contains(self._h, chunk_id, C.byref(out)))
         return bool(out.value)
+
+    def store_chunk_tokens(self, chunk_id: int) -> int:
+        n = C.c_int64()
+        _check(lib().tkv_store_chunk_tokens(self._h, chunk_id, C.byref(n)))
+        return n.value
+
+    def chunk_framed_tokens(self, chunk_id: int) -> np.ndarray:
+        """The framed tokens a chunk was ingested from (ChunkRecord::tokens, retrieval.hpp:25-30): kept host-side
+        for the full-concat comparison path."""
+        if chunk_id not in self._framed:
+            raise NotFoundError(f"chunk {chunk_id:016x}: tokens not held by this engine")
+        return self._framed[chunk_id]
 
     def store_read(self, chunk_id: int, layer: int, which: str = "k") -> np.ndarray:
         n = C.c_int64()

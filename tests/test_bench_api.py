@@ -82,3 +82,46 @@ def test_run_bench_qwen_dims_rows_flops_and_acceptance():
     assert speedups == sorted(speedups), f"speedup not monotone over the grid: {speedups}"
     assert summary[-1].doc_tokens == 4096 and summary[-1].turbo_median_ms * 3.0 <= summary[-1].naive_median_ms
     eng.close()
+
+
+def test_flops_model_matches_reference_compare():
+    from paper_2410_07590_b200 import pipeline_api as P
+    cfg = T.ModelConfig.qwen2_7b_like()
+    cmp = P.compare(cfg, 8192, 128)
+    assert cmp.naive.total == O.Port.flops_total(O.QWEN2_7B, 8320, 8320)
+    assert cmp.turbo.total == O.Port.flops_total(O.QWEN2_7B, 128, 8320)
+    assert abs(cmp.reduction_percent - 98.4615) < 1e-3  # proj/README.md:137-138
+    with pytest.raises(T.DomainError):
+        P.flops(cfg, 8, 4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_answer_matches_reference_engine(tmp_path, mode):
+    """Engine::answer end to end (retrieval on the GPU index, KV injection or full concat, greedy decode) on the
+    toy model in f32: same retrieved chunk ids, same answer tokens, same prefill / modeled / decode FLOP counts."""
+    from paper_2410_07590_b200 import pipeline_api as P
+    if not O.Ref.available():
+        pytest.skip("reference sources absent (GPU box)")
+    pays = [O.random_text_tokens(3000 + i, 126) for i in range(6)]
+    eng = T.Engine(T.ModelConfig.toy(), 42, dtype="f32", store_capacity_tokens=4096)
+    eng.ingest_chunks(pays)
+    ref = O.RefEngine(O.TOY, 42, str(tmp_path / "store"))
+    try:
+        for p in pays:
+            ref.ingest(p)
+        question = "which document mentions the river"
+        want = ref.answer(question, 3, mode, 8)
+        got = P.answer(eng, question, 3, P.PathMode(mode), 8)
+        assert got.retrieved == want["retrieved"]
+        assert got.tokens == want["tokens"]
+        for key in ("prefill_flops", "modeled_prefill_flops", "decode_flops", "context_tokens", "query_tokens"):
+            assert getattr(got, key) == want[key], key
+        assert got.prefill_flops == got.modeled_prefill_flops
+        assert got.text == P.decode(want["tokens"]) and got.ttft_ms > 0
+    finally:
+        ref.close()
+        eng.close()
+    with pytest.raises(T.DomainError):
+        P.answer(T.Engine(T.ModelConfig.toy(), 42, dtype="f32", store_capacity_tokens=1024), "", 1,
+                 P.PathMode.TurboReordered, 1)
