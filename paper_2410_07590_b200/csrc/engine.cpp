@@ -474,6 +474,23 @@ struct tkv_engine {
 
     bool use_tc() const { return dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_GEMM); }
 
+    // fused gate/up + down launch (gemm_tc.cu:gemm_mlp_kernel): <= 128 rows, interleaved W_gu whose GEMM runs
+    // without split-K, dims multiples of the 64-wide k-block
+    int fused_mlp = 0;  // TKV_FUSED_MLP=1 (opt-in: measured slower)
+    DevMem mlp_flags, mlp_ctl;
+    bool fused_mlp_ok(int rows) {
+        if (!fused_mlp || !use_tc() || !gu_interleaved || rows > 128 || hid % 64 || I % 64) return false;
+        if (pick_splits(rows, (int)(2 * I), (int)hid, true) != 1) return false;
+        if (!mlp_flags.p) {
+            mlp_flags.ensure((size_t)(2 * I / 128) * sizeof(unsigned));
+            mlp_ctl.ensure(2 * sizeof(unsigned));
+            TKV_CUDA(cudaMemset(mlp_flags.p, 0, (size_t)(2 * I / 128) * sizeof(unsigned)));
+            const unsigned init[2] = {1u, 0u};
+            TKV_CUDA(cudaMemcpy(mlp_ctl.p, init, sizeof init, cudaMemcpyHostToDevice));
+        }
+        return true;
+    }
+
     // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits. With swiglu_act, a tcgen05 GEMM whose
     // K range fits one CTA writes silu(gate)*up straight to swiglu_act and returns 0.
     int gemm(const void* A, int lda, const void* W, int M, int N, int K, void* swiglu_act = nullptr) {
@@ -701,15 +718,25 @@ void tkv_engine::forward(const Fwd& f) {
                             err.as<int>(), stream);
         }
         // --- MLP block: gate|up fused into one GEMM, SwiGLU (with the folded mlp_norm scale) in its epilogue ---
-        next(w_down[l], rows, (int)hid, (int)I);
-        s = gemm(xb.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
-        if (s > 0) {
-            Scope sc(this, PC_EPI, 1);
-            launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, ssp.as<float>(), nb, (int)hid, eps, dt, stream,
-                          gu_interleaved);
+        if (fused_mlp_ok(rows)) {
+            // gate/up + SwiGLU and the down GEMM in ONE persistent launch (the down weights stream during the
+            // gate/up tail; act k-blocks handed over through readiness flags)
+            const int s2 = pick_splits(rows, (int)hid, (int)I, true);
+            partial.ensure((size_t)s2 * rows * hid * sizeof(float));
+            Scope sc(this, PC_GEMM, 1);
+            s = launch_gemm_mlp(xb.p, (int)hid, w_gu[l], act.p, w_down[l], rows, (int)hid, (int)I, partial.as<float>(),
+                                s2, mlp_flags.as<unsigned>(), mlp_ctl.as<unsigned>(), ssp.as<float>(), nb, eps, stream);
+        } else {
+            next(w_down[l], rows, (int)hid, (int)I);
+            s = gemm(xb.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
+            if (s > 0) {
+                Scope sc(this, PC_EPI, 1);
+                launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, ssp.as<float>(), nb, (int)hid, eps, dt,
+                              stream, gu_interleaved);
+            }
+            if (l + 1 < L) next(w_qkv[l + 1], T, (int)nqkv, (int)hid);
+            s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
         }
-        if (l + 1 < L) next(w_qkv[l + 1], T, (int)nqkv, (int)hid);
-        s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
         if (!(skip_mask & 2)) {
             // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
             Scope sc(this, PC_EPI, 1);
@@ -1314,6 +1341,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         if (const char* np = getenv("TKV_GEMM_NEXT_PF")) set_gemm_next_pf(atoi(np));
         if (const char* mp = getenv("TKV_GEMM_NSMP")) set_gemm_nsmp(atoi(mp));
         if (const char* gc = getenv("TKV_GEMM_CLUSTER")) set_gemm_cluster(atoi(gc));
+        if (const char* fm = getenv("TKV_FUSED_MLP")) e->fused_mlp = atoi(fm);
         if (const char* se = getenv("TKV_GEMM_SKIP_EPI")) set_gemm_skip_epi(atoi(se));
         if (const char* ra = getenv("TKV_GEMM_RASTER")) set_gemm_raster(atoi(ra));
         if (const char* gm = getenv("TKV_GEMM_GROUP_MB")) set_gemm_raster(1, atoi(gm));

@@ -497,6 +497,283 @@ __global__ void __launch_bounds__(THREADS_P)
     }
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// Fused MLP for <= 128 tokens (swap-AB): ONE persistent launch runs the gate/up GEMM with its SwiGLU epilogue
+// (phase 1, one 128-row tile of interleaved W_gu per unit, whole K) and then the down GEMM (phase 2, split-K
+// partials). The smem ring and the TMEM accumulators flow from phase 1 into phase 2, so the down weights start
+// streaming while the gate/up tail drains instead of after a kernel boundary. Phase-1 tile t produces act
+// columns [64 t, 64 t + 64) = down k-block t; its epilogue publishes flags[t] = epoch (release, gpu scope) and the
+// phase-2 producer acquires it before that k-block's activation TMA. The epoch lives in device memory (read after
+// griddepcontrol.wait, advanced by the last CTA to finish) so CUDA-graph replays never see a stale match. Every CTA finishes its phase-1 units before
+// its phase-2 units and all CTAs are co-resident (grid <= resident capacity; a dependent grid can only launch
+// once all of this grid's CTAs have started), so the waits cannot deadlock; they trap after ~2 s regardless.
+struct MlpArgs {
+    int M, ntok, stages;
+    uint32_t a_bytes, acc_cols, tmem_cols, scratch_off;
+    int units1, kb1;                    // phase 1: gate/up tiles (= act k-blocks), k-blocks of hidden
+    int n2_tiles, kb2, kb2_per_split, units2, N2;  // phase 2: down
+    __nv_bfloat16* act;                 // [M][inter]
+    float* partial;                     // [splits2][M][N2]
+    const float* ssp;
+    int nb, hidden;
+    float eps;
+    unsigned* flags;
+    unsigned* ctl;  // [0] = this launch's epoch (read after the PDL wait, so graph replays see a fresh one),
+                    // [1] = finished-CTA count; the last CTA to finish advances the epoch
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// every flag of [f, f + n) == epoch: all loads of a poll in flight at once (one round trip per poll, not per flag)
+__device__ __forceinline__ void wait_flags(const unsigned* f, int n, unsigned epoch) {
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0;; ++spin) {
+        bool ok = true;
+        for (int i0 = 0; i0 < n; i0 += 16) {
+            unsigned v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = i0 + i < n ? ld_acquire_u32(f + i0 + i) : epoch;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) ok &= v[i] == epoch;
+        }
+        if (ok) break;
+        if ((spin & 63) == 63) {
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 2000000000ull) __trap();
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void wait_flag(const unsigned* f, unsigned epoch) {
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0; ld_acquire_u32(f) != epoch; ++spin) {
+        if ((spin & 255) == 255) {
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 2000000000ull) __trap();
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA (async proxy) read follows
+}
+
+__global__ void __launch_bounds__(THREADS_P)
+    gemm_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWgu,
+                    const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmWd, MlpArgs m) {
+    pdl_launch();
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t stage_bytes = TILE_W + m.a_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + m.stages * stage_bytes);
+    uint64_t* empty = full + m.stages;
+    uint64_t* tfull = empty + m.stages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < m.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(m.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    // this CTA's work list: phase-1 units b, b + G, ... then phase-2 units b, b + G, ...
+    const int G = gridDim.x, b0 = blockIdx.x;
+    const int n1 = b0 < m.units1 ? (m.units1 - 1 - b0) / G + 1 : 0;
+    const int n2 = b0 < m.units2 ? (m.units2 - 1 - b0) / G + 1 : 0;
+    // unit j of this CTA -> (phase, weight tile, first k-block, k-blocks)
+    auto unit = [&](int j, int& ph, int& nt, int& k0, int& nkb, int& u) {
+        if (j < n1) {
+            ph = 1;
+            u = b0 + j * G;
+            nt = u;
+            k0 = 0;
+            nkb = m.kb1;
+        } else {
+            ph = 2;
+            u = b0 + (j - n1) * G;
+            const int z = u / m.n2_tiles;
+            nt = u - z * m.n2_tiles;
+            k0 = z * m.kb2_per_split;
+            nkb = min(m.kb2, k0 + m.kb2_per_split) - k0;
+        }
+    };
+    auto kblk = [&](int k0, int nkb, int i, int u) { return k0 + (i + (u * 37) % nkb) % nkb; };
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer ----------------
+            const uint64_t wpol = policy_evict_first();
+            int it = 0;
+            bool waited = false;
+            unsigned epoch = 0;
+            for (int j = 0; j < n1 + n2; ++j) {
+                int ph, nt, k0, nkb, u;
+                unit(j, ph, nt, k0, nkb, u);
+                const CUtensorMap* tw = ph == 1 ? &tmWgu : &tmWd;
+                const CUtensorMap* ta = ph == 1 ? &tmX : &tmAct;
+                // weights of up to `stages` k-blocks go out before their activations: before the PDL wait in
+                // phase 1, before the readiness flags in phase 2
+                int i = 0;
+                while (i < nkb) {
+                    // batched (weights first) only for the first ring of each phase; interleaved afterwards
+                    const bool lead = i == 0 && (j == 0 || j == n1);
+                    const int batch = lead ? min(nkb - i, m.stages) : 1;
+                    for (int q = 0; q < batch; ++q) {
+                        const int s = (it + q) % m.stages;
+                        mbar_wait(&empty[s], ((uint32_t)((it + q) / m.stages) & 1u) ^ 1u);
+                        mbar_expect_tx(&full[s], stage_bytes);
+                        tma_load_2d_hint(smem + s * stage_bytes, tw, &full[s], kblk(k0, nkb, i + q, u) * BK, nt * 128, wpol);
+                    }
+                    if (!waited) {
+                        pdl_wait();
+                        epoch = *(volatile unsigned*)m.ctl;
+                        waited = true;
+                    }
+                    if (ph == 2 && i == 0) wait_flags(m.flags + k0, nkb, epoch);  // the unit's whole act k-range
+                    for (int q = 0; q < batch; ++q) {
+                        const int s = (it + q) % m.stages;
+                        const int kb = kblk(k0, nkb, i + q, u);
+                        tma_load_2d(smem + s * stage_bytes + TILE_W, ta, &full[s], kb * BK, 0);
+                    }
+                    it += batch;
+                    i += batch;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer ----------------
+            const uint32_t id = idesc(128, m.ntok);
+            int it = 0;
+            for (int j = 0; j < n1 + n2; ++j) {
+                int ph, nt, k0, nkb, u;
+                unit(j, ph, nt, k0, nkb, u);
+                const int b = j & 1;
+                mbar_wait(&tempty[b], ((uint32_t)(j >> 1) & 1u) ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t acc = tmem + (uint32_t)b * m.acc_cols;
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % m.stages;
+                    mbar_wait(&full[s], (uint32_t)(it / m.stages) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t w = smem_u32(smem + s * stage_bytes), a = w + TILE_W;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        umma_f16(acc, desc_k(w + k * 32), desc_k(a + k * 32), id, (i | k) != 0);
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[b]);
+            }
+        }
+    } else {
+        // ---------------- epilogue warps 2-5: TMEM lane group = warp % 4 ----------------
+        pdl_wait();
+        const unsigned epoch = *(volatile unsigned*)m.ctl;
+        const int lg = warp & 3;
+        const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+        const int et = threadIdx.x - 64;
+        const int inter = m.kb2 * BK;
+        float* up = reinterpret_cast<float*>(smem + m.scratch_off);  // [64][ntok + 1]
+        const int ld = m.ntok + 1;
+        float* tok_scale = up + 64 * ld;
+        for (int j = 0; j < n1 + n2; ++j) {
+            int ph, nt, k0, nkb, u;
+            unit(j, ph, nt, k0, nkb, u);
+            const int b = j & 1;
+            mbar_wait(&tfull[b], (uint32_t)(j >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t acc = tmem + lane_base + (uint32_t)b * m.acc_cols;
+            if (ph == 1) {  // SwiGLU: tile rows 0-63 gate, 64-127 the matching up rows (interleaved W_gu)
+                if (et < m.ntok) tok_scale[et] = et < m.M ? row_scale(m.ssp, m.nb, et, m.hidden, m.eps) : 0.f;
+                if (lg >= 2) {
+#pragma unroll 1
+                    for (int c = 0; c < m.ntok; c += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(acc + (uint32_t)c, r);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) up[((lg - 2) * 32 + lane) * ld + c + q] = __uint_as_float(r[q]);
+                    }
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (lg < 2) {
+                    const int i = nt * 64 + lg * 32 + lane;
+#pragma unroll 1
+                    for (int c = 0; c < m.ntok; c += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(acc + (uint32_t)c, r);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            const int t = c + q;
+                            if (t < m.M && i < inter) {
+                                const float sc = tok_scale[t];
+                                m.act[(int64_t)t * inter + i] =
+                                    __float2bfloat16_rn(silu(sc * __uint_as_float(r[q])) * (sc * up[(lg * 32 + lane) * ld + t]));
+                            }
+                        }
+                    }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by TMA (async proxy)
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");  // tile's act written; scratch reusable
+                if (et == 0) {
+                    __threadfence();
+                    st_release_u32(m.flags + nt, epoch);
+                }
+            } else {  // down: split-K partial plane z, TMEM lane = weight row n, column = token
+                const int z = u / m.n2_tiles;
+                const int n = nt * 128 + lg * 32 + lane;
+                float* out = m.partial + (int64_t)z * m.M * m.N2;
+#pragma unroll 1
+                for (int c = 0; c < m.ntok; c += 16) {
+                    uint32_t r[16];
+                    tmem_ld16(acc + (uint32_t)c, r);
+                    if (n < m.N2) {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q)
+                            if (c + q < m.M) out[(int64_t)(c + q) * m.N2 + n] = __uint_as_float(r[q]);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {  // every CTA has read the epoch by now; the last one advances it for the next launch
+        __threadfence();
+        if (atomicAdd(m.ctl + 1, 1u) == gridDim.x - 1) {
+            m.ctl[1] = 0;
+            atomicAdd(m.ctl, 1u);
+            __threadfence();
+        }
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(m.tmem_cols));
+    }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -653,6 +930,66 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
         swap ? launch_t<true, EPI_PARTIAL>(ta, tw, tn, g, grid, smem, s) : launch_t<false, EPI_PARTIAL>(ta, tw, tn, g, grid, smem, s);
     }
     return eff_splits;
+}
+
+
+int launch_gemm_mlp(const void* xb, int lda, const void* w_gu, void* act, const void* w_down, int M, int hidden,
+                    int inter, float* partial, int splits, unsigned* flags, unsigned* ctl, const float* ssp, int nb,
+                    float eps, cudaStream_t s) {
+    if (M > 128) fail(TKV_ERR_CONFIG, "fused MLP: <= 128 tokens only");
+    if (hidden % BK || inter % BK || (2 * inter) % 128) fail(TKV_ERR_CONFIG, "fused MLP: unsupported dims");
+    MlpArgs m{};
+    m.M = M;
+    m.ntok = ((M + 15) / 16) * 16;
+    m.a_bytes = (uint32_t)m.ntok * BK * 2;
+    m.acc_cols = (uint32_t)m.ntok;
+    m.tmem_cols = 32;
+    while (m.tmem_cols < 2 * m.acc_cols) m.tmem_cols <<= 1;
+    const uint32_t scratch = (uint32_t)((64 * (m.ntok + 1) + m.ntok) * 4 + 1023) / 1024 * 1024;
+    const int budget = g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET;
+    m.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
+                                       (uint32_t)(budget - (int)scratch) / (TILE_W + m.a_bytes));
+    if (m.stages < 2) fail(TKV_ERR_CONFIG, "fused MLP: smem budget too small");
+    m.scratch_off = ((uint32_t)m.stages * (TILE_W + m.a_bytes) + 256 + 1023) / 1024 * 1024;
+    m.units1 = 2 * inter / 128;
+    m.kb1 = hidden / BK;
+    m.n2_tiles = (hidden + 127) / 128;
+    m.kb2 = inter / BK;
+    m.kb2_per_split = (m.kb2 + splits - 1) / splits;
+    const int eff = (m.kb2 + m.kb2_per_split - 1) / m.kb2_per_split;
+    m.units2 = m.n2_tiles * eff;
+    m.N2 = hidden;
+    m.act = (__nv_bfloat16*)act;
+    m.partial = partial;
+    m.ssp = ssp;
+    m.nb = nb;
+    m.hidden = hidden;
+    m.eps = eps;
+    m.flags = flags;
+    m.ctl = ctl;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int cap = sms * gemm_tc_ctas_per_sm(M);  // co-resident CTAs: every phase-2 flag owner is running
+    const int grid = std::min(std::max(m.units1, m.units2), cap);
+    const size_t smem = 1024 + (size_t)m.scratch_off + scratch;
+    TKV_CUDA(cudaFuncSetAttribute(gemm_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TKV_CUDA(cudaFuncSetAttribute(gemm_mlp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    // co-residency from the SM's shared-memory capacity (1 KB reserved per CTA; threads and registers are far
+    // from their limits at 192 threads x <= 64 registers). cudaOccupancyMaxActiveBlocksPerMultiprocessor reports
+    // 1 here for this and the plain GEMM kernel alike, while ncu shows 2 resident, so it is not used.
+    int smem_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const int per_sm = smem_sm / (int)(smem + 1024);
+    if ((int64_t)per_sm * sms < grid)
+        fail(TKV_ERR_CONFIG, "fused MLP: grid of " + std::to_string(grid) + " would not be co-resident");
+    const CUtensorMap tx = make_map(xb, M, hidden, lda, m.ntok);
+    const CUtensorMap twg = make_map(w_gu, 2 * inter, hidden, hidden, 128);
+    const CUtensorMap ta = make_map(act, M, inter, inter, m.ntok);
+    const CUtensorMap twd = make_map(w_down, hidden, inter, inter, 128);
+    launch_k(gemm_mlp_kernel, dim3(grid), dim3(THREADS_P), smem, s, tx, twg, ta, twd, m);
+    TKV_CUDA(cudaGetLastError());
+    return eff;
 }
 
 void set_gemm_next(const void* W, int M, int N, int K, int splits) { g_next = NextGemm{W, M, N, K, splits}; }

@@ -127,6 +127,12 @@ bool gemm_tc_supported(int M, int N, int K, int lda);
 void set_gemm_next(const void* W, int M, int N, int K, int splits);
 void set_gemm_next_pf(int kblocks);
 void set_gemm_nsmp(int mp);
+// Fused MLP (<= 128 tokens): gate/up GEMM + SwiGLU epilogue into act, then the down GEMM's split-K partials, in one
+// persistent launch; flags[2 * inter / 128] readiness words and ctl[2] = {epoch, finished CTAs}, both zeroed
+// once with ctl[0] = 1 before the first launch. Returns the down GEMM's split count.
+int launch_gemm_mlp(const void* xb, int lda, const void* w_gu, void* act, const void* w_down, int M, int hidden,
+                    int inter, float* partial, int splits, unsigned* flags, unsigned* ctl, const float* ssp, int nb,
+                    float eps, cudaStream_t s);
 void set_gemm_cluster(int c);
 void set_gemm_skip_epi(int v);  // timing experiments only: skip the normal-tiling partial stores  // normal tiling: 2 = CTA pairs share each weight tile through TMA multicast
 // normal tiling unit order (0 n-fastest, 1 m-fastest when N > M, 2 m-fastest; group_mb > 0: m-tile groups of
