@@ -200,6 +200,7 @@ struct GemmArgs {
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
 constexpr int THREADS_P = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int XC = 32;          // swapped SwiGLU epilogue: token columns per gate/up exchange pass
 
 __device__ __forceinline__ void unit_coords(const GemmArgs& g, int u, int& nt, int& mt, int& z) {
     const int per = g.n_tiles * g.m_tiles;
@@ -398,40 +399,45 @@ __global__ void __launch_bounds__(THREADS_P)
                         }
                     }
                 } else {
-                    // tile rows 0-63 = gate, 64-127 = the matching up rows (interleaved W_gu layout)
-                    float* up = reinterpret_cast<float*>(smem + g.scratch_off);  // [64][ntok+1]
-                    const int ld = g.ntok + 1;
+                    // tile rows 0-63 = gate, 64-127 = the matching up rows (interleaved W_gu layout); the up rows
+                    // reach the gate warps through a [64][XC + 1] scratch, XC token columns per pass (a small
+                    // scratch leaves the ring one more stage)
+                    float* up = reinterpret_cast<float*>(smem + g.scratch_off);
+                    const int ld = XC + 1;
                     float* tok_scale = up + 64 * ld;  // [ntok]: folded mlp_norm scale per token
                     if (et < g.ntok) tok_scale[et] = m0 + et < g.M ? row_scale(g.ssp, g.nb, m0 + et, g.K, g.eps) : 0.f;
-                    if (lg >= 2) {
+                    const int inter = g.N / 2;
+                    const int i = (n0 / 128) * 64 + lg * 32 + lane;
+                    for (int c0 = 0; c0 < g.ntok; c0 += XC) {
+                        const int c1 = min(g.ntok, c0 + XC);
+                        if (lg >= 2) {
 #pragma unroll 1
-                        for (int c = 0; c < g.ntok; c += 16) {
-                            uint32_t r[16];
-                            tmem_ld16(acc + (uint32_t)c, r);
+                            for (int c = c0; c < c1; c += 16) {
+                                uint32_t r[16];
+                                tmem_ld16(acc + (uint32_t)c, r);
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) up[((lg - 2) * 32 + lane) * ld + c + j] = __uint_as_float(r[j]);
+                                for (int j = 0; j < 16; ++j) up[((lg - 2) * 32 + lane) * ld + c - c0 + j] = __uint_as_float(r[j]);
+                            }
                         }
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (lg < 2) {
-                        const int inter = g.N / 2;
-                        const int i = (n0 / 128) * 64 + lg * 32 + lane;
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (lg < 2) {
 #pragma unroll 1
-                        for (int c = 0; c < g.ntok; c += 16) {
-                            uint32_t r[16];
-                            tmem_ld16(acc + (uint32_t)c, r);
+                            for (int c = c0; c < c1; c += 16) {
+                                uint32_t r[16];
+                                tmem_ld16(acc + (uint32_t)c, r);
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const int m = m0 + c + j;
-                                if (m < g.M && i < inter) {
-                                    const float sc = tok_scale[c + j];
-                                    g.act[(int64_t)m * inter + i] = __float2bfloat16_rn(
-                                        silu(sc * __uint_as_float(r[j])) * (sc * up[(lg * 32 + lane) * ld + c + j]));
+                                for (int j = 0; j < 16; ++j) {
+                                    const int m = m0 + c + j;
+                                    if (m < g.M && i < inter) {
+                                        const float sc = tok_scale[c + j];
+                                        g.act[(int64_t)m * inter + i] = __float2bfloat16_rn(
+                                            silu(sc * __uint_as_float(r[j])) * (sc * up[(lg * 32 + lane) * ld + c - c0 + j]));
+                                    }
                                 }
                             }
                         }
+                        asm volatile("bar.sync 1, 128;" ::: "memory");  // scratch reusable (next pass / unit)
                     }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");  // scratch reusable by the next unit
                 }
             } else {
                 const int m = m0 + mi * 128 + lg * 32 + lane;  // TMEM lane = token row m, column = weight row
@@ -694,8 +700,8 @@ __global__ void __launch_bounds__(THREADS_P)
         const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
         const int et = threadIdx.x - 64;
         const int inter = m.kb2 * BK;
-        float* up = reinterpret_cast<float*>(smem + m.scratch_off);  // [64][ntok + 1]
-        const int ld = m.ntok + 1;
+        float* up = reinterpret_cast<float*>(smem + m.scratch_off);  // [64][XC + 1]
+        const int ld = XC + 1;
         float* tok_scale = up + 64 * ld;
         for (int j = 0; j < n1 + n2; ++j) {
             int ph, nt, k0, nkb, u;
@@ -706,35 +712,38 @@ __global__ void __launch_bounds__(THREADS_P)
             const uint32_t acc = tmem + lane_base + (uint32_t)b * m.acc_cols;
             if (ph == 1) {  // SwiGLU: tile rows 0-63 gate, 64-127 the matching up rows (interleaved W_gu)
                 if (et < m.ntok) tok_scale[et] = et < m.M ? row_scale(m.ssp, m.nb, et, m.hidden, m.eps) : 0.f;
-                if (lg >= 2) {
+                const int i = nt * 64 + lg * 32 + lane;
+                for (int c0 = 0; c0 < m.ntok; c0 += XC) {
+                    const int c1 = min(m.ntok, c0 + XC);
+                    if (lg >= 2) {
 #pragma unroll 1
-                    for (int c = 0; c < m.ntok; c += 16) {
-                        uint32_t r[16];
-                        tmem_ld16(acc + (uint32_t)c, r);
+                        for (int c = c0; c < c1; c += 16) {
+                            uint32_t r[16];
+                            tmem_ld16(acc + (uint32_t)c, r);
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) up[((lg - 2) * 32 + lane) * ld + c + q] = __uint_as_float(r[q]);
-                    }
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (lg < 2) {
-                    const int i = nt * 64 + lg * 32 + lane;
-#pragma unroll 1
-                    for (int c = 0; c < m.ntok; c += 16) {
-                        uint32_t r[16];
-                        tmem_ld16(acc + (uint32_t)c, r);
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) {
-                            const int t = c + q;
-                            if (t < m.M && i < inter) {
-                                const float sc = tok_scale[t];
-                                m.act[(int64_t)t * inter + i] =
-                                    __float2bfloat16_rn(silu(sc * __uint_as_float(r[q])) * (sc * up[(lg * 32 + lane) * ld + t]));
-                            }
+                            for (int q = 0; q < 16; ++q) up[((lg - 2) * 32 + lane) * ld + c - c0 + q] = __uint_as_float(r[q]);
                         }
                     }
-                    asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by TMA (async proxy)
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (lg < 2) {
+#pragma unroll 1
+                        for (int c = c0; c < c1; c += 16) {
+                            uint32_t r[16];
+                            tmem_ld16(acc + (uint32_t)c, r);
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) {
+                                const int t = c + q;
+                                if (t < m.M && i < inter) {
+                                    const float sc = tok_scale[t];
+                                    m.act[(int64_t)t * inter + i] = __float2bfloat16_rn(
+                                        silu(sc * __uint_as_float(r[q])) * (sc * up[(lg * 32 + lane) * ld + t - c0]));
+                                }
+                            }
+                        }
+                        asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by TMA (async proxy)
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");  // scratch reusable; after the last pass: act written
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");  // tile's act written; scratch reusable
                 if (et == 0) {
                     __threadfence();
                     st_release_u32(m.flags + nt, epoch);
@@ -890,7 +899,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.tmem_cols = 32;
     while (g.tmem_cols < (uint32_t)g.nbuf * g.acc_cols) g.tmem_cols <<= 1;
     const uint32_t scratch =
-        (swap && swiglu_act) ? (uint32_t)((64 * (g.ntok + 1) + g.ntok) * 4 + 1023) / 1024 * 1024 : 0;
+        (swap && swiglu_act) ? (uint32_t)((64 * (XC + 1) + g.ntok) * 4 + 1023) / 1024 * 1024 : 0;
     const int budget = swap ? (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET) : g_knobs.ns_smem_kb * 1024;
     g.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
                                        (uint32_t)(budget - (int)scratch) / (g.np * TILE_W + g.a_bytes));
@@ -945,7 +954,7 @@ int launch_gemm_mlp(const void* xb, int lda, const void* w_gu, void* act, const 
     m.acc_cols = (uint32_t)m.ntok;
     m.tmem_cols = 32;
     while (m.tmem_cols < 2 * m.acc_cols) m.tmem_cols <<= 1;
-    const uint32_t scratch = (uint32_t)((64 * (m.ntok + 1) + m.ntok) * 4 + 1023) / 1024 * 1024;
+    const uint32_t scratch = (uint32_t)((64 * (XC + 1) + m.ntok) * 4 + 1023) / 1024 * 1024;
     const int budget = g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET;
     m.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
                                        (uint32_t)(budget - (int)scratch) / (TILE_W + m.a_bytes));
