@@ -113,6 +113,59 @@ def test_turbo_equals_naive_independent_and_composite_defect(golden):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_empty_context_equals_vanilla_prefill(golden, dtype):
+    """Assembling zero chunks and prefilling the query is bitwise the vanilla prefill of the query alone
+    (proj/tests/test_pipeline.cpp:165-180)."""
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], dtype)
+    q = A["c1.query"]
+    with eng.assemble([], T.PositionMode.Reordered) as ctx:
+        assert ctx.total_tokens() == 0 and ctx.next_position == 0
+        turbo = eng.prefill_query(ctx, q)[0]
+    vanilla = eng.naive_prefill([], q, T.MaskMode.Causal, keep_context=False)[0]
+    assert np.array_equal(turbo, vanilla)
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
+def test_single_chunk_four_paths_agree(golden, dtype, tol):
+    """With one retrieved chunk composite == reordered positions and the causal mask == the independent one, so
+    all four paths give the same logits (proj/tests/acceptance_main.cpp:447-471)."""
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], dtype)
+    pay = payloads(A, "c1")[:1]
+    ids = eng.ingest_chunks(pay)
+    q = A["c1.query"]
+    outs = []
+    for mode in (T.PositionMode.Reordered, T.PositionMode.Composite):
+        with eng.assemble(ids, mode) as ctx:
+            outs.append(eng.prefill_query(ctx, q)[0])
+    for mask in (T.MaskMode.Causal, T.MaskMode.Independent):
+        outs.append(eng.naive_prefill([O.frame(p) for p in pay], q, mask, keep_context=False)[0])
+    assert np.array_equal(outs[0], outs[1])  # identical positions -> identical gather and prefill
+    assert np.array_equal(outs[2], outs[3])  # identical masks
+    assert_close(outs[0], outs[2], tol)
+
+
+def test_layer0_kv_is_position_free(golden):
+    """Layer-0 K/V (unrotated) depend only on the token, not on its position (proj/tests/test_model.cpp:157-173):
+    a chunk's stored layer-0 rows equal its rows inside a full-concat forward where it sits behind another chunk."""
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], "f32")
+    pay = payloads(A, "c1")[:2]
+    ids = eng.ingest_chunks(pay)
+    framed = [O.frame(p) for p in pay]
+    with eng.naive_prefill(framed, A["c1.query"], T.MaskMode.Causal) as ctx:
+        k0 = ctx.read_kv(0, "k", rotated=False)
+        v0 = ctx.read_kv(0, "v")
+    n0 = len(framed[0])
+    for which, full in (("k", k0), ("v", v0)):
+        assert np.allclose(eng.store_read(ids[1], 0, which), full[n0:n0 + len(framed[1])], rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_tkvc_import_gather_bit_exact(golden, tmp_path, dtype):
     """Reference-format chunk caches -> HBM store -> fused gather: unrotated pages bit-exact after the
     canonical cast, rotated keys within fp32 rounding of rope(ctx.k, positions)."""
