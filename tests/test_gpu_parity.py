@@ -148,6 +148,25 @@ def test_single_chunk_four_paths_agree(golden, dtype, tol):
     assert_close(outs[0], outs[2], tol)
 
 
+@pytest.mark.parametrize("dtype,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
+def test_incremental_prefill_equals_one_shot(golden, dtype, tol):
+    """Prefilling the query in two pieces on the same context gives the one-shot logits (incremental == one-shot,
+    proj/tests/test_model.cpp:175-194), and the context grows to the same length and next position."""
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], dtype)
+    ids = eng.ingest_chunks(payloads(A, "c1"))
+    q = A["c1.query"]
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        one = eng.prefill_query(ctx, q)[0]
+        n_one, p_one = ctx.total_tokens(), ctx.next_position
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        eng.prefill_query(ctx, q[:13])
+        two = eng.prefill_query(ctx, q[13:])[0]
+        assert (ctx.total_tokens(), ctx.next_position) == (n_one, p_one)
+    assert_close(two, one, tol)
+
+
 def test_layer0_kv_is_position_free(golden):
     """Layer-0 K/V (unrotated) depend only on the token, not on its position (proj/tests/test_model.cpp:157-173):
     a chunk's stored layer-0 rows equal its rows inside a full-concat forward where it sits behind another chunk."""
