@@ -167,6 +167,35 @@ def test_incremental_prefill_equals_one_shot(golden, dtype, tol):
     assert_close(two, one, tol)
 
 
+def test_tkvc_export_loads_in_reference(golden, tmp_path):
+    """Chunks precomputed on the GPU (f32) exported as TKVC files are loaded by the UNMODIFIED reference
+    CacheStore (header, offsets, fingerprint, dims validated, kvstore.cpp:134-207) and its assemble + query
+    prefill over them matches its own recomputed caches within fp32 rounding."""
+    if not O.Ref.available():
+        pytest.skip("reference sources absent (GPU box)")
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], "f32")
+    pays = payloads(A, "c1")
+    ids = eng.ingest_chunks(pays)
+    ref_gpu = O.RefEngine(O.TOY, m["seed"], str(tmp_path / "from_gpu"), f32_store=True)
+    ref_own = O.RefEngine(O.TOY, m["seed"], str(tmp_path / "own"), f32_store=True)
+    try:
+        assert ref_gpu.fingerprint() == eng.fingerprint()
+        for cid in ids:
+            path = ref_gpu.store_path(cid)
+            os.makedirs(os.path.dirname(path), exist_ok=True)
+            eng.export_tkvc(cid, path)
+        assert [ref_own.ingest(p) for p in pays] == ids
+        q = A["c1.query"]
+        got, _ = ref_gpu.assemble(ids, True).prefill_query(q)
+        want, _ = ref_own.assemble(ids, True).prefill_query(q)
+        assert_close(got, want, FP32_TOL)
+    finally:
+        ref_gpu.close()
+        ref_own.close()
+
+
 def test_layer0_kv_is_position_free(golden):
     """Layer-0 K/V (unrotated) depend only on the token, not on its position (proj/tests/test_model.cpp:157-173):
     a chunk's stored layer-0 rows equal its rows inside a full-concat forward where it sits behind another chunk."""
