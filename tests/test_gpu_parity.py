@@ -196,6 +196,20 @@ def test_tkvc_export_loads_in_reference(golden, tmp_path):
         ref_own.close()
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_rope_position_zero_is_identity(golden, dtype):
+    """RoPE at position 0 is the bit-exact identity (proj/tests/test_rope.cpp:42-52): the gathered, rotated key of
+    the context's first token equals its unrotated row bitwise, in every layer."""
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], dtype)
+    ids = eng.ingest_chunks(payloads(A, "c1"))
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        assert ctx.positions[0] == 0
+        for layer in range(cfg_t(m).layer_num):
+            assert np.array_equal(ctx.read_kv(layer, "k", rotated=True)[0], ctx.read_kv(layer, "k", rotated=False)[0])
+
+
 def test_layer0_kv_is_position_free(golden):
     """Layer-0 K/V (unrotated) depend only on the token, not on its position (proj/tests/test_model.cpp:157-173):
     a chunk's stored layer-0 rows equal its rows inside a full-concat forward where it sits behind another chunk."""
