@@ -332,6 +332,7 @@ class Ref:
             L.ref_ingest.argtypes = [C.c_void_p, I32P, C.c_int64, U64P]
             L.ref_answer.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.c_int, C.c_int64, U64P, C.c_int64, I64P,
                                      I32P, C.c_int64, I64P, U64P]
+            L.ref_chunk_document.argtypes = [C.c_char_p, C.c_int64, C.c_int64, I64P, C.c_int64, I64P]
             L.ref_bench_ingest.argtypes = [C.c_void_p, I64P, C.c_int64, C.c_uint64, U64P, C.c_int64, I64P]
             L.ref_store_path.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p, C.c_int64]
             L.ref_assemble.argtypes = [C.c_void_p, U64P, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]
@@ -397,6 +398,14 @@ class Ref:
         out = np.zeros((new, past + new), np.uint8)
         cls.check(cls.lib().ref_causal_rows(new, past, ptr(out, U8P)))
         return out
+
+
+def ref_chunk_lengths(text: bytes, target_len: int) -> list:
+    """The reference's chunk_document (retrieval.cpp:32-58): byte length of every chunk, in order."""
+    out = np.zeros(max(1, len(text)), np.int64)
+    n = C.c_int64()
+    Ref.check(Ref.lib().ref_chunk_document(text, len(text), target_len, ptr(out, I64P), len(out), C.byref(n)))
+    return [int(x) for x in out[:n.value]]
 
 
 class RefEngine:

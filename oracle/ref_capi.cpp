@@ -217,6 +217,15 @@ int ref_answer(void* e, const char* question, int64_t k, int mode, int64_t max_n
     });
 }
 
+// retrieval.cpp chunk_document: chunk lengths (bytes) in order; the tokens are the text's bytes
+int ref_chunk_document(const char* text, int64_t n, int64_t target_len, int64_t* lens_out, int64_t cap, int64_t* n_out) {
+    return guard([&] {
+        const auto chunks = chunk_document(std::string(text, (size_t)n), target_len);
+        *n_out = (int64_t)chunks.size();
+        for (size_t i = 0; i < chunks.size() && (int64_t)i < cap; ++i) lens_out[i] = (int64_t)chunks[i].size();
+    });
+}
+
 // bench.cpp ingest_synthetic (the reference's own bench corpus): chunk ids in ingest order
 int ref_bench_ingest(void* e, const int64_t* grid, int64_t n_grid, uint64_t seed, uint64_t* ids_out, int64_t cap,
                      int64_t* n_out) {

@@ -75,6 +75,50 @@ def compare(config: T.ModelConfig, chunk_tokens: int, query_tokens: int, batch: 
 
 
 @dataclass
+class Document:
+    """pipeline.hpp:31-34"""
+    id: str
+    text: str
+
+
+_SPACE = frozenset(b" \t\n\r\f\v")  # retrieval.cpp:16-18
+
+
+def chunk_document(text: str, target_len: int) -> list:
+    """retrieval.cpp:32-58: byte windows of target_len, each ending after the window's last whitespace byte
+    when it has one (the whitespace stays left, so concatenating the chunks gives the text back)."""
+    if target_len < 8:
+        raise T.DomainError("chunk_document: target_len must be >= 8")
+    data = text.encode("utf-8")
+    out, pos, n = [], 0, len(data)
+    while pos < n:
+        take = min(target_len, n - pos)
+        if pos + take < n:
+            for i in range(take, 0, -1):
+                if data[pos + i - 1] in _SPACE:
+                    take = i
+                    break
+        out.append(np.frombuffer(data[pos:pos + take], np.uint8).astype(np.int32))
+        pos += take
+    return out
+
+
+def ingest(engine: T.Engine, docs, target_len: int) -> T.IngestStats:
+    """Engine::ingest (pipeline.cpp:81-95): every document chunked and its chunks precomputed (one batched
+    block-diagonal forward per document here); duplicates are counted but stored once."""
+    stats = T.IngestStats()
+    for doc in docs:
+        payloads = chunk_document(doc.text, target_len)
+        if not payloads:
+            continue
+        try:
+            engine.ingest_chunks(payloads, stats)
+        except T.Error as e:
+            raise T.Error(f"ingest of document '{doc.id}' failed: {e}") from e
+    return stats
+
+
+@dataclass
 class AnswerResult:
     """pipeline.hpp:42-55"""
     text: str = ""

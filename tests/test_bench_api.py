@@ -125,3 +125,22 @@ def test_answer_matches_reference_engine(tmp_path, mode):
     with pytest.raises(T.DomainError):
         P.answer(T.Engine(T.ModelConfig.toy(), 42, dtype="f32", store_capacity_tokens=1024), "", 1,
                  P.PathMode.TurboReordered, 1)
+
+
+CHUNK_TEXTS = [
+    b"", b"x", b"short text", b"the quick brown fox jumps over the lazy dog " * 30,
+    b"a" * 100, b"word\tword\nword\rword\fword\vword  " * 20, bytes(range(32, 127)) * 9,
+]
+
+
+@pytest.mark.parametrize("target", [8, 12, 32, 48, 100, 256])
+def test_chunk_document_matches_reference(target):
+    from paper_2410_07590_b200 import pipeline_api as P
+    for text in CHUNK_TEXTS:
+        chunks = P.chunk_document(text.decode("latin-1") if max(text, default=0) < 128 else text.decode(), target)
+        assert b"".join(bytes(c.astype(np.uint8)) for c in chunks) == text  # lossless
+        assert all(0 < len(c) <= target for c in chunks)
+        if O.Ref.available():
+            assert [len(c) for c in chunks] == O.ref_chunk_lengths(text, target)
+    with pytest.raises(T.DomainError):
+        P.chunk_document("x", 7)
