@@ -43,9 +43,18 @@ class FlopsReport:
     batch: int
     total: int
 
+    def tflops(self) -> float:
+        return self.total / 1e12
+
+
+def _validated(config: T.ModelConfig) -> T.ModelConfig:
+    config.validate()  # ModelConfig::validate (config.cpp:9-40): ConfigError
+    return config
+
 
 def flops(config: T.ModelConfig, n_input: int, n_context: int, batch: int = 1) -> FlopsReport:
     """costmodel.cpp:28-46 (Appendix C): total = batch * n_input * L * (c_qkv + c_attn(n_context) + c_o + c_mlp)."""
+    _validated(config)
     if n_input < 1 or n_context < 1 or batch < 1:
         raise T.DomainError("flops: n_input, n_context and batch must be >= 1")
     if n_context < n_input:
@@ -56,6 +65,15 @@ def flops(config: T.ModelConfig, n_input: int, n_context: int, batch: int = 1) -
     o = 2 * c.hidden_size * c.hidden_size
     mlp = 2 * 3 * c.hidden_size * c.intermediate_size
     return FlopsReport(qkv, attn, o, mlp, n_input, n_context, batch, batch * n_input * c.layer_num * (qkv + attn + o + mlp))
+
+
+def flops_attention_ramped(config: T.ModelConfig, n_input: int, past: int) -> int:
+    """costmodel.cpp:65-75: attention charged per token over the context it actually sees (token t: past + t + 1)."""
+    _validated(config)
+    if n_input < 1 or past < 0:
+        raise T.DomainError("flops_attention_ramped: bad counts")
+    per = 2 * config.head_num * config.head_size
+    return config.layer_num * per * (n_input * past + n_input * (n_input + 1) // 2)
 
 
 @dataclass

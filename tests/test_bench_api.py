@@ -144,3 +144,45 @@ def test_chunk_document_matches_reference(target):
             assert [len(c) for c in chunks] == O.ref_chunk_lengths(text, target)
     with pytest.raises(T.DomainError):
         P.chunk_document("x", 7)
+
+
+def _unit_config():
+    return T.ModelConfig(layer_num=1, head_num=1, kv_head_num=1, head_size=2, hidden_size=2, intermediate_size=1,
+                         vocab_size=1)
+
+
+def test_costmodel_reference_cases():
+    """proj/tests/test_costmodel.cpp, case by case."""
+    from paper_2410_07590_b200 import pipeline_api as P
+    r = P.flops(_unit_config(), 1, 1, 1)
+    assert (r.c_qkv, r.c_attn, r.c_o, r.c_mlp, r.total) == (24, 4, 8, 12, 48)
+    r10 = P.flops(_unit_config(), 1, 10, 1)
+    assert r10.c_attn == 40 and (r10.c_qkv, r10.c_o, r10.c_mlp) == (r.c_qkv, r.c_o, r.c_mlp)
+    q = T.ModelConfig.qwen2_7b_like()
+    base = P.flops(q, 128, 8320, 1)
+    assert P.flops(q, 128, 8320, 2).total == 2 * base.total and P.flops(q, 128, 8320, 4).total == 4 * base.total
+    assert P.flops(q, 256, 8320, 1).total == 2 * base.total
+    half = T.ModelConfig(**{**vars(q), "layer_num": q.layer_num // 2})
+    assert 2 * P.flops(half, 128, 8320, 1).total == base.total
+    cmp = P.compare(q, 8192, 128, 1)
+    assert abs(cmp.naive.tflops() - 136.36) <= 0.15 * 136.36 and abs(cmp.reduction_percent - 98.46) < 0.5
+    assert (cmp.turbo.n_input, cmp.turbo.n_context, cmp.naive.n_input) == (128, 8320, 8320)
+    none = P.compare(q, 0, 128, 1)
+    assert none.reduction_percent == 0.0 and none.naive.total == none.turbo.total
+    reds = [P.compare(q, c, 128, 1).reduction_percent for c in (512, 2048, 8192, 32768)]
+    assert reds == sorted(reds) and reds[-1] < 100.0
+    firsts = [P.compare(T.ModelConfig(**{**vars(q), "layer_num": n}), 8192, 128, 1).reduction_percent for n in (1, 4, 28)]
+    assert max(firsts) - min(firsts) <= 1e-12 * firsts[0]
+    toy = T.ModelConfig.toy()
+    for args in ((0, 1, 1), (1, 0, 1), (1, 1, 0), (5, 4, 1)):
+        with pytest.raises(T.DomainError):
+            P.flops(toy, *args)
+    for args in ((-1, 8, 1), (8, 0, 1)):
+        with pytest.raises(T.DomainError):
+            P.compare(toy, *args)
+    with pytest.raises(T.ConfigError):
+        P.flops(T.ModelConfig(**{**vars(toy), "head_size": 0}), 1, 1, 1)
+    flat = P.flops(toy, 100, 100, 1)
+    ramped = P.flops_attention_ramped(toy, 100, 0)
+    assert ramped < toy.layer_num * 100 * flat.c_attn
+    assert ramped == toy.layer_num * 2 * toy.head_num * toy.head_size * (100 * 101 // 2)
