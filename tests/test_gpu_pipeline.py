@@ -1,0 +1,89 @@
+"""The reference's pipeline / model behaviour cases (proj/tests/test_pipeline.cpp:74-99, 276-309 and
+proj/tests/test_model.cpp:196-247) on the B200 engine through the caller mirrors (pipeline_api.py)."""
+import numpy as np
+import pytest
+
+from paper_2410_07590_b200 import pipeline_api as P
+from paper_2410_07590_b200 import turbokv as T
+
+pytestmark = pytest.mark.gpu
+
+DOCS = [
+    P.Document("locks", "A pound lock holds water between two gates. Boats enter, the chamber fills or drains, and "
+                        "the far gate opens once the levels match. Paddles in the gates let the water through."),
+    P.Document("tides", "Tides rise and fall twice a day because the moon and the sun pull on the oceans. Spring "
+                        "tides are the largest; neap tides are the smallest."),
+    P.Document("bread", "Bread rises when yeast turns sugar into gas. Kneading builds gluten that traps the gas; "
+                        "baking sets the crumb and browns the crust."),
+]
+
+
+def toy_engine(cap=1 << 14):
+    return T.Engine(T.ModelConfig.toy(), 42, dtype="f32", store_capacity_tokens=cap)
+
+
+def test_ingest_is_lossless_and_idempotent():
+    eng = toy_engine()
+    first = P.ingest(eng, DOCS, 40)
+    assert first.chunks > 3 and first.new_chunks == first.chunks and first.bytes_written > 0
+    assert eng.index_size() == first.chunks
+    payload_bytes = sum(len(eng.chunk_framed_tokens(i)) - 2 for i in eng._framed)
+    assert payload_bytes == sum(len(d.text.encode()) for d in DOCS)
+    again = P.ingest(eng, DOCS, 40)
+    assert again.chunks == first.chunks and again.new_chunks == 0 and again.bytes_written == 0
+    assert eng.index_size() == first.chunks
+    eng.close()
+
+
+def test_answer_identical_across_turbo_and_naive():
+    eng = toy_engine()
+    P.ingest(eng, DOCS, 48)
+    q = "how does a pound lock work?"
+    turbo = P.answer(eng, q, 3, P.PathMode.TurboReordered, 16)
+    naive = P.answer(eng, q, 3, P.PathMode.NaiveIndependent, 16)
+    assert turbo.retrieved == naive.retrieved and turbo.tokens == naive.tokens and turbo.text == naive.text
+    assert (turbo.context_tokens, turbo.query_tokens) == (naive.context_tokens, naive.query_tokens)
+    assert turbo.prefill_flops == turbo.modeled_prefill_flops and naive.prefill_flops == naive.modeled_prefill_flops
+    assert turbo.prefill_flops < naive.prefill_flops and turbo.decode_flops > 0
+    eng.close()
+
+
+def test_answer_refuses_without_context_and_rejects_empty_questions():
+    eng = toy_engine()
+    with pytest.raises(T.NoContextError):
+        P.answer(eng, "anything?", 2, P.PathMode.TurboReordered, 4)
+    eng.ingest_chunk_payload("d", P.encode("now there is context"))
+    with pytest.raises(T.DomainError):
+        P.answer(eng, "", 2, P.PathMode.TurboReordered, 4)
+    r = P.answer(eng, "what is here?", 50, P.PathMode.TurboReordered, 4)  # k beyond the index: everything
+    assert len(r.retrieved) == 1
+    eng.close()
+
+
+def test_greedy_decode_deterministic_and_grows_context():
+    eng = toy_engine()
+    prompt = P.encode("the sea was calm")
+    outs = []
+    for _ in range(2):
+        with eng.assemble([], T.PositionMode.Reordered) as ctx:
+            eng.prefill_query(ctx, prompt)
+            out = eng.greedy_decode(ctx, 12)
+            assert ctx.total_tokens() == len(prompt) + len(out)
+            assert ctx.next_position == ctx.total_tokens() and ctx.positions[-1] == ctx.total_tokens() - 1
+            outs.append(out)
+    assert outs[0] == outs[1]
+    eng.close()
+
+
+def test_decode_edge_cases():
+    eng = toy_engine()
+    prompt = P.encode("abc")
+    with eng.assemble([], T.PositionMode.Reordered) as ctx:
+        eng.prefill_query(ctx, prompt)
+        assert eng.greedy_decode(ctx, 0) == [] and ctx.total_tokens() == 3  # max_new = 0 emits nothing
+        with pytest.raises(T.DomainError):
+            eng.greedy_decode(ctx, -1)
+    with eng.assemble([], T.PositionMode.Reordered) as ctx:  # never prefilled: no logits to decode from
+        with pytest.raises(T.DomainError):
+            eng.greedy_decode(ctx, 4)
+    eng.close()
