@@ -31,6 +31,26 @@ class PathMode(enum.IntEnum):
     NaiveIndependent = 3
 
 
+_PATH_NAMES = {PathMode.TurboReordered: "turbo-reordered", PathMode.TurboComposite: "turbo-composite",
+               PathMode.NaiveCausal: "naive-causal", PathMode.NaiveIndependent: "naive-independent"}
+
+
+def to_string(mode) -> str:
+    """pipeline.cpp:31-43 (PathMode and PositionMode names)."""
+    if isinstance(mode, PathMode):
+        return _PATH_NAMES[mode]
+    return "composite" if mode == T.PositionMode.Composite else "reordered"
+
+
+def path_mode_from_string(name: str) -> PathMode:
+    """pipeline.cpp:45-53"""
+    for m, n in _PATH_NAMES.items():
+        if n == name:
+            return m
+    raise T.ConfigError(f"unknown mode '{name}' (expected turbo-reordered, turbo-composite, naive-causal, "
+                        "or naive-independent)")
+
+
 @dataclass
 class FlopsReport:
     """costmodel.hpp FlopsReport"""

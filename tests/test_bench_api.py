@@ -186,3 +186,13 @@ def test_costmodel_reference_cases():
     ramped = P.flops_attention_ramped(toy, 100, 0)
     assert ramped < toy.layer_num * 100 * flat.c_attn
     assert ramped == toy.layer_num * 2 * toy.head_num * toy.head_size * (100 * 101 // 2)
+
+
+def test_path_mode_names_round_trip():
+    """proj/tests/test_pipeline.cpp:56-64"""
+    from paper_2410_07590_b200 import pipeline_api as P
+    for m in P.PathMode:
+        assert P.path_mode_from_string(P.to_string(m)) == m
+    with pytest.raises(T.ConfigError):
+        P.path_mode_from_string("fast")
+    assert P.to_string(T.PositionMode.Composite) == "composite" and P.to_string(T.PositionMode.Reordered) == "reordered"

@@ -87,3 +87,11 @@ def test_decode_edge_cases():
         with pytest.raises(T.DomainError):
             eng.greedy_decode(ctx, 4)
     eng.close()
+
+
+def test_engine_requires_tokenizer_sized_vocabulary():
+    """proj/tests/test_pipeline.cpp:66-72: structurally valid, too small for the 259-id tokenizer."""
+    cfg = T.ModelConfig(**{**vars(T.ModelConfig.toy()), "vocab_size": 128})
+    cfg.validate()
+    with pytest.raises(T.ConfigError):
+        T.Engine(cfg, 1, dtype="f32", store_capacity_tokens=1024)
