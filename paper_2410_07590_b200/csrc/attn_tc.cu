@@ -769,6 +769,55 @@ __global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat1
         make_uint2(bf16x2_bits(acc[0] * inv, acc[1] * inv), bf16x2_bits(acc[2] * inv, acc[3] * inv));
 }
 
+// Split merge of the BATCHED launch: row groups are (request, kv head, group) with gid = (req * Hkv + g) * groups_x
+// + x; each request's rows / output rows come from its AttnReq (tok0, n).
+__global__ void __launch_bounds__(256) attn_tc_combine_batch_kernel(const __nv_bfloat16* __restrict__ ws_o,
+                                                                    const float2* __restrict__ ws_ml,
+                                                                    __nv_bfloat16* __restrict__ out, int* err,
+                                                                    const AttnReq* __restrict__ reqs, int H, int Hkv,
+                                                                    int splits, int groups_x, int ngroups) {
+    pdl_launch();
+    const int lane = threadIdx.x & 31;
+    const int grow = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int gid = grow / RG, i = grow % RG;
+    const int y = gid / groups_x, req = y / Hkv, g = y - req * Hkv;
+    const int rr = (gid % groups_x) * RG + i;
+    const int group = H / Hkv;
+    pdl_wait();
+    const AttnReq R = reqs[req];
+    if (rr >= R.n * group) return;  // warp-uniform
+    const int64_t plane = (int64_t)ngroups * RG;
+    const uint2* src = reinterpret_cast<const uint2*>(ws_o + (int64_t)grow * D) + lane;
+    uint2 v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        if (k < splits) v[k] = src[(int64_t)k * plane * (D / 4)];
+    const float2 ml = lane < splits ? ws_ml[lane * plane + grow] : make_float2(-INFINITY, 0.f);
+    float M = ml.x;
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float wl = ml.x == -INFINITY ? 0.f : ex2(ml.x - M) * ml.y;
+    float L = wl;
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (M == -INFINITY || L == 0.f) {
+        if (lane == 0) atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
+        return;
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        if (k >= splits) break;
+        const float w = __shfl_sync(0xffffffffu, wl, k);
+        acc[0] = fmaf(__uint_as_float(v[k].x << 16), w, acc[0]);
+        acc[1] = fmaf(__uint_as_float(v[k].x & 0xFFFF0000u), w, acc[1]);
+        acc[2] = fmaf(__uint_as_float(v[k].y << 16), w, acc[2]);
+        acc[3] = fmaf(__uint_as_float(v[k].y & 0xFFFF0000u), w, acc[3]);
+    }
+    const float inv = 1.0f / L;
+    const int64_t mo = (int64_t)(R.tok0 + rr / group) * H + g * group + rr % group;
+    reinterpret_cast<uint2*>(out + mo * D)[lane] =
+        make_uint2(bf16x2_bits(acc[0] * inv, acc[1] * inv), bf16x2_bits(acc[2] * inv, acc[3] * inv));
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -818,7 +867,7 @@ void attn_tc_cache_map(const void* cache, int64_t rows, int64_t cap, int kv_dim,
 
 void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* maps, int n_req, int max_rows, int H,
                                int Hkv, int layer, const int32_t* lo, const int32_t* hi, void* out, int* err,
-                               cudaStream_t s) {
+                               cudaStream_t s, int splits, const AttnWork& ws) {
     TKV_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
     const int group = H / Hkv;
     AttnArgs a{};
@@ -829,7 +878,10 @@ void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* m
     a.err = err;
     a.H = H;
     a.Hkv = Hkv;
-    a.splits = 1;
+    a.splits = splits < 1 ? 1 : splits;
+    if (a.splits > 1 && !ws.o) fail(TKV_ERR_CONFIG, "batched attention split-K needs its workspace");
+    a.ws_o = ws.o;
+    a.ws_ml = ws.ml;
     a.scale = (float)(1.0 / sqrt((double)D));
     a.trace = g_trace_host;
     a.reqs = reqs;
@@ -838,9 +890,35 @@ void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* m
     a.layer = layer;
     CUtensorMap unused;
     memset(&unused, 0, sizeof unused);
-    launch_k(attn_tc_kernel, dim3((max_rows * group + RG - 1) / RG, Hkv * n_req, 1), THREADS, SMEM_BYTES, s, unused,
-             unused, a);
+    const int groups_x = (max_rows * group + RG - 1) / RG;
+    launch_k(attn_tc_kernel, dim3(groups_x, Hkv * n_req, a.splits), THREADS, SMEM_BYTES, s, unused, unused, a);
     TKV_CUDA(cudaGetLastError());
+    if (a.splits > 1) {
+        const int ngroups = groups_x * Hkv * n_req;
+        launch_k(attn_tc_combine_batch_kernel, dim3((ngroups * RG + 7) / 8), dim3(256), 0, s,
+                 reinterpret_cast<const __nv_bfloat16*>(ws.o), reinterpret_cast<const float2*>(ws.ml),
+                 (__nv_bfloat16*)out, err, reqs, H, Hkv, a.splits, groups_x, ngroups);
+        TKV_CUDA(cudaGetLastError());
+    }
+}
+
+// split-K of the batched launch: the smallest split count whose CTA count fills the last wave (>= 95 % of the
+// slots), so the request x kv-head x row-group CTAs do not leave most of a second wave idle; 1 when the key
+// range per split would drop below 8 tiles
+int attn_tc_batch_pick_splits(int ctas, int min_keys, int num_sms) {
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 8; ++s) {
+        if (s > 1 && min_keys / s < 8 * BK) break;
+        const int64_t c = (int64_t)ctas * s;
+        const double eff = (double)c / (double)(((c + num_sms - 1) / num_sms) * num_sms);
+        if (eff > best_eff + 0.02) {
+            best = s;
+            best_eff = eff;
+        }
+        if (eff >= 0.95) break;
+    }
+    return best;
 }
 
 void attn_trace_enable(bool on, unsigned long long** host_view) {

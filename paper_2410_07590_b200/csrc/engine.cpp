@@ -476,6 +476,7 @@ struct tkv_engine {
 
     // fused gate/up + down launch (gemm_tc.cu:gemm_mlp_kernel): <= 128 rows, interleaved W_gu whose GEMM runs
     // without split-K, dims multiples of the 64-wide k-block
+    int batch_attn_splits = 1;  // TKV_BATCH_ATTN_SPLITS (0 = attn_tc_batch_pick_splits; measured on par)
     int fused_mlp = 0;  // TKV_FUSED_MLP=1 (opt-in: measured slower)
     DevMem mlp_flags, mlp_ctl;
     bool fused_mlp_ok(int rows) {
@@ -533,6 +534,7 @@ struct tkv_engine {
         const AttnReq* batch_reqs = nullptr;  // device request table + cache maps of the batched attention
         const void* batch_maps = nullptr;
         int batch_max_n = 0;
+        int batch_min_keys = 0;  // shortest request context (keys) of the batched attention
     };
     void forward(const Fwd& f);
     void check_err(const char* where);
@@ -694,11 +696,24 @@ void tkv_engine::forward(const Fwd& f) {
             }
         };
         if (batch && f.batch_maps) {
-            // one launch for the whole batch (enough row groups to fill the GPU without split-K)
-            Scope sc(this, PC_ATTN, 1);
+            // one launch for the whole batch; split-K only to fill the last wave of (request, kv head, row group)
+            // CTAs, merged by a request-aware combine
+            const int n_req = (int)f.reqs.size();
+            const int groups_x = (f.batch_max_n * (int)(H / Hkv) + 255) / 256;
+            int bs = batch_attn_splits > 0 ? batch_attn_splits
+                                           : attn_tc_batch_pick_splits(groups_x * (int)Hkv * n_req, f.batch_min_keys,
+                                                                       num_sms);
+            AttnWork bws;
+            if (bs > 1) {
+                const size_t rows = (size_t)bs * groups_x * Hkv * n_req * 256;
+                attn_ws.ensure((rows * d / 2 + rows * 2) * sizeof(float));
+                bws.o = attn_ws.as<float>();
+                bws.ml = bws.o + rows * d / 2;
+            }
+            Scope sc(this, PC_ATTN, bs > 1 ? 2 : 1);
             if (trace_layer == (int)l) attn_trace_enable(true, nullptr);
-            launch_attention_tc_batch(q.p, f.batch_reqs, f.batch_maps, (int)f.reqs.size(), f.batch_max_n, (int)H,
-                                      (int)Hkv, (int)l, f.lo, f.hi, attn.p, err.as<int>(), stream);
+            launch_attention_tc_batch(q.p, f.batch_reqs, f.batch_maps, n_req, f.batch_max_n, (int)H, (int)Hkv, (int)l,
+                                      f.lo, f.hi, attn.p, err.as<int>(), stream, bs, bws);
             if (trace_layer == (int)l) attn_trace_enable(false, nullptr);
         } else if (batch) {
             for (const Fwd::Req& r : f.reqs)
@@ -1342,6 +1357,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         if (const char* mp = getenv("TKV_GEMM_NSMP")) set_gemm_nsmp(atoi(mp));
         if (const char* gc = getenv("TKV_GEMM_CLUSTER")) set_gemm_cluster(atoi(gc));
         if (const char* fm = getenv("TKV_FUSED_MLP")) e->fused_mlp = atoi(fm);
+        if (const char* bs = getenv("TKV_BATCH_ATTN_SPLITS")) e->batch_attn_splits = atoi(bs);
         if (const char* se = getenv("TKV_GEMM_SKIP_EPI")) set_gemm_skip_epi(atoi(se));
         if (const char* ra = getenv("TKV_GEMM_RASTER")) set_gemm_raster(atoi(ra));
         if (const char* gm = getenv("TKV_GEMM_GROUP_MB")) set_gemm_raster(1, atoi(gm));
@@ -1833,6 +1849,9 @@ tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int6
             f.batch_reqs = e->d_breq.as<AttnReq>();
             f.batch_maps = e->d_bmaps.p;
             f.batch_max_n = max_n;
+            int min_keys = INT32_MAX;
+            for (const auto& q : f.reqs) min_keys = std::min(min_keys, q.row0 + q.n);
+            f.batch_min_keys = min_keys;
         }
         f.tok = e->d_tok.as<int32_t>();
         f.T = (int)T;

@@ -179,7 +179,8 @@ struct AttnReq {
 void attn_tc_cache_map(const void* cache, int64_t rows, int64_t cap, int kv_dim, int L, void* map128);
 void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* maps, int n_req, int max_rows, int H,
                                int Hkv, int layer, const int32_t* lo, const int32_t* hi, void* out, int* err,
-                               cudaStream_t s);
+                               cudaStream_t s, int splits = 1, const AttnWork& ws = AttnWork{});
+int attn_tc_batch_pick_splits(int ctas, int min_keys, int num_sms);
 void attn_trace_enable(bool on, unsigned long long** device_buf);  // debug timeline of CTA (0,0,0)
 int attn_tc_row_groups(int Tq, int H, int Hkv);
 // workspace of the tcgen05 kernel's split merge (floats); ws.ml = ws.o + *ml_offset

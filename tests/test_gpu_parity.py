@@ -707,3 +707,29 @@ np.save(sys.argv[1], np.concatenate([out, np.asarray(toks, np.float32)]))
     v = 259
     assert_close(outs[1][:v], outs[0][:v], BF16_TOL)
     assert np.array_equal(outs[1][v:], outs[0][v:])
+
+
+def test_batched_attention_split_k_matches(golden, tmp_path):
+    """TKV_BATCH_ATTN_SPLITS=3: the batched single-launch attention with split-K partials and the request-aware
+    combine gives the unsplit batched logits (bf16 tolerance); fresh processes (the knob is read at creation)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "run.py"
+    script.write_text(r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import oracle as O
+from paper_2410_07590_b200 import turbokv as T
+eng = T.Engine(T.ModelConfig(**vars(O.qwen_layers(2))), 7, dtype="bf16", store_capacity_tokens=1 << 16, flags=0x20)
+ids = eng.ingest_chunks([O.random_text_tokens(800 + i, 510) for i in range(6)])
+ctxs = [eng.assemble(ids[i:i + 3], T.PositionMode.Reordered) for i in range(3)]
+qs = [O.random_text_tokens(801 + i, 40 + 11 * i) for i in range(3)]
+np.save(sys.argv[1], eng.prefill_query_batch(ctxs, qs))
+""" % root)
+    outs = []
+    for e in ({"TKV_BATCH_ATTN_SPLITS": "1"}, {"TKV_BATCH_ATTN_SPLITS": "3"}):
+        path = tmp_path / f"o{len(outs)}.npy"
+        subprocess.run([sys.executable, str(script), str(path)], check=True, env={**os.environ, **e}, timeout=300)
+        outs.append(np.load(path))
+    for a, b in zip(outs[1], outs[0]):
+        assert_close(a, b, BF16_TOL)
