@@ -242,3 +242,51 @@ def answer(engine: T.Engine, question: str, k: int, mode: PathMode, max_new: int
     r.decode_flops = sum(flops(cfg, 1, total + i + 1).total for i in range(len(r.tokens)))
     r.text = decode(r.tokens)
     return r
+
+
+# ---- turbokv-report/1 (docs/formats.md "JSON reports"; tools/turbokv_main.cpp:83-93, 220-310, 615-660) ----
+REPORT_SCHEMA = "turbokv-report/1"
+
+
+def hex_id(chunk_id: int) -> str:
+    return f"{chunk_id:016x}"
+
+
+def config_json(c: T.ModelConfig) -> dict:
+    return {"layer_num": c.layer_num, "head_num": c.head_num, "kv_head_num": c.kv_head_num,
+            "head_size": c.head_size, "hidden_size": c.hidden_size, "intermediate_size": c.intermediate_size,
+            "vocab_size": c.vocab_size, "rope_base": c.rope_base, "norm_eps": c.norm_eps}
+
+
+def ask_report(engine: T.Engine, question: str, k: int, mode: str, max_new: int) -> dict:
+    """`turbokv ask --json`: the answer report, or the refusal report when nothing has been ingested."""
+    try:
+        r = answer(engine, question, k, path_mode_from_string(mode), max_new)
+    except T.NoContextError:
+        return {"schema": REPORT_SCHEMA, "command": "ask", "refused": True, "reason": "no documents ingested"}
+    return {"schema": REPORT_SCHEMA, "command": "ask", "refused": False, "mode": mode, "question": question,
+            "answer_text": r.text, "answer_tokens": list(r.tokens), "retrieved": [hex_id(i) for i in r.retrieved],
+            "timings_ms": {"retrieval": r.retrieval_ms, "cache_load": r.cache_load_ms, "ttft": r.ttft_ms,
+                           "decode": r.decode_ms},
+            "flops": {"prefill_measured": r.prefill_flops, "prefill_modeled": r.modeled_prefill_flops,
+                      "decode_measured": r.decode_flops},
+            "context_tokens": r.context_tokens, "query_tokens": r.query_tokens, "seed": engine.seed,
+            "config": config_json(engine.config)}
+
+
+def flops_report(preset: str, chunk_tokens: int, query_tokens: int, batches=(1, 2, 4, 6, 8)) -> dict:
+    """`turbokv flops --json`: the Appendix-C comparison per batch size."""
+    if chunk_tokens < 1:
+        raise T.ConfigError("flops: --chunk-tokens must be >= 1")
+    if query_tokens < 1:
+        raise T.ConfigError("flops: --query-tokens must be >= 1")
+    config = T.ModelConfig.preset(preset)
+    rows = []
+    for b in batches:
+        cmp = compare(config, chunk_tokens, query_tokens, b)
+        rows.append({"batch": b, "naive_total": cmp.naive.total, "turbo_total": cmp.turbo.total,
+                     "naive_tflops": cmp.naive.tflops(), "turbo_tflops": cmp.turbo.tflops(),
+                     "reduction_percent": cmp.reduction_percent})
+    return {"schema": REPORT_SCHEMA, "command": "flops", "preset": preset, "chunk_tokens": chunk_tokens,
+            "query_tokens": query_tokens, "config": config_json(config), "rows": rows}
+

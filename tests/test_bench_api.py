@@ -196,3 +196,34 @@ def test_path_mode_names_round_trip():
     with pytest.raises(T.ConfigError):
         P.path_mode_from_string("fast")
     assert P.to_string(T.PositionMode.Composite) == "composite" and P.to_string(T.PositionMode.Reordered) == "reordered"
+
+
+def test_flops_report_schema():
+    """docs/formats.md "JSON reports" (flops): keys, rows per batch, totals from the cost model."""
+    from paper_2410_07590_b200 import pipeline_api as P
+    rep = P.flops_report("qwen2-7b", 8192, 128)
+    assert rep["schema"] == "turbokv-report/1" and rep["command"] == "flops"
+    assert set(rep) == {"schema", "command", "preset", "chunk_tokens", "query_tokens", "config", "rows"}
+    assert [r["batch"] for r in rep["rows"]] == [1, 2, 4, 6, 8]
+    r1 = rep["rows"][0]
+    assert set(r1) == {"batch", "naive_total", "turbo_total", "naive_tflops", "turbo_tflops", "reduction_percent"}
+    assert r1["naive_total"] == O.Port.flops_total(O.QWEN2_7B, 8320, 8320)
+    assert 100.0 < r1["naive_tflops"] < 160.0  # proj/tests/test_cli.cpp flops --json bounds
+    with pytest.raises(T.ConfigError):
+        P.flops_report("qwen2-7b", 0, 128)
+
+
+@pytest.mark.gpu
+def test_ask_report_schema():
+    from paper_2410_07590_b200 import pipeline_api as P
+    eng = T.Engine(T.ModelConfig.toy(), 42, dtype="f32", store_capacity_tokens=4096)
+    ref = P.ask_report(eng, "anything?", 2, "turbo-reordered", 4)
+    assert ref == {"schema": "turbokv-report/1", "command": "ask", "refused": True, "reason": "no documents ingested"}
+    P.ingest(eng, [P.Document("d", "canal locks hold water between gates while boats rise or fall")], 24)
+    rep = P.ask_report(eng, "how do locks work?", 2, "naive-independent", 4)
+    assert {"schema", "command", "refused", "mode", "question", "answer_text", "answer_tokens", "retrieved",
+            "timings_ms", "flops", "context_tokens", "query_tokens", "seed", "config"} == set(rep)
+    assert rep["refused"] is False and all(len(h) == 16 for h in rep["retrieved"])
+    assert rep["flops"]["prefill_measured"] == rep["flops"]["prefill_modeled"]
+    assert set(rep["timings_ms"]) == {"retrieval", "cache_load", "ttft", "decode"}
+    eng.close()
