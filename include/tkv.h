@@ -147,6 +147,8 @@ tkv_status tkv_export_tkvc(tkv_engine* eng, uint64_t chunk_id, const char* path)
 tkv_status tkv_store_contains(const tkv_engine* eng, uint64_t chunk_id, int* out);
 tkv_status tkv_store_chunk_tokens(const tkv_engine* eng, uint64_t chunk_id, int64_t* out);
 tkv_status tkv_store_count(const tkv_engine* eng, int64_t* chunks, int64_t* pages_used, int64_t* pages_total);
+/* CacheStore::ids (kvstore.cpp): every stored chunk id, ascending; ids_out may be NULL to query the count. */
+tkv_status tkv_store_ids(const tkv_engine* eng, uint64_t* ids_out, int64_t capacity, int64_t* n_out);
 /* Drop a chunk from the store and return its pages (no reference analogue: the reference store is a directory
  * of TKVC files, kvstore.cpp:78-211; this is the capacity policy of the HBM store). Contexts assembled earlier
  * keep their gathered KV; only their unrotated re-read (tkv_context_read_kv, rotated=0) then fails StaleCache. */

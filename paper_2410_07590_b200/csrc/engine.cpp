@@ -1731,6 +1731,21 @@ tkv_status tkv_store_count(const tkv_engine* e, int64_t* chunks, int64_t* used, 
     });
 }
 
+tkv_status tkv_store_ids(const tkv_engine* e, uint64_t* ids_out, int64_t capacity, int64_t* n_out) {
+    return guard([&] {
+        need(e, "engine");
+        std::vector<uint64_t> ids;
+        ids.reserve(e->chunks.size());
+        for (const auto& kv : e->chunks) ids.push_back(kv.first);
+        std::sort(ids.begin(), ids.end());  // CacheStore::ids: ascending (kvstore.cpp)
+        if (n_out) *n_out = (int64_t)ids.size();
+        if (ids_out) {
+            if (capacity < (int64_t)ids.size()) fail(TKV_ERR_SHAPE, "store_ids: output capacity too small");
+            std::copy(ids.begin(), ids.end(), ids_out);
+        }
+    });
+}
+
 tkv_status tkv_store_read(const tkv_engine* ce, uint64_t id, int64_t layer, tkv_kv_which which, float* host_out,
                           int64_t capacity) {
     return guard([&] {

@@ -126,6 +126,7 @@ def lib():
         L.tkv_store_contains.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int)]
         L.tkv_store_chunk_tokens.argtypes = [C.c_void_p, C.c_uint64, I64P]
         L.tkv_store_count.argtypes = [C.c_void_p, I64P, I64P, I64P]
+        L.tkv_store_ids.argtypes = [C.c_void_p, U64P, C.c_int64, I64P]
         L.tkv_store_evict.argtypes = [C.c_void_p, C.c_uint64]
         L.tkv_embed.argtypes = [I32P, C.c_int64, C.c_int64, C.POINTER(C.c_double)]
         L.tkv_index_add.argtypes = [C.c_void_p, C.c_uint64, I32P, C.c_int64, C.POINTER(C.c_int)]
@@ -488,6 +489,14 @@ class Engine:
         if chunk_id not in self._framed:
             raise NotFoundError(f"chunk {chunk_id:016x}: tokens not held by this engine")
         return self._framed[chunk_id]
+
+    def store_ids(self) -> list:
+        """CacheStore::ids: every stored chunk id, ascending."""
+        n = C.c_int64()
+        _check(lib().tkv_store_ids(self._h, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.uint64)
+        _check(lib().tkv_store_ids(self._h, _p(out, U64P), len(out), C.byref(n)))
+        return [int(x) for x in out[:n.value]]
 
     def store_read(self, chunk_id: int, layer: int, which: str = "k") -> np.ndarray:
         n = C.c_int64()

@@ -95,3 +95,17 @@ def test_engine_requires_tokenizer_sized_vocabulary():
     cfg.validate()
     with pytest.raises(T.ConfigError):
         T.Engine(cfg, 1, dtype="f32", store_capacity_tokens=1024)
+
+
+def test_store_ids_sorted_and_ingest_is_a_noop_for_known_ids():
+    """proj/tests/test_kvstore.cpp:89-110: storing the same id twice is a no-op; ids come back sorted."""
+    eng = toy_engine()
+    pays = [P.encode(f"chunk number {i} " * (3 + i)) for i in (5, 1, 4, 2, 3)]
+    ids = eng.ingest_chunks(pays)
+    assert eng.store_ids() == sorted(ids)
+    st = T.IngestStats()
+    assert eng.ingest_chunks(pays[:2], st) == ids[:2] and st.new_chunks == 0 and st.bytes_written == 0
+    assert eng.store_ids() == sorted(ids)
+    eng.store_evict(ids[0])
+    assert eng.store_ids() == sorted(ids[1:])
+    eng.close()
