@@ -283,7 +283,7 @@ __device__ __forceinline__ void rotate_vec(uint4& v, const float2* cs) {
 // grid-stride loop is short (C2: 14 336 units over 1 184 resident CTAs). Every thread issues
 // all of its 16-byte loads (and, for keys, its cos/sin loads) before the first store.
 #ifndef GATHER_ROWS_CFG
-#define GATHER_ROWS_CFG 32
+#define GATHER_ROWS_CFG 64
 #endif
 #ifndef GATHER_U_CFG
 #define GATHER_U_CFG 4
