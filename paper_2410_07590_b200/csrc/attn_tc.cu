@@ -42,7 +42,13 @@ namespace tkv {
 namespace {
 
 constexpr int D = 128, BR = 128, BK = 128, RG = 2 * BR;  // rows per tile, keys per tile, rows per CTA
-constexpr int KST = 3, VST = 2;                          // K / V ring depths
+#ifndef ATTN_KST
+#define ATTN_KST 3
+#endif
+#ifndef ATTN_VST
+#define ATTN_VST 2
+#endif
+constexpr int KST = ATTN_KST, VST = ATTN_VST;            // K / V ring depths (Q 64 KB + (KST + VST) x 32 KB <= 224 KB)
 constexpr int SM_THREADS = 256, THREADS = SM_THREADS + 64;
 #ifndef POLY_PAIRS
 #define POLY_PAIRS 6
