@@ -74,7 +74,8 @@ typedef struct {
     int32_t page_tokens;          /* tokens per KV-store page (default 64)                          */
     int64_t store_capacity_tokens;/* HBM store capacity in tokens (0 = 1/4 of free HBM)             */
     int64_t max_position;         /* RoPE table length (0 = 32768; grows on demand)                 */
-    int32_t exact_fingerprint;    /* 1 = reference FNV weights checksum, 0 = fast, -1 = auto        */
+    int32_t exact_fingerprint;    /* != 0: reference FNV weights checksum (hashed on the GPU, default);  */
+                                  /* 0: a fast identity that is NOT the reference's (opt-in)          */
     int32_t flags;                /* TKV_FLAG_*                                                     */
     int64_t host_spill_tokens;    /* pinned, device-mapped host tier for chunks that do not fit the  */
                                   /* HBM store (0 = none); the gather kernel reads it zero-copy      */
@@ -82,7 +83,7 @@ typedef struct {
 
 #define TKV_FLAG_SIMT_GEMM 0x1    /* bf16: use the SIMT GEMM instead of tcgen05 (debug/compare)  */
 #define TKV_FLAG_SIMT_ATTN 0x2    /* bf16: use the SIMT attention instead of tcgen05              */
-#define TKV_FLAG_NO_GRAPHS 0x4    /* do not capture prefill launch chains into CUDA graphs        */
+/* 0x4: reserved */
 #define TKV_FLAG_NO_PDL 0x8       /* launch kernels without programmatic dependent launch          */
 #define TKV_FLAG_L2_PREFETCH 0x10  /* reserved (attention-time L2 weight prefetch: measured no gain) */
 #define TKV_FLAG_BATCH_ATTN 0x20   /* batched prefill: one attention launch even when the batch cannot fill the GPU */
@@ -180,7 +181,10 @@ tkv_status tkv_assemble(tkv_engine* eng, const uint64_t* chunk_ids, int64_t n, t
  * in place; logits_out[vocab] receives the last query token's logits (the TTFT logits). */
 tkv_status tkv_prefill_query(tkv_engine* eng, tkv_context* ctx, const int32_t* query, int64_t n,
                              float* logits_out, tkv_flops* flops);
-/* Same, with tokens and logits already in device memory (no host copies, no sync). */
+/* Same, with tokens and logits already in device memory (no host copies, no sync). Device-side errors of
+ * this call (token outside vocab, non-finite logits, degenerate rows) are deferred: tkv_engine_check reports
+ * them. The context keeps no host logits, so tkv_greedy_decode on it fails with TKV_ERR_DOMAIN. */
+tkv_status tkv_engine_check(tkv_engine* eng); /* sync the engine stream; report deferred device errors */
 tkv_status tkv_prefill_query_device(tkv_engine* eng, tkv_context* ctx, const int32_t* d_query, int64_t n,
                                     float* d_logits_out);
 /* Batched query prefill (BASELINE config 3: batch 32): request r prefills queries[offsets[r], offsets[r+1]) over
@@ -263,6 +267,14 @@ tkv_status tkv_debug_set_mask_fault(tkv_engine* eng, int64_t row, int64_t col);
  * the [lo, hi] row predicate; q [Tq, H*d], k/v [Tk, Hkv*d], out [Tq, H*d]. impl: 0 = the engine's choice
  * (tcgen05 for bf16 head_size 128), 1 = SIMT, 2 = the decode-sized kernel (bf16, d = 128, Tq * H / Hkv in
  * {4, 7, 8, 16}). */
+/* weights_checksum / model_fingerprint (model.cpp:94-118) of (cfg, seed): device >= 0 hashes on that GPU
+ * (the engine's path), device = -1 streams the generator through FNV-1a on one host core (slow; tests). */
+tkv_status tkv_debug_weights_checksum(const tkv_model_config* cfg, uint64_t seed, int device, uint64_t* checksum,
+                                      uint64_t* fingerprint);
+/* Rows [row0, row0 + nrows) of a device weight tensor as float32 (bf16 widened), in the device layout ([out][in]):
+ * which 0 = Wqkv (wq | wk | wv rows), 1 = Wo, 2 = Wgu (gate / up rows interleaved in 64-row blocks when
+ * intermediate_size % 64 == 0), 3 = Wdown, 4 = lm_head, 5 = embedding (f32 [vocab][hidden]). */
+tkv_status tkv_debug_weight_rows(tkv_engine* eng, int64_t layer, int which, int64_t row0, int64_t nrows, float* out);
 tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* A, const float* W, int64_t M,
                           int64_t N, int64_t K, int splits, float* out);
 /* GEMM tuning/timing (tools/gemm_sweep.py): knobs = ring stages, smem budget KB, CTAs per SM, weight

@@ -131,6 +131,10 @@ class Port:
             L.tko_model_destroy.argtypes = [C.c_void_p]
             L.tko_weights_checksum.restype = C.c_uint64
             L.tko_weights_checksum.argtypes = [C.c_void_p]
+            L.tko_weights_checksum_stream.restype = C.c_uint64
+            L.tko_weights_checksum_stream.argtypes = [C.POINTER(OracleCfg), C.c_uint64]
+            L.tko_fingerprint_of.restype = C.c_uint64
+            L.tko_fingerprint_of.argtypes = [C.POINTER(OracleCfg), C.c_uint64]
             L.tko_model_fingerprint.restype = C.c_uint64
             L.tko_model_fingerprint.argtypes = [C.c_void_p]
             L.tko_weight.restype = F64P
@@ -171,6 +175,13 @@ class Port:
     def _check(self, rc: int):
         if rc:
             raise OracleError(rc, self.lib().tko_last_error().decode())
+
+    @classmethod
+    def stream_identity(cls, cfg: Cfg, seed: int):
+        """(checksum, fingerprint) streamed from the generator: no materialised weights (full-size models)."""
+        L = cls.lib()
+        ck = L.tko_weights_checksum_stream(C.byref(cfg.c()), seed)
+        return ck, L.tko_fingerprint_of(C.byref(cfg.c()), ck)
 
     def checksum(self) -> int:
         return self.lib().tko_weights_checksum(self.h)

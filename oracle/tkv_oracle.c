@@ -213,6 +213,55 @@ uint64_t tko_weights_checksum(tko_model* m) {
     return f.h;
 }
 
+/* weights_checksum (model.cpp:94-112) over init_random's draws (model.cpp:68-92) WITHOUT materialising the
+ * weights: the same bytes in the same order, each value drawn on the fly (full-size models are 52 GB of f64). */
+static void ck_draws(fnv* f, uint64_t seed, uint64_t* cursor, int64_t r, int64_t c, double scale) {
+    fnv_u64(f, (uint64_t)r);
+    fnv_u64(f, (uint64_t)c);
+    const uint64_t n = (uint64_t)(r * c);
+    for (uint64_t i = 0; i < n; ++i) {
+        const double u = (double)(tko_splitmix_at(seed, *cursor + i) >> 11) * 0x1.0p-53;
+        fnv_f64(f, (2.0 * u - 1.0) * scale);
+    }
+    *cursor += n;
+}
+static void ck_ones(fnv* f, int64_t n) {
+    fnv_u64(f, (uint64_t)n);
+    for (int64_t i = 0; i < n; ++i) fnv_f64(f, 1.0);
+}
+uint64_t tko_weights_checksum_stream(const tko_config* c, uint64_t seed) {
+    const int64_t qd = c->head_num * c->head_size, kvd = c->kv_head_num * c->head_size, H = c->hidden_size;
+    const int64_t I = c->intermediate_size;
+    const double scale = 1.0 / sqrt((double)H);
+    uint64_t cur = 0;
+    fnv f;
+    fnv_init(&f);
+    ck_draws(&f, seed, &cur, c->vocab_size, H, scale);
+    for (int64_t l = 0; l < c->layer_num; ++l) {
+        ck_ones(&f, H);
+        ck_ones(&f, H);
+        ck_draws(&f, seed, &cur, H, qd, scale);
+        ck_draws(&f, seed, &cur, H, kvd, scale);
+        ck_draws(&f, seed, &cur, H, kvd, scale);
+        ck_draws(&f, seed, &cur, qd, H, scale);
+        ck_draws(&f, seed, &cur, H, I, scale);
+        ck_draws(&f, seed, &cur, H, I, scale);
+        ck_draws(&f, seed, &cur, I, H, scale);
+    }
+    ck_ones(&f, H);
+    ck_draws(&f, seed, &cur, H, c->vocab_size, scale);
+    return f.h;
+}
+
+/* model_fingerprint (model.cpp:114-118) from a streamed checksum */
+uint64_t tko_fingerprint_of(const tko_config* c, uint64_t checksum) {
+    fnv f;
+    fnv_init(&f);
+    fnv_u64(&f, tko_fingerprint_seed(c));
+    fnv_u64(&f, checksum);
+    return f.h;
+}
+
 /* model_fingerprint (model.cpp:114-118) */
 uint64_t tko_model_fingerprint(tko_model* m) {
     fnv f;

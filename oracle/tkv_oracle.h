@@ -78,6 +78,11 @@ int tko_prefill_query(const tko_model* m, const double* ctx_k, const double* ctx
 int tko_naive_prefill(const tko_model* m, const int32_t* tokens, const int64_t* offsets, int64_t n_chunks,
                       const int32_t* q, int64_t nq, int independent, double* logits);
 
+/* weights_checksum (model.cpp:94-112) streamed from the generator (no materialised weights), and
+ * model_fingerprint (model.cpp:114-118) of a checksum. */
+uint64_t tko_weights_checksum_stream(const tko_config* c, uint64_t seed);
+uint64_t tko_fingerprint_of(const tko_config* c, uint64_t checksum);
+
 /* rope_rotate_heads_inplace (rope.cpp:75-88). */
 int tko_rope_rotate(double* rows, int64_t n_rows, int64_t cols, const int64_t* positions, int64_t head_size,
                     double base);

@@ -30,9 +30,11 @@
 namespace tkv {
 
 static thread_local std::string g_last_error;
-static std::atomic<bool> g_pdl{true};
-bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed); }
-void set_pdl_enabled(bool on) { g_pdl.store(on, std::memory_order_relaxed); }
+// PDL on/off is an ENGINE option (TKV_FLAG_NO_PDL): every ABI entry binds its engine, which sets the calling
+// thread's launch mode, so engines with different flags can share a process.
+static thread_local bool g_pdl = true;
+bool pdl_enabled() { return g_pdl; }
+void set_pdl_enabled(bool on) { g_pdl = on; }
 
 void fail(tkv_status code, const std::string& msg) { throw Failure{code, msg}; }
 
@@ -128,13 +130,6 @@ static uint64_t fp_seed(const tkv_model_config& c) {  // config.cpp:31-42
     return f.h;
 }
 
-static uint64_t total_draws(const tkv_model_config& c) {
-    const uint64_t H = c.hidden_size, qd = c.head_num * c.head_size, kvd = c.kv_head_num * c.head_size,
-                   I = c.intermediate_size;
-    const uint64_t per_layer = H * qd + 2 * H * kvd + qd * H + 2 * H * I + I * H;
-    return (uint64_t)c.vocab_size * H + (uint64_t)c.layer_num * per_layer + H * (uint64_t)c.vocab_size;
-}
-
 // weights_checksum (model.cpp:94-112) streamed from the generator: same bytes as hashing the f64 tensors.
 static uint64_t weights_checksum_stream(const tkv_model_config& c, uint64_t seed) {
     const int64_t H = c.hidden_size, qd = c.head_num * c.head_size, kvd = c.kv_head_num * c.head_size,
@@ -171,6 +166,55 @@ static uint64_t weights_checksum_stream(const tkv_model_config& c, uint64_t seed
     ones(H);
     mat(H, c.vocab_size);
     return f.h;
+}
+
+// The same byte stream as weights_checksum_stream, as the word segments the device hash consumes
+// (fingerprint.cu): every dimension header a literal word, every norm vector a run of 1.0, every matrix a
+// range of generator draws.
+static std::vector<FpSeg> checksum_segments(const tkv_model_config& c) {
+    const int64_t H = c.hidden_size, qd = c.head_num * c.head_size, kvd = c.kv_head_num * c.head_size,
+                  I = c.intermediate_size;
+    const double scale = 1.0 / std::sqrt((double)H);
+    std::vector<FpSeg> segs;
+    uint64_t word = 0, cur = 0;
+    auto lit = [&](uint64_t v, uint64_t n) {
+        segs.push_back(FpSeg{word, n, v, 0.0, n == 1 ? 0 : 1, 0});
+        word += n;
+    };
+    auto mat = [&](int64_t r, int64_t cc) {
+        lit((uint64_t)r, 1);
+        lit((uint64_t)cc, 1);
+        const uint64_t n = (uint64_t)(r * cc);
+        segs.push_back(FpSeg{word, n, cur, scale, 2, 0});
+        word += n;
+        cur += n;
+    };
+    uint64_t one_bits;
+    const double one = 1.0;
+    std::memcpy(&one_bits, &one, 8);
+    auto ones = [&](int64_t n) {
+        lit((uint64_t)n, 1);
+        lit(one_bits, (uint64_t)n);
+    };
+    mat(c.vocab_size, H);
+    for (int64_t l = 0; l < c.layer_num; ++l) {
+        ones(H);
+        ones(H);
+        mat(H, qd);
+        mat(H, kvd);
+        mat(H, kvd);
+        mat(qd, H);
+        mat(H, I);
+        mat(H, I);
+        mat(I, H);
+    }
+    ones(H);
+    mat(H, c.vocab_size);
+    return segs;
+}
+
+static uint64_t weights_checksum_device(const tkv_model_config& c, uint64_t seed, cudaStream_t s) {
+    return device_fnv_words(checksum_segments(c), seed, Fnv{}.h, s);
 }
 
 static uint64_t fingerprint_of(const tkv_model_config& c, uint64_t checksum) {  // model.cpp:114-118
@@ -342,7 +386,10 @@ struct tkv_engine {
     int64_t fault_row = -1, fault_col = -1;
 
     ~tkv_engine();
-    void bind() const { TKV_CUDA(cudaSetDevice(device)); }
+    void bind() const {
+        TKV_CUDA(cudaSetDevice(device));
+        set_pdl_enabled(!(opts.flags & TKV_FLAG_NO_PDL));
+    }
 
     // ---- profiling ----
     cudaEvent_t take_event() {
@@ -924,7 +971,10 @@ void extend(tkv_engine* e, tkv_context* c, const int32_t* host_tok, const int32_
     c->total = P + n;
     c->extend_query_segment(n);
     c->next_position += n;
+    // device-only calls leave no host logits: a later greedy_decode fails cleanly instead of decoding from the
+    // logits of an earlier prefill (its device errors surface at tkv_engine_check)
     if (host_logits) c->last_logits.assign(host_logits, host_logits + e->V);
+    else c->last_logits.clear();
 }
 
 tkv_context* assemble_impl(tkv_engine* e, const uint64_t* ids, int64_t n, int mode) {
@@ -1285,11 +1335,13 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
             fail(TKV_ERR_CONFIG, "head_size must be one of 8/16/32/64/128 for the device kernels");
 
         // ---- identity chain ----
-        const uint64_t draws = total_draws(c);
-        e->exact_fp = e->opts.exact_fingerprint > 0 || (e->opts.exact_fingerprint < 0 && draws <= 600000000ULL);
+        // reference-exact at every size: the FNV-1a of all f64 weights, hashed in parallel on the device
+        // (fingerprint.cu; 52 GB of hashed bytes for Qwen2-7B); exact_fingerprint = 0 opts into a fast
+        // non-reference identity
+        e->exact_fp = e->opts.exact_fingerprint != 0;
         if (e->exact_fp) {
-            e->fingerprint = fingerprint_of(c, weights_checksum_stream(c, seed));
-        } else {  // documented fast identity for full-size models
+            e->fingerprint = fingerprint_of(c, weights_checksum_device(c, seed, e->stream));
+        } else {  // opt-in fast identity: NOT the reference's
             Fnv f;
             f.u64(fp_seed(c));
             f.u64(seed);
@@ -1348,16 +1400,19 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         e->launches += 3 + 7 * e->L;
 
         e->err.ensure(64);
+#ifdef TKV_TUNING
+        // Tuning / cost-attribution knobs (tools/*.sh). Compiled into TUNING builds only (make TUNING=1): several
+        // of them skip work or change numerics, so the release library never reads them.
         if (const char* pfm = getenv("TKV_L2_PREFETCH_MB")) e->l2_prefetch_bytes = (size_t)atol(pfm) << 20;
         if (const char* sk = getenv("TKV_TIMING_SKIP")) e->skip_mask = atoi(sk);
         if (const char* tl = getenv("TKV_TRACE_LAYER")) e->trace_layer = atoi(tl);
-        if (const char* as = getenv("TKV_ATTN_SPLITS")) e->attn_split_override = atoi(as);
+        if (const char* as = getenv("TKV_ATTN_SPLITS")) e->attn_split_override = std::min(32, std::max(0, atoi(as)));
         if (const char* dr = getenv("TKV_DECODE_ROWS")) e->decode_rows_max = atol(dr);
         if (const char* np = getenv("TKV_GEMM_NEXT_PF")) set_gemm_next_pf(atoi(np));
         if (const char* mp = getenv("TKV_GEMM_NSMP")) set_gemm_nsmp(atoi(mp));
         if (const char* gc = getenv("TKV_GEMM_CLUSTER")) set_gemm_cluster(atoi(gc));
         if (const char* fm = getenv("TKV_FUSED_MLP")) e->fused_mlp = atoi(fm);
-        if (const char* bs = getenv("TKV_BATCH_ATTN_SPLITS")) e->batch_attn_splits = atoi(bs);
+        if (const char* bs = getenv("TKV_BATCH_ATTN_SPLITS")) e->batch_attn_splits = std::min(32, std::max(0, atoi(bs)));
         if (const char* se = getenv("TKV_GEMM_SKIP_EPI")) set_gemm_skip_epi(atoi(se));
         if (const char* ra = getenv("TKV_GEMM_RASTER")) set_gemm_raster(atoi(ra));
         if (const char* gm = getenv("TKV_GEMM_GROUP_MB")) set_gemm_raster(1, atoi(gm));
@@ -1366,6 +1421,7 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
             if (sscanf(gk, "%d,%d,%d,%d,%d,%d,%d", &st, &sm, &cps, &ef, &np, &pf, &kr) >= 3)
                 set_gemm_knobs(st, sm, cps, ef, np, pf, kr);
         }
+#endif
         TKV_CUDA(cudaMemsetAsync(e->err.p, 0, 64, e->stream));
         e->logits.ensure((size_t)V * 4);
         e->ensure_rope(e->opts.max_position > 0 ? e->opts.max_position - 1 : 32767);
@@ -1443,7 +1499,16 @@ tkv_status tkv_ingest_chunks(tkv_engine* e, const int32_t* payloads, const int64
             const uint64_t id = content_id(e->fingerprint, framed.data(), (int64_t)framed.size());
             if (ids_out) ids_out[c] = id;
             if (stats) stats->chunks += 1;
-            if (e->chunks.count(id) || batch_ids.count(id)) continue;  // idempotent (pipeline.cpp:104-123)
+            auto known = e->chunks.find(id);
+            if (known != e->chunks.end()) {
+                // idempotent: no prefill, no bytes written (pipeline.cpp:104-123) -- but, like the reference
+                // (:124-131), a chunk that reached the store without a record (TKVC import) gets its framed
+                // tokens and its retrieval-index entry now
+                if (known->second.framed.empty()) known->second.framed = framed;
+                if (n > 0 && !e->idx_row.count(id)) e->index_add(id, framed.data() + 1, n, nullptr);
+                continue;
+            }
+            if (batch_ids.count(id)) continue;
             batch_ids.insert(id);
             todo.push_back({id, std::move(framed)});
         }
@@ -1582,8 +1647,8 @@ tkv_status tkv_import_tkvc(tkv_engine* e, const char* path, uint64_t* id_out) {
         Chunk ch;
         ch.len = ntok;
         store_chunk_pages(e, ch);
+        try {
         // convert f64/f32 -> f32 -> engine dtype on the host, page by page, then one H2D per page
-        const size_t es = dt_size(e->dt);
         std::vector<uint8_t> page(e->page_bytes);
         for (size_t p = 0; p < ch.pages.size(); ++p) {
             std::fill(page.begin(), page.end(), 0);
@@ -1618,7 +1683,10 @@ tkv_status tkv_import_tkvc(tkv_engine* e, const char* path, uint64_t* id_out) {
                         }
                 }
             TKV_CUDA(cudaMemcpy(page_ptr(e, ch.slot, ch.pages[p]), page.data(), e->page_bytes, cudaMemcpyDefault));
-            (void)es;
+        }
+        } catch (...) {
+            release_chunk_pages(e, ch);  // a failed copy must not leak store capacity
+            throw;
         }
         e->chunks.emplace(id, std::move(ch));
     });
@@ -1906,6 +1974,61 @@ tkv_status tkv_prefill_query_device(tkv_engine* e, tkv_context* c, const int32_t
         if (c->eng != e) fail(TKV_ERR_STALE_CACHE, "context was assembled under a different model");
         e->bind();
         extend(e, c, nullptr, d_query, n, nullptr, d_logits);
+    });
+}
+
+tkv_status tkv_debug_weights_checksum(const tkv_model_config* cfg, uint64_t seed, int device, uint64_t* checksum,
+                                      uint64_t* fingerprint) {
+    return guard([&] {
+        need(cfg, "cfg");
+        validate_cfg(*cfg);
+        uint64_t ck;
+        if (device < 0) {
+            ck = weights_checksum_stream(*cfg, seed);
+        } else {
+            TKV_CUDA(cudaSetDevice(device));
+            ck = weights_checksum_device(*cfg, seed, 0);
+        }
+        if (checksum) *checksum = ck;
+        if (fingerprint) *fingerprint = fingerprint_of(*cfg, ck);
+    });
+}
+
+tkv_status tkv_debug_weight_rows(tkv_engine* e, int64_t layer, int which, int64_t row0, int64_t nrows, float* out) {
+    return guard([&] {
+        need(e, "engine");
+        need(out, "out");
+        e->bind();
+        const void* base = nullptr;
+        int64_t rows = 0, cols = 0;
+        bool f32 = e->dt == DT::F32;
+        if (which == 4 || which == 5) {
+            rows = e->V, cols = e->hid;
+            base = which == 4 ? e->w_lm : (const void*)e->emb;
+            if (which == 5) f32 = true;
+        } else {
+            if (layer < 0 || layer >= e->L) fail(TKV_ERR_SHAPE, "layer out of range");
+            const void* t[] = {e->w_qkv[layer], e->w_o[layer], e->w_gu[layer], e->w_down[layer]};
+            const int64_t r[] = {e->nqkv, e->hid, 2 * e->I, e->hid}, c[] = {e->hid, e->qd, e->hid, e->I};
+            if (which < 0 || which > 3) fail(TKV_ERR_DOMAIN, "which must be 0..5");
+            base = t[which], rows = r[which], cols = c[which];
+        }
+        if (row0 < 0 || nrows < 0 || row0 + nrows > rows) fail(TKV_ERR_SHAPE, "rows out of range");
+        const size_t es = f32 ? 4 : 2;
+        DevMem tmp;
+        tmp.ensure((size_t)(nrows * cols) * 4);
+        launch_to_f32(static_cast<const uint8_t*>(base) + (size_t)(row0 * cols) * es, nrows * cols, tmp.as<float>(),
+                      f32 ? DT::F32 : DT::BF16, e->stream);
+        TKV_CUDA(cudaMemcpyAsync(out, tmp.p, (size_t)(nrows * cols) * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+    });
+}
+
+tkv_status tkv_engine_check(tkv_engine* e) {
+    return guard([&] {
+        need(e, "engine");
+        e->bind();
+        e->check_err("deferred device work");
     });
 }
 

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/tkv.h"
 
@@ -196,6 +197,15 @@ size_t index_topk_scratch_bytes(int64_t n, int k);
 int64_t launch_index_top_k(const double* emb, const double* nb, const uint64_t* ids, int64_t n, int64_t cap,
                            const double* q, double na, int k, void* scratch, uint64_t* ids_out, double* scores_out,
                            cudaStream_t s);
+// Reference-exact weights_checksum on the device (fingerprint.cu): FNV-1a 64 over a stream of 8-byte words given
+// as segments -- kind 0 literal / 1 constant: the word `a` repeated n times; kind 2: the draws
+// next_signed(seed, a + i) * scale (init_random, model.cpp:15-21). Returns the hash continued from h0.
+struct FpSeg {
+    uint64_t word0, n, a;
+    double scale;
+    int32_t kind, pad;
+};
+uint64_t device_fnv_words(const std::vector<FpSeg>& segs, uint64_t seed, uint64_t h0, cudaStream_t s);
 // Decode-sized attention (attn_decode.cu): bf16, d = 128, Tq * group in {4, 7, 8, 16} rows per kv head; split-K
 // flash decoding on CUDA cores with the SIMT workspace layout, merged by launch_attention_combine.
 bool attention_decode_supported(int Tq, int H, int Hkv, int d, DT dt);

@@ -69,7 +69,9 @@ class Dtype(enum.IntEnum):
 
 FLAG_SIMT_GEMM = 0x1
 FLAG_SIMT_ATTN = 0x2
-FLAG_NO_GRAPHS = 0x4
+FLAG_NO_PDL = 0x8
+FLAG_BATCH_ATTN = 0x20
+FLAG_DECODE_ATTN = 0x40
 
 DOC_START, DOC_END, EOS, VOCAB = 256, 257, 258, 259  # tokenizer.hpp:19-22
 
@@ -114,6 +116,9 @@ def lib():
         L.tkv_config_fingerprint_seed.restype = C.c_uint64
         L.tkv_config_fingerprint_seed.argtypes = [C.POINTER(_Cfg)]
         L.tkv_weights_identity.argtypes = [C.POINTER(_Cfg), C.c_uint64, U64P, U64P]
+        L.tkv_debug_weights_checksum.argtypes = [C.POINTER(_Cfg), C.c_uint64, C.c_int, U64P, U64P]
+        L.tkv_engine_check.argtypes = [C.c_void_p]
+        L.tkv_debug_weight_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int64, F32P]
         L.tkv_chunk_content_id.restype = C.c_uint64
         L.tkv_chunk_content_id.argtypes = [C.c_uint64, I32P, C.c_int64]
         L.tkv_engine_opts_default.argtypes = [C.POINTER(_Opts)]
@@ -276,6 +281,13 @@ def weights_identity(config: ModelConfig, seed: int):
     return ck.value, fp.value
 
 
+def weights_identity_device(config: ModelConfig, seed: int, device: int = 0):
+    """(weights_checksum, model_fingerprint) hashed on GPU `device` (the engine's path, fingerprint.cu)."""
+    ck, fp = C.c_uint64(), C.c_uint64()
+    _check(lib().tkv_debug_weights_checksum(C.byref(config._c()), seed, device, C.byref(ck), C.byref(fp)))
+    return ck.value, fp.value
+
+
 def chunk_content_id(framed, model_fingerprint: int) -> int:
     """kvstore.cpp:58-64"""
     f = _i32(framed)
@@ -407,6 +419,16 @@ class Engine:
         out = C.c_uint64()
         _check(lib().tkv_engine_fingerprint(self._h, C.byref(out)))
         return out.value
+
+    def check(self) -> None:
+        """Synchronise the engine stream and raise deferred device errors (tkv_engine_check)."""
+        _check(lib().tkv_engine_check(self._h))
+
+    def weight_rows(self, layer: int, which: int, row0: int, nrows: int, cols: int) -> np.ndarray:
+        """Device weight rows as float32 (tkv_debug_weight_rows; layout in include/tkv.h)."""
+        out = np.zeros((nrows, cols), np.float32)
+        _check(lib().tkv_debug_weight_rows(self._h, layer, which, row0, nrows, _p(out, F32P)))
+        return out
 
     # ---- offline precompute ----
     def ingest_chunks(self, payloads, stats: IngestStats | None = None) -> list[int]:

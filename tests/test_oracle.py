@@ -161,3 +161,33 @@ def test_retrieval_restatement_matches_reference():
             assert np.all(np.diff(scores) <= 0)
     with pytest.raises(O.OracleError):
         O.Port.top_k(emb, ids, q, 0)
+
+
+def test_streamed_identity_equals_reference(golden):
+    """The streamed weights_checksum (no materialised weights; used for the full-size identities in
+    tests/golden/identity_full.json) equals the reference's own checksum at every size it can hold here."""
+    meta, _ = golden
+    g = meta["toy_identity"]
+    assert O.Port.stream_identity(O.TOY, 42) == (int(g["checksum42"], 16), int(g["fingerprint42"], 16))
+    assert O.Port.stream_identity(O.TOY, 7)[0] == int(g["checksum7"], 16)
+    q1 = meta["qwen1"]
+    assert O.Port.stream_identity(cfg_of(q1), q1["seed"])[1] == int(q1["fingerprint"], 16)
+    if O.Ref.available():
+        for cfg, seed in ((O.Cfg(2, 4, 2, 16, 64, 96), 5), (O.Cfg(1, 8, 8, 32, 256, 512, 300, 5e5, 1e-5), 11)):
+            assert O.Port.stream_identity(cfg, seed) == O.Ref.identity(cfg, seed)[:2]
+
+
+def test_large_golden_ids_follow_the_reference_identity():
+    """golden_large chunk ids are FNV(fingerprint, framed tokens) under the case's reference fingerprint."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "golden_large.json")
+    meta = json.load(open(path))
+    A = np.load(path.replace(".json", ".npz"))
+    for name, m in meta.items():
+        fp = int(m["fingerprint"], 16)
+        offs = A[f"{name}.payload_offsets"]
+        pays = [A[f"{name}.payloads"][offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
+        for p, cid in zip(pays, m["ids"]):
+            f = O.frame(p)
+            assert O.Port.lib().tko_chunk_content_id(fp, f.ctypes.data_as(O.I32P), len(f)) == int(cid, 16)
