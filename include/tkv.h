@@ -231,7 +231,8 @@ typedef struct {
 } tkv_ipc_handle;
 /* cudaIpcGetMemHandle of this engine's page pool (one process per GPU: share it with the peers). */
 tkv_status tkv_store_export_ipc(tkv_engine* eng, tkv_ipc_handle* out, uint64_t* pool_bytes);
-/* Map a peer process's pool (cudaIpcOpenMemHandle, lazy peer access) into peer slot `slot` (1..15). */
+/* Map a peer process's pool (cudaIpcOpenMemHandle, lazy peer access) into peer slot `slot` (1..14). The raw
+ * handle carries no model identity or geometry: prefer tkv_store_import_directory, which validates both. */
 tkv_status tkv_store_attach_ipc(tkv_engine* eng, int32_t slot, const tkv_ipc_handle* handle);
 /* Same, for a peer engine in this process (possibly another GPU: enables peer access). */
 tkv_status tkv_store_attach_engine(tkv_engine* eng, int32_t slot, tkv_engine* peer);
@@ -244,6 +245,19 @@ tkv_status tkv_store_register_remote(tkv_engine* eng, uint64_t chunk_id, int32_t
                                      const int32_t* pages, int64_t n_pages, const int32_t* framed);
 /* Copy a registered remote chunk into the local store (fetch-once cache policy). */
 tkv_status tkv_store_fetch_remote(tkv_engine* eng, uint64_t chunk_id);
+/* Store directory blob of this engine's locally owned chunks (ids, token counts, page lists, framed tokens) with
+ * its pool's IPC handle, fingerprint and page geometry: what a peer needs to read these chunks over NVLink.
+ * buf = NULL returns the size only. Little-endian layout: "TKVD", u32 version, u64 fingerprint, u64 page_bytes,
+ * i64 page_tokens, i64 pool pages, 64 B cudaIpcMemHandle, i64 n, then n x {u64 id, i64 len, i64 n_pages,
+ * i32 pages[n_pages], i64 n_framed, i32 framed[n_framed]} sorted by id. Exported chunks become SHARED: peers
+ * read their pages, so tkv_store_evict refuses them (TKV_ERR_CONFIG). The transport (NCCL, MPI, sockets,
+ * torch.distributed) is the caller's. */
+tkv_status tkv_store_export_directory(tkv_engine* eng, uint8_t* buf, int64_t capacity, int64_t* size);
+/* Register a peer's directory under peer slot `slot` (1..14): TKV_ERR_STALE_CACHE when the fingerprint or the
+ * page geometry differs from this engine's, TKV_ERR_FORMAT for a corrupt blob or a page index outside the
+ * peer's pool (nothing is registered then); opens the peer pool through its IPC handle unless the slot is
+ * already attached (tkv_store_attach_engine for a peer engine in this process). */
+tkv_status tkv_store_import_directory(tkv_engine* eng, int32_t slot, const uint8_t* blob, int64_t size);
 /* KV bytes read from peer pools so far (NVLink traffic of the gather + fetches). */
 int64_t tkv_remote_bytes(const tkv_engine* eng);
 
@@ -256,6 +270,9 @@ tkv_status tkv_profile_read(tkv_engine* eng, const char* kernel_class, double* t
 tkv_status tkv_profile_reset(tkv_engine* eng);
 /* Count of kernels launched by the engine since creation (all classes). */
 int64_t tkv_launch_count(const tkv_engine* eng);
+/* Host->device and device->host bytes the engine has copied for its callers since creation (query tokens,
+ * positions, mask ranges, gather descriptors, logits, error words): the e2e accounting of bench.py. */
+tkv_status tkv_io_bytes(const tkv_engine* eng, int64_t* h2d, int64_t* d2h);
 
 /* Debug: corrupt the independent mask of the next naive prefill (testing::mask_fault_hook,
  * include/turbokv/pipeline.hpp:57-62): lets row `row` see column `col`. row < 0 disables. */

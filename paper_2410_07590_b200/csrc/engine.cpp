@@ -311,6 +311,7 @@ struct Chunk {
     std::vector<int32_t> pages;
     std::vector<int32_t> framed;  // empty for TKVC-imported chunks
     int32_t slot = 0;             // page pool holding the pages: 0 = local HBM, >0 = a peer GPU (NVLink)
+    bool shared = false;          // listed in an exported directory: peers read its pages, so it cannot be evicted
 };
 
 }  // namespace tkv
@@ -361,6 +362,7 @@ struct tkv_engine {
     void index_add(uint64_t id, const int32_t* payload, int64_t n, bool* added);
     std::unordered_map<uint64_t, Chunk> chunks;
     PoolTable pools;                     // slot 0 = pool.p; peers attached via IPC or same-process P2P
+    int64_t peer_pages[kMaxPools] = {};  // page count of each attached peer pool (0 = unknown: raw IPC attach)
     std::vector<void*> ipc_opened;       // peer pools opened with cudaIpcOpenMemHandle (closed on destroy)
     int64_t remote_bytes = 0;            // bytes of KV gathered from peer pools (bench reporting)
 
@@ -438,8 +440,10 @@ struct tkv_engine {
     // ---- helpers ----
     void sync() { TKV_CUDA(cudaStreamSynchronize(stream)); }
     // copy host data into the current staging slot at `off` and enqueue its H2D copy
+    int64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device bytes moved by the request path (bench e2e accounting)
     void upload(uint8_t* slot, void* dst, const void* src, size_t bytes, size_t off) {
         if (bytes == 0) return;
+        h2d_bytes += (int64_t)bytes;
         std::memcpy(slot + off, src, bytes);
         TKV_CUDA(cudaMemcpyAsync(dst, slot + off, bytes, cudaMemcpyHostToDevice, stream));
     }
@@ -640,6 +644,7 @@ tkv_engine::~tkv_engine() {
 void tkv_engine::check_err(const char* where) {
     int e = 0;
     TKV_CUDA(cudaMemcpyAsync(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    d2h_bytes += sizeof(int);
     sync();
     if (e == 0) return;
     TKV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
@@ -964,6 +969,7 @@ void extend(tkv_engine* e, tkv_context* c, const int32_t* host_tok, const int32_
         TKV_CUDA(cudaMemcpyAsync(dev_logits, e->logits.p, e->V * 4, cudaMemcpyDeviceToDevice, e->stream));
     if (host_logits) {
         TKV_CUDA(cudaMemcpyAsync(host_logits, e->logits.p, e->V * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->d2h_bytes += e->V * 4;
         e->check_err("prefill");
     }
     remember_mask(c, s, P + n);
@@ -1754,6 +1760,8 @@ tkv_status tkv_store_evict(tkv_engine* e, uint64_t id) {
         need(e, "engine");
         auto it = e->chunks.find(id);
         if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(id) + " not in store");
+        if (it->second.shared)
+            fail(TKV_ERR_CONFIG, "chunk " + hex_id(id) + " is listed in an exported directory: peers read its pages");
         release_chunk_pages(e, it->second);  // peer-registered chunks only drop the entry
         e->chunks.erase(it);
         e->store_epoch += 1;
@@ -1929,6 +1937,7 @@ tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int6
             e->d_bmaps.ensure(maps.size());
             TKV_CUDA(cudaMemcpyAsync(e->d_breq.p, rq.data(), rq.size() * sizeof(AttnReq), cudaMemcpyHostToDevice, e->stream));
             TKV_CUDA(cudaMemcpyAsync(e->d_bmaps.p, maps.data(), maps.size(), cudaMemcpyHostToDevice, e->stream));
+            e->h2d_bytes += (int64_t)(rq.size() * sizeof(AttnReq) + maps.size());
             f.batch_reqs = e->d_breq.as<AttnReq>();
             f.batch_maps = e->d_bmaps.p;
             f.batch_max_n = max_n;
@@ -1945,6 +1954,7 @@ tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int6
         e->forward(f);
         std::vector<float> lg((size_t)n_req * e->V);
         TKV_CUDA(cudaMemcpyAsync(lg.data(), e->logits.p, lg.size() * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->d2h_bytes += (int64_t)lg.size() * 4;
         e->check_err("prefill_query_batch");
         if (logits_out) std::memcpy(logits_out, lg.data(), lg.size() * 4);
         for (int64_t r = 0; r < n_req; ++r) {  // the same bookkeeping as prefill_query (pipeline.cpp:166-186)
@@ -2244,6 +2254,14 @@ tkv_status tkv_profile_reset(tkv_engine* e) {
 
 int64_t tkv_launch_count(const tkv_engine* e) { return e ? e->launches : -1; }
 
+tkv_status tkv_io_bytes(const tkv_engine* e, int64_t* h2d, int64_t* d2h) {
+    return guard([&] {
+        need(e, "engine");
+        if (h2d) *h2d = e->h2d_bytes;
+        if (d2h) *d2h = e->d2h_bytes;
+    });
+}
+
 tkv_status tkv_debug_set_mask_fault(tkv_engine* e, int64_t row, int64_t col) {
     return guard([&] {
         need(e, "engine");
@@ -2305,6 +2323,7 @@ tkv_status tkv_store_attach_engine(tkv_engine* e, int32_t slot, tkv_engine* peer
             cudaGetLastError();
         }
         e->pools.p[slot] = peer->pool.p;
+        e->peer_pages[slot] = peer->n_pages;
     });
 }
 
@@ -2334,6 +2353,10 @@ tkv_status tkv_store_register_remote(tkv_engine* e, uint64_t id, int32_t slot, i
         if (!e->pools.p[slot]) fail(TKV_ERR_CONFIG, "peer slot " + std::to_string(slot) + " is not attached");
         if (len < 1 || n_pages != (len + e->page_tokens - 1) / e->page_tokens)
             fail(TKV_ERR_SHAPE, "remote chunk: page count does not match its length");
+        if (e->peer_pages[slot] > 0)
+            for (int64_t i = 0; i < n_pages; ++i)
+                if (pages[i] < 0 || pages[i] >= e->peer_pages[slot])
+                    fail(TKV_ERR_FORMAT, "remote chunk " + hex_id(id) + ": page index outside the peer pool");
         if (e->chunks.count(id)) return;  // already local (or registered): keep the local copy
         Chunk ch;
         ch.len = len;
@@ -2366,6 +2389,134 @@ tkv_status tkv_store_fetch_remote(tkv_engine* e, uint64_t id) {
 }
 
 int64_t tkv_remote_bytes(const tkv_engine* e) { return e ? e->remote_bytes : -1; }
+// ---- directory blobs: the store exchange of a sharded deployment, behind the C ABI ----
+}  // extern "C"
+namespace {
+constexpr uint32_t kDirVersion = 1;
+struct Writer {
+    std::vector<uint8_t> b;
+    void raw(const void* p, size_t n) { b.insert(b.end(), (const uint8_t*)p, (const uint8_t*)p + n); }
+    template <typename T>
+    void v(T x) { raw(&x, sizeof x); }
+};
+struct Reader {
+    const uint8_t* p;
+    size_t n, at = 0;
+    void raw(void* d, size_t k) {
+        if (at + k > n) fail(TKV_ERR_FORMAT, "directory blob truncated");
+        std::memcpy(d, p + at, k);
+        at += k;
+    }
+    template <typename T>
+    T v() {
+        T x;
+        raw(&x, sizeof x);
+        return x;
+    }
+};
+}  // namespace
+extern "C" {
+
+tkv_status tkv_store_export_directory(tkv_engine* e, uint8_t* buf, int64_t capacity, int64_t* size) {
+    return guard([&] {
+        need(e, "engine");
+        need(size, "size");
+        e->bind();
+        Writer w;
+        w.raw("TKVD", 4);
+        w.v<uint32_t>(kDirVersion);
+        w.v<uint64_t>(e->fingerprint);
+        w.v<uint64_t>((uint64_t)e->page_bytes);
+        w.v<int64_t>(e->page_tokens);
+        w.v<int64_t>(e->n_pages);
+        cudaIpcMemHandle_t h;
+        TKV_CUDA(cudaIpcGetMemHandle(&h, e->pool.p));
+        uint8_t hb[64] = {};
+        std::memcpy(hb, &h, sizeof h);
+        w.raw(hb, 64);
+        std::vector<std::pair<uint64_t, Chunk*>> own;
+        for (auto& kv : e->chunks)
+            if (kv.second.slot == 0) own.emplace_back(kv.first, &kv.second);
+        std::sort(own.begin(), own.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        w.v<int64_t>((int64_t)own.size());
+        for (auto& [id, ch] : own) {
+            w.v<uint64_t>(id);
+            w.v<int64_t>(ch->len);
+            w.v<int64_t>((int64_t)ch->pages.size());
+            w.raw(ch->pages.data(), ch->pages.size() * 4);
+            w.v<int64_t>((int64_t)ch->framed.size());
+            w.raw(ch->framed.data(), ch->framed.size() * 4);
+        }
+        *size = (int64_t)w.b.size();
+        if (!buf) return;  // size query
+        if (capacity < *size) fail(TKV_ERR_SHAPE, "directory buffer too small");
+        std::memcpy(buf, w.b.data(), w.b.size());
+        for (auto& [id, ch] : own) ch->shared = true;  // peers will read these pages: no eviction from now on
+    });
+}
+
+tkv_status tkv_store_import_directory(tkv_engine* e, int32_t slot, const uint8_t* blob, int64_t size) {
+    return guard([&] {
+        need(e, "engine");
+        need(blob, "blob");
+        check_slot(slot);
+        e->bind();
+        Reader r{blob, (size_t)size};
+        char magic[4];
+        r.raw(magic, 4);
+        if (std::memcmp(magic, "TKVD", 4) != 0) fail(TKV_ERR_FORMAT, "not a store directory blob");
+        if (r.v<uint32_t>() != kDirVersion) fail(TKV_ERR_FORMAT, "unsupported directory version");
+        const uint64_t fp = r.v<uint64_t>(), page_bytes = r.v<uint64_t>();
+        const int64_t page_tokens = r.v<int64_t>(), n_pages = r.v<int64_t>();
+        uint8_t hb[64];
+        r.raw(hb, 64);
+        if (fp != e->fingerprint)
+            fail(TKV_ERR_STALE_CACHE, "peer store was built under a different model fingerprint");
+        if (page_bytes != (uint64_t)e->page_bytes || page_tokens != e->page_tokens || n_pages < 1)
+            fail(TKV_ERR_STALE_CACHE, "peer store page geometry does not match this engine");
+        struct Entry {
+            uint64_t id;
+            int64_t len;
+            std::vector<int32_t> pages, framed;
+        };
+        std::vector<Entry> ents((size_t)std::max<int64_t>(0, r.v<int64_t>()));
+        for (Entry& en : ents) {  // parse and validate everything before touching the engine
+            en.id = r.v<uint64_t>();
+            en.len = r.v<int64_t>();
+            const int64_t np = r.v<int64_t>();
+            if (en.len < 1 || np != (en.len + e->page_tokens - 1) / e->page_tokens)
+                fail(TKV_ERR_FORMAT, "directory entry " + hex_id(en.id) + ": page count does not match its length");
+            en.pages.resize((size_t)np);
+            r.raw(en.pages.data(), (size_t)np * 4);
+            for (int32_t pg : en.pages)
+                if (pg < 0 || pg >= n_pages)
+                    fail(TKV_ERR_FORMAT, "directory entry " + hex_id(en.id) + ": page index outside the peer pool");
+            const int64_t nf = r.v<int64_t>();
+            if (nf != 0 && nf != en.len) fail(TKV_ERR_FORMAT, "directory entry " + hex_id(en.id) + ": token record");
+            en.framed.resize((size_t)nf);
+            r.raw(en.framed.data(), (size_t)nf * 4);
+        }
+        if (!e->pools.p[slot]) {
+            cudaIpcMemHandle_t mh;
+            std::memcpy(&mh, hb, sizeof mh);
+            void* p = nullptr;
+            TKV_CUDA(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+            e->ipc_opened.push_back(p);
+            e->pools.p[slot] = p;
+        }
+        e->peer_pages[slot] = n_pages;
+        for (Entry& en : ents) {
+            if (e->chunks.count(en.id)) continue;  // already local (or registered): keep it
+            Chunk ch;
+            ch.len = en.len;
+            ch.slot = slot;
+            ch.pages = std::move(en.pages);
+            ch.framed = std::move(en.framed);
+            e->chunks.emplace(en.id, std::move(ch));
+        }
+    });
+}
+
 
 // ---- kernel-level test entry points ----
 namespace {

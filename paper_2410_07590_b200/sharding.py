@@ -3,15 +3,19 @@
 * One process (and one Engine) per GPU. Every chunk has exactly one OWNER rank, chosen by document
   (owner = FNV-1a(doc id) mod world, so all chunks of a document are co-resident); only the owner
   prefills it into its HBM store.
-* Ranks exchange their store directories (chunk id -> page list, token count) and CUDA-IPC handles of
-  their page pools with one all_gather_object over the process group; every rank then registers the
-  other ranks' chunks under a peer slot. No collective runs on the data path: the gather kernel of a
+* Ranks exchange their store directories with one all_gather_object over the process group. A directory
+  is the engine's own serialised blob (tkv_store_export_directory: chunk id -> page list, token count,
+  framed tokens, plus the pool's CUDA-IPC handle, model fingerprint and page geometry), and every rank
+  registers the other ranks' blobs with tkv_store_import_directory, which rejects a peer built under a
+  different model or page geometry and any page index outside the peer's pool. The blob format is in
+  include/tkv.h, so a C/C++ host shards the same way over its own transport (MPI, NCCL, sockets). No collective runs on the data path: the gather kernel of a
   request reads a remote chunk's pages directly from the owner's HBM over NVLink (P2P loads fused
   with the RoPE re-rotation), or the chunk is copied once into the local store (cache policy).
 * The router sends a request to the rank owning most of its chunk tokens, breaking ties by load.
 """
 from __future__ import annotations
 
+import struct
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -27,6 +31,40 @@ def fnv1a64(data: bytes) -> int:
 def owner_of(doc_id: str, world: int) -> int:
     """Owner rank of every chunk of document `doc_id` (ChunkRecord.doc_id, retrieval.hpp:25-30)."""
     return fnv1a64(doc_id.encode()) % world if world > 1 else 0
+
+
+_DIR_HEAD = struct.Struct("<4sIQQqq64sq")
+
+
+def pack_directory(fingerprint: int, page_bytes: int, page_tokens: int, pool_pages: int, ipc: bytes, entries) -> bytes:
+    """The tkv_store_export_directory blob layout (include/tkv.h); entries: (id, length, pages, framed)."""
+    out = [_DIR_HEAD.pack(b"TKVD", 1, fingerprint, page_bytes, page_tokens, pool_pages, ipc, len(entries))]
+    for cid, length, pages, framed in sorted(entries, key=lambda e: e[0]):
+        pages = np.asarray(pages, np.int32)
+        framed = np.asarray(framed if framed is not None else [], np.int32)
+        out += [struct.pack("<Qqq", cid, length, len(pages)), pages.tobytes(), struct.pack("<q", len(framed)),
+                framed.tobytes()]
+    return b"".join(out)
+
+
+def parse_directory(blob: bytes) -> dict:
+    """Decode a directory blob (host-side inspection and tests; the engine validates it itself on import)."""
+    magic, ver, fp, pb, pt, npages, ipc, n = _DIR_HEAD.unpack_from(blob, 0)
+    if magic != b"TKVD" or ver != 1:
+        raise ValueError("not a version-1 store directory blob")
+    at, entries = _DIR_HEAD.size, []
+    for _ in range(n):
+        cid, length, np_ = struct.unpack_from("<Qqq", blob, at)
+        at += 24
+        pages = np.frombuffer(blob, np.int32, np_, at).tolist()
+        at += 4 * np_
+        (nf,) = struct.unpack_from("<q", blob, at)
+        at += 8
+        framed = np.frombuffer(blob, np.int32, nf, at).tolist()
+        at += 4 * nf
+        entries.append((cid, length, pages, framed or None))
+    return {"fingerprint": fp, "page_bytes": pb, "page_tokens": pt, "pool_pages": npages, "ipc": ipc,
+            "entries": entries}
 
 
 @dataclass
@@ -73,12 +111,12 @@ class ShardedStore:
         return ids
 
     def exchange(self, group=None, all_gather_object=None) -> None:
-        """Share directories + IPC pool handles; register every peer's chunks under its slot."""
+        """Share directory blobs; register every peer's chunks under its slot (validated by the engine)."""
         if self.world == 1:
             return
         import torch.distributed as dist
         gather = all_gather_object or dist.all_gather_object
-        local = {"rank": self.rank, "ipc": self.engine.export_ipc(),
+        local = {"rank": self.rank, "blob": self.engine.export_directory(),
                  "dir": [vars(e) for e in self.directory.values() if e.owner == self.rank]}
         everyone = [None] * self.world
         gather(everyone, local, group=group) if all_gather_object is None else gather(everyone, local)
@@ -86,11 +124,10 @@ class ShardedStore:
             if peer["rank"] == self.rank:
                 continue
             slot = self.slot_of(self.rank, peer["rank"])
-            self.engine.attach_ipc(slot, peer["ipc"])
+            self.engine.import_directory(slot, peer["blob"])
             for e in peer["dir"]:
                 entry = DirEntry(**e)
                 self.directory[entry.chunk_id] = entry
-                self.engine.register_remote(entry.chunk_id, slot, entry.length, entry.pages, entry.framed)
 
     def route(self, chunk_ids) -> int:
         """Rank for a request: most locally-owned chunk tokens, then least loaded."""

@@ -167,6 +167,7 @@ def lib():
         L.tkv_profile_enable.argtypes = [C.c_void_p, C.c_int]
         L.tkv_profile_read.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_double), I64P]
         L.tkv_profile_reset.argtypes = [C.c_void_p]
+        L.tkv_io_bytes.argtypes = [C.c_void_p, I64P, I64P]
         L.tkv_launch_count.restype = C.c_int64
         L.tkv_launch_count.argtypes = [C.c_void_p]
         L.tkv_debug_set_mask_fault.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
@@ -176,6 +177,8 @@ def lib():
         L.tkv_store_chunk_pages.argtypes = [C.c_void_p, C.c_uint64, I32P, C.c_int64, I64P, I64P]
         L.tkv_store_register_remote.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, I32P, C.c_int64, I32P]
         L.tkv_store_fetch_remote.argtypes = [C.c_void_p, C.c_uint64]
+        L.tkv_store_export_directory.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, I64P]
+        L.tkv_store_import_directory.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64]
         L.tkv_remote_bytes.restype = C.c_int64
         L.tkv_remote_bytes.argtypes = [C.c_void_p]
         L.tkv_debug_attn_trace.argtypes = [C.c_int, U64P, C.c_int64]
@@ -612,6 +615,18 @@ class Engine:
         C.memmove(h.bytes, handle, 64)
         _check(lib().tkv_store_attach_ipc(self._h, slot, C.byref(h)))
 
+    def export_directory(self) -> bytes:
+        """tkv_store_export_directory: this engine's owned chunks + pool IPC handle + identity, as one blob."""
+        n = C.c_int64()
+        _check(lib().tkv_store_export_directory(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        _check(lib().tkv_store_export_directory(self._h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def import_directory(self, slot: int, blob: bytes) -> None:
+        """tkv_store_import_directory: validate a peer's blob and register its chunks under peer slot `slot`."""
+        _check(lib().tkv_store_import_directory(self._h, slot, blob, len(blob)))
+
     def attach_engine(self, slot: int, peer: "Engine") -> None:
         _check(lib().tkv_store_attach_engine(self._h, slot, peer.handle))
 
@@ -651,6 +666,12 @@ class Engine:
 
     def launch_count(self) -> int:
         return lib().tkv_launch_count(self._h)
+
+    def io_bytes(self) -> tuple[int, int]:
+        """(host->device, device->host) bytes copied by the engine since creation."""
+        h, d = C.c_int64(), C.c_int64()
+        _check(lib().tkv_io_bytes(self._h, C.byref(h), C.byref(d)))
+        return h.value, d.value
 
     def set_mask_fault(self, row: int, col: int) -> None:
         _check(lib().tkv_debug_set_mask_fault(self._h, row, col))

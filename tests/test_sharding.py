@@ -1,5 +1,5 @@
 """CPU, world_size 2 over gloo: the multi-GPU host logic (paper_2410_07590_b200/sharding.py) — document
-ownership, directory + IPC-handle exchange, remote registration under peer slots, locality routing.
+ownership, directory-blob exchange (the tkv_store_export_directory layout), remote registration under peer slots, locality routing.
 The engine is a stand-in with the Engine method surface (no GPU here); the GPU side of remote chunks
 (gather kernel reading a peer pool) is covered by tests/test_gpu_parity.py::test_remote_chunks_*."""
 import os
@@ -34,14 +34,17 @@ class FakeEngine:
     def chunk_pages(self, cid):
         return self.pages[cid]
 
-    def export_ipc(self):
-        return bytes([self.rank]) * 64
+    def export_directory(self):  # the engine's blob layout (include/tkv.h), built host-side
+        return S.pack_directory(FP, 64 * 1024, 64, 1000, bytes([self.rank]) * 64,
+                                [(c, n, p, None) for c, (p, n) in self.pages.items()])
 
-    def attach_ipc(self, slot, handle):
-        self.attached[slot] = handle
-
-    def register_remote(self, cid, slot, length, pages, framed):
-        self.remote[cid] = (slot, length, list(pages), framed)
+    def import_directory(self, slot, blob):  # what tkv_store_import_directory validates and registers
+        d = S.parse_directory(blob)
+        assert d["fingerprint"] == FP and d["page_tokens"] == 64
+        self.attached[slot] = d["ipc"]
+        for cid, length, pages, framed in d["entries"]:
+            assert all(0 <= p < d["pool_pages"] for p in pages)
+            self.remote[cid] = (slot, length, list(pages), framed)
 
     def fetch_remote(self, cid):
         self.fetched.append(cid)

@@ -12,7 +12,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second",
         "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum"]
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+         "ns": 1e-3, "us": 1, "ms": 1e3}  # durations -> microseconds
 
 
 def rows_of(path):
@@ -25,7 +26,7 @@ def rows_of(path):
 
 def main(tag, src="gpurun_out", dst="profiles"):
     out, traffic = [], {}
-    for k in ["gather_rope", "attn_tc_kernel", "attn_tc_combine", "gemm_tc_kernel", "gemm_bigM"]:
+    for k in ["gather_rope", "attn_tc_kernel", "attn_tc_combine", "gemm_tc", "residual_kernel", "qkv_epilogue"]:
         path = os.path.join(src, f"{tag}_full_{k}.ncu-rep")
         if not os.path.exists(path):
             continue
@@ -45,6 +46,9 @@ def main(tag, src="gpurun_out", dst="profiles"):
             t = vals.get("dram__bytes_read.sum", 0) + vals.get("dram__bytes_write.sum", 0)
             traffic.setdefault(k, []).append({"dram_bytes": t, "duration_us": vals.get("gpu__time_duration.sum"),
                                               "grid": vals.get("launch__grid_size")})
+    if len(traffic.get("gemm_tc", [])) == 4:  # one layer's QKV, O, gate/up, down: bytes per layer
+        traffic["gemm_layer"] = [{"dram_bytes": sum(x["dram_bytes"] for x in traffic["gemm_tc"]),
+                                  "duration_us": sum(x["duration_us"] or 0 for x in traffic["gemm_tc"]), "grid": None}]
     with open(os.path.join(dst, f"{tag}_ncu_full_summary.txt"), "w") as f:
         f.write("\n".join(out) + "\n")
     with open(os.path.join(dst, "ncu_traffic.json"), "w") as f:
