@@ -275,8 +275,12 @@ int64_t tkv_launch_count(const tkv_engine* eng);
  * positions, mask ranges, gather descriptors, logits, error words): the e2e accounting of bench.py. */
 tkv_status tkv_io_bytes(const tkv_engine* eng, int64_t* h2d, int64_t* d2h);
 
-/* Debug: corrupt the independent mask of the next naive prefill (testing::mask_fault_hook,
- * include/turbokv/pipeline.hpp:57-62): lets row `row` see column `col`. row < 0 disables. */
+/* Debug (testing::mask_fault_hook, include/turbokv/pipeline.hpp:57-62): override the visible key range of mask rows
+ * of the NEXT naive prefill -- row rows[i] (negative: counted from the end) sees exactly keys [lo[i], hi[i]]; cleared
+ * after that prefill. The reference's `verify --inject-fault` corruption (the last query row loses column 0,
+ * tools/turbokv_main.cpp:593-599) is rows = {-1}, lo = {1}, hi = {N - 1}. */
+tkv_status tkv_debug_set_mask_rows(tkv_engine* eng, const int64_t* rows, const int32_t* lo, const int32_t* hi, int64_t n);
+/* Same, widening: row `row` additionally sees columns down to `col` (a row of chunk 1 may see chunk 0). */
 tkv_status tkv_debug_set_mask_fault(tkv_engine* eng, int64_t row, int64_t col);
 
 /* Kernel-level entry points for unit tests (host buffers in, host fp32 out; inputs are rounded to

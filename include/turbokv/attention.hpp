@@ -1,0 +1,3 @@
+// Reference header name (proj/include/turbokv/attention.hpp) -> the B200 engine shim (see shim.hpp).
+#pragma once
+#include "shim.hpp"

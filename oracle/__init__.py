@@ -356,6 +356,7 @@ class Ref:
             L.ref_naive_prefill.argtypes = [C.c_void_p, I32P, I64P, C.c_int64, I32P, C.c_int64, C.c_int, F64P,
                                             C.POINTER(C.c_void_p)]
             L.ref_greedy_decode.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, I32P, I64P]
+            L.ref_set_inject_fault.argtypes = [C.c_int]
             L.ref_build_mask.argtypes = [I64P, C.c_int64, C.c_int, U8P]
             L.ref_causal_rows.argtypes = [C.c_int64, C.c_int64, U8P]
             L.ref_rope_rotate.argtypes = [F64P, C.c_int64, C.c_int64, I64P, C.c_int64, C.c_double, F64P]

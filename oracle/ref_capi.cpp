@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <limits>
 #include <memory>
 #include <string>
 #include <vector>
@@ -314,6 +315,19 @@ int ref_naive_prefill(void* e, const int32_t* tokens, const int64_t* offsets, in
                     static_cast<size_t>(c->ctx.last_logits.size()) * sizeof(double));
         if (ctx_out) *ctx_out = c;
         else delete c;
+    });
+}
+
+// `turbokv verify --inject-fault` (tools/turbokv_main.cpp:593-599): the naive path's mask loses the last row's view of
+// column 0, through the reference's own testing::mask_fault_hook (pipeline.hpp:57-62). on = 0 clears it.
+int ref_set_inject_fault(int on) {
+    return guard([&] {
+        if (on)
+            testing::mask_fault_hook = [](Matrix& mask) {
+                mask.at(mask.rows() - 1, 0) = -std::numeric_limits<double>::infinity();
+            };
+        else
+            testing::mask_fault_hook = nullptr;
     });
 }
 

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -385,7 +386,9 @@ struct tkv_engine {
     double prof_ms[PC_N] = {};
     int64_t prof_n[PC_N] = {};
     int64_t launches = 0;
-    int64_t fault_row = -1, fault_col = -1;
+    // testing::mask_fault_hook (pipeline.hpp:57-62): row-range overrides {row (< 0: from the end), lo, hi} applied
+    // to the NEXT naive prefill's mask, then cleared
+    std::vector<std::array<int64_t, 3>> mask_override;
 
     ~tkv_engine();
     void bind() const {
@@ -1243,10 +1246,18 @@ void naive_impl(tkv_engine* e, const int32_t* framed, const int64_t* offsets, in
         }
         off += len;
     }
-    if (e->fault_row >= 0 && e->fault_row < N) {  // testing::mask_fault_hook (pipeline.cpp:215)
-        s.lo[e->fault_row] = (int32_t)std::min<int64_t>(s.lo[e->fault_row], e->fault_col);
-        e->fault_row = -1;
+    for (const auto& o : e->mask_override) {  // testing::mask_fault_hook (pipeline.cpp:215)
+        const int64_t r = o[0] < 0 ? N + o[0] : o[0];
+        if (r < 0 || r >= N) continue;
+        if (o[1] == -2) {  // tkv_debug_set_mask_fault: widen the row down to column o[2]
+            s.lo[r] = (int32_t)std::min<int64_t>(s.lo[r], o[2]);
+            continue;
+        }
+        if (o[1] < 0 || o[2] >= N || o[1] > o[2]) fail(TKV_ERR_DOMAIN, "mask override: range outside the sequence");
+        s.lo[r] = (int32_t)o[1];
+        s.hi[r] = (int32_t)o[2];
     }
+    e->mask_override.clear();
     tkv_context* c = new_context(e, N);
     try {
         e->ensure_rope(N);
@@ -2455,11 +2466,26 @@ tkv_status tkv_io_bytes(const tkv_engine* e, int64_t* h2d, int64_t* d2h) {
     });
 }
 
+tkv_status tkv_debug_set_mask_rows(tkv_engine* e, const int64_t* rows, const int32_t* lo, const int32_t* hi, int64_t n) {
+    return guard([&] {
+        need(e, "engine");
+        if (n > 0) {
+            need(rows, "rows");
+            need(lo, "lo");
+            need(hi, "hi");
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            if (lo[i] < 0 || hi[i] < lo[i]) fail(TKV_ERR_DOMAIN, "mask override: need 0 <= lo <= hi");
+            e->mask_override.push_back({rows[i], lo[i], hi[i]});
+        }
+    });
+}
+
 tkv_status tkv_debug_set_mask_fault(tkv_engine* e, int64_t row, int64_t col) {
     return guard([&] {
         need(e, "engine");
-        e->fault_row = row;
-        e->fault_col = col;
+        // widen row `row` so it also sees column `col` (its range grows down to col)
+        e->mask_override.push_back({row, -2, col});
     });
 }
 

@@ -173,6 +173,7 @@ def lib():
         L.tkv_launch_count.restype = C.c_int64
         L.tkv_launch_count.argtypes = [C.c_void_p]
         L.tkv_debug_set_mask_fault.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+        L.tkv_debug_set_mask_rows.argtypes = [C.c_void_p, I64P, I32P, I32P, C.c_int64]
         L.tkv_store_export_ipc.argtypes = [C.c_void_p, C.POINTER(_Ipc), C.POINTER(C.c_uint64)]
         L.tkv_store_attach_ipc.argtypes = [C.c_void_p, C.c_int32, C.POINTER(_Ipc)]
         L.tkv_store_attach_engine.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
@@ -674,6 +675,12 @@ class Engine:
         h, d = C.c_int64(), C.c_int64()
         _check(lib().tkv_io_bytes(self._h, C.byref(h), C.byref(d)))
         return h.value, d.value
+
+    def set_mask_rows(self, rows, lo, hi) -> None:
+        """Override mask rows of the next naive prefill (testing::mask_fault_hook): row r sees keys [lo, hi]."""
+        r = np.ascontiguousarray(rows, np.int64)
+        a, b = _i32(lo), _i32(hi)
+        _check(lib().tkv_debug_set_mask_rows(self._h, _p(r, I64P), _p(a, I32P), _p(b, I32P), len(r)))
 
     def set_mask_fault(self, row: int, col: int) -> None:
         _check(lib().tkv_debug_set_mask_fault(self._h, row, col))

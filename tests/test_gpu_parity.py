@@ -428,6 +428,33 @@ def test_mask_fault_breaks_equivalence(golden):
     assert np.abs(faulty - clean).max() > 1e-6
 
 
+@pytest.mark.skipif(not O.Ref.available(), reason="reference library not built")
+@pytest.mark.parametrize("dtype,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
+def test_inject_fault_reproduces_reference(golden, dtype, tol, tmp_path):
+    """The reference's exact `verify --inject-fault` corruption (tools/turbokv_main.cpp:593-599: the last query row
+    loses column 0, through testing::mask_fault_hook) on both sides: the faulty naive-independent logits of this
+    engine equal the UNMODIFIED reference's faulty logits, and differ from the clean ones."""
+    meta, A = golden
+    m = meta["c1"]
+    eng = engine(cfg_t(m), m["seed"], dtype)
+    framed = [O.frame(p) for p in payloads(A, "c1")]
+    q = A["c1.query"]
+    n = sum(len(f) for f in framed) + len(q)
+    eng.set_mask_rows([-1], [1], [n - 1])
+    faulty = eng.naive_prefill(framed, q, T.MaskMode.Independent, keep_context=False)[0]
+    ref_eng = O.RefEngine(O.Cfg(**m["config"]), m["seed"], str(tmp_path))
+    O.Ref.check(O.Ref.lib().ref_set_inject_fault(1))
+    try:
+        ref_faulty = ref_eng.naive_prefill(framed, q, True)
+    finally:
+        O.Ref.check(O.Ref.lib().ref_set_inject_fault(0))
+        ref_eng.close()
+    assert_close(faulty, ref_faulty, tol)
+    clean = A["c1.naive_independent.logits"]
+    assert np.abs(ref_faulty - clean).max() > 1e-3  # the fault is visible in the reference itself
+    assert np.abs(faulty.astype(np.float64) - clean).max() > 1e-3
+
+
 def test_gather_roundtrip_at_c2_chunk_shape():
     """Size-independent properties at the C2 chunk shape (Qwen dims, 16 x 512-token chunks, 2 layers):
     the identity gather reproduces the store bit for bit, and rotated rows equal R(pos) applied to them."""
