@@ -259,6 +259,11 @@ tkv_status tkv_store_export_directory(tkv_engine* eng, uint8_t* buf, int64_t cap
  * peer's pool (nothing is registered then); opens the peer pool through its IPC handle unless the slot is
  * already attached (tkv_store_attach_engine for a peer engine in this process). */
 tkv_status tkv_store_import_directory(tkv_engine* eng, int32_t slot, const uint8_t* blob, int64_t size);
+/* Two-tier store policy: every retrieval (tkv_assemble) counts a hit for its chunks; rebalance moves the most-retrieved
+ * chunks of the pinned host tier into HBM (demoting the least-retrieved HBM chunks when HBM is full, only while the
+ * incoming chunk has more hits), at most max_moves page-list moves, then halves every hit count. Chunks listed in an
+ * exported directory stay where they are. */
+tkv_status tkv_store_rebalance(tkv_engine* eng, int64_t max_moves, int64_t* promoted, int64_t* demoted);
 /* KV bytes read from peer pools so far (NVLink traffic of the gather + fetches). */
 int64_t tkv_remote_bytes(const tkv_engine* eng);
 

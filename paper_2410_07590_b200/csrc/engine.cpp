@@ -313,6 +313,7 @@ struct Chunk {
     std::vector<int32_t> framed;  // empty for TKVC-imported chunks
     int32_t slot = 0;             // page pool holding the pages: 0 = local HBM, >0 = a peer GPU (NVLink)
     bool shared = false;          // listed in an exported directory: peers read its pages, so it cannot be evicted
+    uint32_t hits = 0;            // retrievals since the last tier rebalance (halved at each rebalance)
 };
 
 }  // namespace tkv
@@ -1170,6 +1171,7 @@ tkv_context* assemble_impl(tkv_engine* e, const uint64_t* ids, int64_t n, int mo
     for (int64_t i = 0; i < n; ++i) {
         auto it = e->chunks.find(ids[i]);
         if (it == e->chunks.end()) fail(TKV_ERR_NOT_FOUND, "chunk " + hex_id(ids[i]) + " not in store");
+        it->second.hits += 1;  // access frequency for the HBM <-> host tier policy (tkv_store_rebalance)
         cs.push_back(&it->second);
         P += it->second.len;
         max_len = std::max(max_len, it->second.len);
@@ -1969,6 +1971,66 @@ tkv_status tkv_store_tiers(const tkv_engine* e, int64_t* hbm_used, int64_t* hbm_
         if (hbm_total) *hbm_total = e->n_pages;
         if (host_used) *host_used = e->n_host_pages - (int64_t)e->host_free.size();
         if (host_total) *host_total = e->n_host_pages;
+    });
+}
+
+tkv_status tkv_store_rebalance(tkv_engine* e, int64_t max_moves, int64_t* promoted, int64_t* demoted) {
+    return guard([&] {
+        need(e, "engine");
+        e->bind();
+        int64_t up = 0, down = 0;
+        if (e->n_host_pages > 0 && max_moves > 0) {
+            // frequency policy: the most-retrieved host-tier chunks move into HBM; when HBM is full, the least-retrieved
+            // HBM chunks move out to make room, but only while the incoming chunk is hotter than the outgoing one
+            std::vector<std::pair<uint32_t, uint64_t>> cold_hbm, hot_host;
+            for (auto& kv : e->chunks) {
+                if (kv.second.shared) continue;  // peers hold its page indices
+                if (kv.second.slot == 0) cold_hbm.emplace_back(kv.second.hits, kv.first);
+                else if (kv.second.slot == kHostPool && kv.second.hits > 0) hot_host.emplace_back(kv.second.hits, kv.first);
+            }
+            std::sort(hot_host.begin(), hot_host.end(), [](auto& a, auto& b) { return a.first != b.first ? a.first > b.first : a.second < b.second; });
+            std::sort(cold_hbm.begin(), cold_hbm.end());
+            size_t victim = 0;
+            auto move = [&](Chunk& ch, bool to_hbm) {
+                Chunk dst;
+                dst.len = ch.len;
+                const int64_t np = (int64_t)ch.pages.size();
+                std::vector<int32_t>& fl = to_hbm ? e->free_pages : e->host_free;
+                if ((int64_t)fl.size() < np) return false;
+                for (int64_t p = 0; p < np; ++p) {
+                    dst.pages.push_back(fl.back());
+                    fl.pop_back();
+                }
+                dst.slot = to_hbm ? 0 : kHostPool;
+                for (int64_t p = 0; p < np; ++p)  // PCIe / C2C copies of whole pages
+                    TKV_CUDA(cudaMemcpyAsync(page_ptr(e, dst.slot, dst.pages[(size_t)p]), page_ptr(e, ch.slot, ch.pages[(size_t)p]),
+                                             e->page_bytes, cudaMemcpyDefault, e->stream));
+                release_chunk_pages(e, ch);
+                ch.pages = std::move(dst.pages);
+                ch.slot = dst.slot;
+                return true;
+            };
+            for (auto& h : hot_host) {
+                if (up + down >= max_moves) break;
+                Chunk& ch = e->chunks[h.second];
+                const int64_t np = (int64_t)ch.pages.size();
+                while ((int64_t)e->free_pages.size() < np && victim < cold_hbm.size() && cold_hbm[victim].first < h.first &&
+                       up + down < max_moves) {
+                    Chunk& v = e->chunks[cold_hbm[victim++].second];
+                    if (!move(v, false)) break;
+                    ++down;
+                }
+                if ((int64_t)e->free_pages.size() < np) break;
+                if (move(ch, true)) ++up;
+            }
+            if (up + down > 0) {
+                e->sync();
+                e->store_epoch += 1;  // contexts that re-read store pages must not use the old page lists
+            }
+        }
+        for (auto& kv : e->chunks) kv.second.hits >>= 1;  // decay: recent retrievals count most
+        if (promoted) *promoted = up;
+        if (demoted) *demoted = down;
     });
 }
 

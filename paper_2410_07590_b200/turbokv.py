@@ -180,6 +180,7 @@ def lib():
         L.tkv_store_chunk_pages.argtypes = [C.c_void_p, C.c_uint64, I32P, C.c_int64, I64P, I64P]
         L.tkv_store_register_remote.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, I32P, C.c_int64, I32P]
         L.tkv_store_fetch_remote.argtypes = [C.c_void_p, C.c_uint64]
+        L.tkv_store_rebalance.argtypes = [C.c_void_p, C.c_int64, I64P, I64P]
         L.tkv_store_export_directory.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, I64P]
         L.tkv_store_import_directory.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64]
         L.tkv_remote_bytes.restype = C.c_int64
@@ -617,6 +618,12 @@ class Engine:
         h = _Ipc()
         C.memmove(h.bytes, handle, 64)
         _check(lib().tkv_store_attach_ipc(self._h, slot, C.byref(h)))
+
+    def store_rebalance(self, max_moves: int = 1 << 30) -> tuple[int, int]:
+        """tkv_store_rebalance: frequency-driven HBM <-> host tier moves; returns (promoted, demoted)."""
+        up, down = C.c_int64(), C.c_int64()
+        _check(lib().tkv_store_rebalance(self._h, max_moves, C.byref(up), C.byref(down)))
+        return up.value, down.value
 
     def export_directory(self) -> bytes:
         """tkv_store_export_directory: this engine's owned chunks + pool IPC handle + identity, as one blob."""

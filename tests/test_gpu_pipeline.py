@@ -109,3 +109,32 @@ def test_store_ids_sorted_and_ingest_is_a_noop_for_known_ids():
     eng.store_evict(ids[0])
     assert eng.store_ids() == sorted(ids[1:])
     eng.close()
+
+
+def test_tier_rebalance_promotes_hot_chunks_and_keeps_kv_bitwise():
+    """tkv_store_rebalance (the C4 two-tier policy): chunks retrieved often from the pinned host tier move into HBM,
+    the coldest HBM chunks move out, and a request over moved chunks gives bitwise the logits it gave before."""
+    import oracle as O
+    eng = T.Engine(T.ModelConfig.toy(), 42, dtype="bf16", store_capacity_tokens=4 * 64, host_spill_tokens=8 * 64)
+    try:
+        pays = [O.random_text_tokens(4400 + i, 62) for i in range(8)]
+        ids = eng.ingest_chunks(pays)
+        assert [eng.store_chunk_tier(i) for i in ids] == [0] * 4 + [1] * 4  # HBM fills first
+        hot = ids[5:8]
+        q = O.random_text_tokens(77, 12)
+        with eng.assemble(hot, T.PositionMode.Reordered) as ctx:
+            before = eng.prefill_query(ctx, q).copy()
+        for _ in range(3):
+            eng.assemble(hot, T.PositionMode.Reordered).close()
+        up, down = eng.store_rebalance()
+        assert up == 3 and down == 3
+        assert all(eng.store_chunk_tier(i) == 0 for i in hot)
+        assert sum(eng.store_chunk_tier(i) == 1 for i in ids) == 4
+        with eng.assemble(hot, T.PositionMode.Reordered) as ctx:
+            after = eng.prefill_query(ctx, q).copy()
+        assert np.array_equal(before, after)
+        for i in ids:  # every chunk still reads back (demoted ones from the host tier)
+            assert np.isfinite(eng.store_read(i, 0, "k")).all()
+        assert eng.store_rebalance() == (0, 0)  # nothing hotter left outside HBM
+    finally:
+        eng.close()
