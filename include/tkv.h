@@ -128,6 +128,17 @@ void tkv_engine_opts_default(tkv_engine_opts* opts);
 tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const tkv_engine_opts* opts,
                              tkv_engine** out);
 void tkv_engine_destroy(tkv_engine* eng);
+/* TKVW weights files (docs/formats.md "TKVW"; save_weights / load_weights, src/model.cpp:120-196).
+ * create_from_weights: an engine whose weights come from the file (any values: norm weights included) -- the config
+ * is read from the header (returned in cfg_out when non-null), every tensor is shape-checked against it, and the
+ * trailing weights_checksum is recomputed (on the GPU) and must match: TKV_ERR_NOT_FOUND (missing file),
+ * TKV_ERR_FORMAT (magic, version, truncation, shapes, checksum), TKV_ERR_CONFIG (an invalid config). The engine's
+ * fingerprint is model_fingerprint(config, checksum), so chunk ids agree with a reference engine on the same weights.
+ * save_weights: writes init_random(cfg, seed) as a TKVW file (byte-identical to the reference's save_weights), the
+ * f64 draws generated on `device`. */
+tkv_status tkv_engine_create_from_weights(const char* path, const tkv_engine_opts* opts, tkv_engine** out,
+                                          tkv_model_config* cfg_out);
+tkv_status tkv_save_weights(const tkv_model_config* cfg, uint64_t seed, const char* path, int device);
 tkv_status tkv_engine_fingerprint(const tkv_engine* eng, uint64_t* out);
 tkv_status tkv_engine_config(const tkv_engine* eng, tkv_model_config* out);
 

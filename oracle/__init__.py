@@ -357,6 +357,9 @@ class Ref:
                                             C.POINTER(C.c_void_p)]
             L.ref_greedy_decode.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, I32P, I64P]
             L.ref_set_inject_fault.argtypes = [C.c_int]
+            L.ref_save_weights.argtypes = [C.POINTER(OracleCfg), C.c_uint64, C.c_char_p]
+            L.ref_load_weights.argtypes = [C.c_char_p, C.POINTER(OracleCfg), U64P]
+            L.ref_forward_file.argtypes = [C.c_char_p, I32P, C.c_int64, F64P]
             L.ref_build_mask.argtypes = [I64P, C.c_int64, C.c_int, U8P]
             L.ref_causal_rows.argtypes = [C.c_int64, C.c_int64, U8P]
             L.ref_rope_rotate.argtypes = [F64P, C.c_int64, C.c_int64, I64P, C.c_int64, C.c_double, F64P]

@@ -318,6 +318,35 @@ int ref_naive_prefill(void* e, const int32_t* tokens, const int64_t* offsets, in
     });
 }
 
+// TKVW files (model.cpp:120-196): save_weights of init_random(cfg, seed); load_weights -> (config, checksum); and a
+// vanilla causal forward_tokens over a loaded file's weights (last row's logits), for weights other than init_random's
+int ref_save_weights(const RefConfig* c, uint64_t seed, const char* path) {
+    return guard([&] {
+        const ModelConfig cfg = to_cfg(c);
+        save_weights(path, cfg, init_random(cfg, seed));
+    });
+}
+
+int ref_load_weights(const char* path, RefConfig* cfg_out, uint64_t* checksum) {
+    return guard([&] {
+        ModelWeights w;
+        const ModelConfig m = load_weights(path, w);
+        *cfg_out = RefConfig{m.layer_num, m.head_num,         m.kv_head_num, m.head_size, m.hidden_size,
+                             m.intermediate_size, m.vocab_size, m.rope_base, m.norm_eps};
+        *checksum = weights_checksum(w);
+    });
+}
+
+int ref_forward_file(const char* path, const int32_t* tokens, int64_t n, double* logits) {
+    return guard([&] {
+        ModelWeights w;
+        const ModelConfig cfg = load_weights(path, w);
+        ForwardResult fw = forward_tokens(cfg, w, to_tokens(tokens, n), PositionIds::sequential(n, 0), nullptr,
+                                          causal_rows(n, 0));
+        std::memcpy(logits, fw.logits.row(n - 1), static_cast<size_t>(cfg.vocab_size) * sizeof(double));
+    });
+}
+
 // `turbokv verify --inject-fault` (tools/turbokv_main.cpp:593-599): the naive path's mask loses the last row's view of
 // column 0, through the reference's own testing::mask_fault_hook (pipeline.hpp:57-62). on = 0 clears it.
 int ref_set_inject_fault(int on) {

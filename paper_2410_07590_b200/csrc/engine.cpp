@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <set>
@@ -338,6 +339,10 @@ struct tkv_engine {
     DevMem wmem;
     float* emb = nullptr;
     float* ones = nullptr;
+    float* norms = nullptr;  // RMSNorm weights, f32: attn_norm(l) at 2l, mlp_norm(l) at 2l + 1, final_norm at 2L (x hid)
+    float* norm_attn(int64_t l) const { return norms + (size_t)(2 * l) * hid; }
+    float* norm_mlp(int64_t l) const { return norms + (size_t)(2 * l + 1) * hid; }
+    float* norm_after_mlp(int64_t l) const { return norms + (size_t)(l + 1 < L ? 2 * (l + 1) : 2 * L) * hid; }
     std::vector<void*> w_qkv, w_o, w_gu, w_down;
     void* w_lm = nullptr;
 
@@ -748,7 +753,7 @@ void tkv_engine::forward_mk(const Fwd& f) {
     const unsigned grid = (unsigned)mk_grid(device);
     {
         Scope sc(this, PC_EPI, 1);
-        launch_embed(f.tok, T, emb, (int)hid, (int)V, ones, x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
+        launch_embed(f.tok, T, emb, (int)hid, (int)V, norm_attn(0), x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
                      stream);
     }
     // phase slots: 0 O, 1 residual, 2 gate/up, 3 down, 4 residual, 5 QKV, 6 QKV epilogue
@@ -785,12 +790,13 @@ void tkv_engine::forward_mk(const Fwd& f) {
         if (!swiglu) part_floats = std::max(part_floats, (size_t)eff * M * N);
         return eff;
     };
-    auto elem = [&](Plan& p, int slot, int kind, const float* rpartial, int rsplits) {
+    auto elem = [&](Plan& p, int slot, int kind, const float* rpartial, int rsplits, const float* w = nullptr) {
         MkPhase& ph = p.a.ph[p.a.n_phases++];
         ph.kind = kind;
         ph.slot = slot;
         ph.rpartial = rpartial;
         ph.rsplits = rsplits;
+        ph.rw = w;
     };
     auto common = [&](Plan& p, int M, float* x_rows) {
         MkArgs& a = p.a;
@@ -802,7 +808,6 @@ void tkv_engine::forward_mk(const Fwd& f) {
         a.x = x_rows;
         a.xb = xb.p;
         a.ssp = ssp.as<float>();
-        a.w = ones;
         a.hidden = (int)hid;
         a.nb = nb;
         a.eps = eps;
@@ -823,10 +828,10 @@ void tkv_engine::forward_mk(const Fwd& f) {
     };
     auto mlp = [&](Plan& p, int64_t layer, int M) {
         const int so = gemm(p, S_O, w_o[layer], attn.p, M, (int)hid, (int)qd, false);
-        elem(p, S_R1, MK_RESIDUAL, partial.as<float>(), so);
+        elem(p, S_R1, MK_RESIDUAL, partial.as<float>(), so, norm_mlp(layer));
         gemm(p, S_GU, w_gu[layer], xb.p, M, (int)(2 * I), (int)hid, true);
         const int sd = gemm(p, S_D, w_down[layer], act.p, M, (int)hid, (int)I, false);
-        elem(p, S_R2, MK_RESIDUAL, partial.as<float>(), sd);
+        elem(p, S_R2, MK_RESIDUAL, partial.as<float>(), sd, norm_after_mlp(layer));
     };
     auto launch = [&](Plan& p) {
         for (int i = 0; i < p.a.n_phases; ++i) {
@@ -893,7 +898,7 @@ void tkv_engine::forward(const Fwd& f) {
     act.ensure((size_t)T * I * es);
     {
         Scope sc(this, PC_EPI, 1);
-        launch_embed(f.tok, T, emb, (int)hid, (int)V, ones, x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
+        launch_embed(f.tok, T, emb, (int)hid, (int)V, norm_attn(0), x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
                      stream);
     }
     // the next GEMM of the forward, for the current GEMM's tail L2 warm-up (TKV_GEMM_NEXT_PF)
@@ -963,7 +968,7 @@ void tkv_engine::forward(const Fwd& f) {
         s = gemm(attn_rows, (int)qd, w_o[l], rows, (int)hid, (int)qd);
         if (!(skip_mask & 1)) {
             Scope sc(this, PC_EPI, 1);
-            launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, ones, xb.p, ssp.as<float>(), dt,
+            launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, norm_mlp(l), xb.p, ssp.as<float>(), dt,
                             err.as<int>(), stream);
         }
         // --- MLP block: gate|up fused into one GEMM, SwiGLU (with the folded mlp_norm scale) in its epilogue ---
@@ -989,7 +994,7 @@ void tkv_engine::forward(const Fwd& f) {
         if (!(skip_mask & 2)) {
             // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
             Scope sc(this, PC_EPI, 1);
-            launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, ones, xb.p, ssp.as<float>(), dt,
+            launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, norm_after_mlp(l), xb.p, ssp.as<float>(), dt,
                             err.as<int>(), stream);
         }
     }
@@ -1491,8 +1496,15 @@ void tkv_engine_opts_default(tkv_engine_opts* o) {
     o->flags = 0;
 }
 
-tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const tkv_engine_opts* opts,
-                             tkv_engine** out) {
+}  // extern "C"
+namespace {
+struct WeightsFile;  // a TKVW file positioned after its header (tkv_engine_create_from_weights)
+void load_tkvw(tkv_engine* e, WeightsFile& wf);
+}  // namespace
+extern "C" {
+
+static tkv_status create_engine(const tkv_model_config* cfg, uint64_t seed, const tkv_engine_opts* opts, tkv_engine** out,
+                                WeightsFile* wf) {
     std::unique_ptr<tkv_engine> e;
     tkv_status st = guard([&] {
         need(cfg, "cfg");
@@ -1535,8 +1547,10 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         // reference-exact at every size: the FNV-1a of all f64 weights, hashed in parallel on the device
         // (fingerprint.cu; 52 GB of hashed bytes for Qwen2-7B); exact_fingerprint = 0 opts into a fast
         // non-reference identity
-        e->exact_fp = e->opts.exact_fingerprint != 0;
-        if (e->exact_fp) {
+        e->exact_fp = e->opts.exact_fingerprint != 0 || wf;
+        if (wf) {
+            // fingerprint from the file's own weights: set by load_tkvw below
+        } else if (e->exact_fp) {
             e->fingerprint = fingerprint_of(c, weights_checksum_device(c, seed, e->stream));
         } else {  // opt-in fast identity: NOT the reference's
             Fnv f;
@@ -1552,26 +1566,37 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         const size_t per_layer = (size_t)(e->nqkv * H_ + H_ * qd + 2 * I * H_ + H_ * I) * es;
         auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
         const size_t emb_b = al((size_t)V * H_ * 4), ones_b = al((size_t)std::max(H_, I) * 4);
+        const size_t norms_b = al((size_t)(2 * e->L + 1) * H_ * 4);
         const size_t lm_b = al((size_t)V * H_ * es);
-        const size_t total_b = emb_b + ones_b + lm_b + e->L * al(per_layer);
+        const size_t total_b = emb_b + ones_b + norms_b + lm_b + e->L * al(per_layer);
         uint8_t* base = static_cast<uint8_t*>(e->wmem.ensure(total_b));
         e->emb = reinterpret_cast<float*>(base);
         e->ones = reinterpret_cast<float*>(base + emb_b);
-        e->w_lm = base + emb_b + ones_b;
-        uint8_t* lp = base + emb_b + ones_b + lm_b;
+        e->norms = reinterpret_cast<float*>(base + emb_b + ones_b);
+        e->w_lm = base + emb_b + ones_b + norms_b;
+        uint8_t* lp = base + emb_b + ones_b + norms_b + lm_b;
         const double scale = 1.0 / std::sqrt((double)H_);
         uint64_t cur = 0;
+        for (int64_t l = 0; l < e->L; ++l) {
+            uint8_t* qkv = lp;
+            e->w_qkv.push_back(qkv);
+            e->w_o.push_back(qkv + (size_t)e->nqkv * H_ * es);
+            e->w_gu.push_back(qkv + (size_t)e->nqkv * H_ * es + (size_t)H_ * qd * es);
+            e->w_down.push_back(qkv + (size_t)e->nqkv * H_ * es + (size_t)H_ * qd * es + (size_t)2 * I * H_ * es);
+            lp += al(per_layer);
+        }
+        launch_fill_f32(e->ones, 1.0f, std::max(H_, I), e->stream);
+        if (wf) {
+            load_tkvw(e.get(), *wf);  // weights, norms and the reference identity from the file
+        } else {
+        launch_fill_f32(e->norms, 1.0f, (2 * e->L + 1) * H_, e->stream);  // init_random: every norm weight is 1.0
         launch_init_rowmajor_f32(e->emb, seed, cur, V, H_, scale, e->stream);
         cur += (uint64_t)(V * H_);
         for (int64_t l = 0; l < e->L; ++l) {
-            uint8_t* qkv = lp;
-            uint8_t* o = qkv + (size_t)e->nqkv * H_ * es;
-            uint8_t* gu = o + (size_t)H_ * qd * es;
-            uint8_t* dn = gu + (size_t)2 * I * H_ * es;
-            e->w_qkv.push_back(qkv);
-            e->w_o.push_back(o);
-            e->w_gu.push_back(gu);
-            e->w_down.push_back(dn);
+            uint8_t* qkv = static_cast<uint8_t*>(e->w_qkv[l]);
+            uint8_t* o = static_cast<uint8_t*>(e->w_o[l]);
+            uint8_t* gu = static_cast<uint8_t*>(e->w_gu[l]);
+            uint8_t* dn = static_cast<uint8_t*>(e->w_down[l]);
             // [in, out] draws written as [out][in] rows: wq | wk | wv stacked, gate | up stacked
             launch_init_transposed(qkv, e->dt, seed, cur, H_, qd, scale, e->stream);
             cur += (uint64_t)(H_ * qd);
@@ -1590,11 +1615,10 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
             cur += (uint64_t)(H_ * I);
             launch_init_transposed(dn, e->dt, seed, cur, I, H_, scale, e->stream);
             cur += (uint64_t)(I * H_);
-            lp += al(per_layer);
         }
         launch_init_transposed(e->w_lm, e->dt, seed, cur, H_, V, scale, e->stream);
-        launch_fill_f32(e->ones, 1.0f, std::max(H_, I), e->stream);
         e->launches += 3 + 7 * e->L;
+        }
 
         e->err.ensure(64);
 #ifdef TKV_TUNING
@@ -1656,6 +1680,185 @@ tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const t
         *out = e.release();
     });
     return st;
+}
+
+tkv_status tkv_engine_create(const tkv_model_config* cfg, uint64_t seed, const tkv_engine_opts* opts,
+                             tkv_engine** out) {
+    return create_engine(cfg, seed, opts, out, nullptr);
+}
+
+// ---- TKVW weights files (docs/formats.md "TKVW"; src/model.cpp:120-196) ----
+}  // extern "C"
+namespace {
+struct WeightsFile {
+    std::ifstream in;
+    std::string path;
+    tkv_model_config cfg{};
+    void read(void* dst, size_t n, const char* what) {
+        in.read(static_cast<char*>(dst), (std::streamsize)n);
+        if ((size_t)in.gcount() != n) fail(TKV_ERR_FORMAT, std::string(what) + ": truncated weights file " + path);
+    }
+    template <typename T>
+    T get(const char* what) {
+        T v;
+        read(&v, sizeof v, what);
+        return v;
+    }
+};
+
+// header (magic, version, config) -- FormatError / NotFoundError like load_weights (model.cpp:152-172)
+void open_tkvw(WeightsFile& wf, const char* path) {
+    wf.path = path;
+    wf.in.open(path, std::ios::binary);
+    if (!wf.in) fail(TKV_ERR_NOT_FOUND, std::string("no such file: ") + path);
+    char magic[4];
+    wf.read(magic, 4, "weights magic");
+    if (std::memcmp(magic, "TKVW", 4) != 0) fail(TKV_ERR_FORMAT, std::string("not a weights file: ") + path);
+    const uint32_t version = wf.get<uint32_t>("weights version");
+    if (version != 1) fail(TKV_ERR_FORMAT, "unsupported weights version " + std::to_string(version));
+    tkv_model_config& c = wf.cfg;
+    c.layer_num = wf.get<int64_t>("weights config");
+    c.head_num = wf.get<int64_t>("weights config");
+    c.kv_head_num = wf.get<int64_t>("weights config");
+    c.head_size = wf.get<int64_t>("weights config");
+    c.hidden_size = wf.get<int64_t>("weights config");
+    c.intermediate_size = wf.get<int64_t>("weights config");
+    c.vocab_size = wf.get<int64_t>("weights config");
+    c.rope_base = wf.get<double>("weights config");
+    c.norm_eps = wf.get<double>("weights config");
+    validate_cfg(c);
+}
+
+// The tensors in draw order: each shape-checked against the config, streamed in pieces through pinned host memory to
+// the device, FNV-hashed there (the bytes ARE weights_checksum's stream) and cast into the engine layout; the trailing
+// checksum must match (FormatError otherwise).
+void load_tkvw(tkv_engine* e, WeightsFile& wf) {
+    const int64_t H = e->hid, qd = e->qd, kvd = e->kvd, I = e->I, V = e->V;
+    const size_t es = dt_size(e->dt);
+    const int64_t piece = std::min<int64_t>(int64_t(1) << 25, std::max({V * H, H * I, qd * H, H * V}));
+    void* host = nullptr;
+    TKV_CUDA(cudaHostAlloc(&host, (size_t)piece * 8, cudaHostAllocDefault));
+    std::unique_ptr<void, void (*)(void*)> host_guard(host, [](void* p) { cudaFreeHost(p); });
+    DevMem dbuf;
+    dbuf.ensure((size_t)piece * 8);
+    uint64_t h = Fnv{}.h;
+    // store(dev values, element offset e0, count n) of one tensor
+    auto tensor = [&](bool mat, int64_t rows, int64_t cols, const char* name,
+                      const std::function<void(const double*, int64_t, int64_t)>& store) {
+        std::vector<FpSeg> head;
+        uint64_t w = 0;
+        if (mat) {
+            const uint64_t r = wf.get<uint64_t>("tensor shape"), c = wf.get<uint64_t>("tensor shape");
+            if ((int64_t)r != rows || (int64_t)c != cols)
+                fail(TKV_ERR_FORMAT, std::string(name) + ": tensor shape does not match the weights config");
+            head.push_back(FpSeg{w++, 1, r, 0.0, 0, 0});
+            head.push_back(FpSeg{w++, 1, c, 0.0, 0, 0});
+        } else {
+            const uint64_t n = wf.get<uint64_t>("tensor shape");
+            if ((int64_t)n != cols) fail(TKV_ERR_FORMAT, std::string(name) + ": vector size does not match the config");
+            head.push_back(FpSeg{w++, 1, n, 0.0, 0, 0});
+        }
+        const int64_t total = rows * cols;
+        for (int64_t e0 = 0; e0 < total || (total == 0 && e0 == 0); e0 += piece) {
+            const int64_t n = std::min(piece, total - e0);
+            wf.read(host, (size_t)n * 8, name);
+            TKV_CUDA(cudaMemcpyAsync(dbuf.p, host, (size_t)n * 8, cudaMemcpyHostToDevice, e->stream));
+            std::vector<FpSeg> segs = e0 == 0 ? head : std::vector<FpSeg>{};
+            const uint64_t w0 = segs.empty() ? 0 : w;
+            segs.push_back(FpSeg{w0, (uint64_t)n, (uint64_t)(uintptr_t)dbuf.p, 0.0, 3, 0});
+            h = device_fnv_words(segs, 0, h, e->stream);  // synchronises: the pinned piece is free afterwards
+            store(dbuf.as<double>(), e0, n);
+            if (total == 0) break;
+        }
+    };
+    auto vec = [&](float* dst, const char* name) {
+        tensor(false, 1, H, name, [&](const double* src, int64_t e0, int64_t n) {
+            launch_store_f32_from_f64(dst + e0, src, n, e->stream);
+        });
+    };
+    auto mat = [&](void* dst, int64_t rows, int64_t cols, const char* name, int rb = 0, int off = 0) {
+        tensor(true, rows, cols, name, [&](const double* src, int64_t e0, int64_t n) {
+            launch_store_transposed_f64(dst, e->dt, src, e0, n, rows, cols, e->stream, rb, off);
+        });
+    };
+    tensor(true, V, H, "embedding", [&](const double* src, int64_t e0, int64_t n) {
+        launch_store_f32_from_f64(e->emb + e0, src, n, e->stream);
+    });
+    const int rb = e->gu_interleaved ? 64 : 0;
+    for (int64_t l = 0; l < e->L; ++l) {
+        uint8_t* qkv = static_cast<uint8_t*>(e->w_qkv[l]);
+        uint8_t* gu = static_cast<uint8_t*>(e->w_gu[l]);
+        vec(e->norm_attn(l), "attn_norm");
+        vec(e->norm_mlp(l), "mlp_norm");
+        mat(qkv, H, qd, "wq");
+        mat(qkv + (size_t)qd * H * es, H, kvd, "wk");
+        mat(qkv + (size_t)(qd + kvd) * H * es, H, kvd, "wv");
+        mat(e->w_o[l], qd, H, "wo");
+        mat(gu, H, I, "w_gate", rb, 0);
+        mat(rb ? gu : gu + (size_t)I * H * es, H, I, "w_up", rb, rb ? 64 : 0);
+        mat(e->w_down[l], I, H, "w_down");
+    }
+    vec(e->norms + (size_t)2 * e->L * H, "final_norm");
+    mat(e->w_lm, H, V, "lm_head");
+    const uint64_t stored = wf.get<uint64_t>("weights checksum");
+    e->sync();
+    if (stored != h) fail(TKV_ERR_FORMAT, "weights checksum mismatch: " + wf.path);
+    e->fingerprint = fingerprint_of(e->cfg, h);
+}
+}  // namespace
+extern "C" {
+
+tkv_status tkv_engine_create_from_weights(const char* path, const tkv_engine_opts* opts, tkv_engine** out,
+                                          tkv_model_config* cfg_out) {
+    WeightsFile wf;
+    const tkv_status st = guard([&] {
+        need(path, "path");
+        need(out, "out");
+        open_tkvw(wf, path);
+        if (cfg_out) *cfg_out = wf.cfg;
+    });
+    if (st != TKV_OK) return st;
+    return create_engine(&wf.cfg, 0, opts, out, &wf);
+}
+
+tkv_status tkv_save_weights(const tkv_model_config* cfg, uint64_t seed, const char* path, int device) {
+    return guard([&] {
+        need(cfg, "cfg");
+        need(path, "path");
+        validate_cfg(*cfg);
+        TKV_CUDA(cudaSetDevice(device));
+        std::string head("TKVW", 4);
+        auto put = [&](const void* p, size_t n) { head.append(static_cast<const char*>(p), n); };
+        const uint32_t version = 1;
+        put(&version, 4);
+        const int64_t ints[7] = {cfg->layer_num, cfg->head_num, cfg->kv_head_num, cfg->head_size, cfg->hidden_size,
+                                 cfg->intermediate_size, cfg->vocab_size};
+        put(ints, sizeof ints);
+        put(&cfg->rope_base, 8);
+        put(&cfg->norm_eps, 8);
+        const std::vector<FpSeg> segs = checksum_segments(*cfg);  // the tensor stream: shapes, 1.0 norms, draws
+        uint64_t words = 0;
+        for (const FpSeg& g : segs) words = std::max(words, g.word0 + g.n);
+        const std::string tmp = std::string(path) + ".tmp";
+        std::ofstream f(tmp, std::ios::binary | std::ios::trunc);
+        if (!f) fail(TKV_ERR_IO, "cannot open " + tmp + " for writing");
+        f.write(head.data(), (std::streamsize)head.size());
+        const int64_t piece = int64_t(1) << 24;
+        DevMem d;
+        d.ensure((size_t)std::min<uint64_t>(words, piece) * 8 + 8);
+        std::vector<uint64_t> buf((size_t)std::min<uint64_t>(words, piece));
+        for (uint64_t w0 = 0; w0 < words; w0 += piece) {
+            const int64_t n = (int64_t)std::min<uint64_t>(piece, words - w0);
+            device_words(segs, seed, w0, n, d.as<uint64_t>(), 0);
+            TKV_CUDA(cudaMemcpy(buf.data(), d.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+            f.write(reinterpret_cast<const char*>(buf.data()), (std::streamsize)(n * 8));
+        }
+        const uint64_t ck = device_fnv_words(segs, seed, Fnv{}.h, 0);
+        f.write(reinterpret_cast<const char*>(&ck), 8);
+        f.close();
+        if (!f) fail(TKV_ERR_IO, "write failed: " + tmp);
+        if (std::rename(tmp.c_str(), path) != 0) fail(TKV_ERR_IO, std::string("rename to ") + path + " failed");
+    });
 }
 
 void tkv_engine_destroy(tkv_engine* eng) {

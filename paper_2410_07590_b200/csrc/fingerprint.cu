@@ -49,6 +49,7 @@ __device__ __forceinline__ uint64_t word_at(const FpSeg* segs, int n_segs, uint6
     while (s > 0 && segs[s].word0 > w) --s;
     *hint = s;
     const FpSeg& g = segs[s];
+    if (g.kind == 3) return reinterpret_cast<const uint64_t*>(g.a)[w - g.word0];  // words already in device memory
     if (g.kind == 2) {  // a drawn weight: next_signed() * scale (model.cpp:15-21), no FMA contraction
         const double u = __dmul_rn((double)(sm_at(seed, g.a + (w - g.word0)) >> 11), 0x1.0p-53);
         return (uint64_t)__double_as_longlong(__dmul_rn(__dadd_rn(__dmul_rn(2.0, u), -1.0), g.scale));
@@ -164,6 +165,16 @@ __global__ void __launch_bounds__(128) affine_kernel(const FpSeg* __restrict__ s
     S_out[blk] = S;
 }
 
+// the words of a segment list, materialised (the TKVW writer streams them to a file)
+__global__ void words_kernel(const FpSeg* __restrict__ segs, int n_segs, uint64_t seed, uint64_t w0, int64_t n,
+                             uint64_t* __restrict__ out) {
+    const int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 16;
+    if (i0 >= n) return;
+    int hint = first_seg(segs, n_segs, w0 + i0);
+    const int64_t i1 = i0 + 16 < n ? i0 + 16 : n;
+    for (int64_t i = i0; i < i1; ++i) out[i] = word_at(segs, n_segs, seed, w0 + i, &hint);
+}
+
 uint64_t pow_mod(uint64_t b, uint64_t e) {
     uint64_t r = 1;
     while (e) {
@@ -233,6 +244,18 @@ uint64_t device_fnv_words(const std::vector<FpSeg>& segs, uint64_t seed, uint64_
         h = h * (nw == (uint64_t)kBlockWords ? p_full : pow_mod(kFnvPrime, nw * 8)) + h_S[(size_t)b];
     }
     return h;
+}
+
+void device_words(const std::vector<FpSeg>& segs, uint64_t seed, uint64_t w0, int64_t n, uint64_t* d_out,
+                  cudaStream_t s) {
+    if (n <= 0) return;
+    FpSeg* d_segs = nullptr;
+    TKV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_segs), segs.size() * sizeof(FpSeg), s));
+    TKV_CUDA(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(FpSeg), cudaMemcpyHostToDevice, s));
+    const int64_t threads = (n + 15) / 16;
+    words_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d_segs, (int)segs.size(), seed, w0, n, d_out);
+    TKV_CUDA(cudaGetLastError());
+    TKV_CUDA(cudaFreeAsync(d_segs, s));
 }
 
 }  // namespace tkv

@@ -70,6 +70,25 @@ __global__ void init_transposed_kernel(T* dst, uint64_t seed, uint64_t base, int
     }
 }
 
+template <typename T>
+__global__ void store_transposed_f64_kernel(T* dst, const double* __restrict__ src, int64_t e0, int64_t n, int64_t rows,
+                                            int64_t cols, int row_block, int row_off) {
+    pdl_launch();
+    pdl_wait();
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = e0 + o, i = e / cols, j = e - i * cols;  // source [in = i][out = j]
+        const int64_t pj = row_block ? (j / row_block) * 2 * row_block + row_off + j % row_block : j;
+        stf(dst, pj * rows + i, __double2float_rn(src[o]));  // the canonical cast
+    }
+}
+
+__global__ void f32_from_f64_kernel(float* dst, const double* __restrict__ src, int64_t n) {
+    pdl_launch();
+    pdl_wait();
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
+        dst[o] = __double2float_rn(src[o]);
+}
+
 __global__ void init_rowmajor_kernel(float* dst, uint64_t seed, uint64_t base, int64_t n, double scale) {
     pdl_launch();
     pdl_wait();
@@ -512,6 +531,18 @@ void launch_embed(const int32_t* tok, int T_, const float* emb, int hidden, int 
                   void* xb, float* ssp, DT dt, int* err, cudaStream_t s) {
     const dim3 grid(row_ctas(hidden), T_);
     DISPATCH_DT(dt, launch_k(embed_kernel<T>, grid, 256, 0, s, tok, emb, hidden, vocab, w, x, (T*)xb, ssp, err));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_store_transposed_f64(void* dst, DT dt, const double* src, int64_t e0, int64_t n, int64_t rows, int64_t cols,
+                                 cudaStream_t s, int row_block, int row_off) {
+    DISPATCH_DT(dt, launch_k(store_transposed_f64_kernel<T>, grid_for(n, 256), 256, 0, s, (T*)dst, src, e0, n, rows, cols,
+                             row_block, row_off));
+    TKV_CUDA(cudaGetLastError());
+}
+
+void launch_store_f32_from_f64(float* dst, const double* src, int64_t n, cudaStream_t s) {
+    launch_k(f32_from_f64_kernel, grid_for(n, 256), 256, 0, s, dst, src, n);
     TKV_CUDA(cudaGetLastError());
 }
 

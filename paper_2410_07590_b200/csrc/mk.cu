@@ -79,7 +79,7 @@ __device__ __forceinline__ V sum_splits(const float* p, int splits, int64_t plan
 
 // x[t][blk] += sum_s partial[s][t][blk]; xb = x * w; ssp[t][blk] = sum of squares (kernels.cu:residual_kernel):
 // one warp per (token, 128-column block), the same per-lane columns, split order and shuffle tree
-__device__ __forceinline__ void residual_finish(const MkArgs& a, int t, int blk, int lane, float4 s4) {
+__device__ __forceinline__ void residual_finish(const MkArgs& a, const float* w, int t, int blk, int lane, float4 s4) {
     const int hidden = a.hidden, c0 = blk * 128 + lane * 4;
     float* xrow = a.x + (int64_t)t * hidden;
     const float v[4] = {s4.x, s4.y, s4.z, s4.w};
@@ -88,7 +88,7 @@ __device__ __forceinline__ void residual_finish(const MkArgs& a, int t, int blk,
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         xrow[c0 + e] = v[e];
-        ((bf16*)a.xb)[(int64_t)t * hidden + c0 + e] = __float2bfloat16_rn(v[e] * a.w[c0 + e]);
+        ((bf16*)a.xb)[(int64_t)t * hidden + c0 + e] = __float2bfloat16_rn(v[e] * w[c0 + e]);
         ss += v[e] * v[e];
         bad |= !isfinite(v[e]);
     }
@@ -124,8 +124,8 @@ __device__ void residual_phase(const MkArgs& a, const MkPhase& ph, int ew, int l
                     add_to(acc1, v1[i]);
                 }
         }
-        residual_finish(a, t0, b0, lane, acc0);
-        if (it2 < n_items) residual_finish(a, t1, b1, lane, acc1);
+        residual_finish(a, ph.rw, t0, b0, lane, acc0);
+        if (it2 < n_items) residual_finish(a, ph.rw, t1, b1, lane, acc1);
     }
 }
 

@@ -215,6 +215,7 @@ struct MkPhase {
     MkGemm g;
     const float* rpartial;  // RESIDUAL: the partial planes to add ([splits][M][hidden])
     int rsplits;
+    const float* rw;        // RESIDUAL: the next RMSNorm's weight (xb = x * rw)
 };
 struct MkArgs {
     int M, ntok, stages, n_phases, n_maps;
@@ -228,7 +229,6 @@ struct MkArgs {
     float* x;       // residual stream rows [M][hidden]
     void* xb;       // bf16 [M][hidden]
     float* ssp;     // [M][nb]
-    const float* w; // norm weight (1.0)
     int hidden, nb;
     float eps;
     int* err;
@@ -249,13 +249,21 @@ void launch_mk(MkArgs a, const MkMapSpec* specs, int n_maps, cudaStream_t s);
 
 // Reference-exact weights_checksum on the device (fingerprint.cu): FNV-1a 64 over a stream of 8-byte words given
 // as segments -- kind 0 literal / 1 constant: the word `a` repeated n times; kind 2: the draws
-// next_signed(seed, a + i) * scale (init_random, model.cpp:15-21). Returns the hash continued from h0.
+// next_signed(seed, a + i) * scale (init_random, model.cpp:15-21); kind 3: n words already in device memory at
+// address a. Returns the hash continued from h0. device_words materialises words [w0, w0 + n) of the list.
 struct FpSeg {
     uint64_t word0, n, a;
     double scale;
     int32_t kind, pad;
 };
 uint64_t device_fnv_words(const std::vector<FpSeg>& segs, uint64_t seed, uint64_t h0, cudaStream_t s);
+void device_words(const std::vector<FpSeg>& segs, uint64_t seed, uint64_t w0, int64_t n, uint64_t* d_out, cudaStream_t s);
+// TKVW loading: element range [e0, e0 + n) of a row-major f64 [rows][cols] reference tensor, cast f64 -> f32 (RN)
+// [-> bf16 (RNE)] and stored like launch_init_transposed (transposed, optional gate/up row interleave), or
+// row-major f32 (embedding, norm vectors)
+void launch_store_transposed_f64(void* dst, DT dt, const double* src, int64_t e0, int64_t n, int64_t rows, int64_t cols,
+                                 cudaStream_t s, int row_block = 0, int row_off = 0);
+void launch_store_f32_from_f64(float* dst, const double* src, int64_t n, cudaStream_t s);
 // Decode-sized attention (attn_decode.cu): bf16, d = 128, Tq * group in {4, 7, 8, 16} rows per kv head; split-K
 // flash decoding on CUDA cores with the SIMT workspace layout, merged by launch_attention_combine.
 bool attention_decode_supported(int Tq, int H, int Hkv, int d, DT dt);

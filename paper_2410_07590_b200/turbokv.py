@@ -126,6 +126,8 @@ def lib():
         L.tkv_engine_opts_default.argtypes = [C.POINTER(_Opts)]
         L.tkv_engine_create.argtypes = [C.POINTER(_Cfg), C.c_uint64, C.POINTER(_Opts), C.POINTER(C.c_void_p)]
         L.tkv_engine_destroy.argtypes = [C.c_void_p]
+        L.tkv_engine_create_from_weights.argtypes = [C.c_char_p, C.POINTER(_Opts), C.POINTER(C.c_void_p), C.POINTER(_Cfg)]
+        L.tkv_save_weights.argtypes = [C.POINTER(_Cfg), C.c_uint64, C.c_char_p, C.c_int]
         L.tkv_engine_fingerprint.argtypes = [C.c_void_p, U64P]
         L.tkv_ingest_chunks.argtypes = [C.c_void_p, I32P, I64P, C.c_int64, U64P, C.POINTER(_Stats)]
         L.tkv_import_tkvc.argtypes = [C.c_void_p, C.c_char_p, U64P]
@@ -288,6 +290,11 @@ def weights_identity(config: ModelConfig, seed: int):
     return ck.value, fp.value
 
 
+def save_weights(config: ModelConfig, seed: int, path: str, device: int = 0) -> None:
+    """TKVW file of init_random(config, seed) (tkv_save_weights; byte-identical to the reference's save_weights)."""
+    _check(lib().tkv_save_weights(C.byref(config._c()), seed, str(path).encode(), device))
+
+
 def weights_identity_device(config: ModelConfig, seed: int, device: int = 0):
     """(weights_checksum, model_fingerprint) hashed on GPU `device` (the engine's path, fingerprint.cu)."""
     ck, fp = C.c_uint64(), C.c_uint64()
@@ -391,7 +398,9 @@ class Engine:
 
     def __init__(self, config: ModelConfig, seed: int, dtype: str | Dtype = "bf16", device: int = 0,
                  page_tokens: int = 64, store_capacity_tokens: int = 0, max_position: int = 0,
-                 exact_fingerprint: int = -1, flags: int = 0, host_spill_tokens: int = 0):
+                 exact_fingerprint: int = -1, flags: int = 0, host_spill_tokens: int = 0, weights_path: str | None = None):
+        """Weights from (config, seed) in init_random's draw order, or -- weights_path -- from a TKVW file (the config
+        is then read from the file; `config` may be None)."""
         self.config = config
         self.seed = seed
         self._framed = {}  # chunk id -> framed tokens (host copy for the naive path / answer)
@@ -404,7 +413,12 @@ class Engine:
         o.host_spill_tokens = host_spill_tokens
         self.dtype = Dtype(o.dtype)
         h = C.c_void_p()
-        _check(lib().tkv_engine_create(C.byref(config._c()), seed, C.byref(o), C.byref(h)))
+        if weights_path is not None:
+            c = _Cfg()
+            _check(lib().tkv_engine_create_from_weights(str(weights_path).encode(), C.byref(o), C.byref(h), C.byref(c)))
+            self.config = ModelConfig(*[getattr(c, f) for f, _ in _Cfg._fields_])
+        else:
+            _check(lib().tkv_engine_create(C.byref(config._c()), seed, C.byref(o), C.byref(h)))
         self._h = h
 
     def close(self):
