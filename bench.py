@@ -298,18 +298,41 @@ def run_ours(args):
     payloads, query = workload()
     t0 = time.perf_counter()
     remote_frac = 0.0
+    routing = None
     if ws > 1:
-        # document-sharded store: chunk c belongs to document "chunk-c"; its owner prefills it, the other
-        # ranks register it under the owner's peer slot and the gather kernel reads it over NVLink
+        # document-sharded store over a corpus of N_CHUNKS x world chunks (4 chunks per document, owner = FNV(doc) mod
+        # world): the owner prefills a chunk, the other ranks register it under the owner's peer slot and the gather
+        # kernel reads it over NVLink. A front-end router (ShardedStore.route, simulated identically on every rank)
+        # sends each request of the global stream to the rank owning most of its chunk tokens, load-balanced; each
+        # rank then serves the requests routed to it (weak scaling: world x (warmup + steps) requests in total).
         from paper_2410_07590_b200.sharding import ShardedStore
+        corpus = [synth_payload(1000 + c, CHUNK_TOKENS - 2) for c in range(N_CHUNKS * ws)]
         store = ShardedStore(eng, rank, ws)
-        ids = store.ingest(payloads, [f"chunk-{c}" for c in range(N_CHUNKS)])
+        all_ids = store.ingest(corpus, [f"doc-{c // 4}" for c in range(len(corpus))])
         store.exchange()
+        rrng = np.random.default_rng(0xD0C)
+        mine, routed = [], [0] * ws
+        while len(mine) < args.warmup + args.steps:
+            req = [all_ids[i] for i in rrng.choice(len(corpus), N_CHUNKS, replace=False)]
+            dst = store.route(req)
+            routed[dst] += 1
+            if dst == rank:
+                mine.append(req)
+            if sum(routed) > 64 * ws * (args.warmup + args.steps):
+                raise RuntimeError("router starved this rank")
         if args.remote == "fetch":
-            store.cache_remote(ids)
-        remote_frac = store.remote_fraction(ids)
+            for req in mine:
+                store.cache_remote(req)
+        remote_frac = statistics.mean(store.remote_fraction(r) for r in mine)
+        routing = {"policy": "most locally-owned chunk tokens, then least loaded", "requests_routed": routed,
+                   "corpus_chunks": len(corpus)}
+        import itertools
+        req_iter = itertools.cycle(mine)
+        next_ids = lambda: next(req_iter)  # noqa: E731
+        ids = mine[0]  # the e2e / full-concat legs use one routed request
     else:
         ids = eng.ingest_chunks(payloads)
+        next_ids = lambda: ids  # noqa: E731
     torch.cuda.synchronize(dev)
     ingest_s = time.perf_counter() - t0
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
@@ -317,7 +340,7 @@ def run_ours(args):
     d_logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=dev)
 
     def step():
-        ctx = eng.assemble(ids, T.PositionMode.Reordered)
+        ctx = eng.assemble(next_ids(), T.PositionMode.Reordered)
         eng.prefill_query_device(ctx, d_query.data_ptr(), QUERY_TOKENS, d_logits.data_ptr())
         ctx.close()
 
@@ -334,6 +357,7 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    remote0 = eng.remote_bytes()
     with ClockSampler(local) as clocks:
         big0 = torch.cuda.Event(enable_timing=True)
         big1 = torch.cuda.Event(enable_timing=True)
@@ -345,7 +369,7 @@ def run_ours(args):
         big1.record(stream)
         torch.cuda.synchronize(dev)
     gpu_launches = eng.launch_count() - launches0
-    remote0 = eng.remote_bytes()
+    remote_step = (eng.remote_bytes() - remote0) / args.steps
     if args.turbo_only:
         print(json.dumps({"p50_ttft_ms": statistics.median([s.elapsed_time(e) for s, e in zip(starts, ends)])}))
         return
@@ -651,7 +675,11 @@ def run_ours(args):
         "c3_batch": c3,
         "c4_zipf_store": c4,
         "store": {"sharding": f"by document over {ws} GPU(s)", "remote_chunk_token_fraction": remote_frac,
-                  "remote_policy": args.remote if ws > 1 else "n/a"},
+                  "remote_policy": args.remote if ws > 1 else "n/a", "routing": routing,
+                  "remote_bytes_per_request": remote_step,
+                  "remote_gbs": remote_step / (ms_per_step / 1e3) / 1e9 if remote_step else 0.0,
+                  "remote_note": "KV bytes the gather read from peer pools (NVLink P2P on a multi-GPU box) per "
+                                 "request, and that traffic over the step time"},
         # per-class device time from CUDA events around every launch of a separate profiled pass: events between
         # kernels stop PDL overlap, so these are per-kernel durations in isolation (upper bounds; they sum to more
         # than ms_per_step). The ncu share below is the non-perturbing breakdown.
