@@ -323,6 +323,10 @@ tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* 
 /* attention pipeline timeline of CTA (0,0,0): on=1 arms it; out != NULL reads [32 tiles][10 events] clock64 */
 tkv_status tkv_debug_attn_trace(int on, uint64_t* out, int64_t capacity);
 tkv_status tkv_debug_set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first);
+/* GEMM pipeline trace of CTA 0 of the next tcgen05 GEMM launches (on != 0 arms and clears it; out != NULL first copies
+ * the last trace): clock64 per stage [it][3] = producer issue, MMA saw the stage full, MMA committed it (1024 stages),
+ * then [unit][2] = epilogue start / end (64 units). */
+tkv_status tkv_debug_gemm_trace(int on, uint64_t* out, int64_t capacity);
 tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int splits, int swiglu, int iters,
                                 double* ms_per_launch);
 tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const float* q, const float* k,

@@ -3063,6 +3063,10 @@ tkv_status tkv_debug_attn_trace(int on, uint64_t* out, int64_t capacity) {
     });
 }
 
+tkv_status tkv_debug_gemm_trace(int on, uint64_t* out, int64_t capacity) {
+    return guard([&] { gemm_trace_enable(on != 0, reinterpret_cast<unsigned long long*>(out), capacity); });
+}
+
 tkv_status tkv_debug_set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first) {
     return guard([&] { set_gemm_knobs(stages, smem_kb, ctas_per_sm, w_evict_first); });
 }
@@ -3078,6 +3082,9 @@ tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int
         w.ensure((size_t)N * K * 2);
         launch_init_transposed(a.p, DT::BF16, 1, 0, K, M, 0.01, 0);
         launch_init_transposed(w.p, DT::BF16, 2, 0, K, N, 0.01, 0);
+        if (swiglu & 2) TKV_CUDA(cudaMemset(w.p, 0, (size_t)N * K * 2));  // constant weights (data-dependence probe)
+        if (swiglu & 4) TKV_CUDA(cudaMemset(a.p, 0, (size_t)M * K * 2));
+        swiglu &= 1;
         const int nb = norm_blocks((int)K);
         ssp.ensure((size_t)M * nb * 4);
         launch_fill_f32(ssp.as<float>(), 1.0f, M * nb, 0);

@@ -83,6 +83,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         if (spin > (1u << 26)) __trap();
     }
 }
+// Same, for waits that last a whole mainloop (the epilogue warps on the accumulator): back off between polls so
+// the waiting warps do not compete with the MMA issuer and the TMA for the shared-memory / mbarrier unit.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    for (uint32_t spin = 0;; ++spin) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(256);
+        if (spin > (1u << 24)) __trap();
+    }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -154,6 +172,30 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
+// Warp-collective forms: called by all 32 lanes with warp-uniform operands; elect.sync picks the issuing lane (the
+// same one every time, so a commit tracks the MMAs that lane issued).
+__device__ __forceinline__ void umma_f16_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc_elect(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -196,7 +238,18 @@ struct GemmArgs {
     // nx_pf weight k-blocks of the next GEMM's units blockIdx.x, blockIdx.x + grid, ... (tmN), so that GEMM's
     // ring fill hits L2 while this one drains and runs its epilogue
     int nx_pf, nx_units, nx_n_tiles, nx_kb_total, nx_kb_per_split, nx_np;
+    unsigned long long* trace;    // debug (tkv_debug_gemm_trace): CTA 0 clock64 per stage [it][3] = producer issue,
+                                  // MMA saw full, MMA committed; [GT_UNIT + lu][2] = epilogue start / end per unit
 };
+constexpr int GT_STAGES = 1024, GT_UNIT = 3 * GT_STAGES, GT_EPI = GT_UNIT + 2 * 64 + 4 * 64, GT_SIZE = GT_EPI + 32;
+unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ void gtrace(unsigned long long* t, int slot) {
+    if (t && blockIdx.x == 0 && slot < GT_SIZE) {
+        unsigned long long c;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+        t[slot] = c;
+    }
+}
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
 constexpr int THREADS_P = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
@@ -310,6 +363,7 @@ __global__ void __launch_bounds__(THREADS_P)
                         tma_prefetch_2d(&tmW, kblk(k0, nkb, i + g.pf, u) * BK, nt * 128 * g.np);
                     const int s = it % g.stages;
                     mbar_wait(&empty[s], ((uint32_t)(it / g.stages) & 1u) ^ 1u);
+                    if (it < GT_STAGES) gtrace(g.trace, 3 * it);
                     uint8_t* w = smem + s * stage_bytes;
                     mbar_expect_tx(&full[s], stage_bytes);
                     const int kb = kblk(k0, nkb, i, u);
@@ -326,42 +380,58 @@ __global__ void __launch_bounds__(THREADS_P)
                 }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer ----------------
-            const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128 * g.np);
-            int it = 0, lu = 0;
-            for (int u = u0; u < g.units; u += ustep, ++lu) {
-                int nt, mt, z;
-                coords(u, nt, mt, z);
-                const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
-                const int b = lu % g.nbuf;
-                mbar_wait(&tempty[b], ((uint32_t)(lu / g.nbuf) & 1u) ^ 1u);
+        // ---------------- MMA issuer ----------------
+        // The whole warp walks the loop, so every operand (stage address, descriptors, TMEM address) is warp-uniform
+        // and lives in uniform registers; one elected lane issues each tcgen05.mma / commit. (A lane-0-only loop made
+        // the compiler move every operand through an R2UR waterfall: ~165 cycles per MMA issue, which capped one CTA
+        // at one 64-deep k-block per ~1100 cycles, i.e. ~28 GB/s of weights.)
+        const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128 * g.np);
+        int it = 0, lu = 0;
+        for (int u = u0; u < g.units; u += ustep, ++lu) {
+            int nt, mt, z;
+            coords(u, nt, mt, z);
+            const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
+            const int b = lu % g.nbuf;
+            mbar_wait(&tempty[b], ((uint32_t)(lu / g.nbuf) & 1u) ^ 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t acc = tmem + (uint32_t)b * g.acc_cols;
+            int s = it % g.stages;
+            uint32_t ph = (uint32_t)(it / g.stages) & 1u;
+            for (int i = 0; i < nkb; ++i, ++it) {
+                mbar_wait(&full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t acc = tmem + (uint32_t)b * g.acc_cols;
-                for (int i = 0; i < nkb; ++i, ++it) {
-                    const int s = it % g.stages;
-                    mbar_wait(&full[s], (uint32_t)(it / g.stages) & 1u);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t w = smem_u32(smem + s * stage_bytes);
-                    const uint32_t a = w + wbytes;
+                if (lane == 0 && it < GT_STAGES) gtrace(g.trace, 3 * it + 1);
+                const uint32_t w = smem_u32(smem + s * stage_bytes);
+                const uint32_t a = w + wbytes;
+                if (SWAP) {
+                    const uint64_t da = desc_k(a);
+                    for (int p = 0; p < g.np; ++p) {  // one activation tile, np weight tiles
+                        const uint64_t dw = desc_k(w + p * TILE_W);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {  // 16 bf16 = 32 B along K inside the 128 B swizzle row
-                        if (SWAP) {
-                            for (int p = 0; p < g.np; ++p)  // one activation tile, np weight tiles
-                                umma_f16(acc + (uint32_t)(p * g.ntok), desc_k(w + p * TILE_W + k * 32),
-                                         desc_k(a + k * 32), id, (i | k) != 0);
-                        } else {
-                            for (int mi = 0; mi < g.mp; ++mi)  // mp activation sub-tiles share the weight tile
-                                umma_f16(acc + (uint32_t)(mi * 128 * g.np), desc_k(a + mi * 16384 + k * 32),
-                                         desc_k(w + k * 32), id, (i | k) != 0);
-                        }
+                        for (int k = 0; k < BK / 16; ++k)  // +32 B along K inside the 128 B swizzle row = +2 in the
+                                                           // descriptor's 16-byte address field
+                            umma_f16_elect(acc + (uint32_t)(p * g.ntok), dw + 2 * k, da + 2 * k, id, (i | k) != 0);
                     }
-                    if (cl > 1)
-                        umma_commit_mc(&empty[s], (uint16_t)((1u << cl) - 1));  // both CTAs read the weight tile
-                    else
-                        umma_commit(&empty[s]);
+                } else {
+                    const uint64_t dw = desc_k(w);
+                    for (int mi = 0; mi < g.mp; ++mi) {  // mp activation sub-tiles share the weight tile
+                        const uint64_t da = desc_k(a + mi * 16384);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k)
+                            umma_f16_elect(acc + (uint32_t)(mi * 128 * g.np), da + 2 * k, dw + 2 * k, id, (i | k) != 0);
+                    }
                 }
-                umma_commit(&tfull[b]);
+                if (cl > 1)
+                    umma_commit_mc_elect(&empty[s], (uint16_t)((1u << cl) - 1));  // both CTAs read the weight tile
+                else
+                    umma_commit_elect(&empty[s]);
+                if (lane == 0 && it < GT_STAGES) gtrace(g.trace, 3 * it + 2);
+                if (++s == g.stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
+            umma_commit_elect(&tfull[b]);
         }
     } else {
         // ---------------- epilogue warps 2-5: TMEM lane group = warp % 4 ----------------
@@ -374,8 +444,9 @@ __global__ void __launch_bounds__(THREADS_P)
             int nt, mt, z;
             coords(u, nt, mt, z);
             const int b = lu % g.nbuf;
-            mbar_wait(&tfull[b], (uint32_t)(lu / g.nbuf) & 1u);
+            mbar_wait_sleep(&tfull[b], (uint32_t)(lu / g.nbuf) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (et == 0 && lu < 64) gtrace(g.trace, GT_UNIT + 2 * lu);
             const uint32_t acc_u = tmem + lane_base + (uint32_t)b * g.acc_cols;
             const int m0 = mt * mstep;
             for (int pm = 0; pm < g.np * (SWAP ? 1 : g.mp); ++pm) {
@@ -408,6 +479,9 @@ __global__ void __launch_bounds__(THREADS_P)
                     if (et < g.ntok) tok_scale[et] = m0 + et < g.M ? row_scale(g.ssp, g.nb, m0 + et, g.K, g.eps) : 0.f;
                     const int inter = g.N / 2;
                     const int i = (n0 / 128) * 64 + lg * 32 + lane;
+                    int ev = 0;
+                    auto tr = [&]() { if (lu == 0 && (et == 64 || et == 0)) gtrace(g.trace, GT_EPI + (et ? 16 : 0) + ev); ++ev; };
+                    tr();
                     for (int c0 = 0; c0 < g.ntok; c0 += XC) {
                         const int c1 = min(g.ntok, c0 + XC);
                         if (lg >= 2) {
@@ -419,7 +493,9 @@ __global__ void __launch_bounds__(THREADS_P)
                                 for (int j = 0; j < 16; ++j) up[((lg - 2) * 32 + lane) * ld + c - c0 + j] = __uint_as_float(r[j]);
                             }
                         }
+                        tr();
                         asm volatile("bar.sync 1, 128;" ::: "memory");
+                        tr();
                         if (lg < 2) {
 #pragma unroll 1
                             for (int c = c0; c < c1; c += 16) {
@@ -436,7 +512,9 @@ __global__ void __launch_bounds__(THREADS_P)
                                 }
                             }
                         }
+                        tr();
                         asm volatile("bar.sync 1, 128;" ::: "memory");  // scratch reusable (next pass / unit)
+                        tr();
                     }
                 }
             } else {
@@ -492,6 +570,7 @@ __global__ void __launch_bounds__(THREADS_P)
             }  // p
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
+            if (et == 0 && lu < 64) gtrace(g.trace, GT_UNIT + 2 * lu + 1);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -908,6 +987,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.scratch_off = (uint32_t)g.stages * (g.np * TILE_W + g.a_bytes) + 256;  // after the ring and its barriers
     g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;
     g.partial = partial;
+    g.trace = g_gemm_trace;
     g.act = (__nv_bfloat16*)swiglu_act;
     g.ssp = ssp;
     g.nb = nb;
@@ -999,6 +1079,17 @@ int launch_gemm_mlp(const void* xb, int lda, const void* w_gu, void* act, const 
     launch_k(gemm_mlp_kernel, dim3(grid), dim3(THREADS_P), smem, s, tx, twg, ta, twd, m);
     TKV_CUDA(cudaGetLastError());
     return eff;
+}
+
+void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap) {
+    static unsigned long long* buf = nullptr;
+    if (host_out && buf) {
+        TKV_CUDA(cudaDeviceSynchronize());
+        TKV_CUDA(cudaMemcpy(host_out, buf, (size_t)std::min<int64_t>(cap, GT_SIZE) * 8, cudaMemcpyDeviceToHost));
+    }
+    if (on && !buf) TKV_CUDA(cudaMalloc(&buf, GT_SIZE * 8));
+    if (on) TKV_CUDA(cudaMemset(buf, 0, GT_SIZE * 8));
+    g_gemm_trace = on ? buf : nullptr;
 }
 
 void set_gemm_next(const void* W, int M, int N, int K, int splits) { g_next = NextGemm{W, M, N, K, splits}; }

@@ -189,6 +189,7 @@ def lib():
         L.tkv_remote_bytes.argtypes = [C.c_void_p]
         L.tkv_debug_attn_trace.argtypes = [C.c_int, U64P, C.c_int64]
         L.tkv_debug_set_gemm_knobs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+        L.tkv_debug_gemm_trace.argtypes = [C.c_int, U64P, C.c_int64]
         L.tkv_debug_gemm_bench.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
                                            C.POINTER(C.c_double)]
         L.tkv_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, F32P, F32P, C.c_int64, C.c_int64, C.c_int64,

@@ -1,0 +1,44 @@
+"""Per-stage pipeline trace of CTA 0 of one tcgen05 GEMM (tkv_debug_gemm_trace): producer issue / MMA-saw-full /
+MMA-commit clock64 stamps, summarised as cycles between consecutive stages and producer-vs-MMA slack.
+usage: python tools/gemm_trace.py M N K splits swiglu stages smem_kb ctas_per_sm"""
+import ctypes as C
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+from paper_2410_07590_b200 import turbokv as T
+
+L = T.lib()
+M, N, K, sp, sw, st, smk, cps = (int(v) for v in sys.argv[1:9])
+T._check(L.tkv_debug_set_gemm_knobs(st, smk, cps, 1))
+ms = C.c_double()
+T._check(L.tkv_debug_gemm_bench(0, M, N, K, sp, sw, 5, C.byref(ms)))  # warm
+T._check(L.tkv_debug_gemm_trace(1, None, 0))
+T._check(L.tkv_debug_gemm_bench(0, M, N, K, sp, sw, 1, C.byref(ms)))
+buf = np.zeros(3 * 1024 + 128 + 256 + 32, np.uint64)
+T._check(L.tkv_debug_gemm_trace(0, buf.ctypes.data_as(C.POINTER(C.c_uint64)), buf.size))
+st3 = buf[:3072].reshape(1024, 3).astype(np.int64)
+n = int((st3[:, 1] > 0).sum())
+st3 = st3[:n]
+t0 = st3[st3 > 0].min()
+rel = (st3 - t0)
+full = rel[:, 1]
+print(f"M={M} N={N} K={K} splits={sp} swiglu={sw} stages={st} smem={smk} cps={cps}: {ms.value*1e3:.2f} us/launch, CTA0 {n} stages")
+d = np.diff(full)
+print(f"  MMA-saw-full interval: median {np.median(d):.0f} cyc, mean {d.mean():.0f}, p90 {np.percentile(d, 90):.0f}")
+print(f"  MMA issue cost (commit - full): median {np.median(rel[:, 2] - rel[:, 1]):.0f} cyc")
+iss = rel[:, 0]
+valid = iss > 0
+lat = (full - iss)[valid]
+print(f"  producer issue -> full (load latency incl. queueing): median {np.median(lat):.0f} cyc, min {lat.min()}, max {lat.max()}")
+print("  first 12 stages (issue, full, commit):", [tuple(int(x) for x in r) for r in rel[:12]])
+u = buf[3072:3072 + 128].reshape(64, 2).astype(np.int64)
+mm = buf[3200:3456].reshape(64, 4).astype(np.int64)
+for r in range(8, 12):
+    print(f'  stage {r}: full {int(rel[r, 1])} mma-issued', [int(x - t0) for x in mm[r]], 'commit', int(rel[r, 2]))
+u = u[u[:, 0] > 0] - t0
+print("  epilogue per unit (start, end):", [tuple(int(x) for x in r) for r in u[:8]])
+ep = buf[3072 + 384:].astype(np.int64)
+print("  swiglu epilogue unit 0, gate warp:", [int(x - t0) if x else 0 for x in ep[:9]], " up warp:", [int(x - t0) if x else 0 for x in ep[16:25]])
+print(f"  last stage full at {int(full[-1])} cyc")

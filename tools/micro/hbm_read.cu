@@ -1,6 +1,7 @@
 // Pure-read HBM bandwidth ceiling (the weight stream of a batch-1 forward is read-only).
 // nvcc -O3 -gencode arch=compute_100a,code=sm_100a hbm_read.cu -o hbm_read
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 __global__ void rd(const uint4* __restrict__ p, size_t n, unsigned* out) {
     unsigned acc = 0;
@@ -19,8 +20,8 @@ __global__ void cp(const uint4* __restrict__ a, uint4* __restrict__ b, size_t n)
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) b[i] = a[i];
 }
-int main() {
-    const size_t bytes = (size_t)4 << 30, n = bytes / 16;
+int main(int argc, char** argv) {
+    const size_t bytes = argc > 1 ? (size_t)atol(argv[1]) << 20 : (size_t)4 << 30, n = bytes / 16;
     uint4 *a, *b;
     unsigned* o;
     cudaMalloc(&a, bytes);

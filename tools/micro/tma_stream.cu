@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 __device__ __forceinline__ uint32_t su(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
     uint32_t d = 0;
@@ -85,15 +86,24 @@ __global__ void stream(const __grid_constant__ CUtensorMap tm, const __grid_cons
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tslot));
     }
 }
+__global__ void fill_rand(uint32_t* p, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t x = (uint32_t)i * 2654435761u ^ 0x9E3779B9u;
+        x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
+        p[i] = (x & 0x3FFF3FFFu) | 0x3C003C00u;  // small bf16 pairs, random mantissas and signs off
+    }
+}
 typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                         const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                         CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-int main() {
-    const int N = 37888, K = 3584, kb = K / 64, n_tiles = N / 128;
+int main(int argc, char** argv) {
+    const int N = 37888 * (argc > 1 ? atoi(argv[1]) : 1), K = 3584, kb = K / 64, n_tiles = N / 128;
     const size_t bytes = (size_t)N * K * 2;
     uint8_t* w;
     cudaMalloc(&w, bytes);
     cudaMemset(w, 1, bytes);
+    const bool rnd = argc > 2;
+    if (rnd) fill_rand<<<1184, 256>>>((uint32_t*)w, bytes / 4);
     void* fn;
     cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
@@ -105,6 +115,7 @@ int main() {
     uint8_t* act;
     cudaMalloc(&act, (size_t)64 * K * 2);
     cudaMemset(act, 1, (size_t)64 * K * 2);
+    if (rnd) fill_rand<<<64, 256>>>((uint32_t*)act, (size_t)64 * K / 2);
     CUtensorMap ta;
     const cuuint64_t adims[2] = {(cuuint64_t)K, 64}, astr[1] = {(cuuint64_t)K * 2};
     const cuuint32_t abox[2] = {64, 64};
@@ -113,7 +124,7 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int mode = 0; mode < 6; ++mode)
+    for (int mode = (argc > 3 ? atoi(argv[3]) : 0); mode < 6; ++mode)
         for (int cfg = 0; cfg < 4; ++cfg) {
             const int cps = cfg < 2 ? 2 : 1, stages = cfg == 0 ? 4 : cfg == 1 ? 6 : cfg == 2 ? 8 : 12;
             const size_t smem = 1024 + stages * ((mode == 2 || mode == 3 || mode == 5) ? 24576 : 16384) + 256;
