@@ -87,7 +87,7 @@ typedef struct {
 #define TKV_FLAG_NO_PDL 0x8       /* launch kernels without programmatic dependent launch          */
 #define TKV_FLAG_L2_PREFETCH 0x10  /* reserved (attention-time L2 weight prefetch: measured no gain) */
 #define TKV_FLAG_BATCH_ATTN 0x20   /* batched prefill: one attention launch even when the batch cannot fill the GPU */
-#define TKV_FLAG_LAYER_KERNEL 0x80 /* <= 128-token bf16 forwards: one persistent layer kernel per layer (mk.cu) instead of the kernel chain */
+#define TKV_FLAG_LAYER_KERNEL 0x80 /* reserved (the persistent layer-kernel experiment was measured slower and removed) */
 #define TKV_FLAG_DECODE_ATTN 0x40 /* bf16: decode-sized (<= 16 rows / kv head) forwards use the split-K mma.sync kernel */
 
 /* IngestStats (pipeline.hpp:35-39) */
@@ -313,9 +313,6 @@ tkv_status tkv_debug_weights_checksum(const tkv_model_config* cfg, uint64_t seed
  * which 0 = Wqkv (wq | wk | wv rows), 1 = Wo, 2 = Wgu (gate / up rows interleaved in 64-row blocks when
  * intermediate_size % 64 == 0), 3 = Wdown, 4 = lm_head, 5 = embedding (f32 [vocab][hidden]). */
 tkv_status tkv_debug_weight_rows(tkv_engine* eng, int64_t layer, int which, int64_t row0, int64_t nrows, float* out);
-/* Layer-kernel timeline of the launch selected by TKV_MK_TRACE=<layer> (TUNING builds): [cta][32] globaltimer ns;
- * slot 0 = worker start, 1 + p = end of phase p, 8 + p = A-producer past phase p's dependency, 16 + p = workers past it. */
-tkv_status tkv_debug_mk_trace(tkv_engine* eng, uint64_t* out, int64_t capacity);
 tkv_status tkv_debug_gemm(int device, tkv_dtype dtype, int use_tc, const float* A, const float* W, int64_t M,
                           int64_t N, int64_t K, int splits, float* out);
 /* GEMM tuning/timing (tools/gemm_sweep.py): knobs = ring stages, smem budget KB, CTAs per SM, weight

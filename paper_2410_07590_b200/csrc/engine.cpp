@@ -334,6 +334,7 @@ struct tkv_engine {
     bool exact_fp = false;
     int64_t L, H, Hkv, d, hid, I, V, qd, kvd, nqkv;
     bool gu_interleaved = false;
+    int gu_block = 0;  // W_gu rows in blocks of gu_block gate + gu_block up rows (128 | 64 | 0 = gate rows then up rows)
 
     // weights
     DevMem wmem;
@@ -534,23 +535,7 @@ struct tkv_engine {
 
     bool use_tc() const { return dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_GEMM); }
 
-    // fused gate/up + down launch (gemm_tc.cu:gemm_mlp_kernel): <= 128 rows, interleaved W_gu whose GEMM runs
-    // without split-K, dims multiples of the 64-wide k-block
     int batch_attn_splits = 1;  // TKV_BATCH_ATTN_SPLITS (0 = attn_tc_batch_pick_splits; measured on par)
-    int fused_mlp = 0;  // TKV_FUSED_MLP=1 (opt-in: measured slower)
-    DevMem mlp_flags, mlp_ctl;
-    bool fused_mlp_ok(int rows) {
-        if (!fused_mlp || !use_tc() || !gu_interleaved || rows > 128 || hid % 64 || I % 64) return false;
-        if (pick_splits(rows, (int)(2 * I), (int)hid, true) != 1) return false;
-        if (!mlp_flags.p) {
-            mlp_flags.ensure((size_t)(2 * I / 128) * sizeof(unsigned));
-            mlp_ctl.ensure(2 * sizeof(unsigned));
-            TKV_CUDA(cudaMemset(mlp_flags.p, 0, (size_t)(2 * I / 128) * sizeof(unsigned)));
-            const unsigned init[2] = {1u, 0u};
-            TKV_CUDA(cudaMemcpy(mlp_ctl.p, init, sizeof init, cudaMemcpyHostToDevice));
-        }
-        return true;
-    }
 
     // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits. With swiglu_act, a tcgen05 GEMM whose
     // K range fits one CTA writes silu(gate)*up straight to swiglu_act and returns 0.
@@ -562,7 +547,8 @@ struct tkv_engine {
         const int s = pick_splits(M, N, K, tc);
         Scope sc(this, PC_GEMM, 1);
         if (tc && swiglu_act && s == 1 && gu_interleaved) {
-            launch_gemm_tc(A, lda, W, M, N, K, nullptr, 1, stream, swiglu_act, ssp.as<float>(), nb, (float)cfg.norm_eps);
+            launch_gemm_tc(A, lda, W, M, N, K, nullptr, 1, stream, swiglu_act, ssp.as<float>(), nb, (float)cfg.norm_eps,
+                           gu_block);
             return 0;
         }
         partial.ensure((size_t)s * M * N * sizeof(float));
@@ -597,16 +583,6 @@ struct tkv_engine {
         int batch_min_keys = 0;  // shortest request context (keys) of the batched attention
     };
     void forward(const Fwd& f);
-    // the persistent layer kernel path (mk.cu) of forward() for <= 128-token bf16 forwards
-    bool mk_eligible(const Fwd& f) const;
-    void forward_mk(const Fwd& f);
-    DevMem mk_bar;                     // phase counters of the layer kernel (monotone across launches)
-    int mk_l2_ahead = 0;               // TKV_MK_L2_AHEAD (tuning): weight tiles pulled into L2 beyond the ring
-    int mk_krot = 0;                   // TKV_MK_KROT (tuning)
-    int mk_nodep = 0;                  // TKV_MK_NODEP (timing only: results invalid)
-    int mk_trace_layer = -1;           // TKV_MK_TRACE (tuning): timeline of that layer's layer-kernel launch
-    DevMem mk_trace;
-    unsigned mk_uses[MK_MAX_PHASES] = {};
     void attend_layer(int64_t l, int T, const void* qrows, tkv_context* actx, const int32_t* lo, const int32_t* hi,
                       void* out, int arows, int aTk, int kv_ready);
     void check_err(const char* where);
@@ -723,168 +699,7 @@ void tkv_engine::attend_layer(int64_t l, int T, const void* qrows, tkv_context* 
     }
 }
 
-bool tkv_engine::mk_eligible(const Fwd& f) const {
-    if (!use_tc() || !(opts.flags & TKV_FLAG_LAYER_KERNEL) || !f.reqs.empty() || f.kv_only || !gu_interleaved) return false;
-    if (!mk_supported(f.T, (int)hid, (int)I, (int)qd, (int)kvd)) return false;
-    return pick_splits(f.T, (int)(2 * I), (int)hid, true) == 1 && pick_splits(1, (int)(2 * I), (int)hid, true) == 1;
-}
-
-// forward() through the persistent layer kernel (mk.cu): per layer ONE attention launch (+ its split merge) and ONE
-// layer-kernel launch running O-proj, residual, gate/up + SwiGLU, down, residual and the NEXT layer's QKV + QKV
-// epilogue; the same unit partitions, k-block orders and split-K summation orders as the kernel chain of forward(),
-// so the logits are bitwise those of the chain. Opt-in (TKV_FLAG_LAYER_KERNEL): measured slower than the PDL-overlapped
-// chain at C2 (the weight stream of this tiling is the limit either way, and the phase barriers
-// plus the element-wise phases on 8 warps per SM cost more than the chain's overlapped epilogue kernels).
-void tkv_engine::forward_mk(const Fwd& f) {
-    const int T = f.T, Tk = f.row0 + f.T;
-    const size_t es = dt_size(dt);
-    const float eps = (float)cfg.norm_eps;
-    x.ensure((size_t)T * hid * 4);
-    xb.ensure((size_t)T * hid * es);
-    const int nb = norm_blocks((int)hid);
-    ssp.ensure((size_t)T * nb * 4);
-    q.ensure((size_t)T * qd * es);
-    attn.ensure((size_t)T * qd * es);
-    act.ensure((size_t)T * I * es);
-    if (!mk_bar.p) {
-        mk_bar.ensure(64 * sizeof(unsigned));
-        TKV_CUDA(cudaMemsetAsync(mk_bar.p, 0, 64 * sizeof(unsigned), stream));
-    }
-    const unsigned grid = (unsigned)mk_grid(device);
-    {
-        Scope sc(this, PC_EPI, 1);
-        launch_embed(f.tok, T, emb, (int)hid, (int)V, norm_attn(0), x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
-                     stream);
-    }
-    // phase slots: 0 O, 1 residual, 2 gate/up, 3 down, 4 residual, 5 QKV, 6 QKV epilogue
-    enum { S_O = 0, S_R1, S_GU, S_D, S_R2, S_QKV, S_QE };
-    size_t part_floats = 0;
-    struct Plan {
-        MkArgs a{};
-        MkMapSpec maps[MK_MAX_MAPS];
-        int n_maps = 0;
-    };
-    auto map = [&](Plan& p, const void* base, int rows, int cols, int box) {
-        p.maps[p.n_maps] = MkMapSpec{base, rows, cols, cols, box};
-        return p.n_maps++;
-    };
-    auto gemm = [&](Plan& p, int slot, const void* W, const void* A, int M, int N, int K, bool swiglu) -> int {
-        MkPhase& ph = p.a.ph[p.a.n_phases++];
-        ph.kind = MK_GEMM;
-        ph.slot = slot;
-        const int ntok = ((M + 15) / 16) * 16;
-        ph.g.map_w = map(p, W, N, K, 128);
-        ph.g.map_a = map(p, A, M, K, ntok);
-        ph.g.N = N;
-        ph.g.K = K;
-        ph.g.kb_total = (K + 63) / 64;
-        const int s = pick_splits(M, N, K, true);  // the chain's split count: identical partial planes
-        ph.g.kb_per_split = (ph.g.kb_total + s - 1) / s;
-        const int eff = (ph.g.kb_total + ph.g.kb_per_split - 1) / ph.g.kb_per_split;
-        ph.g.n_tiles = (N + 127) / 128;
-        ph.g.units = ph.g.n_tiles * eff;
-        ph.g.swiglu = swiglu ? 1 : 0;
-        ph.g.partial = partial.as<float>();
-        ph.g.act = act.p;
-        if (swiglu && eff != 1) fail(TKV_ERR_CONFIG, "layer kernel: SwiGLU epilogue needs one split");
-        if (!swiglu) part_floats = std::max(part_floats, (size_t)eff * M * N);
-        return eff;
-    };
-    auto elem = [&](Plan& p, int slot, int kind, const float* rpartial, int rsplits, const float* w = nullptr) {
-        MkPhase& ph = p.a.ph[p.a.n_phases++];
-        ph.kind = kind;
-        ph.slot = slot;
-        ph.rpartial = rpartial;
-        ph.rsplits = rsplits;
-        ph.rw = w;
-    };
-    auto common = [&](Plan& p, int M, float* x_rows) {
-        MkArgs& a = p.a;
-        a.M = M;
-        a.l2_ahead = mk_l2_ahead;
-        a.krot = mk_krot;
-        a.nodep = mk_nodep;
-        a.bar = mk_bar.as<unsigned>();
-        a.x = x_rows;
-        a.xb = xb.p;
-        a.ssp = ssp.as<float>();
-        a.hidden = (int)hid;
-        a.nb = nb;
-        a.eps = eps;
-        a.err = err.as<int>();
-        a.H = (int)H, a.Hkv = (int)Hkv, a.d = (int)d;
-        a.pos = f.pos;
-        a.rope = rope.as<float2>();
-        a.q = q.p;
-        a.row0 = f.row0;
-    };
-    auto qkv = [&](Plan& p, int64_t layer) {
-        const int s = gemm(p, S_QKV, w_qkv[layer], xb.p, T, (int)nqkv, (int)hid, false);
-        elem(p, S_QE, MK_QKV_EPI, nullptr, 0);
-        p.a.qpartial = partial.as<float>();
-        p.a.qsplits = s;
-        p.a.kc = kv_plane(f.ctx, layer, 0);
-        p.a.vc = kv_plane(f.ctx, layer, 1);
-    };
-    auto mlp = [&](Plan& p, int64_t layer, int M) {
-        const int so = gemm(p, S_O, w_o[layer], attn.p, M, (int)hid, (int)qd, false);
-        elem(p, S_R1, MK_RESIDUAL, partial.as<float>(), so, norm_mlp(layer));
-        gemm(p, S_GU, w_gu[layer], xb.p, M, (int)(2 * I), (int)hid, true);
-        const int sd = gemm(p, S_D, w_down[layer], act.p, M, (int)hid, (int)I, false);
-        elem(p, S_R2, MK_RESIDUAL, partial.as<float>(), sd, norm_after_mlp(layer));
-    };
-    auto launch = [&](Plan& p) {
-        for (int i = 0; i < p.a.n_phases; ++i) {
-            MkPhase& ph = p.a.ph[i];
-            mk_uses[ph.slot] += 1;
-            ph.target = mk_uses[ph.slot] * grid;  // wraps with the counter
-        }
-        partial.ensure(part_floats * sizeof(float));
-        for (int i = 0; i < p.a.n_phases; ++i) {  // the partial buffer may have been (re)allocated
-            if (p.a.ph[i].kind == MK_GEMM) p.a.ph[i].g.partial = partial.as<float>();
-            if (p.a.ph[i].kind == MK_RESIDUAL) p.a.ph[i].rpartial = partial.as<float>();
-        }
-        if (p.a.qsplits) p.a.qpartial = partial.as<float>();
-        Scope sc(this, PC_GEMM, 1);
-        launch_mk(p.a, p.maps, p.n_maps, stream);
-    };
-    {  // layer 0's QKV projection + epilogue
-        Plan p;
-        common(p, T, x.as<float>());
-        qkv(p, 0);
-        launch(p);
-    }
-    for (int64_t l = 0; l < L; ++l) {
-        // in the last layer only the final row feeds the logits: attention, O-proj and the MLP run on it alone
-        const bool tail = (l == L - 1) && f.logits;
-        const int rows = tail ? 1 : T;
-        const int64_t r0 = tail ? T - 1 : 0;
-        attend_layer(l, T, static_cast<uint8_t*>(q.p) + (size_t)r0 * qd * es, f.ctx, f.lo + r0, f.hi + r0, attn.p, rows,
-                     Tk, f.row0);
-        Plan p;
-        common(p, rows, x.as<float>() + r0 * hid);
-        mlp(p, l, rows);
-        if (l + 1 < L) qkv(p, l + 1);
-        if (mk_trace_layer == (int)l) {
-            mk_trace.ensure(4096 * 32 * 8);
-            TKV_CUDA(cudaMemsetAsync(mk_trace.p, 0, 4096 * 32 * 8, stream));
-            p.a.trace = mk_trace.as<unsigned long long>();
-        }
-        launch(p);
-    }
-    if (f.logits) {  // after the tail layer, xb row 0 holds final_norm(x) of the last token
-        Scope sc(this, PC_OTHER, 1);
-        launch_lm_head(xb.p, w_lm, (int)hid, (int)V, logits.as<float>(), ssp.as<float>(), nb, eps, dt, err.as<int>(),
-                       stream);
-    }
-}
-
-// One decoder forward (model.cpp:198-272) over T new tokens whose K/V go to cache rows [row0, row0+T).
 void tkv_engine::forward(const Fwd& f) {
-    if (mk_eligible(f)) {
-        forward_mk(f);
-        return;
-    }
     const int T = f.T, Tk = f.row0 + f.T;
     const bool batch = !f.reqs.empty();
     const size_t es = dt_size(dt);
@@ -972,25 +787,15 @@ void tkv_engine::forward(const Fwd& f) {
                             err.as<int>(), stream);
         }
         // --- MLP block: gate|up fused into one GEMM, SwiGLU (with the folded mlp_norm scale) in its epilogue ---
-        if (fused_mlp_ok(rows)) {
-            // gate/up + SwiGLU and the down GEMM in ONE persistent launch (the down weights stream during the
-            // gate/up tail; act k-blocks handed over through readiness flags)
-            const int s2 = pick_splits(rows, (int)hid, (int)I, true);
-            partial.ensure((size_t)s2 * rows * hid * sizeof(float));
-            Scope sc(this, PC_GEMM, 1);
-            s = launch_gemm_mlp(xb.p, (int)hid, w_gu[l], act.p, w_down[l], rows, (int)hid, (int)I, partial.as<float>(),
-                                s2, mlp_flags.as<unsigned>(), mlp_ctl.as<unsigned>(), ssp.as<float>(), nb, eps, stream);
-        } else {
-            next(w_down[l], rows, (int)hid, (int)I);
-            s = gemm(xb.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
-            if (s > 0) {
-                Scope sc(this, PC_EPI, 1);
-                launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, ssp.as<float>(), nb, (int)hid, eps, dt,
-                              stream, gu_interleaved);
-            }
-            if (l + 1 < L) next(w_qkv[l + 1], T, (int)nqkv, (int)hid);
-            s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
+        next(w_down[l], rows, (int)hid, (int)I);
+        s = gemm(xb.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
+        if (s > 0) {
+            Scope sc(this, PC_EPI, 1);
+            launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, ssp.as<float>(), nb, (int)hid, eps, dt,
+                          stream, gu_block);
         }
+        if (l + 1 < L) next(w_qkv[l + 1], T, (int)nqkv, (int)hid);
+        s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
         if (!(skip_mask & 2)) {
             // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
             Scope sc(this, PC_EPI, 1);
@@ -1539,7 +1344,8 @@ static tkv_status create_engine(const tkv_model_config* cfg, uint64_t seed, cons
         e->L = c.layer_num, e->H = c.head_num, e->Hkv = c.kv_head_num, e->d = c.head_size, e->hid = c.hidden_size;
         e->I = c.intermediate_size, e->V = c.vocab_size, e->qd = e->H * e->d, e->kvd = e->Hkv * e->d;
         e->nqkv = e->qd + 2 * e->kvd;
-        e->gu_interleaved = e->I % 64 == 0;
+        e->gu_block = e->I % 128 == 0 ? 128 : e->I % 64 == 0 ? 64 : 0;
+        e->gu_interleaved = e->gu_block > 0;
         if (e->d != 8 && e->d != 16 && e->d != 32 && e->d != 64 && e->d != 128)
             fail(TKV_ERR_CONFIG, "head_size must be one of 8/16/32/64/128 for the device kernels");
 
@@ -1606,12 +1412,12 @@ static tkv_status create_engine(const tkv_model_config* cfg, uint64_t seed, cons
             cur += (uint64_t)(H_ * kvd);
             launch_init_transposed(o, e->dt, seed, cur, qd, H_, scale, e->stream);
             cur += (uint64_t)(qd * H_);
-            // gate | up rows: interleaved in 64-row blocks when I % 64 == 0 (fused SwiGLU epilogue)
-            const int rb = e->gu_interleaved ? 64 : 0;
+            // gate | up rows: interleaved in gu_block-row blocks (fused SwiGLU epilogue)
+            const int rb = e->gu_block;
             launch_init_transposed(gu, e->dt, seed, cur, H_, I, scale, e->stream, rb, 0);
             cur += (uint64_t)(H_ * I);
             launch_init_transposed(rb ? gu : gu + (size_t)I * H_ * es, e->dt, seed, cur, H_, I, scale, e->stream, rb,
-                                   rb ? 64 : 0);
+                                   rb);
             cur += (uint64_t)(H_ * I);
             launch_init_transposed(dn, e->dt, seed, cur, I, H_, scale, e->stream);
             cur += (uint64_t)(I * H_);
@@ -1632,11 +1438,6 @@ static tkv_status create_engine(const tkv_model_config* cfg, uint64_t seed, cons
         if (const char* np = getenv("TKV_GEMM_NEXT_PF")) set_gemm_next_pf(atoi(np));
         if (const char* mp = getenv("TKV_GEMM_NSMP")) set_gemm_nsmp(atoi(mp));
         if (const char* gc = getenv("TKV_GEMM_CLUSTER")) set_gemm_cluster(atoi(gc));
-        if (const char* fm = getenv("TKV_FUSED_MLP")) e->fused_mlp = atoi(fm);
-        if (const char* la = getenv("TKV_MK_L2_AHEAD")) e->mk_l2_ahead = atoi(la);
-        if (const char* mt = getenv("TKV_MK_TRACE")) e->mk_trace_layer = atoi(mt);
-        if (const char* kr = getenv("TKV_MK_KROT")) e->mk_krot = atoi(kr);
-        if (const char* nd = getenv("TKV_MK_NODEP")) e->mk_nodep = atoi(nd);
         if (const char* bs = getenv("TKV_BATCH_ATTN_SPLITS")) e->batch_attn_splits = std::min(32, std::max(0, atoi(bs)));
         if (const char* se = getenv("TKV_GEMM_SKIP_EPI")) set_gemm_skip_epi(atoi(se));
         if (const char* ra = getenv("TKV_GEMM_RASTER")) set_gemm_raster(atoi(ra));
@@ -1784,7 +1585,7 @@ void load_tkvw(tkv_engine* e, WeightsFile& wf) {
     tensor(true, V, H, "embedding", [&](const double* src, int64_t e0, int64_t n) {
         launch_store_f32_from_f64(e->emb + e0, src, n, e->stream);
     });
-    const int rb = e->gu_interleaved ? 64 : 0;
+    const int rb = e->gu_block;
     for (int64_t l = 0; l < e->L; ++l) {
         uint8_t* qkv = static_cast<uint8_t*>(e->w_qkv[l]);
         uint8_t* gu = static_cast<uint8_t*>(e->w_gu[l]);
@@ -1795,7 +1596,7 @@ void load_tkvw(tkv_engine* e, WeightsFile& wf) {
         mat(qkv + (size_t)(qd + kvd) * H * es, H, kvd, "wv");
         mat(e->w_o[l], qd, H, "wo");
         mat(gu, H, I, "w_gate", rb, 0);
-        mat(rb ? gu : gu + (size_t)I * H * es, H, I, "w_up", rb, rb ? 64 : 0);
+        mat(rb ? gu : gu + (size_t)I * H * es, H, I, "w_up", rb, rb);
         mat(e->w_down[l], I, H, "w_down");
     }
     vec(e->norms + (size_t)2 * e->L * H, "final_norm");
@@ -2462,17 +2263,6 @@ tkv_status tkv_debug_weights_checksum(const tkv_model_config* cfg, uint64_t seed
     });
 }
 
-tkv_status tkv_debug_mk_trace(tkv_engine* e, uint64_t* out, int64_t capacity) {
-    return guard([&] {
-        need(e, "engine");
-        need(out, "out");
-        e->bind();
-        e->sync();
-        if (!e->mk_trace.p) fail(TKV_ERR_NOT_FOUND, "no layer-kernel trace recorded (TUNING build, TKV_MK_TRACE)");
-        TKV_CUDA(cudaMemcpy(out, e->mk_trace.p, (size_t)std::min<int64_t>(capacity, 4096 * 32) * 8, cudaMemcpyDeviceToHost));
-    });
-}
-
 tkv_status tkv_debug_weight_rows(tkv_engine* e, int64_t layer, int which, int64_t row0, int64_t nrows, float* out) {
     return guard([&] {
         need(e, "engine");
@@ -3097,7 +2887,7 @@ tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int
         auto run = [&] {
             if (swiglu)
                 launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, nullptr, 1, st, act.p, ssp.as<float>(), nb,
-                               1e-6f);
+                               1e-6f, N % 256 == 0 ? 128 : 64);
             else
                 launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, part.as<float>(), splits, st);
         };

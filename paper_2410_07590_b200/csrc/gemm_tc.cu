@@ -204,7 +204,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
 __device__ __forceinline__ float silu(float z) { return z / (1.0f + __expf(-z)); }
+// silu with the approximate divide (z -> -inf: 1 + e^-z overflows to inf and __fdividef returns 0, the limit)
+__device__ __forceinline__ float silu_fast(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
 
 struct GemmArgs {
     int M, N, K;
@@ -214,6 +223,10 @@ struct GemmArgs {
     int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128 * mp
     int mp;                       // normal: 128-row activation sub-tiles per unit (each its own MMA + accumulator)
     int nbuf;                     // TMEM accumulator buffers (2: epilogue overlaps the next unit's mainloop)
+    int gub;                      // EPI_SWIGLU: W_gu rows interleaved in blocks of gub gate rows + gub up rows. 128
+                                  // (np = 2): weight tile 0 of a unit = gate rows, tile 1 = the matching up rows, so a
+                                  // TMEM lane (swapped: weight row) holds its gate AND up accumulators; 64: one 128-row
+                                  // tile holds 64 gate + 64 up rows (the swapped epilogue exchanges them through smem)
     int skip_epi;                 // debug timing knob: normal-tiling partial epilogue skipped (results invalid)
     int cl;                       // normal tiling: CTAs per cluster (2: the pair computes m-tiles 2i and 2i+1 of
                                   // one n-tile; rank 0 multicasts the weight tile to both; m_tiles counts pairs)
@@ -439,6 +452,12 @@ __global__ void __launch_bounds__(THREADS_P)
         const int lg = warp & 3;
         const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
         const int et = threadIdx.x - 64;  // 0..127
+        if (SWAP && EPI == EPI_SWIGLU && g.gub == 128) {
+            // folded mlp_norm scale of every token (swapped tiling: all units cover tokens [0, ntok)), once per CTA
+            float* ts = reinterpret_cast<float*>(smem + g.scratch_off);
+            if (et < g.ntok) ts[et] = et < g.M ? row_scale(g.ssp, g.nb, et, g.K, g.eps) : 0.f;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         int lu = 0;
         for (int u = u0; u < g.units; u += ustep, ++lu) {
             int nt, mt, z;
@@ -467,6 +486,52 @@ __global__ void __launch_bounds__(THREADS_P)
                                 const int m = m0 + c + j;
                                 if (m < g.M) out[(int64_t)m * g.N + n] = __uint_as_float(r[j]);
                             }
+                        }
+                    }
+                } else if (g.gub == 128) {
+                    // gate tile (p = 0) and up tile (p = 1) of intermediate rows [nt * 128, nt * 128 + 128): this lane's
+                    // row i has its gate accumulators at acc, its up accumulators ntok columns further. The chunk's
+                    // token scales are read (ld.shared) before any of its stores: a generic load behind a global store
+                    // is ordered after it, which serialised every element on the store (~200 cycles each).
+                    if (p == 0) {
+                        const uint32_t ts = smem_u32(smem + g.scratch_off);
+                        const int inter = g.N / 2;
+                        const int i = nt * 128 + lg * 32 + lane;
+#pragma unroll 1
+                        for (int c = 0; c < g.ntok; c += 16) {
+                            uint32_t gr[16], ur[16];
+                            tmem_ld16_nowait(acc + (uint32_t)c, gr);
+                            tmem_ld16_nowait(acc + (uint32_t)(g.ntok + c), ur);
+                            float sc[16];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                             : "=f"(sc[4 * q]), "=f"(sc[4 * q + 1]), "=f"(sc[4 * q + 2]), "=f"(sc[4 * q + 3])
+                                             : "r"(ts + (uint32_t)(c + 4 * q) * 4));
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                            // transpose the warp's [32 rows][16 tokens] through its 1 KB smem block, then store
+                            // whole 16-byte pieces of token rows (2 per lane) instead of 16 scattered 2-byte stores
+                            const uint32_t xs = ts + 1024u + (uint32_t)lg * 1024u;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const __nv_bfloat16 o = __float2bfloat16_rn(
+                                    silu_fast(sc[j] * __uint_as_float(gr[j])) * (sc[j] * __uint_as_float(ur[j])));
+                                asm volatile("st.shared.b16 [%0], %1;" ::"r"(xs + (uint32_t)(j * 64 + lane * 2)),
+                                             "h"(__bfloat16_as_ushort(o)) : "memory");
+                            }
+                            __syncwarp();
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int ch = lane + 32 * h, tk = ch >> 2, part = ch & 3;
+                                uint4 v;
+                                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                             : "r"(xs + (uint32_t)(tk * 64 + part * 16)) : "memory");
+                                const int m = m0 + c + tk, col = i - lane + part * 8;
+                                if (m < g.M && col < inter)
+                                    *reinterpret_cast<uint4*>(g.act + (int64_t)m * inter + col) = v;
+                            }
+                            __syncwarp();
                         }
                     }
                 } else {
@@ -543,6 +608,34 @@ __global__ void __launch_bounds__(THREADS_P)
                     }
                 } else {
                     const int inter = g.N / 2;
+                    if (g.gub == 128) {
+                        // half p = 0 of the 256-wide unit = gate rows [nt * 128, +128), half 1 = the matching up rows
+                        if (p != 0) continue;
+                        const int i0 = nt * 128;
+                        const float sc = m < g.M ? row_scale(g.ssp, g.nb, m, g.K, g.eps) : 0.f;
+#pragma unroll 1
+                        for (int c = 0; c < 128; c += 16) {
+                            uint32_t gr[16], ur[16];
+                            tmem_ld16_nowait(acc + (uint32_t)c, gr);
+                            tmem_ld16_nowait(acc + (uint32_t)(128 + c), ur);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                            if (m < g.M) {
+                                __align__(16) __nv_bfloat16 o[16];
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    o[j] = __float2bfloat16_rn(silu(sc * __uint_as_float(gr[j])) * (sc * __uint_as_float(ur[j])));
+                                __nv_bfloat16* dst = g.act + (int64_t)m * inter + i0 + c;
+                                if (i0 + c + 16 <= inter && (inter % 8) == 0) {
+                                    reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<uint4*>(o)[0];
+                                    reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<uint4*>(o)[1];
+                                } else {
+                                    for (int j = 0; j < 16; ++j)
+                                        if (i0 + c + j < inter) dst[j] = o[j];
+                                }
+                            }
+                        }
+                        continue;
+                    }
                     const int i0 = (n0 / 128) * 64;
                     const float sc = m < g.M ? row_scale(g.ssp, g.nb, m, g.K, g.eps) : 0.f;  // folded mlp_norm
 #pragma unroll 1
@@ -579,286 +672,6 @@ __global__ void __launch_bounds__(THREADS_P)
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
-    }
-}
-
-// ---------------------------------------------------------------------------------------------------------------
-// Fused MLP for <= 128 tokens (swap-AB): ONE persistent launch runs the gate/up GEMM with its SwiGLU epilogue
-// (phase 1, one 128-row tile of interleaved W_gu per unit, whole K) and then the down GEMM (phase 2, split-K
-// partials). The smem ring and the TMEM accumulators flow from phase 1 into phase 2, so the down weights start
-// streaming while the gate/up tail drains instead of after a kernel boundary. Phase-1 tile t produces act
-// columns [64 t, 64 t + 64) = down k-block t; its epilogue publishes flags[t] = epoch (release, gpu scope) and the
-// phase-2 producer acquires it before that k-block's activation TMA. The epoch lives in device memory (read after
-// griddepcontrol.wait, advanced by the last CTA to finish) so CUDA-graph replays never see a stale match. Every CTA finishes its phase-1 units before
-// its phase-2 units and all CTAs are co-resident (grid <= resident capacity; a dependent grid can only launch
-// once all of this grid's CTAs have started), so the waits cannot deadlock; they trap after ~2 s regardless.
-struct MlpArgs {
-    int M, ntok, stages;
-    uint32_t a_bytes, acc_cols, tmem_cols, scratch_off;
-    int units1, kb1;                    // phase 1: gate/up tiles (= act k-blocks), k-blocks of hidden
-    int n2_tiles, kb2, kb2_per_split, units2, N2;  // phase 2: down
-    __nv_bfloat16* act;                 // [M][inter]
-    float* partial;                     // [splits2][M][N2]
-    const float* ssp;
-    int nb, hidden;
-    float eps;
-    unsigned* flags;
-    unsigned* ctl;  // [0] = this launch's epoch (read after the PDL wait, so graph replays see a fresh one),
-                    // [1] = finished-CTA count; the last CTA to finish advances the epoch
-};
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// every flag of [f, f + n) == epoch: all loads of a poll in flight at once (one round trip per poll, not per flag)
-__device__ __forceinline__ void wait_flags(const unsigned* f, int n, unsigned epoch) {
-    uint64_t t0 = 0;
-    for (uint32_t spin = 0;; ++spin) {
-        bool ok = true;
-        for (int i0 = 0; i0 < n; i0 += 16) {
-            unsigned v[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = i0 + i < n ? ld_acquire_u32(f + i0 + i) : epoch;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) ok &= v[i] == epoch;
-        }
-        if (ok) break;
-        if ((spin & 63) == 63) {
-            uint64_t now;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-            if (t0 == 0) t0 = now;
-            else if (now - t0 > 2000000000ull) __trap();
-        }
-    }
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-__device__ __forceinline__ void wait_flag(const unsigned* f, unsigned epoch) {
-    uint64_t t0 = 0;
-    for (uint32_t spin = 0; ld_acquire_u32(f) != epoch; ++spin) {
-        if ((spin & 255) == 255) {
-            uint64_t now;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-            if (t0 == 0) t0 = now;
-            else if (now - t0 > 2000000000ull) __trap();
-        }
-    }
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA (async proxy) read follows
-}
-
-__global__ void __launch_bounds__(THREADS_P)
-    gemm_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWgu,
-                    const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmWd, MlpArgs m) {
-    pdl_launch();
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t stage_bytes = TILE_W + m.a_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + m.stages * stage_bytes);
-    uint64_t* empty = full + m.stages;
-    uint64_t* tfull = empty + m.stages;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < m.stages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(m.tmem_cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-    // this CTA's work list: phase-1 units b, b + G, ... then phase-2 units b, b + G, ...
-    const int G = gridDim.x, b0 = blockIdx.x;
-    const int n1 = b0 < m.units1 ? (m.units1 - 1 - b0) / G + 1 : 0;
-    const int n2 = b0 < m.units2 ? (m.units2 - 1 - b0) / G + 1 : 0;
-    // unit j of this CTA -> (phase, weight tile, first k-block, k-blocks)
-    auto unit = [&](int j, int& ph, int& nt, int& k0, int& nkb, int& u) {
-        if (j < n1) {
-            ph = 1;
-            u = b0 + j * G;
-            nt = u;
-            k0 = 0;
-            nkb = m.kb1;
-        } else {
-            ph = 2;
-            u = b0 + (j - n1) * G;
-            const int z = u / m.n2_tiles;
-            nt = u - z * m.n2_tiles;
-            k0 = z * m.kb2_per_split;
-            nkb = min(m.kb2, k0 + m.kb2_per_split) - k0;
-        }
-    };
-    auto kblk = [&](int k0, int nkb, int i, int u) { return k0 + (i + (u * 37) % nkb) % nkb; };
-
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer ----------------
-            const uint64_t wpol = policy_evict_first();
-            int it = 0;
-            bool waited = false;
-            unsigned epoch = 0;
-            for (int j = 0; j < n1 + n2; ++j) {
-                int ph, nt, k0, nkb, u;
-                unit(j, ph, nt, k0, nkb, u);
-                const CUtensorMap* tw = ph == 1 ? &tmWgu : &tmWd;
-                const CUtensorMap* ta = ph == 1 ? &tmX : &tmAct;
-                // weights of up to `stages` k-blocks go out before their activations: before the PDL wait in
-                // phase 1, before the readiness flags in phase 2
-                int i = 0;
-                while (i < nkb) {
-                    // batched (weights first) only for the first ring of each phase; interleaved afterwards
-                    const bool lead = i == 0 && (j == 0 || j == n1);
-                    const int batch = lead ? min(nkb - i, m.stages) : 1;
-                    for (int q = 0; q < batch; ++q) {
-                        const int s = (it + q) % m.stages;
-                        mbar_wait(&empty[s], ((uint32_t)((it + q) / m.stages) & 1u) ^ 1u);
-                        mbar_expect_tx(&full[s], stage_bytes);
-                        tma_load_2d_hint(smem + s * stage_bytes, tw, &full[s], kblk(k0, nkb, i + q, u) * BK, nt * 128, wpol);
-                    }
-                    if (!waited) {
-                        pdl_wait();
-                        epoch = *(volatile unsigned*)m.ctl;
-                        waited = true;
-                    }
-                    if (ph == 2 && i == 0) wait_flags(m.flags + k0, nkb, epoch);  // the unit's whole act k-range
-                    for (int q = 0; q < batch; ++q) {
-                        const int s = (it + q) % m.stages;
-                        const int kb = kblk(k0, nkb, i + q, u);
-                        tma_load_2d(smem + s * stage_bytes + TILE_W, ta, &full[s], kb * BK, 0);
-                    }
-                    it += batch;
-                    i += batch;
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer ----------------
-            const uint32_t id = idesc(128, m.ntok);
-            int it = 0;
-            for (int j = 0; j < n1 + n2; ++j) {
-                int ph, nt, k0, nkb, u;
-                unit(j, ph, nt, k0, nkb, u);
-                const int b = j & 1;
-                mbar_wait(&tempty[b], ((uint32_t)(j >> 1) & 1u) ^ 1u);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t acc = tmem + (uint32_t)b * m.acc_cols;
-                for (int i = 0; i < nkb; ++i, ++it) {
-                    const int s = it % m.stages;
-                    mbar_wait(&full[s], (uint32_t)(it / m.stages) & 1u);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t w = smem_u32(smem + s * stage_bytes), a = w + TILE_W;
-#pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        umma_f16(acc, desc_k(w + k * 32), desc_k(a + k * 32), id, (i | k) != 0);
-                    umma_commit(&empty[s]);
-                }
-                umma_commit(&tfull[b]);
-            }
-        }
-    } else {
-        // ---------------- epilogue warps 2-5: TMEM lane group = warp % 4 ----------------
-        pdl_wait();
-        const unsigned epoch = *(volatile unsigned*)m.ctl;
-        const int lg = warp & 3;
-        const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
-        const int et = threadIdx.x - 64;
-        const int inter = m.kb2 * BK;
-        float* up = reinterpret_cast<float*>(smem + m.scratch_off);  // [64][XC + 1]
-        const int ld = XC + 1;
-        float* tok_scale = up + 64 * ld;
-        for (int j = 0; j < n1 + n2; ++j) {
-            int ph, nt, k0, nkb, u;
-            unit(j, ph, nt, k0, nkb, u);
-            const int b = j & 1;
-            mbar_wait(&tfull[b], (uint32_t)(j >> 1) & 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t acc = tmem + lane_base + (uint32_t)b * m.acc_cols;
-            if (ph == 1) {  // SwiGLU: tile rows 0-63 gate, 64-127 the matching up rows (interleaved W_gu)
-                if (et < m.ntok) tok_scale[et] = et < m.M ? row_scale(m.ssp, m.nb, et, m.hidden, m.eps) : 0.f;
-                const int i = nt * 64 + lg * 32 + lane;
-                for (int c0 = 0; c0 < m.ntok; c0 += XC) {
-                    const int c1 = min(m.ntok, c0 + XC);
-                    if (lg >= 2) {
-#pragma unroll 1
-                        for (int c = c0; c < c1; c += 16) {
-                            uint32_t r[16];
-                            tmem_ld16(acc + (uint32_t)c, r);
-#pragma unroll
-                            for (int q = 0; q < 16; ++q) up[((lg - 2) * 32 + lane) * ld + c - c0 + q] = __uint_as_float(r[q]);
-                        }
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (lg < 2) {
-#pragma unroll 1
-                        for (int c = c0; c < c1; c += 16) {
-                            uint32_t r[16];
-                            tmem_ld16(acc + (uint32_t)c, r);
-#pragma unroll
-                            for (int q = 0; q < 16; ++q) {
-                                const int t = c + q;
-                                if (t < m.M && i < inter) {
-                                    const float sc = tok_scale[t];
-                                    m.act[(int64_t)t * inter + i] = __float2bfloat16_rn(
-                                        silu(sc * __uint_as_float(r[q])) * (sc * up[(lg * 32 + lane) * ld + t - c0]));
-                                }
-                            }
-                        }
-                        asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by TMA (async proxy)
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");  // scratch reusable; after the last pass: act written
-                }
-                if (et == 0) {
-                    __threadfence();
-                    st_release_u32(m.flags + nt, epoch);
-                }
-            } else {  // down: split-K partial plane z, TMEM lane = weight row n, column = token
-                const int z = u / m.n2_tiles;
-                const int n = nt * 128 + lg * 32 + lane;
-                float* out = m.partial + (int64_t)z * m.M * m.N2;
-#pragma unroll 1
-                for (int c = 0; c < m.ntok; c += 16) {
-                    uint32_t r[16];
-                    tmem_ld16(acc + (uint32_t)c, r);
-                    if (n < m.N2) {
-#pragma unroll
-                        for (int q = 0; q < 16; ++q)
-                            if (c + q < m.M) out[(int64_t)(c + q) * m.N2 + n] = __uint_as_float(r[q]);
-                    }
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {  // every CTA has read the epoch by now; the last one advances it for the next launch
-        __threadfence();
-        if (atomicAdd(m.ctl + 1, 1u) == gridDim.x - 1) {
-            m.ctl[1] = 0;
-            atomicAdd(m.ctl, 1u);
-            __threadfence();
-        }
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(m.tmem_cols));
     }
 }
 
@@ -946,16 +759,22 @@ int gemm_tc_tiles(int M, int N) {
 }
 
 int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
-                   cudaStream_t s, void* swiglu_act, const float* ssp, int nb, float eps) {
+                   cudaStream_t s, void* swiglu_act, const float* ssp, int nb, float eps, int gu_block) {
     const bool swap = M <= 128;
+    // W_gu in 128-row gate / up blocks: a unit = one gate tile + its up tile (np = 2); swapped, one CTA per SM with a
+    // 5-deep ring of 40 KB stages (the two weight tiles share each activation tile)
+    const bool gu128 = swiglu_act && gu_block == 128;
+    if (swiglu_act && gu_block != 128 && gu_block != 64) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs 64- or 128-row gate/up blocks");
     GemmArgs g{};
+    g.gub = gu_block;
     g.M = M;
     g.N = N;
     g.K = K;
     g.kb_total = (K + BK - 1) / BK;
     g.kb_per_split = (g.kb_total + splits - 1) / splits;
     const int eff_splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;  // every unit non-empty
-    g.np = np_for(M, N);
+    g.np = gu128 ? 2 : np_for(M, N);
+    if (gu128 && N % 256) fail(TKV_ERR_CONFIG, "128-row gate/up blocks need N % 256 == 0");
     g.mp = mp_for(M);
     g.n_tiles = (N + 128 * g.np - 1) / (128 * g.np);
     g.m_tiles = swap ? 1 : (M + 128 * g.mp - 1) / (128 * g.mp);
@@ -977,9 +796,13 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     }
     g.tmem_cols = 32;
     while (g.tmem_cols < (uint32_t)g.nbuf * g.acc_cols) g.tmem_cols <<= 1;
-    const uint32_t scratch =
-        (swap && swiglu_act) ? (uint32_t)((64 * (XC + 1) + g.ntok) * 4 + 1023) / 1024 * 1024 : 0;
-    const int budget = swap ? (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET) : g_knobs.ns_smem_kb * 1024;
+    const uint32_t scratch = !(swap && swiglu_act) ? 0
+                             : gu128 ? 1024u + 4096u  // token scales + the four warps' transpose blocks
+                                     : (uint32_t)((64 * (XC + 1) + g.ntok) * 4 + 1023) / 1024 * 1024;
+    const int cps = (swap && gu128) ? 1 : gemm_tc_ctas_per_sm(M);
+    const int budget = (swap && gu128) ? 208 * 1024
+                       : swap          ? (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET)
+                                       : g_knobs.ns_smem_kb * 1024;
     g.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
                                        (uint32_t)(budget - (int)scratch) / (g.np * TILE_W + g.a_bytes));
     if (g.stages < 2) fail(TKV_ERR_CONFIG, "GEMM smem budget too small");
@@ -997,7 +820,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int grid = std::min(g.units, sms * gemm_tc_ctas_per_sm(M) / g.cl) * g.cl;  // cluster mode: whole pairs
+    int grid = std::min(g.units, sms * cps / g.cl) * g.cl;  // cluster mode: whole pairs
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
     const CUtensorMap tw = make_map(W, N, K, K, 128 * g.np);
     CUtensorMap tn = tw;
@@ -1022,64 +845,6 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
 }
 
 
-int launch_gemm_mlp(const void* xb, int lda, const void* w_gu, void* act, const void* w_down, int M, int hidden,
-                    int inter, float* partial, int splits, unsigned* flags, unsigned* ctl, const float* ssp, int nb,
-                    float eps, cudaStream_t s) {
-    if (M > 128) fail(TKV_ERR_CONFIG, "fused MLP: <= 128 tokens only");
-    if (hidden % BK || inter % BK || (2 * inter) % 128) fail(TKV_ERR_CONFIG, "fused MLP: unsupported dims");
-    MlpArgs m{};
-    m.M = M;
-    m.ntok = ((M + 15) / 16) * 16;
-    m.a_bytes = (uint32_t)m.ntok * BK * 2;
-    m.acc_cols = (uint32_t)m.ntok;
-    m.tmem_cols = 32;
-    while (m.tmem_cols < 2 * m.acc_cols) m.tmem_cols <<= 1;
-    const uint32_t scratch = (uint32_t)((64 * (XC + 1) + m.ntok) * 4 + 1023) / 1024 * 1024;
-    const int budget = g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET;
-    m.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
-                                       (uint32_t)(budget - (int)scratch) / (TILE_W + m.a_bytes));
-    if (m.stages < 2) fail(TKV_ERR_CONFIG, "fused MLP: smem budget too small");
-    m.scratch_off = ((uint32_t)m.stages * (TILE_W + m.a_bytes) + 256 + 1023) / 1024 * 1024;
-    m.units1 = 2 * inter / 128;
-    m.kb1 = hidden / BK;
-    m.n2_tiles = (hidden + 127) / 128;
-    m.kb2 = inter / BK;
-    m.kb2_per_split = (m.kb2 + splits - 1) / splits;
-    const int eff = (m.kb2 + m.kb2_per_split - 1) / m.kb2_per_split;
-    m.units2 = m.n2_tiles * eff;
-    m.N2 = hidden;
-    m.act = (__nv_bfloat16*)act;
-    m.partial = partial;
-    m.ssp = ssp;
-    m.nb = nb;
-    m.hidden = hidden;
-    m.eps = eps;
-    m.flags = flags;
-    m.ctl = ctl;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int cap = sms * gemm_tc_ctas_per_sm(M);  // co-resident CTAs: every phase-2 flag owner is running
-    const int grid = std::min(std::max(m.units1, m.units2), cap);
-    const size_t smem = 1024 + (size_t)m.scratch_off + scratch;
-    TKV_CUDA(cudaFuncSetAttribute(gemm_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    TKV_CUDA(cudaFuncSetAttribute(gemm_mlp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    // co-residency from the SM's shared-memory capacity (1 KB reserved per CTA; threads and registers are far
-    // from their limits at 192 threads x <= 64 registers). cudaOccupancyMaxActiveBlocksPerMultiprocessor reports
-    // 1 here for this and the plain GEMM kernel alike, while ncu shows 2 resident, so it is not used.
-    int smem_sm = 0;
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    const int per_sm = smem_sm / (int)(smem + 1024);
-    if ((int64_t)per_sm * sms < grid)
-        fail(TKV_ERR_CONFIG, "fused MLP: grid of " + std::to_string(grid) + " would not be co-resident");
-    const CUtensorMap tx = make_map(xb, M, hidden, lda, m.ntok);
-    const CUtensorMap twg = make_map(w_gu, 2 * inter, hidden, hidden, 128);
-    const CUtensorMap ta = make_map(act, M, inter, inter, m.ntok);
-    const CUtensorMap twd = make_map(w_down, hidden, inter, inter, 128);
-    launch_k(gemm_mlp_kernel, dim3(grid), dim3(THREADS_P), smem, s, tx, twg, ta, twd, m);
-    TKV_CUDA(cudaGetLastError());
-    return eff;
-}
 
 void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap) {
     static unsigned long long* buf = nullptr;

@@ -193,14 +193,14 @@ __global__ void __launch_bounds__(256) residual_kernel(float* x, const float* pa
 
 template <typename T>
 __global__ void swiglu_kernel(const float* partial, int splits, int T_, int inter, T* act, const float* ssp, int nb,
-                              int hidden, float eps, int interleave64) {
+                              int hidden, float eps, int gub) {
     pdl_launch();
     pdl_wait();
     const int64_t n = (int64_t)T_ * inter, plane = (int64_t)T_ * 2 * inter;
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = o / inter, i = o - t * inter;
-        const int64_t gc = interleave64 ? (i >> 6) * 128 + (i & 63) : i;
-        const int64_t uc = interleave64 ? gc + 64 : inter + i;
+        const int64_t gc = gub ? (i / gub) * 2 * gub + i % gub : i;
+        const int64_t uc = gub ? gc + gub : inter + i;
         float g = sum_splits(partial + t * 2 * inter + gc, splits, plane, 0.f);
         float u = sum_splits(partial + t * 2 * inter + uc, splits, plane, 0.f);
         const float sc = row_scale(ssp, nb, t, hidden, eps);
@@ -556,8 +556,8 @@ void launch_residual(float* x, const float* partial, int splits, int T_, int hid
 }
 
 void launch_swiglu(const float* partial, int splits, int T_, int inter, void* act, const float* ssp, int nb,
-                   int hidden, float eps, DT dt, cudaStream_t s, bool interleave64) {
-    DISPATCH_DT(dt, launch_k(swiglu_kernel<T>, grid_for((int64_t)T_ * inter, 256), 256, 0, s, partial, splits, T_, inter, (T*)act, ssp, nb, hidden, eps, (int)interleave64));
+                   int hidden, float eps, DT dt, cudaStream_t s, int gu_block) {
+    DISPATCH_DT(dt, launch_k(swiglu_kernel<T>, grid_for((int64_t)T_ * inter, 256), 256, 0, s, partial, splits, T_, inter, (T*)act, ssp, nb, hidden, eps, gu_block));
     TKV_CUDA(cudaGetLastError());
 }
 

@@ -57,9 +57,9 @@ void launch_embed(const int32_t* tok, int T, const float* emb, int hidden, int v
 void launch_residual(float* x, const float* partial, int splits, int T, int hidden, const float* w, void* xb,
                      float* ssp, DT dt, int* err, cudaStream_t s);
 // act[t][i] = silu(s_t * sum_s P[s][t][gate(i)]) * (s_t * sum_s P[s][t][up(i)]), s_t = row_scale(ssp, t)
-// (dtype). interleave64: gate/up columns in 64-wide blocks (gate(i) = (i/64)*128 + i%64, up = gate + 64).
+// (dtype). gu_block B > 0: gate/up columns in B-wide blocks (gate(i) = (i/B)*2B + i%B, up = gate + B).
 void launch_swiglu(const float* partial, int splits, int T, int inter, void* act, const float* ssp, int nb,
-                   int hidden, float eps, DT dt, cudaStream_t s, bool interleave64 = false);
+                   int hidden, float eps, DT dt, cudaStream_t s, int gu_block = 0);
 
 // QKV epilogue: reduce the split-K partials of [T, (H+2Hkv)*d], rotate q and k by pos[t]
 // (interleaved pairs, cos/sin table [max_pos][d/2] of float2), write q (dtype [T, H*d]),
@@ -129,12 +129,6 @@ void set_gemm_next(const void* W, int M, int N, int K, int splits);
 void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap);  // debug: CTA 0 per-stage clock64 trace
 void set_gemm_next_pf(int kblocks);
 void set_gemm_nsmp(int mp);
-// Fused MLP (<= 128 tokens): gate/up GEMM + SwiGLU epilogue into act, then the down GEMM's split-K partials, in one
-// persistent launch; flags[2 * inter / 128] readiness words and ctl[2] = {epoch, finished CTAs}, both zeroed
-// once with ctl[0] = 1 before the first launch. Returns the down GEMM's split count.
-int launch_gemm_mlp(const void* xb, int lda, const void* w_gu, void* act, const void* w_down, int M, int hidden,
-                    int inter, float* partial, int splits, unsigned* flags, unsigned* ctl, const float* ssp, int nb,
-                    float eps, cudaStream_t s);
 void set_gemm_cluster(int c);
 void set_gemm_skip_epi(int v);  // timing experiments only: skip the normal-tiling partial stores  // normal tiling: 2 = CTA pairs share each weight tile through TMA multicast
 // normal tiling unit order (0 n-fastest, 1 m-fastest when N > M, 2 m-fastest; group_mb > 0: m-tile groups of
@@ -148,7 +142,7 @@ int gemm_tc_ctas_per_sm(int M);  // resident GEMM CTAs per SM the launcher plans
 // The SwiGLU epilogue applies the folded RMSNorm scale row_scale(ssp, token) (ssp/nb/eps: see launch_residual).
 int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, float* partial, int splits,
                    cudaStream_t s, void* swiglu_act = nullptr, const float* ssp = nullptr, int nb = 0,
-                   float eps = 0.f);
+                   float eps = 0.f, int gu_block = 64);
 
 // Flash attention, SIMT (fp32 math): q [Tq][H*d], k/v rows [Tk][Hkv*d] (stride kv_stride elements),
 // row t attends keys j with lo[t] <= j <= hi[t]. out [Tq][H*d] (dtype). ws: split-K workspace.
@@ -198,55 +192,6 @@ size_t index_topk_scratch_bytes(int64_t n, int k);
 int64_t launch_index_top_k(const double* emb, const double* nb, const uint64_t* ids, int64_t n, int64_t cap,
                            const double* q, double na, int k, void* scratch, uint64_t* ids_out, double* scores_out,
                            cudaStream_t s);
-// Persistent layer kernel (mk.cu) for <= 128-token bf16 forwards: a list of phases -- GEMM (swap-AB tcgen05, fp32
-// split-K partials or the fused SwiGLU epilogue), RESIDUAL (x += sum of a GEMM's partials; xb, ssp) and QKV_EPI
-// (split-K reduce + RoPE + q / request-cache rows) -- run by one CTA per SM; phase p waits for phase p-1 through
-// the global counter bar[ph[p-1].slot] reaching ph[p-1].target (every CTA adds 1 per launch).
-constexpr int MK_MAX_PHASES = 7, MK_MAX_MAPS = 8;
-enum { MK_GEMM = 0, MK_RESIDUAL = 1, MK_QKV_EPI = 2 };
-struct MkGemm {
-    int map_w, map_a;  // tensor maps: weights [N][K], activations [M][K]
-    int N, K, kb_total, kb_per_split, n_tiles, units, swiglu;
-    float* partial;    // !swiglu: [splits][M][N]
-    void* act;         // swiglu: [M][N / 2] bf16
-};
-struct MkPhase {
-    int kind, slot;
-    unsigned target;
-    MkGemm g;
-    const float* rpartial;  // RESIDUAL: the partial planes to add ([splits][M][hidden])
-    int rsplits;
-    const float* rw;        // RESIDUAL: the next RMSNorm's weight (xb = x * rw)
-};
-struct MkArgs {
-    int M, ntok, stages, n_phases, n_maps;
-    int l2_ahead;  // weight tiles the producer pulls into L2 beyond the smem ring
-    int nodep;     // timing experiments only: no phase waits, no element-wise work (results invalid)
-    int krot;      // rotate each unit's k-block order by (u * 37) % nkb (spreads the shared activation-tile reads)
-    unsigned long long* trace;  // debug timeline (nullptr = off): [cta][32] globaltimer stamps
-    uint32_t a_bytes, tmem_cols, scratch_off;
-    MkPhase ph[MK_MAX_PHASES];
-    unsigned* bar;
-    float* x;       // residual stream rows [M][hidden]
-    void* xb;       // bf16 [M][hidden]
-    float* ssp;     // [M][nb]
-    int hidden, nb;
-    float eps;
-    int* err;
-    const float* qpartial;  // QKV_EPI: [qsplits][M][(H + 2 Hkv) d]
-    int qsplits, H, Hkv, d;
-    const int32_t* pos;
-    const float2* rope;
-    void *q, *kc, *vc;  // bf16: q [M][H d], cache rows [row0, row0 + M) of the layer's K and V planes
-    int row0;
-};
-struct MkMapSpec {
-    const void* base;
-    int rows, cols, ld, box_rows;
-};
-bool mk_supported(int M, int hidden, int inter, int qd, int kvd);
-int mk_grid(int device);
-void launch_mk(MkArgs a, const MkMapSpec* specs, int n_maps, cudaStream_t s);
 
 // Reference-exact weights_checksum on the device (fingerprint.cu): FNV-1a 64 over a stream of 8-byte words given
 // as segments -- kind 0 literal / 1 constant: the word `a` repeated n times; kind 2: the draws

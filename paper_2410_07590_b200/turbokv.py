@@ -72,7 +72,6 @@ FLAG_SIMT_ATTN = 0x2
 FLAG_NO_PDL = 0x8
 FLAG_BATCH_ATTN = 0x20
 FLAG_DECODE_ATTN = 0x40
-FLAG_LAYER_KERNEL = 0x80
 
 DOC_START, DOC_END, EOS, VOCAB = 256, 257, 258, 259  # tokenizer.hpp:19-22
 
@@ -119,7 +118,6 @@ def lib():
         L.tkv_weights_identity.argtypes = [C.POINTER(_Cfg), C.c_uint64, U64P, U64P]
         L.tkv_debug_weights_checksum.argtypes = [C.POINTER(_Cfg), C.c_uint64, C.c_int, U64P, U64P]
         L.tkv_engine_check.argtypes = [C.c_void_p]
-        L.tkv_debug_mk_trace.argtypes = [C.c_void_p, U64P, C.c_int64]
         L.tkv_debug_weight_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int64, F32P]
         L.tkv_chunk_content_id.restype = C.c_uint64
         L.tkv_chunk_content_id.argtypes = [C.c_uint64, I32P, C.c_int64]

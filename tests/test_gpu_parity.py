@@ -707,35 +707,6 @@ def test_large_m_gemm_tilings_agree(tmp_path, env):
     assert_close(outs[1], outs[0], BF16_TOL)
 
 
-def test_fused_mlp_matches_two_launch_mlp(tmp_path):
-    """TKV_FUSED_MLP=1 (gate/up + SwiGLU + down in one persistent launch, flag hand-over) gives the two-launch
-    path's query-prefill logits and greedy tokens (exact Qwen dims, 2 layers; fresh processes: the switch is
-    read at engine creation)."""
-    import subprocess
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    script = tmp_path / "run.py"
-    script.write_text(r"""
-import sys, numpy as np
-sys.path.insert(0, %r)
-import oracle as O
-from paper_2410_07590_b200 import turbokv as T
-eng = T.Engine(T.ModelConfig(**vars(O.qwen_layers(2))), 7, dtype="bf16", store_capacity_tokens=1 << 16)
-ids = eng.ingest_chunks([O.random_text_tokens(900 + i, 254) for i in range(4)])
-with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
-    out = eng.prefill_query(ctx, O.random_text_tokens(901, 64))[0]
-    toks = eng.greedy_decode(ctx, 4)
-np.save(sys.argv[1], np.concatenate([out, np.asarray(toks, np.float32)]))
-""" % root)
-    outs = []
-    for e in ({"TKV_FUSED_MLP": "0"}, {"TKV_FUSED_MLP": "1"}):
-        path = tmp_path / f"o{len(outs)}.npy"
-        subprocess.run([sys.executable, str(script), str(path)], check=True, env={**os.environ, **e}, timeout=300)
-        outs.append(np.load(path))
-    v = 259
-    assert_close(outs[1][:v], outs[0][:v], BF16_TOL)
-    assert np.array_equal(outs[1][v:], outs[0][v:])
-
-
 def test_batched_attention_split_k_matches(golden, tmp_path):
     """TKV_BATCH_ATTN_SPLITS=3: the batched single-launch attention with split-K partials and the request-aware
     combine gives the unsplit batched logits (bf16 tolerance); fresh processes (the knob is read at creation)."""

@@ -40,5 +40,5 @@ for r in range(8, 12):
 u = u[u[:, 0] > 0] - t0
 print("  epilogue per unit (start, end):", [tuple(int(x) for x in r) for r in u[:8]])
 ep = buf[3072 + 384:].astype(np.int64)
-print("  swiglu epilogue unit 0, gate warp:", [int(x - t0) if x else 0 for x in ep[:9]], " up warp:", [int(x - t0) if x else 0 for x in ep[16:25]])
+print("  epilogue unit 0 stamps:", [int(x - t0) if x else 0 for x in ep[:24]])
 print(f"  last stage full at {int(full[-1])} cyc")
