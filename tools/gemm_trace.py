@@ -27,18 +27,20 @@ full = rel[:, 1]
 print(f"M={M} N={N} K={K} splits={sp} swiglu={sw} stages={st} smem={smk} cps={cps}: {ms.value*1e3:.2f} us/launch, CTA0 {n} stages")
 d = np.diff(full)
 print(f"  MMA-saw-full interval: median {np.median(d):.0f} cyc, mean {d.mean():.0f}, p90 {np.percentile(d, 90):.0f}")
-print(f"  MMA issue cost (commit - full): median {np.median(rel[:, 2] - rel[:, 1]):.0f} cyc")
+if (st3[:, 2] > 0).all():
+    print(f"  MMA issue cost (commit - full): median {np.median(rel[:, 2] - rel[:, 1]):.0f} cyc")
 iss = rel[:, 0]
 valid = iss > 0
 lat = (full - iss)[valid]
-print(f"  producer issue -> full (load latency incl. queueing): median {np.median(lat):.0f} cyc, min {lat.min()}, max {lat.max()}")
-print("  first 12 stages (issue, full, commit):", [tuple(int(x) for x in r) for r in rel[:12]])
+if len(lat):
+    print(f"  producer issue -> full (load latency incl. queueing): median {np.median(lat):.0f} cyc, min {lat.min()}, max {lat.max()}")
+print("  MMA saw stages full at:", [int(x) for x in full[:16]])
 u = buf[3072:3072 + 128].reshape(64, 2).astype(np.int64)
 mm = buf[3200:3456].reshape(64, 4).astype(np.int64)
-for r in range(8, 12):
+for r in range(min(8, n), min(12, n)):
     print(f'  stage {r}: full {int(rel[r, 1])} mma-issued', [int(x - t0) for x in mm[r]], 'commit', int(rel[r, 2]))
 u = u[u[:, 0] > 0] - t0
 print("  epilogue per unit (start, end):", [tuple(int(x) for x in r) for r in u[:8]])
 ep = buf[3072 + 384:].astype(np.int64)
-print("  epilogue unit 0 stamps:", [int(x - t0) if x else 0 for x in ep[:24]])
+print("  epilogue stamps:", [int(x - t0) if x else 0 for x in ep[:24]])
 print(f"  last stage full at {int(full[-1])} cyc")
