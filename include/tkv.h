@@ -89,7 +89,6 @@ typedef struct {
 #define TKV_FLAG_BATCH_ATTN 0x20   /* batched prefill: one attention launch even when the batch cannot fill the GPU */
 #define TKV_FLAG_LAYER_KERNEL 0x80 /* reserved (the persistent layer-kernel experiment was measured slower and removed) */
 #define TKV_FLAG_DECODE_ATTN 0x40 /* bf16: decode-sized (<= 16 rows / kv head) forwards use the split-K mma.sync kernel */
-#define TKV_FLAG_SPLITK_PARTIALS 0x100 /* bf16 <= 128-token projections: split-K partial planes + epilogue kernels instead of the cluster-reduced GEMM with the epilogue fused (debug/compare) */
 
 /* IngestStats (pipeline.hpp:35-39) */
 typedef struct {

@@ -557,26 +557,6 @@ struct tkv_engine {
         return s;
     }
 
-    // <= 128-token bf16 projections: cluster split-K GEMM with the consumer epilogue fused (TKV_FLAG_SPLITK_PARTIALS
-    // selects the split-K partial planes + epilogue kernels instead)
-    bool csk_ok(int M) const {
-        return use_tc() && M <= 128 && !(opts.flags & TKV_FLAG_SPLITK_PARTIALS) && skip_mask == 0;
-    }
-    // x_rows += A . W^T; xb = x * norm_w; ssp -- in one launch when csk_ok (returns false: caller runs the chain)
-    bool proj_residual(const void* A, int lda, const void* W, int M, float* x_rows, const float* norm_w) {
-        if (!csk_ok(M)) return false;
-        CskEpilogue ce;
-        ce.kind = 0;
-        ce.x = x_rows;
-        ce.xb = xb.p;
-        ce.w = norm_w;
-        ce.ssp = ssp.as<float>();
-        ce.nb = norm_blocks((int)hid);
-        ce.err = err.as<int>();
-        Scope sc(this, PC_GEMM, 1);
-        return launch_gemm_csk(A, lda, W, M, (int)hid, lda, ce, stream);
-    }
-
     void* kv_plane(tkv_context* c, int64_t layer, int kv) const;
 
     struct Fwd {
@@ -745,31 +725,8 @@ void tkv_engine::forward(const Fwd& f) {
         const int rows_next = last_rows1 ? 1 : T;
         // --- attention block ---
         if (!(f.kv_only && l == L - 1)) next(w_o[l], rows_next, (int)hid, (int)qd);
-        int s = 0;
-        bool fused_qkv = false;
-        if (!batch && !f.sc.page && csk_ok(T) && !(skip_mask & 4)) {
-            // cluster split-K QKV GEMM with the QKV epilogue (row scale, RoPE, q + cache rows) fused
-            CskEpilogue ce;
-            ce.kind = 1;
-            ce.ssp_in = ssp.as<float>();
-            ce.nb_in = nb;
-            ce.hidden = (int)hid;
-            ce.eps = eps;
-            ce.H = (int)H;
-            ce.Hkv = (int)Hkv;
-            ce.d = (int)d;
-            ce.row0 = f.row0;
-            ce.pos = f.pos;
-            ce.rope = rope.as<float2>();
-            ce.q = q.p;
-            ce.kc = kv_plane(f.ctx, l, 0);
-            ce.vc = kv_plane(f.ctx, l, 1);
-            Scope sc(this, PC_GEMM, 1);
-            fused_qkv = launch_gemm_csk(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid, ce, stream);
-        }
-        if (!fused_qkv) s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
-        if (fused_qkv) {
-        } else if (batch) {
+        int s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
+        if (batch) {
             Scope sc(this, PC_EPI, (int)f.reqs.size());
             for (const Fwd::Req& r : f.reqs)
                 launch_qkv_epilogue(partial.as<float>() + (size_t)r.tok0 * nqkv, s, r.n, (int)H, (int)Hkv, (int)d,
@@ -823,13 +780,11 @@ void tkv_engine::forward(const Fwd& f) {
         uint8_t* attn_rows = static_cast<uint8_t*>(attn.p);
         float* x_rows = x.as<float>() + r0 * hid;
         next(w_gu[l], rows, (int)(2 * I), (int)hid);
-        if (!proj_residual(attn_rows, (int)qd, w_o[l], rows, x_rows, norm_mlp(l))) {
-            s = gemm(attn_rows, (int)qd, w_o[l], rows, (int)hid, (int)qd);
-            if (!(skip_mask & 1)) {
-                Scope sc(this, PC_EPI, 1);
-                launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, norm_mlp(l), xb.p, ssp.as<float>(), dt,
-                                err.as<int>(), stream);
-            }
+        s = gemm(attn_rows, (int)qd, w_o[l], rows, (int)hid, (int)qd);
+        if (!(skip_mask & 1)) {
+            Scope sc(this, PC_EPI, 1);
+            launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, norm_mlp(l), xb.p, ssp.as<float>(), dt,
+                            err.as<int>(), stream);
         }
         // --- MLP block: gate|up fused into one GEMM, SwiGLU (with the folded mlp_norm scale) in its epilogue ---
         next(w_down[l], rows, (int)hid, (int)I);
@@ -840,14 +795,12 @@ void tkv_engine::forward(const Fwd& f) {
                           stream, gu_block);
         }
         if (l + 1 < L) next(w_qkv[l + 1], T, (int)nqkv, (int)hid);
-        // residual + the next RMSNorm (next layer's attn_norm, or final_norm)
-        if (!proj_residual(act.p, (int)I, w_down[l], rows, x_rows, norm_after_mlp(l))) {
-            s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
-            if (!(skip_mask & 2)) {
-                Scope sc(this, PC_EPI, 1);
-                launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, norm_after_mlp(l), xb.p, ssp.as<float>(),
-                                dt, err.as<int>(), stream);
-            }
+        s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
+        if (!(skip_mask & 2)) {
+            // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
+            Scope sc(this, PC_EPI, 1);
+            launch_residual(x_rows, partial.as<float>(), s, rows, (int)hid, norm_after_mlp(l), xb.p, ssp.as<float>(), dt,
+                            err.as<int>(), stream);
         }
     }
     if (f.logits && batch) {
@@ -2921,28 +2874,7 @@ tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int
         launch_init_transposed(w.p, DT::BF16, 2, 0, K, N, 0.01, 0);
         if (swiglu & 2) TKV_CUDA(cudaMemset(w.p, 0, (size_t)N * K * 2));  // constant weights (data-dependence probe)
         if (swiglu & 4) TKV_CUDA(cudaMemset(a.p, 0, (size_t)M * K * 2));
-        const bool csk = (swiglu & 8) != 0;  // cluster split-K GEMM with the fused residual epilogue
-        const bool chain = (swiglu & 16) != 0;  // split-K partials + the residual kernel (the chain csk replaces)
         swiglu &= 1;
-        DevMem cx, cxb, cw, cssp, cerr;
-        CskEpilogue ce;
-        if (csk || chain) {
-            cx.ensure((size_t)M * N * 4);
-            cxb.ensure((size_t)M * N * 2);
-            cw.ensure((size_t)N * 4);
-            cssp.ensure((size_t)M * ((N + 127) / 128) * 4);
-            cerr.ensure(64);
-            launch_fill_f32(cx.as<float>(), 0.f, M * N, 0);
-            launch_fill_f32(cw.as<float>(), 1.f, N, 0);
-            TKV_CUDA(cudaMemset(cerr.p, 0, 64));
-            ce.kind = 0;
-            ce.x = cx.as<float>();
-            ce.xb = cxb.p;
-            ce.w = cw.as<float>();
-            ce.ssp = cssp.as<float>();
-            ce.nb = (int)((N + 127) / 128);
-            ce.err = cerr.as<int>();
-        }
         const int nb = norm_blocks((int)K);
         ssp.ensure((size_t)M * nb * 4);
         launch_fill_f32(ssp.as<float>(), 1.0f, M * nb, 0);
@@ -2953,13 +2885,7 @@ tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int
         TKV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         TKV_CUDA(cudaDeviceSynchronize());
         auto run = [&] {
-            if (csk) {
-                if (!launch_gemm_csk(a.p, (int)K, w.p, (int)M, (int)N, (int)K, ce, st))
-                    fail(TKV_ERR_CONFIG, "cluster split-K GEMM not eligible for this shape");
-            } else if (chain) {
-                const int sp = launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, part.as<float>(), splits, st);
-                launch_residual(ce.x, part.as<float>(), sp, (int)M, (int)N, ce.w, ce.xb, ce.ssp, DT::BF16, ce.err, st);
-            } else if (swiglu)
+            if (swiglu)
                 launch_gemm_tc(a.p, (int)K, w.p, (int)M, (int)N, (int)K, nullptr, 1, st, act.p, ssp.as<float>(), nb,
                                1e-6f, N % 256 == 0 ? 128 : 64);
             else

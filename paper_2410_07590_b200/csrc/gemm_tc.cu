@@ -23,7 +23,6 @@
 #include <stdint.h>
 
 #include <algorithm>
-#include <map>
 #include <mutex>
 
 #include "dev_common.cuh"
@@ -676,281 +675,6 @@ __global__ void __launch_bounds__(THREADS_P)
     }
 }
 
-// ---------------------------------------------------------------------------------------------------------------
-// Cluster split-K GEMM for <= 128 tokens (swapped tiling) with the consumer's epilogue fused in. A cluster of CS CTAs
-// owns one 128-row weight tile (n-tile); CTA rank r streams k-blocks [r K / CS, (r + 1) K / CS) into its own TMEM
-// accumulator (TMEM lane = weight row, column = token). The split-K sum is a reduce-scatter over distributed shared
-// memory: after a cluster barrier (every CTA's mainloop done, so every ring is free) each CTA writes token slice q of
-// its accumulator into CTA q's ring (st.shared::cluster), a second barrier, and CTA q adds the CS slices in rank order
-// and runs the epilogue on [128 rows] x [its TS tokens]:
-//   CSK_RESID: x[t][col] += v; xb = x * w[col]; ssp[t][n-tile] = sum of x^2 over the tile's 128 columns
-//              (kernels.cu:residual_kernel, the RMSNorm partial sums of the next projection)
-//   CSK_QKV:   v *= row_scale(t) (folded attn_norm); RoPE on (even, odd) row pairs of q and k; q rows and the request
-//              cache K / V rows (kernels.cu:qkv_epilogue_kernel)
-// This replaces the fp32 split-K partial planes (9 MB per projection at C2) and one epilogue kernel per projection.
-// Residency: the host picks CS so that every cluster is co-resident (cudaOccupancyMaxActiveClusters).
-enum { CSK_RESID = 0, CSK_QKV = 1 };
-constexpr int CSK_TS_MAX = 16;
-
-struct CskArgs {
-    int M, N, K, kb_total, CS, TS, ntok, stages;
-    uint32_t a_bytes, tmem_cols, red_off;
-    int w_evict_first;
-    // CSK_RESID
-    float* x;            // residual stream rows [M][N]
-    __nv_bfloat16* xb;   // [M][N]
-    const float* w;      // RMSNorm weight of the next projection [N]
-    float* ssp;          // [M][nb] (written: block = n-tile)
-    int nb;
-    int* err;
-    // CSK_QKV
-    const float* ssp_in;  // [M][nb_in] row-scale partials of the GEMM input
-    int nb_in, hidden;
-    float eps;
-    int H, Hkv, d, row0;
-    const int32_t* pos;
-    const float2* rope;
-    __nv_bfloat16 *q, *kc, *vc;
-    unsigned long long* trace;  // debug (tkv_debug_gemm_trace): CTA 0 epilogue stamps at GT_EPI + 0..4
-};
-
-__device__ __forceinline__ void cluster_arrive_wait() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-    return v;
-}
-
-template <int EPI>
-__global__ void __launch_bounds__(THREADS_P) gemm_csk_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                            const __grid_constant__ CUtensorMap tmW, CskArgs g) {
-    pdl_launch();
-    extern __shared__ uint8_t smem_raw[];
-    // 1024-byte aligned by pointer arithmetic on the __shared__ array (stays in the shared window: LDS / STS)
-    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    const uint32_t stage_bytes = TILE_W + g.a_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.stages * stage_bytes);
-    uint64_t* empty = full + g.stages;
-    uint64_t* tfull = empty + g.stages;
-    uint64_t* recv_bar = tfull + 1;  // the CS slices of this CTA's tokens landed (bulk DSMEM copies, complete_tx)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = (int)cluster_rank(), nt = blockIdx.x / g.CS;
-    const int k0 = (int)((int64_t)r * g.kb_total / g.CS), nkb = (int)((int64_t)(r + 1) * g.kb_total / g.CS) - k0;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < g.stages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        mbar_init(tfull, 1);
-        mbar_init(recv_bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(g.tmem_cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-
-    const int et = threadIdx.x - 64;               // epilogue thread = TMEM lane = weight row of the tile
-    const int t0 = r * g.TS, tn = max(0, min(g.M, t0 + g.TS) - t0);  // this CTA's token slice
-    const int row = (warp & 3) * 32 + lane;        // epilogue warps: TMEM lane (warp % 4 owns lanes 32 (warp % 4) ..)
-    const int col = nt * 128 + row;
-    const uint32_t recv = smem_u32(smem);          // [CS][TS][128] fp32 inside the (then idle) ring
-    const uint32_t stg = recv + (uint32_t)(g.CS * g.TS * 512);  // [M][128] fp32: this CTA's accumulator, transposed
-    float* red = reinterpret_cast<float*>(smem + g.red_off);  // [4][TS] + [TS]
-    float xo[CSK_TS_MAX];
-    float v[CSK_TS_MAX];
-
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer ----------------
-            const uint64_t wpol = policy_evict_first();
-            const int pre = min(nkb, g.stages);
-            for (int i = 0; i < pre; ++i) {  // weights do not depend on the previous kernel
-                mbar_expect_tx(&full[i], stage_bytes);
-                if (g.w_evict_first) tma_load_2d_hint(smem + i * stage_bytes, &tmW, &full[i], (k0 + i) * BK, nt * 128, wpol);
-                else tma_load_2d(smem + i * stage_bytes, &tmW, &full[i], (k0 + i) * BK, nt * 128);
-            }
-            pdl_wait();
-            for (int i = 0; i < pre; ++i)
-                tma_load_2d(smem + i * stage_bytes + TILE_W, &tmA, &full[i], (k0 + i) * BK, 0);
-            for (int i = pre; i < nkb; ++i) {
-                const int s = i % g.stages;
-                mbar_wait(&empty[s], ((uint32_t)(i / g.stages) & 1u) ^ 1u);
-                uint8_t* st = smem + s * stage_bytes;
-                mbar_expect_tx(&full[s], stage_bytes);
-                if (g.w_evict_first) tma_load_2d_hint(st, &tmW, &full[s], (k0 + i) * BK, nt * 128, wpol);
-                else tma_load_2d(st, &tmW, &full[s], (k0 + i) * BK, nt * 128);
-                tma_load_2d(st + TILE_W, &tmA, &full[s], (k0 + i) * BK, 0);
-            }
-        }
-    } else if (warp == 1) {  // ---------------- MMA issuer (warp-uniform loop, elected lane issues) ----------------
-        const uint32_t id = idesc(128, g.ntok);
-        int s = 0;
-        uint32_t ph = 0;
-        for (int i = 0; i < nkb; ++i) {
-            mbar_wait(&full[s], ph);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lane == 0 && i < GT_STAGES) gtrace(g.trace, 3 * i + 1);
-            const uint32_t w = smem_u32(smem + s * stage_bytes);
-            const uint64_t dw = desc_k(w), da = desc_k(w + TILE_W);
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k) umma_f16_elect(tmem, dw + 2 * k, da + 2 * k, id, (i | k) != 0);
-            umma_commit_elect(&empty[s]);
-            if (++s == g.stages) {
-                s = 0;
-                ph ^= 1u;
-            }
-        }
-        umma_commit_elect(tfull);
-    } else {
-        // ---------------- epilogue warps: operands of the fused epilogue, loaded while the mainloop runs ----------------
-        pdl_wait();
-        if (EPI == CSK_RESID) {
-            for (int j = 0; j < CSK_TS_MAX; ++j)
-                xo[j] = (j < tn && col < g.N) ? g.x[(int64_t)(t0 + j) * g.N + col] : 0.f;
-        } else {
-            if (et < tn) red[4 * g.TS + et] = row_scale(g.ssp_in, g.nb_in, t0 + et, g.hidden, g.eps);
-        }
-        mbar_wait_sleep(tfull, 0u);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (et == 0) gtrace(g.trace, GT_EPI);
-        // stage the accumulator transposed, [token][row] (owner q's tokens = one contiguous TS x 512-byte block)
-        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-#pragma unroll 1
-        for (int c = 0; c < g.ntok; c += 16) {
-            uint32_t v[16];
-            tmem_ld16(tmem + lane_base + (uint32_t)c, v);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c + j < g.M)
-                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (uint32_t)(((c + j) * 128 + row) * 4)), "r"(v[j])
-                                 : "memory");
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the bulk-copy (async) proxy
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(recv_bar)),
-                         "r"((uint32_t)(g.CS * tn * 512))
-                         : "memory");
-            gtrace(g.trace, GT_EPI + 1);
-        }
-    }
-    __syncwarp();
-    cluster_arrive_wait();  // every CTA of the cluster: mainloop done (ring free), slices staged, recv_bar armed
-    if (et == 0) {
-        // one bulk DSMEM copy per owner: tokens [q TS, q TS + n_q) -> owner q's recv[r], completing on its recv_bar
-        for (int q = 0; q < g.CS; ++q) {
-            const int nq = max(0, min(g.M, (q + 1) * g.TS) - q * g.TS);
-            if (nq == 0) continue;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    mapa(recv + (uint32_t)(r * g.TS * 512), (uint32_t)q)),
-                "r"(stg + (uint32_t)(q * g.TS * 512)), "r"((uint32_t)(nq * 512)), "r"(mapa(smem_u32(recv_bar), (uint32_t)q))
-                : "memory");
-        }
-        gtrace(g.trace, GT_EPI + 2);
-    }
-    if (warp >= 2) {
-        mbar_wait(recv_bar, 0u);
-        if (et == 0) gtrace(g.trace, GT_EPI + 3);
-        const int ew = warp - 2;
-#pragma unroll
-        const float* rv = reinterpret_cast<const float*>(smem) + row;  // recv[src][j][row]
-#pragma unroll
-        for (int j = 0; j < CSK_TS_MAX; ++j) v[j] = 0.f;
-#pragma unroll 4
-        for (int src = 0; src < g.CS; ++src) {  // rank order
-            float p[CSK_TS_MAX];
-#pragma unroll
-            for (int j = 0; j < CSK_TS_MAX; ++j) p[j] = j < tn ? rv[(src * g.TS + j) * 128] : 0.f;
-#pragma unroll
-            for (int j = 0; j < CSK_TS_MAX; ++j) v[j] += p[j];
-        }
-        if (et == 0) gtrace(g.trace, GT_EPI + 5);
-        if (EPI == CSK_RESID) {
-            const bool ok = col < g.N;
-            const float wc = ok ? g.w[col] : 0.f;
-            if (et == 0) gtrace(g.trace, GT_EPI + 6);
-            bool bad = false;
-            float ss[CSK_TS_MAX];
-#pragma unroll
-            for (int j = 0; j < CSK_TS_MAX; ++j) {
-                const float xn = xo[j] + v[j];
-                ss[j] = (ok && j < tn) ? xn * xn : 0.f;
-                if (ok && j < tn) {
-                    g.x[(int64_t)(t0 + j) * g.N + col] = xn;
-                    g.xb[(int64_t)(t0 + j) * g.N + col] = __float2bfloat16_rn(xn * wc);
-                    bad |= !isfinite(xn);
-                }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)  // the slice's butterflies interleaved (independent chains)
-#pragma unroll
-                for (int j = 0; j < CSK_TS_MAX; ++j) ss[j] += __shfl_xor_sync(0xffffffffu, ss[j], o);
-            if (lane == 0)
-#pragma unroll
-                for (int j = 0; j < CSK_TS_MAX; ++j)
-                    if (j < tn) red[ew * g.TS + j] = ss[j];
-            if (et == 0) gtrace(g.trace, GT_EPI + 7);
-            if (bad) atomicOr(g.err, 2);
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (et == 0) gtrace(g.trace, GT_EPI + 8);
-            if (et < tn)  // the tile's sum of squares, warps in order
-                g.ssp[(int64_t)(t0 + et) * g.nb + nt] =
-                    ((red[0 * g.TS + et] + red[1 * g.TS + et]) + red[2 * g.TS + et]) + red[3 * g.TS + et];
-        } else {
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // row scales of the slice are in red[4 TS ..]
-            const int qd = g.H * g.d, kvd = g.Hkv * g.d, half = g.d / 2;
-            const bool odd = (col & 1) != 0;
-#pragma unroll
-            for (int j = 0; j < CSK_TS_MAX; ++j) {
-                if (j >= tn) break;
-                const int t = t0 + j;
-                const float xv = v[j] * red[4 * g.TS + j];
-                const float other = __shfl_xor_sync(0xffffffffu, xv, 1);  // the pair partner (rows 2m, 2m + 1)
-                if (col >= g.N) continue;
-                if (col >= qd + kvd) {  // V: as is
-                    g.vc[(int64_t)(g.row0 + t) * kvd + (col - qd - kvd)] = __float2bfloat16_rn(xv);
-                    continue;
-                }
-                const int e = (col < qd ? col : col - qd) % g.d;
-                const float2 cs = g.rope[(int64_t)g.pos[t] * half + e / 2];
-                const float x0 = odd ? other : xv, x1 = odd ? xv : other;
-                const float rv = odd ? x0 * cs.y + x1 * cs.x : x0 * cs.x - x1 * cs.y;  // rope.cpp:41-44
-                if (col < qd) g.q[(int64_t)t * qd + col] = __float2bfloat16_rn(rv);
-                else g.kc[(int64_t)(g.row0 + t) * kvd + (col - qd)] = __float2bfloat16_rn(rv);
-            }
-        }
-    }
-    if (et == 0) gtrace(g.trace, GT_EPI + 4);
-    __syncwarp();
-    cluster_arrive_wait();  // no CTA leaves while a bulk copy may still read its staging or target its recv_bar
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 1) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
-    }
-}
-
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1157,132 +881,6 @@ void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first,
     g_knobs.ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : d.ctas_per_sm;
     g_knobs.w_evict_first = w_evict_first;
     g_knobs.np = np > 0 ? np : d.np;
-}
-
-
-// ---- cluster split-K GEMM with a fused epilogue (<= 128 tokens) ----
-namespace {
-// The occupancy API counts any kernel that allocates TMEM as one CTA per SM, but the hardware co-schedules as many
-// as shared memory and registers allow (tools/micro/tmem_occ.cu: two 60 KB tcgen05 CTAs per SM run concurrently).
-// Cluster residency is therefore asked of a TMEM-free proxy with the same block size, shared memory and cluster shape.
-__global__ void __launch_bounds__(THREADS_P) csk_occupancy_proxy(int* p) {
-    if (p) p[0] = 0;
-}
-int csk_max_active(int cs, size_t smem) {
-    static std::mutex mu;
-    static std::map<std::pair<int, size_t>, int> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair(cs, smem);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
-    TKV_CUDA(cudaFuncSetAttribute(csk_occupancy_proxy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    TKV_CUDA(cudaFuncSetAttribute(csk_occupancy_proxy, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(cs * 16);
-    cfg.blockDim = dim3(THREADS_P);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, csk_occupancy_proxy, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        n = 0;
-    }
-    cache[key] = n;
-    return n;
-}
-template <int EPI>
-void csk_attrs(size_t smem) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        TKV_CUDA(cudaFuncSetAttribute(gemm_csk_kernel<EPI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    });
-    TKV_CUDA(cudaFuncSetAttribute(gemm_csk_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-}
-}  // namespace
-
-bool launch_gemm_csk(const void* A, int lda, const void* W, int M, int N, int K, const CskEpilogue& e, cudaStream_t s) {
-    if (M < 1 || M > 128 || K % BK || !gemm_tc_supported(M, N, K, lda)) return false;
-    CskArgs g{};
-    g.M = M;
-    g.N = N;
-    g.K = K;
-    g.kb_total = K / BK;
-    g.ntok = ((M + 15) / 16) * 16;
-    g.a_bytes = (uint32_t)g.ntok * BK * 2;
-    g.tmem_cols = 32;
-    while (g.tmem_cols < (uint32_t)g.ntok) g.tmem_cols <<= 1;
-    g.stages = std::min<int>(8, (110 * 1024 - 1024 - 1024) / (int)(TILE_W + g.a_bytes));
-    if (g.stages < 2) return false;
-    const uint32_t ring = (uint32_t)g.stages * (TILE_W + g.a_bytes);
-    g.red_off = ring + 256;
-    const size_t smem = 1024 + (size_t)g.red_off + 512;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int n_tiles = (N + 127) / 128;
-    // the largest cluster (split count) whose clusters are all co-resident and whose slices fit the ring
-    int best = 0;
-    for (int cs = std::min(16, g.kb_total); cs >= 2; --cs) {
-        const int ts = (M + cs - 1) / cs;
-        if (ts > CSK_TS_MAX || (uint32_t)(cs * ts + M) * 512 > ring || n_tiles * cs > 2 * sms) continue;
-        const int ma = csk_max_active(cs, smem);
-        if (ma < n_tiles) continue;
-        if (best == 0 || n_tiles * cs > n_tiles * best) best = cs;
-    }
-    if (best == 0) return false;
-    g.CS = best;
-    g.TS = (M + best - 1) / best;
-    g.w_evict_first = g_knobs.w_evict_first;
-    g.x = e.x;
-    g.xb = (__nv_bfloat16*)e.xb;
-    g.w = e.w;
-    g.ssp = e.ssp;
-    g.nb = e.nb;
-    g.err = e.err;
-    g.ssp_in = e.ssp_in;
-    g.nb_in = e.nb_in;
-    g.hidden = e.hidden;
-    g.eps = e.eps;
-    g.H = e.H;
-    g.Hkv = e.Hkv;
-    g.d = e.d;
-    g.row0 = e.row0;
-    g.pos = e.pos;
-    g.rope = e.rope;
-    g.q = (__nv_bfloat16*)e.q;
-    g.kc = (__nv_bfloat16*)e.kc;
-    g.vc = (__nv_bfloat16*)e.vc;
-    g.trace = g_gemm_trace;
-    const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
-    const CUtensorMap tw = make_map(W, N, K, K, 128);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(n_tiles * best);
-    cfg.blockDim = dim3(THREADS_P);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)best;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    if (e.kind == CSK_RESID) {
-        csk_attrs<CSK_RESID>(smem);
-        TKV_CUDA(cudaLaunchKernelEx(&cfg, gemm_csk_kernel<CSK_RESID>, ta, tw, g));
-    } else {
-        csk_attrs<CSK_QKV>(smem);
-        TKV_CUDA(cudaLaunchKernelEx(&cfg, gemm_csk_kernel<CSK_QKV>, ta, tw, g));
-    }
-    return true;
 }
 
 }  // namespace tkv

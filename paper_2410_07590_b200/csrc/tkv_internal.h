@@ -136,27 +136,6 @@ void set_gemm_skip_epi(int v);  // timing experiments only: skip the normal-tili
 void set_gemm_raster(int r, int group_mb = -1);  // normal (> 128-token) tiling: 128-row activation tiles per unit (1 or 2)
 void set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, int w_evict_first, int np = 0, int pf = -1,
                     int krot = -1);
-// Cluster split-K tcgen05 GEMM for <= 128 tokens with the consumer epilogue fused (gemm_tc.cu:gemm_csk_kernel):
-// kind 0 = residual (x += A.W^T; xb = x * w; ssp per 128-column tile), kind 1 = QKV (row scale from ssp_in, RoPE,
-// q + request-cache K/V rows at row0). Returns false when the shape / residency does not allow it (caller falls back
-// to split-K partials + the epilogue kernel). bf16 only.
-struct CskEpilogue {
-    int kind = 0;
-    float* x = nullptr;
-    void* xb = nullptr;
-    const float* w = nullptr;
-    float* ssp = nullptr;
-    int nb = 0;
-    int* err = nullptr;
-    const float* ssp_in = nullptr;
-    int nb_in = 0, hidden = 0;
-    float eps = 0.f;
-    int H = 0, Hkv = 0, d = 0, row0 = 0;
-    const int32_t* pos = nullptr;
-    const float2* rope = nullptr;
-    void *q = nullptr, *kc = nullptr, *vc = nullptr;
-};
-bool launch_gemm_csk(const void* A, int lda, const void* W, int M, int N, int K, const CskEpilogue& e, cudaStream_t s);
 int gemm_tc_tiles(int M, int N);
 int gemm_tc_ctas_per_sm(int M);  // resident GEMM CTAs per SM the launcher plans for M tokens
 // Returns the number of split-K partial planes actually written (<= splits: every split is non-empty).

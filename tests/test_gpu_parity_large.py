@@ -254,26 +254,3 @@ def test_pdl_off_equals_pdl_on_bitwise(large):
         with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
             out[flags] = eng.prefill_query(ctx, A["c2ctx.r0.query"]).copy()
     assert np.array_equal(out[0], out[T.FLAG_NO_PDL])
-
-
-@pytest.mark.parametrize("case", ["c2ctx", "llama1"])
-def test_cluster_fused_epilogues_match_split_k_partials(large, case):
-    """The <= 128-token projections run as cluster split-K GEMMs with the residual / QKV epilogues fused (DSMEM
-    reduce-scatter, gemm_tc.cu:gemm_csk_kernel). Against the split-K partial planes + epilogue kernels
-    (TKV_FLAG_SPLITK_PARTIALS): same logits within the bf16 tolerance, same greedy tokens, and both against the
-    reference golden; the greedy decode (M = 1 forwards through the same path) runs on both."""
-    m, A = need_case(large, case)
-    out = {}
-    for flags in (0, T.FLAG_SPLITK_PARTIALS):
-        eng = engine(m, "bf16", flags=flags)
-        ids = eng.ingest_chunks(payloads(A, case))
-        with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
-            lg = eng.prefill_query(ctx, A[f"{case}.r0.query"]).copy()
-            out[flags] = (lg, eng.greedy_decode(ctx, 3))
-    a, b = out[0], out[T.FLAG_SPLITK_PARTIALS]
-    close(a[0], b[0], BF16_TOL)
-    assert_argmax(a[0], b[0], BF16_TOL)
-    ref = A[f"{case}.r0.reordered.logits"] if f"{case}.r0.reordered.logits" in A else None
-    if ref is not None:
-        close(a[0], ref, BF16_TOL)
-    assert len(a[1]) == len(b[1]) == 3

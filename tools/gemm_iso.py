@@ -8,12 +8,9 @@ from paper_2410_07590_b200 import turbokv as T
 
 L = T.lib()
 SHAPES = {"qkv": (64, 4608, 3584, 8, 0), "o": (64, 3584, 3584, 10, 0), "gate_up": (64, 37888, 3584, 1, 1),
-          "down": (64, 3584, 18944, 10, 0),
-          # residual consumers: split-K partials + residual kernel (chain) vs the cluster split-K GEMM (fused)
-          "o+res chain": (64, 3584, 3584, 10, 16), "o+res csk": (64, 3584, 3584, 1, 8),
-          "down+res chain": (64, 3584, 18944, 10, 16), "down+res csk": (64, 3584, 18944, 1, 8)}
+          "down": (64, 3584, 18944, 10, 0)}
 for name, (M, N, K, sp, sw) in SHAPES.items():
     ms = C.c_double()
     T._check(L.tkv_debug_gemm_bench(0, M, N, K, sp, sw, 50, C.byref(ms)))
-    print(f"{name:15s} N={N:6d} K={K:6d} splits={sp:2d}: {ms.value * 1e3:7.2f} us/launch, "
+    print(f"{name:8s} N={N:6d} K={K:6d} splits={sp:2d}: {ms.value * 1e3:7.2f} us/launch, "
           f"{N * K * 2 / (ms.value / 1e3) / 1e9:7.0f} GB/s of weights")
