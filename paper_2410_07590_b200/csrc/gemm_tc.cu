@@ -251,10 +251,19 @@ struct GemmArgs {
     // nx_pf weight k-blocks of the next GEMM's units blockIdx.x, blockIdx.x + grid, ... (tmN), so that GEMM's
     // ring fill hits L2 while this one drains and runs its epilogue
     int nx_pf, nx_units, nx_n_tiles, nx_kb_total, nx_kb_per_split, nx_np;
+    int trace_parity;             // debug: which of the two per-CTA entry/exit slot sets this launch writes
     unsigned long long* trace;    // debug (tkv_debug_gemm_trace): CTA 0 clock64 per stage [it][3] = producer issue,
                                   // MMA saw full, MMA committed; [GT_UNIT + lu][2] = epilogue start / end per unit
 };
-constexpr int GT_STAGES = 1024, GT_UNIT = 3 * GT_STAGES, GT_EPI = GT_UNIT + 2 * 64 + 4 * 64, GT_SIZE = GT_EPI + 32;
+constexpr int GT_STAGES = 1024, GT_UNIT = 3 * GT_STAGES, GT_EPI = GT_UNIT + 2 * 64 + 4 * 64, GT_CTA = GT_EPI + 32,
+              GT_SIZE = GT_CTA + 2 * 2 * 1024;  // [launch parity][cta][entry, exit] globaltimer ns
+__device__ __forceinline__ void gtrace_cta(unsigned long long* t, int parity, int exit) {
+    if (t && blockIdx.x < 1024) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        t[GT_CTA + (parity * 1024 + blockIdx.x) * 2 + exit] = ns;
+    }
+}
 unsigned long long* g_gemm_trace = nullptr;
 __device__ __forceinline__ void gtrace(unsigned long long* t, int slot) {
     if (t && blockIdx.x == 0 && slot < GT_SIZE) {
@@ -292,6 +301,7 @@ __global__ void __launch_bounds__(THREADS_P)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                    const __grid_constant__ CUtensorMap tmN, GemmArgs g) {
     pdl_launch();
+    if (threadIdx.x == 0) gtrace_cta(g.trace, g.trace_parity, 0);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t wbytes = (uint32_t)g.np * TILE_W;  // weight bytes per stage
@@ -668,6 +678,7 @@ __global__ void __launch_bounds__(THREADS_P)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) gtrace_cta(g.trace, g.trace_parity, 1);
     if (cl > 1) cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -811,6 +822,8 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;
     g.partial = partial;
     g.trace = g_gemm_trace;
+    static int trace_launch = 0;
+    g.trace_parity = (trace_launch++) & 1;
     g.act = (__nv_bfloat16*)swiglu_act;
     g.ssp = ssp;
     g.nb = nb;

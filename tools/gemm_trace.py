@@ -15,8 +15,8 @@ T._check(L.tkv_debug_set_gemm_knobs(st, smk, cps, 1))
 ms = C.c_double()
 T._check(L.tkv_debug_gemm_bench(0, M, N, K, sp, sw, 5, C.byref(ms)))  # warm
 T._check(L.tkv_debug_gemm_trace(1, None, 0))
-T._check(L.tkv_debug_gemm_bench(0, M, N, K, sp, sw, 1, C.byref(ms)))
-buf = np.zeros(3 * 1024 + 128 + 256 + 32, np.uint64)
+T._check(L.tkv_debug_gemm_bench(0, M, N, K, sp, sw, 2, C.byref(ms)))  # + 3 warm-up launches inside: last two traced
+buf = np.zeros(3 * 1024 + 128 + 256 + 32 + 4096, np.uint64)
 T._check(L.tkv_debug_gemm_trace(0, buf.ctypes.data_as(C.POINTER(C.c_uint64)), buf.size))
 st3 = buf[:3072].reshape(1024, 3).astype(np.int64)
 n = int((st3[:, 1] > 0).sum())
@@ -44,3 +44,13 @@ print("  epilogue per unit (start, end):", [tuple(int(x) for x in r) for r in u[
 ep = buf[3072 + 384:].astype(np.int64)
 print("  epilogue stamps:", [int(x - t0) if x else 0 for x in ep[:24]])
 print(f"  last stage full at {int(full[-1])} cyc")
+
+cta = buf[3072 + 384 + 32:].reshape(2, 1024, 2).astype(np.int64)
+for par in range(2):
+    c = cta[par]
+    c = c[c[:, 0] > 0]
+    if len(c):
+        base = cta[:, :, 0][cta[:, :, 0] > 0].min()
+        st, en = (c[:, 0] - base) / 1e3, (c[:, 1] - base) / 1e3
+        print(f"  launch parity {par}: {len(c)} CTAs, entry min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f} us, "
+              f"exit min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f} us")
