@@ -4,21 +4,19 @@
 // lo[t] <= j <= hi[t] (causal_rows / build_mask, attention.cpp:50-92).
 //
 // GQA packing: rows of ONE kv head g are (token t, head g*group + i), so every K/V tile a CTA streams
-// serves all `group` query heads (C2: 64 tokens x 7 heads = 448 rows per kv head).
+// serves all `group` query heads (C2: 64 tokens x 7 heads = 448 rows per kv head = 3.5 tiles of 128).
 //
-// v4 (ping-pong): a CTA owns a ROW GROUP of 256 rows = two 128-row tiles A and B of the same kv head and
-// streams one split of the key range through them:
-//   tensor pipe:  [PV_A(j-1) S_A(j)] [PV_B(j-1) S_B(j)] [PV_A(j) S_A(j+1)] ...
-//   softmax WG A works on S_A(j) while the pipe runs the B bracket, and vice versa, so the tensor pipe
-//   and the softmax (MUFU + FMA pipes) overlap; every K/V tile is read once for 256 rows.
-// Warps 0-3 = softmax A, 4-7 = softmax B (ONE thread per row: no cross-thread max exchange), warp 8 =
-// TMA producer, warp 9 = MMA issuer. TMEM (512 cols): S_A 0, O_A 128, S_B 256, O_B 384; P_X (bf16 pairs,
-// 64 cols) is written over the first half of S_X and fed to the PV tcgen05.mma as the A operand from TMEM.
-// O accumulates in TMEM; it is rescaled lazily, only when a row max grows by more than 2^8 (the stale max
-// keeps every p <= 2^8, exact in fp32 and bf16 range).
+// v6 (one 128-row tile per CTA, S double-buffered, Q and P in TMEM, 16x256b softmax layout): see attn_tc_kernel.
+// The tensor pipe runs S(j+1) while the softmax works on S(j), so the per-tile critical path is max(softmax, S + PV)
+// rather than their sum (v4 kept two row tiles per CTA with one S buffer each and ping-ponged them: softmax + S + PV
+// per tile, ~3.9 K cycles per pair of tiles; v6 ~1.9 K per tile with a third fewer shared-memory bytes per tile).
+// Measured and dropped (tools/variant_ab.sh, C2 / C3): two softmax threads per row exchanging maxima through shared
+// memory, four, separate K and V producer warps, 2- and 4-CTA clusters multicasting K/V (every ring slot then waits
+// for the slowest CTA), try_wait suspend hints, and MUFU / polynomial exp split by warp.
 // exp2 runs on two pipes: most pairs on MUFU.EX2, POLY_PAIRS of every 16 on the FMA pipe (Cody-Waite +
 // degree-3 minimax, max rel err 7.5e-5, far below the bf16 rounding of P), with packed f32x2 FFMA2/FADD2
-// and three-input FMNMX3 to keep the issue rate down.
+// and three-input FMNMX3 to keep the issue rate down. O is rescaled lazily, only when a row max grows by more
+// than 2^8 (the stale max keeps every p <= 2^8, exact in fp32 and bf16 range).
 // Context K/V rows below `kv_ready` were written before this forward began (the embed kernel that starts
 // every forward does not release its dependents before its own griddepcontrol.wait), so their TMA loads
 // are issued BEFORE griddepcontrol.wait and overlap the previous kernel's tail.
@@ -41,27 +39,38 @@
 namespace tkv {
 namespace {
 
-constexpr int D = 128, BR = 128, BK = 128, RG = 2 * BR;  // rows per tile, keys per tile, rows per CTA
+constexpr int D = 128, BR = 128, BK = 128;                // rows per CTA (one tile), keys per tile
+constexpr int RG = BR;                                    // rows per CTA = rows per workspace row group
+static_assert(RG == kAttnTcRows, "engine-side row-group size");
 #ifndef ATTN_KST
 #define ATTN_KST 3
 #endif
 #ifndef ATTN_VST
 #define ATTN_VST 2
 #endif
-constexpr int KST = ATTN_KST, VST = ATTN_VST;            // K / V ring depths (Q 64 KB + (KST + VST) x 32 KB <= 224 KB)
-constexpr int SM_THREADS = 256, THREADS = SM_THREADS + 64;
+constexpr int KST = ATTN_KST, VST = ATTN_VST;            // K / V ring depths (Q 32 KB + (KST + VST) x 32 KB <= 224 KB)
+// Softmax warps 0-7: warp w owns TMEM lanes [32*(w%4) + 16*(w/4), +16) = 16 whole rows of the tile; with the
+// 16x256b TMEM access shape lane t of the warp holds rows t/4 and t/4 + 8 of them, columns 8k + 2(t%4) + {0,1}
+// (k = 0..15), so a row lives in the 4 lanes of one quad and its max / sum are two shuffles.
+constexpr int SM_WARPS = 8, SM_THREADS = 32 * SM_WARPS;
+constexpr int WARP_TMA = SM_WARPS, WARP_MMA = SM_WARPS + 1, THREADS = 32 * (WARP_MMA + 1);
 #ifndef POLY_PAIRS
 #define POLY_PAIRS 6
 #endif
 constexpr int kPolyPairs = POLY_PAIRS;                          // of every 16 exp2 pairs, this many on the FMA pipe
 constexpr uint32_t SUB = 128 * 64 * 2;                   // [128 rows][64 cols] bf16 SW128 sub-tile = 16 KB
 constexpr uint32_t TILE = 2 * SUB;                       // 128 x 128 bf16
-constexpr uint32_t OFF_Q = 0;                            // Q_A, Q_B
-constexpr uint32_t OFF_K = 2 * TILE;
+constexpr uint32_t OFF_Q = 0;  // epilogue staging of the output tile
+constexpr uint32_t OFF_K = TILE;
 constexpr uint32_t OFF_V = OFF_K + KST * TILE;
 constexpr uint32_t OFF_BAR = OFF_V + VST * TILE;
 constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
-constexpr uint32_t TMEM_COLS = 512;
+static_assert(SMEM_BYTES <= 232448, "attention smem budget");
+// TMEM columns: O [0,128) fp32, S0 [128,256), S1 [256,384) fp32, P0 [384,448), P1 [448,512) bf16 pairs
+// TMEM columns: O [0,128) fp32, S0 / S1 [128,384) fp32, P [384,448) and Q [448,512) bf16 pairs. Q in TMEM makes
+// S = Q.K^T a TS MMA that reads only K from shared memory (an SS MMA at N = 128 reads A and B at ~110 B/clk, most
+// of the SM's shared-memory bandwidth, which the TMA writes of the K/V ring also need).
+constexpr uint32_t TMEM_COLS = 512, T_O = 0, T_S = 128, T_P = 384, T_Q = 448;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_LOG2 = 8.0f;
 
@@ -173,6 +182,37 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
         "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
 }
+// 16-lane shapes: 16x256b.x8 = 16 TMEM lanes x 64 columns; lane t of the warp gets, for k = 0..7, regs 4k, 4k+1 =
+// (lane t/4, columns 8k + 2(t%4) + {0,1}) and regs 4k+2, 4k+3 = the same columns of lane t/4 + 8.
+__device__ __forceinline__ void tmem_ld_16x256_x8(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_16x256_x8(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+// 16x128b.x4 = 16 lanes x 16 columns; regs 2k, 2k+1 = column 4k + t%4 of lanes t/4 and t/4 + 8 (k = 0..3)
+__device__ __forceinline__ void tmem_st_16x128_x4(uint32_t taddr, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.16x128b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -253,7 +293,7 @@ __device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
 // Debug timeline (tkv_debug_attn_trace): CTA (0,0,0) stamps clock64 at pipeline events, slot [j][e]. The
 // buffer pointer travels in the kernel arguments (a uniform constant-bank read, no global load on the path).
 unsigned long long* g_trace_host = nullptr;
-constexpr int TRACE_EV = 10, TRACE_TILES = 32, TRACE_CTA0 = TRACE_EV * TRACE_TILES, TRACE_CTAS = 1024;
+constexpr int TRACE_EV = 16, TRACE_TILES = 32, TRACE_CTA0 = TRACE_EV * TRACE_TILES, TRACE_CTAS = 1024;
 __device__ __forceinline__ void trace_at(unsigned long long* buf, int j, int e) {
     if (buf && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < TRACE_TILES) {
         unsigned long long t;
@@ -262,20 +302,14 @@ __device__ __forceinline__ void trace_at(unsigned long long* buf, int j, int e) 
     }
 }
 #define trace(j, e) trace_at(a.trace, (j), (e))
-#ifndef TRACE_SM
-#define TRACE_SM 0  // 1: events 4-8 stamp softmax-internal points of thread 0 instead of the MMA/TMA warps
-#endif
-#define trace_pipe(j, e) do { if (!TRACE_SM) trace(j, e); } while (0)
-#define trace_mma(j, e) do { if (TRACE_SM == 2) trace(j, e); } while (0)
-#define trace_sm(j, e) do { if (TRACE_SM == 1 && tid == 0) trace(j, e); } while (0)
 
 struct AttnArgs {
     const __nv_bfloat16* q;
     const int32_t* lo;
     const int32_t* hi;
     __nv_bfloat16* out;
-    float* ws_o;       // bf16 [splits][row groups][256][D]: each split's normalized O/l (sized as fp32 ws)
-    float* ws_ml;      // [splits][row groups][256] (m in log2 units, l)
+    float* ws_o;       // bf16 [splits][row groups][BR][D]: each split's normalized O/l (sized as fp32 ws)
+    float* ws_ml;      // [splits][row groups][BR] (m in log2 units, l)
     int* err;
     int Tq, Tk, H, Hkv, splits, kv_ready;
     float scale;
@@ -289,7 +323,30 @@ struct AttnArgs {
     int n_req, layer;
 };
 
-// 10 warps: 3 share an SM sub-partition's 16K registers -> at most 168 registers per thread
+// Warp-collective MMA issue: the whole MMA warp walks the loop (operands stay warp-uniform, in uniform registers);
+// elect.sync picks the issuing lane, the same one every time, so a commit tracks every MMA it issued.
+__device__ __forceinline__ void umma_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+// v6: ONE 128-row tile per CTA, S double-buffered so the tensor pipe runs S(j+1) while the softmax works on S(j):
+//   tensor pipe:  S(0) S(1) PV(0) S(2) PV(1) S(3) PV(2) ...
+// S(j+2) may overwrite S buffer j & 1 once PV(j) was issued (its P chunks were released, so the softmax has loaded
+// S(j)); P is single-buffered (P(j+1) waits for PV(j) to retire). Warps 0-7 = softmax, 16 whole rows each (see
+// SM_WARPS): every row statistic is quad-local and a warp rescales its own O rows. Warp 8 = TMA producer, warp 9 =
+// MMA issuer (whole warp, elected lane).
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
@@ -300,10 +357,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* k_empty = bars + KST;          // [KST]
     uint64_t* v_full = bars + 2 * KST;       // [VST]
     uint64_t* v_empty = v_full + VST;        // [VST]
-    uint64_t* s_full = v_empty + VST;        // [2] S_X(j) in TMEM
-    uint64_t* p_full = s_full + 2;           // [2][4] chunk c (32 keys) of P_X(j) in TMEM (128 threads arrived)
-    uint64_t* o_done = p_full + 8;           // [1] every MMA retired
-    uint64_t* q_ready = o_done + 1;          // [1] Q tiles staged (256 threads arrived)
+    uint64_t* s_full = v_empty + VST;        // [2] S(j) in TMEM buffer j & 1
+    uint64_t* p_full = s_full + 2;           // [2][4] chunk c (32 keys) of P(j) in buffer j & 1 (128 threads arrived)
+    uint64_t* pv_done = p_full + 8;          // [2] PV(j) retired (O current through j; P buffer j & 1 free again)
+    uint64_t* o_done = pv_done + 2;          // [1] every MMA retired
+    uint64_t* q_ready = o_done + 1;          // [1] Q tile staged (256 threads arrived)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 1);
     __shared__ int sh_range[2];
 
@@ -332,10 +390,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     const bool b3 = a.n_req > 0;
     const int rows_total = Tq * group;
-    const int rr0 = blockIdx.x * RG;                       // first row of this row group
-    const int rows_here = min(RG, rows_total - rr0);
-    if (rows_here <= 0) return;                            // batched grid sized for the longest request
-    const bool hasB = rows_here > BR;
+    const int rr0 = blockIdx.x * BR;                       // first row of this tile
+    if (rr0 >= rows_total) return;                         // batched grid sized for the longest request
 
     const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     if (tid == 0 && a.trace && cta_lin < TRACE_CTAS) a.trace[TRACE_CTA0 + 2 * cta_lin] = globaltimer_ns();
@@ -349,21 +405,22 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&v_full[s], 1);
             mbar_init(&v_empty[s], 1);
         }
-        for (int x = 0; x < 2; ++x) {
-            mbar_init(&s_full[x], 1);
-            for (int c = 0; c < 4; ++c) mbar_init(&p_full[x * 4 + c], BR);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s_full[b], 1);
+            mbar_init(&pv_done[b], 1);
+            for (int c = 0; c < 4; ++c) mbar_init(&p_full[b * 4 + c], SM_WARPS);  // one arrive per warp
         }
         mbar_init(o_done, 1);
         mbar_init(q_ready, SM_THREADS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) {
-        // key range of the row group = union of its tokens' [lo, hi] (lo/hi were uploaded before the forward)
+    if (warp == WARP_TMA) {
+        // key range of the tile = union of its tokens' [lo, hi] (lo/hi were uploaded before the forward)
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(mK)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(mV)) : "memory");
         }
-        const int t0 = rr0 / group, t1 = (rr0 + rows_here - 1) / group;
+        const int t0 = rr0 / group, t1 = (min(rr0 + BR, rows_total) - 1) / group;
         int blo = INT32_MAX, bhi = -1;
         for (int t = t0 + lane; t <= t1; t += 32) {
             blo = min(blo, lop[t]);
@@ -378,7 +435,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             sh_range[1] = bhi;
         }
     }
-    if (warp == 9) {
+    if (warp == WARP_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -394,10 +451,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int ke = min(bhi, ks + chunk - 1);
     const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
 
-    if (warp == 8) {
+    if (warp == WARP_TMA) {
         if (lane != 0) {
-            // HBM is mostly idle during attention at query-prefill sizes: lanes 1-31 warm L2 with this CTA's
-            // share of the next projections' weights (bulk prefetch, no completion tracking)
+            // HBM is mostly idle during attention at query-prefill sizes: lanes 1-31 may warm L2 with this CTA's
+            // share of the next projections' weights (bulk prefetch, no completion tracking; off by default)
             const int ncta = gridDim.x * gridDim.y * gridDim.z;
             for (int rg2 = 0; rg2 < 2; ++rg2) {
                 const size_t total = a.pf.bytes[rg2] & ~size_t(15);
@@ -407,221 +464,209 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (size_t off = b0 + (size_t)(lane - 1) * 65536; off < b1; off += (size_t)31 * 65536)
                     prefetch_l2(static_cast<const uint8_t*>(a.pf.ptr[rg2]) + off, (uint32_t)min((size_t)65536, b1 - off));
             }
-        }
-        if (lane == 0) {  // ---------------- TMA producer ----------------
+        } else {  // ---------------- TMA producer: K(j) then V(j) into their rings ----------------
+            auto load_tile = [&](bool k_tile, int j) {
+                const CUtensorMap* m = k_tile ? mK : mV;
+                uint64_t* full = k_tile ? k_full : v_full;
+                uint64_t* empty = k_tile ? k_empty : v_empty;
+                const int st = k_tile ? KST : VST;
+                const int sl = j % st;
+                mbar_wait(&empty[sl], ((uint32_t)(j / st) & 1u) ^ 1u);
+                mbar_expect_tx(&full[sl], TILE);
+                const uint32_t dst = sbase + (k_tile ? OFF_K : OFF_V) + sl * TILE;
+                const int key = ks + j * BK;
+                if (b3) {
+                    const int plane = 2 * a.layer + (k_tile ? 0 : 1);
+                    tma_load_3d(dst, m, &full[sl], g * D, key, plane);
+                    tma_load_3d(dst + SUB, m, &full[sl], g * D + 64, key, plane);
+                } else {
+                    tma_load_2d(dst, m, &full[sl], g * D, key);
+                    tma_load_2d(dst + SUB, m, &full[sl], g * D + 64, key);
+                }
+                trace(j, k_tile ? 6 : 7);
+            };
             bool waited = false;
             for (int j = 0; j < n; ++j) {
-                const int key = ks + j * BK;
-                if (!waited && key + BK > kv_ready) {  // rows written by the previous kernels of this forward
+                if (!waited && ks + j * BK + BK > kv_ready) {  // rows written by the previous kernels of this forward
                     pdl_wait();
                     waited = true;
                 }
-                const int sk = j % KST, sv = j % VST;
-                mbar_wait(&k_empty[sk], ((uint32_t)(j / KST) & 1u) ^ 1u);
-                mbar_expect_tx(&k_full[sk], TILE);
-                const uint32_t kd = sbase + OFF_K + sk * TILE;
-                if (b3) {
-                    tma_load_3d(kd, mK, &k_full[sk], g * D, key, 2 * a.layer);
-                    tma_load_3d(kd + SUB, mK, &k_full[sk], g * D + 64, key, 2 * a.layer);
-                } else {
-                    tma_load_2d(kd, mK, &k_full[sk], g * D, key);
-                    tma_load_2d(kd + SUB, mK, &k_full[sk], g * D + 64, key);
-                }
-                trace_pipe(j, 6);
-                mbar_wait(&v_empty[sv], ((uint32_t)(j / VST) & 1u) ^ 1u);
-                mbar_expect_tx(&v_full[sv], TILE);
-                const uint32_t vd = sbase + OFF_V + sv * TILE;
-                if (b3) {
-                    tma_load_3d(vd, mV, &v_full[sv], g * D, key, 2 * a.layer + 1);
-                    tma_load_3d(vd + SUB, mV, &v_full[sv], g * D + 64, key, 2 * a.layer + 1);
-                } else {
-                    tma_load_2d(vd, mV, &v_full[sv], g * D, key);
-                    tma_load_2d(vd + SUB, mV, &v_full[sv], g * D + 64, key);
-                }
-                trace_pipe(j, 7);
+                load_tile(true, j);
+                load_tile(false, j);
             }
         }
-    } else if (warp == 9) {
-        if (lane == 0) {  // ---------------- MMA issuer ----------------
-            auto issue_s = [&](int x, int j) {  // S_x = Q_x . K_j^T
-                const uint32_t qb = sbase + OFF_Q + x * TILE, kb = sbase + OFF_K + (j % KST) * TILE;
+    } else if (warp == WARP_MMA) {
+        // ---------------- MMA issuer (whole warp, elected lane issues) ----------------
+        mbar_wait(q_ready, 0);
+        tc_fence_after();
+        if (lane == 0) trace(0, 8);
+        for (int j = 0; j <= n; ++j) {
+            if (j < n) {  // S(j) = Q . K_j^T into S buffer j & 1 (free: P(j-2) was consumed, so S(j-2) was loaded)
+                const int sk = j % KST;
+                mbar_wait(&k_full[sk], (uint32_t)(j / KST) & 1u);
+                tc_fence_after();
+                const uint32_t kb = sbase + OFF_K + sk * TILE;
+                const uint32_t sd = tmem + T_S + (uint32_t)(j & 1) * 128;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
-                    umma(tmem + x * 256, desc_k(qb + off), desc_k(kb + off), IDESC_S, kk > 0);
+                    umma_ts_elect(sd, tmem + T_Q + kk * 8, desc_k(kb + off), IDESC_S, kk > 0);
                 }
-                umma_commit(&s_full[x]);
-            };
-            // O_x += P_x . V_j, P from TMEM (8 cols = 16 keys per MMA), chunk by chunk as the softmax stores it
-            auto issue_pv = [&](int x, int j) {
-                const uint32_t vb = sbase + OFF_V + (j % VST) * TILE;
+                commit_elect(&s_full[j & 1]);
+                commit_elect(&k_empty[sk]);
+                if (lane == 0) trace(j, 5);
+            }
+            if (j >= 1) {  // O += P(j-1) . V_{j-1}, P from TMEM, chunk by chunk as the softmax releases it
+                const int jp = j - 1, sv = jp % VST;
+                mbar_wait(&v_full[sv], (uint32_t)(jp / VST) & 1u);
+                const uint32_t vb = sbase + OFF_V + sv * TILE;
+                const uint32_t pb = tmem + T_P;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    mbar_wait(&p_full[x * 4 + c], (uint32_t)j & 1u);
+                    mbar_wait(&p_full[(jp & 1) * 4 + c], (uint32_t)(jp >> 1) & 1u);
                     tc_fence_after();
 #pragma unroll
                     for (int k2 = 0; k2 < 2; ++k2) {
                         const int kk = 2 * c + k2;
-                        umma_ts(tmem + x * 256 + 128, tmem + x * 256 + kk * 8, desc_mn(vb + kk * 2048), IDESC_PV,
-                                (j > 0 || kk > 0) ? 1u : 0u);
+                        umma_ts_elect(tmem + T_O, pb + kk * 8, desc_mn(vb + kk * 2048), IDESC_PV, (jp > 0 || kk > 0) ? 1u : 0u);
                     }
                 }
-            };
-            mbar_wait(q_ready, 0);
-            tc_fence_after();
-            trace_pipe(0, 8);
-            if (n > 0) {
-                mbar_wait(&k_full[0], 0);
-                tc_fence_after();
-                issue_s(0, 0);
-                if (hasB) issue_s(1, 0);
-                umma_commit(&k_empty[0]);
+                commit_elect(&v_empty[sv]);
+                commit_elect(&pv_done[jp & 1]);
+                if (lane == 0) trace(jp, 4);
             }
-            for (int j = 0; j < n; ++j) {
-                const bool more = j + 1 < n;
-                const int sk1 = (j + 1) % KST;
-                mbar_wait(&v_full[j % VST], (uint32_t)(j / VST) & 1u);
-                trace_mma(j, 4);
-                tc_fence_after();
-                issue_pv(0, j);
-                trace_pipe(j, 4);
-                trace_mma(j, 5);
-                if (more) {
-                    mbar_wait(&k_full[sk1], (uint32_t)((j + 1) / KST) & 1u);
-                    trace_mma(j, 6);
-                    tc_fence_after();
-                    issue_s(0, j + 1);
-                    trace_mma(j, 7);
-                }
-                if (hasB) {
-                    trace_mma(j, 8);
-                    issue_pv(1, j);
-                    trace_pipe(j, 5);
-                }
-                umma_commit(&v_empty[j % VST]);
-                if (more) {
-                    if (hasB) issue_s(1, j + 1);
-                    umma_commit(&k_empty[sk1]);
-                }
-            }
-            umma_commit(o_done);
         }
+        commit_elect(o_done);
     } else {
-        // ---------------- softmax: warps 0-3 tile A, 4-7 tile B; one thread per row ----------------
-        const int x = warp >> 2;
-        const int r = (warp & 3) * 32 + lane;  // TMEM lane = tile row
-        const int rr = rr0 + x * BR + r;
-        const bool active = rr < rows_total;
-        const int t = active ? rr / group : 0;
-        const int h = g * group + (active ? rr % group : 0);
-        const int my_lo = active ? lop[t] : INT32_MAX;
-        const int my_hi = active ? min(hip[t], Tk - 1) : -1;
+        // ---------------- softmax: warp w owns tile rows [32*(w%4) + 16*(w/4), +16); lane t holds rows ra = .. + t/4
+        // and rb = ra + 8, key columns 8k + 2*(t%4) + {0,1} of every tile (16x256b TMEM access) ----------------
+        const int t0 = lane & 3;
+        const int wr0 = (warp & 3) * 32 + (warp >> 2) * 16;  // first tile row (TMEM lane) of this warp
+        const int ra = wr0 + (lane >> 2), rb = ra + 8;
+        const bool act_a = rr0 + ra < rows_total, act_b = rr0 + rb < rows_total;
+        const int ta = act_a ? (rr0 + ra) / group : 0, tb = act_b ? (rr0 + rb) / group : 0;
+        const int lo_a = act_a ? lop[ta] : INT32_MAX, hi_a = act_a ? min(hip[ta], Tk - 1) : -1;
+        const int lo_b = act_b ? lop[tb] : INT32_MAX, hi_b = act_b ? min(hip[tb], Tk - 1) : -1;
+        constexpr int RPW = BR / SM_WARPS;  // rows per warp for the coalesced Q staging / output copy
         pdl_wait();  // q is produced by the previous kernel
         if (tid == 0) trace(30, 3);
         {
-            // Coalesced staging: warp w of this tile loads its 32 rows two at a time (16 lanes x 16 B per row),
-            // all 16 loads in flight before the swizzled stores.
-            const uint32_t qb = sbase + OFF_Q + x * TILE;
-            const int c = lane & 15;
-            uint4 v[16];
-            // row qr = token * group + head-in-group, walked two rows at a time without per-row division
-            int qr = rr0 + x * BR + (warp & 3) * 32 + (lane >> 4);
-            int qt = qr / group, qi = qr - qt * group;
-            const uint4* qbase = reinterpret_cast<const uint4*>(qp) + c + (int64_t)g * group * (D / 8);
+            // Q rows ra, rb straight into TMEM: column c of a row holds d = 2c, 2c + 1; with the 16x256b shape this
+            // lane supplies columns 8k + 2*t0 + {0,1}, i.e. d = 16k + 4*t0 + 0..3 (one 8-byte load per row and k)
+            const int qra = rr0 + ra, qrb = rr0 + rb;
+            const uint2* pa = reinterpret_cast<const uint2*>(qp + ((int64_t)(qra / group) * a.H + g * group + qra % group) * D) + t0;
+            const uint2* pb = reinterpret_cast<const uint2*>(qp + ((int64_t)(qrb / group) * a.H + g * group + qrb % group) * D) + t0;
+            uint32_t w[32];
 #pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                v[it] = qr < rows_total ? qbase[((int64_t)qt * a.H + qi) * (D / 8)] : make_uint4(0, 0, 0, 0);
-                qr += 2;
-                qi += 2;
-                while (qi >= group) {
-                    qi -= group;
-                    ++qt;
-                }
+            for (int k = 0; k < 8; ++k) {
+                const uint2 va = act_a ? pa[4 * k] : make_uint2(0u, 0u), vb = act_b ? pb[4 * k] : make_uint2(0u, 0u);
+                w[4 * k] = va.x;
+                w[4 * k + 1] = va.y;
+                w[4 * k + 2] = vb.x;
+                w[4 * k + 3] = vb.y;
             }
-            if (tid == 0 && a.trace) trace_at(a.trace, 30, 4 + (v[0].x == 0x7fc00001u && v[15].w == 1u ? 5 : 0));
-#pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                const int row = (warp & 3) * 32 + it * 2 + (lane >> 4);
-                sts128(qb + (c >> 3) * SUB + swz(row, c & 7), v[it]);
-            }
-            fence_async_smem();
+            tmem_st_16x256_x8(tmem + ((uint32_t)wr0 << 16) + T_Q, w);
+            tmem_wait_st();
+            tc_fence_before();
             if (tid == 0) trace(30, 5);
             mbar_arrive(q_ready);
         }
-        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t tS = tmem + lane_base + x * 256, tO = tS + 128;
+        const uint32_t lane_base = (uint32_t)wr0 << 16;
         const float sl2 = a.scale * LOG2E;
-        float m_used = -INFINITY, l = 0.f;
-        const int nx = (x == 1 && !hasB) ? 0 : n;
-        for (int j = 0; j < nx; ++j) {
-            mbar_wait(&s_full[x], (uint32_t)j & 1u);
+        float mu_a = -INFINITY, mu_b = -INFINITY, l_a = 0.f, l_b = 0.f;  // running max (log2 units, lazy) and sum
+        for (int j = 0; j < n; ++j) {
+            const uint32_t b = (uint32_t)(j & 1);
+            mbar_wait(&s_full[b], (uint32_t)(j >> 1) & 1u);
             tc_fence_after();
             if (tid == 0) trace(j, 0);
             if (tid == 128) trace(j, 2);
-            uint32_t s[128];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
+            uint32_t s[64];  // [k = 0..15][ra c0, ra c1, rb c0, rb c1]
+            const uint32_t tS = tmem + lane_base + T_S + b * 128;
+            tmem_ld_16x256_x8(tS, s);
+            tmem_ld_16x256_x8(tS + 64, s + 32);
             tmem_wait_ld();
-            trace_sm(j, 4);
-            const int key0 = ks + j * BK;
-            if (!(key0 >= my_lo && key0 + BK - 1 <= my_hi)) {  // partially visible tile: masked -> -inf
-                const int clo = my_lo - key0, chi = my_hi - key0;
+            if (tid == 0) trace(j, 10);
+            const int key0 = ks + j * BK + 2 * t0;  // key of element (k, e): key0 + 8k + e
+            if (!(ks + j * BK >= max(lo_a, lo_b) && ks + j * BK + BK - 1 <= min(hi_a, hi_b))) {  // partial tile: mask
 #pragma unroll
-                for (int i = 0; i < 128; ++i)
-                    if (i < clo || i > chi) s[i] = __float_as_uint(-INFINITY);
-            }
-            float m0 = __uint_as_float(s[0]), m1 = __uint_as_float(s[1]), m2 = __uint_as_float(s[2]),
-                  m3 = __uint_as_float(s[3]);
+                for (int k = 0; k < 16; ++k)
 #pragma unroll
-            for (int i = 4; i < 124; i += 8) {
-                m0 = max3(m0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
-                m1 = max3(m1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
-                m2 = max3(m2, __uint_as_float(s[i + 4]), __uint_as_float(s[i + 5]));
-                m3 = max3(m3, __uint_as_float(s[i + 6]), __uint_as_float(s[i + 7]));
+                    for (int e = 0; e < 2; ++e) {
+                        const int key = key0 + 8 * k + e;
+                        if (key < lo_a || key > hi_a) s[4 * k + e] = __float_as_uint(-INFINITY);
+                        if (key < lo_b || key > hi_b) s[4 * k + 2 + e] = __float_as_uint(-INFINITY);
+                    }
             }
-            m0 = max3(m0, __uint_as_float(s[124]), __uint_as_float(s[125]));
-            m1 = max3(m1, __uint_as_float(s[126]), __uint_as_float(s[127]));
-            const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-            trace_sm(j, 5);
-            const float mxs = mx == -INFINITY ? -INFINITY : mx * sl2;
-            // lazy rescale. tcgen05.ld/st are warp-collective (.sync.aligned): the whole warp takes the branch
-            // when any of its rows needs it; rows that do not get alpha = 1.
-            bool grow = false;
-            if (m_used == -INFINITY)
-                m_used = mxs;  // first visible keys: O is still all zeros, nothing to rescale
-            else
-                grow = mxs > m_used + RESCALE_LOG2;
-            if (__any_sync(0xffffffffu, grow)) {
-                // O_x is current through PV_x(j-1): it retired before S_x(j) (in-order tensor pipe)
-                const float alpha = grow ? ex2(m_used - mxs) : 1.0f;
+            float ma0 = __uint_as_float(s[0]), ma1 = __uint_as_float(s[1]);
+            float mb0 = __uint_as_float(s[2]), mb1 = __uint_as_float(s[3]);
+#pragma unroll
+            for (int k = 1; k < 15; k += 2) {
+                ma0 = max3(ma0, __uint_as_float(s[4 * k]), __uint_as_float(s[4 * k + 4]));
+                ma1 = max3(ma1, __uint_as_float(s[4 * k + 1]), __uint_as_float(s[4 * k + 5]));
+                mb0 = max3(mb0, __uint_as_float(s[4 * k + 2]), __uint_as_float(s[4 * k + 6]));
+                mb1 = max3(mb1, __uint_as_float(s[4 * k + 3]), __uint_as_float(s[4 * k + 7]));
+            }
+            float mxa = max3(ma0, ma1, fmaxf(__uint_as_float(s[60]), __uint_as_float(s[61])));
+            float mxb = max3(mb0, mb1, fmaxf(__uint_as_float(s[62]), __uint_as_float(s[63])));
+            // the row max over the quad (the 4 lanes sharing the row)
+            mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 1));
+            mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 1));
+            mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 2));
+            mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 2));
+            const float msa = mxa == -INFINITY ? -INFINITY : mxa * sl2;
+            const float msb = mxb == -INFINITY ? -INFINITY : mxb * sl2;
+            if (tid == 0) trace(j, 11);
+            // lazy rescale: only when a row max grows by more than 2^8 (identical decisions in the 4 lanes of a row).
+            // tcgen05.ld/st are warp-collective, so the whole warp takes the branch; rows that keep their max get 1.
+            bool ga = false, gb = false;
+            if (mu_a == -INFINITY) mu_a = msa;  // first visible keys: O is still all zeros
+            else ga = msa > mu_a + RESCALE_LOG2;
+            if (mu_b == -INFINITY) mu_b = msb;
+            else gb = msb > mu_b + RESCALE_LOG2;
+            if (__any_sync(0xffffffffu, ga || gb)) {
+                // O must be current through PV(j-1) (j >= 1 here: a max was set by an earlier tile). This warp owns its
+                // 16 O rows outright; PV(j) starts only after every warp released its P(j) chunks, i.e. after this.
+                mbar_wait(&pv_done[(j - 1) & 1], (uint32_t)((j - 1) >> 1) & 1u);
+                tc_fence_after();
+                const float al_a = ga ? ex2(mu_a - msa) : 1.0f, al_b = gb ? ex2(mu_b - msb) : 1.0f;
 #pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < 2; ++c) {
                     uint32_t w[32];
-                    tmem_ld32(tO + c * 32, w);
+                    const uint32_t tO = tmem + lane_base + T_O + c * 64;
+                    tmem_ld_16x256_x8(tO, w);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
-                    tmem_st32(tO + c * 32, w);
+                    for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * ((i & 2) ? al_b : al_a));
+                    tmem_st_16x256_x8(tO, w);
                 }
                 tmem_wait_st();
-                if (grow) {
-                    l *= alpha;
-                    m_used = mxs;
+                if (ga) {
+                    l_a *= al_a;
+                    mu_a = msa;
+                }
+                if (gb) {
+                    l_b *= al_b;
+                    mu_b = msb;
                 }
             }
-            const float moff = m_used == -INFINITY ? 0.f : m_used;  // nothing visible yet -> all p = 0
-            const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(-moff, -moff);
-            uint64_t accv = 0;  // (+0, +0)
+            // the P buffer was last read by PV(j-1)
+            if (j >= 1) {
+                mbar_wait(&pv_done[(j - 1) & 1], (uint32_t)((j - 1) >> 1) & 1u);
+                tc_fence_after();
+            }
+            const float oa = mu_a == -INFINITY ? 0.f : mu_a, ob = mu_b == -INFINITY ? 0.f : mu_b;  // none visible: p = 0
+            const uint64_t sc2 = pk2(sl2, sl2), na2 = pk2(-oa, -oa), nb2 = pk2(-ob, -ob);
+            uint64_t acca = 0, accb = 0;  // (+0, +0)
+            const uint32_t tP = tmem + lane_base + T_P;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {  // 32 keys per chunk -> 16 P columns (bf16 pairs), stored as soon as done
-                // every pair's exponent first (independent MUFU / FMA-pipe work), then conversions and a
-                // log-depth sum: no serial accumulation chain behind the MUFU latency
-                uint64_t pv[16];
+            for (int c = 0; c < 4; ++c) {  // chunk c = keys [32c, 32c+32) = k in [4c, 4c+4): 16 P columns, 8 regs
+                uint64_t pv[8];            // [kk][row a, row b] pairs
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int e = c * 32 + 2 * i;
-                    const uint64_t xv = fma2(pk2(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sc2, nm2);
-                    if (i < kPolyPairs) {
+                for (int i = 0; i < 8; ++i) {
+                    const int k = 4 * c + (i >> 1), rsel = i & 1;
+                    const uint64_t xv = fma2(pk2(__uint_as_float(s[4 * k + 2 * rsel]), __uint_as_float(s[4 * k + 2 * rsel + 1])),
+                                             sc2, rsel ? nb2 : na2);
+                    if (((c * 8 + i) & 15) < kPolyPairs) {  // POLY_PAIRS of every 16 pairs on the FMA pipe
                         pv[i] = ex2_poly2(xv);
                     } else {
                         float x0, x1;
@@ -629,75 +674,77 @@ __global__ void __launch_bounds__(THREADS, 1)
                         pv[i] = pk2(ex2(x0), ex2(x1));
                     }
                 }
-                uint32_t pk[16];
+                uint32_t pk[8];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
+                for (int i = 0; i < 8; ++i) {
                     float p0, p1;
                     up2(pv[i], p0, p1);
                     pk[i] = bf16x2_bits(p0, p1);
                 }
-                tmem_st16(tS + c * 16, pk);
-#pragma unroll
-                for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-                    for (int i = 0; i < w; ++i) pv[i] = add2(pv[i], pv[i + w]);
-                accv = add2(accv, pv[0]);
+                if (tid == 0 && c == 0) trace(j, 12);
+                tmem_st_16x128_x4(tP + c * 16, pk);
+                acca = add2(acca, add2(add2(pv[0], pv[2]), add2(pv[4], pv[6])));
+                accb = add2(accb, add2(add2(pv[1], pv[3]), add2(pv[5], pv[7])));
                 tmem_wait_st();
                 tc_fence_before();
-                mbar_arrive(&p_full[x * 4 + c]);  // the PV MMA on these 32 keys may start
-                if (c == 1) trace_sm(j, 6);
-                if (c == 3) trace_sm(j, 7);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[b * 4 + c]);  // the PV MMA on these 32 keys may start
+                if (tid == 0 && c == 0) trace(j, 13);
             }
             float a0, a1;
-            up2(accv, a0, a1);
-            l += a0 + a1;
-            trace_sm(j, 8);
+            up2(acca, a0, a1);
+            l_a += a0 + a1;
+            up2(accb, a0, a1);
+            l_b += a0 + a1;
             if (tid == 0) trace(j, 1);
             if (tid == 128) trace(j, 3);
         }
-        if (nx > 0) {
+        // row sums over the quad
+        l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
+        l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+        l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+        l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
+        if (n > 0) {
             mbar_wait(o_done, 0);
             tc_fence_after();
         }
         if (tid == 0) trace(31, 0);
-        // ---- epilogue: O/l as bf16, staged row-per-thread into the (now idle) Q_x tile with the SW128 chunk
-        // swizzle (conflict-free), then copied out coalesced: 16 lanes x 16 B per 256-byte row ----
-        const bool degenerate = active && l == 0.f;
-        const float inv = l > 0.f ? 1.0f / l : 0.f;
-        const uint32_t stage = sbase + OFF_Q + x * TILE;
+        // ---- epilogue: O/l as bf16 pairs into the (now idle) Q tile with the SW128 chunk swizzle (a quad writes one
+        // 16-byte chunk of a row: conflict-free), then copied out coalesced: 16 lanes x 16 B per 256-byte row ----
+        const float inv_a = l_a > 0.f ? 1.0f / l_a : 0.f, inv_b = l_b > 0.f ? 1.0f / l_b : 0.f;
+        const uint32_t stage = sbase + OFF_Q;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
             uint32_t w[32];
-            if (nx > 0) {
-                tmem_ld32(tO + c * 32, w);  // warp-collective
+            if (n > 0) {
+                tmem_ld_16x256_x8(tmem + lane_base + T_O + c * 64, w);  // warp-collective
                 tmem_wait_ld();
             } else {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) w[i] = 0u;
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int chunk = c * 4 + k;  // 16-byte chunk (8 columns) of the 256-byte row
-                sts128(stage + (chunk >> 3) * SUB + swz(r, chunk & 7),
-                       make_uint4(bf16x2_bits(__uint_as_float(w[8 * k + 0]) * inv, __uint_as_float(w[8 * k + 1]) * inv),
-                                  bf16x2_bits(__uint_as_float(w[8 * k + 2]) * inv, __uint_as_float(w[8 * k + 3]) * inv),
-                                  bf16x2_bits(__uint_as_float(w[8 * k + 4]) * inv, __uint_as_float(w[8 * k + 5]) * inv),
-                                  bf16x2_bits(__uint_as_float(w[8 * k + 6]) * inv, __uint_as_float(w[8 * k + 7]) * inv)));
+            for (int kk = 0; kk < 8; ++kk) {
+                const int ch = c * 8 + kk;  // 16-byte chunk (8 columns) of the 256-byte row
+                const uint32_t off = (ch >> 3) * SUB + 4 * t0;
+                sts32(stage + off + swz(ra, ch & 7),
+                      bf16x2_bits(__uint_as_float(w[4 * kk]) * inv_a, __uint_as_float(w[4 * kk + 1]) * inv_a));
+                sts32(stage + off + swz(rb, ch & 7),
+                      bf16x2_bits(__uint_as_float(w[4 * kk + 2]) * inv_b, __uint_as_float(w[4 * kk + 3]) * inv_b));
             }
         }
-        if (tid == 0) trace(31, 4);
-        named_bar(2 + x, BR);  // this tile's 128 rows are staged
+        named_bar(1, SM_THREADS);  // the whole tile is staged
         if (tid == 0) trace(31, 5);
         const int gid = blockIdx.y * gridDim.x + blockIdx.x;
         const int ngroups = gridDim.x * gridDim.y;
-        // workspace of split s, row group gid: rows [256][D] bf16 (contiguous) and (m, l) [256]
-        const int64_t wrow0 = ((int64_t)split * ngroups + gid) * RG;
+        // workspace of split s, row group gid: rows [BR][D] bf16 (contiguous) and (m, l) [BR]
+        const int64_t wrow0 = ((int64_t)split * ngroups + gid) * BR;
         {
             const int cc = lane & 15;
-#pragma unroll 4
-            for (int it = 0; it < 16; ++it) {
-                const int row = (warp & 3) * 32 + it * 2 + (lane >> 4);
-                const int qr = rr0 + x * BR + row;
+#pragma unroll
+            for (int it = 0; it < RPW / 2; ++it) {
+                const int row = warp * RPW + it * 2 + (lane >> 4);
+                const int qr = rr0 + row;
                 uint4 v;
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -706,22 +753,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (qr < rows_total)
                         reinterpret_cast<uint4*>(outp + ((int64_t)(qr / group) * a.H + g * group + qr % group) * D)[cc] = v;
                 } else {
-                    reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.ws_o) + (wrow0 + x * BR + row) * D)[cc] = v;
+                    reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.ws_o) + (wrow0 + row) * D)[cc] = v;
                 }
             }
         }
         if (tid == 0) trace(31, 6);
-        if (a.splits == 1) {
-            if (degenerate) atomicOr(a.err, 8);  // DegenerateRowError (numerics.cpp:39-42)
-        } else {
-            reinterpret_cast<float2*>(a.ws_ml)[wrow0 + x * BR + r] = make_float2(active ? m_used : -INFINITY, l);
-            if (tid == 0) trace(31, 1);
+        if (t0 == 0) {
+            if (a.splits == 1) {
+                if ((act_a && l_a == 0.f) || (act_b && l_b == 0.f)) atomicOr(a.err, 8);  // DegenerateRowError (numerics.cpp:39-42)
+            } else {
+                float2* ml = reinterpret_cast<float2*>(a.ws_ml) + wrow0;
+                ml[ra] = make_float2(act_a ? mu_a : -INFINITY, l_a);
+                ml[rb] = make_float2(act_b ? mu_b : -INFINITY, l_b);
+                if (tid == 0) trace(31, 1);
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (tid == 0 && a.trace && cta_lin < TRACE_CTAS) a.trace[TRACE_CTA0 + 2 * cta_lin + 1] = globaltimer_ns();
-    if (warp == 9) {
+    if (warp == WARP_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
@@ -937,6 +988,8 @@ void attn_trace_enable(bool on, unsigned long long** host_view) {
     if (host_view) *host_view = buf;
 }
 
+int attn_trace_words() { return TRACE_CTA0 + 2 * TRACE_CTAS; }
+
 bool attention_tc_supported(int d, DT dt) { return d == 128 && dt == DT::BF16; }
 
 int attn_tc_row_groups(int Tq, int H, int Hkv) { return ((Tq * (H / Hkv) + RG - 1) / RG) * Hkv; }
@@ -950,7 +1003,7 @@ size_t attn_tc_workspace_floats(int Tq, int H, int Hkv, int splits, size_t* ml_o
 
 int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms) {
     const int groups = attn_tc_row_groups(Tq, H, Hkv);
-    if (groups * 2 > num_sms) return 1;  // already >= half a wave of row groups: no split-K
+    if (groups * 2 > num_sms) return 1;  // already >= half a wave of row tiles: no split-K
     int s = num_sms / groups;            // one wave (1 CTA / SM)
     const int max_by_keys = ((Tk + BK - 1) / BK + 1) / 2;  // >= 2 key tiles per split
     if (s > max_by_keys) s = max_by_keys;

@@ -535,7 +535,10 @@ struct tkv_engine {
 
     bool use_tc() const { return dt == DT::BF16 && !(opts.flags & TKV_FLAG_SIMT_GEMM); }
 
-    int batch_attn_splits = 1;  // TKV_BATCH_ATTN_SPLITS (0 = attn_tc_batch_pick_splits; measured on par)
+#ifndef TKV_BATCH_SPLITS_DEFAULT
+#define TKV_BATCH_SPLITS_DEFAULT 1
+#endif
+    int batch_attn_splits = TKV_BATCH_SPLITS_DEFAULT;  // TKV_BATCH_ATTN_SPLITS (0 = attn_tc_batch_pick_splits)
 
     // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits. With swiglu_act, a tcgen05 GEMM whose
     // K range fits one CTA writes silu(gate)*up straight to swiglu_act and returns 0.
@@ -753,13 +756,13 @@ void tkv_engine::forward(const Fwd& f) {
             // one launch for the whole batch; split-K only to fill the last wave of (request, kv head, row group)
             // CTAs, merged by a request-aware combine
             const int n_req = (int)f.reqs.size();
-            const int groups_x = (f.batch_max_n * (int)(H / Hkv) + 255) / 256;
+            const int groups_x = (f.batch_max_n * (int)(H / Hkv) + kAttnTcRows - 1) / kAttnTcRows;
             int bs = batch_attn_splits > 0 ? batch_attn_splits
                                            : attn_tc_batch_pick_splits(groups_x * (int)Hkv * n_req, f.batch_min_keys,
                                                                        num_sms);
             AttnWork bws;
             if (bs > 1) {
-                const size_t rows = (size_t)bs * groups_x * Hkv * n_req * 256;
+                const size_t rows = (size_t)bs * groups_x * Hkv * n_req * kAttnTcRows;
                 attn_ws.ensure((rows * d / 2 + rows * 2) * sizeof(float));
                 bws.o = attn_ws.as<float>();
                 bws.ml = bws.o + rows * d / 2;
@@ -2180,7 +2183,7 @@ tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int6
         int64_t row_groups = 0;
         int max_n = 0;
         for (const auto& r : f.reqs) {
-            row_groups += ((int64_t)r.n * group + 255) / 256 * e->Hkv;
+            row_groups += ((int64_t)r.n * group + kAttnTcRows - 1) / kAttnTcRows * e->Hkv;
             max_n = std::max(max_n, r.n);
         }
         if (e->dt == DT::BF16 && !(e->opts.flags & TKV_FLAG_SIMT_ATTN) && attention_tc_supported((int)e->d, e->dt) &&
@@ -2847,7 +2850,7 @@ tkv_status tkv_debug_attn_trace(int on, uint64_t* out, int64_t capacity) {
         if (out) {  // read back the last trace
             attn_trace_enable(true, &buf);
             TKV_CUDA(cudaDeviceSynchronize());
-            TKV_CUDA(cudaMemcpy(out, buf, (size_t)std::min<int64_t>(capacity, 320 + 2048) * 8, cudaMemcpyDeviceToHost));
+            TKV_CUDA(cudaMemcpy(out, buf, (size_t)std::min<int64_t>(capacity, attn_trace_words()) * 8, cudaMemcpyDeviceToHost));
         }
         attn_trace_enable(on != 0, &buf);
     });

@@ -166,6 +166,7 @@ struct L2Prefetch {
 // SIMT; split-K partials (bf16 O/l) are merged by a PDL-launched combine kernel. Key rows
 // < kv_ready were written before the current forward began and are loaded before griddepcontrol.wait.
 bool attention_tc_supported(int d, DT dt);
+constexpr int kAttnTcRows = 128;  // (token, head) rows per CTA = rows per split-workspace row group
 // Batched query prefill: one launch covers every request (rows of request r are tokens [tok0, tok0 + n) of the
 // forward; its keys are [0, row0 + n) of its own cache, read through a 3-D tensor map over the cache
 // [2L][row0 + n][kv_dim] encoded by attn_tc_cache_map). No split-K: the batch supplies the CTAs.
@@ -178,6 +179,7 @@ void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* m
                                cudaStream_t s, int splits = 1, const AttnWork& ws = AttnWork{});
 int attn_tc_batch_pick_splits(int ctas, int min_keys, int num_sms);
 void attn_trace_enable(bool on, unsigned long long** device_buf);  // debug timeline of CTA (0,0,0)
+int attn_trace_words();  // [32 tiles][16 events] clock64 of CTA (0,0,0), then [1024 CTAs][entry, exit] globaltimer
 int attn_tc_row_groups(int Tq, int H, int Hkv);
 // workspace of the tcgen05 kernel's split merge (floats); ws.ml = ws.o + *ml_offset
 size_t attn_tc_workspace_floats(int Tq, int H, int Hkv, int splits, size_t* ml_offset);

@@ -18,10 +18,10 @@ hi = (P + np.arange(Q)).astype(np.int32)
 T._check(L.tkv_debug_attn_trace(1, None, 0))
 for _ in range(3):
     T.debug_attention(q, k, v, lo, hi, H, Hkv, d, dtype="bf16")
-out = np.zeros(320 + 2048, np.uint64)
-T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 320 + 2048))
-ev = out[:320].reshape(32, 10).astype(np.int64)
-cta = out[320:].reshape(1024, 2).astype(np.int64)
+out = np.zeros(512 + 2048, np.uint64)
+T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 512 + 2048))
+ev = out[:512].reshape(32, 16).astype(np.int64)
+cta = out[512:].reshape(1024, 2).astype(np.int64)
 cta = cta[cta[:, 0] > 0]
 if len(cta):
     s0 = cta[:, 0].min()
@@ -31,19 +31,16 @@ if len(cta):
     order = np.argsort(st)
     print("start times (us) by launch index, every 12th:", np.round(st[::12], 2).tolist())
 t0 = ev[ev > 0].min()
-import os
-names_sm = ["smA:S ready", "smA:P arrive", "smB:S ready", "smB:P arrive", "smA:ld done", "smA:max done", "smA:chunk1", "smA:chunk3", "smA:st done"]
-names = ["smA:S ready", "smA:P arrive", "smB:S ready", "smB:P arrive", "mma:PV_A issued", "mma:PV_B issued",
-         "tma:K(j) issue", "tma:V(j) issue", "mma:Q ready"]
+names = ["h0:S ready", "h0:P released", "hN:S ready", "hN:P released", "mma:PV(j) issued", "mma:S(j) issued",
+         "tma:K(j) issue", "tma:V(j) issue", "mma:Q ready", "-", "t0:ld done", "t0:max xchg", "t0:exp c0", "t0:arrive c0",
+         "t0:exp c1", "t0:arrive c1"]
+EV = [0, 10, 11, 12, 13, 14, 15, 1, 2, 3, 5, 4, 6, 7, 8]
 print("kernel entry at", ev[0, 9] - t0, "cycles")
+print("previous kernel done (softmax pdl_wait returned) %d, Q staged %d" % (ev[30, 3] - t0, ev[30, 5] - t0))
+print("epilogue: o_done seen %d, staged %d, copied out %d, (m, l) written %d" % (ev[31, 0] - t0, ev[31, 5] - t0, ev[31, 6] - t0, ev[31, 1] - t0))
 print("cycles since first event (CTA 0); rows = KV tile j")
-if os.environ.get("TRACE_SM") == "1": names = names_sm
-if os.environ.get("TRACE_SM") == "2": names = names[:4] + ["mma:P_A seen", "mma:PV_A issued", "mma:K(j+1) seen", "mma:S_A(j+1) iss", "mma:P_B seen"]
-print("j   " + " ".join(f"{n:>16s}" for n in names))
-print("epilogue: o_done seen %d, partials written %d, grid sync passed %d, merge done %d" % tuple(ev[31, e] - t0 for e in range(4)))
-print("  merge: first partial load back %d, old-line load back %d" % (ev[30, 1] - t0, ev[30, 2] - t0))
-print("  staged %d, stage barrier %d, copied out %d, merge loads issued %d, merge math done %d" % (ev[31, 4] - t0, ev[31, 5] - t0, ev[31, 6] - t0, ev[30, 0] - t0, ev[31, 7] - t0))
+print("j  " + " ".join(f"{names[e][-13:]:>13s}" for e in EV))
 for j in range(30):
-    if (ev[j, :9] == 0).all():
+    if (ev[j, :16] == 0).all():
         continue
-    print(f"{j:<3d} " + " ".join(f"{(ev[j, e] - t0) if ev[j, e] else -1:16d}" for e in range(9)))
+    print(f"{j:<2d} " + " ".join(f"{(ev[j, e] - t0) if ev[j, e] else -1:13d}" for e in EV))

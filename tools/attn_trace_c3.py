@@ -22,10 +22,10 @@ for _ in range(2):
     eng.prefill_query_batch(ctxs, queries)
     for c in ctxs:
         c.close()
-out = np.zeros(320 + 2048, np.uint64)
-T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 320 + 2048))
-ev = out[:320].reshape(32, 10).astype(np.int64)
-cta = out[320:].reshape(1024, 2).astype(np.int64)
+out = np.zeros(512 + 2048, np.uint64)
+T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 512 + 2048))
+ev = out[:512].reshape(32, 16).astype(np.int64)
+cta = out[512:].reshape(1024, 2).astype(np.int64)
 idx = np.nonzero(cta[:, 0] > 0)[0]
 cta = cta[idx]
 s0 = cta[:, 0].min()

@@ -18,10 +18,10 @@ L = T.lib()
 for _ in range(3):
     with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
         eng.prefill_query(ctx, query)
-out = np.zeros(320 + 2048, np.uint64)
-T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 320 + 2048))
-ev = out[:320].reshape(32, 10).astype(np.int64)
-cta = out[320:].reshape(1024, 2).astype(np.int64)
+out = np.zeros(512 + 2048, np.uint64)
+T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 512 + 2048))
+ev = out[:512].reshape(32, 16).astype(np.int64)
+cta = out[512:].reshape(1024, 2).astype(np.int64)
 cta = cta[cta[:, 0] > 0]
 s0 = cta[:, 0].min()
 st, en = (cta[:, 0] - s0) / 1e3, (cta[:, 1] - s0) / 1e3
