@@ -26,8 +26,9 @@ out = np.zeros(512 + 2048, np.uint64)
 T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 512 + 2048))
 ev = out[:512].reshape(32, 16).astype(np.int64)
 cta = out[512:].reshape(1024, 2).astype(np.int64)
-idx = np.nonzero(cta[:, 0] > 0)[0]
-cta = cta[idx]
+ncta = ((Q * 7 + 127) // 128) * 4 * B  # this launch's grid (row tiles x kv heads x requests), no split-K
+cta = cta[:ncta]
+cta = cta[cta[:, 0] > 0]
 s0 = cta[:, 0].min()
 st, en = (cta[:, 0] - s0) / 1e3, (cta[:, 1] - s0) / 1e3
 dur = en - st
@@ -38,5 +39,9 @@ for q in (0.1, 0.5, 0.9, 1.0):
     print(f"  end time quantile {q}: {np.quantile(en, q):.1f} us")
 print("duration by linear CTA index (every 16th):", np.round(dur[::16], 1).tolist())
 t0 = ev[0, 9]
-print("CTA 0: entry->q staged %d, first S ready %d, last round S ready %s, o_done %d, written %d cycles"
-      % (ev[30, 5] - t0, ev[0, 0] - t0, [int(ev[j, 0] - t0) for j in range(25, 30)], ev[31, 0] - t0, ev[31, 1] - t0))
+print("CTA 0: entry->Q staged %d, first S ready %d, o_done %d cycles" % (ev[30, 5] - t0, ev[0, 0] - t0, ev[31, 0] - t0))
+s_ready = ev[:30, 0]
+per = np.diff(s_ready[s_ready > 0])
+print("per-tile period (S ready to S ready), cycles: median %d, tiles 1-29: %s" % (np.median(per), per.tolist()))
+sm = ev[:30, 1] - ev[:30, 0]
+print("softmax S ready -> P released, cycles: median %d" % np.median(sm[ev[:30, 1] > 0]))

@@ -1,7 +1,8 @@
 #!/bin/bash
-# Cost attribution: TTFT with kernel classes dropped (TKV_TIMING_SKIP bitmask; results numerically invalid).
+# Cost attribution of the C2 turbo step: p50 with kernel classes dropped (TKV_TIMING_SKIP bitmask; results
+# numerically invalid), through the TUNING build (make TUNING=1 BUILD=.../build_tuning LIB=.../libtkv_tuning.so).
 # 1 = residual after O-proj, 2 = residual after down-proj, 4 = qkv epilogue, 8 = attention
+export TKV_LIB_PATH=${TKV_LIB_PATH:-paper_2410_07590_b200/libtkv_tuning.so}
 for m in "$@"; do
-  TKV_TIMING_SKIP=$m timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --naive-reps 1 --turbo-only 2>/dev/null | tail -1 | \
-    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('skip', $m, round(d['p50_ttft_ms'],3))"
+  echo -n "skip $m: "; TKV_TIMING_SKIP=$m timeout 300 python tools/c2_step.py 2>/dev/null | tail -1
 done
