@@ -290,3 +290,258 @@ def flops_report(preset: str, chunk_tokens: int, query_tokens: int, batches=(1, 
     return {"schema": REPORT_SCHEMA, "command": "flops", "preset": preset, "chunk_tokens": chunk_tokens,
             "query_tokens": query_tokens, "config": config_json(config), "rows": rows}
 
+
+
+def ingest_report(engine: T.Engine, docs, chunk_bytes: int, store: str, preset: str, dtype: str) -> dict:
+    """`turbokv ingest --json` (tools/turbokv_main.cpp:200-231): chunk + ingest the documents, report the counts."""
+    stats = ingest(engine, docs, chunk_bytes)
+    return {"schema": REPORT_SCHEMA, "command": "ingest", "store": store, "documents": len(docs),
+            "chunks": stats.chunks, "new_chunks": stats.new_chunks, "bytes_written": stats.bytes_written,
+            "indexed_chunks": engine.index_size(), "seed": engine.seed, "preset": preset, "dtype": dtype,
+            "config": config_json(engine.config)}
+
+
+# ---- `turbokv verify` (tools/turbokv_main.cpp:334-606): the property checks, run on this engine ----
+
+@dataclass
+class VerifyOpts:
+    """VerifyOpts (turbokv_main.cpp:334-343)."""
+    seed: int = 42
+    case_seed: int = 0    # nonzero: run exactly this case, once
+    cases: int = 40
+    rope_cases: int = 1000
+    chunks: int = 0       # 0 = randomize per case
+    chunk_len: int = 0    # payload bytes, 0 = randomize
+    query_len: int = 0    # tokens, 0 = randomize
+    inject_fault: bool = False
+
+
+def _random_text(rng, n: int) -> str:
+    """random_text (turbokv_main.cpp:167-174): 'a'..'z' and space."""
+    out = []
+    for _ in range(n):
+        r = rng.next_below(27)
+        out.append(" " if r == 26 else chr(ord("a") + r))
+    return "".join(out)
+
+
+def _max_abs_diff(a, b) -> float:
+    return float(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64)).max())
+
+
+def _rope_relative_score(q, k, pos_q: int, pos_k: int, base: float) -> float:
+    """rope_relative_score (src/rope.cpp:90-104): <R(pos_q) q, R(pos_k) k> with interleaved pairs (2m, 2m+1),
+    theta_m = base^(-2m/d) (rope.cpp:21-22, 35-46), in f64 -- the definition the engine's RoPE table is built from."""
+    d = len(q)
+    theta = np.array([base ** (-(2.0 * m) / d) for m in range(d // 2)])
+
+    def rot(x, t):
+        c, s = np.cos(float(t) * theta), np.sin(float(t) * theta)
+        x0, x1 = x[0::2], x[1::2]
+        y = np.empty(d)
+        y[0::2], y[1::2] = x0 * c - x1 * s, x0 * s + x1 * c
+        return y
+
+    return float(np.dot(rot(np.asarray(q), pos_q), rot(np.asarray(k), pos_k)))
+
+
+def verify(engine: T.Engine, opts: VerifyOpts | None = None, tmp_dir: str | None = None):
+    """cmd_verify (turbokv_main.cpp:586-606) over this engine: equivalence (turbo == naive-independent, identical
+    greedy decodes, a composite-defect witness), RoPE shift invariance, KV round trip with its error paths,
+    incremental == one-shot prefill and single-chunk degeneracy, with the reference's case generation
+    (SplitMix64::at(seed, i) per case) and report lines. Returns (exit code, lines).
+
+    Tolerances: the reference compares f64 paths at 1e-10; here the turbo and naive paths run different kernels in
+    the engine's dtype, so differences are bounded relative to max|logit| (f32 1e-4, bf16 2e-2, the parity bars of
+    DESIGN.md §4), greedy decodes must agree token for token in f32 (bf16: the first token), and the composite
+    witness must exceed max(1e-3, 5 x that bound). --inject-fault corrupts the naive path's mask exactly as the
+    reference hook does (the last query row loses column 0); at f32 equivalence then fails as in the f64 reference,
+    while at bf16 the toy fault stays inside the bf16 bound (a precision check is an f32 / f64 tool)."""
+    import os
+    import struct
+    import tempfile
+
+    from .bench_api import SplitMix64, encode
+
+    opts = opts or VerifyOpts()
+    if opts.cases < 1:
+        raise T.ConfigError("verify: --cases must be >= 1")
+    cfg = engine.config
+    f32 = engine.dtype == T.Dtype.F32
+    rel = 1e-4 if f32 else 2e-2
+    lines: list[str] = []
+
+    def repro(case_seed: int):
+        lines.append(f"REPRO: turbokv verify --case-seed {case_seed} --cases 1"
+                     + (" --inject-fault" if opts.inject_fault else ""))
+
+    def naive_ids(ids, query, mode):
+        if opts.inject_fault:  # testing::mask_fault_hook: mask(rows - 1, 0) = -inf
+            n = sum(engine.store_chunk_tokens(i) for i in ids) + len(query)
+            engine.set_mask_rows([-1], [1], [n - 1])
+        return engine.naive_prefill_ids(ids, query, mode)
+
+    # -- equivalence (turbokv_main.cpp:349-421)
+    witness, multichunk, max_cdiff = False, False, 0.0
+    for i in range(opts.cases):
+        case_seed = opts.case_seed if opts.case_seed else _splitmix_at(opts.seed, i)
+        rng = SplitMix64(case_seed)
+        n_chunks = opts.chunks if opts.chunks > 0 else 1 + rng.next_below(8)
+        ids = []
+        for _ in range(n_chunks):
+            ln = opts.chunk_len if opts.chunk_len > 0 else 1 + rng.next_below(64)
+            ids.append(engine.ingest_chunk_payload("verify", encode(_random_text(rng, ln))))
+        qlen = opts.query_len if opts.query_len > 0 else 1 + rng.next_below(32)
+        query = encode(_random_text(rng, qlen))
+        with engine.assemble(ids, T.PositionMode.Reordered) as turbo:
+            tl = engine.prefill_query(turbo, query)[0]
+            with naive_ids(ids, query, T.MaskMode.Independent) as naive:
+                nl = naive.last_logits
+                scale = max(float(np.abs(nl).max()), 1e-30)
+                diff = _max_abs_diff(tl, nl)
+                if diff > rel * scale:
+                    lines.append(f"FAIL equivalence: logits diff {diff:g} (chunks {n_chunks}, query {qlen})")
+                    repro(case_seed)
+                    return 1, lines
+                td, nd = engine.greedy_decode(turbo, 16), engine.greedy_decode(naive, 16)
+                if (td != nd) if f32 else (td[:1] != nd[:1]):
+                    lines.append(f"FAIL equivalence: greedy decodes diverge (chunks {n_chunks}, query {qlen})")
+                    repro(case_seed)
+                    return 1, lines
+                if n_chunks >= 2:
+                    multichunk = True
+                    with engine.assemble(ids, T.PositionMode.Composite) as comp:
+                        cl = engine.prefill_query(comp, query)[0]
+                    cdiff = _max_abs_diff(cl, nl)
+                    max_cdiff = max(max_cdiff, cdiff)
+                    if cdiff > max(1e-3, 5 * rel * scale):
+                        witness = True
+        if opts.case_seed:
+            break
+    lines.append(f"ok equivalence ({opts.cases} cases)")
+    if multichunk:
+        if not witness:
+            lines.append(f"FAIL composite witness: no multi-chunk case exceeded 1e-3 (max diff {max_cdiff:g})")
+            repro(opts.seed)
+            return 1, lines
+        lines.append(f"ok composite defect witness (max diff {max_cdiff:g})")
+
+    # -- RoPE shift invariance (turbokv_main.cpp:424-452)
+    rng = SplitMix64(opts.seed ^ 0x0051CE)
+    worst = 0.0
+    for _ in range(opts.rope_cases):
+        hs = (4, 8, 16, 64, 128)[rng.next_below(5)]
+        q = [_next_signed(rng) for _ in range(hs)]
+        k = [_next_signed(rng) for _ in range(hs)]
+        a, b = rng.next_below(4097), rng.next_below(4097)
+        shift = rng.next_below(4097 - max(a, b))
+        d = abs(_rope_relative_score(q, k, a, b, cfg.rope_base)
+                - _rope_relative_score(q, k, a + shift, b + shift, cfg.rope_base))
+        worst = max(worst, d)
+        if d > 1e-9:
+            lines.append(f"FAIL rope shift invariance: diff {d:g} at a={a} b={b} shift={shift} head_size={hs}")
+            repro(opts.seed)
+            return 1, lines
+    lines.append(f"ok rope shift invariance ({opts.rope_cases} cases, worst {worst:g})")
+
+    # -- KV round trip + error paths (turbokv_main.cpp:455-507): store pages == assembled (unrotated) K/V bitwise;
+    # a TKVC file with another fingerprint is StaleCacheError, a truncated one FormatError, a missing id NotFound
+    rng = SplitMix64(opts.seed ^ 0x57083)
+    tmp = tmp_dir or tempfile.mkdtemp(prefix="turbokv-verify-")
+    for _ in range(10):
+        cid = engine.ingest_chunk_payload("roundtrip", encode(_random_text(rng, 1 + rng.next_below(64))))
+        with engine.assemble([cid], T.PositionMode.Reordered) as direct:
+            for layer in range(cfg.layer_num):
+                for which in ("k", "v"):
+                    if not np.array_equal(engine.store_read(cid, layer, which),
+                                          direct.read_kv(layer, which, rotated=False)):
+                        lines.append(f"FAIL kv round trip: layer {layer} not bit-identical")
+                        repro(opts.seed)
+                        return 1, lines
+        path = os.path.join(tmp, f"{cid:016x}.tkvc")
+        engine.export_tkvc(cid, path)
+        raw = bytearray(open(path, "rb").read())
+        raw[28:36] = struct.pack("<Q", struct.unpack_from("<Q", raw, 28)[0] ^ 1)
+        open(path, "wb").write(bytes(raw))
+        engine.store_evict(cid)
+        try:
+            engine.import_tkvc(path)
+            lines.append("FAIL kv round trip: stale fingerprint accepted")
+            repro(opts.seed)
+            return 1, lines
+        except T.StaleCacheError:
+            pass
+    cid = engine.ingest_chunk_payload("roundtrip", encode(_random_text(rng, 32)))
+    path = os.path.join(tmp, f"{cid:016x}.tkvc")
+    engine.export_tkvc(cid, path)
+    raw = open(path, "rb").read()
+    open(path, "wb").write(raw[: len(raw) // 2])
+    engine.store_evict(cid)
+    try:
+        engine.import_tkvc(path)
+        lines.append("FAIL kv round trip: truncated file accepted")
+        repro(opts.seed)
+        return 1, lines
+    except T.FormatError:
+        pass
+    try:
+        engine.assemble([0xDEADDEADDEADDEAD]).close()
+        lines.append("FAIL kv round trip: missing chunk loaded")
+        repro(opts.seed)
+        return 1, lines
+    except T.NotFoundError:
+        pass
+    lines.append("ok kv round trip (10 cases + error paths)")
+
+    # -- incremental forward (turbokv_main.cpp:509-553): a causal prefill split in two equals the one-shot prefill
+    # (last-row logits: the engine returns TTFT logits, not every row's)
+    rng = SplitMix64(opts.seed ^ 0x19C8)
+    for _ in range(10):
+        total = 2 + rng.next_below(95)
+        split = 1 + rng.next_below(total - 1)
+        tokens = np.array([rng.next_below(cfg.vocab_size) for _ in range(total)], np.int32)
+        with engine.assemble([]) as one:
+            a = engine.prefill_query(one, tokens)[0]
+        with engine.assemble([]) as two:
+            engine.prefill_query(two, tokens[:split])
+            b = engine.prefill_query(two, tokens[split:])[0]
+        diff = _max_abs_diff(a, b)
+        if diff > rel * max(float(np.abs(a).max()), 1e-30):
+            lines.append(f"FAIL incremental forward: diff {diff:g} (total {total}, split {split})")
+            repro(opts.seed)
+            return 1, lines
+    lines.append("ok incremental forward (10 splits)")
+
+    # -- single-chunk degeneracy (turbokv_main.cpp:555-584): all four paths agree
+    rng = SplitMix64(opts.seed ^ 0x51C6)
+    for _ in range(5):
+        cid = engine.ingest_chunk_payload("single", encode(_random_text(rng, 1 + rng.next_below(64))))
+        query = encode(_random_text(rng, 1 + rng.next_below(16)))
+        outs = []
+        for mode in (T.PositionMode.Reordered, T.PositionMode.Composite):
+            with engine.assemble([cid], mode) as c:
+                outs.append(engine.prefill_query(c, query)[0])
+        for mode in (T.MaskMode.Causal, T.MaskMode.Independent):
+            with naive_ids([cid], query, mode) as c:
+                outs.append(c.last_logits)
+        spread = max(_max_abs_diff(outs[0], o) for o in outs[1:])
+        if spread > rel * max(float(np.abs(outs[0]).max()), 1e-30):
+            lines.append(f"FAIL single-chunk degeneracy: spread {spread:g}")
+            repro(opts.seed)
+            return 1, lines
+    lines.append("ok single-chunk degeneracy (5 cases)")
+    lines.append("all properties hold")
+    return 0, lines
+
+
+def _splitmix_at(seed: int, i: int) -> int:
+    """SplitMix64::at(seed, i) (rng.hpp): the i-th draw of the stream seeded with `seed`."""
+    from .bench_api import SplitMix64
+
+    r = SplitMix64((seed + i * 0x9E3779B97F4A7C15) & ((1 << 64) - 1))
+    return r.next()
+
+
+def _next_signed(rng) -> float:
+    """SplitMix64::next_signed (rng.hpp): 2 * (next() >> 11) * 2^-53 - 1."""
+    return 2.0 * ((rng.next() >> 11) * (1.0 / (1 << 53))) - 1.0

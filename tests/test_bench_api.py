@@ -227,3 +227,62 @@ def test_ask_report_schema():
     assert rep["flops"]["prefill_measured"] == rep["flops"]["prefill_modeled"]
     assert set(rep["timings_ms"]) == {"retrieval", "cache_load", "ttft", "decode"}
     eng.close()
+
+
+def test_verify_helpers_follow_reference(golden):
+    """`turbokv verify` case generation (tools/turbokv_main.cpp:167-174, 349-375): SplitMix64::at per case seed (the
+    reference's own golden streams), random_text over 'a'..'z' + space, next_signed in [-1, 1), and the RoPE
+    relative score's shift invariance at 1e-9."""
+    from paper_2410_07590_b200 import pipeline_api as P
+    from paper_2410_07590_b200.bench_api import SplitMix64
+    meta, _ = golden
+    for seed, outs in meta["splitmix"].items():
+        for i, h in enumerate(outs):
+            assert P._splitmix_at(int(seed), i) == int(h, 16)
+    rng = SplitMix64(7)
+    txt = P._random_text(rng, 500)
+    assert len(txt) == 500 and set(txt) <= set("abcdefghijklmnopqrstuvwxyz ")
+    xs = [P._next_signed(rng) for _ in range(1000)]
+    assert -1.0 <= min(xs) and max(xs) < 1.0
+    q, k = [P._next_signed(rng) for _ in range(64)], [P._next_signed(rng) for _ in range(64)]
+    assert abs(P._rope_relative_score(q, k, 10, 300, 1e4) - P._rope_relative_score(q, k, 1010, 1300, 1e4)) < 1e-9
+    assert abs(P._rope_relative_score(q, k, 10, 300, 1e4) - P._rope_relative_score(q, k, 10, 301, 1e4)) > 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_verify_properties_hold_and_fault_is_caught(dtype, tmp_path):
+    """`turbokv verify` (tools/turbokv_main.cpp:586-606) over the engine: every property holds (equivalence with
+    identical decodes and a composite-defect witness, RoPE shift invariance, KV round trip and its error paths,
+    incremental == one-shot, single-chunk degeneracy); with --inject-fault the f32 engine's equivalence check fails
+    and prints the reproduction line, as in the (f64) reference."""
+    from paper_2410_07590_b200 import pipeline_api as P
+    eng = T.Engine(T.ModelConfig.toy(), 42, dtype=dtype, store_capacity_tokens=1 << 16)
+    rc, lines = P.verify(eng, P.VerifyOpts(cases=12, rope_cases=200), str(tmp_path))
+    assert rc == 0, lines
+    assert lines[0] == "ok equivalence (12 cases)" and lines[1].startswith("ok composite defect witness")
+    assert lines[-1] == "all properties hold" and len(lines) == 7
+    if dtype == "bf16":  # the fault moves toy logits by less than the bf16 bound: a precision (f32 / f64) check
+        eng.close()
+        return
+    rc, lines = P.verify(eng, P.VerifyOpts(cases=3, inject_fault=True), str(tmp_path))
+    assert rc == 1 and lines[0].startswith("FAIL equivalence: logits diff")
+    assert lines[1].startswith("REPRO: turbokv verify --case-seed ") and lines[1].endswith(" --cases 1 --inject-fault")
+    eng.close()
+
+
+@pytest.mark.gpu
+def test_ingest_report_schema():
+    """`turbokv ingest --json` (tools/turbokv_main.cpp:218-231): keys and counts; re-ingesting adds no new chunks."""
+    from paper_2410_07590_b200 import pipeline_api as P
+    eng = T.Engine(T.ModelConfig.toy(), 42, dtype="f32", store_capacity_tokens=4096)
+    docs = [P.Document("a", "canal locks hold water between gates while boats rise or fall"),
+            P.Document("b", "a lighthouse keeper trims the wick every night")]
+    rep = P.ingest_report(eng, docs, 24, "store", "toy", "f32")
+    assert set(rep) == {"schema", "command", "store", "documents", "chunks", "new_chunks", "bytes_written",
+                        "indexed_chunks", "seed", "preset", "dtype", "config"}
+    assert rep["command"] == "ingest" and rep["documents"] == 2 and rep["chunks"] == rep["new_chunks"] > 0
+    assert rep["indexed_chunks"] == rep["chunks"]
+    again = P.ingest_report(eng, docs, 24, "store", "toy", "f32")
+    assert again["new_chunks"] == 0 and again["chunks"] == rep["chunks"]
+    eng.close()
