@@ -539,6 +539,11 @@ struct tkv_engine {
 #define TKV_BATCH_SPLITS_DEFAULT 1
 #endif
     int batch_attn_splits = TKV_BATCH_SPLITS_DEFAULT;  // TKV_BATCH_ATTN_SPLITS (0 = attn_tc_batch_pick_splits)
+    // in-chain GEMM timeline (tkv_gemm_timeline): [kTlMax][2] globaltimer (first wait return, last CTA exit)
+    static constexpr int64_t kTlMax = 8192;
+    DevMem tl_buf;
+    int64_t tl_n = 0;
+    bool tl_on = false;
 
     // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits. With swiglu_act, a tcgen05 GEMM whose
     // K range fits one CTA writes silu(gate)*up straight to swiglu_act and returns 0.
@@ -549,6 +554,7 @@ struct tkv_engine {
             fail(TKV_ERR_CONFIG, "shape not supported by the tcgen05 GEMM (rows must be 16-byte aligned)");
         const int s = pick_splits(M, N, K, tc);
         Scope sc(this, PC_GEMM, 1);
+        if (tl_on && tc && tl_n < kTlMax) set_gemm_timeline_slot(tl_buf.as<unsigned long long>() + 2 * tl_n++);
         if (tc && swiglu_act && s == 1 && gu_interleaved) {
             launch_gemm_tc(A, lda, W, M, N, K, nullptr, 1, stream, swiglu_act, ssp.as<float>(), nb, (float)cfg.norm_eps,
                            gu_block);
@@ -2853,6 +2859,28 @@ tkv_status tkv_debug_attn_trace(int on, uint64_t* out, int64_t capacity) {
             TKV_CUDA(cudaMemcpy(out, buf, (size_t)std::min<int64_t>(capacity, attn_trace_words()) * 8, cudaMemcpyDeviceToHost));
         }
         attn_trace_enable(on != 0, &buf);
+    });
+}
+
+tkv_status tkv_gemm_timeline(tkv_engine* e, int on, uint64_t* out, int64_t capacity, int64_t* n_launches) {
+    return guard([&] {
+        need(e, "engine");
+        e->bind();
+        if (on) {
+            e->tl_buf.ensure((size_t)tkv_engine::kTlMax * 16);
+            // slot[0] starts at ~0 (atomicMin), slot[1] at 0 (atomicMax): two strided memsets
+            TKV_CUDA(cudaMemset2DAsync(e->tl_buf.p, 16, 0xFF, 8, tkv_engine::kTlMax, e->stream));
+            TKV_CUDA(cudaMemset2DAsync(static_cast<uint8_t*>(e->tl_buf.p) + 8, 16, 0, 8, tkv_engine::kTlMax, e->stream));
+            e->tl_n = 0;
+            e->tl_on = true;
+            return;
+        }
+        e->tl_on = false;
+        e->sync();
+        if (n_launches) *n_launches = e->tl_n;
+        if (out && e->tl_n > 0)
+            TKV_CUDA(cudaMemcpy(out, e->tl_buf.p, (size_t)std::min<int64_t>(capacity / 2, e->tl_n) * 16,
+                                cudaMemcpyDeviceToHost));
     });
 }
 

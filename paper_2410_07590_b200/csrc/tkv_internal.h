@@ -126,7 +126,10 @@ bool gemm_tc_supported(int M, int N, int K, int lda);
 // The GEMM that follows the next launch_gemm_tc in the forward (consumed by that launch) and how many of its
 // weight k-blocks per unit the current GEMM warms into L2 at its tail (0 = off)
 void set_gemm_next(const void* W, int M, int N, int K, int splits);
-void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap);  // debug: CTA 0 per-stage clock64 trace
+void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap);
+// In-chain timeline of the NEXT tcgen05 GEMM launch: slot[0] = atomicMin of the globaltimer when its CTAs' griddepcontrol.wait
+// returns (the predecessor grid has completed), slot[1] = atomicMax at CTA exit (null: off). Non-perturbing (PDL intact).
+void set_gemm_timeline_slot(unsigned long long* slot);  // debug: CTA 0 per-stage clock64 trace
 void set_gemm_next_pf(int kblocks);
 void set_gemm_nsmp(int mp);
 void set_gemm_cluster(int c);
