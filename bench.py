@@ -391,19 +391,26 @@ def run_ours(args):
         step()
     stream.synchronize()
     eng.profile(False)
-    # in-chain GEMM timeline over another pass (device globaltimer stamps inside the GEMM kernel, PDL overlap intact):
-    # per launch, from the first CTA past griddepcontrol.wait (the predecessor grid completed) to the last CTA exit
-    eng.gemm_timeline(True)
+    # in-chain kernel timeline over another pass (device globaltimer stamps inside every launch, PDL overlap intact):
+    # per launch, from the first CTA past griddepcontrol.wait (the predecessor grid completed) to the last warp done
+    eng.kernel_timeline(True)
+    tl_t0 = torch.cuda.Event(enable_timing=True)
+    tl_t1 = torch.cuda.Event(enable_timing=True)
+    tl_t0.record(stream)
     for _ in range(prof_steps):
         step()
+    tl_t1.record(stream)
     stream.synchronize()
-    tl = eng.gemm_timeline(False)
+    tl, tl_cls = eng.kernel_timeline(False)
+    tl_step_ms = tl_t0.elapsed_time(tl_t1) / prof_steps
     tl_dur = np.clip(tl[:, 1] - tl[:, 0], 0, None) / 1e6  # ms per launch
-    gemm_chain_ms = float(tl_dur.sum()) / prof_steps
-    gemm_chain_launches = len(tl) / prof_steps
+    class_chain_ms = {k: float(tl_dur[tl_cls == i].sum()) / prof_steps for i, k in enumerate(T.Engine.TIMELINE_CLASSES)}
+    gemm_dur = tl_dur[tl_cls == T.Engine.TIMELINE_CLASSES.index("gemm")]
+    gemm_chain_ms = float(gemm_dur.sum()) / prof_steps
+    gemm_chain_launches = len(gemm_dur) / prof_steps
     per_gemm_us = None
-    if len(tl_dur) == prof_steps * 4 * cfg.layer_num:  # QKV, O, gate/up, down per layer
-        d = tl_dur.reshape(prof_steps, cfg.layer_num, 4)[:, :-1, :]  # the last layer's O / MLP run on one row
+    if len(gemm_dur) == prof_steps * 4 * cfg.layer_num:  # QKV, O, gate/up, down per layer
+        d = gemm_dur.reshape(prof_steps, cfg.layer_num, 4)[:, :-1, :]  # the last layer's O / MLP run on one row
         per_gemm_us = {k: float(d[:, :, i].mean()) * 1e3 for i, k in enumerate(["qkv", "o", "gate_up", "down"])}
     gather_ms, gather_n = eng.profile_read("gather_rope")
     attn_ms, attn_n = eng.profile_read("attention")
@@ -700,6 +707,11 @@ def run_ours(args):
         # than ms_per_step). The ncu share below is the non-perturbing breakdown.
         "class_ms_events_isolated": {"gather_rope": gather_ms / prof_steps, "attention": attn_ms / prof_steps,
                                      "gemm": gemm_ms_step, "epilogue": epi_ms / prof_steps},
+        # the same classes measured live in the real chain (device timers inside every launch, PDL intact): per launch
+        # last warp done - first CTA past griddepcontrol.wait, summed per request; gaps between launches are the rest
+        "class_ms_in_chain": {**class_chain_ms, "sum": sum(class_chain_ms.values()), "step_ms_of_this_pass": tl_step_ms,
+                              "handoff_gaps": tl_step_ms - sum(class_chain_ms.values()),
+                              "launches_per_request": len(tl) / prof_steps},
         "class_share_ncu": ({"source": ncu_share.get("source"),
                              "ms_scaled_to_step": {k: v * ms_per_step for k, v in share.items()}, "share": share}
                             if share else None),
@@ -710,7 +722,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_request": gemm_bytes, "launches_per_request": gemm_chain_launches,
                      "device_ms_per_request": gemm_chain_ms, "per_launch_us_layers_0_to_L-2": per_gemm_us,
                      "timing": "in the real PDL chain: device globaltimer stamps inside every GEMM launch of a separate "
-                               "pass of the same step (tkv_gemm_timeline), duration = last CTA exit - first CTA past "
+                               "pass of the same step (tkv_kernel_timeline), duration = last CTA exit - first CTA past "
                                "griddepcontrol.wait (the predecessor grid completed), summed per request",
                      "isolated_events": {"achieved": gemm_gbs, "frac": gemm_gbs / peaks["hbm_gbs"],
                                          "device_ms_per_request": gemm_ms_step, "launches_per_request": gemm_n / prof_steps,
@@ -720,11 +732,15 @@ def run_ours(args):
                             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                             "traffic": traffic_of("gather_rope"), "algorithmic_bytes_per_launch": kv_bytes,
                             "avg_launch_ms": gather_avg_ms},
-        "attention_roofline": {"bound": "tensor", "achieved": attn_flops / (attn_ms / prof_steps / 1e3) / 1e12,
+        "attention_roofline": {"bound": "tensor", "achieved": attn_flops / (class_chain_ms["attention"] / 1e3) / 1e12,
                                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                               "frac": attn_flops / (attn_ms / prof_steps / 1e3) / 1e12 / peaks["bf16_tflops"],
+                               "frac": attn_flops / (class_chain_ms["attention"] / 1e3) / 1e12 / peaks["bf16_tflops"],
                                "flops_per_request": attn_flops, "traffic": traffic_of("attn_tc_kernel"),
-                               "device_ms_per_request": attn_ms / prof_steps},
+                               "device_ms_per_request": class_chain_ms["attention"],
+                               "timing": "in the real chain (tkv_kernel_timeline): attention + split-merge launches",
+                               "isolated_events": {"device_ms_per_request": attn_ms / prof_steps,
+                                                   "frac": attn_flops / (attn_ms / prof_steps / 1e3) / 1e12
+                                                   / peaks["bf16_tflops"]}},
         "request_roofline": {"bound": "hbm", "algorithmic_bytes": req_bytes,
                              "achieved": req_bytes / (ms_per_step / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
                              "unit": "GB/s", "frac": req_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"],

@@ -324,11 +324,14 @@ tkv_status tkv_debug_set_gemm_knobs(int stages, int smem_kb, int ctas_per_sm, in
  * the last trace): clock64 per stage [it][3] = producer issue, MMA saw the stage full, MMA committed it (1024 stages),
  * then [unit][2] = epilogue start / end (64 units). */
 tkv_status tkv_debug_gemm_trace(int on, uint64_t* out, int64_t capacity);
-/* In-chain timeline of the tcgen05 GEMM launches of this engine (non-perturbing: PDL overlap intact). on = 1 clears and
- * arms it; on = 0 disarms, synchronises and copies [launch][2] globaltimer ns = (first CTA past griddepcontrol.wait,
- * i.e. the predecessor grid completed; last CTA exit) in stream order, *n_launches = launches recorded. The time a GEMM
- * holds the kernel chain is exit - wait; its weight prefetch before the wait overlaps the predecessor. */
-tkv_status tkv_gemm_timeline(tkv_engine* eng, int on, uint64_t* out, int64_t capacity, int64_t* n_launches);
+/* Kernel timeline of this engine's launches (non-perturbing: PDL overlap intact). on = 1 clears and arms it; on = 0
+ * disarms, synchronises and copies, per launch in stream order, out[2i..2i+1] = globaltimer ns (first CTA past
+ * griddepcontrol.wait, i.e. the predecessor grid completed; last warp done) and classes[i] = 0 KV gather, 1 attention
+ * (+ split merge), 2 projection GEMM, 3 epilogue (embed, residual, QKV), 4 other (lm_head); capacity = launches;
+ * *n_launches = launches recorded. Instrumented: GEMM, attention, split merge, residual / QKV epilogues, embed,
+ * lm_head, KV gather. */
+tkv_status tkv_kernel_timeline(tkv_engine* eng, int on, uint64_t* out, int32_t* classes, int64_t capacity,
+                               int64_t* n_launches);
 tkv_status tkv_debug_gemm_bench(int device, int64_t M, int64_t N, int64_t K, int splits, int swiglu, int iters,
                                 double* ms_per_launch);
 tkv_status tkv_debug_attention(int device, tkv_dtype dtype, int impl, const float* q, const float* k,

@@ -321,6 +321,7 @@ struct AttnArgs {
     const AttnReq* reqs;
     const CUtensorMap* maps3;
     int n_req, layer;
+    unsigned long long* tl;  // kernel timeline slot (tl_take)
 };
 
 // Warp-collective MMA issue: the whole MMA warp walks the loop (operands stay warp-uniform, in uniform registers);
@@ -549,6 +550,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int lo_b = act_b ? lop[tb] : INT32_MAX, hi_b = act_b ? min(hip[tb], Tk - 1) : -1;
         constexpr int RPW = BR / SM_WARPS;  // rows per warp for the coalesced Q staging / output copy
         pdl_wait();  // q is produced by the previous kernel
+        tl_wait(a.tl);
         if (tid == 0) trace(30, 3);
         {
             // Q rows ra, rb straight into TMEM: column c of a row holds d = 2c, 2c + 1; with the 16x256b shape this
@@ -772,6 +774,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
     __syncthreads();
     if (tid == 0 && a.trace && cta_lin < TRACE_CTAS) a.trace[TRACE_CTA0 + 2 * cta_lin + 1] = globaltimer_ns();
+    if (tid == 0 && a.tl) atomicMax(a.tl + 1, gtimer_ns());
     if (warp == WARP_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
@@ -784,7 +787,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 __global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat16* __restrict__ ws_o,
                                                               const float2* __restrict__ ws_ml,
                                                               __nv_bfloat16* __restrict__ out, int* err, int Tq, int H,
-                                                              int Hkv, int splits, int groups_x) {
+                                                              int Hkv, int splits, int groups_x, unsigned long long* tl) {
     pdl_launch();
     const int lane = threadIdx.x & 31;
     const int grow = blockIdx.x * 8 + (threadIdx.x >> 5);  // row over all row groups: gid * RG + i
@@ -794,6 +797,7 @@ __global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat1
     const bool ok = rr < Tq * group;
     const int64_t plane = (int64_t)groups_x * Hkv * RG;
     pdl_wait();
+    tl_wait(tl);
     if (!ok) return;  // warp-uniform
     const uint2* src = reinterpret_cast<const uint2*>(ws_o + (int64_t)grow * D) + lane;
     uint2 v[32];
@@ -824,6 +828,7 @@ __global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat1
     const int64_t mo = (int64_t)(rr / group) * H + g * group + rr % group;
     reinterpret_cast<uint2*>(out + mo * D)[lane] =
         make_uint2(bf16x2_bits(acc[0] * inv, acc[1] * inv), bf16x2_bits(acc[2] * inv, acc[3] * inv));
+    tl_exit(tl);
 }
 
 // Split merge of the BATCHED launch: row groups are (request, kv head, group) with gid = (req * Hkv + g) * groups_x
@@ -948,6 +953,7 @@ void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* m
     CUtensorMap unused;
     memset(&unused, 0, sizeof unused);
     const int groups_x = (max_rows * group + RG - 1) / RG;
+    a.tl = tl_take();
     launch_k(attn_tc_kernel, dim3(groups_x, Hkv * n_req, a.splits), THREADS, SMEM_BYTES, s, unused, unused, a);
     TKV_CUDA(cudaGetLastError());
     if (a.splits > 1) {
@@ -1037,12 +1043,13 @@ void launch_attention_tc(const void* q, const void* k, const void* v, int kv_str
     a.pf = pf;
     const CUtensorMap tk = kv_map(k, Tk, kv_stride, kv_stride);
     const CUtensorMap tv = kv_map(v, Tk, kv_stride, kv_stride);
+    a.tl = tl_take();
     launch_k(attn_tc_kernel, grid, THREADS, SMEM_BYTES, s, tk, tv, a);
     TKV_CUDA(cudaGetLastError());
     if (splits > 1) {
         const int rows = (int)(grid.x * grid.y) * RG;
         launch_k(attn_tc_combine_kernel, dim3(rows / 8), dim3(256), 0, s, (const __nv_bfloat16*)ws.o,
-                 (const float2*)ws.ml, (__nv_bfloat16*)out, err, Tq, H, Hkv, splits, (int)grid.x);
+                 (const float2*)ws.ml, (__nv_bfloat16*)out, err, Tq, H, Hkv, splits, (int)grid.x, tl_take());
         TKV_CUDA(cudaGetLastError());
     }
 }

@@ -20,6 +20,20 @@ namespace tkv {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Kernel timeline (tkv_kernel_timeline, armed only by measurement passes): slot[0] = atomicMin of the globaltimer when a
+// CTA is past griddepcontrol.wait (the predecessor grid has completed), slot[1] = atomicMax when a warp finishes.
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void tl_wait(unsigned long long* tl) {
+    if (tl && threadIdx.x == 0) atomicMin(tl, gtimer_ns());
+}
+__device__ __forceinline__ void tl_exit(unsigned long long* tl) {
+    if (tl && (threadIdx.x & 31) == 0) atomicMax(tl + 1, gtimer_ns());
+}
+
 // RMSNorm folded into the consumer (numerics.cpp:84-101): the producer of x writes xb = x * w and per-block
 // partial sums of squares ssp[t][0..nb) (fixed order, deterministic); a consumer of a linear map of xb
 // multiplies by this per-row scale, since rms(x) . W = scale(x) * ((x * w) . W).

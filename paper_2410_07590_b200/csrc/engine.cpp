@@ -306,6 +306,21 @@ struct StagingRing {
 };
 
 enum ProfClass { PC_GATHER = 0, PC_ATTN, PC_GEMM, PC_EPI, PC_OTHER, PC_N };
+
+// Kernel timeline state (tl_take / tkv_kernel_timeline): process-global, armed by one engine at a time.
+struct TimelineState {
+    unsigned long long* base = nullptr;
+    int64_t cap = 0, n = 0;
+    int cls = PC_OTHER;
+    std::vector<int32_t> classes;
+};
+TimelineState g_tl;
+unsigned long long* tl_take() {
+    if (!g_tl.base || g_tl.n >= g_tl.cap) return nullptr;
+    g_tl.classes.push_back(g_tl.cls);
+    return g_tl.base + 2 * g_tl.n++;
+}
+void tl_set_class(int cls) { g_tl.cls = cls; }
 static const char* kProfNames[PC_N] = {"gather_rope", "attention", "gemm", "epilogue", "other"};
 
 struct Chunk {
@@ -420,12 +435,14 @@ struct tkv_engine {
         cudaEvent_t a = nullptr;
         Scope(tkv_engine* eng, int c, int n_launch) : e(eng), cls(c) {
             e->launches += n_launch;
+            tl_set_class(c);
             if (e->prof_on) {
                 a = e->take_event();
                 cudaEventRecord(a, e->stream);
             }
         }
         ~Scope() {
+            tl_set_class(PC_OTHER);
             if (a) {
                 cudaEvent_t b = e->take_event();
                 cudaEventRecord(b, e->stream);
@@ -539,11 +556,9 @@ struct tkv_engine {
 #define TKV_BATCH_SPLITS_DEFAULT 1
 #endif
     int batch_attn_splits = TKV_BATCH_SPLITS_DEFAULT;  // TKV_BATCH_ATTN_SPLITS (0 = attn_tc_batch_pick_splits)
-    // in-chain GEMM timeline (tkv_gemm_timeline): [kTlMax][2] globaltimer (first wait return, last CTA exit)
+    // kernel timeline buffer (tkv_kernel_timeline): [kTlMax][2] globaltimer (first CTA past the wait, last warp done)
     static constexpr int64_t kTlMax = 8192;
     DevMem tl_buf;
-    int64_t tl_n = 0;
-    bool tl_on = false;
 
     // partial[splits][M][N] = A[M][lda] . W[N][K]^T ; returns splits. With swiglu_act, a tcgen05 GEMM whose
     // K range fits one CTA writes silu(gate)*up straight to swiglu_act and returns 0.
@@ -554,7 +569,6 @@ struct tkv_engine {
             fail(TKV_ERR_CONFIG, "shape not supported by the tcgen05 GEMM (rows must be 16-byte aligned)");
         const int s = pick_splits(M, N, K, tc);
         Scope sc(this, PC_GEMM, 1);
-        if (tl_on && tc && tl_n < kTlMax) set_gemm_timeline_slot(tl_buf.as<unsigned long long>() + 2 * tl_n++);
         if (tc && swiglu_act && s == 1 && gu_interleaved) {
             launch_gemm_tc(A, lda, W, M, N, K, nullptr, 1, stream, swiglu_act, ssp.as<float>(), nb, (float)cfg.norm_eps,
                            gu_block);
@@ -2862,7 +2876,8 @@ tkv_status tkv_debug_attn_trace(int on, uint64_t* out, int64_t capacity) {
     });
 }
 
-tkv_status tkv_gemm_timeline(tkv_engine* e, int on, uint64_t* out, int64_t capacity, int64_t* n_launches) {
+tkv_status tkv_kernel_timeline(tkv_engine* e, int on, uint64_t* out, int32_t* classes, int64_t capacity,
+                               int64_t* n_launches) {
     return guard([&] {
         need(e, "engine");
         e->bind();
@@ -2871,16 +2886,19 @@ tkv_status tkv_gemm_timeline(tkv_engine* e, int on, uint64_t* out, int64_t capac
             // slot[0] starts at ~0 (atomicMin), slot[1] at 0 (atomicMax): two strided memsets
             TKV_CUDA(cudaMemset2DAsync(e->tl_buf.p, 16, 0xFF, 8, tkv_engine::kTlMax, e->stream));
             TKV_CUDA(cudaMemset2DAsync(static_cast<uint8_t*>(e->tl_buf.p) + 8, 16, 0, 8, tkv_engine::kTlMax, e->stream));
-            e->tl_n = 0;
-            e->tl_on = true;
+            g_tl = TimelineState{};
+            g_tl.base = e->tl_buf.as<unsigned long long>();
+            g_tl.cap = tkv_engine::kTlMax;
             return;
         }
-        e->tl_on = false;
+        const int64_t n = g_tl.n;
+        std::vector<int32_t> cls = g_tl.classes;
+        g_tl = TimelineState{};
         e->sync();
-        if (n_launches) *n_launches = e->tl_n;
-        if (out && e->tl_n > 0)
-            TKV_CUDA(cudaMemcpy(out, e->tl_buf.p, (size_t)std::min<int64_t>(capacity / 2, e->tl_n) * 16,
-                                cudaMemcpyDeviceToHost));
+        if (n_launches) *n_launches = n;
+        const int64_t m = std::min<int64_t>(capacity, n);
+        if (out && m > 0) TKV_CUDA(cudaMemcpy(out, e->tl_buf.p, (size_t)m * 16, cudaMemcpyDeviceToHost));
+        if (classes && m > 0) std::memcpy(classes, cls.data(), (size_t)m * sizeof(int32_t));
     });
 }
 

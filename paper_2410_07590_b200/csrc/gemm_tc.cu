@@ -252,8 +252,7 @@ struct GemmArgs {
     // ring fill hits L2 while this one drains and runs its epilogue
     int nx_pf, nx_units, nx_n_tiles, nx_kb_total, nx_kb_per_split, nx_np;
     int trace_parity;             // debug: which of the two per-CTA entry/exit slot sets this launch writes
-    unsigned long long* tl;       // in-chain timeline (tkv_gemm_timeline): [0] = first griddepcontrol.wait return (min
-                                  // over CTAs), [1] = last CTA exit (max), globaltimer ns; null = off
+    unsigned long long* tl;       // kernel timeline slot (tl_take): first CTA past griddepcontrol.wait, last CTA exit
     unsigned long long* trace;    // debug (tkv_debug_gemm_trace): CTA 0 clock64 per stage [it][3] = producer issue,
                                   // MMA saw full, MMA committed; [GT_UNIT + lu][2] = epilogue start / end per unit
 };
@@ -267,12 +266,7 @@ __device__ __forceinline__ void gtrace_cta(unsigned long long* t, int parity, in
     }
 }
 unsigned long long* g_gemm_trace = nullptr;
-unsigned long long* g_gemm_tl = nullptr;  // timeline slot of the next launch (set_gemm_timeline_slot)
-__device__ __forceinline__ unsigned long long globaltimer_now() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
+
 __device__ __forceinline__ void gtrace(unsigned long long* t, int slot) {
     if (t && blockIdx.x == 0 && slot < GT_SIZE) {
         unsigned long long c;
@@ -467,7 +461,7 @@ __global__ void __launch_bounds__(THREADS_P)
     } else {
         // ---------------- epilogue warps 2-5: TMEM lane group = warp % 4 ----------------
         pdl_wait();
-        if (g.tl && threadIdx.x == 64) atomicMin(g.tl, globaltimer_now());  // the predecessor grid has completed
+        if (g.tl && threadIdx.x == 64) atomicMin(g.tl, gtimer_ns());  // the predecessor grid has completed
         const int lg = warp & 3;
         const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
         const int et = threadIdx.x - 64;  // 0..127
@@ -688,7 +682,7 @@ __global__ void __launch_bounds__(THREADS_P)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) gtrace_cta(g.trace, g.trace_parity, 1);
-    if (g.tl && threadIdx.x == 0) atomicMax(g.tl + 1, globaltimer_now());
+    if (g.tl && threadIdx.x == 0) atomicMax(g.tl + 1, gtimer_ns());
     if (cl > 1) cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -832,8 +826,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;
     g.partial = partial;
     g.trace = g_gemm_trace;
-    g.tl = g_gemm_tl;
-    g_gemm_tl = nullptr;  // one launch per slot
+    g.tl = tl_take();
     static int trace_launch = 0;
     g.trace_parity = (trace_launch++) & 1;
     g.act = (__nv_bfloat16*)swiglu_act;
@@ -870,8 +863,6 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
 }
 
 
-
-void set_gemm_timeline_slot(unsigned long long* slot) { g_gemm_tl = slot; }
 
 void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap) {
     static unsigned long long* buf = nullptr;

@@ -141,12 +141,14 @@ __device__ __forceinline__ void finish_row_block(float* __restrict__ xrow, const
 
 template <typename T>
 __global__ void __launch_bounds__(256) embed_kernel(const int32_t* tok, const float* emb, int hidden, int vocab,
-                                                    const float* w, float* x, T* xb, float* ssp, int* err) {
+                                                    const float* w, float* x, T* xb, float* ssp, int* err,
+                                                    unsigned long long* tl) {
     // First kernel of every forward: release dependents only AFTER the wait, so any later kernel of this
     // forward that starts implies every earlier grid (previous forwards, the KV gather, uploads) has
     // completed — the attention kernel relies on this to TMA-load context K/V before its own wait.
     pdl_wait();
     pdl_launch();
+    tl_wait(tl);
     __shared__ float red[32];
     const int t = blockIdx.y, nb = norm_blocks(hidden);
     const int id = tok[t];
@@ -160,14 +162,17 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* tok, const fl
     for (int e = 0; e < 4; ++e) v[e] = (c0 + e < hidden) ? emb[(int64_t)id * hidden + c0 + e] : 0.f;
     finish_row_block(x + (int64_t)t * hidden, w, xb + (int64_t)t * hidden, ssp + (int64_t)t * nb, v, c0, hidden, red,
                      err);
+    tl_exit(tl);
 }
 
 // Residual add of the split-K partials (x += a . W), many CTAs per row (nb x T grid).
 template <typename T>
 __global__ void __launch_bounds__(256) residual_kernel(float* x, const float* partial, int splits, int64_t plane,
-                                                       int hidden, const float* w, T* xb, float* ssp, int* err) {
+                                                       int hidden, const float* w, T* xb, float* ssp, int* err,
+                                                       unsigned long long* tl) {
     pdl_launch();
     pdl_wait();
+    tl_wait(tl);
     __shared__ float red[32];
     const int64_t t = blockIdx.y;
     const int nb = norm_blocks(hidden);
@@ -189,6 +194,7 @@ __global__ void __launch_bounds__(256) residual_kernel(float* x, const float* pa
         }
     }
     finish_row_block(xrow, w, xb + t * hidden, ssp + t * nb, v, c0, hidden, red, err);
+    tl_exit(tl);
 }
 
 template <typename T>
@@ -227,9 +233,10 @@ template <typename T>
 __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
                                     const int32_t* pos, const float2* rope, T* q, T* kc, T* vc, int row0,
                                     StoreScatter sc, int layer, const float* ssp, int nb, int hidden, float eps,
-                                    int64_t plane) {
+                                    int64_t plane, unsigned long long* tl) {
     pdl_launch();
     pdl_wait();
+    tl_wait(tl);
     const int qd = H * d, kvd = Hkv * d, N = qd + 2 * kvd, half = d / 2;
     const int64_t pairs = (int64_t)T_ * (N / 2);
     int64_t cached_t = -1;
@@ -275,6 +282,7 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
             }
         }
     }
+    tl_exit(tl);
 }
 
 // ---- KV gather + fused RoPE ------------------------------------------------------------------
@@ -316,9 +324,11 @@ template <typename T>
 __global__ void __launch_bounds__(256) gather_rope_vec_kernel(PoolTable pools, int page_tokens,
                                                               const GatherSeg* __restrict__ segs, int n_units, int L,
                                                               int kvd, int d, const float2* __restrict__ rope,
-                                                              T* __restrict__ cache, int64_t cap, int rotate) {
+                                                              T* __restrict__ cache, int64_t cap, int rotate,
+                                                              unsigned long long* tl) {
     pdl_launch();
     pdl_wait();
+    tl_wait(tl);
     constexpr int N = Vec16<T>::N;
     constexpr int U = GATHER_U_CFG;
     const int vec_per_row = kvd / N, half = d / 2;
@@ -367,6 +377,7 @@ __global__ void __launch_bounds__(256) gather_rope_vec_kernel(PoolTable pools, i
             }
         }
     }
+    tl_exit(tl);
 }
 
 // Generic fallback: one pair per thread (any even head_size / kv_dim).
@@ -400,9 +411,10 @@ __global__ void gather_rope_pair_kernel(PoolTable pools, int page_tokens, const 
 
 template <typename T>
 __global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, float* logits, const float* ssp, int nb,
-                               float eps, int* err) {
+                               float eps, int* err, unsigned long long* tl) {
     pdl_launch();
     pdl_wait();
+    tl_wait(tl);
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= vocab) return;
     float acc = 0.f;
@@ -438,6 +450,7 @@ __global__ void lm_head_kernel(const T* h, const T* W, int hidden, int vocab, fl
         logits[warp] = acc;
         if (!isfinite(acc)) atomicOr(err, 4);  // Matrix::require_finite("logits"), model.cpp:268
     }
+    tl_exit(tl);
 }
 
 __global__ void mask_kernel(const int32_t* lo, const int32_t* hi, int rows, int cols, uint8_t* out) {
@@ -530,7 +543,8 @@ void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t s) {
 void launch_embed(const int32_t* tok, int T_, const float* emb, int hidden, int vocab, const float* w, float* x,
                   void* xb, float* ssp, DT dt, int* err, cudaStream_t s) {
     const dim3 grid(row_ctas(hidden), T_);
-    DISPATCH_DT(dt, launch_k(embed_kernel<T>, grid, 256, 0, s, tok, emb, hidden, vocab, w, x, (T*)xb, ssp, err));
+    unsigned long long* tl = tl_take();
+    DISPATCH_DT(dt, launch_k(embed_kernel<T>, grid, 256, 0, s, tok, emb, hidden, vocab, w, x, (T*)xb, ssp, err, tl));
     TKV_CUDA(cudaGetLastError());
 }
 
@@ -550,8 +564,9 @@ void launch_residual(float* x, const float* partial, int splits, int T_, int hid
                      float* ssp, DT dt, int* err, cudaStream_t s) {
     const int64_t plane = (int64_t)T_ * hidden;
     const dim3 grid(row_ctas(hidden), T_);
+    unsigned long long* tl = tl_take();
     DISPATCH_DT(dt, launch_k(residual_kernel<T>, grid, 256, 0, s, x, partial, splits, plane, hidden, w, (T*)xb, ssp,
-                             err));
+                             err, tl));
     TKV_CUDA(cudaGetLastError());
 }
 
@@ -566,9 +581,10 @@ void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hk
                          const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s, int64_t plane) {
     const int64_t pairs = (int64_t)T_ * (H + 2 * Hkv) * d / 2;
     if (plane <= 0) plane = (int64_t)T_ * (H + 2 * Hkv) * d;
+    unsigned long long* tl = tl_take();
     DISPATCH_DT(dt, launch_k(qkv_epilogue_kernel<T>, grid_for(pairs, 256), 256, 0, s,
                         partial, splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden,
-                        eps, plane));
+                        eps, plane, tl));
     TKV_CUDA(cudaGetLastError());
 }
 
@@ -582,8 +598,9 @@ void launch_gather_rope(const PoolTable& pools, int page_tokens, const GatherSeg
     if (n_units == 0) return;
     const int grid = n_units < num_sms * GATHER_GRID_MULT ? n_units : num_sms * GATHER_GRID_MULT;
     if (vec_ok) {
+        unsigned long long* tl = tl_take();
         DISPATCH_DT(dt, launch_k(gather_rope_vec_kernel<T>, grid, 256, 0, s, pools, page_tokens, segs, n_units, L,
-                                                                       kvd, d, rope, (T*)cache, cap, rotate));
+                                                                       kvd, d, rope, (T*)cache, cap, rotate, tl));
     } else {
         DISPATCH_DT(dt, launch_k(gather_rope_pair_kernel<T>, grid, 256, 0, s, pools, page_tokens, segs, n_units, L,
                                                                         kvd, d, rope, (T*)cache, cap, rotate));
@@ -594,8 +611,9 @@ void launch_gather_rope(const PoolTable& pools, int page_tokens, const GatherSeg
 void launch_lm_head(const void* h, const void* W, int hidden, int vocab, float* logits, const float* ssp, int nb,
                     float eps, DT dt, int* err, cudaStream_t s) {
     const int threads = 256, warps_per_block = threads / 32;
-    DISPATCH_DT(dt, launch_k(lm_head_kernel<T>, (vocab + warps_per_block - 1) / warps_per_block, threads, 0, s, 
-                        (const T*)h, (const T*)W, hidden, vocab, logits, ssp, nb, eps, err));
+    unsigned long long* tl = tl_take();
+    DISPATCH_DT(dt, launch_k(lm_head_kernel<T>, (vocab + warps_per_block - 1) / warps_per_block, threads, 0, s,
+                        (const T*)h, (const T*)W, hidden, vocab, logits, ssp, nb, eps, err, tl));
     TKV_CUDA(cudaGetLastError());
 }
 

@@ -127,9 +127,11 @@ bool gemm_tc_supported(int M, int N, int K, int lda);
 // weight k-blocks per unit the current GEMM warms into L2 at its tail (0 = off)
 void set_gemm_next(const void* W, int M, int N, int K, int splits);
 void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap);
-// In-chain timeline of the NEXT tcgen05 GEMM launch: slot[0] = atomicMin of the globaltimer when its CTAs' griddepcontrol.wait
-// returns (the predecessor grid has completed), slot[1] = atomicMax at CTA exit (null: off). Non-perturbing (PDL intact).
-void set_gemm_timeline_slot(unsigned long long* slot);  // debug: CTA 0 per-stage clock64 trace
+// Kernel timeline (tkv_kernel_timeline): while armed, every launch of an instrumented kernel (GEMM, attention, split
+// merge, residual / QKV epilogues, embed, lm_head, KV gather) takes the next slot [2] of globaltimer ns (first CTA past
+// griddepcontrol.wait, last warp done), tagged with the engine's current launch class. Process-global; null when off.
+unsigned long long* tl_take();
+void tl_set_class(int cls);  // debug: CTA 0 per-stage clock64 trace
 void set_gemm_next_pf(int kblocks);
 void set_gemm_nsmp(int mp);
 void set_gemm_cluster(int c);

@@ -116,7 +116,7 @@ def lib():
         L.tkv_config_fingerprint_seed.restype = C.c_uint64
         L.tkv_config_fingerprint_seed.argtypes = [C.POINTER(_Cfg)]
         L.tkv_weights_identity.argtypes = [C.POINTER(_Cfg), C.c_uint64, U64P, U64P]
-        L.tkv_gemm_timeline.argtypes = [C.c_void_p, C.c_int, U64P, C.c_int64, C.POINTER(C.c_int64)]
+        L.tkv_kernel_timeline.argtypes = [C.c_void_p, C.c_int, U64P, I32P, C.c_int64, C.POINTER(C.c_int64)]
         L.tkv_debug_weights_checksum.argtypes = [C.POINTER(_Cfg), C.c_uint64, C.c_int, U64P, U64P]
         L.tkv_engine_check.argtypes = [C.c_void_p]
         L.tkv_debug_weight_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int64, F32P]
@@ -697,16 +697,23 @@ class Engine:
         _check(lib().tkv_io_bytes(self._h, C.byref(h), C.byref(d)))
         return h.value, d.value
 
-    def gemm_timeline(self, on: bool) -> np.ndarray | None:
-        """tkv_gemm_timeline: arm (on=True) / read (on=False) the in-chain GEMM timeline; returns [launches][2]
-        globaltimer ns (first CTA past griddepcontrol.wait, last CTA exit) in stream order."""
+    TIMELINE_CLASSES = ("gather_rope", "attention", "gemm", "epilogue", "other")
+
+    def kernel_timeline(self, on: bool):
+        """tkv_kernel_timeline: arm (on=True) / read (on=False) the in-chain kernel timeline; returns
+        ([launches][2] globaltimer ns = (first CTA past griddepcontrol.wait, last warp done), [launches] class index
+        into TIMELINE_CLASSES) in stream order."""
         if on:
-            _check(lib().tkv_gemm_timeline(self._h, 1, None, 0, None))
+            _check(lib().tkv_kernel_timeline(self._h, 1, None, None, 0, None))
             return None
-        buf = np.zeros(2 * 8192, np.uint64)
+        cap = 8192
+        buf = np.zeros(2 * cap, np.uint64)
+        cls = np.zeros(cap, np.int32)
         n = C.c_int64()
-        _check(lib().tkv_gemm_timeline(self._h, 0, buf.ctypes.data_as(U64P), buf.size, C.byref(n)))
-        return buf[:2 * n.value].reshape(-1, 2).astype(np.int64)
+        _check(lib().tkv_kernel_timeline(self._h, 0, buf.ctypes.data_as(U64P), cls.ctypes.data_as(I32P), cap,
+                                         C.byref(n)))
+        m = min(n.value, cap)
+        return buf[:2 * m].reshape(-1, 2).astype(np.int64), cls[:m].copy()
 
     def set_mask_rows(self, rows, lo, hi) -> None:
         """Override mask rows of the next naive prefill (testing::mask_fault_hook): row r sees keys [lo, hi]."""
