@@ -1460,6 +1460,7 @@ static tkv_status create_engine(const tkv_model_config* cfg, uint64_t seed, cons
         if (const char* dr = getenv("TKV_DECODE_ROWS")) e->decode_rows_max = atol(dr);
         if (const char* np = getenv("TKV_GEMM_NEXT_PF")) set_gemm_next_pf(atoi(np));
         if (const char* mp = getenv("TKV_GEMM_NSMP")) set_gemm_nsmp(atoi(mp));
+        if (const char* pp = getenv("TKV_GEMM_PRE_PF_MB")) set_gemm_pre_pf_mb(atoi(pp));
         if (const char* gc = getenv("TKV_GEMM_CLUSTER")) set_gemm_cluster(atoi(gc));
         if (const char* bs = getenv("TKV_BATCH_ATTN_SPLITS")) e->batch_attn_splits = std::min(32, std::max(0, atoi(bs)));
         if (const char* se = getenv("TKV_GEMM_SKIP_EPI")) set_gemm_skip_epi(atoi(se));

@@ -32,6 +32,9 @@ namespace tkv {
 namespace {
 
 constexpr int BK = 64, THREADS = 128;
+#ifndef PRE_PF_MB_DEFAULT
+#define PRE_PF_MB_DEFAULT 0
+#endif
 constexpr uint32_t TILE_W = 128 * BK * 2;  // 16 KB: 128 rows x 64 k, bf16
 constexpr int SMEM_BUDGET = 200 * 1024;
 
@@ -43,6 +46,9 @@ struct Knobs {
     // of the weight stream in k-blocks (0 = off)
     int stages = 0, smem_kb = 110, ctas_per_sm = 2, w_evict_first = 1, np = 1, pf = 0, krot = 1;
     int next_pf = 0;  // k-blocks per unit of the NEXT GEMM warmed into L2 at this GEMM's tail (0 = off)
+    // swapped tiling: L2 prefetch of the first unit's weight k-blocks beyond the ring, issued BEFORE griddepcontrol.wait
+    // (weights do not depend on the previous kernel), capped at pre_pf_mb per launch over the whole grid
+    int pre_pf_mb = PRE_PF_MB_DEFAULT;
     // normal (> 128 tokens) tiling: nsnp 128-column halves per MMA (UMMA N = 128 * nsnp); N = 256 halves the
     // shared-memory traffic per FLOP of the SS-mode MMA (the 128 x 128 tile is smem-bandwidth bound at ~50 %)
     int nsnp = 2, ns_smem_kb = 208;
@@ -245,6 +251,7 @@ struct GemmArgs {
     float eps;
     int w_evict_first;
     int pf;                       // weight L2 prefetch distance (k-blocks ahead of the ring)
+    int pre_pf;                   // k-blocks of the first unit beyond the ring L2-prefetched before griddepcontrol.wait
     int krot;                     // rotate each unit's k-block order (spreads the shared activation tiles'
                                   // L2 reads over time instead of every CTA hitting the same lines at once)
     // next GEMM of the forward (swapped): once this CTA has issued its last loads, it warms L2 with the first
@@ -371,6 +378,8 @@ __global__ void __launch_bounds__(THREADS_P)
                 mbar_expect_tx(&full[i], stage_bytes);
                 load_w(smem + i * stage_bytes, &full[i], kblk(kb0, nkb0, i, u0) * BK, nt * 128 * g.np);
             }
+            for (int i = pre; i < min(nkb0, pre + g.pre_pf); ++i)  // the rest of the unit's weights into L2, pre-wait
+                tma_prefetch_2d(&tmW, kblk(kb0, nkb0, i, u0) * BK, nt * 128 * g.np);
             pdl_wait();
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(smem + i * stage_bytes + wbytes, &tmA, &full[i], kblk(kb0, nkb0, i, u0) * BK, mt * mstep);
@@ -839,6 +848,10 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int grid = std::min(g.units, sms * cps / g.cl) * g.cl;  // cluster mode: whole pairs
+    if (swap && g_knobs.pre_pf_mb > 0) {
+        const int64_t budget_kb = ((int64_t)g_knobs.pre_pf_mb << 20) / ((int64_t)grid * TILE_W * g.np);
+        g.pre_pf = (int)std::min<int64_t>(std::max(0, g.kb_per_split - g.stages), budget_kb);
+    }
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
     const CUtensorMap tw = make_map(W, N, K, K, 128 * g.np);
     CUtensorMap tn = tw;
@@ -880,6 +893,7 @@ void set_gemm_next(const void* W, int M, int N, int K, int splits) { g_next = Ne
 void set_gemm_next_pf(int kblocks) { g_knobs.next_pf = kblocks; }
 
 void set_gemm_nsmp(int mp) { g_knobs.nsmp = mp > 0 ? mp : 1; }
+void set_gemm_pre_pf_mb(int mb) { g_knobs.pre_pf_mb = mb > 0 ? mb : 0; }
 
 void set_gemm_cluster(int c) { g_knobs.cluster = c; }
 

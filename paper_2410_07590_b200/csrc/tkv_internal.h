@@ -134,6 +134,7 @@ unsigned long long* tl_take();
 void tl_set_class(int cls);  // debug: CTA 0 per-stage clock64 trace
 void set_gemm_next_pf(int kblocks);
 void set_gemm_nsmp(int mp);
+void set_gemm_pre_pf_mb(int mb);  // TUNING: pre-wait weight L2 prefetch budget per launch (MB, 0 = off)
 void set_gemm_cluster(int c);
 void set_gemm_skip_epi(int v);  // timing experiments only: skip the normal-tiling partial stores  // normal tiling: 2 = CTA pairs share each weight tile through TMA multicast
 // normal tiling unit order (0 n-fastest, 1 m-fastest when N > M, 2 m-fastest; group_mb > 0: m-tile groups of

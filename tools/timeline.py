@@ -1,0 +1,55 @@
+"""In-chain kernel timeline of the C2 turbo step (tkv_kernel_timeline): per-class time per request and the four
+projection GEMMs' mean in-chain durations, plus the p50 step. TUNING builds read TKV_* knobs (sweeps)."""
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2410_07590_b200 import turbokv as T  # noqa: E402
+
+
+def main(steps=10):
+    cfg = T.ModelConfig.qwen2_7b_like()
+    eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=16 * 512 * 2, exact_fingerprint=0)
+    payloads, query = bench.workload()
+    ids = eng.ingest_chunks(payloads)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
+    dq = torch.from_numpy(query).to(dev)
+    dl = torch.empty(cfg.vocab_size, dtype=torch.float32, device=dev)
+
+    def step():
+        ctx = eng.assemble(ids, T.PositionMode.Reordered)
+        eng.prefill_query_device(ctx, dq.data_ptr(), len(query), dl.data_ptr())
+        ctx.close()
+
+    for _ in range(5):
+        step()
+    ts = []
+    for _ in range(20):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    eng.kernel_timeline(True)
+    for _ in range(steps):
+        step()
+    stream.synchronize()
+    tl, cls = eng.kernel_timeline(False)
+    dur = np.clip(tl[:, 1] - tl[:, 0], 0, None) / 1e3  # us
+    per = {k: dur[cls == i].sum() / steps / 1e3 for i, k in enumerate(T.Engine.TIMELINE_CLASSES)}
+    g = dur[cls == T.Engine.TIMELINE_CLASSES.index("gemm")].reshape(steps, cfg.layer_num, 4)[:, :-1]
+    env = {k: v for k, v in os.environ.items() if k.startswith("TKV_") and k != "TKV_LIB_PATH"}
+    print(f"{env} p50 {statistics.median(ts):.3f} ms | in-chain ms: " + " ".join(f"{k} {v:.3f}" for k, v in per.items())
+          + f" | gemm us qkv {g[..., 0].mean():.2f} o {g[..., 1].mean():.2f} gate_up {g[..., 2].mean():.2f}"
+            f" down {g[..., 3].mean():.2f}")
+
+
+if __name__ == "__main__":
+    main()
