@@ -392,7 +392,11 @@ struct tkv_engine {
     // forward workspace
     // x: fp32 residual stream; xb = x * norm_w (GEMM input; the RMSNorm scale is folded into consumers); ssp:
     // per-row partial sums of squares (norm_blocks(hid) per row)
-    DevMem x, xb, ssp, q, attn, act, partial, attn_ws, d_breq, d_bmaps, logits, err, d_tok, d_pos, d_lo, d_hi, d_page, d_slot, d_segs;
+    DevMem x, xb, ssp, q, attn, act, partial, attn_ws, d_breq, d_bmaps, logits, err, d_stage, d_segs;
+    // per-forward staging arrays (tokens, positions, mask row ranges, store page / slot of each new token): ONE
+    // device buffer laid out like the pinned staging slot, so upload_stage is a single H2D copy (one copy node in
+    // the stream instead of up to six, each with its own latency before the forward's first kernel)
+    int32_t *p_tok = nullptr, *p_pos = nullptr, *p_lo = nullptr, *p_hi = nullptr, *p_page = nullptr, *p_slot = nullptr;
     StagingRing staging;
     std::vector<std::pair<size_t, void*>> ctx_free;  // recycled request-cache buffers
     std::set<tkv_context*> live;
@@ -928,22 +932,19 @@ struct Stage {
 
 void upload_stage(tkv_engine* e, const Stage& s, bool with_tokens) {
     const int64_t T = (int64_t)s.pos.size();
-    const size_t b = (size_t)T * 4;
-    e->d_tok.ensure(b);
-    e->d_pos.ensure(b);
-    e->d_lo.ensure(b);
-    e->d_hi.ensure(b);
+    const size_t b = ((size_t)T * 4 + 15) & ~size_t(15);  // 16-byte aligned sections
+    const int nsec = s.page.empty() ? 4 : 6;
+    int32_t* base = static_cast<int32_t*>(e->d_stage.ensure(6 * b + 64));
+    int32_t** ptrs[6] = {&e->p_tok, &e->p_pos, &e->p_lo, &e->p_hi, &e->p_page, &e->p_slot};
+    for (int i = 0; i < 6; ++i) *ptrs[i] = base + i * (b / 4);
     uint8_t* slot = e->staging.begin(6 * b + 64);
-    if (with_tokens) e->upload(slot, e->d_tok.p, s.tok.data(), b, 0);
-    e->upload(slot, e->d_pos.p, s.pos.data(), b, b);
-    e->upload(slot, e->d_lo.p, s.lo.data(), b, 2 * b);
-    e->upload(slot, e->d_hi.p, s.hi.data(), b, 3 * b);
-    if (!s.page.empty()) {
-        e->d_page.ensure(b);
-        e->d_slot.ensure(b);
-        e->upload(slot, e->d_page.p, s.page.data(), b, 4 * b);
-        e->upload(slot, e->d_slot.p, s.slot.data(), b, 5 * b);
-    }
+    const std::vector<int32_t>* src[6] = {&s.tok, &s.pos, &s.lo, &s.hi, &s.page, &s.slot};
+    for (int i = 0; i < nsec; ++i)
+        if (i > 0 || with_tokens) std::memcpy(slot + i * b, src[i]->data(), (size_t)T * 4);
+    const size_t first = with_tokens ? 0 : b;  // device tokens: the token section is not copied
+    e->h2d_bytes += (int64_t)(nsec * b - first);
+    TKV_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(base) + first, slot + first, nsec * b - first,
+                             cudaMemcpyHostToDevice, e->stream));
     e->staging.end(e->stream);
 }
 
@@ -971,13 +972,13 @@ void extend(tkv_engine* e, tkv_context* c, const int32_t* host_tok, const int32_
     if (host_tok) s.tok.assign(host_tok, host_tok + n);
     upload_stage(e, s, host_tok != nullptr);
     tkv_engine::Fwd f;
-    f.tok = host_tok ? e->d_tok.as<int32_t>() : dev_tok;
+    f.tok = host_tok ? e->p_tok : dev_tok;
     f.T = (int)n;
-    f.pos = e->d_pos.as<int32_t>();
+    f.pos = e->p_pos;
     f.ctx = c;
     f.row0 = (int)P;
-    f.lo = e->d_lo.as<int32_t>();
-    f.hi = e->d_hi.as<int32_t>();
+    f.lo = e->p_lo;
+    f.hi = e->p_hi;
     f.logits = true;
     e->forward(f);
     if (dev_logits)
@@ -1098,13 +1099,13 @@ void naive_impl(tkv_engine* e, const int32_t* framed, const int64_t* offsets, in
         e->ensure_rope(N);
         upload_stage(e, s, true);
         tkv_engine::Fwd f;
-        f.tok = e->d_tok.as<int32_t>();
+        f.tok = e->p_tok;
         f.T = (int)N;
-        f.pos = e->d_pos.as<int32_t>();
+        f.pos = e->p_pos;
         f.ctx = c;
         f.row0 = 0;
-        f.lo = e->d_lo.as<int32_t>();
-        f.hi = e->d_hi.as<int32_t>();
+        f.lo = e->p_lo;
+        f.hi = e->p_hi;
         f.logits = true;
         e->forward(f);
         std::vector<float> lg((size_t)e->V);
@@ -1777,18 +1778,18 @@ tkv_status tkv_ingest_chunks(tkv_engine* e, const int32_t* payloads, const int64
                     e->ensure_rope(T);
                     upload_stage(e, s, true);
                     tkv_engine::Fwd f;
-                    f.tok = e->d_tok.as<int32_t>();
+                    f.tok = e->p_tok;
                     f.T = (int)T;
-                    f.pos = e->d_pos.as<int32_t>();
+                    f.pos = e->p_pos;
                     f.ctx = scratch;
                     f.row0 = 0;
-                    f.lo = e->d_lo.as<int32_t>();
-                    f.hi = e->d_hi.as<int32_t>();
+                    f.lo = e->p_lo;
+                    f.hi = e->p_hi;
                     f.logits = false;
                     f.kv_only = true;
                     f.sc.pool = e->pool.p;
-                    f.sc.page = e->d_page.as<int32_t>();
-                    f.sc.slot = e->d_slot.as<int32_t>();
+                    f.sc.page = e->p_page;
+                    f.sc.slot = e->p_slot;
                     f.sc.page_tokens = (int)e->page_tokens;
                     f.sc.layer_num = (int)e->L;
                     f.sc.host_pool = const_cast<void*>(e->pools.p[kHostPool]);
@@ -2228,11 +2229,11 @@ tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int6
             for (const auto& q : f.reqs) min_keys = std::min(min_keys, q.row0 + q.n);
             f.batch_min_keys = min_keys;
         }
-        f.tok = e->d_tok.as<int32_t>();
+        f.tok = e->p_tok;
         f.T = (int)T;
-        f.pos = e->d_pos.as<int32_t>();
-        f.lo = e->d_lo.as<int32_t>();
-        f.hi = e->d_hi.as<int32_t>();
+        f.pos = e->p_pos;
+        f.lo = e->p_lo;
+        f.hi = e->p_hi;
         f.logits = true;
         e->forward(f);
         std::vector<float> lg((size_t)n_req * e->V);

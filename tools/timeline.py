@@ -45,6 +45,17 @@ def main(steps=10):
     dur = np.clip(tl[:, 1] - tl[:, 0], 0, None) / 1e3  # us
     per = {k: dur[cls == i].sum() / steps / 1e3 for i, k in enumerate(T.Engine.TIMELINE_CLASSES)}
     g = dur[cls == T.Engine.TIMELINE_CLASSES.index("gemm")].reshape(steps, cfg.layer_num, 4)[:, :-1]
+    # handoff gap between consecutive launches: next first-CTA-past-wait minus previous last-warp-done
+    names = T.Engine.TIMELINE_CLASSES
+    gaps = {}
+    for i in range(1, len(tl)):
+        if tl[i, 0] <= 0 or tl[i - 1, 1] <= 0:
+            continue
+        key = f"{names[cls[i - 1]]}->{names[cls[i]]}"
+        gaps.setdefault(key, []).append((tl[i, 0] - tl[i - 1, 1]) / 1e3)
+    if os.environ.get("TL_GAPS", "1") == "1":
+        for k, v in sorted(gaps.items(), key=lambda kv: -sum(kv[1])):
+            print(f"  gap {k:28s} n/step {len(v) / steps:6.1f}  median {np.median(v):6.2f} us  total/step {sum(v) / steps:7.1f} us")
     env = {k: v for k, v in os.environ.items() if k.startswith("TKV_") and k != "TKV_LIB_PATH"}
     print(f"{env} p50 {statistics.median(ts):.3f} ms | in-chain ms: " + " ".join(f"{k} {v:.3f}" for k, v in per.items())
           + f" | gemm us qkv {g[..., 0].mean():.2f} o {g[..., 1].mean():.2f} gate_up {g[..., 2].mean():.2f}"
