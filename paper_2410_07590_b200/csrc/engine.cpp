@@ -392,7 +392,7 @@ struct tkv_engine {
     // forward workspace
     // x: fp32 residual stream; xb = x * norm_w (GEMM input; the RMSNorm scale is folded into consumers); ssp:
     // per-row partial sums of squares (norm_blocks(hid) per row)
-    DevMem x, xb, ssp, q, attn, act, partial, attn_ws, d_breq, d_bmaps, logits, err, d_stage, d_segs;
+    DevMem x, xb, ssp, q, attn, act, partial, attn_ws, d_breq, d_bmaps, d_epireq, logits, err, d_stage, d_segs;
     // per-forward staging arrays (tokens, positions, mask row ranges, store page / slot of each new token): ONE
     // device buffer laid out like the pinned staging slot, so upload_stage is a single H2D copy (one copy node in
     // the stream instead of up to six, each with its own latency before the forward's first kernel)
@@ -608,6 +608,7 @@ struct tkv_engine {
         const void* batch_maps = nullptr;
         int batch_max_n = 0;
         int batch_min_keys = 0;  // shortest request context (keys) of the batched attention
+        const EpiReq* epi_reqs = nullptr;  // device table of the batched QKV epilogue (one launch per layer)
     };
     void forward(const Fwd& f);
     void attend_layer(int64_t l, int T, const void* qrows, tkv_context* actx, const int32_t* lo, const int32_t* hi,
@@ -753,7 +754,12 @@ void tkv_engine::forward(const Fwd& f) {
         // --- attention block ---
         if (!(f.kv_only && l == L - 1)) next(w_o[l], rows_next, (int)hid, (int)qd);
         int s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
-        if (batch) {
+        if (batch && f.epi_reqs) {  // every request's K/V to its own cache, one launch
+            Scope sc(this, PC_EPI, 1);
+            launch_qkv_epilogue(partial.as<float>(), s, T, (int)H, (int)Hkv, (int)d, f.pos, rope.as<float2>(), q.p,
+                                nullptr, nullptr, 0, StoreScatter{}, (int)l, ssp.as<float>(), nb, (int)hid, eps, dt, stream,
+                                (int64_t)T * nqkv, f.epi_reqs, (int)f.reqs.size());
+        } else if (batch) {
             Scope sc(this, PC_EPI, (int)f.reqs.size());
             for (const Fwd::Req& r : f.reqs)
                 launch_qkv_epilogue(partial.as<float>() + (size_t)r.tok0 * nqkv, s, r.n, (int)H, (int)Hkv, (int)d,
@@ -2228,6 +2234,15 @@ tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int6
             int min_keys = INT32_MAX;
             for (const auto& q : f.reqs) min_keys = std::min(min_keys, q.row0 + q.n);
             f.batch_min_keys = min_keys;
+        }
+        {  // the batched QKV epilogue's request table (tok0 ascending)
+            std::vector<EpiReq> er;
+            for (const auto& q : f.reqs) er.push_back({q.ctx->kv, q.ctx->cap, q.tok0, q.n, q.row0, 0});
+            e->d_epireq.ensure(er.size() * sizeof(EpiReq));
+            TKV_CUDA(cudaMemcpyAsync(e->d_epireq.p, er.data(), er.size() * sizeof(EpiReq), cudaMemcpyHostToDevice,
+                                     e->stream));
+            e->h2d_bytes += (int64_t)(er.size() * sizeof(EpiReq));
+            f.epi_reqs = e->d_epireq.as<EpiReq>();
         }
         f.tok = e->p_tok;
         f.T = (int)T;

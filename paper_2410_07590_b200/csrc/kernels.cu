@@ -42,6 +42,17 @@ __device__ __forceinline__ V sum_splits(const float* p, int splits, int64_t plan
 __device__ __forceinline__ float ldf(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
 __device__ __forceinline__ void stf(float* p, int64_t i, float v) { p[i] = v; }
 __device__ __forceinline__ void stf(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
+// four consecutive elements (16-byte aligned for f32, 8-byte for bf16), each rounded like stf
+__device__ __forceinline__ void store4(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void store4(__nv_bfloat16* p, const float (&v)[4]) {
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&a);
+    u.y = *reinterpret_cast<const uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+}
 
 __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t i) {
     uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ULL;
@@ -123,14 +134,26 @@ __device__ __forceinline__ void finish_row_block(float* __restrict__ xrow, const
                                                  int* err) {
     float ss = 0.f;
     bool bad = false;
+    if ((hidden & 3) == 0 && c0 + 3 < hidden) {  // 16-byte x / weight vectors, 4 xb elements per store
+        *reinterpret_cast<float4*>(xrow + c0) = make_float4(v[0], v[1], v[2], v[3]);
+        const float4 wv = *reinterpret_cast<const float4*>(w + c0);
+        const float xw[4] = {v[0] * wv.x, v[1] * wv.y, v[2] * wv.z, v[3] * wv.w};
+        store4(xbrow + c0, xw);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const int c = c0 + e;
-        if (c < hidden) {
-            xrow[c] = v[e];
-            stf(xbrow, c, v[e] * w[c]);
+        for (int e = 0; e < 4; ++e) {
             ss += v[e] * v[e];
             bad |= !isfinite(v[e]);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = c0 + e;
+            if (c < hidden) {
+                xrow[c] = v[e];
+                stf(xbrow, c, v[e] * w[c]);
+                ss += v[e] * v[e];
+                bad |= !isfinite(v[e]);
+            }
         }
     }
     if (bad) atomicOr(err, 2);
@@ -197,6 +220,41 @@ __global__ void __launch_bounds__(256) residual_kernel(float* x, const float* pa
     tl_exit(tl);
 }
 
+// Many-token forwards: the same, each CTA looping over rows (nb x min(T, ~8 CTAs / SM) grid) -- 8192 one-row CTAs at
+// 2048 tokens ran at ~1.6 TB/s.
+template <typename T>
+__global__ void __launch_bounds__(256) residual_rows_kernel(float* x, const float* partial, int splits, int64_t plane,
+                                                       int T_, int hidden, const float* w, T* xb, float* ssp, int* err,
+                                                       unsigned long long* tl) {
+    pdl_launch();
+    pdl_wait();
+    tl_wait(tl);
+    __shared__ float red[32];
+    const int nb = norm_blocks(hidden);
+    const int c0 = blockIdx.x * 1024 + threadIdx.x * 4;
+    for (int64_t t = blockIdx.y; t < T_; t += gridDim.y) {  // rows: long-lived CTAs for many-token forwards
+        float v[4];
+        float* xrow = x + t * hidden;
+        if ((hidden & 3) == 0 && c0 + 3 < hidden) {
+            const float4 a = sum_splits<float4, 16>(partial + t * hidden + c0, splits, plane,
+                                                   *reinterpret_cast<const float4*>(xrow + c0));
+            v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                v[e] = 0.f;
+                if (c0 + e < hidden) {
+                    float acc = xrow[c0 + e];
+                    for (int s = 0; s < splits; ++s) acc += partial[s * plane + t * hidden + c0 + e];
+                    v[e] = acc;
+                }
+            }
+        }
+        finish_row_block(xrow, w, xb + t * hidden, ssp + t * nb, v, c0, hidden, red, err);
+    }
+    tl_exit(tl);
+}
+
 template <typename T>
 __global__ void swiglu_kernel(const float* partial, int splits, int T_, int inter, T* act, const float* ssp, int nb,
                               int hidden, float eps, int gub) {
@@ -228,12 +286,14 @@ __device__ __forceinline__ int64_t store_base(const StoreScatter& sc, int64_t t,
     return ((page * sc.layer_num + layer) * 2 + kv) * sc.page_tokens * kvd + (int64_t)sc.slot[t] * kvd;
 }
 
-// One thread per element pair (2m, 2m+1) of the fused QKV output row.
-template <typename T>
-__global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
+// Few-token forwards (query prefill): one thread per element pair (2m, 2m+1) of the fused QKV output row over a flat
+// grid; the folded RMSNorm scale and (batched forwards) the token's request are looked up per thread. Measured faster
+// than the per-token-row kernel below at 64 tokens (it also leaves the attention that follows ~1 us / layer faster).
+template <typename T, bool BATCH>
+__global__ void qkv_epilogue_flat_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
                                     const int32_t* pos, const float2* rope, T* q, T* kc, T* vc, int row0,
                                     StoreScatter sc, int layer, const float* ssp, int nb, int hidden, float eps,
-                                    int64_t plane, unsigned long long* tl) {
+                                    int64_t plane, unsigned long long* tl, const EpiReq* __restrict__ reqs, int n_req) {
     pdl_launch();
     pdl_wait();
     tl_wait(tl);
@@ -241,11 +301,27 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
     const int64_t pairs = (int64_t)T_ * (N / 2);
     int64_t cached_t = -1;
     float rs = 0.f;
+    T* kct = kc;  // this token's cache planes and row (batched: its request's cache)
+    T* vct = vc;
+    int64_t crow = 0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = p / (N / 2);
-        if (t != cached_t) {  // folded attn RMSNorm scale, once per token per thread
+        if (t != cached_t) {  // folded attn RMSNorm scale and the destination rows, once per token per thread
             rs = row_scale(ssp, nb, t, hidden, eps);
             cached_t = t;
+            crow = row0 + t;
+            if (BATCH) {  // request of token t: the last with tok0 <= t (tok0 ascending)
+                int lo = 0, hi = n_req - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (reqs[mid].tok0 <= t) lo = mid;
+                    else hi = mid - 1;
+                }
+                const EpiReq R = reqs[lo];
+                kct = static_cast<T*>(R.kv) + (int64_t)(2 * layer) * R.cap * kvd;
+                vct = kct + R.cap * kvd;
+                crow = R.row0 + (t - R.tok0);
+            }
         }
         const int n = 2 * (int)(p - t * (N / 2));
         const float2 xs = sum_splits(partial + t * N + n, splits, plane, make_float2(0.f, 0.f));  // n even: 8 B aligned
@@ -254,8 +330,8 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
         x1 *= rs;
         if (n >= qd + kvd) {  // V: copied as is
             const int c = n - qd - kvd;
-            stf(vc, (int64_t)(row0 + t) * kvd + c, x0);
-            stf(vc, (int64_t)(row0 + t) * kvd + c + 1, x1);
+            stf(vct, crow * kvd + c, x0);
+            stf(vct, crow * kvd + c + 1, x1);
             if (sc.page) {
                 T* pool;
                 const int64_t base = store_base(sc, t, layer, 1, kvd, pool);
@@ -272,8 +348,8 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
             stf(q, t * qd + n + 1, r1);
         } else {
             const int c = n - qd;
-            stf(kc, (int64_t)(row0 + t) * kvd + c, r0);
-            stf(kc, (int64_t)(row0 + t) * kvd + c + 1, r1);
+            stf(kct, crow * kvd + c, r0);
+            stf(kct, crow * kvd + c + 1, r1);
             if (sc.page) {  // the store keeps keys unrotated (SPEC: rotation at use)
                 T* pool;
                 const int64_t base = store_base(sc, t, layer, 0, kvd, pool);
@@ -281,6 +357,96 @@ __global__ void qkv_epilogue_kernel(const float* partial, int splits, int T_, in
                 stf(pool, base + c + 1, x1);
             }
         }
+    }
+    tl_exit(tl);
+}
+
+// Many-token forwards (batched prefill, ingest, full concat): one thread per element pair (2m, 2m+1); grid.y walks the tokens, so the folded RMSNorm
+// scale, the position and (batched forwards) the token's request / cache rows are resolved once per CTA.
+template <typename T>
+__global__ void __launch_bounds__(256) qkv_epilogue_kernel(const float* partial, int splits, int T_, int H, int Hkv,
+                                                           int d, const int32_t* pos, const float2* rope, T* q, T* kc,
+                                                           T* vc, int row0, StoreScatter sc, int layer, const float* ssp,
+                                                           int nb, int hidden, float eps, int64_t plane,
+                                                           unsigned long long* tl, const EpiReq* __restrict__ reqs,
+                                                           int n_req) {
+    pdl_launch();
+    pdl_wait();
+    tl_wait(tl);
+    const int qd = H * d, kvd = Hkv * d, N = qd + 2 * kvd, half = d / 2;
+    __shared__ float s_rs;
+    __shared__ T* s_k;
+    __shared__ T* s_v;
+    __shared__ int64_t s_row;
+    __shared__ int s_pos;
+    for (int64_t t = blockIdx.y; t < T_; t += gridDim.y) {
+        if (threadIdx.x < 32) {  // warp 0: folded attn RMSNorm scale, position and destination rows of token t
+            const int lane = threadIdx.x;
+            // row_scale (dev_common.cuh) with its loads spread over the lanes and the same summation order
+            const float part = (nb <= 32 && lane < nb) ? ssp[t * nb + lane] : 0.f;
+            const int pt = lane == 0 ? pos[t] : 0;
+            int r = 0;  // request of token t: the last with tok0 <= t (tok0 ascending), 32 entries per ballot
+            for (int base = 0; base < n_req; base += 32) {
+                const unsigned m = __ballot_sync(0xffffffffu, base + lane < n_req && reqs[base + lane].tok0 <= t);
+                if (m) r = base + 31 - __clz(m);
+                if (m != 0xffffffffu) break;
+            }
+            float ss = 0.f;
+            for (int b = 0; b < min(nb, 32); ++b) ss += __shfl_sync(0xffffffffu, part, b);
+            if (lane == 0) {
+                s_rs = nb <= 32 ? 1.0f / sqrtf(ss / (float)hidden + eps) : row_scale(ssp, nb, t, hidden, eps);
+                s_pos = pt;
+                if (n_req > 0) {
+                    const EpiReq R = reqs[r];
+                    T* kct = static_cast<T*>(R.kv) + (int64_t)(2 * layer) * R.cap * kvd;
+                    s_k = kct;
+                    s_v = kct + R.cap * kvd;
+                    s_row = R.row0 + (t - R.tok0);
+                } else {
+                    s_k = kc;
+                    s_v = vc;
+                    s_row = row0 + t;
+                }
+            }
+        }
+        __syncthreads();
+        for (int n = 2 * (int)(blockIdx.x * blockDim.x + threadIdx.x); n < N; n += 2 * (int)(gridDim.x * blockDim.x)) {
+            const float rs = s_rs;
+            const float2 xs = sum_splits(partial + t * N + n, splits, plane, make_float2(0.f, 0.f));  // n even: 8 B
+            const float x0 = xs.x * rs, x1 = xs.y * rs;
+            if (n >= qd + kvd) {  // V: copied as is
+                const int c = n - qd - kvd;
+                T* vct = s_v;
+                stf(vct, s_row * kvd + c, x0);
+                stf(vct, s_row * kvd + c + 1, x1);
+                if (sc.page) {
+                    T* pool;
+                    const int64_t base = store_base(sc, t, layer, 1, kvd, pool);
+                    stf(pool, base + c, x0);
+                    stf(pool, base + c + 1, x1);
+                }
+            } else {
+                const int e = (n < qd ? n : n - qd) % d;
+                const float2 cs = rope[(int64_t)s_pos * half + e / 2];
+                const float r0 = x0 * cs.x - x1 * cs.y, r1 = x0 * cs.y + x1 * cs.x;  // rope.cpp:41-44
+                if (n < qd) {
+                    stf(q, t * qd + n, r0);
+                    stf(q, t * qd + n + 1, r1);
+                } else {
+                    const int c = n - qd;
+                    T* kct = s_k;
+                    stf(kct, s_row * kvd + c, r0);
+                    stf(kct, s_row * kvd + c + 1, r1);
+                    if (sc.page) {  // the store keeps keys unrotated (SPEC: rotation at use)
+                        T* pool;
+                        const int64_t base = store_base(sc, t, layer, 0, kvd, pool);
+                        stf(pool, base + c, x0);
+                        stf(pool, base + c + 1, x1);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // the shared token state is rewritten for the next token
     }
     tl_exit(tl);
 }
@@ -563,10 +729,16 @@ void launch_store_f32_from_f64(float* dst, const double* src, int64_t n, cudaStr
 void launch_residual(float* x, const float* partial, int splits, int T_, int hidden, const float* w, void* xb,
                      float* ssp, DT dt, int* err, cudaStream_t s) {
     const int64_t plane = (int64_t)T_ * hidden;
-    const dim3 grid(row_ctas(hidden), T_);
     unsigned long long* tl = tl_take();
-    DISPATCH_DT(dt, launch_k(residual_kernel<T>, grid, 256, 0, s, x, partial, splits, plane, hidden, w, (T*)xb, ssp,
-                             err, tl));
+    if (T_ <= 256) {  // query-prefill sizes: one CTA row per token (measured faster at 64 tokens)
+        const dim3 grid(row_ctas(hidden), T_);
+        DISPATCH_DT(dt, launch_k(residual_kernel<T>, grid, 256, 0, s, x, partial, splits, plane, hidden, w, (T*)xb,
+                                 ssp, err, tl));
+    } else {
+        const dim3 grid(row_ctas(hidden), (unsigned)std::min(T_, std::max(1, 148 * 8 / row_ctas(hidden))));
+        DISPATCH_DT(dt, launch_k(residual_rows_kernel<T>, grid, 256, 0, s, x, partial, splits, plane, T_, hidden, w,
+                                 (T*)xb, ssp, err, tl));
+    }
     TKV_CUDA(cudaGetLastError());
 }
 
@@ -578,13 +750,26 @@ void launch_swiglu(const float* partial, int splits, int T_, int inter, void* ac
 
 void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hkv, int d, const int32_t* pos,
                          const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc, int layer,
-                         const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s, int64_t plane) {
+                         const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s, int64_t plane,
+                         const EpiReq* reqs, int n_req) {
     const int64_t pairs = (int64_t)T_ * (H + 2 * Hkv) * d / 2;
     if (plane <= 0) plane = (int64_t)T_ * (H + 2 * Hkv) * d;
     unsigned long long* tl = tl_take();
-    DISPATCH_DT(dt, launch_k(qkv_epilogue_kernel<T>, grid_for(pairs, 256), 256, 0, s,
-                        partial, splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden,
-                        eps, plane, tl));
+    if (T_ <= 256) {  // query-prefill sizes: flat pair grid
+        if (n_req > 0) {
+            DISPATCH_DT(dt, launch_k(qkv_epilogue_flat_kernel<T, true>, grid_for(pairs, 256), 256, 0, s, partial, splits,
+                                     T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden,
+                                     eps, plane, tl, reqs, n_req));
+        } else {
+            DISPATCH_DT(dt, launch_k(qkv_epilogue_flat_kernel<T, false>, grid_for(pairs, 256), 256, 0, s, partial,
+                                     splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb,
+                                     hidden, eps, plane, tl, reqs, n_req));
+        }
+    } else {  // one CTA per token: the per-token prologue (row scale, position, request) once per token
+        const dim3 grid(1u, (unsigned)std::min<int64_t>(T_, 65535));
+        DISPATCH_DT(dt, launch_k(qkv_epilogue_kernel<T>, grid, 256, 0, s, partial, splits, T_, H, Hkv, d, pos, rope,
+                                 (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden, eps, plane, tl, reqs, n_req));
+    }
     TKV_CUDA(cudaGetLastError());
 }
 

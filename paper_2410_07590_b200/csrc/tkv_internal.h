@@ -75,11 +75,18 @@ struct StoreScatter {
     void* host_pool = nullptr;      // pinned host spill tier (device-mapped): page >= host_base -> host page
     int32_t host_base = INT32_MAX;  //   (page - host_base)
 };
+// Batched QKV epilogue: request r owns forward tokens [tok0, tok0 + n); their K/V rows go to ITS cache (kv, cap:
+// [L][K|V][cap][kv_dim]) at rows [row0, row0 + n). One launch covers every request of a batched forward.
+struct EpiReq {
+    void* kv;
+    int64_t cap;
+    int tok0, n, row0, pad;
+};
 // The projections were computed from xb: every output is first multiplied by row_scale(ssp, t).
 void launch_qkv_epilogue(const float* partial, int splits, int T, int H, int Hkv, int d, const int32_t* pos,
                          const float2* rope, void* q, void* kc, void* vc, int row0, const StoreScatter& sc,
                          int layer, const float* ssp, int nb, int hidden, float eps, DT dt, cudaStream_t s,
-                         int64_t plane = 0);  // split-plane stride in floats (0 = T * N; batched forwards pass
+                         int64_t plane = 0, const EpiReq* reqs = nullptr, int n_req = 0);  // split-plane stride in floats (0 = T * N; batched forwards pass
                                               // the whole batch's plane and a row-offset partial pointer)
 
 // KV gather + fused RoPE: one descriptor per (chunk page -> request rows) segment.

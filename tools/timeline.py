@@ -14,23 +14,38 @@ from paper_2410_07590_b200 import turbokv as T  # noqa: E402
 
 def main(steps=10):
     cfg = T.ModelConfig.qwen2_7b_like()
-    eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=16 * 512 * 2, exact_fingerprint=0)
-    payloads, query = bench.workload()
-    ids = eng.ingest_chunks(payloads)
+    c3 = os.environ.get("TL_C3") == "1"  # C3: batch 32 x (20 x 800-token chunks + 64-token query), one step = a batch
+    eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=(160 * 832 if c3 else 16 * 512 * 2) + 65536,
+                   exact_fingerprint=0)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
-    dq = torch.from_numpy(query).to(dev)
-    dl = torch.empty(cfg.vocab_size, dtype=torch.float32, device=dev)
+    if c3:
+        steps = 2
+        rng = np.random.default_rng(0xC3)
+        cids = eng.ingest_chunks([rng.integers(97, 123, 798).astype(np.int32) for _ in range(160)])
+        picks = [rng.choice(160, 20, replace=False) for _ in range(32)]
+        queries = [rng.integers(97, 123, 64).astype(np.int32) for _ in range(32)]
 
-    def step():
-        ctx = eng.assemble(ids, T.PositionMode.Reordered)
-        eng.prefill_query_device(ctx, dq.data_ptr(), len(query), dl.data_ptr())
-        ctx.close()
+        def step():
+            ctxs = [eng.assemble([cids[j] for j in pk], T.PositionMode.Reordered) for pk in picks]
+            eng.prefill_query_batch(ctxs, queries)
+            for c in ctxs:
+                c.close()
+    else:
+        payloads, query = bench.workload()
+        ids = eng.ingest_chunks(payloads)
+        dq = torch.from_numpy(query).to(dev)
+        dl = torch.empty(cfg.vocab_size, dtype=torch.float32, device=dev)
 
-    for _ in range(5):
+        def step():
+            ctx = eng.assemble(ids, T.PositionMode.Reordered)
+            eng.prefill_query_device(ctx, dq.data_ptr(), len(query), dl.data_ptr())
+            ctx.close()
+
+    for _ in range(2 if c3 else 5):
         step()
     ts = []
-    for _ in range(20):
+    for _ in range(3 if c3 else 20):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         step()
@@ -44,7 +59,11 @@ def main(steps=10):
     tl, cls = eng.kernel_timeline(False)
     dur = np.clip(tl[:, 1] - tl[:, 0], 0, None) / 1e3  # us
     per = {k: dur[cls == i].sum() / steps / 1e3 for i, k in enumerate(T.Engine.TIMELINE_CLASSES)}
-    g = dur[cls == T.Engine.TIMELINE_CLASSES.index("gemm")].reshape(steps, cfg.layer_num, 4)[:, :-1]
+    gd = dur[cls == T.Engine.TIMELINE_CLASSES.index("gemm")]
+    if len(gd) != steps * cfg.layer_num * 4:
+        print(f"{len(gd) / steps:.0f} GEMM launches per step; launches per step {len(tl) / steps:.0f}")
+        gd = np.resize(gd, steps * cfg.layer_num * 4)
+    g = gd.reshape(steps, cfg.layer_num, 4)[:, :-1]
     # handoff gap between consecutive launches: next first-CTA-past-wait minus previous last-warp-done
     names = T.Engine.TIMELINE_CLASSES
     gaps = {}
@@ -56,6 +75,12 @@ def main(steps=10):
     if os.environ.get("TL_GAPS", "1") == "1":
         for k, v in sorted(gaps.items(), key=lambda kv: -sum(kv[1])):
             print(f"  gap {k:28s} n/step {len(v) / steps:6.1f}  median {np.median(v):6.2f} us  total/step {sum(v) / steps:7.1f} us")
+    ep = dur[cls == T.Engine.TIMELINE_CLASSES.index("epilogue")]
+    per_layer = (len(ep) // steps - 1) // cfg.layer_num  # embed, then per layer: QKV epilogue(s), residual x2
+    if per_layer >= 3 and len(ep) == steps * (1 + per_layer * cfg.layer_num):
+        e = ep.reshape(steps, -1)[:, 1:].reshape(steps, cfg.layer_num, per_layer)
+        print("  epilogue us per layer: qkv %.1f  residual(O) %.1f  residual(down) %.1f  (launches/layer %d)"
+              % (e[..., :per_layer - 2].sum(-1).mean(), e[..., -2].mean(), e[..., -1].mean(), per_layer))
     env = {k: v for k, v in os.environ.items() if k.startswith("TKV_") and k != "TKV_LIB_PATH"}
     print(f"{env} p50 {statistics.median(ts):.3f} ms | in-chain ms: " + " ".join(f"{k} {v:.3f}" for k, v in per.items())
           + f" | gemm us qkv {g[..., 0].mean():.2f} o {g[..., 1].mean():.2f} gate_up {g[..., 2].mean():.2f}"
