@@ -286,11 +286,69 @@ __device__ __forceinline__ int64_t store_base(const StoreScatter& sc, int64_t t,
     return ((page * sc.layer_num + layer) * 2 + kv) * sc.page_tokens * kvd + (int64_t)sc.slot[t] * kvd;
 }
 
-// Few-token forwards (query prefill): one thread per element pair (2m, 2m+1) of the fused QKV output row over a flat
+// Non-batched few-token forwards (C2 query prefill): one thread per element pair (2m, 2m+1) of the fused QKV output
+// row over a flat grid (64 registers: 4 CTAs / SM, one wave at 64 tokens).
+template <typename T>
+__global__ void qkv_epilogue_single_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
+                                    const int32_t* pos, const float2* rope, T* q, T* kc, T* vc, int row0,
+                                    StoreScatter sc, int layer, const float* ssp, int nb, int hidden, float eps,
+                                    int64_t plane, unsigned long long* tl) {
+    pdl_launch();
+    pdl_wait();
+    tl_wait(tl);
+    const int qd = H * d, kvd = Hkv * d, N = qd + 2 * kvd, half = d / 2;
+    const int64_t pairs = (int64_t)T_ * (N / 2);
+    int64_t cached_t = -1;
+    float rs = 0.f;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = p / (N / 2);
+        if (t != cached_t) {  // folded attn RMSNorm scale, once per token per thread
+            rs = row_scale(ssp, nb, t, hidden, eps);
+            cached_t = t;
+        }
+        const int n = 2 * (int)(p - t * (N / 2));
+        const float2 xs = sum_splits(partial + t * N + n, splits, plane, make_float2(0.f, 0.f));  // n even: 8 B aligned
+        float x0 = xs.x, x1 = xs.y;
+        x0 *= rs;
+        x1 *= rs;
+        if (n >= qd + kvd) {  // V: copied as is
+            const int c = n - qd - kvd;
+            stf(vc, (int64_t)(row0 + t) * kvd + c, x0);
+            stf(vc, (int64_t)(row0 + t) * kvd + c + 1, x1);
+            if (sc.page) {
+                T* pool;
+                const int64_t base = store_base(sc, t, layer, 1, kvd, pool);
+                stf(pool, base + c, x0);
+                stf(pool, base + c + 1, x1);
+            }
+            continue;
+        }
+        const int e = (n < qd ? n : n - qd) % d;
+        const float2 cs = rope[(int64_t)pos[t] * half + e / 2];
+        const float r0 = x0 * cs.x - x1 * cs.y, r1 = x0 * cs.y + x1 * cs.x;  // rope.cpp:41-44
+        if (n < qd) {
+            stf(q, t * qd + n, r0);
+            stf(q, t * qd + n + 1, r1);
+        } else {
+            const int c = n - qd;
+            stf(kc, (int64_t)(row0 + t) * kvd + c, r0);
+            stf(kc, (int64_t)(row0 + t) * kvd + c + 1, r1);
+            if (sc.page) {  // the store keeps keys unrotated (SPEC: rotation at use)
+                T* pool;
+                const int64_t base = store_base(sc, t, layer, 0, kvd, pool);
+                stf(pool, base + c, x0);
+                stf(pool, base + c + 1, x1);
+            }
+        }
+    }
+    tl_exit(tl);
+}
+
+// Few-token BATCHED forwards: one thread per element pair (2m, 2m+1) of the fused QKV output row over a flat
 // grid; the folded RMSNorm scale and (batched forwards) the token's request are looked up per thread. Measured faster
 // than the per-token-row kernel below at 64 tokens (it also leaves the attention that follows ~1 us / layer faster).
 template <typename T, bool BATCH>
-__global__ void qkv_epilogue_flat_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
+__global__ void __launch_bounds__(256, 4) qkv_epilogue_flat_kernel(const float* partial, int splits, int T_, int H, int Hkv, int d,
                                     const int32_t* pos, const float2* rope, T* q, T* kc, T* vc, int row0,
                                     StoreScatter sc, int layer, const float* ssp, int nb, int hidden, float eps,
                                     int64_t plane, unsigned long long* tl, const EpiReq* __restrict__ reqs, int n_req) {
@@ -761,9 +819,9 @@ void launch_qkv_epilogue(const float* partial, int splits, int T_, int H, int Hk
                                      T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden,
                                      eps, plane, tl, reqs, n_req));
         } else {
-            DISPATCH_DT(dt, launch_k(qkv_epilogue_flat_kernel<T, false>, grid_for(pairs, 256), 256, 0, s, partial,
-                                     splits, T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb,
-                                     hidden, eps, plane, tl, reqs, n_req));
+            DISPATCH_DT(dt, launch_k(qkv_epilogue_single_kernel<T>, grid_for(pairs, 256), 256, 0, s, partial, splits,
+                                     T_, H, Hkv, d, pos, rope, (T*)q, (T*)kc, (T*)vc, row0, sc, layer, ssp, nb, hidden,
+                                     eps, plane, tl));
         }
     } else {  // one CTA per token: the per-token prologue (row scale, position, request) once per token
         const dim3 grid(1u, (unsigned)std::min<int64_t>(T_, 65535));
