@@ -731,3 +731,56 @@ np.save(sys.argv[1], eng.prefill_query_batch(ctxs, qs))
         outs.append(np.load(path))
     for a, b in zip(outs[1], outs[0]):
         assert_close(a, b, BF16_TOL)
+
+
+def test_batched_prefill_many_tokens_matches_per_request():
+    """A batched forward above 256 query tokens (the per-token-row QKV epilogue writing every request's K/V to its
+    own cache through the request table, many-token residuals, the single batched attention launch with its
+    automatic split-K) gives each request the logits of its own prefill_query, and leaves the same query K/V rows
+    in its cache (Qwen dims, 2 layers; bf16 tolerance, argmax checked)."""
+    cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
+    eng = engine(cfg, 7, "bf16", flags=0x20)  # TKV_FLAG_BATCH_ATTN: one attention launch for the batch
+    ids = eng.ingest_chunks([O.random_text_tokens(900 + i, 300 + 37 * i) for i in range(8)])
+    qs = [O.random_text_tokens(950 + r, 48 + 3 * r) for r in range(6)]
+    assert sum(len(q) for q in qs) > 256
+    picks = [ids[r:r + 3] for r in range(6)]
+    ctxs = [eng.assemble(p, T.PositionMode.Reordered if r % 2 else T.PositionMode.Composite)
+            for r, p in enumerate(picks)]
+    batched = eng.prefill_query_batch(ctxs, qs)
+    for r, (p, q) in enumerate(zip(picks, qs)):
+        with eng.assemble(p, T.PositionMode.Reordered if r % 2 else T.PositionMode.Composite) as single:
+            ref = eng.prefill_query(single, q)[0]
+            assert_close(batched[r], ref, BF16_TOL)
+            assert_argmax(batched[r], ref, BF16_TOL)
+            for layer in (0, cfg.layer_num - 1):
+                n = single.total_tokens()
+                kb = ctxs[r].read_kv(layer, "k", rotated=True)[n - len(q):n]
+                ks = single.read_kv(layer, "k", rotated=True)[n - len(q):n]
+                assert_close(kb, ks, BF16_TOL)
+    for c in ctxs:
+        c.close()
+
+
+def test_kernel_timeline_covers_the_forward():
+    """tkv_kernel_timeline: every hot launch of a query prefill is stamped in stream order with its class (one gather,
+    embed, 4 GEMMs + QKV epilogue + attention (+ merge) + 2 residuals per layer, lm_head), every duration is
+    positive, the launches do not overlap out of order, and disarming leaves later launches unstamped."""
+    cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
+    eng = engine(cfg, 5, "bf16")
+    ids = eng.ingest_chunks([O.random_text_tokens(700 + i, 200) for i in range(3)])
+    q = O.random_text_tokens(77, 33)
+    eng.kernel_timeline(True)
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        eng.prefill_query(ctx, q)
+    tl, cls = eng.kernel_timeline(False)
+    names = [T.Engine.TIMELINE_CLASSES[c] for c in cls]
+    assert names[0] == "gather_rope" and names[1] == "epilogue" and names[-1] == "other"
+    assert names.count("gemm") == 4 * cfg.layer_num
+    assert names.count("epilogue") == 1 + 3 * cfg.layer_num
+    assert cfg.layer_num <= names.count("attention") <= 2 * cfg.layer_num
+    assert (tl[:, 1] > tl[:, 0]).all() and (tl[:, 0] > 0).all()
+    assert (np.diff(tl[:, 1]) > 0).all()  # each launch finishes after its predecessor (stream order)
+    with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        eng.prefill_query(ctx, q)
+    tl2, _ = eng.kernel_timeline(False)
+    assert len(tl2) == 0
