@@ -453,19 +453,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
 
     if (warp == WARP_TMA) {
-        if (lane != 0) {
-            // HBM is mostly idle during attention at query-prefill sizes: lanes 1-31 may warm L2 with this CTA's
-            // share of the next projections' weights (bulk prefetch, no completion tracking; off by default)
-            const int ncta = gridDim.x * gridDim.y * gridDim.z;
-            for (int rg2 = 0; rg2 < 2; ++rg2) {
-                const size_t total = a.pf.bytes[rg2] & ~size_t(15);
-                if (!a.pf.ptr[rg2] || total == 0) continue;
-                const size_t share = ((total + ncta - 1) / ncta + 15) & ~size_t(15);
-                const size_t b0 = (size_t)cta_lin * share, b1 = min(b0 + share, total);
-                for (size_t off = b0 + (size_t)(lane - 1) * 65536; off < b1; off += (size_t)31 * 65536)
-                    prefetch_l2(static_cast<const uint8_t*>(a.pf.ptr[rg2]) + off, (uint32_t)min((size_t)65536, b1 - off));
-            }
-        } else {  // ---------------- TMA producer: K(j) then V(j) into their rings ----------------
+        if (lane == 0) {  // ---------------- TMA producer: K(j) then V(j) into their rings ----------------
             auto load_tile = [&](bool k_tile, int j) {
                 const CUtensorMap* m = k_tile ? mK : mV;
                 uint64_t* full = k_tile ? k_full : v_full;
@@ -494,6 +482,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 load_tile(true, j);
                 load_tile(false, j);
+            }
+            // HBM is mostly idle for the rest of the attention at query-prefill sizes: once this CTA's K/V loads are
+            // all issued, warm L2 with its share of the next projections' weights (bulk prefetch, no completion
+            // tracking). Issued earlier, the prefetch delays the first K/V tiles (measured).
+            const int ncta = gridDim.x * gridDim.y * gridDim.z;
+            for (int rg2 = 0; rg2 < 2; ++rg2) {
+                const size_t total = a.pf.bytes[rg2] & ~size_t(15);
+                if (!a.pf.ptr[rg2] || total == 0) continue;
+                const size_t share = ((total + ncta - 1) / ncta + 15) & ~size_t(15);
+                const size_t b0 = (size_t)cta_lin * share, b1 = min(b0 + share, total);
+                for (size_t off = b0; off < b1; off += 65536)
+                    prefetch_l2(static_cast<const uint8_t*>(a.pf.ptr[rg2]) + off, (uint32_t)min((size_t)65536, b1 - off));
             }
         }
     } else if (warp == WARP_MMA) {

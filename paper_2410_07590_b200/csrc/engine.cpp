@@ -533,7 +533,9 @@ struct tkv_engine {
         if (p) ctx_free.emplace_back(bytes, p);
     }
 
-    size_t l2_prefetch_bytes = 0;  // TKV_L2_PREFETCH_MB (tuning knob)
+    // L2 warm-up of the O-proj weights and the head of gate/up, issued by each attention CTA once its K/V loads are
+    // out (query-prefill forwards): C2 step 3.60 -> 3.54 ms at 40 MB (26 / 64 MB: 3.55 / 3.54, attention slower at 64)
+    size_t l2_prefetch_bytes = (size_t)40 << 20;  // TKV_L2_PREFETCH_MB (tuning knob)
     int skip_mask = 0;             // TKV_TIMING_SKIP: drop kernels for cost attribution (results invalid)
     int trace_layer = -1;          // TKV_TRACE_LAYER: clock64 pipeline trace of that layer's attention launch
     int attn_split_override = 0;   // TKV_ATTN_SPLITS: force the tcgen05 attention's split-K count
