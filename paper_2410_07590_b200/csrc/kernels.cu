@@ -223,34 +223,49 @@ __global__ void __launch_bounds__(256) residual_kernel(float* x, const float* pa
 // Many-token forwards: the same, each CTA looping over rows (nb x min(T, ~8 CTAs / SM) grid) -- 8192 one-row CTAs at
 // 2048 tokens ran at ~1.6 TB/s.
 template <typename T>
-__global__ void __launch_bounds__(256) residual_rows_kernel(float* x, const float* partial, int splits, int64_t plane,
-                                                       int T_, int hidden, const float* w, T* xb, float* ssp, int* err,
-                                                       unsigned long long* tl) {
+__global__ void __launch_bounds__(256, 4) residual_rows_kernel(float* x, const float* partial, int splits,
+                                                          int64_t plane, int T_, int hidden, const float* w, T* xb,
+                                                          float* ssp, int* err, unsigned long long* tl) {
     pdl_launch();
     pdl_wait();
     tl_wait(tl);
     __shared__ float red[32];
     const int nb = norm_blocks(hidden);
     const int c0 = blockIdx.x * 1024 + threadIdx.x * 4;
-    for (int64_t t = blockIdx.y; t < T_; t += gridDim.y) {  // rows: long-lived CTAs for many-token forwards
-        float v[4];
-        float* xrow = x + t * hidden;
-        if ((hidden & 3) == 0 && c0 + 3 < hidden) {
-            const float4 a = sum_splits<float4, 16>(partial + t * hidden + c0, splits, plane,
-                                                   *reinterpret_cast<const float4*>(xrow + c0));
+    const bool vec = (hidden & 3) == 0 && c0 + 3 < hidden;
+    // rows t and t + gridDim.y per iteration: both rows' loads in flight before either is finished (few split planes
+    // at these sizes, so a 2-deep split batch keeps the registers at 4 CTAs / SM)
+    for (int64_t t = blockIdx.y; t < T_; t += 2 * (int64_t)gridDim.y) {
+        const int64_t t2 = t + gridDim.y;
+        const bool two = t2 < T_;
+        float v[4], u[4];
+        if (vec) {
+            const float4 a = sum_splits<float4, 2>(partial + t * hidden + c0, splits, plane,
+                                                  *reinterpret_cast<const float4*>(x + t * hidden + c0));
+            float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (two)
+                b = sum_splits<float4, 2>(partial + t2 * hidden + c0, splits, plane,
+                                          *reinterpret_cast<const float4*>(x + t2 * hidden + c0));
             v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+            u[0] = b.x, u[1] = b.y, u[2] = b.z, u[3] = b.w;
         } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                v[e] = 0.f;
+                v[e] = u[e] = 0.f;
                 if (c0 + e < hidden) {
-                    float acc = xrow[c0 + e];
-                    for (int s = 0; s < splits; ++s) acc += partial[s * plane + t * hidden + c0 + e];
+                    float acc = x[t * hidden + c0 + e];
+                    for (int s2 = 0; s2 < splits; ++s2) acc += partial[s2 * plane + t * hidden + c0 + e];
                     v[e] = acc;
+                    if (two) {
+                        float acc2 = x[t2 * hidden + c0 + e];
+                        for (int s2 = 0; s2 < splits; ++s2) acc2 += partial[s2 * plane + t2 * hidden + c0 + e];
+                        u[e] = acc2;
+                    }
                 }
             }
         }
-        finish_row_block(xrow, w, xb + t * hidden, ssp + t * nb, v, c0, hidden, red, err);
+        finish_row_block(x + t * hidden, w, xb + t * hidden, ssp + t * nb, v, c0, hidden, red, err);
+        if (two) finish_row_block(x + t2 * hidden, w, xb + t2 * hidden, ssp + t2 * nb, u, c0, hidden, red, err);
     }
     tl_exit(tl);
 }
@@ -468,8 +483,8 @@ __global__ void __launch_bounds__(256) qkv_epilogue_kernel(const float* partial,
             }
         }
         __syncthreads();
+        const float rs = s_rs;
         for (int n = 2 * (int)(blockIdx.x * blockDim.x + threadIdx.x); n < N; n += 2 * (int)(gridDim.x * blockDim.x)) {
-            const float rs = s_rs;
             const float2 xs = sum_splits(partial + t * N + n, splits, plane, make_float2(0.f, 0.f));  // n even: 8 B
             const float x0 = xs.x * rs, x1 = xs.y * rs;
             if (n >= qd + kvd) {  // V: copied as is
@@ -793,7 +808,7 @@ void launch_residual(float* x, const float* partial, int splits, int T_, int hid
         DISPATCH_DT(dt, launch_k(residual_kernel<T>, grid, 256, 0, s, x, partial, splits, plane, hidden, w, (T*)xb,
                                  ssp, err, tl));
     } else {
-        const dim3 grid(row_ctas(hidden), (unsigned)std::min(T_, std::max(1, 148 * 8 / row_ctas(hidden))));
+        const dim3 grid(row_ctas(hidden), (unsigned)std::min(T_, std::max(1, 148 * 4 / row_ctas(hidden))));
         DISPATCH_DT(dt, launch_k(residual_rows_kernel<T>, grid, 256, 0, s, x, partial, splits, plane, T_, hidden, w,
                                  (T*)xb, ssp, err, tl));
     }

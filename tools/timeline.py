@@ -15,11 +15,23 @@ from paper_2410_07590_b200 import turbokv as T  # noqa: E402
 def main(steps=10):
     cfg = T.ModelConfig.qwen2_7b_like()
     c3 = os.environ.get("TL_C3") == "1"  # C3: batch 32 x (20 x 800-token chunks + 64-token query), one step = a batch
-    eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=(160 * 832 if c3 else 16 * 512 * 2) + 65536,
+    eng = T.Engine(cfg, 42, dtype="bf16", store_capacity_tokens=(160 * 832 if os.environ.get("TL_C3") == "1" else 64 * 512) + 65536,
                    exact_fingerprint=0)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
-    if c3:
+    c5 = os.environ.get("TL_C5") == "1"  # C5: one block-diagonal ingest forward of 32 x 512-token chunks = a step
+    if c5:
+        steps = 3
+        rng = np.random.default_rng(0xC5)
+        rounds = iter(range(1 << 30))
+
+        def step():
+            r = next(rounds)
+            pays = [rng.integers(97, 123, 510).astype(np.int32) for _ in range(32)]
+            ids = eng.ingest_chunks(pays)
+            for i in ids:
+                eng.store_evict(i)
+    elif c3:
         steps = 2
         rng = np.random.default_rng(0xC3)
         cids = eng.ingest_chunks([rng.integers(97, 123, 798).astype(np.int32) for _ in range(160)])
@@ -42,10 +54,10 @@ def main(steps=10):
             eng.prefill_query_device(ctx, dq.data_ptr(), len(query), dl.data_ptr())
             ctx.close()
 
-    for _ in range(2 if c3 else 5):
+    for _ in range(2 if (c3 or c5) else 5):
         step()
     ts = []
-    for _ in range(3 if c3 else 20):
+    for _ in range(3 if (c3 or c5) else 20):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         step()
