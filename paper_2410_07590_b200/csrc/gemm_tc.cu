@@ -32,6 +32,7 @@ namespace tkv {
 namespace {
 
 constexpr int BK = 64, THREADS = 128;
+constexpr int EPI_LD = 66;  // row stride (floats) of the normal-tiling partial epilogue's per-warp staging block
 #ifndef PRE_PF_MB_DEFAULT
 #define PRE_PF_MB_DEFAULT 0
 #endif
@@ -51,7 +52,7 @@ struct Knobs {
     int pre_pf_mb = PRE_PF_MB_DEFAULT;
     // normal (> 128 tokens) tiling: nsnp 128-column halves per MMA (UMMA N = 128 * nsnp); N = 256 halves the
     // shared-memory traffic per FLOP of the SS-mode MMA (the 128 x 128 tile is smem-bandwidth bound at ~50 %)
-    int nsnp = 2, ns_smem_kb = 208;
+    int nsnp = 2, ns_smem_kb = 226;  // 3 stages of 64 KB + the partial epilogue staging block: 227 KB
     // normal tiling: nsmp 128-row activation tiles per unit share each weight tile (M = 128 * nsmp per unit):
     // the per-FLOP L2 -> smem traffic drops by 1/3 at nsmp = 2 (A 32 KB + W 32 KB per 64-deep k-block for
     // 2 x 128 x 256 outputs); the two 128 x 256 fp32 accumulators fill TMEM, so a unit's epilogue is not
@@ -609,24 +610,38 @@ __global__ void __launch_bounds__(THREADS_P)
                 if (EPI == EPI_PARTIAL) {
                     float* out = g.partial + (int64_t)z * g.M * g.N + (int64_t)m * g.N;
                     if (g.skip_epi) continue;  // timing experiment only (TKV_GEMM_SKIP_EPI): results invalid
+                    // 64 columns per tcgen05.wait::ld, staged through this warp's padded smem block (row stride 66
+                    // floats: conflict-free 8-byte writes) and written back row by row as 256-byte segments: the
+                    // row-per-lane float4 stores cost one L2 transaction per 16 bytes (~23 K cycles per 256 x 256 unit)
+                    float* stg = reinterpret_cast<float*>(smem + g.scratch_off) + lg * 32 * EPI_LD;
 #pragma unroll 1
-                    for (int c = 0; c < 128; c += 16) {
-                        uint32_t r[16];
-                        tmem_ld16(acc + (uint32_t)c, r);
-                        if (m < g.M) {
-                            const int n = n0 + c;
-                            if (n + 16 <= g.N && (g.N % 4) == 0) {
-                                float4* o4 = reinterpret_cast<float4*>(out + n);
+                    for (int c = 0; c < 128; c += 64) {
+                        uint32_t r[64];
 #pragma unroll
-                                for (int j = 0; j < 4; ++j)
-                                    o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-                            } else {
+                        for (int q4 = 0; q4 < 4; ++q4)
+                            tmem_ld16_nowait(acc + (uint32_t)(c + 16 * q4), *reinterpret_cast<uint32_t(*)[16]>(r + 16 * q4));
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                                for (int j = 0; j < 16; ++j)
-                                    if (n + j < g.N) out[n + j] = __uint_as_float(r[j]);
+                        for (int j = 0; j < 32; ++j)
+                            *reinterpret_cast<float2*>(stg + lane * EPI_LD + 2 * j) =
+                                make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+                        __syncwarp();
+                        const int mrow0 = m0 + mi * 128 + lg * 32, n = n0 + c + 2 * lane;
+                        float* outz = g.partial + (int64_t)z * g.M * g.N;
+#pragma unroll 4
+                        for (int rr = 0; rr < 32; ++rr) {
+                            const float2 v2 = *reinterpret_cast<const float2*>(stg + rr * EPI_LD + 2 * lane);
+                            const int mr = mrow0 + rr;
+                            if (mr < g.M) {
+                                float* o = outz + (int64_t)mr * g.N + n;
+                                if (n + 1 < g.N && (g.N % 2) == 0) *reinterpret_cast<float2*>(o) = v2;
+                                else {
+                                    if (n < g.N) o[0] = v2.x;
+                                    if (n + 1 < g.N) o[1] = v2.y;
+                                }
                             }
                         }
+                        __syncwarp();
                     }
                 } else {
                     const int inter = g.N / 2;
@@ -635,17 +650,25 @@ __global__ void __launch_bounds__(THREADS_P)
                         if (p != 0) continue;
                         const int i0 = nt * 128;
                         const float sc = m < g.M ? row_scale(g.ssp, g.nb, m, g.K, g.eps) : 0.f;
-#pragma unroll 1
+                        // software-pipelined: the next 16 (gate, up) column pairs load while this chunk's SwiGLU runs
+                        // (one load pair + wait per chunk made the 256 x 256 unit's epilogue ~35 K cycles)
+                        uint32_t gr[2][16], ur[2][16];
+                        tmem_ld16_nowait(acc, gr[0]);
+                        tmem_ld16_nowait(acc + 128u, ur[0]);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
                         for (int c = 0; c < 128; c += 16) {
-                            uint32_t gr[16], ur[16];
-                            tmem_ld16_nowait(acc + (uint32_t)c, gr);
-                            tmem_ld16_nowait(acc + (uint32_t)(128 + c), ur);
-                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                            const int cb = (c >> 4) & 1;
+                            if (c + 16 < 128) {
+                                tmem_ld16_nowait(acc + (uint32_t)(c + 16), gr[cb ^ 1]);
+                                tmem_ld16_nowait(acc + (uint32_t)(128 + c + 16), ur[cb ^ 1]);
+                            }
                             if (m < g.M) {
                                 __align__(16) __nv_bfloat16 o[16];
 #pragma unroll
                                 for (int j = 0; j < 16; ++j)
-                                    o[j] = __float2bfloat16_rn(silu(sc * __uint_as_float(gr[j])) * (sc * __uint_as_float(ur[j])));
+                                    o[j] = __float2bfloat16_rn(silu_fast(sc * __uint_as_float(gr[cb][j])) *
+                                                               (sc * __uint_as_float(ur[cb][j])));
                                 __nv_bfloat16* dst = g.act + (int64_t)m * inter + i0 + c;
                                 if (i0 + c + 16 <= inter && (inter % 8) == 0) {
                                     reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<uint4*>(o)[0];
@@ -655,6 +678,7 @@ __global__ void __launch_bounds__(THREADS_P)
                                         if (i0 + c + j < inter) dst[j] = o[j];
                                 }
                             }
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                         }
                         continue;
                     }
@@ -820,7 +844,8 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     }
     g.tmem_cols = 32;
     while (g.tmem_cols < (uint32_t)g.nbuf * g.acc_cols) g.tmem_cols <<= 1;
-    const uint32_t scratch = !(swap && swiglu_act) ? 0
+    const uint32_t scratch = (!swap && !swiglu_act) ? (uint32_t)(4 * 32 * EPI_LD * 4)  // partial epilogue staging
+                             : !(swap && swiglu_act) ? 0
                              : gu128 ? 1024u + 4096u  // token scales + the four warps' transpose blocks
                                      : (uint32_t)((64 * (XC + 1) + g.ntok) * 4 + 1023) / 1024 * 1024;
     const int cps = (swap && gu128) ? 1 : gemm_tc_ctas_per_sm(M);
