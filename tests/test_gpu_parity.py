@@ -707,30 +707,28 @@ def test_large_m_gemm_tilings_agree(tmp_path, env):
     assert_close(outs[1], outs[0], BF16_TOL)
 
 
-def test_batched_attention_split_k_matches(golden, tmp_path):
-    """TKV_BATCH_ATTN_SPLITS=3: the batched single-launch attention with split-K partials and the request-aware
-    combine gives the unsplit batched logits (bf16 tolerance); fresh processes (the knob is read at creation)."""
-    import subprocess
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    script = tmp_path / "run.py"
-    script.write_text(r"""
-import sys, numpy as np
-sys.path.insert(0, %r)
-import oracle as O
-from paper_2410_07590_b200 import turbokv as T
-eng = T.Engine(T.ModelConfig(**vars(O.qwen_layers(2))), 7, dtype="bf16", store_capacity_tokens=1 << 16, flags=0x20)
-ids = eng.ingest_chunks([O.random_text_tokens(800 + i, 510) for i in range(6)])
-ctxs = [eng.assemble(ids[i:i + 3], T.PositionMode.Reordered) for i in range(3)]
-qs = [O.random_text_tokens(801 + i, 40 + 11 * i) for i in range(3)]
-np.save(sys.argv[1], eng.prefill_query_batch(ctxs, qs))
-""" % root)
-    outs = []
-    for e in ({"TKV_BATCH_ATTN_SPLITS": "1"}, {"TKV_BATCH_ATTN_SPLITS": "3"}):
-        path = tmp_path / f"o{len(outs)}.npy"
-        subprocess.run([sys.executable, str(script), str(path)], check=True, env={**os.environ, **e}, timeout=300)
-        outs.append(np.load(path))
-    for a, b in zip(outs[1], outs[0]):
-        assert_close(a, b, BF16_TOL)
+def test_batched_attention_split_k_matches():
+    """The batched single-launch attention with split-K partials and the request-aware combine: 10 requests x
+    (3 x 800-token chunks + a 64-token query) give 160 (request, kv head, row tile) CTAs, for which the automatic
+    split picker (attn_tc_batch_pick_splits) chooses 2 splits to fill the last wave; every request's logits equal its
+    own prefill_query (bf16 tolerance, argmax checked)."""
+    cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
+    eng = engine(cfg, 7, "bf16", flags=0x20)  # TKV_FLAG_BATCH_ATTN
+    ids = eng.ingest_chunks([O.random_text_tokens(800 + i, 798) for i in range(12)])
+    picks = [[ids[(r + k) % 12] for k in range(3)] for r in range(10)]
+    qs = [O.random_text_tokens(860 + r, 64) for r in range(10)]
+    ctxs = [eng.assemble(p) for p in picks]
+    eng.kernel_timeline(True)
+    batched = eng.prefill_query_batch(ctxs, qs)
+    _, cls = eng.kernel_timeline(False)
+    assert (cls == T.Engine.TIMELINE_CLASSES.index("attention")).sum() == 2 * cfg.layer_num  # attention + split merge
+    for c in ctxs:
+        c.close()
+    for r in (0, 4, 9):
+        with eng.assemble(picks[r]) as single:
+            ref = eng.prefill_query(single, qs[r])[0]
+        assert_close(batched[r], ref, BF16_TOL)
+        assert_argmax(batched[r], ref, BF16_TOL)
 
 
 def test_batched_prefill_many_tokens_matches_per_request():
