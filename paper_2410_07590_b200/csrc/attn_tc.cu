@@ -837,7 +837,8 @@ __global__ void __launch_bounds__(256) attn_tc_combine_batch_kernel(const __nv_b
                                                                     const float2* __restrict__ ws_ml,
                                                                     __nv_bfloat16* __restrict__ out, int* err,
                                                                     const AttnReq* __restrict__ reqs, int H, int Hkv,
-                                                                    int splits, int groups_x, int ngroups) {
+                                                                    int splits, int groups_x, int ngroups,
+                                                                    unsigned long long* tl) {
     pdl_launch();
     const int lane = threadIdx.x & 31;
     const int grow = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -846,6 +847,7 @@ __global__ void __launch_bounds__(256) attn_tc_combine_batch_kernel(const __nv_b
     const int rr = (gid % groups_x) * RG + i;
     const int group = H / Hkv;
     pdl_wait();
+    tl_wait(tl);
     const AttnReq R = reqs[req];
     if (rr >= R.n * group) return;  // warp-uniform
     const int64_t plane = (int64_t)ngroups * RG;
@@ -878,6 +880,7 @@ __global__ void __launch_bounds__(256) attn_tc_combine_batch_kernel(const __nv_b
     const int64_t mo = (int64_t)(R.tok0 + rr / group) * H + g * group + rr % group;
     reinterpret_cast<uint2*>(out + mo * D)[lane] =
         make_uint2(bf16x2_bits(acc[0] * inv, acc[1] * inv), bf16x2_bits(acc[2] * inv, acc[3] * inv));
+    tl_exit(tl);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -960,7 +963,7 @@ void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* m
         const int ngroups = groups_x * Hkv * n_req;
         launch_k(attn_tc_combine_batch_kernel, dim3((ngroups * RG + 7) / 8), dim3(256), 0, s,
                  reinterpret_cast<const __nv_bfloat16*>(ws.o), reinterpret_cast<const float2*>(ws.ml),
-                 (__nv_bfloat16*)out, err, reqs, H, Hkv, a.splits, groups_x, ngroups);
+                 (__nv_bfloat16*)out, err, reqs, H, Hkv, a.splits, groups_x, ngroups, tl_take());
         TKV_CUDA(cudaGetLastError());
     }
 }
