@@ -32,7 +32,8 @@ namespace tkv {
 namespace {
 
 constexpr int BK = 64, THREADS = 128;
-constexpr int EPI_LD = 66;  // row stride (floats) of the normal-tiling partial epilogue's per-warp staging block
+constexpr int EPI_LD = 33;  // row stride (floats) of the normal-tiling partial epilogue's per-warp staging block
+                            // (odd: the 4-byte row-per-lane writes and the row reads are both conflict-free)
 #ifndef PRE_PF_MB_DEFAULT
 #define PRE_PF_MB_DEFAULT 0
 #endif
@@ -284,7 +285,10 @@ __device__ __forceinline__ void gtrace(unsigned long long* t, int slot) {
 }
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
-constexpr int THREADS_P = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int THREADS_P = 192;  // swapped tiling: warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+// normal (large-M) tiling: warps 2-9 = epilogue, two per TMEM lane quadrant, each on half the columns of a unit (the
+// 256 x 256 unit's epilogue is not overlapped with the next mainloop: TMEM holds only the one accumulator)
+constexpr int threads_for(bool swap) { return swap ? THREADS_P : THREADS_P + 128; }
 constexpr int XC = 32;          // swapped SwiGLU epilogue: token columns per gate/up exchange pass
 
 __device__ __forceinline__ void unit_coords(const GemmArgs& g, int u, int& nt, int& mt, int& z) {
@@ -307,7 +311,7 @@ __device__ __forceinline__ void unit_coords(const GemmArgs& g, int u, int& nt, i
 // flows across units without draining; two TMEM accumulators let the epilogue of unit i overlap the
 // mainloop of unit i+1.
 template <bool SWAP, int EPI>
-__global__ void __launch_bounds__(THREADS_P)
+__global__ void __launch_bounds__(threads_for(SWAP))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                    const __grid_constant__ CUtensorMap tmN, GemmArgs g) {
     pdl_launch();
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(THREADS_P)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128);
+            mbar_init(&tempty[b], threads_for(SWAP) - 64);  // every epilogue thread
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -474,7 +478,8 @@ __global__ void __launch_bounds__(THREADS_P)
         if (g.tl && threadIdx.x == 64) atomicMin(g.tl, gtimer_ns());  // the predecessor grid has completed
         const int lg = warp & 3;
         const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
-        const int et = threadIdx.x - 64;  // 0..127
+        const int et = threadIdx.x - 64;  // 0..127 (swapped) / 0..255 (normal)
+        const int half = SWAP ? 0 : (warp - 2) >> 2;  // normal tiling: which half of a unit's columns this warp owns
         if (SWAP && EPI == EPI_SWIGLU && g.gub == 128) {
             // folded mlp_norm scale of every token (swapped tiling: all units cover tokens [0, ntok)), once per CTA
             float* ts = reinterpret_cast<float*>(smem + g.scratch_off);
@@ -613,33 +618,24 @@ __global__ void __launch_bounds__(THREADS_P)
                     // 64 columns per tcgen05.wait::ld, staged through this warp's padded smem block (row stride 66
                     // floats: conflict-free 8-byte writes) and written back row by row as 256-byte segments: the
                     // row-per-lane float4 stores cost one L2 transaction per 16 bytes (~23 K cycles per 256 x 256 unit)
-                    float* stg = reinterpret_cast<float*>(smem + g.scratch_off) + lg * 32 * EPI_LD;
+                    float* stg = reinterpret_cast<float*>(smem + g.scratch_off) + (warp - 2) * 32 * EPI_LD;
+                    // this warp's half of the subtile: 64 columns, two 32-column chunks through the staging block
 #pragma unroll 1
-                    for (int c = 0; c < 128; c += 64) {
-                        uint32_t r[64];
-#pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4)
-                            tmem_ld16_nowait(acc + (uint32_t)(c + 16 * q4), *reinterpret_cast<uint32_t(*)[16]>(r + 16 * q4));
+                    for (int c = 64 * half; c < 64 * half + 64; c += 32) {
+                        uint32_t r[32];
+                        tmem_ld16_nowait(acc + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(r));
+                        tmem_ld16_nowait(acc + (uint32_t)(c + 16), *reinterpret_cast<uint32_t(*)[16]>(r + 16));
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            *reinterpret_cast<float2*>(stg + lane * EPI_LD + 2 * j) =
-                                make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+                        for (int j = 0; j < 32; ++j) stg[lane * EPI_LD + j] = __uint_as_float(r[j]);
                         __syncwarp();
-                        const int mrow0 = m0 + mi * 128 + lg * 32, n = n0 + c + 2 * lane;
+                        const int mrow0 = m0 + mi * 128 + lg * 32, n = n0 + c + lane;
                         float* outz = g.partial + (int64_t)z * g.M * g.N;
 #pragma unroll 4
                         for (int rr = 0; rr < 32; ++rr) {
-                            const float2 v2 = *reinterpret_cast<const float2*>(stg + rr * EPI_LD + 2 * lane);
+                            const float v = stg[rr * EPI_LD + lane];
                             const int mr = mrow0 + rr;
-                            if (mr < g.M) {
-                                float* o = outz + (int64_t)mr * g.N + n;
-                                if (n + 1 < g.N && (g.N % 2) == 0) *reinterpret_cast<float2*>(o) = v2;
-                                else {
-                                    if (n < g.N) o[0] = v2.x;
-                                    if (n + 1 < g.N) o[1] = v2.y;
-                                }
-                            }
+                            if (mr < g.M && n < g.N) outz[(int64_t)mr * g.N + n] = v;  // 128-byte row segments
                         }
                         __syncwarp();
                     }
@@ -653,13 +649,15 @@ __global__ void __launch_bounds__(THREADS_P)
                         // software-pipelined: the next 16 (gate, up) column pairs load while this chunk's SwiGLU runs
                         // (one load pair + wait per chunk made the 256 x 256 unit's epilogue ~35 K cycles)
                         uint32_t gr[2][16], ur[2][16];
-                        tmem_ld16_nowait(acc, gr[0]);
-                        tmem_ld16_nowait(acc + 128u, ur[0]);
+                        const int cs = 64 * half;  // this warp's 64 (gate, up) column pairs
+                        tmem_ld16_nowait(acc + (uint32_t)cs, gr[0]);
+                        tmem_ld16_nowait(acc + (uint32_t)(128 + cs), ur[0]);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                        for (int c = 0; c < 128; c += 16) {
-                            const int cb = (c >> 4) & 1;
-                            if (c + 16 < 128) {
+                        for (int cc = 0; cc < 64; cc += 16) {
+                            const int c = cs + cc;
+                            const int cb = (cc >> 4) & 1;
+                            if (cc + 16 < 64) {
                                 tmem_ld16_nowait(acc + (uint32_t)(c + 16), gr[cb ^ 1]);
                                 tmem_ld16_nowait(acc + (uint32_t)(128 + c + 16), ur[cb ^ 1]);
                             }
@@ -685,7 +683,7 @@ __global__ void __launch_bounds__(THREADS_P)
                     const int i0 = (n0 / 128) * 64;
                     const float sc = m < g.M ? row_scale(g.ssp, g.nb, m, g.K, g.eps) : 0.f;  // folded mlp_norm
 #pragma unroll 1
-                    for (int c = 0; c < 64; c += 16) {
+                    for (int c = 32 * half; c < 32 * half + 32; c += 16) {
                         uint32_t gr[16], ur[16];
                         tmem_ld16(acc + (uint32_t)c, gr);
                         tmem_ld16(acc + (uint32_t)(64 + c), ur);
@@ -759,12 +757,12 @@ void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const CUtensorMap& t
               size_t smem, cudaStream_t s) {
     TKV_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<SWAP, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (SWAP || g.cl <= 1) {
-        launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(THREADS_P), smem, s, ta, tw, tn, g);
+        launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(threads_for(SWAP)), smem, s, ta, tw, tn, g);
         return;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(THREADS_P);
+    cfg.blockDim = dim3(threads_for(SWAP));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[2];
@@ -844,7 +842,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     }
     g.tmem_cols = 32;
     while (g.tmem_cols < (uint32_t)g.nbuf * g.acc_cols) g.tmem_cols <<= 1;
-    const uint32_t scratch = (!swap && !swiglu_act) ? (uint32_t)(4 * 32 * EPI_LD * 4)  // partial epilogue staging
+    const uint32_t scratch = (!swap && !swiglu_act) ? (uint32_t)(8 * 32 * EPI_LD * 4)  // partial epilogue staging
                              : !(swap && swiglu_act) ? 0
                              : gu128 ? 1024u + 4096u  // token scales + the four warps' transpose blocks
                                      : (uint32_t)((64 * (XC + 1) + g.ntok) * 4 + 1023) / 1024 * 1024;
