@@ -536,6 +536,7 @@ struct tkv_engine {
     // L2 warm-up of the O-proj weights and the head of gate/up, issued by each attention CTA once its K/V loads are
     // out (query-prefill forwards): C2 step 3.60 -> 3.54 ms at 40 MB (26 / 64 MB: 3.55 / 3.54, attention slower at 64)
     size_t l2_prefetch_bytes = (size_t)40 << 20;  // TKV_L2_PREFETCH_MB (tuning knob)
+    int l2_pf_next_qkv = 0;                       // TKV_L2_PF_NEXT_QKV (tuning): second region = next layer's QKV
     int skip_mask = 0;             // TKV_TIMING_SKIP: drop kernels for cost attribution (results invalid)
     int trace_layer = -1;          // TKV_TRACE_LAYER: clock64 pipeline trace of that layer's attention launch
     int attn_split_override = 0;   // TKV_ATTN_SPLITS: force the tcgen05 attention's split-K count
@@ -717,8 +718,13 @@ void tkv_engine::attend_layer(int64_t l, int T, const void* qrows, tkv_context* 
             const size_t ob = (size_t)hid * qd * es, gb = (size_t)2 * I * hid * es;
             pf.ptr[0] = w_o[l];
             pf.bytes[0] = std::min(ob, l2_prefetch_bytes);
-            pf.ptr[1] = w_gu[l];
-            pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
+            if (l2_pf_next_qkv && l + 1 < L) {  // TUNING: the next layer's QKV weights instead of the head of gate/up
+                pf.ptr[1] = w_qkv[l + 1];
+                pf.bytes[1] = std::min((size_t)nqkv * hid * es, l2_prefetch_bytes - pf.bytes[0]);
+            } else {
+                pf.ptr[1] = w_gu[l];
+                pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
+            }
         }
         if (trace_layer == (int)l) attn_trace_enable(true, nullptr);
         launch_attention_tc(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
@@ -1464,6 +1470,7 @@ static tkv_status create_engine(const tkv_model_config* cfg, uint64_t seed, cons
         // Tuning / cost-attribution knobs (tools/*.sh). Compiled into TUNING builds only (make TUNING=1): several
         // of them skip work or change numerics, so the release library never reads them.
         if (const char* pfm = getenv("TKV_L2_PREFETCH_MB")) e->l2_prefetch_bytes = (size_t)atol(pfm) << 20;
+        if (const char* nq = getenv("TKV_L2_PF_NEXT_QKV")) e->l2_pf_next_qkv = atoi(nq);
         if (const char* sk = getenv("TKV_TIMING_SKIP")) e->skip_mask = atoi(sk);
         if (const char* tl = getenv("TKV_TRACE_LAYER")) e->trace_layer = atoi(tl);
         if (const char* as = getenv("TKV_ATTN_SPLITS")) e->attn_split_override = std::min(32, std::max(0, atoi(as)));
