@@ -85,7 +85,8 @@ typedef struct {
 #define TKV_FLAG_SIMT_ATTN 0x2    /* bf16: use the SIMT attention instead of tcgen05              */
 /* 0x4: reserved */
 #define TKV_FLAG_NO_PDL 0x8       /* launch kernels without programmatic dependent launch          */
-#define TKV_FLAG_L2_PREFETCH 0x10  /* reserved (attention-time L2 weight prefetch: measured no gain) */
+#define TKV_FLAG_L2_PREFETCH 0x10  /* reserved (the attention-time L2 weight prefetch is on by default) */
+#define TKV_FLAG_NO_GRAPHS 0x100   /* launch the query-prefill forward kernel by kernel (no CUDA-graph capture / replay) */
 #define TKV_FLAG_BATCH_ATTN 0x20   /* batched prefill: one attention launch even when the batch cannot fill the GPU */
 #define TKV_FLAG_LAYER_KERNEL 0x80 /* reserved (the persistent layer-kernel experiment was measured slower and removed) */
 #define TKV_FLAG_DECODE_ATTN 0x40 /* bf16: decode-sized (<= 16 rows / kv head) forwards use the split-K mma.sync kernel */

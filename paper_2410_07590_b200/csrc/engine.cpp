@@ -19,6 +19,7 @@
 #include <cstring>
 #include <fstream>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <set>
@@ -244,6 +245,10 @@ static std::string hex_id(uint64_t id) {
 struct DevMem {
     void* p = nullptr;
     size_t n = 0;
+    static std::atomic<uint64_t>& generation() {
+        static std::atomic<uint64_t> g{0};
+        return g;
+    }
     DevMem() = default;
     DevMem(const DevMem&) = delete;
     DevMem& operator=(const DevMem&) = delete;
@@ -255,6 +260,7 @@ struct DevMem {
     }
     void* ensure(size_t bytes) {
         if (bytes <= n) return p;
+        ++generation();  // captured forward graphs hold these pointers: a reallocation retires them
         release();
         size_t want = std::max(bytes, (size_t)256);
         TKV_CUDA(cudaMalloc(&p, want));
@@ -321,6 +327,7 @@ unsigned long long* tl_take() {
     return g_tl.base + 2 * g_tl.n++;
 }
 void tl_set_class(int cls) { g_tl.cls = cls; }
+bool tl_armed() { return g_tl.base != nullptr; }
 static const char* kProfNames[PC_N] = {"gather_rope", "attention", "gemm", "epilogue", "other"};
 
 struct Chunk {
@@ -615,6 +622,17 @@ struct tkv_engine {
         const EpiReq* epi_reqs = nullptr;  // device table of the batched QKV epilogue (one launch per layer)
     };
     void forward(const Fwd& f);
+    // CUDA-graph replay of the query-prefill forward (extend): the second forward with the same key (context cache,
+    // row offset, token count, input / staging / output buffers, RoPE table, buffer generation) is captured with its
+    // PDL edges, later ones replay the graph (launch handoffs 0.90 -> 0.61 us in tools/micro/pdl_gap.cu).
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+    };
+    std::map<std::vector<uint64_t>, GraphEntry> graphs;
+    std::set<std::vector<uint64_t>> graph_seen;
+    bool graphs_ok = true;
+    void forward_graph(const Fwd& f);
     void attend_layer(int64_t l, int T, const void* qrows, tkv_context* actx, const int32_t* lo, const int32_t* hi,
                       void* out, int arows, int aTk, int kv_ready);
     void check_err(const char* where);
@@ -667,6 +685,7 @@ tkv_engine::~tkv_engine() {
         cudaEventDestroy(r.b);
     }
     for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -734,6 +753,59 @@ void tkv_engine::attend_layer(int64_t l, int T, const void* qrows, tkv_context* 
         launch_attention_simt(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
                               aTk, (int)H, (int)Hkv, (int)d, splits, ws, err.as<int>(), dt, stream);
     }
+}
+
+void tkv_engine::forward_graph(const Fwd& f) {
+    const bool eligible = graphs_ok && !(opts.flags & TKV_FLAG_NO_GRAPHS) && !prof_on && trace_layer < 0 && !tl_armed() &&
+                          f.reqs.empty() && !f.kv_only && !f.sc.page && f.ctx;
+    if (!eligible) {
+        forward(f);
+        return;
+    }
+    const std::vector<uint64_t> key = {(uint64_t)(uintptr_t)f.ctx->kv, (uint64_t)f.ctx->cap, (uint64_t)f.row0,
+                                       (uint64_t)f.T, (uint64_t)(uintptr_t)f.tok, (uint64_t)(uintptr_t)f.pos,
+                                       (uint64_t)(uintptr_t)f.lo, (uint64_t)(uintptr_t)f.hi, (uint64_t)(uintptr_t)rope.p,
+                                       (uint64_t)(uintptr_t)logits.p, DevMem::generation().load(), (uint64_t)f.logits};
+    auto it = graphs.find(key);
+    if (it != graphs.end()) {
+        TKV_CUDA(cudaGraphLaunch(it->second.exec, stream));
+        launches += it->second.launches;
+        return;
+    }
+    if (!graph_seen.count(key)) {  // first sighting: run it (sizes every buffer), capture on the next one
+        if (graph_seen.size() >= 64) graph_seen.clear();
+        graph_seen.insert(key);
+        forward(f);
+        return;
+    }
+    if (graphs.size() >= 16) {  // bounded cache
+        for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
+        graphs.clear();
+    }
+    const int64_t l0 = launches;
+    TKV_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        forward(f);
+    } catch (...) {
+        cudaGraph_t dropped = nullptr;
+        cudaStreamEndCapture(stream, &dropped);
+        if (dropped) cudaGraphDestroy(dropped);
+        throw;
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(stream, &g);
+    cudaGraphExec_t ex = nullptr;
+    if (ce != cudaSuccess || !g || cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) {  // not capturable here: no graphs
+        (void)cudaGetLastError();
+        if (g) cudaGraphDestroy(g);
+        graphs_ok = false;
+        launches = l0;
+        forward(f);
+        return;
+    }
+    cudaGraphDestroy(g);
+    graphs[key] = GraphEntry{ex, launches - l0};
+    TKV_CUDA(cudaGraphLaunch(ex, stream));
 }
 
 void tkv_engine::forward(const Fwd& f) {
@@ -995,7 +1067,7 @@ void extend(tkv_engine* e, tkv_context* c, const int32_t* host_tok, const int32_
     f.lo = e->p_lo;
     f.hi = e->p_hi;
     f.logits = true;
-    e->forward(f);
+    e->forward_graph(f);
     if (dev_logits)
         TKV_CUDA(cudaMemcpyAsync(dev_logits, e->logits.p, e->V * 4, cudaMemcpyDeviceToDevice, e->stream));
     if (host_logits) {

@@ -138,7 +138,8 @@ void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap);
 // merge, residual / QKV epilogues, embed, lm_head, KV gather) takes the next slot [2] of globaltimer ns (first CTA past
 // griddepcontrol.wait, last warp done), tagged with the engine's current launch class. Process-global; null when off.
 unsigned long long* tl_take();
-void tl_set_class(int cls);  // debug: CTA 0 per-stage clock64 trace
+void tl_set_class(int cls);
+bool tl_armed();  // debug: CTA 0 per-stage clock64 trace
 void set_gemm_next_pf(int kblocks);
 void set_gemm_nsmp(int mp);
 void set_gemm_pre_pf_mb(int mb);  // TUNING: pre-wait weight L2 prefetch budget per launch (MB, 0 = off)

@@ -70,6 +70,7 @@ class Dtype(enum.IntEnum):
 FLAG_SIMT_GEMM = 0x1
 FLAG_SIMT_ATTN = 0x2
 FLAG_NO_PDL = 0x8
+FLAG_NO_GRAPHS = 0x100
 FLAG_BATCH_ATTN = 0x20
 FLAG_DECODE_ATTN = 0x40
 

@@ -782,3 +782,32 @@ def test_kernel_timeline_covers_the_forward():
         eng.prefill_query(ctx, q)
     tl2, _ = eng.kernel_timeline(False)
     assert len(tl2) == 0
+
+
+def test_graph_replay_is_bitwise_the_kernel_chain():
+    """CUDA-graph replay of the query-prefill forward (captured on the second forward with the same shape and
+    buffers, replayed afterwards) gives bitwise the logits and cache rows of the kernel-by-kernel chain
+    (TKV_FLAG_NO_GRAPHS), over recycled contexts, device-token prefill, and a changed query."""
+    import torch
+    cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
+    outs = {}
+    for flags in (0, T.FLAG_NO_GRAPHS):
+        eng = engine(cfg, 5, "bf16", flags=flags)
+        ids = eng.ingest_chunks([O.random_text_tokens(700 + i, 300) for i in range(4)])
+        res = []
+        for rep in range(4):
+            q = O.random_text_tokens(90 + (rep // 3), 40)  # the 4th request changes the query tokens
+            with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+                res.append(eng.prefill_query(ctx, q)[0].copy())
+                res.append(ctx.read_kv(1, "k", rotated=True)[-40:].copy())
+        dq = torch.from_numpy(O.random_text_tokens(91, 40)).cuda()
+        dl = torch.empty(cfg.vocab_size, dtype=torch.float32, device="cuda")
+        for rep in range(3):
+            with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+                eng.prefill_query_device(ctx, dq.data_ptr(), 40, dl.data_ptr())
+                eng.check()
+                res.append(dl.cpu().numpy().copy())
+        outs[flags] = res
+        eng.close()
+    for a, b in zip(outs[0], outs[T.FLAG_NO_GRAPHS]):
+        assert np.array_equal(a, b)
