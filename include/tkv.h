@@ -17,6 +17,8 @@
  *    exception classes (include/turbokv/errors.hpp:10-67).
  *  - There is no CPU fallback: with no usable sm_100 device,
  *    tkv_engine_create fails with TKV_ERR_CUDA.
+ *  - An engine (and its contexts) is driven from one host thread at a time, like the reference Engine: its
+ *    activation buffers, staging ring and captured forward graphs are per engine. Separate engines are independent.
  */
 #ifndef TKV_H
 #define TKV_H
