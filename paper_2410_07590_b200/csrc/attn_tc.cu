@@ -21,8 +21,8 @@
 // every forward does not release its dependents before its own griddepcontrol.wait), so their TMA loads
 // are issued BEFORE griddepcontrol.wait and overlap the previous kernel's tail.
 // Split-K over keys: every split stages its normalized output O/l (bf16) in shared memory, writes it
-// coalesced to a per-row-group workspace with (m, l), and exits; attn_tc_combine_kernel (launched with PDL
-// right behind, one warp per row, every load in flight) merges the splits. An in-kernel merge behind a
+// coalesced to a per-row-group workspace with (m, l), and exits; attn_tc_merge_kernel (launched with PDL
+// right behind, one half-warp per row, every load in flight) merges the splits. An in-kernel merge behind a
 // grid-wide arrive counter was measured slower: the row group's CTAs wait for the slowest sibling and
 // the merge loads then run at low memory-level parallelism.
 #include <cuda.h>
@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -70,7 +71,7 @@ static_assert(SMEM_BYTES <= 232448, "attention smem budget");
 // TMEM columns: O [0,128) fp32, S0 / S1 [128,384) fp32, P [384,448) and Q [448,512) bf16 pairs. Q in TMEM makes
 // S = Q.K^T a TS MMA that reads only K from shared memory (an SS MMA at N = 128 reads A and B at ~110 B/clk, most
 // of the SM's shared-memory bandwidth, which the TMA writes of the K/V ring also need).
-constexpr uint32_t TMEM_COLS = 512, T_O = 0, T_S = 128, T_P = 384, T_Q = 448;
+constexpr uint32_t TMEM_COLS = 512, T_O = 0, T_S = 128, T_Q = 448;  // P(j) bf16 over S(j); [384, 448) spare
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_LOG2 = 8.0f;
 
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int jp = j - 1, sv = jp % VST;
                 mbar_wait(&v_full[sv], (uint32_t)(jp / VST) & 1u);
                 const uint32_t vb = sbase + OFF_V + sv * TILE;
-                const uint32_t pb = tmem + T_P;
+                const uint32_t pb = tmem + T_S + (uint32_t)(jp & 1) * 128;  // P(jp) over S(jp)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     mbar_wait(&p_full[(jp & 1) * 4 + c], (uint32_t)(jp >> 1) & 1u);
@@ -651,15 +652,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mu_b = msb;
                 }
             }
-            // the P buffer was last read by PV(j-1)
-            if (j >= 1) {
-                mbar_wait(&pv_done[(j - 1) & 1], (uint32_t)((j - 1) >> 1) & 1u);
-                tc_fence_after();
-            }
+            // P(j) overwrites S(j) in place (bf16 pairs in the buffer's first 64 columns; S(j) is already in registers):
+            // its previous P(j-2) was read by PV(j-2), which the tensor pipe retired before S(j), so no wait here
             const float oa = mu_a == -INFINITY ? 0.f : mu_a, ob = mu_b == -INFINITY ? 0.f : mu_b;  // none visible: p = 0
             const uint64_t sc2 = pk2(sl2, sl2), na2 = pk2(-oa, -oa), nb2 = pk2(-ob, -ob);
             uint64_t acca = 0, accb = 0;  // (+0, +0)
-            const uint32_t tP = tmem + lane_base + T_P;
+            const uint32_t tP = tS;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {  // chunk c = keys [32c, 32c+32) = k in [4c, 4c+4): 16 P columns, 8 regs
                 uint64_t pv[8];            // [kk][row a, row b] pairs
@@ -781,9 +779,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-// Split merge (PDL-launched right behind the attention grid): one warp per row of a row group, lane = 4
-// columns; all `splits` partial loads are issued before use. out = sum_s w_s (O_s / l_s) / sum_s w_s,
-// w_s = 2^(m_s - M) * l_s (numerics.cpp:31-60 softmax, regrouped over key splits).
+// Many-split merge of the single-request launch (C2: 9 splits over 16 row groups): one warp per row, lane = 4
+// columns, every split's load in flight; measured faster there than the half-warp kernel below (2.0 vs 3.3 us).
 __global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat16* __restrict__ ws_o,
                                                               const float2* __restrict__ ws_ml,
                                                               __nv_bfloat16* __restrict__ out, int* err, int Tq, int H,
@@ -831,56 +828,95 @@ __global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat1
     tl_exit(tl);
 }
 
-// Split merge of the BATCHED launch: row groups are (request, kv head, group) with gid = (req * Hkv + g) * groups_x
-// + x; each request's rows / output rows come from its AttnReq (tok0, n).
-__global__ void __launch_bounds__(256) attn_tc_combine_batch_kernel(const __nv_bfloat16* __restrict__ ws_o,
-                                                                    const float2* __restrict__ ws_ml,
-                                                                    __nv_bfloat16* __restrict__ out, int* err,
-                                                                    const AttnReq* __restrict__ reqs, int H, int Hkv,
-                                                                    int splits, int groups_x, int ngroups,
-                                                                    unsigned long long* tl) {
+// Split merge (PDL-launched right behind the attention grid): one half-warp per row (16 lanes x 8 columns), rows
+// grid-strided, every split's partial and (m, l) loaded before use; MAXS (power of two >= splits) sizes the
+// in-flight loads so few-split merges keep a full SM of warps resident. out = sum_s w_s (O_s / l_s) / sum_s w_s,
+// w_s = 2^(m_s - M) * l_s (numerics.cpp:31-60 softmax, regrouped over key splits). Row groups are (kv head, x)
+// or, BATCHED, (request, kv head, x) with each request's rows / output rows from its AttnReq (tok0, n).
+template <bool BATCH, int MAXS>
+__global__ void __launch_bounds__(256) attn_tc_merge_kernel(const __nv_bfloat16* __restrict__ ws_o,
+                                                            const float2* __restrict__ ws_ml,
+                                                            __nv_bfloat16* __restrict__ out, int* err,
+                                                            const AttnReq* __restrict__ reqs, int Tq, int H, int Hkv,
+                                                            int splits, int groups_x, int nrows,
+                                                            unsigned long long* tl) {
     pdl_launch();
-    const int lane = threadIdx.x & 31;
-    const int grow = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int gid = grow / RG, i = grow % RG;
-    const int y = gid / groups_x, req = y / Hkv, g = y - req * Hkv;
-    const int rr = (gid % groups_x) * RG + i;
+    const int hl = threadIdx.x & 15;
+    const unsigned hm = (threadIdx.x & 16) ? 0xFFFF0000u : 0x0000FFFFu;
     const int group = H / Hkv;
+    const int64_t plane = nrows;  // rows per split plane
     pdl_wait();
     tl_wait(tl);
-    const AttnReq R = reqs[req];
-    if (rr >= R.n * group) return;  // warp-uniform
-    const int64_t plane = (int64_t)ngroups * RG;
-    const uint2* src = reinterpret_cast<const uint2*>(ws_o + (int64_t)grow * D) + lane;
-    uint2 v[32];
+    for (int grow = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 4); grow < nrows; grow += gridDim.x * 16) {
+        const int gid = grow / RG, i = grow % RG;
+        const int y = gid / groups_x, rr = (gid % groups_x) * RG + i;
+        int g = y, tok0 = 0, n = Tq;
+        if (BATCH) {
+            const int req = y / Hkv;
+            g = y - req * Hkv;
+            const AttnReq R = reqs[req];
+            tok0 = R.tok0;
+            n = R.n;
+        }
+        if (rr >= n * group) continue;  // half-warp-uniform
+        const uint4* src = reinterpret_cast<const uint4*>(ws_o + (int64_t)grow * D) + hl;
+        uint4 v[MAXS];
 #pragma unroll
-    for (int k = 0; k < 32; ++k)
-        if (k < splits) v[k] = src[(int64_t)k * plane * (D / 4)];
-    const float2 ml = lane < splits ? ws_ml[lane * plane + grow] : make_float2(-INFINITY, 0.f);
-    float M = ml.x;
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    const float wl = ml.x == -INFINITY ? 0.f : ex2(ml.x - M) * ml.y;
-    float L = wl;
-    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-    if (M == -INFINITY || L == 0.f) {
-        if (lane == 0) atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
-        return;
-    }
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int k = 0; k < MAXS; ++k)
+            if (k < splits) v[k] = src[(int64_t)k * plane * (D / 8)];
+        const float2 ml0 = hl < splits ? ws_ml[hl * plane + grow] : make_float2(-INFINITY, 0.f);
+        const float2 ml1 = (MAXS > 16 && hl + 16 < splits) ? ws_ml[(hl + 16) * plane + grow] : make_float2(-INFINITY, 0.f);
+        float M = fmaxf(ml0.x, ml1.x);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        if (k >= splits) break;
-        const float w = __shfl_sync(0xffffffffu, wl, k);
-        acc[0] = fmaf(__uint_as_float(v[k].x << 16), w, acc[0]);
-        acc[1] = fmaf(__uint_as_float(v[k].x & 0xFFFF0000u), w, acc[1]);
-        acc[2] = fmaf(__uint_as_float(v[k].y << 16), w, acc[2]);
-        acc[3] = fmaf(__uint_as_float(v[k].y & 0xFFFF0000u), w, acc[3]);
+        for (int o = 8; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(hm, M, o, 16));
+        const float w0 = ml0.x == -INFINITY ? 0.f : ex2(ml0.x - M) * ml0.y;
+        const float w1 = ml1.x == -INFINITY ? 0.f : ex2(ml1.x - M) * ml1.y;
+        float L = w0 + w1;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) L += __shfl_xor_sync(hm, L, o, 16);
+        if (M == -INFINITY || L == 0.f) {
+            if (hl == 0) atomicOr(err, 8);  // DegenerateRowError (numerics.cpp:39-42)
+            continue;
+        }
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k) {
+            if (k >= splits) break;
+            const float w = __shfl_sync(hm, k < 16 ? w0 : w1, k & 15, 16);
+            const uint32_t u[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                acc[2 * c] = fmaf(__uint_as_float(u[c] << 16), w, acc[2 * c]);
+                acc[2 * c + 1] = fmaf(__uint_as_float(u[c] & 0xFFFF0000u), w, acc[2 * c + 1]);
+            }
+        }
+        const float inv = 1.0f / L;
+        const int64_t mo = (int64_t)(tok0 + rr / group) * H + g * group + rr % group;
+        reinterpret_cast<uint4*>(out + mo * D)[hl] =
+            make_uint4(bf16x2_bits(acc[0] * inv, acc[1] * inv), bf16x2_bits(acc[2] * inv, acc[3] * inv),
+                       bf16x2_bits(acc[4] * inv, acc[5] * inv), bf16x2_bits(acc[6] * inv, acc[7] * inv));
     }
-    const float inv = 1.0f / L;
-    const int64_t mo = (int64_t)(R.tok0 + rr / group) * H + g * group + rr % group;
-    reinterpret_cast<uint2*>(out + mo * D)[lane] =
-        make_uint2(bf16x2_bits(acc[0] * inv, acc[1] * inv), bf16x2_bits(acc[2] * inv, acc[3] * inv));
     tl_exit(tl);
+}
+
+template <bool BATCH>
+void launch_merge(const AttnWork& ws, void* out, int* err, const AttnReq* reqs, int Tq, int H, int Hkv, int splits,
+                  int groups_x, int nrows, cudaStream_t s) {
+    const dim3 grid((unsigned)std::min((nrows + 15) / 16, 148 * 8)), block(256);
+    const auto* o = reinterpret_cast<const __nv_bfloat16*>(ws.o);
+    const auto* ml = reinterpret_cast<const float2*>(ws.ml);
+    auto* dst = static_cast<__nv_bfloat16*>(out);
+    unsigned long long* tl = tl_take();
+#define TKV_MERGE(S)                                                                                                 \
+    launch_k(attn_tc_merge_kernel<BATCH, S>, grid, block, 0, s, o, ml, dst, err, reqs, Tq, H, Hkv, splits, groups_x, \
+             nrows, tl)
+    if (splits <= 2) TKV_MERGE(2);
+    else if (splits <= 4) TKV_MERGE(4);
+    else if (splits <= 8) TKV_MERGE(8);
+    else if (splits <= 16) TKV_MERGE(16);
+    else TKV_MERGE(32);
+#undef TKV_MERGE
+    TKV_CUDA(cudaGetLastError());
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -959,13 +995,8 @@ void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* m
     a.tl = tl_take();
     launch_k(attn_tc_kernel, dim3(groups_x, Hkv * n_req, a.splits), THREADS, SMEM_BYTES, s, unused, unused, a);
     TKV_CUDA(cudaGetLastError());
-    if (a.splits > 1) {
-        const int ngroups = groups_x * Hkv * n_req;
-        launch_k(attn_tc_combine_batch_kernel, dim3((ngroups * RG + 7) / 8), dim3(256), 0, s,
-                 reinterpret_cast<const __nv_bfloat16*>(ws.o), reinterpret_cast<const float2*>(ws.ml),
-                 (__nv_bfloat16*)out, err, reqs, H, Hkv, a.splits, groups_x, ngroups, tl_take());
-        TKV_CUDA(cudaGetLastError());
-    }
+    if (a.splits > 1)
+        launch_merge<true>(ws, out, err, reqs, 0, H, Hkv, a.splits, groups_x, groups_x * Hkv * n_req * RG, s);
 }
 
 // split-K of the batched launch: the smallest split count whose CTA count fills the last wave (>= 95 % of the
@@ -1049,11 +1080,13 @@ void launch_attention_tc(const void* q, const void* k, const void* v, int kv_str
     a.tl = tl_take();
     launch_k(attn_tc_kernel, grid, THREADS, SMEM_BYTES, s, tk, tv, a);
     TKV_CUDA(cudaGetLastError());
-    if (splits > 1) {
+    if (splits > 4) {
         const int rows = (int)(grid.x * grid.y) * RG;
         launch_k(attn_tc_combine_kernel, dim3(rows / 8), dim3(256), 0, s, (const __nv_bfloat16*)ws.o,
                  (const float2*)ws.ml, (__nv_bfloat16*)out, err, Tq, H, Hkv, splits, (int)grid.x, tl_take());
         TKV_CUDA(cudaGetLastError());
+    } else if (splits > 1) {
+        launch_merge<false>(ws, out, err, nullptr, Tq, H, Hkv, splits, (int)grid.x, (int)(grid.x * grid.y) * RG, s);
     }
 }
 

@@ -93,6 +93,10 @@ def main(steps=10):
         e = ep.reshape(steps, -1)[:, 1:].reshape(steps, cfg.layer_num, per_layer)
         print("  epilogue us per layer: qkv %.1f  residual(O) %.1f  residual(down) %.1f  (launches/layer %d)"
               % (e[..., :per_layer - 2].sum(-1).mean(), e[..., -2].mean(), e[..., -1].mean(), per_layer))
+    at = dur[cls == T.Engine.TIMELINE_CLASSES.index("attention")]
+    if len(at) == steps * cfg.layer_num * 2:  # attention, then its split merge, per layer
+        a2 = at.reshape(steps, cfg.layer_num, 2)
+        print("  attention us per layer: kernel %.2f  merge %.2f" % (a2[..., 0].mean(), a2[..., 1].mean()))
     env = {k: v for k, v in os.environ.items() if k.startswith("TKV_") and k != "TKV_LIB_PATH"}
     print(f"{env} p50 {statistics.median(ts):.3f} ms | in-chain ms: " + " ".join(f"{k} {v:.3f}" for k, v in per.items())
           + f" | gemm us qkv {g[..., 0].mean():.2f} o {g[..., 1].mean():.2f} gate_up {g[..., 2].mean():.2f}"
