@@ -55,6 +55,9 @@ constexpr int KST = ATTN_KST, VST = ATTN_VST;            // K / V ring depths (Q
 // (k = 0..15), so a row lives in the 4 lanes of one quad and its max / sum are two shuffles.
 constexpr int SM_WARPS = 8, SM_THREADS = 32 * SM_WARPS;
 constexpr int WARP_TMA = SM_WARPS, WARP_MMA = SM_WARPS + 1, THREADS = 32 * (WARP_MMA + 1);
+#ifndef ATTN_DIAG
+#define ATTN_DIAG 0  // cost-attribution variants (tools/attn_diag.sh); 0 = the product kernel
+#endif
 #ifndef POLY_PAIRS
 #define POLY_PAIRS 6
 #endif
@@ -323,6 +326,9 @@ struct AttnArgs {
     const CUtensorMap* maps3;
     int n_req, layer;
     unsigned long long* tl;  // kernel timeline slot (tl_take)
+    // single-request split-K with a compact last row tile (attn_tc_split_plan): gx row tiles; splits_c > 0 flattens the
+    // grid to blockIdx.x = the (gx - 1) full tiles x Hkv x `splits` CTAs, then the last tile's Hkv x splits_c CTAs
+    int gx, splits_c;
 };
 
 // Warp-collective MMA issue: the whole MMA warp walks the loop (operands stay warp-uniform, in uniform registers);
@@ -346,7 +352,7 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
 // v6: ONE 128-row tile per CTA, S double-buffered so the tensor pipe runs S(j+1) while the softmax works on S(j):
 //   tensor pipe:  S(0) S(1) PV(0) S(2) PV(1) S(3) PV(2) ...
 // S(j+2) may overwrite S buffer j & 1 once PV(j) was issued (its P chunks were released, so the softmax has loaded
-// S(j)); P is single-buffered (P(j+1) waits for PV(j) to retire). Warps 0-7 = softmax, 16 whole rows each (see
+// S(j)); P(j) is written over S(j) (bf16 pairs), so it is double-buffered with S. Warps 0-7 = softmax, 16 whole rows each (see
 // SM_WARPS): every row statistic is quad-local and a warp rescales its own O rows. Warp 8 = TMA producer, warp 9 =
 // MMA issuer (whole warp, elected lane).
 __global__ void __launch_bounds__(THREADS, 1)
@@ -369,8 +375,25 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     pdl_launch();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int group = a.H / a.Hkv, split = blockIdx.z;
-    int g = blockIdx.y, Tq = a.Tq, Tk = a.Tk, kv_ready = a.kv_ready;
+    const int group = a.H / a.Hkv;
+    int bx = blockIdx.x, by = blockIdx.y, split = blockIdx.z, nsplit = a.splits;
+    if (a.splits_c > 0) {  // flattened single-request grid (see AttnArgs::splits_c)
+        const int per = (a.gx - 1) * a.Hkv, nf = per * a.splits;
+        int b = blockIdx.x;
+        if (b < nf) {
+            split = b / per;
+            b -= split * per;
+            by = b / (a.gx - 1);
+            bx = b - by * (a.gx - 1);
+        } else {
+            b -= nf;
+            split = b / a.Hkv;
+            by = b - split * a.Hkv;
+            bx = a.gx - 1;
+            nsplit = a.splits_c;
+        }
+    }
+    int g = by, Tq = a.Tq, Tk = a.Tk, kv_ready = a.kv_ready;
     const __nv_bfloat16* qp = a.q;
     const int32_t* lop = a.lo;
     const int32_t* hip = a.hi;
@@ -378,8 +401,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const CUtensorMap* mK = &tmK;
     const CUtensorMap* mV = &tmV;
     if (a.n_req > 0) {  // batched: this CTA's request (the table was uploaded before the forward began)
-        const int req = blockIdx.y / a.Hkv;
-        g = blockIdx.y - req * a.Hkv;
+        const int req = by / a.Hkv;
+        g = by - req * a.Hkv;
         const AttnReq R = a.reqs[req];
         Tq = R.n;
         Tk = R.row0 + R.n;
@@ -392,10 +415,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     const bool b3 = a.n_req > 0;
     const int rows_total = Tq * group;
-    const int rr0 = blockIdx.x * BR;                       // first row of this tile
+    const int rr0 = bx * BR;                               // first row of this tile
     if (rr0 >= rows_total) return;                         // batched grid sized for the longest request
+    // Compact tile (<= 64 valid rows, e.g. the last of 3.5 GQA tiles): row i of quadrant q (TMEM lanes 32q + i) holds
+    // tile row 16q + i for i < 16, so each SMSP's softmax warp w < 4 has 16 valid rows and warps 4-7 have none (they
+    // skip the tile loop): the softmax, which bounds the per-tile period, costs half an SMSP's issue per tile.
+    const int nv = min(BR, rows_total - rr0);
+    const bool compact = nv <= BR / 2;
+    const int act_warps = compact ? SM_WARPS / 2 : SM_WARPS;
 
-    const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);  // launch order
     if (tid == 0 && a.trace && cta_lin < TRACE_CTAS) a.trace[TRACE_CTA0 + 2 * cta_lin] = globaltimer_ns();
     if (tid == 0) {
         trace(0, 9);
@@ -410,7 +439,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int b = 0; b < 2; ++b) {
             mbar_init(&s_full[b], 1);
             mbar_init(&pv_done[b], 1);
-            for (int c = 0; c < 4; ++c) mbar_init(&p_full[b * 4 + c], SM_WARPS);  // one arrive per warp
+            for (int c = 0; c < 4; ++c) mbar_init(&p_full[b * 4 + c], act_warps);  // one arrive per active warp
         }
         mbar_init(o_done, 1);
         mbar_init(q_ready, SM_THREADS);
@@ -448,7 +477,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tmem = *tmem_slot;
     const int blo = sh_range[0], bhi = sh_range[1];
     const int span = bhi - blo + 1;
-    const int chunk = span > 0 ? ((span + a.splits - 1) / a.splits + BK - 1) / BK * BK : 0;
+    const int chunk = span > 0 ? ((span + nsplit - 1) / nsplit + BK - 1) / BK * BK : 0;
     const int ks = blo + split * chunk;
     const int ke = min(bhi, ks + chunk - 1);
     const int n = (span > 0 && ke >= ks) ? (ke - ks + BK) / BK : 0;
@@ -475,13 +504,24 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 trace(j, k_tile ? 6 : 7);
             };
+            // K runs one tile ahead of V (K(j+1) before V(j)): V(j) waits for PV(j-2) to free its slot, and S(j+1)
+            // must not queue behind that wait
             bool waited = false;
-            for (int j = 0; j < n; ++j) {
+            auto ready = [&](int j) {
                 if (!waited && ks + j * BK + BK > kv_ready) {  // rows written by the previous kernels of this forward
                     pdl_wait();
                     waited = true;
                 }
-                load_tile(true, j);
+            };
+            if (n > 0) {
+                ready(0);
+                load_tile(true, 0);
+            }
+            for (int j = 0; j < n; ++j) {
+                if (j + 1 < n) {
+                    ready(j + 1);
+                    load_tile(true, j + 1);
+                }
                 load_tile(false, j);
             }
             // HBM is mostly idle for the rest of the attention at query-prefill sizes: once this CTA's K/V loads are
@@ -507,6 +547,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int sk = j % KST;
                 mbar_wait(&k_full[sk], (uint32_t)(j / KST) & 1u);
                 tc_fence_after();
+                if (lane == 0) trace(j, 14);
                 const uint32_t kb = sbase + OFF_K + sk * TILE;
                 const uint32_t sd = tmem + T_S + (uint32_t)(j & 1) * 128;
 #pragma unroll
@@ -527,10 +568,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int c = 0; c < 4; ++c) {
                     mbar_wait(&p_full[(jp & 1) * 4 + c], (uint32_t)(jp >> 1) & 1u);
                     tc_fence_after();
+                    if (c == 3 && lane == 0) trace(jp, 15);
 #pragma unroll
                     for (int k2 = 0; k2 < 2; ++k2) {
                         const int kk = 2 * c + k2;
+#if ATTN_DIAG != 2  // 2: cost attribution only (wrong results): no PV MMAs
                         umma_ts_elect(tmem + T_O, pb + kk * 8, desc_mn(vb + kk * 2048), IDESC_PV, (jp > 0 || kk > 0) ? 1u : 0u);
+#endif
                     }
                 }
                 commit_elect(&v_empty[sv]);
@@ -544,9 +588,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         // and rb = ra + 8, key columns 8k + 2*(t%4) + {0,1} of every tile (16x256b TMEM access) ----------------
         const int t0 = lane & 3;
         const int wr0 = (warp & 3) * 32 + (warp >> 2) * 16;  // first tile row (TMEM lane) of this warp
-        const int ra = wr0 + (lane >> 2), rb = ra + 8;
-        const bool act_a = rr0 + ra < rows_total, act_b = rr0 + rb < rows_total;
-        const int ta = act_a ? (rr0 + ra) / group : 0, tb = act_b ? (rr0 + rb) / group : 0;
+        const int ra = wr0 + (lane >> 2), rb = ra + 8;  // TMEM lanes
+        // tile rows held by those lanes (compact: 16 per quadrant; BR = none)
+        const int pa = compact ? ((ra & 31) < 16 ? 16 * (ra >> 5) + (ra & 31) : BR) : ra;
+        const int pb = compact ? ((rb & 31) < 16 ? 16 * (rb >> 5) + (rb & 31) : BR) : rb;
+        const bool act_a = pa < nv, act_b = pb < nv;
+        const bool warp_on = warp < act_warps;
+        const int ta = act_a ? (rr0 + pa) / group : 0, tb = act_b ? (rr0 + pb) / group : 0;
         const int lo_a = act_a ? lop[ta] : INT32_MAX, hi_a = act_a ? min(hip[ta], Tk - 1) : -1;
         const int lo_b = act_b ? lop[tb] : INT32_MAX, hi_b = act_b ? min(hip[tb], Tk - 1) : -1;
         constexpr int RPW = BR / SM_WARPS;  // rows per warp for the coalesced Q staging / output copy
@@ -556,13 +604,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         {
             // Q rows ra, rb straight into TMEM: column c of a row holds d = 2c, 2c + 1; with the 16x256b shape this
             // lane supplies columns 8k + 2*t0 + {0,1}, i.e. d = 16k + 4*t0 + 0..3 (one 8-byte load per row and k)
-            const int qra = rr0 + ra, qrb = rr0 + rb;
-            const uint2* pa = reinterpret_cast<const uint2*>(qp + ((int64_t)(qra / group) * a.H + g * group + qra % group) * D) + t0;
-            const uint2* pb = reinterpret_cast<const uint2*>(qp + ((int64_t)(qrb / group) * a.H + g * group + qrb % group) * D) + t0;
+            const int qra = rr0 + (act_a ? pa : 0), qrb = rr0 + (act_b ? pb : 0);
+            const uint2* qa = reinterpret_cast<const uint2*>(qp + ((int64_t)(qra / group) * a.H + g * group + qra % group) * D) + t0;
+            const uint2* qb = reinterpret_cast<const uint2*>(qp + ((int64_t)(qrb / group) * a.H + g * group + qrb % group) * D) + t0;
             uint32_t w[32];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const uint2 va = act_a ? pa[4 * k] : make_uint2(0u, 0u), vb = act_b ? pb[4 * k] : make_uint2(0u, 0u);
+                const uint2 va = act_a ? qa[4 * k] : make_uint2(0u, 0u), vb = act_b ? qb[4 * k] : make_uint2(0u, 0u);
                 w[4 * k] = va.x;
                 w[4 * k + 1] = va.y;
                 w[4 * k + 2] = vb.x;
@@ -577,7 +625,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t lane_base = (uint32_t)wr0 << 16;
         const float sl2 = a.scale * LOG2E;
         float mu_a = -INFINITY, mu_b = -INFINITY, l_a = 0.f, l_b = 0.f;  // running max (log2 units, lazy) and sum
-        for (int j = 0; j < n; ++j) {
+        for (int j = 0; j < (warp_on ? n : 0); ++j) {
             const uint32_t b = (uint32_t)(j & 1);
             mbar_wait(&s_full[b], (uint32_t)(j >> 1) & 1u);
             tc_fence_after();
@@ -666,6 +714,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const int k = 4 * c + (i >> 1), rsel = i & 1;
                     const uint64_t xv = fma2(pk2(__uint_as_float(s[4 * k + 2 * rsel]), __uint_as_float(s[4 * k + 2 * rsel + 1])),
                                              sc2, rsel ? nb2 : na2);
+#if ATTN_DIAG == 1  // cost attribution only (wrong results): no exp work
+                    if (true) {
+                        pv[i] = xv;
+                    } else
+#endif
                     if (((c * 8 + i) & 15) < kPolyPairs) {  // POLY_PAIRS of every 16 pairs on the FMA pipe
                         pv[i] = ex2_poly2(xv);
                     } else {
@@ -704,7 +757,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
         l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
         l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
-        if (n > 0) {
+        if (n > 0 && warp_on) {
             mbar_wait(o_done, 0);
             tc_fence_after();
         }
@@ -714,7 +767,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float inv_a = l_a > 0.f ? 1.0f / l_a : 0.f, inv_b = l_b > 0.f ? 1.0f / l_b : 0.f;
         const uint32_t stage = sbase + OFF_Q;
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < (warp_on ? 2 : 0); ++c) {  // compact tile: warps 4-7 hold no rows
             uint32_t w[32];
             if (n > 0) {
                 tmem_ld_16x256_x8(tmem + lane_base + T_O + c * 64, w);  // warp-collective
@@ -727,16 +780,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int kk = 0; kk < 8; ++kk) {
                 const int ch = c * 8 + kk;  // 16-byte chunk (8 columns) of the 256-byte row
                 const uint32_t off = (ch >> 3) * SUB + 4 * t0;
-                sts32(stage + off + swz(ra, ch & 7),
+                sts32(stage + off + swz(pa, ch & 7),
                       bf16x2_bits(__uint_as_float(w[4 * kk]) * inv_a, __uint_as_float(w[4 * kk + 1]) * inv_a));
-                sts32(stage + off + swz(rb, ch & 7),
+                sts32(stage + off + swz(pb, ch & 7),
                       bf16x2_bits(__uint_as_float(w[4 * kk + 2]) * inv_b, __uint_as_float(w[4 * kk + 3]) * inv_b));
             }
         }
         named_bar(1, SM_THREADS);  // the whole tile is staged
         if (tid == 0) trace(31, 5);
-        const int gid = blockIdx.y * gridDim.x + blockIdx.x;
-        const int ngroups = gridDim.x * gridDim.y;
+        const int gid = by * a.gx + bx;  // row group (kv head or request x kv head, row tile)
+        const int ngroups = a.splits_c > 0 ? a.gx * a.Hkv : a.gx * gridDim.y;
         // workspace of split s, row group gid: rows [BR][D] bf16 (contiguous) and (m, l) [BR]
         const int64_t wrow0 = ((int64_t)split * ngroups + gid) * BR;
         {
@@ -758,13 +811,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
         if (tid == 0) trace(31, 6);
-        if (t0 == 0) {
+        if (t0 == 0 && warp_on) {
             if (a.splits == 1) {
                 if ((act_a && l_a == 0.f) || (act_b && l_b == 0.f)) atomicOr(a.err, 8);  // DegenerateRowError (numerics.cpp:39-42)
             } else {
                 float2* ml = reinterpret_cast<float2*>(a.ws_ml) + wrow0;
-                ml[ra] = make_float2(act_a ? mu_a : -INFINITY, l_a);
-                ml[rb] = make_float2(act_b ? mu_b : -INFINITY, l_b);
+                ml[pa] = make_float2(act_a ? mu_a : -INFINITY, l_a);
+                ml[pb] = make_float2(act_b ? mu_b : -INFINITY, l_b);
                 if (tid == 0) trace(31, 1);
             }
         }
@@ -784,7 +837,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 __global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat16* __restrict__ ws_o,
                                                               const float2* __restrict__ ws_ml,
                                                               __nv_bfloat16* __restrict__ out, int* err, int Tq, int H,
-                                                              int Hkv, int splits, int groups_x, unsigned long long* tl) {
+                                                              int Hkv, int splits, int groups_x, int splits_c,
+                                                              unsigned long long* tl) {
     pdl_launch();
     const int lane = threadIdx.x & 31;
     const int grow = blockIdx.x * 8 + (threadIdx.x >> 5);  // row over all row groups: gid * RG + i
@@ -793,6 +847,7 @@ __global__ void __launch_bounds__(256) attn_tc_combine_kernel(const __nv_bfloat1
     const int group = H / Hkv;
     const bool ok = rr < Tq * group;
     const int64_t plane = (int64_t)groups_x * Hkv * RG;
+    if (splits_c > 0 && gid % groups_x == groups_x - 1) splits = splits_c;  // the compact last tile's split count
     pdl_wait();
     tl_wait(tl);
     if (!ok) return;  // warp-uniform
@@ -838,7 +893,7 @@ __global__ void __launch_bounds__(256) attn_tc_merge_kernel(const __nv_bfloat16*
                                                             const float2* __restrict__ ws_ml,
                                                             __nv_bfloat16* __restrict__ out, int* err,
                                                             const AttnReq* __restrict__ reqs, int Tq, int H, int Hkv,
-                                                            int splits, int groups_x, int nrows,
+                                                            int splits_all, int groups_x, int nrows, int splits_c,
                                                             unsigned long long* tl) {
     pdl_launch();
     const int hl = threadIdx.x & 15;
@@ -850,6 +905,7 @@ __global__ void __launch_bounds__(256) attn_tc_merge_kernel(const __nv_bfloat16*
     for (int grow = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 4); grow < nrows; grow += gridDim.x * 16) {
         const int gid = grow / RG, i = grow % RG;
         const int y = gid / groups_x, rr = (gid % groups_x) * RG + i;
+        const int splits = (splits_c > 0 && gid % groups_x == groups_x - 1) ? splits_c : splits_all;
         int g = y, tok0 = 0, n = Tq;
         if (BATCH) {
             const int req = y / Hkv;
@@ -901,7 +957,7 @@ __global__ void __launch_bounds__(256) attn_tc_merge_kernel(const __nv_bfloat16*
 
 template <bool BATCH>
 void launch_merge(const AttnWork& ws, void* out, int* err, const AttnReq* reqs, int Tq, int H, int Hkv, int splits,
-                  int groups_x, int nrows, cudaStream_t s) {
+                  int groups_x, int nrows, cudaStream_t s, int splits_c = 0) {
     const dim3 grid((unsigned)std::min((nrows + 15) / 16, 148 * 8)), block(256);
     const auto* o = reinterpret_cast<const __nv_bfloat16*>(ws.o);
     const auto* ml = reinterpret_cast<const float2*>(ws.ml);
@@ -909,7 +965,7 @@ void launch_merge(const AttnWork& ws, void* out, int* err, const AttnReq* reqs, 
     unsigned long long* tl = tl_take();
 #define TKV_MERGE(S)                                                                                                 \
     launch_k(attn_tc_merge_kernel<BATCH, S>, grid, block, 0, s, o, ml, dst, err, reqs, Tq, H, Hkv, splits, groups_x, \
-             nrows, tl)
+             nrows, splits_c, tl)
     if (splits <= 2) TKV_MERGE(2);
     else if (splits <= 4) TKV_MERGE(4);
     else if (splits <= 8) TKV_MERGE(8);
@@ -992,6 +1048,7 @@ void launch_attention_tc_batch(const void* q, const AttnReq* reqs, const void* m
     CUtensorMap unused;
     memset(&unused, 0, sizeof unused);
     const int groups_x = (max_rows * group + RG - 1) / RG;
+    a.gx = groups_x;
     a.tl = tl_take();
     launch_k(attn_tc_kernel, dim3(groups_x, Hkv * n_req, a.splits), THREADS, SMEM_BYTES, s, unused, unused, a);
     TKV_CUDA(cudaGetLastError());
@@ -1046,9 +1103,22 @@ int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms) {
     if (groups * 2 > num_sms) return 1;  // already >= half a wave of row tiles: no split-K
     int s = num_sms / groups;            // one wave (1 CTA / SM)
     const int max_by_keys = ((Tk + BK - 1) / BK + 1) / 2;  // >= 2 key tiles per split
+    const int rows = Tq * (H / Hkv), gx = (rows + RG - 1) / RG;
+    // a compact last row tile takes fewer, longer splits: the SMs it frees go to more splits of the full tiles
+    while (s + 1 <= max_by_keys && s + 1 <= 32 && attn_tc_compact_splits(rows, gx, s + 1) > 0 &&
+           (gx - 1) * Hkv * (s + 1) + Hkv * attn_tc_compact_splits(rows, gx, s + 1) <= num_sms)
+        ++s;
     if (s > max_by_keys) s = max_by_keys;
     if (s > 32) s = 32;
     return s < 1 ? 1 : s;
+}
+
+// split count of a compact last row tile (<= BR / 2 valid rows, behind >= 1 full tile) under `splits` for the full
+// tiles: its per-tile period is ~0.65 of a full tile's (one softmax warp per SMSP instead of two); 0 = no compact tile
+int attn_tc_compact_splits(int rows, int gx, int splits) {
+    const int last = rows - (gx - 1) * RG;
+    if (gx < 2 || splits < 2 || last > RG / 2) return 0;
+    return std::max(1, (13 * splits + 19) / 20);
 }
 
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
@@ -1077,16 +1147,19 @@ void launch_attention_tc(const void* q, const void* k, const void* v, int kv_str
     a.pf = pf;
     const CUtensorMap tk = kv_map(k, Tk, kv_stride, kv_stride);
     const CUtensorMap tv = kv_map(v, Tk, kv_stride, kv_stride);
+    a.gx = (int)grid.x;
+    a.splits_c = attn_tc_compact_splits(Tq * group, (int)grid.x, splits);
+    const dim3 lgrid = a.splits_c > 0 ? dim3((grid.x - 1) * Hkv * splits + Hkv * a.splits_c) : grid;
     a.tl = tl_take();
-    launch_k(attn_tc_kernel, grid, THREADS, SMEM_BYTES, s, tk, tv, a);
+    launch_k(attn_tc_kernel, lgrid, THREADS, SMEM_BYTES, s, tk, tv, a);
     TKV_CUDA(cudaGetLastError());
+    const int rows = (int)(grid.x * grid.y) * RG;
     if (splits > 4) {
-        const int rows = (int)(grid.x * grid.y) * RG;
         launch_k(attn_tc_combine_kernel, dim3(rows / 8), dim3(256), 0, s, (const __nv_bfloat16*)ws.o,
-                 (const float2*)ws.ml, (__nv_bfloat16*)out, err, Tq, H, Hkv, splits, (int)grid.x, tl_take());
+                 (const float2*)ws.ml, (__nv_bfloat16*)out, err, Tq, H, Hkv, splits, (int)grid.x, a.splits_c, tl_take());
         TKV_CUDA(cudaGetLastError());
     } else if (splits > 1) {
-        launch_merge<false>(ws, out, err, nullptr, Tq, H, Hkv, splits, (int)grid.x, (int)(grid.x * grid.y) * RG, s);
+        launch_merge<false>(ws, out, err, nullptr, Tq, H, Hkv, splits, (int)grid.x, rows, s, a.splits_c);
     }
 }
 

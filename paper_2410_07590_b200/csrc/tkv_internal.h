@@ -198,6 +198,7 @@ int attn_tc_row_groups(int Tq, int H, int Hkv);
 // workspace of the tcgen05 kernel's split merge (floats); ws.ml = ws.o + *ml_offset
 size_t attn_tc_workspace_floats(int Tq, int H, int Hkv, int splits, size_t* ml_offset);
 int attn_tc_pick_splits(int Tq, int H, int Hkv, int Tk, int num_sms);
+int attn_tc_compact_splits(int rows, int gx, int splits);  // key splits of a compact (<= 64-row) last row tile
 void launch_attention_tc(const void* q, const void* k, const void* v, int kv_stride, const int32_t* lo,
                          const int32_t* hi, void* out, int Tq, int Tk, int H, int Hkv, int splits, const AttnWork& ws,
                          int* err, cudaStream_t s, int kv_ready, const L2Prefetch& pf = L2Prefetch());

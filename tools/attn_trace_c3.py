@@ -45,9 +45,10 @@ per = np.diff(s_ready[s_ready > 0])
 print("per-tile period (S ready to S ready), cycles: median %d, tiles 1-29: %s" % (np.median(per), per.tolist()))
 sm = ev[:30, 1] - ev[:30, 0]
 print("softmax S ready -> P released, cycles: median %d" % np.median(sm[ev[:30, 1] > 0]))
-# per-tile event table of CTA 0 (cycles relative to this tile's S-ready): K / V TMA issued, S MMAs issued, PV MMAs
+# per-tile event table of CTA 0 (cycles relative to this tile's S-ready): K / V TMA issued, MMA warp past the K wait,
+# S MMAs issued, MMA warp past the last P chunk wait, PV MMAs
 # issued, S loaded from TMEM, row max done, first P chunk stored / released, all P released
-names = {6: "K issued", 7: "V issued", 5: "S issued", 4: "PV issued", 10: "S loaded", 11: "max", 12: "P0 stored",
+names = {6: "K issued", 7: "V issued", 14: "K ready@mma", 5: "S issued", 15: "P3 seen@mma", 4: "PV issued", 10: "S loaded", 11: "max", 12: "P0 stored",
          13: "P0 released", 1: "P released"}
 print("tile " + " ".join(f"{v:>11s}" for v in names.values()))
 for j in range(8, 16):
