@@ -68,6 +68,14 @@ def workload():
     return payloads, query
 
 
+def tensor_peak(peaks):
+    """Dense bf16 peak for a kernel timed INSIDE a long step (every tensor roofline here: the C2 / C3 attention in
+    the request chain, the C3 / C5 projections): MEASURED_PEAKS.json's sustained figure (torch.matmul back to back
+    for 4 s, i.e. at the power-capped clock such work runs at), per the profiling recipe; the burst figure is
+    reported beside it."""
+    return peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -489,7 +497,8 @@ def run_ours(args):
               "chunks": n_chunks, "seconds": sec_all,
               "chunks_per_s": n_chunks / sec_all, "tokens_per_s": n_chunks * c / sec_all,
               "tflops": n_chunks * flop_chunk / sec_all / 1e12,
-              "tensor_frac": n_chunks * flop_chunk / sec_all / 1e12 / peaks["bf16_tflops"],
+              "tensor_frac": n_chunks * flop_chunk / sec_all / 1e12 / tensor_peak(peaks),
+              "tensor_frac_of_burst_peak": n_chunks * flop_chunk / sec_all / 1e12 / peaks["bf16_tflops"],
               "round_ms_p50": statistics.median(ts) * 1e3, "round_ms_max": max(ts) * 1e3,
               "flop_per_chunk": flop_chunk, "kv_bytes_per_chunk": c * cfg.layer_num * 2 * cfg.kv_dim * 2,
               "projection_1m_chunks_h": 1e6 / (n_chunks / sec_all) / 3600}
@@ -543,12 +552,15 @@ def run_ours(args):
             2 * cfg.hidden_size * (cfg.head_num + 2 * cfg.kv_head_num) * cfg.head_size
             + 2 * cfg.head_num * cfg.head_size * cfg.hidden_size + 6 * cfg.hidden_size * cfg.intermediate_size)
         c3["attention_roofline"] = {"bound": "tensor", "device_ms": a_ms, "flops": a_flops,
-                                    "achieved": a_flops / (a_ms / 1e3) / 1e12, "peak": peaks["bf16_tflops"],
-                                    "unit": "TFLOP/s", "frac": a_flops / (a_ms / 1e3) / 1e12 / peaks["bf16_tflops"]}
+                                    "achieved": a_flops / (a_ms / 1e3) / 1e12, "peak": tensor_peak(peaks),
+                                    "peak_kind": "sustained", "unit": "TFLOP/s",
+                                    "frac": a_flops / (a_ms / 1e3) / 1e12 / tensor_peak(peaks),
+                                    "frac_of_burst_peak": a_flops / (a_ms / 1e3) / 1e12 / peaks["bf16_tflops"]}
         c3["projection_gemm_roofline"] = {"bound": "tensor", "device_ms": g_ms, "flops": g_flops,
-                                          "achieved": g_flops / (g_ms / 1e3) / 1e12, "peak": peaks["bf16_tflops"],
-                                          "unit": "TFLOP/s",
-                                          "frac": g_flops / (g_ms / 1e3) / 1e12 / peaks["bf16_tflops"]}
+                                          "achieved": g_flops / (g_ms / 1e3) / 1e12, "peak": tensor_peak(peaks),
+                                          "peak_kind": "sustained", "unit": "TFLOP/s",
+                                          "frac": g_flops / (g_ms / 1e3) / 1e12 / tensor_peak(peaks),
+                                          "frac_of_burst_peak": g_flops / (g_ms / 1e3) / 1e12 / peaks["bf16_tflops"]}
 
     c4 = None
     if args.c4_requests > 0:
@@ -733,14 +745,17 @@ def run_ours(args):
                             "traffic": traffic_of("gather_rope"), "algorithmic_bytes_per_launch": kv_bytes,
                             "avg_launch_ms": gather_avg_ms},
         "attention_roofline": {"bound": "tensor", "achieved": attn_flops / (class_chain_ms["attention"] / 1e3) / 1e12,
-                               "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                               "frac": attn_flops / (class_chain_ms["attention"] / 1e3) / 1e12 / peaks["bf16_tflops"],
+                               "peak": tensor_peak(peaks), "peak_kind": "sustained (timed inside the long step)",
+                               "unit": "TFLOP/s",
+                               "frac": attn_flops / (class_chain_ms["attention"] / 1e3) / 1e12 / tensor_peak(peaks),
+                               "frac_of_burst_peak": attn_flops / (class_chain_ms["attention"] / 1e3) / 1e12
+                               / peaks["bf16_tflops"],
                                "flops_per_request": attn_flops, "traffic": traffic_of("attn_tc_kernel"),
                                "device_ms_per_request": class_chain_ms["attention"],
                                "timing": "in the real chain (tkv_kernel_timeline): attention + split-merge launches",
                                "isolated_events": {"device_ms_per_request": attn_ms / prof_steps,
                                                    "frac": attn_flops / (attn_ms / prof_steps / 1e3) / 1e12
-                                                   / peaks["bf16_tflops"]}},
+                                                   / tensor_peak(peaks)}},
         "request_roofline": {"bound": "hbm", "algorithmic_bytes": req_bytes,
                              "achieved": req_bytes / (ms_per_step / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
                              "unit": "GB/s", "frac": req_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"],

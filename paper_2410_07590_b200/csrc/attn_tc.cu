@@ -819,6 +819,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ml[pa] = make_float2(act_a ? mu_a : -INFINITY, l_a);
                 ml[pb] = make_float2(act_b ? mu_b : -INFINITY, l_b);
                 if (tid == 0) trace(31, 1);
+                if (tid == 0 && a.trace && cta_lin == 0) a.trace[31 * TRACE_EV + 7] = globaltimer_ns();  // clock check
             }
         }
     }

@@ -22,14 +22,25 @@ out = np.zeros(512 + 2048, np.uint64)
 T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 512 + 2048))
 ev = out[:512].reshape(32, 16).astype(np.int64)
 cta = out[512:].reshape(1024, 2).astype(np.int64)
-cta = cta[cta[:, 0] > 0]
+# this launch's CTAs (the single-request split-K grid: (gx - 1) x Hkv x s full-tile CTAs, then Hkv x s_c for the
+# compact last tile; the rest of the buffer may hold other launches' stamps)
+NCTA, NFULL = int(os.environ.get("C2_CTAS", 148)), int(os.environ.get("C2_FULL_CTAS", 120))
+cta = cta[:NCTA]
 s0 = cta[:, 0].min()
 st, en = (cta[:, 0] - s0) / 1e3, (cta[:, 1] - s0) / 1e3
+dur = en - st
 print(f"layer {os.environ['TKV_TRACE_LAYER']}: {len(cta)} CTAs, start spread {st.max():.2f} us, "
       f"end min/median/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f} us")
+print("CTA duration us, full tiles min/median/max %.2f/%.2f/%.2f, compact tile %.2f/%.2f/%.2f"
+      % (dur[:NFULL].min(), np.median(dur[:NFULL]), dur[:NFULL].max(), dur[NFULL:].min(), np.median(dur[NFULL:]),
+         dur[NFULL:].max()))
 t0 = ev[0, 9]
 names = ["smA:S ready", "smA:P arrive", "smB:S ready", "smB:P arrive", "mma:PV_A issued", "mma:PV_B issued",
          "tma:K(j) issue", "tma:V(j) issue", "mma:Q ready"]
+if ev[31, 7] > 0 and ev[31, 1] > 0:
+    print("CTA 0 entry -> partials written: %d cycles in %.2f us = %.2f GHz; CTA 0 exit %.2f us after entry"
+          % (ev[31, 1] - ev[0, 9], (ev[31, 7] - cta[0, 0]) / 1e3, (ev[31, 1] - ev[0, 9]) / (ev[31, 7] - cta[0, 0]),
+             (cta[0, 1] - cta[0, 0]) / 1e3))
 print("cycles since CTA (0,0,0) entry")
 print("previous kernel done (softmax pdl_wait returned) %d, Q loads back %d, Q staged %d"
       % (ev[30, 3] - t0, ev[30, 4] - t0, ev[30, 5] - t0))
@@ -39,3 +50,6 @@ for j in range(30):
     if (ev[j, :9] == 0).all():
         continue
     print(f"{j:<3d} " + " ".join(f"{(ev[j, e] - t0) if ev[j, e] else -1:16d}" for e in range(9)))
+print("CTA start / duration us by launch index:")
+for b in range(0, len(cta), 4):
+    print("  " + "  ".join(f"{b + i:3d}: {st[b + i]:5.2f}+{dur[b + i]:5.2f}" for i in range(4) if b + i < len(cta)))
