@@ -5,7 +5,10 @@
 #     epilogue kernels -> DRAM bytes per launch (roofline.traffic) and the key metrics
 set -u
 T=${1:-r2}
-B="python bench.py --steps 2 --warmup 3 --turbo-only --no-cpu-baseline"
+# --flags 256 = TKV_FLAG_NO_GRAPHS: under ncu a graph-replayed gate/up GEMM node of the bench fails to launch
+# ("LaunchFailed", grid 0,0,0; r2p) although the same graphs profile fine from tools/c2_step.py and the bench is
+# memcheck-clean; ncu serializes every launch anyway, so the kernels and their durations are those of the graph path
+B="python bench.py --steps 2 --warmup 3 --turbo-only --no-cpu-baseline --flags 256"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv $B > /dev/null 2>&1
 python tools/step_breakdown.py gpurun_out/${T}_launches.csv gpurun_out/${T}_launch_share.json > gpurun_out/${T}_launches_summary.txt
 # launch indices inside the first measured turbo step: skip the warm-up steps' kernels
