@@ -60,6 +60,10 @@ ATTN_CASES = [
     (37, 2000, 32, 8, 128, "query"),    # group 4: 148 rows -> tile B partially filled
     (64, 3000, 28, 4, 128, "query_hot"),  # large scores: exercises the lazy O rescale
     (20, 20, 28, 4, 128, "causal"),     # one key tile, heavy masking
+    # compact last row tile (<= 64 valid rows: 16 per TMEM quadrant, half the softmax warps) with the split plan
+    (48, 4000, 32, 8, 128, "query"),    # group 4: 192 rows -> last tile exactly 64 rows (compact)
+    (192, 2500, 4, 4, 128, "query"),    # group 1: 192 rows -> last tile 64 rows (compact)
+    (193, 2500, 4, 4, 128, "query"),    # group 1: 193 rows -> last tile 65 rows (not compact)
 ]
 
 
