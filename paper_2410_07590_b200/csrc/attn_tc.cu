@@ -744,6 +744,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (lane == 0) mbar_arrive(&p_full[b * 4 + c]);  // the PV MMA on these 32 keys may start
                 if (tid == 0 && c == 0) trace(j, 13);
             }
+            // observe PV(j-1) retiring (it ran during this tile's softmax): P no longer waits on it, but every pv_done
+            // phase is consumed before its next arrive, so the parity wait of the lazy rescale stays unambiguous
+            if (j >= 1) mbar_wait(&pv_done[(j - 1) & 1], (uint32_t)((j - 1) >> 1) & 1u);
             float a0, a1;
             up2(acca, a0, a1);
             l_a += a0 + a1;
