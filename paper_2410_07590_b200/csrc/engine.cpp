@@ -543,7 +543,6 @@ struct tkv_engine {
     // L2 warm-up of the O-proj weights and the head of gate/up, issued by each attention CTA once its K/V loads are
     // out (query-prefill forwards): C2 step 3.60 -> 3.54 ms at 40 MB (26 / 64 MB: 3.55 / 3.54, attention slower at 64)
     size_t l2_prefetch_bytes = (size_t)40 << 20;  // TKV_L2_PREFETCH_MB (tuning knob)
-    int l2_pf_next_qkv = 0;                       // TKV_L2_PF_NEXT_QKV (tuning): second region = next layer's QKV
     int skip_mask = 0;             // TKV_TIMING_SKIP: drop kernels for cost attribution (results invalid)
     int trace_layer = -1;          // TKV_TRACE_LAYER: clock64 pipeline trace of that layer's attention launch
     int attn_split_override = 0;   // TKV_ATTN_SPLITS: force the tcgen05 attention's split-K count
@@ -737,13 +736,8 @@ void tkv_engine::attend_layer(int64_t l, int T, const void* qrows, tkv_context* 
             const size_t ob = (size_t)hid * qd * es, gb = (size_t)2 * I * hid * es;
             pf.ptr[0] = w_o[l];
             pf.bytes[0] = std::min(ob, l2_prefetch_bytes);
-            if (l2_pf_next_qkv && l + 1 < L) {  // TUNING: the next layer's QKV weights instead of the head of gate/up
-                pf.ptr[1] = w_qkv[l + 1];
-                pf.bytes[1] = std::min((size_t)nqkv * hid * es, l2_prefetch_bytes - pf.bytes[0]);
-            } else {
-                pf.ptr[1] = w_gu[l];
-                pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
-            }
+            pf.ptr[1] = w_gu[l];
+            pf.bytes[1] = std::min(gb, l2_prefetch_bytes - pf.bytes[0]);
         }
         if (trace_layer == (int)l) attn_trace_enable(true, nullptr);
         launch_attention_tc(qrows, kv_plane(actx, l, 0), kv_plane(actx, l, 1), (int)kvd, lo, hi, out, arows,
@@ -825,15 +819,8 @@ void tkv_engine::forward(const Fwd& f) {
         launch_embed(f.tok, T, emb, (int)hid, (int)V, norm_attn(0), x.as<float>(), xb.p, ssp.as<float>(), dt, err.as<int>(),
                      stream);
     }
-    // the next GEMM of the forward, for the current GEMM's tail L2 warm-up (TKV_GEMM_NEXT_PF)
-    auto next = [&](const void* W, int M, int N, int K) {
-        if (use_tc()) set_gemm_next(W, M, N, K, pick_splits(M, N, K, true));
-    };
     for (int64_t l = 0; l < L; ++l) {
-        const bool last_rows1 = (l == L - 1) && f.logits && !batch;  // the last layer's O-proj / MLP run one row
-        const int rows_next = last_rows1 ? 1 : T;
         // --- attention block ---
-        if (!(f.kv_only && l == L - 1)) next(w_o[l], rows_next, (int)hid, (int)qd);
         int s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
         if (batch && f.epi_reqs) {  // every request's K/V to its own cache, one launch
             Scope sc(this, PC_EPI, 1);
@@ -893,7 +880,6 @@ void tkv_engine::forward(const Fwd& f) {
         }
         uint8_t* attn_rows = static_cast<uint8_t*>(attn.p);
         float* x_rows = x.as<float>() + r0 * hid;
-        next(w_gu[l], rows, (int)(2 * I), (int)hid);
         s = gemm(attn_rows, (int)qd, w_o[l], rows, (int)hid, (int)qd);
         if (!(skip_mask & 1)) {
             Scope sc(this, PC_EPI, 1);
@@ -901,14 +887,12 @@ void tkv_engine::forward(const Fwd& f) {
                             err.as<int>(), stream);
         }
         // --- MLP block: gate|up fused into one GEMM, SwiGLU (with the folded mlp_norm scale) in its epilogue ---
-        next(w_down[l], rows, (int)hid, (int)I);
         s = gemm(xb.p, (int)hid, w_gu[l], rows, (int)(2 * I), (int)hid, act.p);
         if (s > 0) {
             Scope sc(this, PC_EPI, 1);
             launch_swiglu(partial.as<float>(), s, rows, (int)I, act.p, ssp.as<float>(), nb, (int)hid, eps, dt,
                           stream, gu_block);
         }
-        if (l + 1 < L) next(w_qkv[l + 1], T, (int)nqkv, (int)hid);
         s = gemm(act.p, (int)I, w_down[l], rows, (int)hid, (int)I);
         if (!(skip_mask & 2)) {
             // residual + the next RMSNorm (next layer's attn_norm, or final_norm): all weights are 1.0
@@ -1542,15 +1526,11 @@ static tkv_status create_engine(const tkv_model_config* cfg, uint64_t seed, cons
         // Tuning / cost-attribution knobs (tools/*.sh). Compiled into TUNING builds only (make TUNING=1): several
         // of them skip work or change numerics, so the release library never reads them.
         if (const char* pfm = getenv("TKV_L2_PREFETCH_MB")) e->l2_prefetch_bytes = (size_t)atol(pfm) << 20;
-        if (const char* nq = getenv("TKV_L2_PF_NEXT_QKV")) e->l2_pf_next_qkv = atoi(nq);
         if (const char* sk = getenv("TKV_TIMING_SKIP")) e->skip_mask = atoi(sk);
         if (const char* tl = getenv("TKV_TRACE_LAYER")) e->trace_layer = atoi(tl);
         if (const char* as = getenv("TKV_ATTN_SPLITS")) e->attn_split_override = std::min(32, std::max(0, atoi(as)));
         if (const char* dr = getenv("TKV_DECODE_ROWS")) e->decode_rows_max = atol(dr);
-        if (const char* np = getenv("TKV_GEMM_NEXT_PF")) set_gemm_next_pf(atoi(np));
         if (const char* mp = getenv("TKV_GEMM_NSMP")) set_gemm_nsmp(atoi(mp));
-        if (const char* pp = getenv("TKV_GEMM_PRE_PF_MB")) set_gemm_pre_pf_mb(atoi(pp));
-        if (const char* gc = getenv("TKV_GEMM_CLUSTER")) set_gemm_cluster(atoi(gc));
         if (const char* bs = getenv("TKV_BATCH_ATTN_SPLITS")) e->batch_attn_splits = std::min(32, std::max(0, atoi(bs)));
         if (const char* se = getenv("TKV_GEMM_SKIP_EPI")) set_gemm_skip_epi(atoi(se));
         if (const char* ra = getenv("TKV_GEMM_RASTER")) set_gemm_raster(atoi(ra));

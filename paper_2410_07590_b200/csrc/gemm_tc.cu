@@ -34,9 +34,6 @@ namespace {
 constexpr int BK = 64, THREADS = 128;
 constexpr int EPI_LD = 33;  // row stride (floats) of the normal-tiling partial epilogue's per-warp staging block
                             // (odd: the 4-byte row-per-lane writes and the row reads are both conflict-free)
-#ifndef PRE_PF_MB_DEFAULT
-#define PRE_PF_MB_DEFAULT 0
-#endif
 constexpr uint32_t TILE_W = 128 * BK * 2;  // 16 KB: 128 rows x 64 k, bf16
 constexpr int SMEM_BUDGET = 200 * 1024;
 
@@ -47,10 +44,6 @@ struct Knobs {
     // (np = 2 with one 208 KB CTA per SM measured slower than np = 1 at 2 x 110 KB); pf = L2 prefetch distance
     // of the weight stream in k-blocks (0 = off)
     int stages = 0, smem_kb = 110, ctas_per_sm = 2, w_evict_first = 1, np = 1, pf = 0, krot = 1;
-    int next_pf = 0;  // k-blocks per unit of the NEXT GEMM warmed into L2 at this GEMM's tail (0 = off)
-    // swapped tiling: L2 prefetch of the first unit's weight k-blocks beyond the ring, issued BEFORE griddepcontrol.wait
-    // (weights do not depend on the previous kernel), capped at pre_pf_mb per launch over the whole grid
-    int pre_pf_mb = PRE_PF_MB_DEFAULT;
     // normal (> 128 tokens) tiling: nsnp 128-column halves per MMA (UMMA N = 128 * nsnp); N = 256 halves the
     // shared-memory traffic per FLOP of the SS-mode MMA (the 128 x 128 tile is smem-bandwidth bound at ~50 %)
     int nsnp = 2, ns_smem_kb = 226;  // 3 stages of 64 KB + the partial epilogue staging block: 227 KB
@@ -62,7 +55,6 @@ struct Knobs {
     int raster = 1;  // normal tiling unit order: 0 = n-fastest, 1 = m-fastest when N > M (W larger), 2 = m-fastest,
                      // 3 = m-fastest in groups of group_mb MB of activation rows (always)
     int group_mb = 32;
-    int cluster = 1;  // normal tiling: 2 = CTA pairs share (multicast) each weight tile
     int skip_epi = 0;
 };
 Knobs g_knobs;
@@ -132,28 +124,6 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
                  "r"(c0), "r"(c1)
                  : "memory");
 }
-// Multicast variants (2-CTA clusters, normal tiling): the weight tile lands at the same smem offset in every CTA
-// of ctaMask and completes bytes on each CTA's barrier at the same offset.
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                               uint16_t mask, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
-        : "memory");
-}
-__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                 ::"r"(smem_u32(bar)), "h"(mask) : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -197,13 +167,6 @@ __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void umma_commit_mc_elect(uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
-        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
-}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -236,8 +199,6 @@ struct GemmArgs {
                                   // TMEM lane (swapped: weight row) holds its gate AND up accumulators; 64: one 128-row
                                   // tile holds 64 gate + 64 up rows (the swapped epilogue exchanges them through smem)
     int skip_epi;                 // debug timing knob: normal-tiling partial epilogue skipped (results invalid)
-    int cl;                       // normal tiling: CTAs per cluster (2: the pair computes m-tiles 2i and 2i+1 of
-                                  // one n-tile; rank 0 multicasts the weight tile to both; m_tiles counts pairs)
     int m_group;                  // unit raster (normal tiling): 0 = n-tiles fastest; G > 0 = groups of G m-tiles,
                                   // m fastest inside a group and the group's activation rows kept L2-resident
                                   // while every n-tile streams past them (W from DRAM once per group)
@@ -253,13 +214,8 @@ struct GemmArgs {
     float eps;
     int w_evict_first;
     int pf;                       // weight L2 prefetch distance (k-blocks ahead of the ring)
-    int pre_pf;                   // k-blocks of the first unit beyond the ring L2-prefetched before griddepcontrol.wait
     int krot;                     // rotate each unit's k-block order (spreads the shared activation tiles'
                                   // L2 reads over time instead of every CTA hitting the same lines at once)
-    // next GEMM of the forward (swapped): once this CTA has issued its last loads, it warms L2 with the first
-    // nx_pf weight k-blocks of the next GEMM's units blockIdx.x, blockIdx.x + grid, ... (tmN), so that GEMM's
-    // ring fill hits L2 while this one drains and runs its epilogue
-    int nx_pf, nx_units, nx_n_tiles, nx_kb_total, nx_kb_per_split, nx_np;
     int trace_parity;             // debug: which of the two per-CTA entry/exit slot sets this launch writes
     unsigned long long* tl;       // kernel timeline slot (tl_take): first CTA past griddepcontrol.wait, last CTA exit
     unsigned long long* trace;    // debug (tkv_debug_gemm_trace): CTA 0 clock64 per stage [it][3] = producer issue,
@@ -312,8 +268,7 @@ __device__ __forceinline__ void unit_coords(const GemmArgs& g, int u, int& nt, i
 // mainloop of unit i+1.
 template <bool SWAP, int EPI>
 __global__ void __launch_bounds__(threads_for(SWAP))
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
-                   const __grid_constant__ CUtensorMap tmN, GemmArgs g) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, GemmArgs g) {
     pdl_launch();
     if (threadIdx.x == 0) gtrace_cta(g.trace, g.trace_parity, 0);
     extern __shared__ uint8_t smem_raw[];
@@ -326,18 +281,13 @@ __global__ void __launch_bounds__(threads_for(SWAP))
     uint64_t* tempty = tfull + 2;        // [2] accumulator drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cl = SWAP ? 1 : g.cl;
-    const int rank = cl > 1 ? (int)cluster_rank() : 0;
-    const int u0 = blockIdx.x / cl, ustep = gridDim.x / cl;  // this CTA's (pair) units: u0, u0 + ustep, ...
-    auto coords = [&](int u, int& nt, int& mt, int& z) {
-        unit_coords(g, u, nt, mt, z);
-        if (cl > 1) mt = mt * cl + rank;
-    };
+    const int u0 = blockIdx.x, ustep = gridDim.x;  // this CTA's units: u0, u0 + ustep, ...
+    auto coords = [&](int u, int& nt, int& mt, int& z) { unit_coords(g, u, nt, mt, z); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < g.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], cl);  // released by the MMA of every CTA whose tile reads the stage's weights
+            mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
@@ -354,7 +304,6 @@ __global__ void __launch_bounds__(threads_for(SWAP))
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (cl > 1) cluster_sync_all();  // the partner's barriers are initialised before any multicast targets them
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     const int mstep = SWAP ? g.ntok : 128 * g.mp;
@@ -363,9 +312,7 @@ __global__ void __launch_bounds__(threads_for(SWAP))
         if (lane == 0) {  // ---------------- TMA producer ----------------
             const uint64_t wpol = policy_evict_first();
             auto load_w = [&](void* dst, uint64_t* bar, int c0, int c1) {
-                if (cl > 1) {  // rank 0 brings the weight tile into both CTAs
-                    if (rank == 0) tma_load_2d_mc(dst, &tmW, bar, c0, c1, (uint16_t)((1u << cl) - 1), wpol);
-                } else if (g.w_evict_first)
+                if (g.w_evict_first)
                     tma_load_2d_hint(dst, &tmW, bar, c0, c1, wpol);
                 else
                     tma_load_2d(dst, &tmW, bar, c0, c1);
@@ -383,8 +330,6 @@ __global__ void __launch_bounds__(threads_for(SWAP))
                 mbar_expect_tx(&full[i], stage_bytes);
                 load_w(smem + i * stage_bytes, &full[i], kblk(kb0, nkb0, i, u0) * BK, nt * 128 * g.np);
             }
-            for (int i = pre; i < min(nkb0, pre + g.pre_pf); ++i)  // the rest of the unit's weights into L2, pre-wait
-                tma_prefetch_2d(&tmW, kblk(kb0, nkb0, i, u0) * BK, nt * 128 * g.np);
             pdl_wait();
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(smem + i * stage_bytes + wbytes, &tmA, &full[i], kblk(kb0, nkb0, i, u0) * BK, mt * mstep);
@@ -410,13 +355,6 @@ __global__ void __launch_bounds__(threads_for(SWAP))
                     tma_load_2d(w + wbytes, &tmA, &full[s], kb * BK, mt * mstep);
                 }
             }
-            if (g.nx_pf > 0)
-                for (int u = blockIdx.x; u < g.nx_units; u += gridDim.x) {
-                    const int z2 = u / g.nx_n_tiles, nt2 = u - z2 * g.nx_n_tiles;
-                    const int k0 = z2 * g.nx_kb_per_split, nkb = min(g.nx_kb_total, k0 + g.nx_kb_per_split) - k0;
-                    for (int i = 0; i < min(nkb, g.nx_pf); ++i)
-                        tma_prefetch_2d(&tmN, kblk(k0, nkb, i, u) * BK, nt2 * 128 * g.nx_np);
-                }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
@@ -460,9 +398,6 @@ __global__ void __launch_bounds__(threads_for(SWAP))
                             umma_f16_elect(acc + (uint32_t)(mi * 128 * g.np), da + 2 * k, dw + 2 * k, id, (i | k) != 0);
                     }
                 }
-                if (cl > 1)
-                    umma_commit_mc_elect(&empty[s], (uint16_t)((1u << cl) - 1));  // both CTAs read the weight tile
-                else
                     umma_commit_elect(&empty[s]);
                 if (lane == 0 && it < GT_STAGES) gtrace(g.trace, 3 * it + 2);
                 if (++s == g.stages) {
@@ -714,7 +649,6 @@ __global__ void __launch_bounds__(threads_for(SWAP))
     __syncthreads();
     if (threadIdx.x == 0) gtrace_cta(g.trace, g.trace_parity, 1);
     if (g.tl && threadIdx.x == 0) atomicMax(g.tl + 1, gtimer_ns());
-    if (cl > 1) cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
@@ -753,34 +687,10 @@ CUtensorMap make_map(const void* base, int rows, int cols_k, int ld_elems, int b
 }
 
 template <bool SWAP, int EPI>
-void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const CUtensorMap& tn, const GemmArgs& g, int grid,
-              size_t smem, cudaStream_t s) {
+void launch_t(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g, int grid, size_t smem, cudaStream_t s) {
     TKV_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<SWAP, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (SWAP || g.cl <= 1) {
-        launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(threads_for(SWAP)), smem, s, ta, tw, tn, g);
-        return;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(threads_for(SWAP));
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)g.cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    TKV_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<SWAP, EPI>, ta, tw, tn, g));
+    launch_k(gemm_tc_kernel<SWAP, EPI>, dim3(grid), dim3(threads_for(SWAP)), smem, s, ta, tw, g);
 }
-
-struct NextGemm {
-    const void* W = nullptr;
-    int M = 0, N = 0, K = 0, splits = 1;
-} g_next;
 
 }  // namespace
 
@@ -824,9 +734,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.mp = mp_for(M);
     g.n_tiles = (N + 128 * g.np - 1) / (128 * g.np);
     g.m_tiles = swap ? 1 : (M + 128 * g.mp - 1) / (128 * g.mp);
-    g.cl = (!swap && g_knobs.cluster > 1 && g.m_tiles >= 2) ? 2 : 1;
     g.skip_epi = g_knobs.skip_epi;
-    if (g.cl > 1) g.m_tiles = (g.m_tiles + 1) / 2;  // units count m-tile PAIRS (the odd tail's partner is all OOB)
     g.units = g.n_tiles * g.m_tiles * eff_splits;
     g.ntok = swap ? ((M + 15) / 16) * 16 : 128 * g.mp;
     g.a_bytes = (uint32_t)g.ntok * BK * 2;
@@ -870,30 +778,14 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int grid = std::min(g.units, sms * cps / g.cl) * g.cl;  // cluster mode: whole pairs
-    if (swap && g_knobs.pre_pf_mb > 0) {
-        const int64_t budget_kb = ((int64_t)g_knobs.pre_pf_mb << 20) / ((int64_t)grid * TILE_W * g.np);
-        g.pre_pf = (int)std::min<int64_t>(std::max(0, g.kb_per_split - g.stages), budget_kb);
-    }
+    const int grid = std::min(g.units, sms * cps);
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
     const CUtensorMap tw = make_map(W, N, K, K, 128 * g.np);
-    CUtensorMap tn = tw;
-    if (g_knobs.next_pf > 0 && swap && g_next.W && g_next.M <= 128) {
-        const NextGemm& nx = g_next;
-        g.nx_pf = g_knobs.next_pf;
-        g.nx_np = np_for(nx.M, nx.N);
-        g.nx_n_tiles = (nx.N + 128 * g.nx_np - 1) / (128 * g.nx_np);
-        g.nx_kb_total = (nx.K + BK - 1) / BK;
-        g.nx_kb_per_split = (g.nx_kb_total + nx.splits - 1) / nx.splits;
-        g.nx_units = g.nx_n_tiles * ((g.nx_kb_total + g.nx_kb_per_split - 1) / g.nx_kb_per_split);
-        tn = make_map(nx.W, nx.N, nx.K, nx.K, 128 * g.nx_np);
-    }
-    g_next = NextGemm{};
     if (swiglu_act) {
         if (eff_splits != 1) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the whole K range in one unit");
-        swap ? launch_t<true, EPI_SWIGLU>(ta, tw, tn, g, grid, smem, s) : launch_t<false, EPI_SWIGLU>(ta, tw, tn, g, grid, smem, s);
+        swap ? launch_t<true, EPI_SWIGLU>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_SWIGLU>(ta, tw, g, grid, smem, s);
     } else {
-        swap ? launch_t<true, EPI_PARTIAL>(ta, tw, tn, g, grid, smem, s) : launch_t<false, EPI_PARTIAL>(ta, tw, tn, g, grid, smem, s);
+        swap ? launch_t<true, EPI_PARTIAL>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_PARTIAL>(ta, tw, g, grid, smem, s);
     }
     return eff_splits;
 }
@@ -911,14 +803,7 @@ void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap) {
     g_gemm_trace = on ? buf : nullptr;
 }
 
-void set_gemm_next(const void* W, int M, int N, int K, int splits) { g_next = NextGemm{W, M, N, K, splits}; }
-
-void set_gemm_next_pf(int kblocks) { g_knobs.next_pf = kblocks; }
-
 void set_gemm_nsmp(int mp) { g_knobs.nsmp = mp > 0 ? mp : 1; }
-void set_gemm_pre_pf_mb(int mb) { g_knobs.pre_pf_mb = mb > 0 ? mb : 0; }
-
-void set_gemm_cluster(int c) { g_knobs.cluster = c; }
 
 void set_gemm_skip_epi(int v) { g_knobs.skip_epi = v; }
 

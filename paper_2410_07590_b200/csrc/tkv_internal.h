@@ -130,9 +130,6 @@ void launch_gemm_simt(const void* A, int lda, const void* W, int M, int N, int K
 // M <= 128 uses the swapped tiling (weights on the UMMA M side). With swiglu_act != nullptr (splits must
 // be 1, W rows interleaved in 64-row gate/up blocks) the epilogue writes act[M][N/2] = silu(g)*u in bf16.
 bool gemm_tc_supported(int M, int N, int K, int lda);
-// The GEMM that follows the next launch_gemm_tc in the forward (consumed by that launch) and how many of its
-// weight k-blocks per unit the current GEMM warms into L2 at its tail (0 = off)
-void set_gemm_next(const void* W, int M, int N, int K, int splits);
 void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap);
 // Kernel timeline (tkv_kernel_timeline): while armed, every launch of an instrumented kernel (GEMM, attention, split
 // merge, residual / QKV epilogues, embed, lm_head, KV gather) takes the next slot [2] of globaltimer ns (first CTA past
@@ -140,11 +137,8 @@ void gemm_trace_enable(bool on, unsigned long long* host_out, int64_t cap);
 unsigned long long* tl_take();
 void tl_set_class(int cls);
 bool tl_armed();  // debug: CTA 0 per-stage clock64 trace
-void set_gemm_next_pf(int kblocks);
 void set_gemm_nsmp(int mp);
-void set_gemm_pre_pf_mb(int mb);  // TUNING: pre-wait weight L2 prefetch budget per launch (MB, 0 = off)
-void set_gemm_cluster(int c);
-void set_gemm_skip_epi(int v);  // timing experiments only: skip the normal-tiling partial stores  // normal tiling: 2 = CTA pairs share each weight tile through TMA multicast
+void set_gemm_skip_epi(int v);  // timing experiments only: skip the normal-tiling partial stores
 // normal tiling unit order (0 n-fastest, 1 m-fastest when N > M, 2 m-fastest; group_mb > 0: m-tile groups of
 // that many MB of activation rows)
 void set_gemm_raster(int r, int group_mb = -1);  // normal (> 128-token) tiling: 128-row activation tiles per unit (1 or 2)
