@@ -58,6 +58,9 @@ constexpr int WARP_TMA = SM_WARPS, WARP_MMA = SM_WARPS + 1, THREADS = 32 * (WARP
 #ifndef ATTN_DIAG
 #define ATTN_DIAG 0  // cost-attribution variants (tools/attn_diag.sh); 0 = the product kernel
 #endif
+#ifndef ATTN_DEFER_REL
+#define ATTN_DEFER_REL 1  // release P chunk c-1 after chunk c's exps (no wait::st stall per chunk)
+#endif
 #ifndef POLY_PAIRS
 #define POLY_PAIRS 6
 #endif
@@ -735,6 +738,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                     pk[i] = bf16x2_bits(p0, p1);
                 }
                 if (tid == 0 && c == 0) trace(j, 12);
+#if ATTN_DEFER_REL
+                // chunk c-1's store had this chunk's exp work to land: release it now (no stall on tcgen05.wait::st)
+                if (c > 0) {
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&p_full[b * 4 + c - 1]);  // the PV MMA on those 32 keys may start
+                    if (tid == 0 && c == 1) trace(j, 13);
+                }
+                tmem_st_16x128_x4(tP + c * 16, pk);
+                acca = add2(acca, add2(add2(pv[0], pv[2]), add2(pv[4], pv[6])));
+                accb = add2(accb, add2(add2(pv[1], pv[3]), add2(pv[5], pv[7])));
+#else
                 tmem_st_16x128_x4(tP + c * 16, pk);
                 acca = add2(acca, add2(add2(pv[0], pv[2]), add2(pv[4], pv[6])));
                 accb = add2(accb, add2(add2(pv[1], pv[3]), add2(pv[5], pv[7])));
@@ -743,7 +759,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&p_full[b * 4 + c]);  // the PV MMA on these 32 keys may start
                 if (tid == 0 && c == 0) trace(j, 13);
+#endif
             }
+#if ATTN_DEFER_REL
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[b * 4 + 3]);
+#endif
             // observe PV(j-1) retiring (it ran during this tile's softmax): P no longer waits on it, but every pv_done
             // phase is consumed before its next arrive, so the parity wait of the lazy rescale stays unambiguous
             if (j >= 1) mbar_wait(&pv_done[(j - 1) & 1], (uint32_t)((j - 1) >> 1) & 1u);
