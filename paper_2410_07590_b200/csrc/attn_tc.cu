@@ -329,8 +329,8 @@ struct AttnArgs {
     const CUtensorMap* maps3;
     int n_req, layer;
     unsigned long long* tl;  // kernel timeline slot (tl_take)
-    // single-request split-K with a compact last row tile (attn_tc_split_plan): gx row tiles; splits_c > 0 flattens the
-    // grid to blockIdx.x = the (gx - 1) full tiles x Hkv x `splits` CTAs, then the last tile's Hkv x splits_c CTAs
+    // single-request split-K with a compact last row tile (attn_tc_pick_splits): gx row tiles; splits_c > 0 flattens the
+    // grid to blockIdx.x = the last tile's Hkv x splits_c CTAs, then the (gx - 1) full tiles x Hkv x `splits` CTAs
     int gx, splits_c;
 };
 
@@ -380,20 +380,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int group = a.H / a.Hkv;
     int bx = blockIdx.x, by = blockIdx.y, split = blockIdx.z, nsplit = a.splits;
-    if (a.splits_c > 0) {  // flattened single-request grid (see AttnArgs::splits_c)
-        const int per = (a.gx - 1) * a.Hkv, nf = per * a.splits;
+    if (a.splits_c > 0) {  // flattened single-request grid (see AttnArgs::splits_c); the compact tile's CTAs, which
+                           // carry the most key tiles, are launched first
+        const int per = (a.gx - 1) * a.Hkv, nc = a.Hkv * a.splits_c;
         int b = blockIdx.x;
-        if (b < nf) {
-            split = b / per;
-            b -= split * per;
-            by = b / (a.gx - 1);
-            bx = b - by * (a.gx - 1);
-        } else {
-            b -= nf;
+        if (b < nc) {
             split = b / a.Hkv;
             by = b - split * a.Hkv;
             bx = a.gx - 1;
             nsplit = a.splits_c;
+        } else {
+            b -= nc;
+            split = b / per;
+            b -= split * per;
+            by = b / (a.gx - 1);
+            bx = b - by * (a.gx - 1);
         }
     }
     int g = by, Tq = a.Tq, Tk = a.Tk, kv_ready = a.kv_ready;

@@ -22,18 +22,18 @@ out = np.zeros(512 + 2048, np.uint64)
 T._check(L.tkv_debug_attn_trace(0, out.ctypes.data_as(T.U64P), 512 + 2048))
 ev = out[:512].reshape(32, 16).astype(np.int64)
 cta = out[512:].reshape(1024, 2).astype(np.int64)
-# this launch's CTAs (the single-request split-K grid: (gx - 1) x Hkv x s full-tile CTAs, then Hkv x s_c for the
-# compact last tile; the rest of the buffer may hold other launches' stamps)
-NCTA, NFULL = int(os.environ.get("C2_CTAS", 148)), int(os.environ.get("C2_FULL_CTAS", 120))
+# this launch's CTAs (the single-request split-K grid: Hkv x s_c CTAs of the compact last tile, then the
+# (gx - 1) x Hkv x s full-tile CTAs; the rest of the buffer may hold other launches' stamps)
+NCTA, NCOMP = int(os.environ.get("C2_CTAS", 148)), int(os.environ.get("C2_COMPACT_CTAS", 28))
 cta = cta[:NCTA]
 s0 = cta[:, 0].min()
 st, en = (cta[:, 0] - s0) / 1e3, (cta[:, 1] - s0) / 1e3
 dur = en - st
 print(f"layer {os.environ['TKV_TRACE_LAYER']}: {len(cta)} CTAs, start spread {st.max():.2f} us, "
       f"end min/median/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f} us")
-print("CTA duration us, full tiles min/median/max %.2f/%.2f/%.2f, compact tile %.2f/%.2f/%.2f"
-      % (dur[:NFULL].min(), np.median(dur[:NFULL]), dur[:NFULL].max(), dur[NFULL:].min(), np.median(dur[NFULL:]),
-         dur[NFULL:].max()))
+print("CTA duration us, compact tile min/median/max %.2f/%.2f/%.2f, full tiles %.2f/%.2f/%.2f"
+      % (dur[:NCOMP].min(), np.median(dur[:NCOMP]), dur[:NCOMP].max(), dur[NCOMP:].min(), np.median(dur[NCOMP:]),
+         dur[NCOMP:].max()))
 t0 = ev[0, 9]
 names = ["smA:S ready", "smA:P arrive", "smB:S ready", "smB:P arrive", "mma:PV_A issued", "mma:PV_B issued",
          "tma:K(j) issue", "tma:V(j) issue", "mma:Q ready"]
