@@ -88,6 +88,11 @@ def main(steps=10):
         for k, v in sorted(gaps.items(), key=lambda kv: -sum(kv[1])):
             print(f"  gap {k:28s} n/step {len(v) / steps:6.1f}  median {np.median(v):6.2f} us  total/step {sum(v) / steps:7.1f} us")
     ep = dur[cls == T.Engine.TIMELINE_CLASSES.index("epilogue")]
+    if c5 and len(ep) % steps == 0 and (len(ep) // steps - 2) % 3 == 0:
+        # ingest forwards stop after the last layer's K/V: embed, 3 per layer, the last layer's QKV epilogue only
+        e5 = ep.reshape(steps, -1)[:, 1:-1].reshape(steps, -1, 3)
+        print("  epilogue us per layer: qkv %.1f  residual(O) %.1f  residual(down) %.1f"
+              % (e5[..., 0].mean(), e5[..., 1].mean(), e5[..., 2].mean()))
     per_layer = (len(ep) // steps - 1) // cfg.layer_num  # embed, then per layer: QKV epilogue(s), residual x2
     if per_layer >= 3 and len(ep) == steps * (1 + per_layer * cfg.layer_num):
         e = ep.reshape(steps, -1)[:, 1:].reshape(steps, cfg.layer_num, per_layer)
