@@ -787,7 +787,8 @@ def test_kernel_timeline_covers_the_forward():
 def test_graph_replay_is_bitwise_the_kernel_chain():
     """CUDA-graph replay of the query-prefill forward (captured on the second forward with the same shape and
     buffers, replayed afterwards) gives bitwise the logits and cache rows of the kernel-by-kernel chain
-    (TKV_FLAG_NO_GRAPHS), over recycled contexts, device-token prefill, and a changed query."""
+    (TKV_FLAG_NO_GRAPHS), over recycled contexts, device-token prefill, a changed query, and a different chunk order
+    of the same length (same graph key: the cache contents and positions change under the captured pointers)."""
     import torch
     cfg = T.ModelConfig(**vars(O.qwen_layers(2)))
     outs = {}
@@ -802,12 +803,14 @@ def test_graph_replay_is_bitwise_the_kernel_chain():
                 res.append(ctx.read_kv(1, "k", rotated=True)[-40:].copy())
         dq = torch.from_numpy(O.random_text_tokens(91, 40)).cuda()
         dl = torch.empty(cfg.vocab_size, dtype=torch.float32, device="cuda")
-        for rep in range(3):
-            with eng.assemble(ids, T.PositionMode.Reordered) as ctx:
+        for rep in range(4):
+            order = ids if rep < 3 else ids[::-1]  # the 4th request: same length, other chunk order
+            with eng.assemble(order, T.PositionMode.Reordered) as ctx:
                 eng.prefill_query_device(ctx, dq.data_ptr(), 40, dl.data_ptr())
                 eng.check()
                 res.append(dl.cpu().numpy().copy())
         outs[flags] = res
         eng.close()
+    assert not np.array_equal(outs[0][-1], outs[0][-2])  # the reordered context really changed the logits
     for a, b in zip(outs[0], outs[T.FLAG_NO_GRAPHS]):
         assert np.array_equal(a, b)
