@@ -31,6 +31,9 @@
 namespace tkv {
 namespace {
 
+#ifndef GEMM_WN224
+#define GEMM_WN224 1
+#endif
 constexpr int BK = 64, THREADS = 128;
 constexpr int EPI_LD = 33;  // row stride (floats) of the normal-tiling partial epilogue's per-warp staging block
                             // (odd: the 4-byte row-per-lane writes and the row reads are both conflict-free)
@@ -52,6 +55,7 @@ struct Knobs {
     // 2 x 128 x 256 outputs); the two 128 x 256 fp32 accumulators fill TMEM, so a unit's epilogue is not
     // overlapped with the next mainloop
     int nsmp = 2;
+    int wn224 = GEMM_WN224;  // normal tiling: allow 224-wide n-tiles when they fill the waves better (0 = always 128 * nsnp)
     int raster = 1;  // normal tiling unit order: 0 = n-fastest, 1 = m-fastest when N > M (W larger), 2 = m-fastest,
                      // 3 = m-fastest in groups of group_mb MB of activation rows (always)
     int group_mb = 32;
@@ -193,6 +197,8 @@ struct GemmArgs {
     int np;                       // swapped: 128-row weight tiles per unit (n_tiles counts units along N)
     int ntok;                     // swapped: tokens per tile (MMA N, multiple of 16); normal: 128 * mp
     int mp;                       // normal: 128-row activation sub-tiles per unit (each its own MMA + accumulator)
+    int wn;                       // normal: weight rows per unit = UMMA N (128 * np, or 224 when 224-wide n-tiles fill
+                                  // the last wave better: C3 / C5 O and down, N = 3584 = 16 x 224)
     int nbuf;                     // TMEM accumulator buffers (2: epilogue overlaps the next unit's mainloop)
     int gub;                      // EPI_SWIGLU: W_gu rows interleaved in blocks of gub gate rows + gub up rows. 128
                                   // (np = 2): weight tile 0 of a unit = gate rows, tile 1 = the matching up rows, so a
@@ -273,7 +279,8 @@ __global__ void __launch_bounds__(threads_for(SWAP))
     if (threadIdx.x == 0) gtrace_cta(g.trace, g.trace_parity, 0);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t wbytes = (uint32_t)g.np * TILE_W;  // weight bytes per stage
+    const uint32_t wbytes = SWAP ? (uint32_t)g.np * TILE_W : (uint32_t)g.wn * (BK * 2);  // weight bytes per stage
+    const int wrows = SWAP ? 128 * g.np : g.wn;                                             // weight rows per unit
     const uint32_t stage_bytes = wbytes + g.a_bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.stages * stage_bytes);
     uint64_t* empty = full + g.stages;
@@ -328,30 +335,30 @@ __global__ void __launch_bounds__(threads_for(SWAP))
             const int pre = min(nkb0, g.stages);
             for (int i = 0; i < pre; ++i) {
                 mbar_expect_tx(&full[i], stage_bytes);
-                load_w(smem + i * stage_bytes, &full[i], kblk(kb0, nkb0, i, u0) * BK, nt * 128 * g.np);
+                load_w(smem + i * stage_bytes, &full[i], kblk(kb0, nkb0, i, u0) * BK, nt * wrows);
             }
             pdl_wait();
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(smem + i * stage_bytes + wbytes, &tmA, &full[i], kblk(kb0, nkb0, i, u0) * BK, mt * mstep);
             // L2 prefetch of the first unit's next pf weight tiles (beyond the ring)
             for (int i = pre; i < min(nkb0, pre + g.pf); ++i)
-                tma_prefetch_2d(&tmW, kblk(kb0, nkb0, i, u0) * BK, nt * 128 * g.np);
+                tma_prefetch_2d(&tmW, kblk(kb0, nkb0, i, u0) * BK, nt * wrows);
             int it = pre;
             for (int u = u0; u < g.units; u += ustep) {
                 coords(u, nt, mt, z);
                 const int k0 = z * g.kb_per_split, nkb = min(g.kb_total, k0 + g.kb_per_split) - k0;
                 if (u != u0)
-                    for (int i = 0; i < min(nkb, g.pf); ++i) tma_prefetch_2d(&tmW, kblk(k0, nkb, i, u) * BK, nt * 128 * g.np);
+                    for (int i = 0; i < min(nkb, g.pf); ++i) tma_prefetch_2d(&tmW, kblk(k0, nkb, i, u) * BK, nt * wrows);
                 for (int i = (u == u0 ? pre : 0); i < nkb; ++i, ++it) {
                     if (g.pf > 0 && i + g.pf < nkb && i + g.pf >= (u == u0 ? pre + g.pf : g.pf))
-                        tma_prefetch_2d(&tmW, kblk(k0, nkb, i + g.pf, u) * BK, nt * 128 * g.np);
+                        tma_prefetch_2d(&tmW, kblk(k0, nkb, i + g.pf, u) * BK, nt * wrows);
                     const int s = it % g.stages;
                     mbar_wait(&empty[s], ((uint32_t)(it / g.stages) & 1u) ^ 1u);
                     if (it < GT_STAGES) gtrace(g.trace, 3 * it);
                     uint8_t* w = smem + s * stage_bytes;
                     mbar_expect_tx(&full[s], stage_bytes);
                     const int kb = kblk(k0, nkb, i, u);
-                    load_w(w, &full[s], kb * BK, nt * 128 * g.np);
+                    load_w(w, &full[s], kb * BK, nt * wrows);
                     tma_load_2d(w + wbytes, &tmA, &full[s], kb * BK, mt * mstep);
                 }
             }
@@ -362,7 +369,7 @@ __global__ void __launch_bounds__(threads_for(SWAP))
         // and lives in uniform registers; one elected lane issues each tcgen05.mma / commit. (A lane-0-only loop made
         // the compiler move every operand through an R2UR waterfall: ~165 cycles per MMA issue, which capped one CTA
         // at one 64-deep k-block per ~1100 cycles, i.e. ~28 GB/s of weights.)
-        const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, 128 * g.np);
+        const uint32_t id = SWAP ? idesc(128, g.ntok) : idesc(128, g.wn);
         int it = 0, lu = 0;
         for (int u = u0; u < g.units; u += ustep, ++lu) {
             int nt, mt, z;
@@ -395,7 +402,7 @@ __global__ void __launch_bounds__(threads_for(SWAP))
                         const uint64_t da = desc_k(a + mi * 16384);
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k)
-                            umma_f16_elect(acc + (uint32_t)(mi * 128 * g.np), da + 2 * k, dw + 2 * k, id, (i | k) != 0);
+                            umma_f16_elect(acc + (uint32_t)(mi * g.wn), da + 2 * k, dw + 2 * k, id, (i | k) != 0);
                     }
                 }
                     umma_commit_elect(&empty[s]);
@@ -433,8 +440,10 @@ __global__ void __launch_bounds__(threads_for(SWAP))
             const int m0 = mt * mstep;
             for (int pm = 0; pm < g.np * (SWAP ? 1 : g.mp); ++pm) {
             const int p = pm % g.np, mi = pm / g.np;  // weight sub-tile, activation sub-tile (normal tiling)
-            const uint32_t acc = acc_u + (uint32_t)(SWAP ? p * g.ntok : (mi * g.np + p) * 128);
-            const int n0 = (nt * g.np + p) * 128;
+            // normal tiling: activation sub-tile mi's accumulator holds wn weight columns (the partial epilogue takes
+            // them all at p == 0; the SwiGLU epilogue runs at wn = 256 with gate | up halves)
+            const uint32_t acc = acc_u + (uint32_t)(SWAP ? p * g.ntok : mi * g.wn + p * 128);
+            const int n0 = SWAP ? (nt * g.np + p) * 128 : nt * g.wn + p * 128;
             if (SWAP) {
                 const int n = n0 + lg * 32 + lane;  // TMEM lane = weight row n, column = token
                 if (EPI == EPI_PARTIAL) {
@@ -548,29 +557,36 @@ __global__ void __launch_bounds__(threads_for(SWAP))
             } else {
                 const int m = m0 + mi * 128 + lg * 32 + lane;  // TMEM lane = token row m, column = weight row
                 if (EPI == EPI_PARTIAL) {
-                    float* out = g.partial + (int64_t)z * g.M * g.N + (int64_t)m * g.N;
+                    if (p != 0) continue;  // the p == 0 pass covers all wn columns of activation sub-tile mi
                     if (g.skip_epi) continue;  // timing experiment only (TKV_GEMM_SKIP_EPI): results invalid
-                    // 64 columns per tcgen05.wait::ld, staged through this warp's padded smem block (row stride 66
-                    // floats: conflict-free 8-byte writes) and written back row by row as 256-byte segments: the
-                    // row-per-lane float4 stores cost one L2 transaction per 16 bytes (~23 K cycles per 256 x 256 unit)
+                    // 32 columns per tcgen05.wait::ld, staged through this warp's padded smem block (row stride 33
+                    // floats: conflict-free) and written back row by row as 128-byte segments: the row-per-lane
+                    // float4 stores cost one L2 transaction per 16 bytes (~23 K cycles per 256 x 256 unit)
                     float* stg = reinterpret_cast<float*>(smem + g.scratch_off) + (warp - 2) * 32 * EPI_LD;
-                    // this warp's half of the subtile: 64 columns, two 32-column chunks through the staging block
+                    // this warp's half of the subtile: wn / 2 columns (128 or 112) in 32- and 16-column chunks
+                    const int cs = (g.wn / 2) * half, ce = cs + g.wn / 2;
 #pragma unroll 1
-                    for (int c = 64 * half; c < 64 * half + 64; c += 32) {
+                    for (int c = cs; c < ce; c += 32) {
+                        const bool two = c + 32 <= ce;
                         uint32_t r[32];
                         tmem_ld16_nowait(acc + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(r));
-                        tmem_ld16_nowait(acc + (uint32_t)(c + 16), *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+                        if (two) tmem_ld16_nowait(acc + (uint32_t)(c + 16), *reinterpret_cast<uint32_t(*)[16]>(r + 16));
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) stg[lane * EPI_LD + j] = __uint_as_float(r[j]);
+                        for (int j = 0; j < 16; ++j) stg[lane * EPI_LD + j] = __uint_as_float(r[j]);
+                        if (two) {
+#pragma unroll
+                            for (int j = 16; j < 32; ++j) stg[lane * EPI_LD + j] = __uint_as_float(r[j]);
+                        }
                         __syncwarp();
                         const int mrow0 = m0 + mi * 128 + lg * 32, n = n0 + c + lane;
+                        const bool col_ok = n < g.N && (two || lane < 16);
                         float* outz = g.partial + (int64_t)z * g.M * g.N;
 #pragma unroll 4
                         for (int rr = 0; rr < 32; ++rr) {
                             const float v = stg[rr * EPI_LD + lane];
                             const int mr = mrow0 + rr;
-                            if (mr < g.M && n < g.N) outz[(int64_t)mr * g.N + n] = v;  // 128-byte row segments
+                            if (mr < g.M && col_ok) outz[(int64_t)mr * g.N + n] = v;  // 128-byte row segments
                         }
                         __syncwarp();
                     }
@@ -732,13 +748,24 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.np = gu128 ? 2 : np_for(M, N);
     if (gu128 && N % 256) fail(TKV_ERR_CONFIG, "128-row gate/up blocks need N % 256 == 0");
     g.mp = mp_for(M);
-    g.n_tiles = (N + 128 * g.np - 1) / (128 * g.np);
+    g.wn = 128 * g.np;
     g.m_tiles = swap ? 1 : (M + 128 * g.mp - 1) / (128 * g.mp);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!swap && !swiglu_act && g.wn == 256 && g_knobs.wn224) {
+        // 224-wide n-tiles when they fill the waves better: time ~ waves x unit width (C3 / C5 O and down: 112 -> 128
+        // units of 256 x 224 in one wave at M = 2048, 896 -> 1024 in 7 waves at M = 16384)
+        const int64_t u256 = (int64_t)((N + 255) / 256) * g.m_tiles * eff_splits;
+        const int64_t u224 = (int64_t)((N + 223) / 224) * g.m_tiles * eff_splits;
+        if (((u224 + sms - 1) / sms) * 224 < ((u256 + sms - 1) / sms) * 256) g.wn = 224;
+    }
+    g.n_tiles = (N + (swap ? 128 * g.np : g.wn) - 1) / (swap ? 128 * g.np : g.wn);
     g.skip_epi = g_knobs.skip_epi;
     g.units = g.n_tiles * g.m_tiles * eff_splits;
     g.ntok = swap ? ((M + 15) / 16) * 16 : 128 * g.mp;
     g.a_bytes = (uint32_t)g.ntok * BK * 2;
-    g.acc_cols = swap ? (uint32_t)(g.ntok * g.np) : 128u * (uint32_t)(g.np * g.mp);
+    g.acc_cols = swap ? (uint32_t)(g.ntok * g.np) : (uint32_t)(g.wn * g.mp);
     g.nbuf = 2 * g.acc_cols <= 512 ? 2 : 1;
     g.m_group = 0;
     if (!swap && g_knobs.raster != 0 && (g_knobs.raster == 2 || N > M)) {
@@ -750,6 +777,7 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     }
     g.tmem_cols = 32;
     while (g.tmem_cols < (uint32_t)g.nbuf * g.acc_cols) g.tmem_cols <<= 1;
+    const uint32_t wbytes = swap ? (uint32_t)g.np * TILE_W : (uint32_t)g.wn * (BK * 2);  // weight bytes per stage
     const uint32_t scratch = (!swap && !swiglu_act) ? (uint32_t)(8 * 32 * EPI_LD * 4)  // partial epilogue staging
                              : !(swap && swiglu_act) ? 0
                              : gu128 ? 1024u + 4096u  // token scales + the four warps' transpose blocks
@@ -759,10 +787,10 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
                        : swap          ? (g_knobs.smem_kb > 0 ? g_knobs.smem_kb * 1024 : SMEM_BUDGET)
                                        : g_knobs.ns_smem_kb * 1024;
     g.stages = (int)std::min<uint32_t>(g_knobs.stages > 0 ? g_knobs.stages : 8,
-                                       (uint32_t)(budget - (int)scratch) / (g.np * TILE_W + g.a_bytes));
+                                       (uint32_t)(budget - (int)scratch) / (wbytes + g.a_bytes));
     if (g.stages < 2) fail(TKV_ERR_CONFIG, "GEMM smem budget too small");
     g.w_evict_first = g_knobs.w_evict_first;
-    g.scratch_off = (uint32_t)g.stages * (g.np * TILE_W + g.a_bytes) + 256;  // after the ring and its barriers
+    g.scratch_off = (uint32_t)g.stages * (wbytes + g.a_bytes) + 256;  // after the ring and its barriers
     g.scratch_off = (g.scratch_off + 1023) / 1024 * 1024;
     g.partial = partial;
     g.trace = g_gemm_trace;
@@ -775,12 +803,9 @@ int launch_gemm_tc(const void* A, int lda, const void* W, int M, int N, int K, f
     g.eps = eps;
     if (swiglu_act && !ssp) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the folded-norm partial sums");
     const size_t smem = 1024 + (size_t)g.scratch_off + scratch;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = std::min(g.units, sms * cps);
     const CUtensorMap ta = make_map(A, M, K, lda, g.ntok);
-    const CUtensorMap tw = make_map(W, N, K, K, 128 * g.np);
+    const CUtensorMap tw = make_map(W, N, K, K, swap ? 128 * g.np : g.wn);
     if (swiglu_act) {
         if (eff_splits != 1) fail(TKV_ERR_CONFIG, "fused SwiGLU epilogue needs the whole K range in one unit");
         swap ? launch_t<true, EPI_SWIGLU>(ta, tw, g, grid, smem, s) : launch_t<false, EPI_SWIGLU>(ta, tw, g, grid, smem, s);
