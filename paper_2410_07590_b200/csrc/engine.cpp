@@ -9,6 +9,7 @@
 //   request cache [layer][K|V][cap][kv_dim] per context; keys ROTATED by the context positions once, at
 //                 injection time (the reference re-rotates every layer, model.cpp:253-254)
 //   masks         never materialised: per-row [lo, hi] key ranges (attention.cpp:50-92)
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -309,6 +310,15 @@ struct StagingRing {
         TKV_CUDA(cudaEventRecord(s.ev, st));
         s.pending = true;
     }
+};
+
+// NVTX ranges for Nsight Systems / `ncu --nvtx`: one per ABI call, per forward and per layer (host-side push/pop,
+// free when no tool is attached; inside a graph capture they mark the capture, replays carry one range)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 enum ProfClass { PC_GATHER = 0, PC_ATTN, PC_GEMM, PC_EPI, PC_OTHER, PC_N };
@@ -762,6 +772,7 @@ void tkv_engine::forward_graph(const Fwd& f) {
                                        (uint64_t)(uintptr_t)logits.p, DevMem::generation().load(), (uint64_t)f.logits};
     auto it = graphs.find(key);
     if (it != graphs.end()) {
+        NvtxRange nvtx("forward (graph replay)");
         TKV_CUDA(cudaGraphLaunch(it->second.exec, stream));
         launches += it->second.launches;
         return;
@@ -803,6 +814,7 @@ void tkv_engine::forward_graph(const Fwd& f) {
 }
 
 void tkv_engine::forward(const Fwd& f) {
+    NvtxRange nvtx("forward");
     const int T = f.T, Tk = f.row0 + f.T;
     const bool batch = !f.reqs.empty();
     const size_t es = dt_size(dt);
@@ -820,6 +832,7 @@ void tkv_engine::forward(const Fwd& f) {
                      stream);
     }
     for (int64_t l = 0; l < L; ++l) {
+        NvtxRange nvtx_layer("layer");
         // --- attention block ---
         int s = gemm(xb.p, (int)hid, w_qkv[l], T, (int)nqkv, (int)hid);
         if (batch && f.epi_reqs) {  // every request's K/V to its own cache, one launch
@@ -1780,6 +1793,7 @@ tkv_status tkv_engine_config(const tkv_engine* eng, tkv_model_config* out) {
 tkv_status tkv_ingest_chunks(tkv_engine* e, const int32_t* payloads, const int64_t* offsets, int64_t n_chunks,
                              uint64_t* ids_out, tkv_ingest_stats* stats) {
     return guard([&] {
+        NvtxRange nvtx("tkv_ingest_chunks");
         need(e, "engine");
         need(offsets, "offsets");
         e->bind();
@@ -2205,6 +2219,7 @@ tkv_status tkv_store_read(const tkv_engine* ce, uint64_t id, int64_t layer, tkv_
 
 tkv_status tkv_assemble(tkv_engine* e, const uint64_t* ids, int64_t n, tkv_position_mode mode, tkv_context** out) {
     return guard([&] {
+        NvtxRange nvtx("tkv_assemble");
         need(e, "engine");
         need(out, "out");
         if (n > 0) need(ids, "chunk_ids");
@@ -2217,6 +2232,7 @@ tkv_status tkv_assemble(tkv_engine* e, const uint64_t* ids, int64_t n, tkv_posit
 tkv_status tkv_prefill_query(tkv_engine* e, tkv_context* c, const int32_t* query, int64_t n, float* logits_out,
                              tkv_flops* fl) {
     return guard([&] {
+        NvtxRange nvtx("tkv_prefill_query");
         need(e, "engine");
         need(c, "context");
         if (n <= 0) fail(TKV_ERR_DOMAIN, "prefill_query: empty query");  // pipeline.cpp:169
@@ -2235,6 +2251,7 @@ tkv_status tkv_prefill_query(tkv_engine* e, tkv_context* c, const int32_t* query
 tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int64_t n_req, const int32_t* queries,
                                    const int64_t* offsets, float* logits_out, tkv_flops* fl) {
     return guard([&] {
+        NvtxRange nvtx("tkv_prefill_query_batch");
         need(e, "engine");
         need(ctxs, "contexts");
         need(offsets, "offsets");
@@ -2338,6 +2355,7 @@ tkv_status tkv_prefill_query_batch(tkv_engine* e, tkv_context* const* ctxs, int6
 tkv_status tkv_prefill_query_device(tkv_engine* e, tkv_context* c, const int32_t* d_query, int64_t n,
                                     float* d_logits) {
     return guard([&] {
+        NvtxRange nvtx("tkv_prefill_query_device");
         need(e, "engine");
         need(c, "context");
         if (n <= 0) fail(TKV_ERR_DOMAIN, "prefill_query: empty query");
@@ -2407,6 +2425,7 @@ tkv_status tkv_naive_prefill(tkv_engine* e, const int32_t* framed, const int64_t
                              const int32_t* query, int64_t nq, tkv_mask_mode mode, float* logits_out, tkv_flops* fl,
                              tkv_context** ctx_out) {
     return guard([&] {
+        NvtxRange nvtx("tkv_naive_prefill");
         need(e, "engine");
         if (n_chunks > 0) {
             need(framed, "framed");
@@ -2422,6 +2441,7 @@ tkv_status tkv_naive_prefill(tkv_engine* e, const int32_t* framed, const int64_t
 tkv_status tkv_naive_prefill_ids(tkv_engine* e, const uint64_t* ids, int64_t n, const int32_t* query, int64_t nq,
                                  tkv_mask_mode mode, float* logits_out, tkv_flops* fl, tkv_context** ctx_out) {
     return guard([&] {
+        NvtxRange nvtx("tkv_naive_prefill_ids");
         need(e, "engine");
         std::vector<int32_t> toks;
         std::vector<int64_t> offs{0};
@@ -2440,6 +2460,7 @@ tkv_status tkv_naive_prefill_ids(tkv_engine* e, const uint64_t* ids, int64_t n, 
 
 tkv_status tkv_greedy_decode(tkv_engine* e, tkv_context* c, int64_t max_new, int32_t* tokens_out, int64_t* n_out) {
     return guard([&] {
+        NvtxRange nvtx("tkv_greedy_decode");
         need(e, "engine");
         need(c, "context");
         if (max_new < 0) fail(TKV_ERR_DOMAIN, "greedy_decode: negative max_new");
