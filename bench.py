@@ -503,6 +503,44 @@ def run_ours(args):
               "flop_per_chunk": flop_chunk, "kv_bytes_per_chunk": c * cfg.layer_num * 2 * cfg.kv_dim * 2,
               "projection_1m_chunks_h": 1e6 / (n_chunks / sec_all) / 3600}
 
+    # C2 with the chunk KV in the pinned host tier (the paper's "TurboRAG with h2d" TTFT): a second engine whose HBM
+    # store has no room, so every chunk lands in the device-mapped host tier and the gather + RoPE kernel reads each page
+    # over PCIe (the host-to-device copy fused with the re-rotation)
+    c2h = None
+    if args.c2_host_steps > 0 and rank == 0 and ws == 1:
+        eng_h = T.Engine(cfg, SEED, dtype="bf16", device=local, store_capacity_tokens=256,
+                         host_spill_tokens=N_CHUNKS * CHUNK_TOKENS * 2, exact_fingerprint=0, flags=args.flags)
+        ids_h = eng_h.ingest_chunks(payloads)
+        tiers = {eng_h.store_chunk_tier(i) for i in ids_h}
+        if tiers != {1}:
+            raise RuntimeError(f"host-tier sample: chunks not all in the host tier ({tiers})")
+        stream_h = torch.cuda.ExternalStream(eng_h.stream_ptr(), device=dev)
+
+        def step_h():
+            ctx = eng_h.assemble(ids_h, T.PositionMode.Reordered)
+            eng_h.prefill_query_device(ctx, d_query.data_ptr(), QUERY_TOKENS, d_logits.data_ptr())
+            ctx.close()
+
+        for _ in range(3):
+            step_h()
+        stream_h.synchronize()
+        hs = [torch.cuda.Event(enable_timing=True) for _ in range(args.c2_host_steps)]
+        he = [torch.cuda.Event(enable_timing=True) for _ in range(args.c2_host_steps)]
+        for i in range(args.c2_host_steps):
+            hs[i].record(stream_h)
+            step_h()
+            he[i].record(stream_h)
+        stream_h.synchronize()
+        hp50 = statistics.median(a.elapsed_time(b) for a, b in zip(hs, he))
+        host_bytes = N_CHUNKS * CHUNK_TOKENS * cfg.layer_num * 2 * cfg.kv_dim * 2  # every chunk's K and V, bf16
+        c2h = {"workload": "C2 with every chunk's KV in the pinned host tier (paper: TurboRAG with h2d); the gather "
+                           "reads the pages over PCIe zero-copy", "steps": args.c2_host_steps, "p50_ttft_ms": hp50,
+               "kv_bytes_from_host_per_request": host_bytes,
+               "host_read_gbs_over_the_request": host_bytes / (hp50 / 1e3) / 1e9,
+               "ttft_speedup_vs_full_concat": naive["causal"] / hp50 if "causal" in naive else None}
+        eng_h.close()
+        del eng_h
+
     # C3 (BASELINE configs[2]) sample: LongBench-multidoc shape, batch 32 requests x (20 chunks x 800 tokens
     # + 64-token query), chunks retrieved from a 160-chunk corpus; one step = assemble 32 contexts + one batched
     # prefill (tkv_prefill_query_batch); composite vs reordered positions
@@ -705,6 +743,7 @@ def run_ours(args):
         "ttft_speedup_vs_full_concat": naive["causal"] / p50,
         "kv_inject_gbs": achieved,
         "ingest_s_16_chunks": ingest_s,
+        "c2_host_tier": c2h,
         "c5_ingest": c5,
         "c3_batch": c3,
         "c4_zipf_store": c4,
@@ -786,6 +825,8 @@ def main():
     ap.add_argument("--turbo-only", action="store_true", help="timed turbo steps only (for ncu captures)")
     ap.add_argument("--c5-rounds", type=int, default=32, help="C5 offline-precompute rounds of 32 chunks (0 = skip)")
     ap.add_argument("--c3-steps", type=int, default=20, help="C3 batch-32 sample steps per position mode (0 = skip)")
+    ap.add_argument("--c2-host-steps", type=int, default=10,
+                    help="C2 TTFT with the chunk KV in the pinned host tier (TurboRAG with h2d) sample steps (0 = skip)")
     ap.add_argument("--c4-requests", type=int, default=200, help="C4 measured requests (0 = skip)")
     ap.add_argument("--c4-warmup", type=int, default=400, help="C4 requests before measuring (the tier policy learns)")
     ap.add_argument("--c4-shard", type=int, default=12288, help="C4 chunks in this GPU's shard")
